@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""bench.py — seconds to top-k triplets and Gram-vector effective GB/s (BASELINE.json metric).
+
+One step = one full tsvd_run: Alg. 1 over k components, each an Alg. 2 power iteration
+(fused Gram-vector pass + reductions + stop test, a CUDA-graph WHILE loop) followed by the
+u = A v / sigma extraction, on the BASELINE.json configs[1] workload (65536 x 16384 fp32,
+k = 16, in HBM) with a known (Hadamard, rank 32, s_i = 0.8^i) spectrum.  A (4 GiB) is larger
+than L2 (126 MB), so no L2 flush is needed between steps.
+
+  value      = whole-job bytes of A streamed (4 m n per Gram pass and per extraction pass)
+               / device time of the K timed steps (CUDA events on the library's stream, max over ranks)
+  e2e        = the same metric through the public API with A in pinned HOST memory: every step
+               copies A host->device and reads U, S, V back
+  roofline   = the fused kernel N1: algorithmic bytes per launch / its CUDA-event duration
+  cpu_baseline = the fp64 oracle (oracle/) on a bounded sample of the same workload
+
+Multi-GPU (torchrun): rows split across ranks, one NCCL all-reduce per iteration,
+strong scaling (total work fixed).  `--impl reference` times the CPU oracle as the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+CONFIGS = {
+    "c2": dict(workload="dense fp32 65536x16384 in-HBM, k=16, eps=1e-6 (BASELINE configs[1]); "
+                        "Hadamard known spectrum rank 32, s_i=0.8^i; V0 ~ N(0,1) seed 2",
+               m=65536, n=16384, k=16, eps=1e-6, family="hadamard", rank=32, rho=0.8, s0=1.0),
+    "c1": dict(workload="dense fp32 512x256 known spectrum k=8 eps=1e-6 (BASELINE configs[0])",
+               m=512, n=256, k=8, eps=1e-6, family="qr", rank=256, rho=0.8, s0=10.0),
+}
+METRIC = "seconds to top-k triplets; Gram-vector effective GB/s vs HBM/H2D peak @1/2/4/8"
+
+
+def slab(world, rank, m):
+    base, rem = divmod(m, world)
+    r0 = rank * base + min(rank, rem)
+    return r0, r0 + base + (1 if rank < rem else 0)
+
+
+def make_A(cfg, r0, r1):
+    s = cfg["s0"] * cfg["rho"] ** np.arange(cfg["rank"])
+    if cfg["family"] == "hadamard":
+        return synth.hadamard_lowrank(cfg["m"], cfg["n"], s, seed=1, rows=(r0, r1))
+    A = synth.known_spectrum_qr(cfg["m"], cfg["n"], s, seed=1)
+    return np.ascontiguousarray(A[r0:r1])
+
+
+def planted(cfg):
+    return cfg["s0"] * cfg["rho"] ** np.arange(cfg["k"])
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled every 200 ms DURING the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy of 1 Gi bf16)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(cfg_name):
+    p = os.path.join(ROOT, "profiles", "ncu_n1_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(cfg_name, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_baseline(A, cfg, budget_s=15.0):
+    """The oracle (as it stands) on a bounded sample: component 1 with a fixed iteration count."""
+    import oracle
+    m_s, n = A.shape
+    V0 = synth.v0_normal(n, 1, seed=2)
+    t0 = time.perf_counter()
+    oracle.tsvd(A, 1, cfg["eps"], V0, fixed_T=1)       # 1 Gram pass + 1 extraction pass
+    per_pass = (time.perf_counter() - t0) / 2.0
+    T = int(max(1, min(50, budget_s / max(per_pass, 1e-9) - 1)))
+    t0 = time.perf_counter()
+    oracle.tsvd(A, 1, cfg["eps"], V0, fixed_T=T)
+    dt = time.perf_counter() - t0
+    passes = T + 1
+    return {"value": 4.0 * m_s * n * passes / dt / 1e9, "unit": "GB/s", "cores": oracle.num_threads(),
+            "kind": "oracle",
+            "sample": f"component 1 of {cfg['m']}x{n} (rows {m_s}), fixed T={T} Gram passes + 1 extraction, "
+                      f"fp64 plain C, {dt:.2f} s"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    A = make_A(cfg, 0, cfg["m"])
+    import oracle
+    V0 = synth.v0_normal(cfg["n"], 1, seed=2)
+    t0 = time.perf_counter()
+    oracle.tsvd(A, 1, cfg["eps"], V0, fixed_T=1)
+    per_pass = (time.perf_counter() - t0) / 2.0
+    step_budget = max(2.0, min(20.0, 150.0 / (args.steps + args.warmup)))
+    T = int(max(1, min(50, step_budget / per_pass - 1)))
+    for _ in range(args.warmup):
+        oracle.tsvd(A, 1, cfg["eps"], V0, fixed_T=T)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.tsvd(A, 1, cfg["eps"], V0, fixed_T=T)
+    dt = time.perf_counter() - t0
+    val = 4.0 * cfg["m"] * cfg["n"] * (T + 1) * args.steps / dt / 1e9
+    sample = f"component 1, fixed T={T} Gram passes + 1 extraction per step, fp64 plain C oracle"
+    line = {"metric": METRIC, "value": val, "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "m": cfg["m"], "n": cfg["n"], "k": cfg["k"]},
+            "cpu_baseline": {"value": val, "unit": "GB/s", "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tsvd", choices=["tsvd", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2208_08410_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    m, n, k, eps = cfg["m"], cfg["n"], cfg["k"], cfg["eps"]
+    r0, r1 = slab(world, rank, m)
+    A_host = make_A(cfg, r0, r1)
+    A_dev = torch.from_numpy(A_host).cuda()
+    V0 = synth.v0_normal(n, k, seed=2)
+
+    uid = None
+    if world > 1:
+        obj = [P.tsvd_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    t = P.TSVD(m, n, k, eps, rank=rank, world=world, uid=uid, device=local)
+    t.set_init(V0)
+    t.set_dense(A_dev, r0, r1)
+    stream = torch.cuda.ExternalStream(t.stream())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        tt = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    def one_step():
+        t.set_factors(None, None, None)  # restart from component 0
+        return t.run()
+
+    for _ in range(args.warmup):
+        one_step()
+    barrier()
+    launches = 0
+    with ClockSampler(local) as clocks:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            rc = one_step()
+            launches += t.report()["kernel_launches"]
+        e1.record(stream)
+        e1.synchronize()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    rep = t.report()
+    kf, iters, dots = t.info()
+    U, S, V = t.result()
+    passes = int(np.sum(iters[:kf])) + kf
+    bytes_step = 4.0 * m * n * passes
+    value = bytes_step * args.steps / (ms / 1e3) / 1e9
+    sig_err = float(np.max(np.abs(S[:kf] - planted(cfg)[:kf]) / planted(cfg)[:kf])) if kf else None
+
+    # ---- roofline of the dominant kernel (N1): per-launch CUDA events, same workload, one step
+    t.set_option(P.OPT_TIMING, 1)
+    t.set_factors(None, None, None)
+    t.run()
+    rt = t.report()
+    t.set_option(P.OPT_TIMING, 0)
+    mg = r1 - r0
+    alg_bytes = sum(int(iters[l]) * (4.0 * mg * n + 4.0 * mg * (l if l % 4 == 0 else (l + 3) // 4 * 4) + 4.0 * n)
+                    for l in range(kf))
+    n1_ms_per_launch = rt["n1_ms"] / max(rt["n1_launches"], 1)
+    per_launch_bytes = alg_bytes / max(rt["n1_launches"], 1)
+    achieved = per_launch_bytes / (n1_ms_per_launch / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+    traffic = ncu_traffic(args.config) if world == 1 else None
+
+    # ---- end to end through the public API with host (pinned) A
+    e2e = None
+    if not args.no_e2e:
+        A_pin = torch.from_numpy(A_host).pin_memory()
+        t2 = P.TSVD(m, n, k, eps, rank=rank, world=world, uid=None, device=local) if world == 1 else None
+        te = t2 if t2 is not None else t
+        te.set_init(V0)
+        te.set_dense(A_pin, r0, r1)
+        s2 = torch.cuda.ExternalStream(te.stream())
+        te.set_factors(None, None, None)
+        te.run()
+        te.result()
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(s2)
+        for _ in range(args.steps):
+            te.set_factors(None, None, None)
+            te.run()
+            te.result()
+        f1.record(s2)
+        f1.synchronize()
+        barrier()
+        ems = max_over_ranks(f0.elapsed_time(f1))
+        h2d = 4 * mg * n + 8 * k * n
+        d2h = 4 * mg * k + 8 * k + 8 * n * k + k * 64
+        e2e = {"value": bytes_step * args.steps / (ems / 1e3) / 1e9, "unit": "GB/s",
+               "seconds_to_topk": ems / args.steps / 1e3, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+        if t2 is not None:
+            t2.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(A_host, cfg)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "seconds_to_topk": ms / args.steps / 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": cfg["workload"], "m": m, "n": n, "k": k, "eps": eps,
+                       "parallelism": f"row-partition x{world}", "l2": "no flush: A (4 GiB) > L2 (126 MB)"},
+            "iterations": [int(x) for x in iters[:kf]], "k_found": kf, "status": rc,
+            "check": {"sigma_max_rel_err_vs_planted": sig_err},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "gv_fused (N1)",
+                         "per_launch_ms": n1_ms_per_launch, "alg_bytes_per_launch": per_launch_bytes,
+                         "share_of_step": rt["n1_ms"] / rt["run_ms"] if rt["run_ms"] else None,
+                         "peak_source": peak_src, "rank0_rows": mg},
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks.summary(),
+            "plan": rep["plan"], "loop": rep["loop"],
+        }
+        print(json.dumps(line), flush=True)
+    t.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

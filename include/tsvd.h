@@ -1,0 +1,169 @@
+/*
+ * tsvd.h — C ABI of libtsvd.so, the B200-native (sm_100a) hot path of the power-method
+ * truncated SVD of arXiv 2208.08410 ("Distributed Out-of-Memory SVD on CPU/GPU
+ * Architectures").  Citations "P:nnn" are lines of the paper text.
+ *
+ * What the library computes:
+ *   Alg. 1: for l = 0..k-1, with the first l components (U, S, V) found,
+ *   Alg. 2 SVD_1D on the deflated X' = A - U diag(S) V^T: starting from
+ *   v = x / ||x|| (x ~ N(0, I)), repeat
+ *        y  = X'^T (X' v)          implicit Gram-vector product, Eq. 2 in the exact
+ *                                   factored form  c = S (V^T v); t = A v - U c;
+ *                                   w = S (U^T t); y = A^T t - V w   (X' never formed)
+ *        v1 = y / ||y||
+ *   until |v . v1| >= 1 - eps, then extracts u = A v1 / sigma, sigma = ||A v1||
+ *   with the ORIGINAL A.
+ *
+ * Orientation: m >= n runs the V-first (X'^T X') branch.  m < n is
+ * not in this version (TSVD_ERR_UNSUPPORTED).
+ *
+ * Conventions for every function:
+ *   - No exceptions cross the ABI.  Every call returns a tsvd_status (warnings > 0, errors < 0)
+ *     and stores a message retrievable with tsvd_last_error(h).
+ *   - Input pointers are BORROWED: they must stay valid and unmodified until the call that
+ *     consumes them (tsvd_run / tsvd_gram_apply) returns.  Outputs are copied into caller-owned
+ *     buffers.  The handle owns every device buffer, stream, graph and communicator it creates.
+ *   - A handle is not thread-safe; one host thread per handle.  One handle per GPU per process.
+ *   - Multi-GPU (row partition): each rank owns rows [row_begin, row_end) of A and
+ *     of U; S and V are replicated.  Every rank calls every function with the same (m, n, k, eps)
+ *     and options.  One NCCL all-reduce of [y_g | w_g] per iteration (Alg. 4 lines 6, 8, 16,
+ *     P:269-279, merged into one).
+ */
+#ifndef TSVD_H
+#define TSVD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tsvd_s *tsvd_t; /* opaque handle */
+
+typedef enum { TSVD_F32 = 0 /* A, U stored fp32, all cross-thread sums fp64 */, TSVD_F64 = 1 /* reserved */ } tsvd_dtype;
+typedef enum { TSVD_ROW_MAJOR = 0, TSVD_COL_MAJOR = 1 /* reserved */ } tsvd_layout;
+typedef enum { TSVD_MEM_DEVICE = 0, TSVD_MEM_HOST_PINNED = 1, TSVD_MEM_HOST_PAGEABLE = 2 } tsvd_mem;
+
+typedef enum {
+    TSVD_OK = 0,
+    TSVD_WARN_NOT_CONVERGED = 1,   /* some component hit MAX_ITER (not fatal)              */
+    TSVD_WARN_RANK_EXHAUSTED = 2,  /* ||X'^T X' v|| == 0 or sigma == 0: fewer than k found */
+    TSVD_ERR_ARG = -1,             /* k > min(m,n), eps not in (0,1), null pointer, ...    */
+    TSVD_ERR_SHAPE = -2,           /* row range / leading dimension inconsistent          */
+    TSVD_ERR_UNSUPPORTED = -3,     /* layout / orientation / size not in this version     */
+    TSVD_ERR_NOMEM = -4,           /* device allocation failed (incl. OOM degree 2) */
+    TSVD_ERR_CUDA = -5,
+    TSVD_ERR_NCCL = -6,
+    TSVD_ERR_NUMERIC = -7,         /* non-finite value or zero initial vector              */
+    TSVD_ERR_STATE = -8            /* call out of order (e.g. run before set_dense)        */
+} tsvd_status;
+
+typedef enum {
+    TSVD_OPT_MAX_ITER = 1,       /* iterations cap per component; default 10000 (reading R5)       */
+    TSVD_OPT_FIXED_ITERS = 2,    /* > 0: exactly T iterations, convergence test off */
+    TSVD_OPT_SEED = 3,           /* seed of the internal x ~ N(0,1) generator (used when no
+                                    tsvd_set_init): splitmix64(seed, l, i) + Box-Muller, fp64     */
+    TSVD_OPT_GRAPH = 4,          /* 1 (default): iteration loop as a CUDA-graph WHILE node;
+                                    0: host-driven loop (one D2H flag read per iteration)         */
+    TSVD_OPT_TIMING = 5,         /* 1: host loop with CUDA events around every fused-kernel launch;
+                                    totals appear in tsvd_get_report                              */
+    TSVD_OPT_RUN_ROWS = 6,       /* rows per fp32 accumulation run before an fp64 flush (def 1024) */
+    TSVD_OPT_CTAS_PER_SM = 7     /* 0 = auto (occupancy); testing knob                              */
+} tsvd_option;
+
+/*
+ * tsvd_create — new handle for an m x n fp32 problem, k components (k == -1 -> min(m, n),
+ * P:71-72), stop rule |v0 . v1| >= 1 - eps.  Binds the current CUDA device.
+ * Errors: TSVD_ERR_ARG (m, n < 1; k < -1 or 0 or > min(m,n); eps not in (0,1); out == NULL),
+ *         TSVD_ERR_UNSUPPORTED (dtype != F32, layout != ROW_MAJOR, m < n), TSVD_ERR_CUDA.
+ */
+tsvd_status tsvd_create(tsvd_t *out, int64_t m, int64_t n, int32_t k, double eps, tsvd_dtype dtype,
+                        tsvd_layout layout);
+
+/* tsvd_get_unique_id — writes a 128-byte ncclUniqueId into out128 (rank 0 calls it and
+ * broadcasts the bytes, e.g. through torch.distributed).  Errors: TSVD_ERR_NCCL. */
+tsvd_status tsvd_get_unique_id(void *out128);
+
+/* tsvd_set_comm — join an NCCL communicator of `world` ranks (this rank = `rank`) on CUDA
+ * device `device`.  Optional; world == 1 needs no call.  Must precede tsvd_set_dense.
+ * Errors: TSVD_ERR_ARG, TSVD_ERR_NCCL, TSVD_ERR_CUDA. */
+tsvd_status tsvd_set_comm(tsvd_t h, int32_t rank, int32_t world, const void *nccl_unique_id, int32_t device);
+
+/* tsvd_set_option — see tsvd_option.  Errors: TSVD_ERR_ARG (unknown key / bad value). */
+tsvd_status tsvd_set_option(tsvd_t h, int32_t key, int64_t value);
+
+/* tsvd_set_init — host fp64 initial samples x, k x n row-major (= n x k column-major:
+ * row l is component l's x, NOT normalised; the library normalises it).  Copied.
+ * Errors: TSVD_ERR_ARG (NULL). */
+tsvd_status tsvd_set_init(tsvd_t h, const double *V0);
+
+/*
+ * tsvd_set_dense — this rank's row slab A[row_begin:row_end, 0:n], fp32 row-major with
+ * leading dimension ld >= n (elements).  mem = DEVICE: the pointer is used in place when it
+ * is 16-byte aligned and ld % 4 == 0, otherwise copied once into a padded device buffer.
+ * mem = HOST_*: copied host->device inside every tsvd_run (end-to-end semantics).
+ * The union of all ranks' slabs must be [0, m) with contiguous, disjoint ranges.
+ * Errors: TSVD_ERR_ARG (NULL, ld < n), TSVD_ERR_SHAPE (range outside [0, m) or empty),
+ *         TSVD_ERR_NOMEM (slab does not fit in HBM: out-of-memory streaming is a later row).
+ */
+tsvd_status tsvd_set_dense(tsvd_t h, const float *A, int64_t ld, int64_t row_begin, int64_t row_end, tsvd_mem mem);
+
+/*
+ * tsvd_set_csr — sparse CSR slab.  Not in this version: returns TSVD_ERR_UNSUPPORTED.
+ */
+tsvd_status tsvd_set_csr(tsvd_t h, const int64_t *row_ptr, const int32_t *col_idx, const float *val, int64_t nnz,
+                         int64_t row_begin, int64_t row_end, tsvd_mem mem);
+
+/*
+ * tsvd_set_factors — resume / inject the deflation state: the first l components
+ * (checkpoint after component l).  Host buffers: U this rank's slab, (row_end -
+ * row_begin) x l fp32 row-major; S fp64[l]; V n x l fp64 row-major.  A later tsvd_run starts at
+ * component l.  Errors: TSVD_ERR_ARG (l < 0 or > k, NULL with l > 0), TSVD_ERR_STATE.
+ */
+tsvd_status tsvd_set_factors(tsvd_t h, int32_t l, const float *U, const double *S, const double *V);
+
+/*
+ * tsvd_gram_apply — ONE implicit Gram-vector product y = X'^T (X' v) for the current l
+ * factors (Eq. 2 in exact factored form; includes the cross-rank all-reduce).  v, y: host
+ * fp64[n] (v is used as given, not normalised).  Blocking.  Errors: TSVD_ERR_STATE, CUDA/NCCL.
+ */
+tsvd_status tsvd_gram_apply(tsvd_t h, const double *v, double *y);
+
+/*
+ * tsvd_run — Alg. 1 from the current component to k (blocking, internal stream).
+ * Returns TSVD_OK, TSVD_WARN_NOT_CONVERGED, TSVD_WARN_RANK_EXHAUSTED (k_found < k) or an error.
+ */
+tsvd_status tsvd_run(tsvd_t h);
+
+/* tsvd_get_U_S_V — copy results to caller-owned host buffers (any may be NULL):
+ * U: (row_end-row_begin) x k fp32 row-major (this rank's slab), S: fp64[k], V: n x k fp32
+ * row-major.  Columns >= k_found are zero. */
+tsvd_status tsvd_get_U_S_V(tsvd_t h, float *U, double *S, float *V);
+
+/* tsvd_get_info — k_found, per-component iteration counts iters[k] and final |v0 . v1| dots[k]
+ * (any pointer may be NULL). */
+tsvd_status tsvd_get_info(tsvd_t h, int32_t *k_found, int32_t *iters, double *dots);
+
+/* tsvd_get_report — JSON report (plan, iterations, timings, bytes) into buf (NUL-terminated,
+ * truncated to cap).  Returns TSVD_ERR_ARG if cap == 0. */
+tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap);
+
+/* tsvd_time_gram_kernel — average duration (ms) of `reps` back-to-back launches of the fused
+ * Gram-vector kernel on the current state, timed with CUDA events on the library stream. */
+tsvd_status tsvd_time_gram_kernel(tsvd_t h, int32_t reps, double *ms_per_launch);
+
+/* tsvd_get_stream — the handle's CUDA stream (cudaStream_t) on which every kernel of the path is
+ * launched; lets a caller bracket calls with CUDA events on the launching stream.  NULL if h is. */
+void *tsvd_get_stream(tsvd_t h);
+
+/* tsvd_last_error — message of the last failing call on h (static string if h == NULL). */
+const char *tsvd_last_error(tsvd_t h);
+
+/* tsvd_destroy — free everything the handle owns.  Safe on NULL. */
+void tsvd_destroy(tsvd_t h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSVD_H */

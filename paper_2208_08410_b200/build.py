@@ -1,0 +1,53 @@
+"""In-tree build of libtsvd.so for sm_100a (nvcc cross-compiles without a GPU)."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "libtsvd.so")
+SOURCES = [os.path.join(CSRC, f) for f in ("tsvd.cu",)]
+DEPS = SOURCES + [os.path.join(CSRC, "gram_kernels.cuh"), os.path.join(ROOT, "include", "tsvd.h")]
+
+
+def nccl_dir() -> str:
+    """The NCCL torch loads (pip nvidia-nccl), so one libnccl.so.2 lives in the process."""
+    import nvidia.nccl  # noqa: F401  (namespace package of the pip wheel)
+    for p in nvidia.nccl.__path__:
+        if os.path.exists(os.path.join(p, "include", "nccl.h")):
+            return p
+    raise RuntimeError("pip NCCL headers not found")
+
+
+def nvcc() -> str:
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc"):
+        if c and os.path.exists(c):
+            return c
+    return "nvcc"
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in DEPS):
+        return LIB
+    nd = nccl_dir()
+    tmp = LIB + f".{os.getpid()}.tmp"
+    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+           "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
+           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
+           *SOURCES, "-o", tmp,
+           "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(nd, "lib")]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed building libtsvd.so")
+    if verbose:
+        sys.stderr.write(r.stderr)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

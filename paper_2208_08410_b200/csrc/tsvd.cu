@@ -1,0 +1,788 @@
+// tsvd.cu — libtsvd.so: the C ABI of include/tsvd.h and the Alg. 1 / Alg. 2 driver.
+//
+// The driver is host code that only plans, allocates and launches; every arithmetic step of
+// the power iteration (Gram-vector product, reductions, normalisation, stop test, extraction)
+// runs in the kernels of gram_kernels.cuh.  One process per GPU; multi-GPU = row partition
+// with one NCCL all-reduce of [y_g | w_g] per iteration (merges Alg. 4 lines 6, 8,
+// 16).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tsvd.h"
+#include "gram_kernels.cuh"
+
+using namespace tsvd;
+
+namespace {
+
+constexpr int kMaxThreadsPerCta = 512;
+constexpr int kRingTargetBytes = 192 * 1024;  // bytes in flight per SM (Little's law)
+constexpr int kSmemBudget = 220 * 1024;       // per SM, leaves room for barriers/scratch
+
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+using GvFn = void (*)(const GvParams);
+
+template <int T, bool EX>
+GvFn pick_nv(int nv) {
+    switch (nv) {
+    case 1: return gv_fused<T, 1, EX>;
+    case 2: return gv_fused<T, 2, EX>;
+    case 4: return gv_fused<T, 4, EX>;
+    case 8: return gv_fused<T, 8, EX>;
+    default: return nullptr;
+    }
+}
+template <bool EX>
+GvFn pick_gv(int T, int nv) {
+    switch (T) {
+    case 32: return pick_nv<32, EX>(nv);
+    case 64: return pick_nv<64, EX>(nv);
+    case 128: return pick_nv<128, EX>(nv);
+    case 256: return pick_nv<256, EX>(nv);
+    case 512: return pick_nv<512, EX>(nv);
+    default: return nullptr;
+    }
+}
+
+}  // namespace
+
+struct tsvd_s {
+    // problem
+    int64_t m = 0, n = 0;
+    int32_t k = 0, kpad = 4;
+    double eps = 1e-6;
+    // device / comm
+    int dev = 0, sms = 148;
+    cudaStream_t stream = nullptr;
+    int32_t rank = 0, world = 1;
+    ncclComm_t comm = nullptr;
+    // options
+    int max_iter = 10000, fixed_T = 0, use_graph = 1, timing = 0, run_rows = 1024, cps_opt = 0;
+    uint64_t seed = 0;
+    // input
+    int64_t row_begin = 0, row_end = 0, m_g = 0;
+    const float *A_user = nullptr;
+    int64_t ld_user = 0;
+    tsvd_mem mem = TSVD_MEM_DEVICE;
+    bool have_A = false;
+    float *A_own = nullptr;
+    int64_t ld_own = 0;
+    const float *A_use = nullptr;
+    int64_t ld_use = 0;
+    std::vector<double> V0;
+    bool have_V0 = false;
+    // factors (device)
+    float *U32 = nullptr;   // m_g x kpad
+    double *V64 = nullptr;  // n x k
+    double *S64 = nullptr;  // k
+    int32_t l_found = 0;
+    // vectors / workspaces (device)
+    double *v64 = nullptr, *yw = nullptr, *c64 = nullptr, *ypart = nullptr, *wpart = nullptr, *part = nullptr;
+    double *u64 = nullptr, *sq_part = nullptr, *sig2 = nullptr;
+    float *v32 = nullptr;
+    LoopState *st = nullptr;
+    LoopState *st_host = nullptr;  // pinned
+    double *x_host = nullptr;      // pinned staging for initial vectors
+    int64_t wofs = 0;              // offset of w inside yw
+    int fin_blocks = 0, part_ld = 0;
+    bool allocated = false;
+    // plan
+    int T = 0, NV = 0, S = 0, grid = 0, cps = 0, stage_bytes = 0, row_bytes = 0;
+    size_t smem = 0;
+    GvFn gv = nullptr, gv_ex = nullptr;
+    // results / report
+    std::vector<int32_t> iters;
+    std::vector<double> dots;
+    int32_t k_found = 0;
+    double n1_ms = 0.0, run_ms = 0.0, h2d_ms = 0.0;
+    int64_t n1_launches = 0, total_iters = 0, launches = 0;
+    std::string loop_mode = "none";
+    std::string err;
+
+    tsvd_status fail(tsvd_status s, const char *fmt, ...) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        err = buf;
+        return s;
+    }
+};
+
+#define CK(call)                                                                                    \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess) return h->fail(TSVD_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+#define NK(call)                                                                                    \
+    do {                                                                                            \
+        ncclResult_t r_ = (call);                                                                   \
+        if (r_ != ncclSuccess) return h->fail(TSVD_ERR_NCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
+    } while (0)
+#define TRY(expr)                        \
+    do {                                 \
+        tsvd_status s_ = (expr);         \
+        if (s_ < 0) return s_;           \
+    } while (0)
+
+static thread_local std::string g_err;
+
+// ------------------------------------------------------------------------------------ planning
+static tsvd_status plan(tsvd_t h) {
+    const int64_t n = h->n;
+    int T = 32;
+    while ((int64_t)4 * T * 8 < n && T < kMaxThreadsPerCta) T *= 2;
+    if ((int64_t)4 * T * 8 < n)
+        return h->fail(TSVD_ERR_UNSUPPORTED, "n = %lld > 16384 needs the 2-CTA cluster variant (not in this version)",
+                       (long long)n);
+    int NV = 1;
+    while ((int64_t)4 * T * NV < n) NV *= 2;
+    const int n4 = (int)((n + 3) / 4);
+    h->row_bytes = n4 * 16;
+    h->stage_bytes = (int)round_up(h->row_bytes + h->kpad * 4, 128);
+    int cps = h->cps_opt > 0 ? h->cps_opt : std::max(1, 512 / T);
+    int S = (int)std::min<int64_t>(kMaxStages, std::max<int64_t>(2, (kRingTargetBytes + (int64_t)h->stage_bytes * cps - 1) /
+                                                                     ((int64_t)h->stage_bytes * cps)));
+    while ((int64_t)S * h->stage_bytes * cps > kSmemBudget && S > 2) --S;
+    while ((int64_t)S * h->stage_bytes * cps > kSmemBudget && cps > 1) --cps;
+    h->T = T;
+    h->NV = NV;
+    h->S = S;
+    h->smem = (size_t)S * h->stage_bytes + kMaxStages * sizeof(uint64_t) + 2 * (T / 32) * sizeof(double);
+    h->gv = pick_gv<false>(T, NV);
+    h->gv_ex = pick_gv<true>(T, NV);
+    CK(cudaFuncSetAttribute(h->gv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem));
+    CK(cudaFuncSetAttribute(h->gv_ex, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->gv, T, h->smem));
+    if (occ < 1) return h->fail(TSVD_ERR_UNSUPPORTED, "fused kernel does not fit on an SM (T=%d smem=%zu)", T, h->smem);
+    h->cps = std::min(cps, occ);
+    h->grid = (int)std::min<int64_t>((int64_t)h->sms * h->cps, h->m_g);
+    return TSVD_OK;
+}
+
+static tsvd_status ensure_alloc(tsvd_t h) {
+    if (h->allocated) return TSVD_OK;
+    TRY(plan(h));
+    const int64_t n = h->n, mg = h->m_g;
+    const int64_t vpad = std::max<int64_t>(round_up(n, 4), (int64_t)4 * h->T * h->NV);
+    h->wofs = round_up(n, 32);
+    h->fin_blocks = (int)((n + kFinThreads - 1) / kFinThreads);
+    h->part_ld = 2 + h->kpad;
+    const int64_t ypart_ld = round_up(n, 4);
+    auto dm = [&](void **p, size_t bytes) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(bytes, 16)); };
+    cudaError_t e = cudaSuccess;
+    if (!e) e = dm((void **)&h->U32, (size_t)mg * h->kpad * sizeof(float));
+    if (!e) e = dm((void **)&h->V64, (size_t)n * h->k * sizeof(double));
+    if (!e) e = dm((void **)&h->S64, (size_t)h->k * sizeof(double));
+    if (!e) e = dm((void **)&h->v64, (size_t)n * sizeof(double));
+    if (!e) e = dm((void **)&h->v32, (size_t)vpad * sizeof(float));
+    if (!e) e = dm((void **)&h->yw, (size_t)(h->wofs + h->kpad) * sizeof(double));
+    if (!e) e = dm((void **)&h->c64, (size_t)h->kpad * sizeof(double));
+    if (!e) e = dm((void **)&h->ypart, (size_t)h->grid * ypart_ld * sizeof(double));
+    if (!e) e = dm((void **)&h->wpart, (size_t)h->grid * h->kpad * sizeof(double));
+    if (!e) e = dm((void **)&h->part, (size_t)h->fin_blocks * h->part_ld * sizeof(double));
+    if (!e) e = dm((void **)&h->u64, (size_t)mg * sizeof(double));
+    if (!e) e = dm((void **)&h->sq_part, (size_t)h->grid * sizeof(double));
+    if (!e) e = dm((void **)&h->sig2, sizeof(double));
+    if (!e) e = dm((void **)&h->st, sizeof(LoopState));
+    if (!e) e = cudaMallocHost((void **)&h->st_host, sizeof(LoopState) + 2 * sizeof(double));
+    if (!e) e = cudaMallocHost((void **)&h->x_host, (size_t)n * sizeof(double));
+    if (e == cudaErrorMemoryAllocation) return h->fail(TSVD_ERR_NOMEM, "device workspace allocation failed");
+    CK(e);
+    CK(cudaMemsetAsync(h->U32, 0, (size_t)mg * h->kpad * sizeof(float), h->stream));
+    CK(cudaMemsetAsync(h->V64, 0, (size_t)n * h->k * sizeof(double), h->stream));
+    CK(cudaMemsetAsync(h->S64, 0, (size_t)h->k * sizeof(double), h->stream));
+    CK(cudaMemsetAsync(h->v32, 0, (size_t)vpad * sizeof(float), h->stream));
+    CK(cudaMemsetAsync(h->v64, 0, (size_t)n * sizeof(double), h->stream));
+    CK(cudaMemsetAsync(h->c64, 0, (size_t)h->kpad * sizeof(double), h->stream));
+    CK(cudaMemsetAsync(h->yw, 0, (size_t)(h->wofs + h->kpad) * sizeof(double), h->stream));
+    CK(cudaMemsetAsync(h->st, 0, sizeof(LoopState), h->stream));
+    h->allocated = true;
+    return TSVD_OK;
+}
+
+// Make A resident on the device for this run (host input: H2D copy, counted in e2e timing).
+static tsvd_status stage_A(tsvd_t h) {
+    if (h->mem == TSVD_MEM_DEVICE) return TSVD_OK;
+    const int64_t n4 = (h->n + 3) / 4;
+    if (!h->A_own) {
+        h->ld_own = n4 * 4;
+        size_t bytes = (size_t)h->m_g * h->ld_own * sizeof(float);
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        if (bytes + (256ull << 20) > fr)
+            return h->fail(TSVD_ERR_NOMEM, "row slab (%zu B) does not fit in HBM (%zu B free); streaming is a later row",
+                           bytes, fr);
+        cudaError_t e = cudaMalloc((void **)&h->A_own, bytes);
+        if (e == cudaErrorMemoryAllocation) return h->fail(TSVD_ERR_NOMEM, "A device buffer allocation failed");
+        CK(e);
+        if (h->ld_own != h->n) CK(cudaMemsetAsync(h->A_own, 0, bytes, h->stream));
+    }
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, h->stream));
+    CK(cudaMemcpy2DAsync(h->A_own, h->ld_own * sizeof(float), h->A_user, h->ld_user * sizeof(float),
+                         h->n * sizeof(float), h->m_g, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaEventRecord(e1, h->stream));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    h->h2d_ms += ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    h->A_use = h->A_own;
+    h->ld_use = h->ld_own;
+    return TSVD_OK;
+}
+
+// ------------------------------------------------------------------------------------ launches
+static GvParams gv_params(tsvd_t h, int l, bool extract, const int32_t *done) {
+    GvParams p{};
+    p.A = h->A_use;
+    p.ld = h->ld_use;
+    p.rows = h->m_g;
+    p.n = (int32_t)h->n;
+    p.n4 = (int32_t)((h->n + 3) / 4);
+    p.U = h->U32;
+    p.ldu = h->kpad;
+    p.l = extract ? 0 : l;
+    p.v32 = h->v32;
+    p.c = h->c64;
+    p.ypart = h->ypart;
+    p.ypart_ld = round_up(h->n, 4);
+    p.wpart = h->wpart;
+    p.wpart_ld = h->kpad;
+    p.stages = h->S;
+    p.stage_bytes = h->stage_bytes;
+    p.row_bytes = h->row_bytes;
+    p.u_bytes = (extract || l == 0) ? 0 : (int32_t)(round_up(l, 4) * 4);
+    p.run_rows = h->run_rows;
+    p.u_out = h->u64;
+    p.sq_part = h->sq_part;
+    p.done = done;
+    return p;
+}
+
+static tsvd_status launch_gv(tsvd_t h, int l, const int32_t *done) {
+    GvParams p = gv_params(h, l, false, done);
+    h->gv<<<h->grid, h->T, h->smem, h->stream>>>(p);
+    CK(cudaGetLastError());
+    return TSVD_OK;
+}
+
+static tsvd_status allreduce(tsvd_t h, double *buf, size_t count) {
+    if (h->world <= 1) return TSVD_OK;
+    NK(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, h->comm, h->stream));
+    return TSVD_OK;
+}
+
+// Everything after N1 in one iteration: N7, all-reduce, N5a-c.
+static tsvd_status launch_tail(tsvd_t h, int l, int fin_mode, const int32_t *done, unsigned long long cond, int use_cond) {
+    const int n = (int)h->n;
+    double *y = h->yw, *w = h->yw + h->wofs;
+    reduce_partials<<<(n + 255) / 256, 256, 0, h->stream>>>(h->ypart, h->grid, round_up(n, 4), n, h->wpart, h->kpad, l,
+                                                           y, w, done);
+    CK(cudaGetLastError());
+    TRY(allreduce(h, h->yw, (size_t)(h->wofs + h->kpad)));
+    fin_partial<<<h->fin_blocks, kFinThreads, (size_t)std::max(l, 1) * sizeof(double), h->stream>>>(
+        fin_mode, n, l, h->S64, h->V64, h->k, w, y, h->v64, h->part, h->part_ld, done);
+    CK(cudaGetLastError());
+    if (fin_mode == 0) {
+        fin_scalar<<<1, kFinThreads, 0, h->stream>>>(0, h->fin_blocks, h->part_ld, l, h->S64, h->part, h->c64, h->st,
+                                                     h->eps, h->fixed_T, h->max_iter, cond, use_cond);
+        CK(cudaGetLastError());
+        fin_normalize<<<std::min(h->fin_blocks, 1184), kFinThreads, 0, h->stream>>>(n, y, h->st, h->v64, h->v32, 1);
+        CK(cudaGetLastError());
+    }
+    return TSVD_OK;
+}
+
+// x (host, fp64) -> v = x / ||x|| and c = S (V^T v), all on the device.
+static tsvd_status init_component(tsvd_t h, int l, const double *x) {
+    const int n = (int)h->n;
+    memcpy(h->x_host, x, (size_t)n * sizeof(double));
+    CK(cudaMemcpyAsync(h->yw, h->x_host, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    fin_partial<<<h->fin_blocks, kFinThreads, (size_t)std::max(l, 1) * sizeof(double), h->stream>>>(
+        1, n, l, h->S64, h->V64, h->k, h->yw + h->wofs, h->yw, h->v64, h->part, h->part_ld, nullptr);
+    CK(cudaGetLastError());
+    fin_scalar<<<1, kFinThreads, 0, h->stream>>>(1, h->fin_blocks, h->part_ld, l, h->S64, h->part, h->c64, h->st,
+                                                 h->eps, h->fixed_T, h->max_iter, 0ull, 0);
+    CK(cudaGetLastError());
+    fin_normalize<<<std::min(h->fin_blocks, 1184), kFinThreads, 0, h->stream>>>(n, h->yw, h->st, h->v64, h->v32, 0);
+    CK(cudaGetLastError());
+    return TSVD_OK;
+}
+
+static void gen_x(uint64_t seed, int l, int64_t n, double *x) {
+    const uint64_t key = splitmix64(splitmix64(seed) ^ (uint64_t)l);
+    const double two_pi = 6.283185307179586476925286766559;
+    for (int64_t i = 0; i < n; i += 2) {
+        const double u1 = (double)(splitmix64(key ^ (uint64_t)i) >> 11) * 0x1.0p-53;
+        const double u2 = (double)(splitmix64(key ^ (uint64_t)(i + 1)) >> 11) * 0x1.0p-53;
+        const double r = std::sqrt(-2.0 * std::log(1.0 - u1));
+        x[i] = r * std::cos(two_pi * u2);
+        if (i + 1 < n) x[i + 1] = r * std::sin(two_pi * u2);
+    }
+}
+
+// The power iteration of one component as a CUDA-graph WHILE loop (no host round trip).
+static tsvd_status iterate_graph(tsvd_t h, int l) {
+#if CUDART_VERSION >= 12040
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    CK(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle cond;
+    CK(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(h->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    tsvd_status s = launch_gv(h, l, nullptr);
+    if (s >= 0) s = launch_tail(h, l, 0, nullptr, (unsigned long long)cond, 1);
+    cudaGraph_t captured = nullptr;
+    cudaError_t e = cudaStreamEndCapture(h->stream, &captured);
+    if (s < 0) {
+        cudaGraphDestroy(graph);
+        return s;
+    }
+    CK(e);
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+    CK(cudaGraphLaunch(exec, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    h->loop_mode = "graph-while";
+    return TSVD_OK;
+#else
+    return h->fail(TSVD_ERR_UNSUPPORTED, "CUDA graph conditional nodes need CUDA >= 12.4");
+#endif
+}
+
+// Host-driven loop: one pinned D2H flag read per iteration; optional CUDA events around N1.
+static tsvd_status iterate_host(tsvd_t h, int l) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (h->timing) {
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+    }
+    for (;;) {
+        if (h->timing) CK(cudaEventRecord(e0, h->stream));
+        TRY(launch_gv(h, l, nullptr));
+        if (h->timing) CK(cudaEventRecord(e1, h->stream));
+        TRY(launch_tail(h, l, 0, nullptr, 0ull, 0));
+        CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        if (h->timing) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            h->n1_ms += ms;
+            h->n1_launches += 1;
+        }
+        if (h->st_host->done) break;
+    }
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    h->loop_mode = h->timing ? "host+events" : "host";
+    return TSVD_OK;
+}
+
+static tsvd_status extract_component(tsvd_t h, int l) {
+    GvParams p = gv_params(h, l, true, nullptr);
+    h->gv_ex<<<h->grid, h->T, h->smem, h->stream>>>(p);
+    CK(cudaGetLastError());
+    ext_reduce<<<1, 32, 0, h->stream>>>(h->sq_part, h->grid, h->sig2);
+    CK(cudaGetLastError());
+    TRY(allreduce(h, h->sig2, 1));
+    const int64_t work = std::max<int64_t>(h->m_g, h->n);
+    const int blocks = (int)std::min<int64_t>((work + 255) / 256, (int64_t)h->sms * 8);
+    ext_scale<<<blocks, 256, 0, h->stream>>>(h->m_g, (int)h->n, l, h->u64, h->sig2, h->v64, h->U32, h->kpad, h->V64,
+                                           h->k, h->S64);
+    CK(cudaGetLastError());
+    return TSVD_OK;
+}
+
+// ------------------------------------------------------------------------------------ ABI
+extern "C" {
+
+tsvd_status tsvd_create(tsvd_t *out, int64_t m, int64_t n, int32_t k, double eps, tsvd_dtype dtype,
+                        tsvd_layout layout) {
+    if (!out) {
+        g_err = "out == NULL";
+        return TSVD_ERR_ARG;
+    }
+    *out = nullptr;
+    const int64_t mn = std::min(m, n);
+    if (m < 1 || n < 1 || k == 0 || k < -1 || (k > 0 && k > mn) || !(eps > 0.0 && eps < 1.0)) {
+        g_err = "bad arguments: need m,n >= 1, k in [1, min(m,n)] or -1, 0 < eps < 1";
+        return TSVD_ERR_ARG;
+    }
+    if (dtype != TSVD_F32 || layout != TSVD_ROW_MAJOR || m < n) {
+        g_err = "only fp32 row-major with m >= n in this version";
+        return TSVD_ERR_UNSUPPORTED;
+    }
+    if (k == -1 && mn > INT32_MAX) {
+        g_err = "k too large";
+        return TSVD_ERR_ARG;
+    }
+    tsvd_t h = new tsvd_s();
+    h->m = m;
+    h->n = n;
+    h->k = k == -1 ? (int32_t)mn : k;
+    h->kpad = (int32_t)round_up(h->k, 4);
+    h->eps = eps;
+    h->row_begin = 0;
+    h->row_end = m;
+    h->m_g = m;
+    h->iters.assign(h->k, 0);
+    h->dots.assign(h->k, 0.0);
+    cudaError_t e = cudaGetDevice(&h->dev);
+    if (!e) e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->dev);
+    if (!e) e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+    if (e) {
+        g_err = std::string("CUDA: ") + cudaGetErrorString(e);
+        delete h;
+        return TSVD_ERR_CUDA;
+    }
+    *out = h;
+    return TSVD_OK;
+}
+
+tsvd_status tsvd_get_unique_id(void *out128) {
+    if (!out128) return TSVD_ERR_ARG;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return TSVD_ERR_NCCL;
+    memcpy(out128, &id, sizeof(id));
+    return TSVD_OK;
+}
+
+tsvd_status tsvd_set_comm(tsvd_t h, int32_t rank, int32_t world, const void *uid, int32_t device) {
+    if (!h) return TSVD_ERR_ARG;
+    if (world < 1 || rank < 0 || rank >= world || (world > 1 && !uid))
+        return h->fail(TSVD_ERR_ARG, "bad rank/world");
+    if (h->allocated || h->have_A) return h->fail(TSVD_ERR_STATE, "set_comm must precede set_dense");
+    if (device != h->dev) {
+        CK(cudaSetDevice(device));
+        if (h->stream) cudaStreamDestroy(h->stream);
+        h->dev = device;
+        CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->dev));
+        CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    }
+    h->rank = rank;
+    h->world = world;
+    if (world > 1) {
+        ncclUniqueId id;
+        memcpy(&id, uid, sizeof(id));
+        NK(ncclCommInitRank(&h->comm, world, id, rank));
+    }
+    return TSVD_OK;
+}
+
+tsvd_status tsvd_set_option(tsvd_t h, int32_t key, int64_t value) {
+    if (!h) return TSVD_ERR_ARG;
+    switch (key) {
+    case TSVD_OPT_MAX_ITER:
+        if (value < 1 || value > INT32_MAX) return h->fail(TSVD_ERR_ARG, "MAX_ITER must be >= 1");
+        h->max_iter = (int)value;
+        break;
+    case TSVD_OPT_FIXED_ITERS:
+        if (value < 0 || value > INT32_MAX) return h->fail(TSVD_ERR_ARG, "FIXED_ITERS must be >= 0");
+        h->fixed_T = (int)value;
+        break;
+    case TSVD_OPT_SEED: h->seed = (uint64_t)value; break;
+    case TSVD_OPT_GRAPH: h->use_graph = value != 0; break;
+    case TSVD_OPT_TIMING: h->timing = value != 0; break;
+    case TSVD_OPT_RUN_ROWS:
+        if (value < 1 || value > INT32_MAX) return h->fail(TSVD_ERR_ARG, "RUN_ROWS must be >= 1");
+        h->run_rows = (int)value;
+        break;
+    case TSVD_OPT_CTAS_PER_SM:
+        if (value < 0 || value > 32) return h->fail(TSVD_ERR_ARG, "CTAS_PER_SM in [0, 32]");
+        if (h->allocated) return h->fail(TSVD_ERR_STATE, "CTAS_PER_SM must precede set_dense");
+        h->cps_opt = (int)value;
+        break;
+    default: return h->fail(TSVD_ERR_ARG, "unknown option %d", key);
+    }
+    return TSVD_OK;
+}
+
+tsvd_status tsvd_set_init(tsvd_t h, const double *V0) {
+    if (!h) return TSVD_ERR_ARG;
+    if (!V0) return h->fail(TSVD_ERR_ARG, "V0 == NULL");
+    h->V0.assign(V0, V0 + (size_t)h->k * h->n);
+    h->have_V0 = true;
+    return TSVD_OK;
+}
+
+tsvd_status tsvd_set_dense(tsvd_t h, const float *A, int64_t ld, int64_t row_begin, int64_t row_end, tsvd_mem mem) {
+    if (!h) return TSVD_ERR_ARG;
+    if (!A || ld < h->n) return h->fail(TSVD_ERR_ARG, "A == NULL or ld < n");
+    if (row_begin < 0 || row_end > h->m || row_end <= row_begin)
+        return h->fail(TSVD_ERR_SHAPE, "row range [%lld, %lld) outside [0, %lld)", (long long)row_begin,
+                       (long long)row_end, (long long)h->m);
+    if (mem != TSVD_MEM_DEVICE && mem != TSVD_MEM_HOST_PINNED && mem != TSVD_MEM_HOST_PAGEABLE)
+        return h->fail(TSVD_ERR_ARG, "bad mem kind");
+    CK(cudaSetDevice(h->dev));
+    if (h->allocated && (row_end - row_begin) != h->m_g)
+        return h->fail(TSVD_ERR_STATE, "row slab size cannot change after the first run");
+    h->row_begin = row_begin;
+    h->row_end = row_end;
+    h->m_g = row_end - row_begin;
+    h->A_user = A;
+    h->ld_user = ld;
+    h->mem = mem;
+    h->have_A = true;
+    if (mem == TSVD_MEM_DEVICE) {
+        const bool aligned = ((uintptr_t)A % 16 == 0) && (ld % 4 == 0);
+        if (aligned) {
+            h->A_use = A;
+            h->ld_use = ld;
+        } else {  // pack once into a 16-B aligned, ld % 4 == 0 copy (TMA bulk-copy alignment)
+            const int64_t ldp = round_up(h->n, 4);
+            if (h->A_own) cudaFree(h->A_own);
+            h->A_own = nullptr;
+            cudaError_t e = cudaMalloc((void **)&h->A_own, (size_t)h->m_g * ldp * sizeof(float));
+            if (e == cudaErrorMemoryAllocation) return h->fail(TSVD_ERR_NOMEM, "no room for an aligned copy of A");
+            CK(e);
+            CK(cudaMemsetAsync(h->A_own, 0, (size_t)h->m_g * ldp * sizeof(float), h->stream));
+            CK(cudaMemcpy2DAsync(h->A_own, ldp * sizeof(float), A, ld * sizeof(float), h->n * sizeof(float), h->m_g,
+                                 cudaMemcpyDeviceToDevice, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            h->ld_own = ldp;
+            h->A_use = h->A_own;
+            h->ld_use = ldp;
+        }
+    }
+    return TSVD_OK;
+}
+
+tsvd_status tsvd_set_csr(tsvd_t h, const int64_t *, const int32_t *, const float *, int64_t, int64_t, int64_t,
+                         tsvd_mem) {
+    if (!h) return TSVD_ERR_ARG;
+    return h->fail(TSVD_ERR_UNSUPPORTED, "sparse CSR path is not in this version");
+}
+
+tsvd_status tsvd_set_factors(tsvd_t h, int32_t l, const float *U, const double *S, const double *V) {
+    if (!h) return TSVD_ERR_ARG;
+    if (l < 0 || l > h->k || (l > 0 && (!U || !S || !V))) return h->fail(TSVD_ERR_ARG, "bad factors");
+    if (!h->have_A) return h->fail(TSVD_ERR_STATE, "set_dense first");
+    CK(cudaSetDevice(h->dev));
+    TRY(ensure_alloc(h));
+    if (l > 0) {
+        CK(cudaMemcpy2DAsync(h->U32, h->kpad * sizeof(float), U, l * sizeof(float), l * sizeof(float), h->m_g,
+                             cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->S64, S, l * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemcpy2DAsync(h->V64, h->k * sizeof(double), V, l * sizeof(double), l * sizeof(double), h->n,
+                             cudaMemcpyHostToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    h->l_found = l;
+    h->k_found = l;
+    return TSVD_OK;
+}
+
+tsvd_status tsvd_gram_apply(tsvd_t h, const double *v, double *y) {
+    if (!h) return TSVD_ERR_ARG;
+    if (!v || !y) return h->fail(TSVD_ERR_ARG, "NULL vector");
+    if (!h->have_A) return h->fail(TSVD_ERR_STATE, "set_dense first");
+    CK(cudaSetDevice(h->dev));
+    TRY(ensure_alloc(h));
+    TRY(stage_A(h));
+    const int n = (int)h->n, l = h->l_found;
+    CK(cudaMemcpyAsync(h->v64, v, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    to_f32<<<std::min(h->fin_blocks, 1184), kFinThreads, 0, h->stream>>>(n, h->v64, h->v32);
+    CK(cudaGetLastError());
+    // c = S (V^T v) for the given (unnormalised) v
+    fin_partial<<<h->fin_blocks, kFinThreads, (size_t)std::max(l, 1) * sizeof(double), h->stream>>>(
+        2, n, l, h->S64, h->V64, h->k, h->yw + h->wofs, h->v64, h->v64, h->part, h->part_ld, nullptr);
+    CK(cudaGetLastError());
+    fin_scalar<<<1, kFinThreads, 0, h->stream>>>(2, h->fin_blocks, h->part_ld, l, h->S64, h->part, h->c64, h->st,
+                                                 h->eps, h->fixed_T, h->max_iter, 0ull, 0);
+    CK(cudaGetLastError());
+    TRY(launch_gv(h, l, nullptr));
+    const double *yw = h->yw;
+    const int nn = n;
+    reduce_partials<<<(nn + 255) / 256, 256, 0, h->stream>>>(h->ypart, h->grid, round_up(nn, 4), nn, h->wpart,
+                                                             h->kpad, l, h->yw, h->yw + h->wofs, nullptr);
+    CK(cudaGetLastError());
+    TRY(allreduce(h, h->yw, (size_t)(h->wofs + h->kpad)));
+    fin_partial<<<h->fin_blocks, kFinThreads, (size_t)std::max(l, 1) * sizeof(double), h->stream>>>(
+        0, n, l, h->S64, h->V64, h->k, h->yw + h->wofs, h->yw, h->v64, h->part, h->part_ld, nullptr);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(y, yw, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return TSVD_OK;
+}
+
+tsvd_status tsvd_run(tsvd_t h) {
+    if (!h) return TSVD_ERR_ARG;
+    if (!h->have_A) return h->fail(TSVD_ERR_STATE, "set_dense first");
+    CK(cudaSetDevice(h->dev));
+    auto t0 = std::chrono::steady_clock::now();
+    TRY(ensure_alloc(h));
+    TRY(stage_A(h));
+    h->n1_ms = 0.0;
+    h->n1_launches = 0;
+    h->total_iters = 0;
+    h->launches = 0;
+    tsvd_status result = TSVD_OK;
+    std::vector<double> xbuf;
+    for (int l = h->l_found; l < h->k; ++l) {
+        const double *x;
+        if (h->have_V0) {
+            x = h->V0.data() + (size_t)l * h->n;
+        } else {
+            xbuf.resize(h->n);
+            gen_x(h->seed, l, h->n, xbuf.data());
+            x = xbuf.data();
+        }
+        TRY(init_component(h, l, x));
+        const bool graph = h->use_graph && !h->timing && h->world == 1;
+        if (graph) TRY(iterate_graph(h, l));
+        else TRY(iterate_host(h, l));
+        TRY(extract_component(h, l));
+        CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
+        double *sig2_host = reinterpret_cast<double *>(h->st_host + 1);
+        CK(cudaMemcpyAsync(sig2_host, h->sig2, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        const LoopState st = *h->st_host;
+        if (st.status == -7) return h->fail(TSVD_ERR_NUMERIC, "non-finite value or zero initial vector at component %d", l);
+        if (st.status == 2 || !(*sig2_host > 0.0)) {
+            result = TSVD_WARN_RANK_EXHAUSTED;
+            break;
+        }
+        if (!std::isfinite(*sig2_host)) return h->fail(TSVD_ERR_NUMERIC, "non-finite sigma at component %d", l);
+        h->iters[l] = st.it;
+        h->dots[l] = st.d;
+        h->total_iters += st.it;
+        h->launches += 3 + 5 * (int64_t)st.it + 3;  // init (N5a-c), iterations (N1, N7, N5a-c), extraction
+        if (st.status == 1 && result == TSVD_OK) result = TSVD_WARN_NOT_CONVERGED;
+        h->l_found = l + 1;
+        h->k_found = l + 1;
+    }
+    h->run_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (result == TSVD_WARN_RANK_EXHAUSTED) h->err = "rank exhausted before k components";
+    return result;
+}
+
+tsvd_status tsvd_get_U_S_V(tsvd_t h, float *U, double *S, float *V) {
+    if (!h) return TSVD_ERR_ARG;
+    if (!h->allocated) return h->fail(TSVD_ERR_STATE, "nothing computed yet");
+    CK(cudaSetDevice(h->dev));
+    if (U)
+        CK(cudaMemcpy2DAsync(U, h->k * sizeof(float), h->U32, h->kpad * sizeof(float), h->k * sizeof(float), h->m_g,
+                             cudaMemcpyDeviceToHost, h->stream));
+    if (S) CK(cudaMemcpyAsync(S, h->S64, h->k * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    std::vector<double> vt;
+    if (V) {
+        vt.resize((size_t)h->n * h->k);
+        CK(cudaMemcpyAsync(vt.data(), h->V64, vt.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    if (V)
+        for (size_t i = 0; i < vt.size(); ++i) V[i] = (float)vt[i];
+    return TSVD_OK;
+}
+
+tsvd_status tsvd_get_info(tsvd_t h, int32_t *k_found, int32_t *iters, double *dots) {
+    if (!h) return TSVD_ERR_ARG;
+    if (k_found) *k_found = h->k_found;
+    if (iters) memcpy(iters, h->iters.data(), h->k * sizeof(int32_t));
+    if (dots) memcpy(dots, h->dots.data(), h->k * sizeof(double));
+    return TSVD_OK;
+}
+
+tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
+    if (!h || !buf || cap == 0) return TSVD_ERR_ARG;
+    std::string s = "{";
+    char tmp[512];
+    snprintf(tmp, sizeof tmp,
+             "\"m\": %lld, \"n\": %lld, \"k\": %d, \"eps\": %.3g, \"rank\": %d, \"world\": %d, \"rows\": [%lld, %lld], "
+             "\"k_found\": %d, \"total_iters\": %lld, \"run_ms\": %.4f, \"h2d_ms\": %.4f, \"n1_ms\": %.6f, "
+             "\"n1_launches\": %lld, \"kernel_launches\": %lld, \"loop\": \"%s\", ",
+             (long long)h->m, (long long)h->n, h->k, h->eps, h->rank, h->world, (long long)h->row_begin,
+             (long long)h->row_end, h->k_found, (long long)h->total_iters, h->run_ms, h->h2d_ms, h->n1_ms,
+             (long long)h->n1_launches, (long long)h->launches, h->loop_mode.c_str());
+    s += tmp;
+    snprintf(tmp, sizeof tmp,
+             "\"plan\": {\"T\": %d, \"NV\": %d, \"stages\": %d, \"ctas_per_sm\": %d, \"grid\": %d, \"smem\": %zu, "
+             "\"stage_bytes\": %d, \"run_rows\": %d}, ",
+             h->T, h->NV, h->S, h->cps, h->grid, h->smem, h->stage_bytes, h->run_rows);
+    s += tmp;
+    s += "\"iters\": [";
+    for (int i = 0; i < h->k; ++i) {
+        snprintf(tmp, sizeof tmp, "%s%d", i ? ", " : "", h->iters[i]);
+        s += tmp;
+    }
+    s += "]}";
+    snprintf(buf, cap, "%s", s.c_str());
+    return TSVD_OK;
+}
+
+tsvd_status tsvd_time_gram_kernel(tsvd_t h, int32_t reps, double *ms) {
+    if (!h || !ms || reps < 1) return TSVD_ERR_ARG;
+    if (!h->have_A) return h->fail(TSVD_ERR_STATE, "set_dense first");
+    CK(cudaSetDevice(h->dev));
+    TRY(ensure_alloc(h));
+    TRY(stage_A(h));
+    const int l = std::min(h->l_found, h->k - 1);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    TRY(launch_gv(h, l, nullptr));  // warm-up
+    CK(cudaEventRecord(e0, h->stream));
+    for (int r = 0; r < reps; ++r) TRY(launch_gv(h, l, nullptr));
+    CK(cudaEventRecord(e1, h->stream));
+    CK(cudaEventSynchronize(e1));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms = (double)t / reps;
+    return TSVD_OK;
+}
+
+void *tsvd_get_stream(tsvd_t h) { return h ? (void *)h->stream : nullptr; }
+
+const char *tsvd_last_error(tsvd_t h) { return h ? h->err.c_str() : g_err.c_str(); }
+
+void tsvd_destroy(tsvd_t h) {
+    if (!h) return;
+    cudaSetDevice(h->dev);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    void *dev_ptrs[] = {h->A_own, h->U32, h->V64, h->S64, h->v64, h->v32, h->yw, h->c64, h->ypart,
+                        h->wpart, h->part, h->u64, h->sq_part, h->sig2, h->st};
+    for (void *p : dev_ptrs)
+        if (p) cudaFree(p);
+    if (h->st_host) cudaFreeHost(h->st_host);
+    if (h->x_host) cudaFreeHost(h->x_host);
+    if (h->comm) ncclCommDestroy(h->comm);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+}  // extern "C"

@@ -59,12 +59,13 @@ def _walsh_factor(size: int, idx: np.ndarray, signs: np.ndarray, rows: slice) ->
 
 
 def hadamard_lowrank(m: int, n: int, s: np.ndarray, seed: int = 1, out: np.ndarray | None = None,
-                     row_chunk: int = 4096) -> np.ndarray:
+                     row_chunk: int = 4096, rows: tuple[int, int] | None = None) -> np.ndarray:
     """fp32 A (m x n) with exactly orthonormal rank-r factors (m, n powers of two).
 
     Left factor column i:  d1 * walsh(a_i) / sqrt(m); right: d2 * walsh(b_i) / sqrt(n),
     with a_i (b_i) distinct random row indices of the m x m (n x n) Walsh matrix.  The
-    exact singular values are s (before the single fp32 rounding of A).
+    exact singular values are s (before the single fp32 rounding of A).  ``rows=(r0, r1)``
+    returns only that row slab (same bits as the full matrix's rows).
     """
     s = np.asarray(s, dtype=np.float64)
     r = s.shape[0]
@@ -77,12 +78,13 @@ def hadamard_lowrank(m: int, n: int, s: np.ndarray, seed: int = 1, out: np.ndarr
     d2 = rng.choice(np.array([-1.0, 1.0]), size=n)
     right = _walsh_factor(n, b, d2, slice(None)) / np.sqrt(n)          # n x r
     rs = (right * s).T.copy()                                           # r x n
+    g0, g1 = (0, m) if rows is None else rows
     if out is None:
-        out = np.empty((m, n), dtype=np.float32)
-    for r0 in range(0, m, row_chunk):
-        sl = slice(r0, min(m, r0 + row_chunk))
-        left = _walsh_factor(m, a, d1, sl) / np.sqrt(m)                # rows x r
-        out[sl] = (left @ rs).astype(np.float32)
+        out = np.empty((g1 - g0, n), dtype=np.float32)
+    for r0 in range(g0, g1, row_chunk):
+        r1 = min(g1, r0 + row_chunk)
+        left = _walsh_factor(m, a, d1, slice(r0, r1)) / np.sqrt(m)     # rows x r
+        out[r0 - g0:r1 - g0] = (left @ rs).astype(np.float32)
     return out
 
 

@@ -1,0 +1,261 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded inputs.
+
+Tolerances:
+  * one Gram-vector product: normwise relative error <= 1e-5.  Derivation: fp32 products with
+    fp32 runs of <= 32 terms inside a thread and fp64 beyond give ~sqrt(32) u32 = 3.4e-7 per
+    t_r and the same order on y; 30x margin.
+  * full t-SVD (north star): sigma relative error <= 1e-4 and |cos(u_gpu, u_oracle)|,
+    |cos(v_gpu, v_oracle)| >= 1 - 1e-4 per pair, same V0 on both sides.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected on the GPU box only
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2208_08410_b200 as P  # noqa: E402
+
+SIG_TOL = 1e-4
+COS_TOL = 1e-4
+
+
+def _cos(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return abs(a @ b) / (np.linalg.norm(a) * np.linalg.norm(b))
+
+
+def _gpu_tsvd(A, k, eps, V0, device=True, **opts):
+    m, n = A.shape
+    t = P.TSVD(m, n, k, eps)
+    for key, val in opts.items():
+        t.set_option(getattr(P, "OPT_" + key.upper()), val)
+    t.set_init(V0)
+    if device:
+        t.set_dense(torch.from_numpy(A).cuda())
+    else:
+        t.set_dense(A)
+    rc = t.run()
+    U, S, V = t.result()
+    kf, iters, dots = t.info()
+    rep = t.report()
+    t.close()
+    return rc, U, S, V, kf, iters, dots, rep
+
+
+def _assert_parity(A, ref, U, S, V, kf, k):
+    assert kf == ref.k_found == k
+    rel = np.abs(S[:k] - ref.S[:k]) / ref.S[:k]
+    assert rel.max() <= SIG_TOL, rel
+    for i in range(k):
+        assert 1 - _cos(V[:, i], ref.V[:, i]) <= COS_TOL, (i, 1 - _cos(V[:, i], ref.V[:, i]))
+        assert 1 - _cos(U[:, i], ref.U[:, i]) <= COS_TOL, (i, 1 - _cos(U[:, i], ref.U[:, i]))
+
+
+# ------------------------------------------------------------------ one Gram-vector product
+
+@pytest.mark.parametrize("m,n,l", [
+    (513, 256, 0), (513, 256, 3), (777, 129, 1), (300, 37, 5), (1000, 1000, 2),
+    (2100, 4099, 4), (3000, 8192, 0), (1600, 16384, 6), (40, 3, 2), (9, 1, 0)])
+def test_gram_apply_vs_oracle(m, n, l):
+    rng = np.random.default_rng(m + 7 * n + l)
+    A = rng.standard_normal((m, n)).astype(np.float32)
+    U = rng.standard_normal((m, l)).astype(np.float32)
+    S = rng.uniform(0.5, 3.0, l)
+    V = rng.standard_normal((n, l))
+    v = rng.standard_normal(n)
+    want = oracle.gram_apply(A, U.astype(np.float64), S, V, v)
+    t = P.TSVD(m, n, max(l, 1), 1e-6)
+    t.set_dense(torch.from_numpy(A).cuda())
+    t.set_factors(U, S, V)
+    got = t.gram_apply(v)
+    t.close()
+    err = np.linalg.norm(got - want) / np.linalg.norm(want)
+    assert err <= 1e-5, err
+
+
+def test_gram_apply_ld_and_host_input():
+    """Leading dimension > n (unaligned rows are packed), pageable host input, pinned host input."""
+    rng = np.random.default_rng(1)
+    big = rng.standard_normal((700, 301)).astype(np.float32)
+    A = big[:, :299]
+    v = rng.standard_normal(299)
+    want = oracle.gram_apply(A, None, None, None, v)
+    outs = []
+    for src in (torch.from_numpy(big).cuda()[:, :299], A, torch.from_numpy(np.ascontiguousarray(A)).pin_memory()):
+        t = P.TSVD(700, 299, 1, 1e-6)
+        t.set_dense(src)
+        outs.append(t.gram_apply(v))
+        t.close()
+    for got in outs:
+        assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-5
+    np.testing.assert_array_equal(outs[1], outs[2])
+
+
+# ------------------------------------------------------------------ full Alg. 1 + Alg. 2
+
+def test_c1_parity():
+    """BASELINE.json configs[0]: 512x256 known spectrum (s_i = 10 * 0.8^i), k = 8, eps = 1e-6."""
+    m, n, k, eps = 512, 256, 8, 1e-6
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(n, 10.0, 0.8), seed=1)
+    V0 = synth.v0_normal(n, k, seed=2)
+    ref = oracle.tsvd(A, k, eps, V0)
+    rc, U, S, V, kf, iters, dots, rep = _gpu_tsvd(A, k, eps, V0)
+    assert rc == P.OK
+    _assert_parity(A, ref, U, S, V, kf, k)
+    assert np.all(np.abs(iters - ref.iters) <= 1), (iters, ref.iters)
+    assert rep["loop"] == "graph-while"
+
+
+@pytest.mark.parametrize("m,n,k,fam", [(1000, 300, 5, "qr"), (333, 333, 4, "qr"), (5000, 4099, 3, "qr"),
+                                       (2048, 1024, 6, "hadamard"), (700, 64, 4, "qr")])
+def test_ragged_parity(m, n, k, fam):
+    eps = 1e-6
+    if fam == "qr":
+        r = min(n, 48)
+        A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(r, 5.0, 0.75), seed=m + n)
+    else:
+        A = synth.hadamard_lowrank(m, n, 0.8 ** np.arange(32), seed=3)
+    V0 = synth.v0_normal(n, k, seed=k)
+    ref = oracle.tsvd(A, k, eps, V0)
+    rc, U, S, V, kf, *_ = _gpu_tsvd(A, k, eps, V0)
+    assert rc == P.OK
+    _assert_parity(A, ref, U, S, V, kf, k)
+
+
+def test_paper_like_uniform_fixed_iterations():
+    """Paper-like U[0,1) input in fixed-iteration mode: trajectory parity."""
+    m, n, k, T = 1500, 400, 3, 12
+    A = synth.uniform_dense(m, n, seed=5)
+    V0 = synth.v0_normal(n, k, seed=6)
+    ref = oracle.tsvd(A, k, 1e-6, V0, fixed_T=T)
+    rc, U, S, V, kf, iters, *_ = _gpu_tsvd(A, k, 1e-6, V0, fixed_iters=T)
+    assert list(iters) == [T] * k
+    _assert_parity(A, ref, U, S, V, kf, k)
+
+
+def test_graph_and_host_loops_bitwise_equal():
+    m, n, k = 900, 200, 4
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(n, 3.0, 0.7), seed=4)
+    V0 = synth.v0_normal(n, k, seed=4)
+    a = _gpu_tsvd(A, k, 1e-8, V0, graph=1)
+    b = _gpu_tsvd(A, k, 1e-8, V0, graph=0)
+    c = _gpu_tsvd(A, k, 1e-8, V0, timing=1)
+    for x in (b, c):
+        np.testing.assert_array_equal(a[1], x[1])
+        np.testing.assert_array_equal(a[2], x[2])
+        np.testing.assert_array_equal(a[3], x[3])
+    assert c[7]["n1_launches"] == int(np.sum(c[5]))
+
+
+def test_run_rows_flush_and_ctas():
+    """fp64 flushes every RUN_ROWS rows and a different CTA count change only rounding."""
+    m, n, k = 4000, 512, 3
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(64, 2.0, 0.8), seed=8)
+    V0 = synth.v0_normal(n, k, seed=8)
+    a = _gpu_tsvd(A, k, 1e-8, V0)
+    b = _gpu_tsvd(A, k, 1e-8, V0, run_rows=7, ctas_per_sm=2)
+    np.testing.assert_allclose(a[2], b[2], rtol=1e-9)
+    for i in range(k):
+        assert 1 - _cos(a[3][:, i], b[3][:, i]) <= 1e-9
+
+
+def test_resume_from_factors():
+    m, n, k = 800, 160, 4
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(n, 4.0, 0.7), seed=12)
+    V0 = synth.v0_normal(n, k, seed=12)
+    _, U, S, V, *_ = _gpu_tsvd(A, k, 1e-8, V0)
+    t = P.TSVD(m, n, k, 1e-8)
+    t.set_init(V0)
+    t.set_dense(torch.from_numpy(A).cuda())
+    t.set_factors(U[:, :2], S[:2], V[:, :2].astype(np.float64))
+    t.run()
+    U2, S2, V2 = t.result()
+    kf, iters, _ = t.info()
+    t.close()
+    assert kf == k and iters[0] == 0 and iters[1] == 0
+    np.testing.assert_allclose(S2[2:], S[2:], rtol=1e-6)
+    for i in (2, 3):
+        assert 1 - _cos(V2[:, i], V[:, i]) <= 1e-8
+
+
+def test_host_input_equals_device_input():
+    m, n, k = 600, 100, 3
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(n, 4.0, 0.6), seed=2)
+    V0 = synth.v0_normal(n, k, seed=3)
+    a = _gpu_tsvd(A, k, 1e-6, V0, device=True)
+    b = _gpu_tsvd(A, k, 1e-6, V0, device=False)
+    np.testing.assert_array_equal(a[2], b[2])
+    np.testing.assert_array_equal(a[1], b[1])
+
+
+# ------------------------------------------------------------------ edge cases / errors
+
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (5, 1, 1), (7, 3, 3), (33, 32, 2)])
+def test_tiny_shapes(m, n, k):
+    rng = np.random.default_rng(m * 10 + n)
+    A = rng.standard_normal((m, n)).astype(np.float32)
+    V0 = synth.v0_normal(n, k, seed=1)
+    ref = oracle.tsvd(A, k, 1e-6, V0)
+    rc, U, S, V, kf, *_ = _gpu_tsvd(A, k, 1e-6, V0)
+    assert kf == ref.k_found
+    np.testing.assert_allclose(S[:kf], ref.S[:kf], rtol=SIG_TOL)
+
+
+def test_zero_matrix_rank_exhausted():
+    A = np.zeros((64, 16), dtype=np.float32)
+    rc, U, S, V, kf, *_ = _gpu_tsvd(A, 2, 1e-6, synth.v0_normal(16, 2))
+    assert rc == P.WARN_RANK_EXHAUSTED and kf == 0
+
+
+def test_nan_input_is_numeric_error():
+    A = np.ones((64, 16), dtype=np.float32)
+    A[3, 4] = np.nan
+    with pytest.raises(P.TsvdError) as ei:
+        _gpu_tsvd(A, 1, 1e-6, synth.v0_normal(16, 1))
+    assert ei.value.status == P.ERR_NUMERIC
+
+
+def test_argument_errors():
+    with pytest.raises(P.TsvdError) as ei:
+        P.tsvd_create(10, 5, 6, 1e-6)
+    assert ei.value.status == P.ERR_ARG
+    with pytest.raises(P.TsvdError) as ei:
+        P.tsvd_create(10, 5, 2, 1.5)
+    assert ei.value.status == P.ERR_ARG
+    with pytest.raises(P.TsvdError) as ei:
+        P.tsvd_create(5, 10, 2, 1e-6)
+    assert ei.value.status == P.ERR_UNSUPPORTED
+    # n > 16384 needs the cluster variant (not in this version)
+    t = P.TSVD(20000, 20000, 1, 1e-6)
+    with pytest.raises(P.TsvdError) as ei:
+        t.set_dense(torch.zeros((20000, 20000), dtype=torch.float32, device="cuda"))
+        t.run()
+    assert ei.value.status == P.ERR_UNSUPPORTED
+    t.close()
+    t = P.TSVD(10, 5, 2, 1e-6)
+    with pytest.raises(P.TsvdError) as ei:
+        t.run()
+    assert ei.value.status == P.ERR_STATE
+    t.close()
+
+
+def test_internal_generator_is_seeded():
+    m, n, k = 300, 64, 2
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(n, 4.0, 0.6), seed=2)
+    outs = []
+    for _ in range(2):
+        t = P.TSVD(m, n, k, 1e-8)
+        t.set_option(P.OPT_SEED, 42)
+        t.set_dense(torch.from_numpy(A).cuda())
+        t.run()
+        outs.append(t.result()[1])
+        t.close()
+    np.testing.assert_array_equal(outs[0], outs[1])
+    np.testing.assert_allclose(outs[0], 4.0 * 0.6 ** np.arange(k), rtol=1e-5)
