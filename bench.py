@@ -179,6 +179,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--loop", default="graph", choices=["graph", "host"],
+                    help="host: host-driven iteration loop (ncu cannot profile kernels inside conditional graphs)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -208,6 +210,8 @@ def main():
     t = P.TSVD(m, n, k, eps, rank=rank, world=world, uid=uid, device=local)
     t.set_init(V0)
     t.set_dense(A_dev, r0, r1)
+    if args.loop == "host":
+        t.set_option(P.OPT_GRAPH, 0)
     stream = torch.cuda.ExternalStream(t.stream())
 
     def barrier():

@@ -1,23 +1,34 @@
 // gram_kernels.cuh — sm_100a kernels of the Gram-vector hot path.
 //
-//   N1 gv_fused      one pass over the row slab of A per power iteration:
-//                      t_r = A_r . v - U_r . c        (= (X' v)_r,  Alg. 4 lines 3-4 + 14)
-//                      y  += t_r A_r^T                 (X'^T X' v before the V correction)
-//                      w  += t_r U_r^T                 (U^T X' v)
-//                    A and U rows are staged by TMA bulk copies (cp.async.bulk) into an S-stage
-//                    shared-memory ring; each staged element is read from shared memory ONCE into
-//                    registers and used for both the dot and the axpy, so A is read from HBM
-//                    exactly once per iteration (the paper's Alg. 4 reads it twice).
-//                    EXTRACT=true runs the same pipeline for u = A v and ||u||^2.
-//   N7 reduce_partials   fixed-order fp64 sum of the per-CTA partials of y and w.
-//   N5 fin_partial / fin_scalar / fin_normalize
-//                    y -= V (S w); ||y||^2, v.y, V^T y in fp64; d = |v.y|/||y||, stop test
-//                    |v0.v1| >= 1-eps, v1 = y/||y||, c_next = S V^T v1.
-//   N6 ext_reduce / ext_scale   sigma = ||A v1||, U[:,l] = A v1 / sigma.
+// One power iteration (Alg. 2 lines 11-14) on one GPU is TWO kernels:
 //
-// Precision (reading R17): A, U and the copy of v fed to N1 are fp32; products are
-// fp32 FMAs inside a thread, every cross-thread / cross-CTA / cross-GPU sum is fp64, and the
-// per-CTA y accumulators are flushed to fp64 every `run_rows` rows.
+//   N1 gv_fused   one pass over the row slab of A:
+//                   t_r = A_r . v - U_r . c        (= (X' v)_r,  Alg. 4 lines 3-4 + 14)
+//                   y  += t_r A_r^T                 (A^T X' v)
+//                   w  += t_r U_r^T                 (U^T X' v)
+//                 A and U rows are staged by 1-D TMA bulk copies (cp.async.bulk) into an S-stage
+//                 shared-memory ring; each staged element is read from shared memory ONCE into
+//                 registers and used for both the dot and the axpy, so A is read from HBM exactly
+//                 once per iteration (the paper's Alg. 4 reads it twice).  The
+//                 prologue builds this thread's slice of v = y_cur / ||y_cur|| in registers (the
+//                 normalisation of P:122 is folded here).  EXTRACT=true runs the same pipeline for
+//                 u = A v and ||u||^2.
+//   N5 fin_iter   per column j: y_j = sum_b ypart[b][j] (fixed order, fp64) - sum_i V[j,i] S_i w_i;
+//                 per block: ||y||^2, v.y, V^T y; the LAST block to finish (arrival counter) sums
+//                 the block partials in block order and takes the scalar decisions: ||y||, the stop
+//                 test |v0 . v1| >= 1 - eps, c_next = S V^T v1, and the CUDA-graph WHILE
+//                 condition.  y_new goes to the other half of a ping-pong buffer, so the next
+//                 iteration's v is y_new / ||y_new|| with no separate normalisation pass.
+//
+// Multi-GPU (row partition) inserts reduce_partials + one NCCL all-reduce of [y_g | w_g] between
+// them, and fin_iter<false> reads the all-reduced vector instead of the per-CTA partials.
+//
+// N6 extraction: gv_fused<EXTRACT> then ext_finish: sigma = ||A v1||, U[:,l] = A v1 / sigma
+// (P:87), V[:,l] = v1, S[l] = sigma.
+//
+// Precision (reading R17): A, U and the copy of v fed to N1 are fp32; products are fp32
+// FMAs inside a thread, every cross-thread / cross-CTA / cross-GPU sum is fp64, and the per-CTA y
+// accumulators are flushed to fp64 every `run_rows` rows.  The master iterate (y, ||y||) is fp64.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -25,40 +36,52 @@
 namespace tsvd {
 
 constexpr int kMaxStages = 8;
+constexpr int kFinThreads = 256;
 
 struct LoopState {
-    double yy;      // ||y||^2 of the last product
-    double ny;      // ||y||
-    double d;       // |v0 . v1| of the last iteration
-    int32_t it;     // iterations done in this component
-    int32_t done;   // loop finished
-    int32_t status; // 0 ok, 1 not converged, 2 rank exhausted, -7 numeric
+    double ny;         // ||y_cur||: the current iterate is v = y_cur / ny
+    double d;          // |v0 . v1| of the last iteration
+    int32_t it;        // iterations completed in this component; y_cur = ybuf[it & 1]
+    int32_t done;      // this component's loop has finished
+    int32_t status;    // 0 ok, 1 not converged (MAX_ITER), 2 rank exhausted, -7 non-finite
+    int32_t stop;      // sticky: rank exhausted / non-finite -> every later kernel is a no-op
+    uint32_t counter;  // arrivals of the last-block-done reduction (returns to 0 after use)
+    int32_t pad;
+};
+
+struct CompStat {  // per component, written by ext_finish
+    double d;
+    double sigma;
+    int32_t it;
+    int32_t status;
+    int32_t valid;
     int32_t pad;
 };
 
 struct GvParams {
-    const float *A;        // row slab base (row 0 of this launch)
-    int64_t ld;            // leading dimension (floats), % 4 == 0
-    int64_t rows;          // rows in this launch
-    int32_t n;             // columns
-    int32_t n4;            // ceil(n / 4): float4 per row
-    const float *U;        // rows x ldu fp32 (row 0 aligned with A's row 0); may be null if l == 0
-    int32_t ldu;           // % 4 == 0
-    int32_t l;             // components already found (U columns used)
-    const float *v32;      // fp32 copy of v, zero padded to >= 4*T*NV
-    const double *c;       // c = S (V^T v), length l
-    double *ypart;         // [gridDim.x][ypart_ld] fp64 per-CTA partial of A^T t
+    const float *A;          // row slab base (row 0 of this launch)
+    int64_t ld;              // leading dimension (floats), % 4 == 0
+    int64_t rows;            // rows in this launch
+    int32_t n;               // columns
+    int32_t n4;              // ceil(n / 4): float4 per row
+    const float *U;          // rows x ldu fp32 (row 0 aligned with A's row 0)
+    int32_t ldu;             // % 4 == 0
+    int32_t l;               // components already found (U columns used)
+    const double *ybuf;      // ping-pong fp64 iterate buffers, [2][ystride]
+    int64_t ystride;
+    const LoopState *st;     // it, ny, done, stop
+    const double *c;         // c = S (V^T v), length l
+    double *ypart;           // [gridDim.x][ypart_ld] fp64 per-CTA partial of A^T t
     int64_t ypart_ld;
-    double *wpart;         // [gridDim.x][wpart_ld] fp64 per-CTA partial of U^T t
+    double *wpart;           // [gridDim.x][wpart_ld] fp64 per-CTA partial of U^T t
     int32_t wpart_ld;
-    int32_t stages;        // S
-    int32_t stage_bytes;   // bytes per ring slot (A row + U row, 128-B aligned)
-    int32_t row_bytes;     // n4 * 16
-    int32_t u_bytes;       // round4(l) * 4 (0 if l == 0 or EXTRACT)
-    int32_t run_rows;      // fp32 run length before flushing to fp64
-    double *u_out;         // EXTRACT: fp64 (A v)_r, indexed by launch row
-    double *sq_part;       // EXTRACT: [gridDim.x] fp64 sum of (A v)_r^2
-    const int32_t *done;   // optional: skip the launch when *done != 0 (speculative loops)
+    int32_t stages;          // S
+    int32_t stage_bytes;     // bytes per ring slot (A row + U row, 128-B aligned)
+    int32_t row_bytes;       // n4 * 16
+    int32_t u_bytes;         // round4(l) * 4 (0 if l == 0 or EXTRACT)
+    int32_t run_rows;        // fp32 run length before flushing to fp64
+    double *u_out;           // EXTRACT: fp64 (A v)_r, indexed by launch row
+    double *sq_part;         // EXTRACT: [gridDim.x] fp64 sum of (A v)_r^2
 };
 
 // ---------------------------------------------------------------- PTX helpers (mbarrier + TMA)
@@ -102,6 +125,12 @@ __device__ __forceinline__ double warp_sum(double x) {
     return x;
 }
 
+__device__ __forceinline__ void set_cond(unsigned long long h, int use, unsigned v) {
+#if CUDART_VERSION >= 12040
+    if (use) cudaGraphSetConditional((cudaGraphConditionalHandle)h, v);
+#endif
+}
+
 // ---------------------------------------------------------------- N1: fused Gram-vector pass
 // Grid: one persistent CTA per (SM x CTAs/SM), each owning a contiguous row range.
 // Block: T threads; thread `tid` owns float4 columns {k*T + tid : k < NV} of every row.
@@ -109,7 +138,8 @@ template <int T, int NV, bool EXTRACT>
 __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int NW = T / 32;
-    if (p.done != nullptr && *p.done) return;
+    const LoopState *st = p.st;
+    if (st->stop || (!EXTRACT && st->done)) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (size_t)p.stages * p.stage_bytes);
     double *red = reinterpret_cast<double *>(bars + kMaxStages);  // [2][NW]
@@ -138,11 +168,20 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
         for (int s = 0; s < pre; ++s) issue(s, r0 + s);
     }
 
-    // this thread's slice of v (fp32, zero padded) and c
+    // this thread's slice of v = y_cur / ||y_cur|| (fp64 master -> fp32), while the ring fills
     float4 vr[NV];
-    const float4 *v4 = reinterpret_cast<const float4 *>(p.v32);
+    {
+        const double ny = st->ny;
+        const double *ycur = p.ybuf + (int64_t)(st->it & 1) * p.ystride;
 #pragma unroll
-    for (int k = 0; k < NV; ++k) vr[k] = v4[k * T + tid];
+        for (int k = 0; k < NV; ++k) {
+            const int j = 4 * (k * T + tid);
+            vr[k].x = j + 0 < p.n ? (float)(ycur[j + 0] / ny) : 0.f;
+            vr[k].y = j + 1 < p.n ? (float)(ycur[j + 1] / ny) : 0.f;
+            vr[k].z = j + 2 < p.n ? (float)(ycur[j + 2] / ny) : 0.f;
+            vr[k].w = j + 3 < p.n ? (float)(ycur[j + 3] / ny) : 0.f;
+        }
+    }
     double cval = 0.0;
     if (!EXTRACT && tid < l) cval = p.c[tid];
     const int tail = p.n & 3;  // valid lanes of the last float4 (0 = full)
@@ -246,64 +285,125 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     }
 }
 
-// ---------------------------------------------------------------- N7: fixed-order partial sum
-// y[j] = sum_{b < parts} ypart[b][j] (b ascending), w[i] likewise.  yw: [y (n) | pad | w (l)].
+// ---------------------------------------------------------------- multi-GPU: local partial sum
+// yw = [ y_g (n) | pad | w_g (l) ], y_g[j] = sum_{b} ypart[b][j] in b order.  Then all-reduce.
 __global__ void reduce_partials(const double *__restrict__ ypart, int parts, int64_t ypart_ld, int n,
-                                const double *__restrict__ wpart, int wpart_ld, int l, double *__restrict__ y,
-                                double *__restrict__ w, const int32_t *done) {
-    if (done != nullptr && *done) return;
+                                const double *__restrict__ wpart, int wpart_ld, int l, double *__restrict__ yw,
+                                int64_t wofs, const LoopState *st) {
+    if (st->stop || st->done) return;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j < n) {
-        double s0 = 0.0;
-        int b = 0;
-        for (; b < parts; ++b) s0 += ypart[(int64_t)b * ypart_ld + j];
-        y[j] = s0;
+        double s = 0.0;
+        for (int b = 0; b < parts; ++b) s += ypart[(int64_t)b * ypart_ld + j];
+        yw[j] = s;
     }
     if (blockIdx.x == 0) {
         for (int i = threadIdx.x; i < l; i += blockDim.x) {
             double s = 0.0;
             for (int b = 0; b < parts; ++b) s += wpart[(int64_t)b * wpart_ld + i];
-            w[i] = s;
+            yw[wofs + i] = s;
         }
     }
 }
 
-// ---------------------------------------------------------------- N5a: correction + partial dots
-// mode 0 (iterate): y_j -= sum_i V[j,i] S_i w_i.   mode 1 (init) / 2 (raw): no correction.
-// Block partials part[b] = { sum y_j^2, sum v_j y_j, (V^T y)_0..l-1 } over the block's j range.
-constexpr int kFinThreads = 256;
-__global__ void __launch_bounds__(kFinThreads)
-    fin_partial(int mode, int n, int l, const double *__restrict__ S, const double *__restrict__ V, int ldv,
-                const double *__restrict__ w, double *__restrict__ y, const double *__restrict__ v,
-                double *__restrict__ part, int part_ld, const int32_t *done) {
-    if (done != nullptr && *done) return;
+// ---------------------------------------------------------------- N5: fin_iter
+enum FinMode { FIN_ITERATE = 0, FIN_INIT = 1, FIN_LOAD_RAW = 2, FIN_APPLY = 3 };
+
+struct FinParams {
+    int mode;
+    int n, l;
+    const double *S;          // sigma[0..l)
+    const double *V;          // n x ldv fp64 row-major
+    int ldv;
+    const double *ypart;      // FUSED: per-CTA partials of N1
+    int parts;
+    int64_t ypart_ld;
+    const double *wpart;
+    int wpart_ld;
+    const double *yw;         // !FUSED: all-reduced [y | w]
+    int64_t wofs;
+    const double *xsrc;       // FIN_INIT / FIN_LOAD_RAW: vector to load
+    double *ybuf;             // [2][ystride]
+    int64_t ystride;
+    double *part;             // [gridDim.x][part_ld]
+    int part_ld;
+    double *c;                // out: c = S V^T v1
+    LoopState *st;
+    double eps;
+    int fixed_T, max_iter;
+    unsigned long long cond;
+    int use_cond;
+};
+
+// FIN_ITERATE : y_new = reduce(partials) - V (S w) -> ybuf[(it+1)&1]; stop test; it += 1
+// FIN_INIT    : ybuf[0] = x; ||x||, c = S V^T (x/||x||); it = 0   (P:112 normalisation)
+// FIN_LOAD_RAW: ybuf[0] = v, ny := 1, c = S V^T v                          (tsvd_gram_apply)
+// FIN_APPLY   : ybuf[1] = reduce(partials) - V (S w); no state change     (tsvd_gram_apply)
+template <bool FUSED>
+__global__ void __launch_bounds__(kFinThreads) fin_iter(const FinParams p) {
     __shared__ double ys[kFinThreads];
     __shared__ double red[2][kFinThreads / 32];
-    extern __shared__ double g[];  // l values of S_i w_i
+    __shared__ int am_last;
+    extern __shared__ double dyn[];  // g[l] then tot[2 + l]
+    double *g = dyn;
+    double *tot = dyn + p.l;
+    LoopState *st = p.st;
     const int tid = threadIdx.x;
-    for (int i = tid; i < l; i += kFinThreads) g[i] = (mode == 0) ? S[i] * w[i] : 0.0;
-    __syncthreads();
+    if (st->stop || (p.mode == FIN_ITERATE && st->done)) {
+        if (blockIdx.x == 0 && tid == 0) set_cond(p.cond, p.use_cond, 0u);
+        return;
+    }
+    const int mode = p.mode, n = p.n, l = p.l;
+    const int it = st->it;
+    const double ny = st->ny;
+    const double *ycur = p.ybuf + (int64_t)(it & 1) * p.ystride;
+    double *ynew = p.ybuf + (int64_t)(mode == FIN_ITERATE ? ((it + 1) & 1) : (mode == FIN_APPLY ? 1 : 0)) * p.ystride;
+
+    const bool reduce = (mode == FIN_ITERATE || mode == FIN_APPLY);
+    if (reduce) {
+        for (int i = tid; i < l; i += kFinThreads) {
+            double w;
+            if (FUSED) {
+                w = 0.0;
+                for (int b = 0; b < p.parts; ++b) w += p.wpart[(int64_t)b * p.wpart_ld + i];
+            } else {
+                w = p.yw[p.wofs + i];
+            }
+            g[i] = p.S[i] * w;
+        }
+        __syncthreads();
+    }
     const int j0 = blockIdx.x * kFinThreads;
     const int j = j0 + tid;
     double yj = 0.0, vj = 0.0;
     if (j < n) {
-        yj = y[j];
-        if (mode == 0 && l > 0) {
-            double corr = 0.0;
-            for (int i = 0; i < l; ++i) corr += V[(int64_t)j * ldv + i] * g[i];
+        if (reduce) {
+            if (FUSED) {
+                const double *col = p.ypart + j;
+                double s0 = 0.0;
+                for (int b = 0; b < p.parts; ++b) s0 += col[(int64_t)b * p.ypart_ld];
+                yj = s0;
+            } else {
+                yj = p.yw[j];
+            }
+            double corr = 0.0;  // (V (S w))_j: the 2nd / 4th terms of Eq. 2 in factored form
+            for (int i = 0; i < l; ++i) corr += p.V[(int64_t)j * p.ldv + i] * g[i];
             yj -= corr;
-            y[j] = yj;
+            if (mode == FIN_ITERATE) vj = ycur[j] / ny;
+        } else {
+            yj = p.xsrc[j];
         }
-        vj = (mode == 0) ? v[j] : 0.0;
+        ynew[j] = yj;
     }
+    if (mode == FIN_APPLY) return;
     ys[tid] = yj;
-    double a = warp_sum(yj * yj), b = warp_sum(vj * yj);
+    const double a = warp_sum(yj * yj), b = warp_sum(vj * yj);
     if ((tid & 31) == 0) {
         red[0][tid >> 5] = a;
         red[1][tid >> 5] = b;
     }
     __syncthreads();
-    double *out = part + (int64_t)blockIdx.x * part_ld;
+    double *out = p.part + (int64_t)blockIdx.x * p.part_ld;
     if (tid == 0) {
         double s0 = 0.0, s1 = 0.0;
         for (int k = 0; k < kFinThreads / 32; ++k) {
@@ -316,87 +416,83 @@ __global__ void __launch_bounds__(kFinThreads)
     const int jn = (n - j0) < kFinThreads ? (n - j0) : kFinThreads;
     for (int i = tid; i < l; i += kFinThreads) {  // (V^T y)_i over this block's rows, coalesced in i
         double s = 0.0;
-        for (int jj = 0; jj < jn; ++jj) s += V[(int64_t)(j0 + jj) * ldv + i] * ys[jj];
+        for (int jj = 0; jj < jn; ++jj) s += p.V[(int64_t)(j0 + jj) * p.ldv + i] * ys[jj];
         out[2 + i] = s;
     }
-}
-
-// ---------------------------------------------------------------- N5b: scalars + stop test
-// mode 0 iterate, 1 init (normalise x), 2 raw (no normalisation; gram_apply).
-__global__ void __launch_bounds__(kFinThreads)
-    fin_scalar(int mode, int parts, int part_ld, int l, const double *__restrict__ S, const double *__restrict__ part,
-               double *__restrict__ c, LoopState *st, double eps, int fixed_T, int max_iter,
-               unsigned long long cond_handle, int use_cond) {
-    __shared__ double tot[2];
-    __shared__ double inv_s;
-    const int tid = threadIdx.x;
-    if (st->done && mode == 0) return;
+    // ---- last block to arrive takes the scalar decisions (sums in block order: deterministic)
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) am_last = (atomicAdd(&st->counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
     for (int q = tid; q < 2 + l; q += kFinThreads) {
         double s = 0.0;
-        for (int b = 0; b < parts; ++b) s += part[(int64_t)b * part_ld + q];  // fixed order
-        if (q < 2) tot[q] = s;
-        else c[q - 2] = s;  // raw V^T y for now
+        for (int bb = 0; bb < (int)gridDim.x; ++bb) s += __ldcg(p.part + (int64_t)bb * p.part_ld + q);
+        tot[q] = s;
     }
     __syncthreads();
+    __shared__ double inv_s;
     if (tid == 0) {
+        st->counter = 0;
         const double yy = tot[0];
-        double ny = sqrt(yy);
-        if (mode == 2) ny = 1.0;
-        st->yy = yy;
-        st->ny = ny;
-        if (mode == 1) {
+        double nyn = sqrt(yy);
+        if (mode == FIN_LOAD_RAW) {
+            st->ny = 1.0;
             st->it = 0;
             st->done = 0;
-            st->status = (isfinite(ny) && ny > 0.0) ? 0 : -7;
-            if (st->status) st->done = 1;
+            st->status = 0;
+            inv_s = 1.0;
+        } else if (mode == FIN_INIT) {
+            st->ny = nyn;
+            st->it = 0;
+            st->done = 0;
             st->d = 0.0;
-        } else if (mode == 0) {
-            const int it = st->it + 1;
-            st->it = it;
-            if (!isfinite(ny)) {
+            if (!(nyn > 0.0) || !isfinite(nyn)) {  // zero or non-finite initial sample
                 st->status = -7;
-                st->done = 1;
-            } else if (ny == 0.0) {
-                st->status = 2;
+                st->stop = 1;
                 st->done = 1;
             } else {
-                const double d = fabs(tot[1]) / ny;  // |v0 . v1| with v1 = y / ||y||
+                st->status = 0;
+            }
+            inv_s = (nyn > 0.0 && isfinite(nyn)) ? nyn : 1.0;
+        } else {  // FIN_ITERATE
+            const int itn = it + 1;
+            st->it = itn;
+            if (!isfinite(nyn)) {
+                st->status = -7;
+                st->stop = 1;
+                st->done = 1;
+            } else if (nyn == 0.0) {  // X'^T X' v = 0: rank exhausted (reading R14)
+                st->status = 2;
+                st->stop = 1;
+                st->done = 1;
+            } else {
+                st->ny = nyn;
+                const double d = fabs(tot[1]) / nyn;  // |v0 . v1| with v1 = y / ||y||
                 st->d = d;
-                if (fixed_T > 0) {
-                    if (it >= fixed_T) st->done = 1;
-                } else if (d >= 1.0 - eps) {
+                if (p.fixed_T > 0) {
+                    if (itn >= p.fixed_T) st->done = 1;
+                } else if (d >= 1.0 - p.eps) {
                     st->done = 1;
-                } else if (it >= max_iter) {
+                } else if (itn >= p.max_iter) {
                     st->done = 1;
                     st->status = 1;
                 }
             }
+            inv_s = (nyn > 0.0 && isfinite(nyn)) ? nyn : 1.0;
+            set_cond(p.cond, p.use_cond, (st->done || st->stop) ? 0u : 1u);
         }
-        inv_s = (ny > 0.0 && isfinite(ny)) ? ny : 1.0;
-#if CUDART_VERSION >= 12030
-        if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond_handle, st->done ? 0u : 1u);
-#endif
     }
     __syncthreads();
-    for (int i = tid; i < l; i += kFinThreads) c[i] = S[i] * (c[i] / inv_s);  // c = S V^T v1
-}
-
-// ---------------------------------------------------------------- N5c: v1 = y / ||y||
-// Writes the fp64 master (for the stop test) and the fp32 copy fed to N1.
-__global__ void fin_normalize(int n, const double *__restrict__ y, const LoopState *st, double *__restrict__ v,
-                              float *__restrict__ v32, int skip_when_failed) {
-    const double ny = st->ny;
-    if (skip_when_failed && (st->status < 0 || st->status == 2)) return;
-    const double inv = (ny > 0.0 && isfinite(ny)) ? ny : 1.0;
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-        const double x = y[j] / inv;
-        v[j] = x;
-        v32[j] = (float)x;
-    }
+    for (int i = tid; i < l; i += kFinThreads) p.c[i] = p.S[i] * (tot[2 + i] / inv_s);  // c = S V^T v1
 }
 
 // ---------------------------------------------------------------- N6: extraction tail
-__global__ void ext_reduce(const double *__restrict__ sq_part, int parts, double *__restrict__ sig2) {
+// multi-GPU: local sum of the per-CTA ||u||^2 partials (then all-reduced)
+__global__ void ext_reduce(const double *__restrict__ sq_part, int parts, double *__restrict__ sig2,
+                           const LoopState *st) {
+    if (st->stop) return;
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         double s = 0.0;
         for (int b = 0; b < parts; ++b) s += sq_part[b];
@@ -404,22 +500,69 @@ __global__ void ext_reduce(const double *__restrict__ sq_part, int parts, double
     }
 }
 
-// U[r, l] = u_r / sigma (fp32 storage), V[j, l] = v1_j, S[l] = sigma
-__global__ void ext_scale(int64_t rows, int n, int l, const double *__restrict__ u, const double *__restrict__ sig2,
-                          const double *__restrict__ v, float *__restrict__ U, int ldu, double *__restrict__ V,
-                          int ldv, double *__restrict__ S) {
-    const double sigma = sqrt(*sig2);
-    const double inv = sigma > 0.0 ? sigma : 1.0;
+struct ExtParams {
+    int64_t rows;
+    int n, l;
+    const double *u;         // (A v1)_r
+    const double *sq_part;   // FUSED: per-CTA sums of u_r^2
+    int parts;
+    const double *sig2;      // !FUSED: all-reduced ||u||^2
+    const double *ybuf;
+    int64_t ystride;
+    float *U;                // m_g x ldu
+    int ldu;
+    double *V;               // n x ldv
+    int ldv;
+    double *S;
+    CompStat *stat;          // stat[l]
+    LoopState *st;
+};
+
+// sigma = ||A v1||, U[r,l] = (A v1)_r / sigma, V[j,l] = v1_j, S[l] = sigma
+template <bool FUSED>
+__global__ void ext_finish(const ExtParams p) {
+    LoopState *st = p.st;
+    if (st->stop) {  // a previous step hit rank exhaustion / non-finite: record and skip
+        if (blockIdx.x == 0 && threadIdx.x == 0 && !p.stat[p.l].valid) {
+            p.stat[p.l].status = st->status;
+            p.stat[p.l].it = st->it;
+        }
+        return;
+    }
+    double sig2;
+    if (FUSED) {
+        sig2 = 0.0;
+        for (int b = 0; b < p.parts; ++b) sig2 += p.sq_part[b];  // every block, same order
+    } else {
+        sig2 = *p.sig2;
+    }
+    const double sigma = sqrt(sig2);
+    if (!(sigma > 0.0) || !isfinite(sigma)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            st->status = isfinite(sigma) ? 2 : -7;
+            st->stop = 1;
+            p.stat[p.l].status = st->status;
+            p.stat[p.l].it = st->it;
+        }
+        return;
+    }
+    const double ny = st->ny;
+    const double *ycur = p.ybuf + (int64_t)(st->it & 1) * p.ystride;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (int64_t r = g; r < rows; r += stride) U[r * ldu + l] = (float)(u[r] / inv);
-    for (int64_t j = g; j < n; j += stride) V[j * ldv + l] = v[j];
-    if (g == 0) S[l] = sigma;
-}
-
-// fp64 -> fp32 copy of a vector (gram_apply input path)
-__global__ void to_f32(int n, const double *__restrict__ x, float *__restrict__ y) {
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) y[j] = (float)x[j];
+    for (int64_t r = g; r < p.rows; r += stride) p.U[r * p.ldu + p.l] = (float)(p.u[r] / sigma);
+    for (int64_t j = g; j < p.n; j += stride) p.V[j * p.ldv + p.l] = ycur[j] / ny;
+    if (g == 0) {
+        p.S[p.l] = sigma;
+        CompStat cs;
+        cs.d = st->d;
+        cs.sigma = sigma;
+        cs.it = st->it;
+        cs.status = st->status;
+        cs.valid = 1;
+        cs.pad = 0;
+        p.stat[p.l] = cs;
+    }
 }
 
 }  // namespace tsvd

@@ -1,10 +1,11 @@
 // tsvd.cu — libtsvd.so: the C ABI of include/tsvd.h and the Alg. 1 / Alg. 2 driver.
 //
-// The driver is host code that only plans, allocates and launches; every arithmetic step of
-// the power iteration (Gram-vector product, reductions, normalisation, stop test, extraction)
-// runs in the kernels of gram_kernels.cuh.  One process per GPU; multi-GPU = row partition
-// with one NCCL all-reduce of [y_g | w_g] per iteration (merges Alg. 4 lines 6, 8,
-// 16).
+// The driver is host code that only plans, allocates and launches; every arithmetic step of the
+// power iteration (Gram-vector product, reductions, normalisation, stop test, extraction) runs
+// in the kernels of gram_kernels.cuh.  A whole tsvd_run (all k components: init, power-iteration
+// WHILE loop, extraction) is ONE CUDA graph with one conditional WHILE node per component, so
+// the host synchronises once per run.  One process per GPU; multi-GPU = row partition
+// with one NCCL all-reduce of [y_g | w_g] per iteration (merges Alg. 4 lines 6, 8, 16).
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -27,6 +28,7 @@ namespace {
 constexpr int kMaxThreadsPerCta = 512;
 constexpr int kRingTargetBytes = 192 * 1024;  // bytes in flight per SM (Little's law)
 constexpr int kSmemBudget = 220 * 1024;       // per SM, leaves room for barriers/scratch
+constexpr int kMaxK = 4096;                   // fin_iter keeps 2k+2 doubles in shared memory
 
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -70,7 +72,7 @@ struct tsvd_s {
     double eps = 1e-6;
     // device / comm
     int dev = 0, sms = 148;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr, body_stream = nullptr;
     int32_t rank = 0, world = 1;
     ncclComm_t comm = nullptr;
     // options
@@ -88,25 +90,32 @@ struct tsvd_s {
     int64_t ld_use = 0;
     std::vector<double> V0;
     bool have_V0 = false;
+    int64_t v0_version = 1, v0_uploaded = 0;
     // factors (device)
     float *U32 = nullptr;   // m_g x kpad
     double *V64 = nullptr;  // n x k
     double *S64 = nullptr;  // k
     int32_t l_found = 0;
     // vectors / workspaces (device)
-    double *v64 = nullptr, *yw = nullptr, *c64 = nullptr, *ypart = nullptr, *wpart = nullptr, *part = nullptr;
-    double *u64 = nullptr, *sq_part = nullptr, *sig2 = nullptr;
-    float *v32 = nullptr;
+    double *ybuf = nullptr, *yw = nullptr, *V0d = nullptr, *c64 = nullptr, *ypart = nullptr, *wpart = nullptr;
+    double *part = nullptr, *u64 = nullptr, *sq_part = nullptr, *sig2 = nullptr;
     LoopState *st = nullptr;
-    LoopState *st_host = nullptr;  // pinned
-    double *x_host = nullptr;      // pinned staging for initial vectors
-    int64_t wofs = 0;              // offset of w inside yw
+    CompStat *stats = nullptr;
+    LoopState *st_host = nullptr;      // pinned
+    CompStat *stats_host = nullptr;    // pinned
+    double *vec_host = nullptr;        // pinned staging (n doubles)
+    int64_t ystride = 0, wofs = 0, ypart_ld = 0;
     int fin_blocks = 0, part_ld = 0;
     bool allocated = false;
     // plan
     int T = 0, NV = 0, S = 0, grid = 0, cps = 0, stage_bytes = 0, row_bytes = 0;
     size_t smem = 0;
     GvFn gv = nullptr, gv_ex = nullptr;
+    // run graph (cached by starting component)
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int graph_l0 = -1;
+    std::string graph_error;
     // results / report
     std::vector<int32_t> iters;
     std::vector<double> dots;
@@ -163,6 +172,9 @@ static tsvd_status plan(tsvd_t h) {
                                                                      ((int64_t)h->stage_bytes * cps)));
     while ((int64_t)S * h->stage_bytes * cps > kSmemBudget && S > 2) --S;
     while ((int64_t)S * h->stage_bytes * cps > kSmemBudget && cps > 1) --cps;
+    if ((int64_t)S * h->stage_bytes > kSmemBudget)
+        return h->fail(TSVD_ERR_UNSUPPORTED, "k = %d too large for the shared-memory ring at n = %lld", h->k,
+                       (long long)n);
     h->T = T;
     h->NV = NV;
     h->S = S;
@@ -171,6 +183,9 @@ static tsvd_status plan(tsvd_t h) {
     h->gv_ex = pick_gv<true>(T, NV);
     CK(cudaFuncSetAttribute(h->gv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem));
     CK(cudaFuncSetAttribute(h->gv_ex, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem));
+    const int fin_dyn = (2 * h->k + 2) * (int)sizeof(double);
+    CK(cudaFuncSetAttribute(fin_iter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_dyn));
+    CK(cudaFuncSetAttribute(fin_iter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_dyn));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->gv, T, h->smem));
     if (occ < 1) return h->fail(TSVD_ERR_UNSUPPORTED, "fused kernel does not fit on an SM (T=%d smem=%zu)", T, h->smem);
@@ -179,45 +194,54 @@ static tsvd_status plan(tsvd_t h) {
     return TSVD_OK;
 }
 
+static tsvd_status reset_state(tsvd_t h) {
+    LoopState s{};
+    s.ny = 1.0;
+    *h->st_host = s;
+    CK(cudaMemcpyAsync(h->st, h->st_host, sizeof(LoopState), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return TSVD_OK;
+}
+
 static tsvd_status ensure_alloc(tsvd_t h) {
     if (h->allocated) return TSVD_OK;
     TRY(plan(h));
     const int64_t n = h->n, mg = h->m_g;
-    const int64_t vpad = std::max<int64_t>(round_up(n, 4), (int64_t)4 * h->T * h->NV);
+    h->ystride = round_up(n, 32);
     h->wofs = round_up(n, 32);
+    h->ypart_ld = round_up(n, 4);
     h->fin_blocks = (int)((n + kFinThreads - 1) / kFinThreads);
     h->part_ld = 2 + h->kpad;
-    const int64_t ypart_ld = round_up(n, 4);
     auto dm = [&](void **p, size_t bytes) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(bytes, 16)); };
     cudaError_t e = cudaSuccess;
     if (!e) e = dm((void **)&h->U32, (size_t)mg * h->kpad * sizeof(float));
     if (!e) e = dm((void **)&h->V64, (size_t)n * h->k * sizeof(double));
     if (!e) e = dm((void **)&h->S64, (size_t)h->k * sizeof(double));
-    if (!e) e = dm((void **)&h->v64, (size_t)n * sizeof(double));
-    if (!e) e = dm((void **)&h->v32, (size_t)vpad * sizeof(float));
+    if (!e) e = dm((void **)&h->ybuf, (size_t)2 * h->ystride * sizeof(double));
     if (!e) e = dm((void **)&h->yw, (size_t)(h->wofs + h->kpad) * sizeof(double));
+    if (!e) e = dm((void **)&h->V0d, (size_t)h->k * n * sizeof(double));
     if (!e) e = dm((void **)&h->c64, (size_t)h->kpad * sizeof(double));
-    if (!e) e = dm((void **)&h->ypart, (size_t)h->grid * ypart_ld * sizeof(double));
+    if (!e) e = dm((void **)&h->ypart, (size_t)h->grid * h->ypart_ld * sizeof(double));
     if (!e) e = dm((void **)&h->wpart, (size_t)h->grid * h->kpad * sizeof(double));
     if (!e) e = dm((void **)&h->part, (size_t)h->fin_blocks * h->part_ld * sizeof(double));
     if (!e) e = dm((void **)&h->u64, (size_t)mg * sizeof(double));
     if (!e) e = dm((void **)&h->sq_part, (size_t)h->grid * sizeof(double));
     if (!e) e = dm((void **)&h->sig2, sizeof(double));
     if (!e) e = dm((void **)&h->st, sizeof(LoopState));
-    if (!e) e = cudaMallocHost((void **)&h->st_host, sizeof(LoopState) + 2 * sizeof(double));
-    if (!e) e = cudaMallocHost((void **)&h->x_host, (size_t)n * sizeof(double));
+    if (!e) e = dm((void **)&h->stats, (size_t)h->k * sizeof(CompStat));
+    if (!e) e = cudaMallocHost((void **)&h->st_host, sizeof(LoopState));
+    if (!e) e = cudaMallocHost((void **)&h->stats_host, (size_t)h->k * sizeof(CompStat));
+    if (!e) e = cudaMallocHost((void **)&h->vec_host, (size_t)n * sizeof(double));
     if (e == cudaErrorMemoryAllocation) return h->fail(TSVD_ERR_NOMEM, "device workspace allocation failed");
     CK(e);
     CK(cudaMemsetAsync(h->U32, 0, (size_t)mg * h->kpad * sizeof(float), h->stream));
     CK(cudaMemsetAsync(h->V64, 0, (size_t)n * h->k * sizeof(double), h->stream));
     CK(cudaMemsetAsync(h->S64, 0, (size_t)h->k * sizeof(double), h->stream));
-    CK(cudaMemsetAsync(h->v32, 0, (size_t)vpad * sizeof(float), h->stream));
-    CK(cudaMemsetAsync(h->v64, 0, (size_t)n * sizeof(double), h->stream));
+    CK(cudaMemsetAsync(h->ybuf, 0, (size_t)2 * h->ystride * sizeof(double), h->stream));
     CK(cudaMemsetAsync(h->c64, 0, (size_t)h->kpad * sizeof(double), h->stream));
     CK(cudaMemsetAsync(h->yw, 0, (size_t)(h->wofs + h->kpad) * sizeof(double), h->stream));
-    CK(cudaMemsetAsync(h->st, 0, sizeof(LoopState), h->stream));
     h->allocated = true;
-    return TSVD_OK;
+    return reset_state(h);
 }
 
 // Make A resident on the device for this run (host input: H2D copy, counted in e2e timing).
@@ -236,6 +260,7 @@ static tsvd_status stage_A(tsvd_t h) {
         if (e == cudaErrorMemoryAllocation) return h->fail(TSVD_ERR_NOMEM, "A device buffer allocation failed");
         CK(e);
         if (h->ld_own != h->n) CK(cudaMemsetAsync(h->A_own, 0, bytes, h->stream));
+        h->graph_l0 = -1;  // A pointer changed: the cached run graph is stale
     }
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
@@ -256,7 +281,7 @@ static tsvd_status stage_A(tsvd_t h) {
 }
 
 // ------------------------------------------------------------------------------------ launches
-static GvParams gv_params(tsvd_t h, int l, bool extract, const int32_t *done) {
+static GvParams gv_params(tsvd_t h, int l, bool extract) {
     GvParams p{};
     p.A = h->A_use;
     p.ld = h->ld_use;
@@ -266,10 +291,12 @@ static GvParams gv_params(tsvd_t h, int l, bool extract, const int32_t *done) {
     p.U = h->U32;
     p.ldu = h->kpad;
     p.l = extract ? 0 : l;
-    p.v32 = h->v32;
+    p.ybuf = h->ybuf;
+    p.ystride = h->ystride;
+    p.st = h->st;
     p.c = h->c64;
     p.ypart = h->ypart;
-    p.ypart_ld = round_up(h->n, 4);
+    p.ypart_ld = h->ypart_ld;
     p.wpart = h->wpart;
     p.wpart_ld = h->kpad;
     p.stages = h->S;
@@ -279,150 +306,238 @@ static GvParams gv_params(tsvd_t h, int l, bool extract, const int32_t *done) {
     p.run_rows = h->run_rows;
     p.u_out = h->u64;
     p.sq_part = h->sq_part;
-    p.done = done;
     return p;
 }
 
-static tsvd_status launch_gv(tsvd_t h, int l, const int32_t *done) {
-    GvParams p = gv_params(h, l, false, done);
-    h->gv<<<h->grid, h->T, h->smem, h->stream>>>(p);
+static tsvd_status launch_gv(tsvd_t h, cudaStream_t s, int l, bool extract) {
+    GvParams p = gv_params(h, l, extract);
+    (extract ? h->gv_ex : h->gv)<<<h->grid, h->T, h->smem, s>>>(p);
     CK(cudaGetLastError());
     return TSVD_OK;
 }
 
-static tsvd_status allreduce(tsvd_t h, double *buf, size_t count) {
+static tsvd_status allreduce(tsvd_t h, cudaStream_t s, double *buf, size_t count) {
     if (h->world <= 1) return TSVD_OK;
-    NK(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, h->comm, h->stream));
+    NK(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, h->comm, s));
     return TSVD_OK;
 }
 
-// Everything after N1 in one iteration: N7, all-reduce, N5a-c.
-static tsvd_status launch_tail(tsvd_t h, int l, int fin_mode, const int32_t *done, unsigned long long cond, int use_cond) {
-    const int n = (int)h->n;
-    double *y = h->yw, *w = h->yw + h->wofs;
-    reduce_partials<<<(n + 255) / 256, 256, 0, h->stream>>>(h->ypart, h->grid, round_up(n, 4), n, h->wpart, h->kpad, l,
-                                                           y, w, done);
+static FinParams fin_params(tsvd_t h, int mode, int l, const double *xsrc, unsigned long long cond, int use_cond) {
+    FinParams p{};
+    p.mode = mode;
+    p.n = (int)h->n;
+    p.l = l;
+    p.S = h->S64;
+    p.V = h->V64;
+    p.ldv = h->k;
+    p.ypart = h->ypart;
+    p.parts = h->grid;
+    p.ypart_ld = h->ypart_ld;
+    p.wpart = h->wpart;
+    p.wpart_ld = h->kpad;
+    p.yw = h->yw;
+    p.wofs = h->wofs;
+    p.xsrc = xsrc;
+    p.ybuf = h->ybuf;
+    p.ystride = h->ystride;
+    p.part = h->part;
+    p.part_ld = h->part_ld;
+    p.c = h->c64;
+    p.st = h->st;
+    p.eps = h->eps;
+    p.fixed_T = h->fixed_T;
+    p.max_iter = h->max_iter;
+    p.cond = cond;
+    p.use_cond = use_cond;
+    return p;
+}
+
+static tsvd_status launch_fin(tsvd_t h, cudaStream_t s, const FinParams &p, bool fused) {
+    const size_t dyn = (size_t)(2 * p.l + 2) * sizeof(double);
+    if (fused) fin_iter<true><<<h->fin_blocks, kFinThreads, dyn, s>>>(p);
+    else fin_iter<false><<<h->fin_blocks, kFinThreads, dyn, s>>>(p);
     CK(cudaGetLastError());
-    TRY(allreduce(h, h->yw, (size_t)(h->wofs + h->kpad)));
-    fin_partial<<<h->fin_blocks, kFinThreads, (size_t)std::max(l, 1) * sizeof(double), h->stream>>>(
-        fin_mode, n, l, h->S64, h->V64, h->k, w, y, h->v64, h->part, h->part_ld, done);
-    CK(cudaGetLastError());
-    if (fin_mode == 0) {
-        fin_scalar<<<1, kFinThreads, 0, h->stream>>>(0, h->fin_blocks, h->part_ld, l, h->S64, h->part, h->c64, h->st,
-                                                     h->eps, h->fixed_T, h->max_iter, cond, use_cond);
+    return TSVD_OK;
+}
+
+// One power iteration: N1, [local partial sum + all-reduce], fin_iter.
+static tsvd_status launch_iteration(tsvd_t h, cudaStream_t s, int l, unsigned long long cond, int use_cond,
+                                    cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr) {
+    if (e0) CK(cudaEventRecord(e0, s));
+    TRY(launch_gv(h, s, l, false));
+    if (e1) CK(cudaEventRecord(e1, s));
+    const bool fused = h->world == 1;
+    if (!fused) {
+        reduce_partials<<<(int)((h->n + 255) / 256), 256, 0, s>>>(h->ypart, h->grid, h->ypart_ld, (int)h->n, h->wpart,
+                                                                  h->kpad, l, h->yw, h->wofs, h->st);
         CK(cudaGetLastError());
-        fin_normalize<<<std::min(h->fin_blocks, 1184), kFinThreads, 0, h->stream>>>(n, y, h->st, h->v64, h->v32, 1);
+        TRY(allreduce(h, s, h->yw, (size_t)(h->wofs + h->kpad)));
+    }
+    return launch_fin(h, s, fin_params(h, FIN_ITERATE, l, nullptr, cond, use_cond), fused);
+}
+
+// x_l (device, fp64) -> y_cur = x, ||x||, c = S V^T (x / ||x||)
+static tsvd_status launch_init(tsvd_t h, cudaStream_t s, int l) {
+    return launch_fin(h, s, fin_params(h, FIN_INIT, l, h->V0d + (size_t)l * h->n, 0ull, 0), true);
+}
+
+static tsvd_status launch_extract(tsvd_t h, cudaStream_t s, int l) {
+    TRY(launch_gv(h, s, l, true));
+    ExtParams p{};
+    p.rows = h->m_g;
+    p.n = (int)h->n;
+    p.l = l;
+    p.u = h->u64;
+    p.sq_part = h->sq_part;
+    p.parts = h->grid;
+    p.sig2 = h->sig2;
+    p.ybuf = h->ybuf;
+    p.ystride = h->ystride;
+    p.U = h->U32;
+    p.ldu = h->kpad;
+    p.V = h->V64;
+    p.ldv = h->k;
+    p.S = h->S64;
+    p.stat = h->stats;
+    p.st = h->st;
+    const int64_t work = std::max<int64_t>(h->m_g, h->n);
+    const int blocks = (int)std::min<int64_t>((work + 255) / 256, (int64_t)h->sms * 8);
+    if (h->world == 1) {
+        ext_finish<true><<<blocks, 256, 0, s>>>(p);
+    } else {
+        ext_reduce<<<1, 32, 0, s>>>(h->sq_part, h->grid, h->sig2, h->st);
         CK(cudaGetLastError());
+        TRY(allreduce(h, s, h->sig2, 1));
+        ext_finish<false><<<blocks, 256, 0, s>>>(p);
     }
-    return TSVD_OK;
-}
-
-// x (host, fp64) -> v = x / ||x|| and c = S (V^T v), all on the device.
-static tsvd_status init_component(tsvd_t h, int l, const double *x) {
-    const int n = (int)h->n;
-    memcpy(h->x_host, x, (size_t)n * sizeof(double));
-    CK(cudaMemcpyAsync(h->yw, h->x_host, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-    fin_partial<<<h->fin_blocks, kFinThreads, (size_t)std::max(l, 1) * sizeof(double), h->stream>>>(
-        1, n, l, h->S64, h->V64, h->k, h->yw + h->wofs, h->yw, h->v64, h->part, h->part_ld, nullptr);
-    CK(cudaGetLastError());
-    fin_scalar<<<1, kFinThreads, 0, h->stream>>>(1, h->fin_blocks, h->part_ld, l, h->S64, h->part, h->c64, h->st,
-                                                 h->eps, h->fixed_T, h->max_iter, 0ull, 0);
-    CK(cudaGetLastError());
-    fin_normalize<<<std::min(h->fin_blocks, 1184), kFinThreads, 0, h->stream>>>(n, h->yw, h->st, h->v64, h->v32, 0);
     CK(cudaGetLastError());
     return TSVD_OK;
 }
 
-static void gen_x(uint64_t seed, int l, int64_t n, double *x) {
-    const uint64_t key = splitmix64(splitmix64(seed) ^ (uint64_t)l);
-    const double two_pi = 6.283185307179586476925286766559;
-    for (int64_t i = 0; i < n; i += 2) {
-        const double u1 = (double)(splitmix64(key ^ (uint64_t)i) >> 11) * 0x1.0p-53;
-        const double u2 = (double)(splitmix64(key ^ (uint64_t)(i + 1)) >> 11) * 0x1.0p-53;
-        const double r = std::sqrt(-2.0 * std::log(1.0 - u1));
-        x[i] = r * std::cos(two_pi * u2);
-        if (i + 1 < n) x[i + 1] = r * std::sin(two_pi * u2);
+// Upload the initial samples x_l of every component once per V0 version.
+static tsvd_status upload_v0(tsvd_t h) {
+    if (h->v0_uploaded == h->v0_version) return TSVD_OK;
+    const int64_t n = h->n;
+    if (h->have_V0) {
+        CK(cudaMemcpyAsync(h->V0d, h->V0.data(), (size_t)h->k * n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    } else {  // documented generator: splitmix64(seed, l, i) -> two 53-bit uniforms -> Box-Muller
+        std::vector<double> x((size_t)h->k * n);
+        const double two_pi = 6.283185307179586476925286766559;
+        for (int l = 0; l < h->k; ++l) {
+            const uint64_t key = splitmix64(splitmix64(h->seed) ^ (uint64_t)l);
+            double *xl = x.data() + (size_t)l * n;
+            for (int64_t i = 0; i < n; i += 2) {
+                const double u1 = (double)(splitmix64(key ^ (uint64_t)i) >> 11) * 0x1.0p-53;
+                const double u2 = (double)(splitmix64(key ^ (uint64_t)(i + 1)) >> 11) * 0x1.0p-53;
+                const double r = std::sqrt(-2.0 * std::log(1.0 - u1));
+                xl[i] = r * std::cos(two_pi * u2);
+                if (i + 1 < n) xl[i + 1] = r * std::sin(two_pi * u2);
+            }
+        }
+        CK(cudaMemcpyAsync(h->V0d, x.data(), x.size() * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
     }
+    h->v0_uploaded = h->v0_version;
+    return TSVD_OK;
 }
 
-// The power iteration of one component as a CUDA-graph WHILE loop (no host round trip).
-static tsvd_status iterate_graph(tsvd_t h, int l) {
+static void drop_graph(tsvd_t h) {
+    if (h->exec) cudaGraphExecDestroy(h->exec);
+    if (h->graph) cudaGraphDestroy(h->graph);
+    h->exec = nullptr;
+    h->graph = nullptr;
+    h->graph_l0 = -1;
+}
+
+// Capture components l0..k-1 as one graph: [init, WHILE(iteration), extraction] per component.
+static tsvd_status build_graph(tsvd_t h, int l0) {
 #if CUDART_VERSION >= 12040
+    drop_graph(h);
+    CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
+    tsvd_status s = TSVD_OK;
+    cudaError_t ce = cudaSuccess;
+    for (int l = l0; l < h->k && s >= 0 && ce == cudaSuccess; ++l) {
+        s = launch_init(h, h->stream, l);
+        if (s < 0) break;
+        cudaStreamCaptureStatus cs;
+        cudaGraph_t g = nullptr;
+        const cudaGraphNode_t *deps = nullptr;
+        size_t nd = 0;
+        ce = cudaStreamGetCaptureInfo(h->stream, &cs, nullptr, &g, &deps, &nd);
+        if (ce) break;
+        cudaGraphConditionalHandle ch;
+        ce = cudaGraphConditionalHandleCreate(&ch, g, 1, cudaGraphCondAssignDefault);
+        if (ce) break;
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = ch;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        ce = cudaGraphAddNode(&node, g, deps, nd, &cp);
+        if (ce) break;
+        ce = cudaStreamUpdateCaptureDependencies(h->stream, &node, 1, cudaStreamSetCaptureDependencies);
+        if (ce) break;
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        ce = cudaStreamBeginCaptureToGraph(h->body_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+        if (ce) break;
+        s = launch_iteration(h, h->body_stream, l, (unsigned long long)ch, 1);
+        cudaGraph_t body_out = nullptr;
+        cudaError_t ce2 = cudaStreamEndCapture(h->body_stream, &body_out);
+        if (s < 0) break;
+        ce = ce2;
+        if (ce) break;
+        s = launch_extract(h, h->stream, l);
+    }
     cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    CK(cudaGraphCreate(&graph, 0));
-    cudaGraphConditionalHandle cond;
-    CK(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
-    cudaGraphNodeParams cp = {};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = cond;
-    cp.conditional.type = cudaGraphCondTypeWhile;
-    cp.conditional.size = 1;
-    cudaGraphNode_t node;
-    CK(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
-    cudaGraph_t body = cp.conditional.phGraph_out[0];
-    CK(cudaStreamBeginCaptureToGraph(h->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    tsvd_status s = launch_gv(h, l, nullptr);
-    if (s >= 0) s = launch_tail(h, l, 0, nullptr, (unsigned long long)cond, 1);
-    cudaGraph_t captured = nullptr;
-    cudaError_t e = cudaStreamEndCapture(h->stream, &captured);
+    cudaError_t ce3 = cudaStreamEndCapture(h->stream, &graph);
     if (s < 0) {
-        cudaGraphDestroy(graph);
+        if (graph) cudaGraphDestroy(graph);
         return s;
     }
-    CK(e);
-    CK(cudaGraphInstantiate(&exec, graph, 0));
-    CK(cudaGraphLaunch(exec, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(graph);
-    h->loop_mode = "graph-while";
+    if (ce || ce3) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        return h->fail(TSVD_ERR_CUDA, "run-graph capture failed: %s", cudaGetErrorString(ce ? ce : ce3));
+    }
+    h->graph = graph;
+    CK(cudaGraphInstantiate(&h->exec, graph, 0));
+    h->graph_l0 = l0;
     return TSVD_OK;
 #else
     return h->fail(TSVD_ERR_UNSUPPORTED, "CUDA graph conditional nodes need CUDA >= 12.4");
 #endif
 }
 
-// Host-driven loop: one pinned D2H flag read per iteration; optional CUDA events around N1.
-static tsvd_status iterate_host(tsvd_t h, int l) {
+// Host-driven loop: one pinned D2H state read per iteration; optional CUDA events around N1.
+static tsvd_status run_host_loop(tsvd_t h, int l0) {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (h->timing) {
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
     }
-    for (;;) {
-        if (h->timing) CK(cudaEventRecord(e0, h->stream));
-        TRY(launch_gv(h, l, nullptr));
-        if (h->timing) CK(cudaEventRecord(e1, h->stream));
-        TRY(launch_tail(h, l, 0, nullptr, 0ull, 0));
+    for (int l = l0; l < h->k; ++l) {
+        TRY(launch_init(h, h->stream, l));
+        for (;;) {
+            TRY(launch_iteration(h, h->stream, l, 0ull, 0, e0, e1));
+            CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            if (h->timing && !h->st_host->stop) {
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, e0, e1));
+                h->n1_ms += ms;
+                h->n1_launches += 1;
+            }
+            if (h->st_host->done || h->st_host->stop) break;
+        }
+        TRY(launch_extract(h, h->stream, l));
         CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
-        if (h->timing) {
-            float ms = 0.f;
-            CK(cudaEventElapsedTime(&ms, e0, e1));
-            h->n1_ms += ms;
-            h->n1_launches += 1;
-        }
-        if (h->st_host->done) break;
+        if (h->st_host->stop) break;
     }
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
     h->loop_mode = h->timing ? "host+events" : "host";
-    return TSVD_OK;
-}
-
-static tsvd_status extract_component(tsvd_t h, int l) {
-    GvParams p = gv_params(h, l, true, nullptr);
-    h->gv_ex<<<h->grid, h->T, h->smem, h->stream>>>(p);
-    CK(cudaGetLastError());
-    ext_reduce<<<1, 32, 0, h->stream>>>(h->sq_part, h->grid, h->sig2);
-    CK(cudaGetLastError());
-    TRY(allreduce(h, h->sig2, 1));
-    const int64_t work = std::max<int64_t>(h->m_g, h->n);
-    const int blocks = (int)std::min<int64_t>((work + 255) / 256, (int64_t)h->sms * 8);
-    ext_scale<<<blocks, 256, 0, h->stream>>>(h->m_g, (int)h->n, l, h->u64, h->sig2, h->v64, h->U32, h->kpad, h->V64,
-                                           h->k, h->S64);
-    CK(cudaGetLastError());
     return TSVD_OK;
 }
 
@@ -445,14 +560,15 @@ tsvd_status tsvd_create(tsvd_t *out, int64_t m, int64_t n, int32_t k, double eps
         g_err = "only fp32 row-major with m >= n in this version";
         return TSVD_ERR_UNSUPPORTED;
     }
-    if (k == -1 && mn > INT32_MAX) {
-        g_err = "k too large";
-        return TSVD_ERR_ARG;
+    const int64_t kk = k == -1 ? mn : k;
+    if (kk > kMaxK) {
+        g_err = "k > 4096 is not supported";
+        return TSVD_ERR_UNSUPPORTED;
     }
     tsvd_t h = new tsvd_s();
     h->m = m;
     h->n = n;
-    h->k = k == -1 ? (int32_t)mn : k;
+    h->k = (int32_t)kk;
     h->kpad = (int32_t)round_up(h->k, 4);
     h->eps = eps;
     h->row_begin = 0;
@@ -463,6 +579,7 @@ tsvd_status tsvd_create(tsvd_t *out, int64_t m, int64_t n, int32_t k, double eps
     cudaError_t e = cudaGetDevice(&h->dev);
     if (!e) e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->dev);
     if (!e) e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+    if (!e) e = cudaStreamCreateWithFlags(&h->body_stream, cudaStreamNonBlocking);
     if (e) {
         g_err = std::string("CUDA: ") + cudaGetErrorString(e);
         delete h;
@@ -488,9 +605,11 @@ tsvd_status tsvd_set_comm(tsvd_t h, int32_t rank, int32_t world, const void *uid
     if (device != h->dev) {
         CK(cudaSetDevice(device));
         if (h->stream) cudaStreamDestroy(h->stream);
+        if (h->body_stream) cudaStreamDestroy(h->body_stream);
         h->dev = device;
         CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->dev));
         CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&h->body_stream, cudaStreamNonBlocking));
     }
     h->rank = rank;
     h->world = world;
@@ -513,7 +632,10 @@ tsvd_status tsvd_set_option(tsvd_t h, int32_t key, int64_t value) {
         if (value < 0 || value > INT32_MAX) return h->fail(TSVD_ERR_ARG, "FIXED_ITERS must be >= 0");
         h->fixed_T = (int)value;
         break;
-    case TSVD_OPT_SEED: h->seed = (uint64_t)value; break;
+    case TSVD_OPT_SEED:
+        h->seed = (uint64_t)value;
+        if (!h->have_V0) h->v0_version++;
+        break;
     case TSVD_OPT_GRAPH: h->use_graph = value != 0; break;
     case TSVD_OPT_TIMING: h->timing = value != 0; break;
     case TSVD_OPT_RUN_ROWS:
@@ -522,11 +644,12 @@ tsvd_status tsvd_set_option(tsvd_t h, int32_t key, int64_t value) {
         break;
     case TSVD_OPT_CTAS_PER_SM:
         if (value < 0 || value > 32) return h->fail(TSVD_ERR_ARG, "CTAS_PER_SM in [0, 32]");
-        if (h->allocated) return h->fail(TSVD_ERR_STATE, "CTAS_PER_SM must precede set_dense");
+        if (h->allocated) return h->fail(TSVD_ERR_STATE, "CTAS_PER_SM must precede the first run");
         h->cps_opt = (int)value;
         break;
     default: return h->fail(TSVD_ERR_ARG, "unknown option %d", key);
     }
+    h->graph_l0 = -1;  // options are baked into the captured kernel parameters
     return TSVD_OK;
 }
 
@@ -535,6 +658,7 @@ tsvd_status tsvd_set_init(tsvd_t h, const double *V0) {
     if (!V0) return h->fail(TSVD_ERR_ARG, "V0 == NULL");
     h->V0.assign(V0, V0 + (size_t)h->k * h->n);
     h->have_V0 = true;
+    h->v0_version++;
     return TSVD_OK;
 }
 
@@ -556,6 +680,7 @@ tsvd_status tsvd_set_dense(tsvd_t h, const float *A, int64_t ld, int64_t row_beg
     h->ld_user = ld;
     h->mem = mem;
     h->have_A = true;
+    h->graph_l0 = -1;
     if (mem == TSVD_MEM_DEVICE) {
         const bool aligned = ((uintptr_t)A % 16 == 0) && (ld % 4 == 0);
         if (aligned) {
@@ -600,6 +725,10 @@ tsvd_status tsvd_set_factors(tsvd_t h, int32_t l, const float *U, const double *
                              cudaMemcpyHostToDevice, h->stream));
         CK(cudaStreamSynchronize(h->stream));
     }
+    for (int i = l; i < h->k; ++i) {
+        h->iters[i] = 0;
+        h->dots[i] = 0.0;
+    }
     h->l_found = l;
     h->k_found = l;
     return TSVD_OK;
@@ -612,29 +741,24 @@ tsvd_status tsvd_gram_apply(tsvd_t h, const double *v, double *y) {
     CK(cudaSetDevice(h->dev));
     TRY(ensure_alloc(h));
     TRY(stage_A(h));
+    TRY(reset_state(h));
     const int n = (int)h->n, l = h->l_found;
-    CK(cudaMemcpyAsync(h->v64, v, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-    to_f32<<<std::min(h->fin_blocks, 1184), kFinThreads, 0, h->stream>>>(n, h->v64, h->v32);
-    CK(cudaGetLastError());
-    // c = S (V^T v) for the given (unnormalised) v
-    fin_partial<<<h->fin_blocks, kFinThreads, (size_t)std::max(l, 1) * sizeof(double), h->stream>>>(
-        2, n, l, h->S64, h->V64, h->k, h->yw + h->wofs, h->v64, h->v64, h->part, h->part_ld, nullptr);
-    CK(cudaGetLastError());
-    fin_scalar<<<1, kFinThreads, 0, h->stream>>>(2, h->fin_blocks, h->part_ld, l, h->S64, h->part, h->c64, h->st,
-                                                 h->eps, h->fixed_T, h->max_iter, 0ull, 0);
-    CK(cudaGetLastError());
-    TRY(launch_gv(h, l, nullptr));
-    const double *yw = h->yw;
-    const int nn = n;
-    reduce_partials<<<(nn + 255) / 256, 256, 0, h->stream>>>(h->ypart, h->grid, round_up(nn, 4), nn, h->wpart,
-                                                             h->kpad, l, h->yw, h->yw + h->wofs, nullptr);
-    CK(cudaGetLastError());
-    TRY(allreduce(h, h->yw, (size_t)(h->wofs + h->kpad)));
-    fin_partial<<<h->fin_blocks, kFinThreads, (size_t)std::max(l, 1) * sizeof(double), h->stream>>>(
-        0, n, l, h->S64, h->V64, h->k, h->yw + h->wofs, h->yw, h->v64, h->part, h->part_ld, nullptr);
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(y, yw, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    memcpy(h->vec_host, v, (size_t)n * sizeof(double));
+    CK(cudaMemcpyAsync(h->yw, h->vec_host, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    TRY(launch_fin(h, h->stream, fin_params(h, FIN_LOAD_RAW, l, h->yw, 0ull, 0), true));  // y_cur = v, c = S V^T v
+    TRY(launch_gv(h, h->stream, l, false));
+    const bool fused = h->world == 1;
+    if (!fused) {
+        reduce_partials<<<(n + 255) / 256, 256, 0, h->stream>>>(h->ypart, h->grid, h->ypart_ld, n, h->wpart, h->kpad,
+                                                               l, h->yw, h->wofs, h->st);
+        CK(cudaGetLastError());
+        TRY(allreduce(h, h->stream, h->yw, (size_t)(h->wofs + h->kpad)));
+    }
+    TRY(launch_fin(h, h->stream, fin_params(h, FIN_APPLY, l, nullptr, 0ull, 0), fused));
+    CK(cudaMemcpyAsync(h->vec_host, h->ybuf + h->ystride, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost,
+                       h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    memcpy(y, h->vec_host, (size_t)n * sizeof(double));
     return TSVD_OK;
 }
 
@@ -645,42 +769,47 @@ tsvd_status tsvd_run(tsvd_t h) {
     auto t0 = std::chrono::steady_clock::now();
     TRY(ensure_alloc(h));
     TRY(stage_A(h));
+    TRY(upload_v0(h));
     h->n1_ms = 0.0;
     h->n1_launches = 0;
     h->total_iters = 0;
     h->launches = 0;
-    tsvd_status result = TSVD_OK;
-    std::vector<double> xbuf;
-    for (int l = h->l_found; l < h->k; ++l) {
-        const double *x;
-        if (h->have_V0) {
-            x = h->V0.data() + (size_t)l * h->n;
+    const int l0 = h->l_found;
+    if (l0 >= h->k) return TSVD_OK;
+    CK(cudaMemsetAsync(h->stats, 0, (size_t)h->k * sizeof(CompStat), h->stream));
+    TRY(reset_state(h));
+    const bool graph = h->use_graph && !h->timing;
+    bool ran = false;
+    if (graph) {
+        tsvd_status gs = TSVD_OK;
+        if (!h->exec || h->graph_l0 != l0) gs = build_graph(h, l0);
+        if (gs >= 0) {
+            CK(cudaGraphLaunch(h->exec, h->stream));
+            h->loop_mode = "graph-while";
+            ran = true;
         } else {
-            xbuf.resize(h->n);
-            gen_x(h->seed, l, h->n, xbuf.data());
-            x = xbuf.data();
+            h->graph_error = h->err;  // fall back to the host loop, keep the reason for the report
+            TRY(reset_state(h));
         }
-        TRY(init_component(h, l, x));
-        const bool graph = h->use_graph && !h->timing && h->world == 1;
-        if (graph) TRY(iterate_graph(h, l));
-        else TRY(iterate_host(h, l));
-        TRY(extract_component(h, l));
-        CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
-        double *sig2_host = reinterpret_cast<double *>(h->st_host + 1);
-        CK(cudaMemcpyAsync(sig2_host, h->sig2, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
-        const LoopState st = *h->st_host;
-        if (st.status == -7) return h->fail(TSVD_ERR_NUMERIC, "non-finite value or zero initial vector at component %d", l);
-        if (st.status == 2 || !(*sig2_host > 0.0)) {
+    }
+    if (!ran) TRY(run_host_loop(h, l0));
+    CK(cudaMemcpyAsync(h->stats_host, h->stats, (size_t)h->k * sizeof(CompStat), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    tsvd_status result = TSVD_OK;
+    const int per_iter = h->world == 1 ? 2 : 3, per_ext = h->world == 1 ? 2 : 3;
+    for (int l = l0; l < h->k; ++l) {
+        const CompStat &cs = h->stats_host[l];
+        h->launches += 1 + per_iter * (int64_t)cs.it + per_ext;
+        if (cs.status == -7) return h->fail(TSVD_ERR_NUMERIC, "non-finite value or zero initial vector at component %d", l);
+        if (!cs.valid || cs.status == 2) {
             result = TSVD_WARN_RANK_EXHAUSTED;
             break;
         }
-        if (!std::isfinite(*sig2_host)) return h->fail(TSVD_ERR_NUMERIC, "non-finite sigma at component %d", l);
-        h->iters[l] = st.it;
-        h->dots[l] = st.d;
-        h->total_iters += st.it;
-        h->launches += 3 + 5 * (int64_t)st.it + 3;  // init (N5a-c), iterations (N1, N7, N5a-c), extraction
-        if (st.status == 1 && result == TSVD_OK) result = TSVD_WARN_NOT_CONVERGED;
+        h->iters[l] = cs.it;
+        h->dots[l] = cs.d;
+        h->total_iters += cs.it;
+        if (cs.status == 1 && result == TSVD_OK) result = TSVD_WARN_NOT_CONVERGED;
         h->l_found = l + 1;
         h->k_found = l + 1;
     }
@@ -705,6 +834,12 @@ tsvd_status tsvd_get_U_S_V(tsvd_t h, float *U, double *S, float *V) {
     CK(cudaStreamSynchronize(h->stream));
     if (V)
         for (size_t i = 0; i < vt.size(); ++i) V[i] = (float)vt[i];
+    // columns >= k_found are zero (contract), whatever a partial run left on the device
+    for (int64_t r = 0; U && r < h->m_g; ++r)
+        for (int c = h->k_found; c < h->k; ++c) U[r * h->k + c] = 0.f;
+    for (int c = h->k_found; S && c < h->k; ++c) S[c] = 0.0;
+    for (int64_t r = 0; V && r < h->n; ++r)
+        for (int c = h->k_found; c < h->k; ++c) V[r * h->k + c] = 0.f;
     return TSVD_OK;
 }
 
@@ -719,7 +854,7 @@ tsvd_status tsvd_get_info(tsvd_t h, int32_t *k_found, int32_t *iters, double *do
 tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
     if (!h || !buf || cap == 0) return TSVD_ERR_ARG;
     std::string s = "{";
-    char tmp[512];
+    char tmp[768];
     snprintf(tmp, sizeof tmp,
              "\"m\": %lld, \"n\": %lld, \"k\": %d, \"eps\": %.3g, \"rank\": %d, \"world\": %d, \"rows\": [%lld, %lld], "
              "\"k_found\": %d, \"total_iters\": %lld, \"run_ms\": %.4f, \"h2d_ms\": %.4f, \"n1_ms\": %.6f, "
@@ -733,7 +868,10 @@ tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
              "\"stage_bytes\": %d, \"run_rows\": %d}, ",
              h->T, h->NV, h->S, h->cps, h->grid, h->smem, h->stage_bytes, h->run_rows);
     s += tmp;
-    s += "\"iters\": [";
+    std::string ge = h->graph_error;
+    for (char &c : ge)
+        if (c == '"' || c == '\\') c = '\'';
+    s += "\"graph_error\": \"" + ge + "\", \"iters\": [";
     for (int i = 0; i < h->k; ++i) {
         snprintf(tmp, sizeof tmp, "%s%d", i ? ", " : "", h->iters[i]);
         s += tmp;
@@ -749,13 +887,14 @@ tsvd_status tsvd_time_gram_kernel(tsvd_t h, int32_t reps, double *ms) {
     CK(cudaSetDevice(h->dev));
     TRY(ensure_alloc(h));
     TRY(stage_A(h));
+    TRY(reset_state(h));  // the kernel skips itself when a loop is done; invalidates iteration state
     const int l = std::min(h->l_found, h->k - 1);
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    TRY(launch_gv(h, l, nullptr));  // warm-up
+    TRY(launch_gv(h, h->stream, l, false));  // warm-up
     CK(cudaEventRecord(e0, h->stream));
-    for (int r = 0; r < reps; ++r) TRY(launch_gv(h, l, nullptr));
+    for (int r = 0; r < reps; ++r) TRY(launch_gv(h, h->stream, l, false));
     CK(cudaEventRecord(e1, h->stream));
     CK(cudaEventSynchronize(e1));
     float t = 0.f;
@@ -774,14 +913,17 @@ void tsvd_destroy(tsvd_t h) {
     if (!h) return;
     cudaSetDevice(h->dev);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    void *dev_ptrs[] = {h->A_own, h->U32, h->V64, h->S64, h->v64, h->v32, h->yw, h->c64, h->ypart,
-                        h->wpart, h->part, h->u64, h->sq_part, h->sig2, h->st};
+    drop_graph(h);
+    void *dev_ptrs[] = {h->A_own, h->U32, h->V64, h->S64, h->ybuf, h->yw, h->V0d, h->c64, h->ypart, h->wpart,
+                        h->part, h->u64, h->sq_part, h->sig2, h->st, h->stats};
     for (void *p : dev_ptrs)
         if (p) cudaFree(p);
     if (h->st_host) cudaFreeHost(h->st_host);
-    if (h->x_host) cudaFreeHost(h->x_host);
+    if (h->stats_host) cudaFreeHost(h->stats_host);
+    if (h->vec_host) cudaFreeHost(h->vec_host);
     if (h->comm) ncclCommDestroy(h->comm);
     if (h->stream) cudaStreamDestroy(h->stream);
+    if (h->body_stream) cudaStreamDestroy(h->body_stream);
     delete h;
 }
 
