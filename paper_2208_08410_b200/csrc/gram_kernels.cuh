@@ -339,16 +339,24 @@ struct FinParams {
 // FIN_INIT    : ybuf[0] = x; ||x||, c = S V^T (x/||x||); it = 0   (P:112 normalisation)
 // FIN_LOAD_RAW: ybuf[0] = v, ny := 1, c = S V^T v                          (tsvd_gram_apply)
 // FIN_APPLY   : ybuf[1] = reduce(partials) - V (S w); no state change     (tsvd_gram_apply)
+//
+// Block = 256 threads = kFinCols (32) columns x kFinGroups (8) partial groups: thread (c, g) sums the
+// per-CTA partials b = g, g+8, ... of column c, the 8 group sums are added in g order (fixed order:
+// bitwise reproducible).  Grid = ceil(n / 32) blocks.
+constexpr int kFinCols = 32;
+constexpr int kFinGroups = kFinThreads / kFinCols;
+
 template <bool FUSED>
 __global__ void __launch_bounds__(kFinThreads) fin_iter(const FinParams p) {
-    __shared__ double ys[kFinThreads];
-    __shared__ double red[2][kFinThreads / 32];
+    __shared__ double gsum[kFinGroups][kFinCols];
+    __shared__ double ys[kFinCols];
     __shared__ int am_last;
+    __shared__ double inv_s;
     extern __shared__ double dyn[];  // g[l] then tot[2 + l]
     double *g = dyn;
     double *tot = dyn + p.l;
     LoopState *st = p.st;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, grp = tid >> 5;
     if (st->stop || (p.mode == FIN_ITERATE && st->done)) {
         if (blockIdx.x == 0 && tid == 0) set_cond(p.cond, p.use_cond, 0u);
         return;
@@ -358,85 +366,90 @@ __global__ void __launch_bounds__(kFinThreads) fin_iter(const FinParams p) {
     const double ny = st->ny;
     const double *ycur = p.ybuf + (int64_t)(it & 1) * p.ystride;
     double *ynew = p.ybuf + (int64_t)(mode == FIN_ITERATE ? ((it + 1) & 1) : (mode == FIN_APPLY ? 1 : 0)) * p.ystride;
-
     const bool reduce = (mode == FIN_ITERATE || mode == FIN_APPLY);
+    const int j0 = blockIdx.x * kFinCols;
+    const int j = j0 + lane;
+
     if (reduce) {
-        for (int i = tid; i < l; i += kFinThreads) {
-            double w;
-            if (FUSED) {
-                w = 0.0;
-                for (int b = 0; b < p.parts; ++b) w += p.wpart[(int64_t)b * p.wpart_ld + i];
-            } else {
-                w = p.yw[p.wofs + i];
+        if (FUSED) {  // g_i = S_i w_i, w = U^T X' v: warp per i, lanes stride the CTA partials
+            for (int i = grp; i < l; i += kFinGroups) {
+                double w = 0.0;
+                for (int b = lane; b < p.parts; b += 32) w += p.wpart[(int64_t)b * p.wpart_ld + i];
+                w = warp_sum(w);
+                if (lane == 0) g[i] = p.S[i] * w;
             }
-            g[i] = p.S[i] * w;
+        } else {
+            for (int i = tid; i < l; i += kFinThreads) g[i] = p.S[i] * p.yw[p.wofs + i];
+        }
+        if (FUSED) {
+            double s = 0.0;
+            if (j < n) {
+                const double *col = p.ypart + j;
+#pragma unroll 4
+                for (int b = grp; b < p.parts; b += kFinGroups) s += col[(int64_t)b * p.ypart_ld];
+            }
+            gsum[grp][lane] = s;
         }
         __syncthreads();
     }
-    const int j0 = blockIdx.x * kFinThreads;
-    const int j = j0 + tid;
-    double yj = 0.0, vj = 0.0;
-    if (j < n) {
-        if (reduce) {
-            if (FUSED) {
-                const double *col = p.ypart + j;
-                double s0 = 0.0;
-                for (int b = 0; b < p.parts; ++b) s0 += col[(int64_t)b * p.ypart_ld];
-                yj = s0;
+    if (grp == 0) {  // one warp finishes the 32 columns
+        double yj = 0.0, vj = 0.0;
+        if (j < n) {
+            if (reduce) {
+                if (FUSED) {
+                    yj = gsum[0][lane];
+#pragma unroll
+                    for (int q = 1; q < kFinGroups; ++q) yj += gsum[q][lane];
+                } else {
+                    yj = p.yw[j];
+                }
+                double corr = 0.0;  // (V (S w))_j: the 2nd / 4th terms of Eq. 2 in factored form
+                for (int i = 0; i < l; ++i) corr += p.V[(int64_t)j * p.ldv + i] * g[i];
+                yj -= corr;
+                if (mode == FIN_ITERATE) vj = ycur[j] / ny;
             } else {
-                yj = p.yw[j];
+                yj = p.xsrc[j];
             }
-            double corr = 0.0;  // (V (S w))_j: the 2nd / 4th terms of Eq. 2 in factored form
-            for (int i = 0; i < l; ++i) corr += p.V[(int64_t)j * p.ldv + i] * g[i];
-            yj -= corr;
-            if (mode == FIN_ITERATE) vj = ycur[j] / ny;
-        } else {
-            yj = p.xsrc[j];
+            ynew[j] = yj;
         }
-        ynew[j] = yj;
+        ys[lane] = yj;
+        const double a = warp_sum(yj * yj), b = warp_sum(vj * yj);
+        if (lane == 0 && mode != FIN_APPLY) {
+            double *out = p.part + (int64_t)blockIdx.x * p.part_ld;
+            out[0] = a;
+            out[1] = b;
+        }
     }
     if (mode == FIN_APPLY) return;
-    ys[tid] = yj;
-    const double a = warp_sum(yj * yj), b = warp_sum(vj * yj);
-    if ((tid & 31) == 0) {
-        red[0][tid >> 5] = a;
-        red[1][tid >> 5] = b;
-    }
     __syncthreads();
-    double *out = p.part + (int64_t)blockIdx.x * p.part_ld;
-    if (tid == 0) {
-        double s0 = 0.0, s1 = 0.0;
-        for (int k = 0; k < kFinThreads / 32; ++k) {
-            s0 += red[0][k];
-            s1 += red[1][k];
+    {
+        double *out = p.part + (int64_t)blockIdx.x * p.part_ld;
+        const int jn = (n - j0) < kFinCols ? (n - j0) : kFinCols;
+        for (int i = tid; i < l; i += kFinThreads) {  // (V^T y)_i over this block's 32 rows of V
+            double s = 0.0;
+            for (int jj = 0; jj < jn; ++jj) s += p.V[(int64_t)(j0 + jj) * p.ldv + i] * ys[jj];
+            out[2 + i] = s;
         }
-        out[0] = s0;
-        out[1] = s1;
     }
-    const int jn = (n - j0) < kFinThreads ? (n - j0) : kFinThreads;
-    for (int i = tid; i < l; i += kFinThreads) {  // (V^T y)_i over this block's rows, coalesced in i
-        double s = 0.0;
-        for (int jj = 0; jj < jn; ++jj) s += p.V[(int64_t)(j0 + jj) * p.ldv + i] * ys[jj];
-        out[2 + i] = s;
-    }
-    // ---- last block to arrive takes the scalar decisions (sums in block order: deterministic)
+    // ---- the last block to arrive takes the scalar decisions (fixed-order sums: deterministic)
     __threadfence();
     __syncthreads();
     if (tid == 0) am_last = (atomicAdd(&st->counter, 1u) == gridDim.x - 1);
     __syncthreads();
     if (!am_last) return;
     __threadfence();
-    for (int q = tid; q < 2 + l; q += kFinThreads) {
+    const int nb = (int)gridDim.x;
+    for (int q = grp; q < 2 + l; q += kFinGroups) {  // warp per quantity, lanes stride the blocks
         double s = 0.0;
-        for (int bb = 0; bb < (int)gridDim.x; ++bb) s += __ldcg(p.part + (int64_t)bb * p.part_ld + q);
-        tot[q] = s;
+        for (int bb = lane; bb < nb; bb += 32) s += __ldcg(p.part + (int64_t)bb * p.part_ld + q);
+        s = warp_sum(s);
+        if (lane == 0) tot[q] = s;
     }
     __syncthreads();
-    __shared__ double inv_s;
     if (tid == 0) {
         st->counter = 0;
         const double yy = tot[0];
-        double nyn = sqrt(yy);
+        const double nyn = sqrt(yy);
         if (mode == FIN_LOAD_RAW) {
             st->ny = 1.0;
             st->it = 0;

@@ -210,7 +210,7 @@ static tsvd_status ensure_alloc(tsvd_t h) {
     h->ystride = round_up(n, 32);
     h->wofs = round_up(n, 32);
     h->ypart_ld = round_up(n, 4);
-    h->fin_blocks = (int)((n + kFinThreads - 1) / kFinThreads);
+    h->fin_blocks = (int)((n + kFinCols - 1) / kFinCols);
     h->part_ld = 2 + h->kpad;
     auto dm = [&](void **p, size_t bytes) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(bytes, 16)); };
     cudaError_t e = cudaSuccess;
