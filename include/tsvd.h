@@ -69,7 +69,10 @@ typedef enum {
     TSVD_OPT_TIMING = 5,         /* 1: host loop with CUDA events around every fused-kernel launch;
                                     totals appear in tsvd_get_report                              */
     TSVD_OPT_RUN_ROWS = 6,       /* rows per fp32 accumulation run before an fp64 flush (def 1024) */
-    TSVD_OPT_CTAS_PER_SM = 7     /* 0 = auto (occupancy); testing knob                              */
+    TSVD_OPT_CTAS_PER_SM = 7,    /* 0 = auto (occupancy); testing knob                              */
+    TSVD_OPT_COLLECTIVE = 8      /* world > 1: 0 (default) = all-reduce fused into the finalize kernel
+                                    over NVLink peer memory (CUDA IPC, in-graph); 1 = ncclAllReduce
+                                    with a host-driven loop (fallback / cross-check)                 */
 } tsvd_option;
 
 /*
@@ -85,9 +88,12 @@ tsvd_status tsvd_create(tsvd_t *out, int64_t m, int64_t n, int32_t k, double eps
  * broadcasts the bytes, e.g. through torch.distributed).  Errors: TSVD_ERR_NCCL. */
 tsvd_status tsvd_get_unique_id(void *out128);
 
-/* tsvd_set_comm — join an NCCL communicator of `world` ranks (this rank = `rank`) on CUDA
- * device `device`.  Optional; world == 1 needs no call.  Must precede tsvd_set_dense.
- * Errors: TSVD_ERR_ARG, TSVD_ERR_NCCL, TSVD_ERR_CUDA. */
+/* tsvd_set_comm — join an NCCL communicator of `world` ranks (this rank = `rank`, world <= 8, one
+ * node) on CUDA device `device`, and map every rank's symmetric reduction buffer into this process
+ * (CUDA IPC handles exchanged with ncclAllGather) for the in-kernel NVLink all-reduce.  Collective:
+ * every rank must call it.  Optional; world == 1 needs no call.  Must precede tsvd_set_dense.
+ * If the peer mapping fails the handle falls back to ncclAllReduce (TSVD_OPT_COLLECTIVE = 1).
+ * Errors: TSVD_ERR_ARG (bad rank/world, world > 8), TSVD_ERR_NCCL, TSVD_ERR_CUDA. */
 tsvd_status tsvd_set_comm(tsvd_t h, int32_t rank, int32_t world, const void *nccl_unique_id, int32_t device);
 
 /* tsvd_set_option — see tsvd_option.  Errors: TSVD_ERR_ARG (unknown key / bad value). */

@@ -13,18 +13,9 @@
 //                 prologue builds this thread's slice of v = y_cur / ||y_cur|| in registers (the
 //                 normalisation of P:122 is folded here).  EXTRACT=true runs the same pipeline for
 //                 u = A v and ||u||^2.
-//   N5 fin_iter   per column j: y_j = sum_b ypart[b][j] (fixed order, fp64) - sum_i V[j,i] S_i w_i;
-//                 per block: ||y||^2, v.y, V^T y; the LAST block to finish (arrival counter) sums
-//                 the block partials in block order and takes the scalar decisions: ||y||, the stop
-//                 test |v0 . v1| >= 1 - eps, c_next = S V^T v1, and the CUDA-graph WHILE
-//                 condition.  y_new goes to the other half of a ping-pong buffer, so the next
-//                 iteration's v is y_new / ||y_new|| with no separate normalisation pass.
+//   N5 fin_iter   (fin_kernels.cuh) reductions, V correction, stop test, c_next, WHILE condition.
 //
-// Multi-GPU (row partition) inserts reduce_partials + one NCCL all-reduce of [y_g | w_g] between
-// them, and fin_iter<false> reads the all-reduced vector instead of the per-CTA partials.
-//
-// N6 extraction: gv_fused<EXTRACT> then ext_finish: sigma = ||A v1||, U[:,l] = A v1 / sigma
-// (P:87), V[:,l] = v1, S[l] = sigma.
+// N6 extraction: gv_fused<EXTRACT> then ext_finish (fin_kernels.cuh).
 //
 // Precision (reading R17): A, U and the copy of v fed to N1 are fp32; products are fp32
 // FMAs inside a thread, every cross-thread / cross-CTA / cross-GPU sum is fp64, and the per-CTA y
@@ -39,13 +30,15 @@ constexpr int kMaxStages = 8;
 constexpr int kFinThreads = 256;
 
 struct LoopState {
-    double ny;         // ||y_cur||: the current iterate is v = y_cur / ny
-    double d;          // |v0 . v1| of the last iteration
-    int32_t it;        // iterations completed in this component; y_cur = ybuf[it & 1]
-    int32_t done;      // this component's loop has finished
-    int32_t status;    // 0 ok, 1 not converged (MAX_ITER), 2 rank exhausted, -7 non-finite
-    int32_t stop;      // sticky: rank exhausted / non-finite -> every later kernel is a no-op
-    uint32_t counter;  // arrivals of the last-block-done reduction (returns to 0 after use)
+    double ny;             // ||y_cur||: the current iterate is v = y_cur / ny
+    double d;              // |v0 . v1| of the last iteration
+    int32_t it;            // iterations completed in this component; y_cur = ybuf[it & 1]
+    int32_t done;          // this component's loop has finished
+    int32_t status;        // 0 ok, 1 not converged (MAX_ITER), 2 rank exhausted, -7 non-finite, -6 peer timeout
+    int32_t stop;          // sticky: rank exhausted / non-finite -> every later kernel is a no-op
+    uint32_t counter;      // arrivals of the last-block-done reductions (returns to 0 after use)
+    uint32_t epoch;        // peer-collective epoch: identical on all ranks, monotone across runs
+    uint32_t pub_counter;  // arrivals of publish_partials
     int32_t pad;
 };
 
@@ -282,299 +275,6 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     } else {
         flush();
         if (tid < l) p.wpart[(int64_t)blockIdx.x * p.wpart_ld + tid] = wacc;
-    }
-}
-
-// ---------------------------------------------------------------- multi-GPU: local partial sum
-// yw = [ y_g (n) | pad | w_g (l) ], y_g[j] = sum_{b} ypart[b][j] in b order.  Then all-reduce.
-__global__ void reduce_partials(const double *__restrict__ ypart, int parts, int64_t ypart_ld, int n,
-                                const double *__restrict__ wpart, int wpart_ld, int l, double *__restrict__ yw,
-                                int64_t wofs, const LoopState *st) {
-    if (st->stop || st->done) return;
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < n) {
-        double s = 0.0;
-        for (int b = 0; b < parts; ++b) s += ypart[(int64_t)b * ypart_ld + j];
-        yw[j] = s;
-    }
-    if (blockIdx.x == 0) {
-        for (int i = threadIdx.x; i < l; i += blockDim.x) {
-            double s = 0.0;
-            for (int b = 0; b < parts; ++b) s += wpart[(int64_t)b * wpart_ld + i];
-            yw[wofs + i] = s;
-        }
-    }
-}
-
-// ---------------------------------------------------------------- N5: fin_iter
-enum FinMode { FIN_ITERATE = 0, FIN_INIT = 1, FIN_LOAD_RAW = 2, FIN_APPLY = 3 };
-
-struct FinParams {
-    int mode;
-    int n, l;
-    const double *S;          // sigma[0..l)
-    const double *V;          // n x ldv fp64 row-major
-    int ldv;
-    const double *ypart;      // FUSED: per-CTA partials of N1
-    int parts;
-    int64_t ypart_ld;
-    const double *wpart;
-    int wpart_ld;
-    const double *yw;         // !FUSED: all-reduced [y | w]
-    int64_t wofs;
-    const double *xsrc;       // FIN_INIT / FIN_LOAD_RAW: vector to load
-    double *ybuf;             // [2][ystride]
-    int64_t ystride;
-    double *part;             // [gridDim.x][part_ld]
-    int part_ld;
-    double *c;                // out: c = S V^T v1
-    LoopState *st;
-    double eps;
-    int fixed_T, max_iter;
-    unsigned long long cond;
-    int use_cond;
-};
-
-// FIN_ITERATE : y_new = reduce(partials) - V (S w) -> ybuf[(it+1)&1]; stop test; it += 1
-// FIN_INIT    : ybuf[0] = x; ||x||, c = S V^T (x/||x||); it = 0   (P:112 normalisation)
-// FIN_LOAD_RAW: ybuf[0] = v, ny := 1, c = S V^T v                          (tsvd_gram_apply)
-// FIN_APPLY   : ybuf[1] = reduce(partials) - V (S w); no state change     (tsvd_gram_apply)
-//
-// Block = 256 threads = kFinCols (32) columns x kFinGroups (8) partial groups: thread (c, g) sums the
-// per-CTA partials b = g, g+8, ... of column c, the 8 group sums are added in g order (fixed order:
-// bitwise reproducible).  Grid = ceil(n / 32) blocks.
-constexpr int kFinCols = 32;
-constexpr int kFinGroups = kFinThreads / kFinCols;
-
-template <bool FUSED>
-__global__ void __launch_bounds__(kFinThreads) fin_iter(const FinParams p) {
-    __shared__ double gsum[kFinGroups][kFinCols];
-    __shared__ double ys[kFinCols];
-    __shared__ int am_last;
-    __shared__ double inv_s;
-    extern __shared__ double dyn[];  // g[l] then tot[2 + l]
-    double *g = dyn;
-    double *tot = dyn + p.l;
-    LoopState *st = p.st;
-    const int tid = threadIdx.x, lane = tid & 31, grp = tid >> 5;
-    if (st->stop || (p.mode == FIN_ITERATE && st->done)) {
-        if (blockIdx.x == 0 && tid == 0) set_cond(p.cond, p.use_cond, 0u);
-        return;
-    }
-    const int mode = p.mode, n = p.n, l = p.l;
-    const int it = st->it;
-    const double ny = st->ny;
-    const double *ycur = p.ybuf + (int64_t)(it & 1) * p.ystride;
-    double *ynew = p.ybuf + (int64_t)(mode == FIN_ITERATE ? ((it + 1) & 1) : (mode == FIN_APPLY ? 1 : 0)) * p.ystride;
-    const bool reduce = (mode == FIN_ITERATE || mode == FIN_APPLY);
-    const int j0 = blockIdx.x * kFinCols;
-    const int j = j0 + lane;
-
-    if (reduce) {
-        if (FUSED) {  // g_i = S_i w_i, w = U^T X' v: warp per i, lanes stride the CTA partials
-            for (int i = grp; i < l; i += kFinGroups) {
-                double w = 0.0;
-                for (int b = lane; b < p.parts; b += 32) w += p.wpart[(int64_t)b * p.wpart_ld + i];
-                w = warp_sum(w);
-                if (lane == 0) g[i] = p.S[i] * w;
-            }
-        } else {
-            for (int i = tid; i < l; i += kFinThreads) g[i] = p.S[i] * p.yw[p.wofs + i];
-        }
-        if (FUSED) {
-            double s = 0.0;
-            if (j < n) {
-                const double *col = p.ypart + j;
-#pragma unroll 4
-                for (int b = grp; b < p.parts; b += kFinGroups) s += col[(int64_t)b * p.ypart_ld];
-            }
-            gsum[grp][lane] = s;
-        }
-        __syncthreads();
-    }
-    if (grp == 0) {  // one warp finishes the 32 columns
-        double yj = 0.0, vj = 0.0;
-        if (j < n) {
-            if (reduce) {
-                if (FUSED) {
-                    yj = gsum[0][lane];
-#pragma unroll
-                    for (int q = 1; q < kFinGroups; ++q) yj += gsum[q][lane];
-                } else {
-                    yj = p.yw[j];
-                }
-                double corr = 0.0;  // (V (S w))_j: the 2nd / 4th terms of Eq. 2 in factored form
-                for (int i = 0; i < l; ++i) corr += p.V[(int64_t)j * p.ldv + i] * g[i];
-                yj -= corr;
-                if (mode == FIN_ITERATE) vj = ycur[j] / ny;
-            } else {
-                yj = p.xsrc[j];
-            }
-            ynew[j] = yj;
-        }
-        ys[lane] = yj;
-        const double a = warp_sum(yj * yj), b = warp_sum(vj * yj);
-        if (lane == 0 && mode != FIN_APPLY) {
-            double *out = p.part + (int64_t)blockIdx.x * p.part_ld;
-            out[0] = a;
-            out[1] = b;
-        }
-    }
-    if (mode == FIN_APPLY) return;
-    __syncthreads();
-    {
-        double *out = p.part + (int64_t)blockIdx.x * p.part_ld;
-        const int jn = (n - j0) < kFinCols ? (n - j0) : kFinCols;
-        for (int i = tid; i < l; i += kFinThreads) {  // (V^T y)_i over this block's 32 rows of V
-            double s = 0.0;
-            for (int jj = 0; jj < jn; ++jj) s += p.V[(int64_t)(j0 + jj) * p.ldv + i] * ys[jj];
-            out[2 + i] = s;
-        }
-    }
-    // ---- the last block to arrive takes the scalar decisions (fixed-order sums: deterministic)
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) am_last = (atomicAdd(&st->counter, 1u) == gridDim.x - 1);
-    __syncthreads();
-    if (!am_last) return;
-    __threadfence();
-    const int nb = (int)gridDim.x;
-    for (int q = grp; q < 2 + l; q += kFinGroups) {  // warp per quantity, lanes stride the blocks
-        double s = 0.0;
-        for (int bb = lane; bb < nb; bb += 32) s += __ldcg(p.part + (int64_t)bb * p.part_ld + q);
-        s = warp_sum(s);
-        if (lane == 0) tot[q] = s;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        st->counter = 0;
-        const double yy = tot[0];
-        const double nyn = sqrt(yy);
-        if (mode == FIN_LOAD_RAW) {
-            st->ny = 1.0;
-            st->it = 0;
-            st->done = 0;
-            st->status = 0;
-            inv_s = 1.0;
-        } else if (mode == FIN_INIT) {
-            st->ny = nyn;
-            st->it = 0;
-            st->done = 0;
-            st->d = 0.0;
-            if (!(nyn > 0.0) || !isfinite(nyn)) {  // zero or non-finite initial sample
-                st->status = -7;
-                st->stop = 1;
-                st->done = 1;
-            } else {
-                st->status = 0;
-            }
-            inv_s = (nyn > 0.0 && isfinite(nyn)) ? nyn : 1.0;
-        } else {  // FIN_ITERATE
-            const int itn = it + 1;
-            st->it = itn;
-            if (!isfinite(nyn)) {
-                st->status = -7;
-                st->stop = 1;
-                st->done = 1;
-            } else if (nyn == 0.0) {  // X'^T X' v = 0: rank exhausted (reading R14)
-                st->status = 2;
-                st->stop = 1;
-                st->done = 1;
-            } else {
-                st->ny = nyn;
-                const double d = fabs(tot[1]) / nyn;  // |v0 . v1| with v1 = y / ||y||
-                st->d = d;
-                if (p.fixed_T > 0) {
-                    if (itn >= p.fixed_T) st->done = 1;
-                } else if (d >= 1.0 - p.eps) {
-                    st->done = 1;
-                } else if (itn >= p.max_iter) {
-                    st->done = 1;
-                    st->status = 1;
-                }
-            }
-            inv_s = (nyn > 0.0 && isfinite(nyn)) ? nyn : 1.0;
-            set_cond(p.cond, p.use_cond, (st->done || st->stop) ? 0u : 1u);
-        }
-    }
-    __syncthreads();
-    for (int i = tid; i < l; i += kFinThreads) p.c[i] = p.S[i] * (tot[2 + i] / inv_s);  // c = S V^T v1
-}
-
-// ---------------------------------------------------------------- N6: extraction tail
-// multi-GPU: local sum of the per-CTA ||u||^2 partials (then all-reduced)
-__global__ void ext_reduce(const double *__restrict__ sq_part, int parts, double *__restrict__ sig2,
-                           const LoopState *st) {
-    if (st->stop) return;
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double s = 0.0;
-        for (int b = 0; b < parts; ++b) s += sq_part[b];
-        *sig2 = s;
-    }
-}
-
-struct ExtParams {
-    int64_t rows;
-    int n, l;
-    const double *u;         // (A v1)_r
-    const double *sq_part;   // FUSED: per-CTA sums of u_r^2
-    int parts;
-    const double *sig2;      // !FUSED: all-reduced ||u||^2
-    const double *ybuf;
-    int64_t ystride;
-    float *U;                // m_g x ldu
-    int ldu;
-    double *V;               // n x ldv
-    int ldv;
-    double *S;
-    CompStat *stat;          // stat[l]
-    LoopState *st;
-};
-
-// sigma = ||A v1||, U[r,l] = (A v1)_r / sigma, V[j,l] = v1_j, S[l] = sigma
-template <bool FUSED>
-__global__ void ext_finish(const ExtParams p) {
-    LoopState *st = p.st;
-    if (st->stop) {  // a previous step hit rank exhaustion / non-finite: record and skip
-        if (blockIdx.x == 0 && threadIdx.x == 0 && !p.stat[p.l].valid) {
-            p.stat[p.l].status = st->status;
-            p.stat[p.l].it = st->it;
-        }
-        return;
-    }
-    double sig2;
-    if (FUSED) {
-        sig2 = 0.0;
-        for (int b = 0; b < p.parts; ++b) sig2 += p.sq_part[b];  // every block, same order
-    } else {
-        sig2 = *p.sig2;
-    }
-    const double sigma = sqrt(sig2);
-    if (!(sigma > 0.0) || !isfinite(sigma)) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            st->status = isfinite(sigma) ? 2 : -7;
-            st->stop = 1;
-            p.stat[p.l].status = st->status;
-            p.stat[p.l].it = st->it;
-        }
-        return;
-    }
-    const double ny = st->ny;
-    const double *ycur = p.ybuf + (int64_t)(st->it & 1) * p.ystride;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (int64_t r = g; r < p.rows; r += stride) p.U[r * p.ldu + p.l] = (float)(p.u[r] / sigma);
-    for (int64_t j = g; j < p.n; j += stride) p.V[j * p.ldv + p.l] = ycur[j] / ny;
-    if (g == 0) {
-        p.S[p.l] = sigma;
-        CompStat cs;
-        cs.d = st->d;
-        cs.sigma = sigma;
-        cs.it = st->it;
-        cs.status = st->status;
-        cs.valid = 1;
-        cs.pad = 0;
-        p.stat[p.l] = cs;
     }
 }
 

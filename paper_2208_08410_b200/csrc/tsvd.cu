@@ -2,10 +2,11 @@
 //
 // The driver is host code that only plans, allocates and launches; every arithmetic step of the
 // power iteration (Gram-vector product, reductions, normalisation, stop test, extraction) runs
-// in the kernels of gram_kernels.cuh.  A whole tsvd_run (all k components: init, power-iteration
-// WHILE loop, extraction) is ONE CUDA graph with one conditional WHILE node per component, so
-// the host synchronises once per run.  One process per GPU; multi-GPU = row partition
-// with one NCCL all-reduce of [y_g | w_g] per iteration (merges Alg. 4 lines 6, 8, 16).
+// in the kernels of gram_kernels.cuh / fin_kernels.cuh.  A whole tsvd_run (all k components:
+// init, power-iteration WHILE loop, extraction) is ONE CUDA graph with one conditional WHILE node
+// per component, so the host synchronises once per run.  One process per GPU; multi-GPU = row
+// partition with one all-reduce of [y_g | w_g] per iteration (merges Alg. 4 lines 6,
+// 8, 16), done inside the finalize kernel over NVLink peer memory (default) or by NCCL.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -19,6 +20,7 @@
 #include <vector>
 
 #include "../../include/tsvd.h"
+#include "fin_kernels.cuh"
 #include "gram_kernels.cuh"
 
 using namespace tsvd;
@@ -26,9 +28,11 @@ using namespace tsvd;
 namespace {
 
 constexpr int kMaxThreadsPerCta = 512;
-constexpr int kRingTargetBytes = 192 * 1024;  // bytes in flight per SM (Little's law, DESIGN §4)
+constexpr int kRingTargetBytes = 192 * 1024;  // bytes in flight per SM (Little's law, DESIGN §6)
 constexpr int kSmemBudget = 220 * 1024;       // per SM, leaves room for barriers/scratch
 constexpr int kMaxK = 4096;                   // fin_iter keeps 2k+2 doubles in shared memory
+
+enum Coll { COLL_NONE = 0, COLL_PEER = 1, COLL_NCCL = 2 };
 
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -75,6 +79,12 @@ struct tsvd_s {
     cudaStream_t stream = nullptr, body_stream = nullptr;
     int32_t rank = 0, world = 1;
     ncclComm_t comm = nullptr;
+    int coll = COLL_NONE;
+    int coll_opt = 0;
+    double *sym = nullptr;                  // this rank's symmetric buffer (peer path)
+    void *peer_map[kMaxRanks] = {};         // IPC-opened peer buffers
+    PeerView pv{};
+    std::string peer_error;
     // options
     int max_iter = 10000, fixed_T = 0, use_graph = 1, timing = 0, run_rows = 1024, cps_opt = 0;
     uint64_t seed = 0;
@@ -154,6 +164,8 @@ struct tsvd_s {
 
 static thread_local std::string g_err;
 
+static int fin_src(tsvd_t h) { return h->coll == COLL_NONE ? SRC_PARTS : (h->coll == COLL_PEER ? SRC_PEER : SRC_YW); }
+
 // ------------------------------------------------------------------------------------ planning
 static tsvd_status plan(tsvd_t h) {
     const int64_t n = h->n;
@@ -184,8 +196,9 @@ static tsvd_status plan(tsvd_t h) {
     CK(cudaFuncSetAttribute(h->gv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem));
     CK(cudaFuncSetAttribute(h->gv_ex, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem));
     const int fin_dyn = (2 * h->k + 2) * (int)sizeof(double);
-    CK(cudaFuncSetAttribute(fin_iter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_dyn));
-    CK(cudaFuncSetAttribute(fin_iter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_dyn));
+    CK(cudaFuncSetAttribute(fin_iter<SRC_PARTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_dyn));
+    CK(cudaFuncSetAttribute(fin_iter<SRC_YW>, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_dyn));
+    CK(cudaFuncSetAttribute(fin_iter<SRC_PEER>, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_dyn));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->gv, T, h->smem));
     if (occ < 1) return h->fail(TSVD_ERR_UNSUPPORTED, "fused kernel does not fit on an SM (T=%d smem=%zu)", T, h->smem);
@@ -194,9 +207,17 @@ static tsvd_status plan(tsvd_t h) {
     return TSVD_OK;
 }
 
+// Fresh loop state; the peer-collective epoch is kept (flags in peer memory are monotone).
 static tsvd_status reset_state(tsvd_t h) {
+    uint32_t epoch = 0;
+    if (h->allocated) {
+        CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        epoch = h->st_host->epoch;
+    }
     LoopState s{};
     s.ny = 1.0;
+    s.epoch = epoch;
     *h->st_host = s;
     CK(cudaMemcpyAsync(h->st, h->st_host, sizeof(LoopState), cudaMemcpyHostToDevice, h->stream));
     CK(cudaStreamSynchronize(h->stream));
@@ -240,8 +261,57 @@ static tsvd_status ensure_alloc(tsvd_t h) {
     CK(cudaMemsetAsync(h->ybuf, 0, (size_t)2 * h->ystride * sizeof(double), h->stream));
     CK(cudaMemsetAsync(h->c64, 0, (size_t)h->kpad * sizeof(double), h->stream));
     CK(cudaMemsetAsync(h->yw, 0, (size_t)(h->wofs + h->kpad) * sizeof(double), h->stream));
+    TRY(reset_state(h));
     h->allocated = true;
-    return reset_state(h);
+    return TSVD_OK;
+}
+
+// Symmetric buffers for the in-kernel all-reduce: [2 slots x (y | w | ||u||^2)] + flags[world].
+// Every rank cudaMallocs its own, the CUDA IPC handles are all-gathered with NCCL and opened.
+static tsvd_status setup_peer(tsvd_t h) {
+    const int64_t wofs = round_up(h->n, 32), sofs = wofs + round_up(h->k, 4);
+    const int64_t slot = round_up(sofs + 1, 32);
+    const size_t flag_off = (size_t)2 * slot * sizeof(double);
+    const size_t bytes = flag_off + 256;
+    CK(cudaMalloc((void **)&h->sym, bytes));
+    CK(cudaMemset(h->sym, 0, bytes));
+    cudaIpcMemHandle_t mine;
+    CK(cudaIpcGetMemHandle(&mine, h->sym));
+    char *dbuf = nullptr;
+    CK(cudaMalloc((void **)&dbuf, sizeof(cudaIpcMemHandle_t) * (h->world + 1)));
+    CK(cudaMemcpy(dbuf, &mine, sizeof(mine), cudaMemcpyHostToDevice));
+    NK(ncclAllGather(dbuf, dbuf + sizeof(mine), sizeof(mine), ncclUint8, h->comm, h->stream));
+    std::vector<cudaIpcMemHandle_t> all(h->world);
+    CK(cudaMemcpyAsync(all.data(), dbuf + sizeof(mine), sizeof(mine) * h->world, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(dbuf);
+    PeerView pv{};
+    pv.world = h->world;
+    pv.rank = h->rank;
+    pv.slot_stride = slot;
+    pv.wofs = wofs;
+    pv.sofs = sofs;
+    for (int r = 0; r < h->world; ++r) {
+        char *base;
+        if (r == h->rank) {
+            base = (char *)h->sym;
+        } else {
+            void *p = nullptr;
+            cudaError_t e = cudaIpcOpenMemHandle(&p, all[r], cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                h->peer_error = std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e);
+                return TSVD_ERR_CUDA;
+            }
+            h->peer_map[r] = p;
+            base = (char *)p;
+        }
+        pv.buf[r] = (double *)base;
+        pv.rflags[r] = (unsigned *)(base + flag_off) + h->rank;
+    }
+    pv.flags = (unsigned *)((char *)h->sym + flag_off);
+    h->pv = pv;
+    return TSVD_OK;
 }
 
 // Make A resident on the device for this run (host input: H2D copy, counted in e2e timing).
@@ -316,12 +386,6 @@ static tsvd_status launch_gv(tsvd_t h, cudaStream_t s, int l, bool extract) {
     return TSVD_OK;
 }
 
-static tsvd_status allreduce(tsvd_t h, cudaStream_t s, double *buf, size_t count) {
-    if (h->world <= 1) return TSVD_OK;
-    NK(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, h->comm, s));
-    return TSVD_OK;
-}
-
 static FinParams fin_params(tsvd_t h, int mode, int l, const double *xsrc, unsigned long long cond, int use_cond) {
     FinParams p{};
     p.mode = mode;
@@ -337,6 +401,7 @@ static FinParams fin_params(tsvd_t h, int mode, int l, const double *xsrc, unsig
     p.wpart_ld = h->kpad;
     p.yw = h->yw;
     p.wofs = h->wofs;
+    p.pv = h->pv;
     p.xsrc = xsrc;
     p.ybuf = h->ybuf;
     p.ystride = h->ystride;
@@ -352,33 +417,60 @@ static FinParams fin_params(tsvd_t h, int mode, int l, const double *xsrc, unsig
     return p;
 }
 
-static tsvd_status launch_fin(tsvd_t h, cudaStream_t s, const FinParams &p, bool fused) {
+static tsvd_status launch_fin(tsvd_t h, cudaStream_t s, const FinParams &p, int src) {
     const size_t dyn = (size_t)(2 * p.l + 2) * sizeof(double);
-    if (fused) fin_iter<true><<<h->fin_blocks, kFinThreads, dyn, s>>>(p);
-    else fin_iter<false><<<h->fin_blocks, kFinThreads, dyn, s>>>(p);
+    switch (src) {
+    case SRC_PARTS: fin_iter<SRC_PARTS><<<h->fin_blocks, kFinThreads, dyn, s>>>(p); break;
+    case SRC_YW: fin_iter<SRC_YW><<<h->fin_blocks, kFinThreads, dyn, s>>>(p); break;
+    default: fin_iter<SRC_PEER><<<h->fin_blocks, kFinThreads, dyn, s>>>(p); break;
+    }
     CK(cudaGetLastError());
     return TSVD_OK;
 }
 
-// One power iteration: N1, [local partial sum + all-reduce], fin_iter.
+static PubParams pub_params(tsvd_t h, int mode, int l) {
+    PubParams p{};
+    p.mode = mode;
+    p.ypart = h->ypart;
+    p.parts = h->grid;
+    p.ypart_ld = h->ypart_ld;
+    p.wpart = h->wpart;
+    p.wpart_ld = h->kpad;
+    p.n = (int)h->n;
+    p.l = l;
+    p.sq_part = h->sq_part;
+    p.pv = h->pv;
+    p.st = h->st;
+    return p;
+}
+
+// The cross-rank part of an iteration before fin_iter: nothing / publish / local sum + NCCL.
+static tsvd_status launch_exchange(tsvd_t h, cudaStream_t s, int l) {
+    if (h->coll == COLL_PEER) {
+        publish<<<h->fin_blocks, kFinThreads, 0, s>>>(pub_params(h, 0, l));
+        CK(cudaGetLastError());
+    } else if (h->coll == COLL_NCCL) {
+        reduce_partials<<<h->fin_blocks, kFinThreads, 0, s>>>(h->ypart, h->grid, h->ypart_ld, (int)h->n, h->wpart,
+                                                              h->kpad, l, h->yw, h->wofs, h->st);
+        CK(cudaGetLastError());
+        NK(ncclAllReduce(h->yw, h->yw, (size_t)(h->wofs + h->kpad), ncclDouble, ncclSum, h->comm, s));
+    }
+    return TSVD_OK;
+}
+
+// One power iteration: N1, [exchange], fin_iter.
 static tsvd_status launch_iteration(tsvd_t h, cudaStream_t s, int l, unsigned long long cond, int use_cond,
                                     cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr) {
     if (e0) CK(cudaEventRecord(e0, s));
     TRY(launch_gv(h, s, l, false));
     if (e1) CK(cudaEventRecord(e1, s));
-    const bool fused = h->world == 1;
-    if (!fused) {
-        reduce_partials<<<(int)((h->n + 255) / 256), 256, 0, s>>>(h->ypart, h->grid, h->ypart_ld, (int)h->n, h->wpart,
-                                                                  h->kpad, l, h->yw, h->wofs, h->st);
-        CK(cudaGetLastError());
-        TRY(allreduce(h, s, h->yw, (size_t)(h->wofs + h->kpad)));
-    }
-    return launch_fin(h, s, fin_params(h, FIN_ITERATE, l, nullptr, cond, use_cond), fused);
+    TRY(launch_exchange(h, s, l));
+    return launch_fin(h, s, fin_params(h, FIN_ITERATE, l, nullptr, cond, use_cond), fin_src(h));
 }
 
 // x_l (device, fp64) -> y_cur = x, ||x||, c = S V^T (x / ||x||)
 static tsvd_status launch_init(tsvd_t h, cudaStream_t s, int l) {
-    return launch_fin(h, s, fin_params(h, FIN_INIT, l, h->V0d + (size_t)l * h->n, 0ull, 0), true);
+    return launch_fin(h, s, fin_params(h, FIN_INIT, l, h->V0d + (size_t)l * h->n, 0ull, 0), SRC_PARTS);
 }
 
 static tsvd_status launch_extract(tsvd_t h, cudaStream_t s, int l) {
@@ -391,6 +483,7 @@ static tsvd_status launch_extract(tsvd_t h, cudaStream_t s, int l) {
     p.sq_part = h->sq_part;
     p.parts = h->grid;
     p.sig2 = h->sig2;
+    p.pv = h->pv;
     p.ybuf = h->ybuf;
     p.ystride = h->ystride;
     p.U = h->U32;
@@ -402,13 +495,17 @@ static tsvd_status launch_extract(tsvd_t h, cudaStream_t s, int l) {
     p.st = h->st;
     const int64_t work = std::max<int64_t>(h->m_g, h->n);
     const int blocks = (int)std::min<int64_t>((work + 255) / 256, (int64_t)h->sms * 8);
-    if (h->world == 1) {
-        ext_finish<true><<<blocks, 256, 0, s>>>(p);
+    if (h->coll == COLL_NONE) {
+        ext_finish<SRC_PARTS><<<blocks, 256, 0, s>>>(p);
+    } else if (h->coll == COLL_PEER) {
+        publish<<<1, kFinThreads, 0, s>>>(pub_params(h, 1, l));
+        CK(cudaGetLastError());
+        ext_finish<SRC_PEER><<<blocks, 256, 0, s>>>(p);
     } else {
         ext_reduce<<<1, 32, 0, s>>>(h->sq_part, h->grid, h->sig2, h->st);
         CK(cudaGetLastError());
-        TRY(allreduce(h, s, h->sig2, 1));
-        ext_finish<false><<<blocks, 256, 0, s>>>(p);
+        NK(ncclAllReduce(h->sig2, h->sig2, 1, ncclDouble, ncclSum, h->comm, s));
+        ext_finish<SRC_YW><<<blocks, 256, 0, s>>>(p);
     }
     CK(cudaGetLastError());
     return TSVD_OK;
@@ -435,8 +532,8 @@ static tsvd_status upload_v0(tsvd_t h) {
             }
         }
         CK(cudaMemcpyAsync(h->V0d, x.data(), x.size() * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
     }
+    CK(cudaStreamSynchronize(h->stream));
     h->v0_uploaded = h->v0_version;
     return TSVD_OK;
 }
@@ -491,13 +588,10 @@ static tsvd_status build_graph(tsvd_t h, int l0) {
     }
     cudaGraph_t graph = nullptr;
     cudaError_t ce3 = cudaStreamEndCapture(h->stream, &graph);
-    if (s < 0) {
-        if (graph) cudaGraphDestroy(graph);
-        return s;
-    }
-    if (ce || ce3) {
+    if (s < 0 || ce || ce3) {
         if (graph) cudaGraphDestroy(graph);
         cudaGetLastError();
+        if (s < 0) return s;
         return h->fail(TSVD_ERR_CUDA, "run-graph capture failed: %s", cudaGetErrorString(ce ? ce : ce3));
     }
     h->graph = graph;
@@ -599,8 +693,8 @@ tsvd_status tsvd_get_unique_id(void *out128) {
 
 tsvd_status tsvd_set_comm(tsvd_t h, int32_t rank, int32_t world, const void *uid, int32_t device) {
     if (!h) return TSVD_ERR_ARG;
-    if (world < 1 || rank < 0 || rank >= world || (world > 1 && !uid))
-        return h->fail(TSVD_ERR_ARG, "bad rank/world");
+    if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world || (world > 1 && !uid))
+        return h->fail(TSVD_ERR_ARG, "bad rank/world (world <= %d)", kMaxRanks);
     if (h->allocated || h->have_A) return h->fail(TSVD_ERR_STATE, "set_comm must precede set_dense");
     if (device != h->dev) {
         CK(cudaSetDevice(device));
@@ -613,10 +707,21 @@ tsvd_status tsvd_set_comm(tsvd_t h, int32_t rank, int32_t world, const void *uid
     }
     h->rank = rank;
     h->world = world;
+    h->coll = COLL_NONE;
     if (world > 1) {
         ncclUniqueId id;
         memcpy(&id, uid, sizeof(id));
         NK(ncclCommInitRank(&h->comm, world, id, rank));
+        // every rank takes part in the handle exchange, then all agree on the collective to use
+        const tsvd_status ps = setup_peer(h);
+        int ok = (ps == TSVD_OK) ? 1 : 0, *dok = nullptr;
+        CK(cudaMalloc((void **)&dok, sizeof(int)));
+        CK(cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice));
+        NK(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, h->comm, h->stream));
+        CK(cudaMemcpyAsync(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        cudaFree(dok);
+        h->coll = (ok && h->coll_opt == 0) ? COLL_PEER : COLL_NCCL;
     }
     return TSVD_OK;
 }
@@ -646,6 +751,11 @@ tsvd_status tsvd_set_option(tsvd_t h, int32_t key, int64_t value) {
         if (value < 0 || value > 32) return h->fail(TSVD_ERR_ARG, "CTAS_PER_SM in [0, 32]");
         if (h->allocated) return h->fail(TSVD_ERR_STATE, "CTAS_PER_SM must precede the first run");
         h->cps_opt = (int)value;
+        break;
+    case TSVD_OPT_COLLECTIVE:
+        if (value < 0 || value > 1) return h->fail(TSVD_ERR_ARG, "COLLECTIVE is 0 (peer) or 1 (nccl)");
+        h->coll_opt = (int)value;
+        if (h->world > 1) h->coll = (value == 1 || !h->sym || !h->pv.flags) ? COLL_NCCL : COLL_PEER;
         break;
     default: return h->fail(TSVD_ERR_ARG, "unknown option %d", key);
     }
@@ -745,19 +855,16 @@ tsvd_status tsvd_gram_apply(tsvd_t h, const double *v, double *y) {
     const int n = (int)h->n, l = h->l_found;
     memcpy(h->vec_host, v, (size_t)n * sizeof(double));
     CK(cudaMemcpyAsync(h->yw, h->vec_host, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-    TRY(launch_fin(h, h->stream, fin_params(h, FIN_LOAD_RAW, l, h->yw, 0ull, 0), true));  // y_cur = v, c = S V^T v
+    // y_cur = v (unnormalised), c = S V^T v
+    TRY(launch_fin(h, h->stream, fin_params(h, FIN_LOAD_RAW, l, h->yw, 0ull, 0), SRC_PARTS));
     TRY(launch_gv(h, h->stream, l, false));
-    const bool fused = h->world == 1;
-    if (!fused) {
-        reduce_partials<<<(n + 255) / 256, 256, 0, h->stream>>>(h->ypart, h->grid, h->ypart_ld, n, h->wpart, h->kpad,
-                                                               l, h->yw, h->wofs, h->st);
-        CK(cudaGetLastError());
-        TRY(allreduce(h, h->stream, h->yw, (size_t)(h->wofs + h->kpad)));
-    }
-    TRY(launch_fin(h, h->stream, fin_params(h, FIN_APPLY, l, nullptr, 0ull, 0), fused));
+    TRY(launch_exchange(h, h->stream, l));
+    TRY(launch_fin(h, h->stream, fin_params(h, FIN_APPLY, l, nullptr, 0ull, 0), fin_src(h)));
     CK(cudaMemcpyAsync(h->vec_host, h->ybuf + h->ystride, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost,
                        h->stream));
+    CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    if (h->st_host->status == -6) return h->fail(TSVD_ERR_NCCL, "peer all-reduce timed out (a rank did not arrive)");
     memcpy(y, h->vec_host, (size_t)n * sizeof(double));
     return TSVD_OK;
 }
@@ -778,7 +885,8 @@ tsvd_status tsvd_run(tsvd_t h) {
     if (l0 >= h->k) return TSVD_OK;
     CK(cudaMemsetAsync(h->stats, 0, (size_t)h->k * sizeof(CompStat), h->stream));
     TRY(reset_state(h));
-    const bool graph = h->use_graph && !h->timing;
+    // the graph needs every collective to be a kernel: single GPU or the peer all-reduce
+    const bool graph = h->use_graph && !h->timing && h->coll != COLL_NCCL;
     bool ran = false;
     if (graph) {
         tsvd_status gs = TSVD_OK;
@@ -796,8 +904,9 @@ tsvd_status tsvd_run(tsvd_t h) {
     CK(cudaMemcpyAsync(h->stats_host, h->stats, (size_t)h->k * sizeof(CompStat), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    if (h->st_host->status == -6) return h->fail(TSVD_ERR_NCCL, "peer all-reduce timed out (a rank did not arrive)");
     tsvd_status result = TSVD_OK;
-    const int per_iter = h->world == 1 ? 2 : 3, per_ext = h->world == 1 ? 2 : 3;
+    const int per_iter = h->coll == COLL_NONE ? 2 : 3, per_ext = h->coll == COLL_NONE ? 2 : 3;
     for (int l = l0; l < h->k; ++l) {
         const CompStat &cs = h->stats_host[l];
         h->launches += 1 + per_iter * (int64_t)cs.it + per_ext;
@@ -855,20 +964,21 @@ tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
     if (!h || !buf || cap == 0) return TSVD_ERR_ARG;
     std::string s = "{";
     char tmp[768];
+    static const char *colls[] = {"none", "peer-nvlink", "nccl"};
     snprintf(tmp, sizeof tmp,
              "\"m\": %lld, \"n\": %lld, \"k\": %d, \"eps\": %.3g, \"rank\": %d, \"world\": %d, \"rows\": [%lld, %lld], "
              "\"k_found\": %d, \"total_iters\": %lld, \"run_ms\": %.4f, \"h2d_ms\": %.4f, \"n1_ms\": %.6f, "
-             "\"n1_launches\": %lld, \"kernel_launches\": %lld, \"loop\": \"%s\", ",
+             "\"n1_launches\": %lld, \"kernel_launches\": %lld, \"loop\": \"%s\", \"collective\": \"%s\", ",
              (long long)h->m, (long long)h->n, h->k, h->eps, h->rank, h->world, (long long)h->row_begin,
              (long long)h->row_end, h->k_found, (long long)h->total_iters, h->run_ms, h->h2d_ms, h->n1_ms,
-             (long long)h->n1_launches, (long long)h->launches, h->loop_mode.c_str());
+             (long long)h->n1_launches, (long long)h->launches, h->loop_mode.c_str(), colls[h->coll]);
     s += tmp;
     snprintf(tmp, sizeof tmp,
              "\"plan\": {\"T\": %d, \"NV\": %d, \"stages\": %d, \"ctas_per_sm\": %d, \"grid\": %d, \"smem\": %zu, "
              "\"stage_bytes\": %d, \"run_rows\": %d}, ",
              h->T, h->NV, h->S, h->cps, h->grid, h->smem, h->stage_bytes, h->run_rows);
     s += tmp;
-    std::string ge = h->graph_error;
+    std::string ge = h->graph_error + (h->peer_error.empty() ? "" : " | " + h->peer_error);
     for (char &c : ge)
         if (c == '"' || c == '\\') c = '\'';
     s += "\"graph_error\": \"" + ge + "\", \"iters\": [";
@@ -913,9 +1023,19 @@ void tsvd_destroy(tsvd_t h) {
     if (!h) return;
     cudaSetDevice(h->dev);
     if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->comm) {  // barrier: no peer may still read our symmetric buffer when it is freed
+        int *d = nullptr;
+        if (cudaMalloc((void **)&d, sizeof(int)) == cudaSuccess) {
+            ncclAllReduce(d, d, 1, ncclInt32, ncclSum, h->comm, h->stream);
+            cudaStreamSynchronize(h->stream);
+            cudaFree(d);
+        }
+    }
     drop_graph(h);
-    void *dev_ptrs[] = {h->A_own, h->U32, h->V64, h->S64, h->ybuf, h->yw, h->V0d, h->c64, h->ypart, h->wpart,
-                        h->part, h->u64, h->sq_part, h->sig2, h->st, h->stats};
+    for (int r = 0; r < kMaxRanks; ++r)
+        if (h->peer_map[r]) cudaIpcCloseMemHandle(h->peer_map[r]);
+    void *dev_ptrs[] = {h->A_own, h->U32, h->V64, h->S64, h->ybuf, h->yw, h->V0d, h->c64, h->ypart,
+                        h->wpart, h->part, h->u64, h->sq_part, h->sig2, h->st, h->stats, h->sym};
     for (void *p : dev_ptrs)
         if (p) cudaFree(p);
     if (h->st_host) cudaFreeHost(h->st_host);

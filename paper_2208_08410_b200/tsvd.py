@@ -23,6 +23,7 @@ ERR_ARG, ERR_SHAPE, ERR_UNSUPPORTED, ERR_NOMEM, ERR_CUDA, ERR_NCCL, ERR_NUMERIC,
 MEM_DEVICE, MEM_HOST_PINNED, MEM_HOST_PAGEABLE = 0, 1, 2
 # tsvd_option
 OPT_MAX_ITER, OPT_FIXED_ITERS, OPT_SEED, OPT_GRAPH, OPT_TIMING, OPT_RUN_ROWS, OPT_CTAS_PER_SM = 1, 2, 3, 4, 5, 6, 7
+OPT_COLLECTIVE = 8  # world > 1: 0 = in-kernel NVLink peer all-reduce (default), 1 = ncclAllReduce
 F32, ROW_MAJOR = 0, 0
 
 _lib = None

@@ -41,6 +41,7 @@ def main():
     obj = [P.tsvd_get_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     t = P.TSVD(m, n, k, eps, rank=rank, world=world, uid=obj[0], device=local)
+    t.set_option(P.OPT_COLLECTIVE, int(os.environ.get("TSVD_COLLECTIVE", "0")))
     t.set_init(V0)
     t.set_dense(torch.from_numpy(np.ascontiguousarray(A[r0:r1])).cuda(), r0, r1)
     # one Gram-vector product with the all-reduce
@@ -52,7 +53,7 @@ def main():
     rep = t.report()
     t.close()
     outs = [None] * world
-    dist.all_gather_object(outs, (r0, r1, U, S, V, kf, list(iters), y, rep["loop"]))
+    dist.all_gather_object(outs, (r0, r1, U, S, V, kf, list(iters), y, rep["loop"] + "/" + rep["collective"]))
     ok = True
     for o in outs:
         ok &= np.array_equal(o[3], S) and np.array_equal(o[4], V) and np.array_equal(o[7], y)
