@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("world,collective", [(2, 0), (2, 1), (4, 0)])
+@pytest.mark.parametrize("world,collective", [(2, 0), (2, 1), (4, 0), (8, 0)])
 def test_row_partition_parity(world, collective):
     """collective 0: all-reduce fused into fin_iter over NVLink peer memory (graph mode);
     collective 1: ncclAllReduce with the host-driven loop."""
