@@ -41,6 +41,14 @@ CONFIGS = {
                m=65536, n=16384, k=16, eps=1e-6, family="hadamard", rank=32, rho=0.8, s0=1.0),
     "c1": dict(workload="dense fp32 512x256 known spectrum k=8 eps=1e-6 (BASELINE configs[0])",
                m=512, n=256, k=8, eps=1e-6, family="qr", rank=256, rho=0.8, s0=10.0),
+    # configs[2] is 4M x 16384 (256 GiB) host-resident; the GPU box has 196 GB of host RAM, so the
+    # out-of-memory path is measured on a 64 GiB slab forced fully streamed (no resident prefix):
+    # every pass moves all of A over the host link, exactly as the 256 GiB case would.
+    "c3s": dict(workload="dense fp32 1048576x16384 (64 GiB) in pinned host memory, streamed host->device every "
+                         "pass (OOM degree 1, no resident prefix), k=2, fixed T=3 (P:404); scaled from "
+                         "BASELINE configs[2] (256 GiB does not fit the box's 196 GB host RAM)",
+                m=1048576, n=16384, k=2, eps=1e-6, family="hadamard", rank=32, rho=0.8, s0=1.0,
+                stream=True, resident_bytes=0, fixed_T=3),
 }
 METRIC = "seconds to top-k triplets; Gram-vector effective GB/s vs HBM/H2D peak @1/2/4/8"
 
@@ -51,12 +59,30 @@ def slab(world, rank, m):
     return r0, r0 + base + (1 if rank < rem else 0)
 
 
-def make_A(cfg, r0, r1):
+def make_A(cfg, r0, r1, out=None):
     s = cfg["s0"] * cfg["rho"] ** np.arange(cfg["rank"])
     if cfg["family"] == "hadamard":
-        return synth.hadamard_lowrank(cfg["m"], cfg["n"], s, seed=1, rows=(r0, r1))
+        return synth.hadamard_lowrank(cfg["m"], cfg["n"], s, seed=1, rows=(r0, r1), out=out)
     A = synth.known_spectrum_qr(cfg["m"], cfg["n"], s, seed=1)
+    if out is not None:
+        out[...] = A[r0:r1]
+        return out
     return np.ascontiguousarray(A[r0:r1])
+
+
+def measure_h2d_peak(torch, device, nbytes=1 << 30):
+    """Pinned host -> device copy bandwidth (best of 5, CUDA events) on this process's GPU."""
+    src = torch.empty(nbytes // 4, dtype=torch.float32, pin_memory=True)
+    dst = torch.empty(nbytes // 4, dtype=torch.float32, device=f"cuda:{device}")
+    best = 0.0
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dst.copy_(src, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = max(best, nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    return best
 
 
 def planted(cfg):
@@ -197,9 +223,15 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     m, n, k, eps = cfg["m"], cfg["n"], cfg["k"], cfg["eps"]
+    stream_cfg = cfg.get("stream", False)
     r0, r1 = slab(world, rank, m)
-    A_host = make_A(cfg, r0, r1)
-    A_dev = torch.from_numpy(A_host).cuda()
+    if stream_cfg:  # out-of-memory degree 1: A lives in pinned host memory, streamed every pass
+        A_pin = torch.empty((r1 - r0, n), dtype=torch.float32, pin_memory=True)
+        A_host = make_A(cfg, r0, r1, out=A_pin.numpy())
+        A_dev = A_pin
+    else:
+        A_host = make_A(cfg, r0, r1)
+        A_dev = torch.from_numpy(A_host).cuda()
     V0 = synth.v0_normal(n, k, seed=2)
 
     uid = None
@@ -209,6 +241,11 @@ def main():
         uid = obj[0]
     t = P.TSVD(m, n, k, eps, rank=rank, world=world, uid=uid, device=local)
     t.set_init(V0)
+    if stream_cfg:
+        t.set_option(P.OPT_PLACEMENT, P.PLACEMENT_STREAM)
+        t.set_option(P.OPT_RESIDENT_BYTES, cfg.get("resident_bytes", 0))
+    if cfg.get("fixed_T"):
+        t.set_option(P.OPT_FIXED_ITERS, cfg["fixed_T"])
     t.set_dense(A_dev, r0, r1)
     if args.loop == "host":
         t.set_option(P.OPT_GRAPH, 0)
@@ -267,10 +304,31 @@ def main():
     achieved = per_launch_bytes / (n1_ms_per_launch / 1e3) / 1e9
     peak, peak_src = measured_peak()
     traffic = ncu_traffic(args.config) if world == 1 else None
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "kernel": "gv_fused (N1)", "per_launch_ms": n1_ms_per_launch,
+            "alg_bytes_per_launch": per_launch_bytes,
+            "share_of_step": rt["n1_ms"] / rt["run_ms"] if rt["run_ms"] else None,
+            "peak_source": peak_src, "rank0_rows": mg}
+    if stream_cfg:  # the pass is host-link bound: streamed bytes per pass over the H2D peak
+        pl = rep["placement"]
+        h2d_peak = measure_h2d_peak(torch, local)
+        streamed_per_step = pl["streamed_bytes"]
+        ach = streamed_per_step * world * args.steps / (ms / 1e3) / 1e9
+        roof = {"bound": "h2d", "achieved": ach, "peak": h2d_peak, "unit": "GB/s", "frac": ach / h2d_peak,
+                "traffic": None, "kernel": "streamed pass (H2D ring + gv_fused)",
+                "peak_source": "measured here: best of 5 cudaMemcpy of a 1 GiB pinned buffer per GPU",
+                "resident_rows": pl["resident_rows"], "batch_rows": pl["batch_rows"],
+                "queue_depth": pl["queue_depth"], "n1_per_launch_ms": n1_ms_per_launch,
+                "n1_hbm_gbs": achieved}
 
     # ---- end to end through the public API with host (pinned) A
     e2e = None
-    if not args.no_e2e:
+    if stream_cfg and not args.no_e2e:  # the timed steps already copy A host->device every pass
+        e2e = {"value": value, "unit": "GB/s", "seconds_to_topk": ms / args.steps / 1e3,
+               "h2d_bytes_per_step": rep["placement"]["streamed_bytes"] + 8 * k * n,
+               "d2h_bytes_per_step": 4 * mg * k + 8 * k + 8 * n * k + k * 64,
+               "note": "streamed config: value is already host-to-host (U, S, V read back after the timed region)"}
+    elif not args.no_e2e:
         A_pin = torch.from_numpy(A_host).pin_memory()
         t2 = P.TSVD(m, n, k, eps, rank=rank, world=world, uid=None, device=local) if world == 1 else None
         te = t2 if t2 is not None else t
@@ -313,11 +371,7 @@ def main():
                        "parallelism": f"row-partition x{world}", "l2": "no flush: A (4 GiB) > L2 (126 MB)"},
             "iterations": [int(x) for x in iters[:kf]], "k_found": kf, "status": rc,
             "check": {"sigma_max_rel_err_vs_planted": sig_err},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "gv_fused (N1)",
-                         "per_launch_ms": n1_ms_per_launch, "alg_bytes_per_launch": per_launch_bytes,
-                         "share_of_step": rt["n1_ms"] / rt["run_ms"] if rt["run_ms"] else None,
-                         "peak_source": peak_src, "rank0_rows": mg},
+            "roofline": roof,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks.summary(),
             "plan": rep["plan"], "loop": rep["loop"],
         }

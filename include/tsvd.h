@@ -70,9 +70,16 @@ typedef enum {
                                     totals appear in tsvd_get_report                              */
     TSVD_OPT_RUN_ROWS = 6,       /* rows per fp32 accumulation run before an fp64 flush (def 1024) */
     TSVD_OPT_CTAS_PER_SM = 7,    /* 0 = auto (occupancy); testing knob                              */
-    TSVD_OPT_COLLECTIVE = 8      /* world > 1: 0 (default) = all-reduce fused into the finalize kernel
+    TSVD_OPT_COLLECTIVE = 8,     /* world > 1: 0 (default) = all-reduce fused into the finalize kernel
                                     over NVLink peer memory (CUDA IPC, in-graph); 1 = ncclAllReduce
                                     with a host-driven loop (fallback / cross-check)                 */
+    TSVD_OPT_PLACEMENT = 9,      /* host input only: 0 auto (resident if the slab fits in HBM, else
+                                    OOM degree 1), 1 resident, 2 stream (resident prefix +
+                                    batches streamed host->device every pass)                        */
+    TSVD_OPT_RESIDENT_BYTES = 10,/* stream mode: cap on the HBM-resident prefix of A (-1 = as much as
+                                    fits; 0 = stream every row)                                       */
+    TSVD_OPT_BATCH_ROWS = 11,    /* stream mode: rows per H2D batch (0 = ~256 MiB batches)            */
+    TSVD_OPT_QUEUE_DEPTH = 12    /* stream mode: device ring slots q_s, 2..8, def. 3   */
 } tsvd_option;
 
 /*
@@ -108,10 +115,15 @@ tsvd_status tsvd_set_init(tsvd_t h, const double *V0);
  * tsvd_set_dense — this rank's row slab A[row_begin:row_end, 0:n], fp32 row-major with
  * leading dimension ld >= n (elements).  mem = DEVICE: the pointer is used in place when it
  * is 16-byte aligned and ld % 4 == 0, otherwise copied once into a padded device buffer.
- * mem = HOST_*: copied host->device inside every tsvd_run (end-to-end semantics).
+ * mem = HOST_*: copied host->device inside every tsvd_run (end-to-end semantics).  If the slab
+ * does not fit in HBM (or TSVD_OPT_PLACEMENT = 2) the run is out of memory of degree 1:
+ * a prefix of rows stays resident and the remaining rows are streamed every pass in row batches
+ * (collinear batching) through a q_s-slot device ring on a copy stream, overlapped with
+ * the fused kernel.  Pageable input is page-locked (cudaHostRegister) for the
+ * duration of a streamed run.
  * The union of all ranks' slabs must be [0, m) with contiguous, disjoint ranges.
  * Errors: TSVD_ERR_ARG (NULL, ld < n), TSVD_ERR_SHAPE (range outside [0, m) or empty),
- *         TSVD_ERR_NOMEM (slab does not fit in HBM: out-of-memory streaming is a later row).
+ *         TSVD_ERR_NOMEM (device input that is unaligned and has no room for an aligned copy).
  */
 tsvd_status tsvd_set_dense(tsvd_t h, const float *A, int64_t ld, int64_t row_begin, int64_t row_end, tsvd_mem mem);
 

@@ -75,6 +75,9 @@ struct GvParams {
     int32_t run_rows;        // fp32 run length before flushing to fp64
     double *u_out;           // EXTRACT: fp64 (A v)_r, indexed by launch row
     double *sq_part;         // EXTRACT: [gridDim.x] fp64 sum of (A v)_r^2
+    int32_t accumulate;      // 1: add into the partials of an earlier launch of the same pass
+                             //    (out-of-memory streaming: resident prefix, then ring batches)
+    int32_t pad_;
 };
 
 // ---------------------------------------------------------------- PTX helpers (mbarrier + TMA)
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) ya[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     double wacc = 0.0, sq = 0.0;
-    bool flushed = false;
+    bool flushed = p.accumulate != 0;
     double *yp = p.ypart + (int64_t)blockIdx.x * p.ypart_ld;
 
     auto flush = [&]() {
@@ -271,10 +274,13 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
         }
     }
     if (EXTRACT) {
-        if (tid == 0) p.sq_part[blockIdx.x] = sq;
+        if (tid == 0) p.sq_part[blockIdx.x] = p.accumulate ? p.sq_part[blockIdx.x] + sq : sq;
     } else {
         flush();
-        if (tid < l) p.wpart[(int64_t)blockIdx.x * p.wpart_ld + tid] = wacc;
+        if (tid < l) {
+            double *wp = p.wpart + (int64_t)blockIdx.x * p.wpart_ld + tid;
+            *wp = p.accumulate ? *wp + wacc : wacc;
+        }
     }
 }
 

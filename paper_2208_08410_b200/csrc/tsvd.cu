@@ -101,6 +101,16 @@ struct tsvd_s {
     std::vector<double> V0;
     bool have_V0 = false;
     int64_t v0_version = 1, v0_uploaded = 0;
+    // out-of-memory degree 1 (host input): resident prefix [0, m_res) + streamed batches
+    int placement = 0, qdepth = 3;
+    int64_t resident_cap = -1, batch_rows_opt = 0;
+    int64_t m_res = 0, batch_rows = 0, own_rows = 0;
+    bool streaming = false, host_registered = false;
+    std::vector<float *> ring;
+    std::vector<cudaEvent_t> ev_full, ev_free;
+    cudaStream_t copy_stream = nullptr;
+    int64_t streamed_bytes = 0, streamed_batches = 0;
+    double stream_pass_ms = 0.0;
     // factors (device)
     float *U32 = nullptr;   // m_g x kpad
     double *V64 = nullptr;  // n x k
@@ -314,39 +324,102 @@ static tsvd_status setup_peer(tsvd_t h) {
     return TSVD_OK;
 }
 
-// Make A resident on the device for this run (host input: H2D copy, counted in e2e timing).
+static void free_ring(tsvd_t h) {
+    for (float *p : h->ring) cudaFree(p);
+    for (cudaEvent_t e : h->ev_full) cudaEventDestroy(e);
+    for (cudaEvent_t e : h->ev_free) cudaEventDestroy(e);
+    h->ring.clear();
+    h->ev_full.clear();
+    h->ev_free.clear();
+}
+
+// Host input: decide the placement and make the resident rows device-resident for this
+// run (H2D copy, counted in e2e timing).  Degree 0: the whole slab.  Degree 1: rows [0, m_res)
+// resident, rows [m_res, m_g) streamed each pass through the ring (launch_pass).
 static tsvd_status stage_A(tsvd_t h) {
-    if (h->mem == TSVD_MEM_DEVICE) return TSVD_OK;
+    if (h->mem == TSVD_MEM_DEVICE) {
+        h->streaming = false;
+        h->m_res = h->m_g;
+        return TSVD_OK;
+    }
     const int64_t n4 = (h->n + 3) / 4;
-    if (!h->A_own) {
-        h->ld_own = n4 * 4;
-        size_t bytes = (size_t)h->m_g * h->ld_own * sizeof(float);
+    const int64_t row_bytes = n4 * 16;
+    h->ld_own = n4 * 4;
+    if (!h->A_own || h->own_rows == 0) {  // first staging for this slab: decide the placement once
         size_t fr = 0, tot = 0;
         CK(cudaMemGetInfo(&fr, &tot));
-        if (bytes + (256ull << 20) > fr)
-            return h->fail(TSVD_ERR_NOMEM, "row slab (%zu B) does not fit in HBM (%zu B free); streaming is a later row",
-                           bytes, fr);
-        cudaError_t e = cudaMalloc((void **)&h->A_own, bytes);
-        if (e == cudaErrorMemoryAllocation) return h->fail(TSVD_ERR_NOMEM, "A device buffer allocation failed");
-        CK(e);
-        if (h->ld_own != h->n) CK(cudaMemsetAsync(h->A_own, 0, bytes, h->stream));
+        const int64_t reserve = (int64_t)1 << 30;
+        const int64_t avail = std::max<int64_t>(0, (int64_t)fr - reserve);
+        const bool fits = row_bytes * h->m_g <= avail;
+        if (h->placement == 1 && !fits)
+            return h->fail(TSVD_ERR_NOMEM, "PLACEMENT=resident but the slab (%lld B) exceeds free HBM (%lld B)",
+                           (long long)(row_bytes * h->m_g), (long long)avail);
+        h->streaming = (h->placement == 2) || (h->placement == 0 && !fits);
+        if (!h->streaming) {
+            h->m_res = h->m_g;
+        } else {
+            h->batch_rows = h->batch_rows_opt > 0 ? h->batch_rows_opt
+                                                  : std::max<int64_t>(1, (256ll << 20) / row_bytes);
+            h->batch_rows = std::min(h->batch_rows, h->m_g);
+            const int64_t ring_bytes = (int64_t)h->qdepth * h->batch_rows * row_bytes;
+            if (ring_bytes > avail)
+                return h->fail(TSVD_ERR_NOMEM, "no room for the %d-slot streaming ring (OOM degree 2, P:173)",
+                               h->qdepth);
+            int64_t res = (avail - ring_bytes) / row_bytes;
+            if (h->resident_cap >= 0) res = std::min(res, h->resident_cap / row_bytes);
+            h->m_res = std::min(res, h->m_g);
+            for (int s = 0; s < h->qdepth; ++s) {
+                float *p = nullptr;
+                cudaEvent_t ef, eb;
+                CK(cudaMalloc((void **)&p, (size_t)h->batch_rows * row_bytes));
+                CK(cudaEventCreateWithFlags(&ef, cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&eb, cudaEventDisableTiming));
+                h->ring.push_back(p);
+                h->ev_full.push_back(ef);
+                h->ev_free.push_back(eb);
+            }
+            if (!h->copy_stream) CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+        }
+        if (h->m_res > 0) {
+            if (h->A_own) cudaFree(h->A_own);
+            h->A_own = nullptr;
+            cudaError_t e = cudaMalloc((void **)&h->A_own, (size_t)h->m_res * row_bytes);
+            if (e == cudaErrorMemoryAllocation) return h->fail(TSVD_ERR_NOMEM, "A device buffer allocation failed");
+            CK(e);
+            if (h->ld_own != h->n) CK(cudaMemsetAsync(h->A_own, 0, (size_t)h->m_res * row_bytes, h->stream));
+        }
+        h->own_rows = std::max<int64_t>(h->m_res, 1);
         h->graph_l0 = -1;  // A pointer changed: the cached run graph is stale
     }
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    CK(cudaEventRecord(e0, h->stream));
-    CK(cudaMemcpy2DAsync(h->A_own, h->ld_own * sizeof(float), h->A_user, h->ld_user * sizeof(float),
-                         h->n * sizeof(float), h->m_g, cudaMemcpyHostToDevice, h->stream));
-    CK(cudaEventRecord(e1, h->stream));
-    CK(cudaEventSynchronize(e1));
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, e0, e1));
-    h->h2d_ms += ms;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    if (h->streaming && h->mem == TSVD_MEM_HOST_PAGEABLE && !h->host_registered) {
+        CK(cudaHostRegister((void *)h->A_user, (size_t)h->m_g * h->ld_user * sizeof(float), cudaHostRegisterDefault));
+        h->host_registered = true;
+    }
+    if (h->m_res > 0) {
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, h->stream));
+        CK(cudaMemcpy2DAsync(h->A_own, h->ld_own * sizeof(float), h->A_user, h->ld_user * sizeof(float),
+                             h->n * sizeof(float), h->m_res, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaEventRecord(e1, h->stream));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        h->h2d_ms += ms;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
     h->A_use = h->A_own;
     h->ld_use = h->ld_own;
+    return TSVD_OK;
+}
+
+static tsvd_status unstage_A(tsvd_t h) {
+    if (h->host_registered) {
+        CK(cudaHostUnregister((void *)h->A_user));
+        h->host_registered = false;
+    }
     return TSVD_OK;
 }
 
@@ -355,7 +428,7 @@ static GvParams gv_params(tsvd_t h, int l, bool extract) {
     GvParams p{};
     p.A = h->A_use;
     p.ld = h->ld_use;
-    p.rows = h->m_g;
+    p.rows = h->m_res;
     p.n = (int32_t)h->n;
     p.n4 = (int32_t)((h->n + 3) / 4);
     p.U = h->U32;
@@ -379,10 +452,41 @@ static GvParams gv_params(tsvd_t h, int l, bool extract) {
     return p;
 }
 
+// One pass of N1 over this rank's rows.  Resident slab: one launch.  Out of memory (degree 1): one
+// launch over the resident prefix, then row batches copied host->device on the copy stream into a
+// q_s-slot ring (slot reuse gated by events) and consumed by N1 launches that accumulate into the
+// same per-CTA partials, so the H2D of batch b+1.. overlaps the kernel on batch b.
 static tsvd_status launch_gv(tsvd_t h, cudaStream_t s, int l, bool extract) {
+    GvFn fn = extract ? h->gv_ex : h->gv;
     GvParams p = gv_params(h, l, extract);
-    (extract ? h->gv_ex : h->gv)<<<h->grid, h->T, h->smem, s>>>(p);
-    CK(cudaGetLastError());
+    if (!h->streaming || h->m_res > 0) {
+        fn<<<h->grid, h->T, h->smem, s>>>(p);
+        CK(cudaGetLastError());
+    }
+    if (!h->streaming) return TSVD_OK;
+    const int64_t row_bytes = (int64_t)h->row_bytes;
+    int b = 0;
+    for (int64_t r0 = h->m_res; r0 < h->m_g; r0 += h->batch_rows, ++b) {
+        const int slot = b % h->qdepth;
+        const int64_t rows = std::min(h->batch_rows, h->m_g - r0);
+        CK(cudaStreamWaitEvent(h->copy_stream, h->ev_free[slot], 0));
+        CK(cudaMemcpy2DAsync(h->ring[slot], row_bytes, h->A_user + r0 * h->ld_user, h->ld_user * sizeof(float),
+                             h->n * sizeof(float), rows, cudaMemcpyHostToDevice, h->copy_stream));
+        CK(cudaEventRecord(h->ev_full[slot], h->copy_stream));
+        CK(cudaStreamWaitEvent(s, h->ev_full[slot], 0));
+        GvParams q = p;
+        q.A = h->ring[slot];
+        q.ld = row_bytes / 4;
+        q.rows = rows;
+        q.U = h->U32 + r0 * h->kpad;
+        q.u_out = h->u64 + r0;
+        q.accumulate = (r0 > 0 || h->m_res > 0) ? 1 : 0;
+        fn<<<h->grid, h->T, h->smem, s>>>(q);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(h->ev_free[slot], s));
+        h->streamed_bytes += rows * h->n * (int64_t)sizeof(float);
+        h->streamed_batches += 1;
+    }
     return TSVD_OK;
 }
 
@@ -757,6 +861,23 @@ tsvd_status tsvd_set_option(tsvd_t h, int32_t key, int64_t value) {
         h->coll_opt = (int)value;
         if (h->world > 1) h->coll = (value == 1 || !h->sym || !h->pv.flags) ? COLL_NCCL : COLL_PEER;
         break;
+    case TSVD_OPT_PLACEMENT:
+    case TSVD_OPT_RESIDENT_BYTES:
+    case TSVD_OPT_BATCH_ROWS:
+    case TSVD_OPT_QUEUE_DEPTH:
+        if (key == TSVD_OPT_PLACEMENT && (value < 0 || value > 2)) return h->fail(TSVD_ERR_ARG, "PLACEMENT in 0..2");
+        if (key == TSVD_OPT_RESIDENT_BYTES && value < -1) return h->fail(TSVD_ERR_ARG, "RESIDENT_BYTES >= -1");
+        if (key == TSVD_OPT_BATCH_ROWS && value < 0) return h->fail(TSVD_ERR_ARG, "BATCH_ROWS >= 0");
+        if (key == TSVD_OPT_QUEUE_DEPTH && (value < 2 || value > 8)) return h->fail(TSVD_ERR_ARG, "QUEUE_DEPTH in 2..8");
+        if (key == TSVD_OPT_PLACEMENT) h->placement = (int)value;
+        if (key == TSVD_OPT_RESIDENT_BYTES) h->resident_cap = value;
+        if (key == TSVD_OPT_BATCH_ROWS) h->batch_rows_opt = value;
+        if (key == TSVD_OPT_QUEUE_DEPTH) h->qdepth = (int)value;
+        if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
+        if (h->stream) cudaStreamSynchronize(h->stream);
+        free_ring(h);
+        h->own_rows = 0;  // re-decide the placement at the next staging
+        break;
     default: return h->fail(TSVD_ERR_ARG, "unknown option %d", key);
     }
     h->graph_l0 = -1;  // options are baked into the captured kernel parameters
@@ -866,6 +987,7 @@ tsvd_status tsvd_gram_apply(tsvd_t h, const double *v, double *y) {
     CK(cudaStreamSynchronize(h->stream));
     if (h->st_host->status == -6) return h->fail(TSVD_ERR_NCCL, "peer all-reduce timed out (a rank did not arrive)");
     memcpy(y, h->vec_host, (size_t)n * sizeof(double));
+    TRY(unstage_A(h));
     return TSVD_OK;
 }
 
@@ -886,7 +1008,10 @@ tsvd_status tsvd_run(tsvd_t h) {
     CK(cudaMemsetAsync(h->stats, 0, (size_t)h->k * sizeof(CompStat), h->stream));
     TRY(reset_state(h));
     // the graph needs every collective to be a kernel: single GPU or the peer all-reduce
-    const bool graph = h->use_graph && !h->timing && h->coll != COLL_NCCL;
+    h->streamed_bytes = 0;
+    h->streamed_batches = 0;
+    // the graph needs every step to be a device kernel: no NCCL call, no host->device streaming
+    const bool graph = h->use_graph && !h->timing && h->coll != COLL_NCCL && !h->streaming;
     bool ran = false;
     if (graph) {
         tsvd_status gs = TSVD_OK;
@@ -922,6 +1047,7 @@ tsvd_status tsvd_run(tsvd_t h) {
         h->l_found = l + 1;
         h->k_found = l + 1;
     }
+    TRY(unstage_A(h));
     h->run_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (result == TSVD_WARN_RANK_EXHAUSTED) h->err = "rank exhausted before k components";
     return result;
@@ -978,6 +1104,12 @@ tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
              "\"stage_bytes\": %d, \"run_rows\": %d}, ",
              h->T, h->NV, h->S, h->cps, h->grid, h->smem, h->stage_bytes, h->run_rows);
     s += tmp;
+    snprintf(tmp, sizeof tmp,
+             "\"placement\": {\"streaming\": %s, \"resident_rows\": %lld, \"batch_rows\": %lld, \"queue_depth\": %d, "
+             "\"streamed_bytes\": %lld, \"streamed_batches\": %lld}, ",
+             h->streaming ? "true" : "false", (long long)h->m_res, (long long)h->batch_rows, h->qdepth,
+             (long long)h->streamed_bytes, (long long)h->streamed_batches);
+    s += tmp;
     std::string ge = h->graph_error + (h->peer_error.empty() ? "" : " | " + h->peer_error);
     for (char &c : ge)
         if (c == '"' || c == '\\') c = '\'';
@@ -1032,6 +1164,10 @@ void tsvd_destroy(tsvd_t h) {
         }
     }
     drop_graph(h);
+    if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
+    free_ring(h);
+    if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+    if (h->host_registered) cudaHostUnregister((void *)h->A_user);
     for (int r = 0; r < kMaxRanks; ++r)
         if (h->peer_map[r]) cudaIpcCloseMemHandle(h->peer_map[r]);
     void *dev_ptrs[] = {h->A_own, h->U32, h->V64, h->S64, h->ybuf, h->yw, h->V0d, h->c64, h->ypart,
