@@ -128,7 +128,15 @@ tsvd_status tsvd_set_init(tsvd_t h, const double *V0);
 tsvd_status tsvd_set_dense(tsvd_t h, const float *A, int64_t ld, int64_t row_begin, int64_t row_end, tsvd_mem mem);
 
 /*
- * tsvd_set_csr — sparse CSR slab.  Not in this version: returns TSVD_ERR_UNSUPPORTED.
+ * tsvd_set_csr — this rank's sparse row slab rows [row_begin, row_end) in CSR: row_ptr
+ * int64[rows + 1] with row_ptr[0] == 0 and row_ptr[rows] == nnz, col_idx int32[nnz] (strictly
+ * increasing inside a row, in [0, n)), val fp32[nnz].  mem = DEVICE: borrowed in place; HOST_*:
+ * copied once.  The CSR is validated on the device, then its CSC is built once on the device
+ * (histogram, scan, scatter, per-column sort: deterministic), so every iteration runs the
+ * row-wise product t = A v - U c and the column-wise, atomics-free y = A^T t.  The CSC doubles
+ * the slab's footprint.  Multi-GPU: the length-n partial y is summed with ncclAllReduce.
+ * Errors: TSVD_ERR_ARG (NULL arrays, bad row_ptr ends, columns out of range or unsorted),
+ *         TSVD_ERR_SHAPE, TSVD_ERR_UNSUPPORTED (n or rows > 2^31 - 1), TSVD_ERR_CUDA / NOMEM.
  */
 tsvd_status tsvd_set_csr(tsvd_t h, const int64_t *row_ptr, const int32_t *col_idx, const float *val, int64_t nnz,
                          int64_t row_begin, int64_t row_end, tsvd_mem mem);

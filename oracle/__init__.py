@@ -63,6 +63,14 @@ def _load():
             lib.oracle_matvec.argtypes = [_f, _i64, _i64, _i64, _d, _d]
             lib.oracle_matvec_t.argtypes = [_f, _i64, _i64, _i64, _d, _d]
             lib.oracle_num_threads.restype = ctypes.c_int
+            _l64 = ctypes.POINTER(ctypes.c_int64)
+            _i32p = ctypes.POINTER(ctypes.c_int32)
+            lib.oracle_gram_apply_csr.argtypes = [_l64, _i32p, _f, _i64, _i64, _d, _i64, _d, _d, _i64, ctypes.c_int,
+                                                  _d, _d]
+            lib.oracle_tsvd_csr.argtypes = [_l64, _i32p, _f, _i64, _i64, ctypes.c_int, ctypes.c_double, _d,
+                                            ctypes.c_int, ctypes.c_int, _d, _d, _d, _i, _d, _i]
+            lib.oracle_csr_matvec.argtypes = [_l64, _i32p, _f, _i64, _d, _d]
+            lib.oracle_csr_matvec_t.argtypes = [_l64, _i32p, _f, _i64, _i64, _d, _d]
             _lib = lib
     return _lib
 
@@ -160,6 +168,61 @@ def tsvd(A, k: int, eps: float, V0, max_iter: int = 10000, fixed_T: int = 0, mod
                              _p(U, _d), _p(S, _d), _p(V, _d), _p(iters, _i), _p(dots, _d), ctypes.byref(kf))
     if rc < 0:
         raise RuntimeError(f"oracle_tsvd rc={rc}")
+    return TSVDResult(U, S, V, iters, dots, kf.value, rc)
+
+
+def _csr(rp, ci, va):
+    rp = np.ascontiguousarray(rp, dtype=np.int64)
+    ci = np.ascontiguousarray(ci, dtype=np.int32)
+    va = np.ascontiguousarray(va, dtype=np.float32)
+    return rp, ci, va, (_p(rp, ctypes.POINTER(ctypes.c_int64)), _p(ci, ctypes.POINTER(ctypes.c_int32)), _p(va, _f))
+
+
+def csr_matvec(rp, ci, va, x):
+    rp, ci, va, ptrs = _csr(rp, ci, va)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty(len(rp) - 1)
+    _load().oracle_csr_matvec(*ptrs, len(rp) - 1, _p(x, _d), _p(out, _d))
+    return out
+
+
+def csr_matvec_t(rp, ci, va, n, x):
+    rp, ci, va, ptrs = _csr(rp, ci, va)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty(n)
+    _load().oracle_csr_matvec_t(*ptrs, len(rp) - 1, n, _p(x, _d), _p(out, _d))
+    return out
+
+
+def gram_apply_csr(rp, ci, va, n, U, S, V, v):
+    """y = X'^T X' v for a CSR A (F2)."""
+    rp, ci, va, ptrs = _csr(rp, ci, va)
+    m = len(rp) - 1
+    U, S, V, l = _factors(U, S, V, m, n)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    y = np.empty(n)
+    rc = _load().oracle_gram_apply_csr(*ptrs, m, n, _p(U, _d), U.shape[1], _p(S, _d), _p(V, _d), V.shape[1], l,
+                                       _p(v, _d), _p(y, _d))
+    if rc != OK:
+        raise RuntimeError(f"oracle_gram_apply_csr rc={rc}")
+    return y
+
+
+def tsvd_csr(rp, ci, va, n, k: int, eps: float, V0, max_iter: int = 10000, fixed_T: int = 0) -> TSVDResult:
+    """Alg. 1 + Alg. 2 (F2) for a CSR A with m >= n."""
+    rp, ci, va, ptrs = _csr(rp, ci, va)
+    m = len(rp) - 1
+    V0 = np.ascontiguousarray(V0, dtype=np.float64)
+    U = np.zeros((m, k))
+    V = np.zeros((n, k))
+    S = np.zeros(k)
+    iters = np.zeros(k, dtype=np.int32)
+    dots = np.zeros(k)
+    kf = ctypes.c_int(0)
+    rc = _load().oracle_tsvd_csr(*ptrs, m, n, k, eps, _p(V0, _d), max_iter, fixed_T, _p(U, _d), _p(S, _d),
+                                 _p(V, _d), _p(iters, _i), _p(dots, _d), ctypes.byref(kf))
+    if rc < 0:
+        raise RuntimeError(f"oracle_tsvd_csr rc={rc}")
     return TSVDResult(U, S, V, iters, dots, kf.value, rc)
 
 

@@ -103,11 +103,51 @@ static double dot(const double *a, const double *b, int64_t n) {
 
 static double nrm2(const double *a, int64_t n) { return sqrt(dot(a, a, n)); }
 
+/* ---- CSR products (sparse A: "stored in a sparse Compressed Sparse Row (CSR) format") */
+
+/* out[r] = sum_k val[k] x[col[k]], k over row r in stored order */
+void oracle_csr_matvec(const int64_t *rp, const int32_t *ci, const float *va, int64_t m, const double *x,
+                       double *out) {
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < m; ++r) {
+        double s = 0.0;
+        for (int64_t k = rp[r]; k < rp[r + 1]; ++k) s += (double)va[k] * x[ci[k]];
+        out[r] = s;
+    }
+}
+
+/* out[j] = sum_r A[r,j] x[r]: rows in order (sequential, so each out[j] sums in row order) */
+void oracle_csr_matvec_t(const int64_t *rp, const int32_t *ci, const float *va, int64_t m, int64_t n,
+                         const double *x, double *out) {
+    for (int64_t j = 0; j < n; ++j) out[j] = 0.0;
+    for (int64_t r = 0; r < m; ++r)
+        for (int64_t k = rp[r]; k < rp[r + 1]; ++k) out[ci[k]] += (double)va[k] * x[r];
+}
+
+/* The operator A of one problem: dense (A != NULL) or CSR. */
+typedef struct {
+    const float *A;
+    int64_t lda;
+    const int64_t *rp;
+    const int32_t *ci;
+    const float *va;
+} op_t;
+
+static void op_mv(const op_t *o, int64_t m, int64_t n, const double *x, double *out) {
+    if (o->A) oracle_matvec(o->A, m, n, o->lda, x, out);
+    else oracle_csr_matvec(o->rp, o->ci, o->va, m, x, out);
+}
+
+static void op_mvt(const op_t *o, int64_t m, int64_t n, const double *x, double *out) {
+    if (o->A) oracle_matvec_t(o->A, m, n, o->lda, x, out);
+    else oracle_csr_matvec_t(o->rp, o->ci, o->va, m, n, x, out);
+}
+
 /* ---- Gram-vector products ---------------------------------------------------- */
 
 /* ORACLE_F2: y = X'^T X' v with X' = A - U diag(S) V^T, never formed.
  * Right-to-left as Eq. 2 asks, but grouped as X'^T (X' v). */
-static int gram_f2(const float *A, int64_t m, int64_t n, int64_t lda, const double *U, int64_t ldu,
+static int gram_f2(const op_t *op, int64_t m, int64_t n, const double *U, int64_t ldu,
                    const double *S, const double *V, int64_t ldv, int l, const double *v, double *y) {
     double *c = (double *)calloc((size_t)(l > 0 ? l : 1), sizeof(double));
     double *w = (double *)calloc((size_t)(l > 0 ? l : 1), sizeof(double));
@@ -120,7 +160,7 @@ static int gram_f2(const float *A, int64_t m, int64_t n, int64_t lda, const doub
         c[i] = S[i] * s;
     }
     /* t_r = sum_j A[r,j] v_j - sum_i U[r,i] c_i     (X' v) */
-    oracle_matvec(A, m, n, lda, v, t);
+    op_mv(op, m, n, v, t);
     for (int64_t r = 0; r < m; ++r) {
         double s = 0.0;
         for (int i = 0; i < l; ++i) s += U[r * ldu + i] * c[i];
@@ -133,7 +173,7 @@ static int gram_f2(const float *A, int64_t m, int64_t n, int64_t lda, const doub
         w[i] = S[i] * s;
     }
     /* y_j = sum_r A[r,j] t_r - sum_i V[j,i] w_i   (X'^T X' v) */
-    oracle_matvec_t(A, m, n, lda, t, y);
+    op_mvt(op, m, n, t, y);
     for (int64_t j = 0; j < n; ++j) {
         double s = 0.0;
         for (int i = 0; i < l; ++i) s += V[j * ldv + i] * w[i];
@@ -216,12 +256,22 @@ static int gram_eq2(const float *A, int64_t m, int64_t n, int64_t lda, const dou
 int oracle_gram_apply(int mode, const float *A, int64_t m, int64_t n, int64_t lda, const double *U, int64_t ldu,
                       const double *S, const double *V, int64_t ldv, int l, const double *v, double *y) {
     if (m <= 0 || n <= 0 || lda < n || l < 0) return OR_ERR_ARG;
+    const op_t op = {A, lda, NULL, NULL, NULL};
     switch (mode) {
-    case ORACLE_F2: return gram_f2(A, m, n, lda, U, ldu, S, V, ldv, l, v, y);
+    case ORACLE_F2: return gram_f2(&op, m, n, U, ldu, S, V, ldv, l, v, y);
     case ORACLE_LITERAL: return gram_literal(A, m, n, lda, U, ldu, S, V, ldv, l, v, y);
     case ORACLE_EQ2: return gram_eq2(A, m, n, lda, U, ldu, S, V, ldv, l, v, y);
     default: return OR_ERR_ARG;
     }
+}
+
+/* Same product for a CSR A (F2 only: the literal / Eq. 2 modes are dense cross-checks). */
+int oracle_gram_apply_csr(const int64_t *rp, const int32_t *ci, const float *va, int64_t m, int64_t n,
+                          const double *U, int64_t ldu, const double *S, const double *V, int64_t ldv, int l,
+                          const double *v, double *y) {
+    if (m <= 0 || n <= 0 || l < 0) return OR_ERR_ARG;
+    const op_t op = {NULL, 0, rp, ci, va};
+    return gram_f2(&op, m, n, U, ldu, S, V, ldv, l, v, y);
 }
 
 /* Mirror for m < n (Eq. 3), exact factored form: y = X' X'^T u,
@@ -278,17 +328,38 @@ int oracle_gram_apply_wide(const float *A, int64_t m, int64_t n, int64_t lda, co
  *   OR_OK, OR_NOT_CONVERGED (some component hit max_iter), OR_RANK_EXHAUSTED (||B v0|| == 0
  *   or sigma == 0 before k components), OR_ERR_ARG, OR_ERR_NUMERIC (non-finite), OR_ERR_NOMEM.
  */
+static int tsvd_core(const op_t *op, int64_t m, int64_t n, int k, double eps, const double *V0, int max_iter,
+                     int fixed_T, int mode, double *U, double *S, double *V, int *iters, double *dots, int *k_found);
+
 int oracle_tsvd(const float *A, int64_t m, int64_t n, int64_t lda, int k, double eps, const double *V0,
                 int max_iter, int fixed_T, int mode, double *U, double *S, double *V, int *iters, double *dots,
                 int *k_found) {
+    *k_found = 0;
+    if (lda < n) return OR_ERR_ARG;
+    const op_t op = {A, lda, NULL, NULL, NULL};
+    return tsvd_core(&op, m, n, k, eps, V0, max_iter, fixed_T, mode, U, S, V, iters, dots, k_found);
+}
+
+/* oracle_tsvd for a CSR A (m >= n, F2): same algorithm, sparse products. */
+int oracle_tsvd_csr(const int64_t *rp, const int32_t *ci, const float *va, int64_t m, int64_t n, int k, double eps,
+                    const double *V0, int max_iter, int fixed_T, double *U, double *S, double *V, int *iters,
+                    double *dots, int *k_found) {
+    *k_found = 0;
+    if (m < n) return OR_ERR_ARG;
+    const op_t op = {NULL, 0, rp, ci, va};
+    return tsvd_core(&op, m, n, k, eps, V0, max_iter, fixed_T, ORACLE_F2, U, S, V, iters, dots, k_found);
+}
+
+static int tsvd_core(const op_t *op, int64_t m, int64_t n, int k, double eps, const double *V0, int max_iter,
+                     int fixed_T, int mode, double *U, double *S, double *V, int *iters, double *dots, int *k_found) {
     const int tall = (m >= n); /* reading R2: square -> V first (P:83 vs P:264) */
     const int64_t len = tall ? n : m;     /* SVD_1D vector length */
     const int64_t other = tall ? m : n;
     if (k == -1) k = (int)(m < n ? m : n);
     *k_found = 0;
-    if (m <= 0 || n <= 0 || lda < n || k <= 0 || k > (m < n ? m : n) || !(eps > 0.0 && eps < 1.0))
+    if (m <= 0 || n <= 0 || k <= 0 || k > (m < n ? m : n) || !(eps > 0.0 && eps < 1.0))
         return OR_ERR_ARG;
-    if (!tall && mode != ORACLE_F2) return OR_ERR_ARG;
+    if ((!tall || !op->A) && mode != ORACLE_F2) return OR_ERR_ARG;
     if (max_iter <= 0) max_iter = 10000;
     double *v0 = (double *)malloc((size_t)len * sizeof(double));
     double *v1 = (double *)malloc((size_t)len * sizeof(double));
@@ -303,8 +374,10 @@ int oracle_tsvd(const float *A, int64_t m, int64_t n, int64_t lda, int k, double
         int it = 0;
         double d = 0.0;
         for (;;) {                           /* P:119 while true */
-            int rc = tall ? oracle_gram_apply(mode, A, m, n, lda, U, k, S, V, k, l, v0, v1)
-                          : oracle_gram_apply_wide(A, m, n, lda, U, k, S, V, k, l, v0, v1);
+            int rc;
+            if (!tall) rc = oracle_gram_apply_wide(op->A, m, n, op->lda, U, k, S, V, k, l, v0, v1);
+            else if (op->A) rc = oracle_gram_apply(mode, op->A, m, n, op->lda, U, k, S, V, k, l, v0, v1);
+            else rc = gram_f2(op, m, n, U, k, S, V, k, l, v0, v1);
             if (rc != OR_OK) { status = rc; goto done; }
             double ny = nrm2(v1, len);
             if (!isfinite(ny)) { status = OR_ERR_NUMERIC; goto done; }
@@ -323,8 +396,8 @@ int oracle_tsvd(const float *A, int64_t m, int64_t n, int64_t lda, int k, double
             memcpy(v0, v1, (size_t)len * sizeof(double));               /* P:126 */
         }
         /* Extraction with the ORIGINAL A (P:85-87 / P:90-92) */
-        if (tall) oracle_matvec(A, m, n, lda, v1, p);
-        else oracle_matvec_t(A, m, n, lda, v1, p);
+        if (tall) op_mv(op, m, n, v1, p);
+        else op_mvt(op, m, n, v1, p);
         double sigma = nrm2(p, other);
         if (!isfinite(sigma)) { status = OR_ERR_NUMERIC; goto done; }
         if (sigma == 0.0) { status = OR_RANK_EXHAUSTED; goto done; }

@@ -78,16 +78,19 @@ __global__ void __launch_bounds__(kFinThreads)
     __shared__ double gsum[kFinGroups][kFinCols];
     if (st->stop || st->done) return;
     const int tid = threadIdx.x, lane = tid & 31, grp = tid >> 5;
-    const int j = blockIdx.x * kFinCols + lane;
-    double s = 0.0;
-    if (j < n)
-        for (int b = grp; b < parts; b += kFinGroups) s += ypart[(int64_t)b * ypart_ld + j];
-    gsum[grp][lane] = s;
-    __syncthreads();
-    if (grp == 0 && j < n) {
-        double y = gsum[0][lane];
-        for (int q = 1; q < kFinGroups; ++q) y += gsum[q][lane];
-        yw[j] = y;
+    for (int64_t ch = blockIdx.x; ch * kFinCols < n; ch += gridDim.x) {
+        const int64_t j = ch * kFinCols + lane;
+        double s = 0.0;
+        if (j < n)
+            for (int b = grp; b < parts; b += kFinGroups) s += ypart[(int64_t)b * ypart_ld + j];
+        gsum[grp][lane] = s;
+        __syncthreads();
+        if (grp == 0 && j < n) {
+            double y = gsum[0][lane];
+            for (int q = 1; q < kFinGroups; ++q) y += gsum[q][lane];
+            yw[j] = y;
+        }
+        __syncthreads();
     }
     if (blockIdx.x == 0)
         for (int i = grp; i < l; i += kFinGroups) {
@@ -122,16 +125,19 @@ __global__ void __launch_bounds__(kFinThreads) publish(const PubParams p) {
     const unsigned e = st->epoch;
     double *slot = p.pv.buf[p.pv.rank] + (int64_t)(e & 1u) * p.pv.slot_stride;
     if (p.mode == 0) {
-        const int j = blockIdx.x * kFinCols + lane;
-        double s = 0.0;
-        if (j < p.n)
-            for (int b = grp; b < p.parts; b += kFinGroups) s += p.ypart[(int64_t)b * p.ypart_ld + j];
-        gsum[grp][lane] = s;
-        __syncthreads();
-        if (grp == 0 && j < p.n) {
-            double y = gsum[0][lane];
-            for (int q = 1; q < kFinGroups; ++q) y += gsum[q][lane];
-            slot[j] = y;
+        for (int64_t ch = blockIdx.x; ch * kFinCols < p.n; ch += gridDim.x) {
+            const int64_t j = ch * kFinCols + lane;
+            double s = 0.0;
+            if (j < p.n)
+                for (int b = grp; b < p.parts; b += kFinGroups) s += p.ypart[(int64_t)b * p.ypart_ld + j];
+            gsum[grp][lane] = s;
+            __syncthreads();
+            if (grp == 0 && j < p.n) {
+                double y = gsum[0][lane];
+                for (int q = 1; q < kFinGroups; ++q) y += gsum[q][lane];
+                slot[j] = y;
+            }
+            __syncthreads();
         }
         if (blockIdx.x == 0)
             for (int i = grp; i < p.l; i += kFinGroups) {
@@ -188,32 +194,41 @@ struct FinParams {
 // FIN_LOAD_RAW: ybuf[0] = v, ny := 1, c = S V^T v                          (tsvd_gram_apply)
 // FIN_APPLY   : ybuf[1] = sum(partials) - V (S w); no state change        (tsvd_gram_apply)
 //
-// Block = 256 threads = 32 columns x 8 partial groups: thread (c, g) sums the per-CTA partials
-// b = g, g+8, ... of column c; the 8 group sums are added in g order.  Grid = ceil(n / 32).
+// Grid-stride over column chunks (grid <= a few blocks per SM, so the last block reduces a bounded
+// number of block partials even at n = 1e8).  SRC_PARTS reductions use 32-column chunks: thread
+// (c, g) sums the per-CTA partials b = g, g+8, ... of column c and the 8 group sums are added in g
+// order.  Other sources use 256-column chunks, one column per thread.  (V^T y)_i for i < 16 is
+// accumulated in registers by the thread that owns the column; components >= 16 go through a
+// shared-memory tile.  Every sum has a fixed order.
+constexpr int kVtReg = 16;
+
 template <int SRC>
 __global__ void __launch_bounds__(kFinThreads) fin_iter(const FinParams p) {
     __shared__ double gsum[kFinGroups][kFinCols];
-    __shared__ double ys[kFinCols];
+    __shared__ double wred[kFinThreads / 32][2 + kVtReg];
     __shared__ int am_last, peer_ok;
     __shared__ double inv_s;
-    extern __shared__ double dyn[];  // g[l] then tot[2 + l]
+    extern __shared__ double dyn[];  // g[l] | tot[2 + l] | vtx[max(0, l - 16)] | ys[256]
+    const int l = p.l;
+    const int lx = l > kVtReg ? l - kVtReg : 0;
     double *g = dyn;
-    double *tot = dyn + p.l;
+    double *tot = g + l;
+    double *vtx = tot + 2 + l;
+    double *ys = vtx + lx;
     LoopState *st = p.st;
     const int tid = threadIdx.x, lane = tid & 31, grp = tid >> 5;
     if (st->stop || (p.mode == FIN_ITERATE && st->done)) {
         if (blockIdx.x == 0 && tid == 0) set_cond(p.cond, p.use_cond, 0u);
         return;
     }
-    const int mode = p.mode, n = p.n, l = p.l;
+    const int mode = p.mode;
+    const int64_t n = p.n;
     const int it = st->it;
     const double ny = st->ny;
     const unsigned e = st->epoch;
     const double *ycur = p.ybuf + (int64_t)(it & 1) * p.ystride;
     double *ynew = p.ybuf + (int64_t)(mode == FIN_ITERATE ? ((it + 1) & 1) : (mode == FIN_APPLY ? 1 : 0)) * p.ystride;
     const bool reduce = (mode == FIN_ITERATE || mode == FIN_APPLY);
-    const int j0 = blockIdx.x * kFinCols;
-    const int j = j0 + lane;
     const int64_t slot_off = (int64_t)(e & 1u) * p.pv.slot_stride;
 
     if (reduce) {
@@ -232,13 +247,6 @@ __global__ void __launch_bounds__(kFinThreads) fin_iter(const FinParams p) {
                 w = warp_sum(w);
                 if (lane == 0) g[i] = p.S[i] * w;
             }
-            double s = 0.0;
-            if (j < n) {
-                const double *col = p.ypart + j;
-#pragma unroll 4
-                for (int b = grp; b < p.parts; b += kFinGroups) s += col[(int64_t)b * p.ypart_ld];
-            }
-            gsum[grp][lane] = s;
         } else if (SRC == SRC_YW) {
             for (int i = tid; i < l; i += kFinThreads) g[i] = p.S[i] * p.yw[p.wofs + i];
         } else {
@@ -248,48 +256,103 @@ __global__ void __launch_bounds__(kFinThreads) fin_iter(const FinParams p) {
                 g[i] = p.S[i] * w;
             }
         }
-        __syncthreads();
     }
-    if (grp == 0) {  // one warp finishes the 32 columns
-        double yj = 0.0, vj = 0.0;
-        if (j < n) {
-            if (reduce) {
-                if (SRC == SRC_PARTS) {
-                    yj = gsum[0][lane];
+    for (int i = tid; i < lx; i += kFinThreads) vtx[i] = 0.0;
+    __syncthreads();
+
+    const bool narrow = (SRC == SRC_PARTS) && reduce;  // 32-column chunks with the 8-group reduction
+    const int cols = narrow ? kFinCols : kFinThreads;
+    const int64_t nchunks = (n + cols - 1) / cols;
+    double a_yy = 0.0, a_vy = 0.0;
+    double acc[kVtReg];
 #pragma unroll
-                    for (int q = 1; q < kFinGroups; ++q) yj += gsum[q][lane];
+    for (int i = 0; i < kVtReg; ++i) acc[i] = 0.0;
+
+    for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+        const int64_t j0 = ch * cols;
+        int64_t j;
+        bool active;
+        double yj = 0.0, vj = 0.0;
+        if (narrow) {
+            j = j0 + lane;
+            double s = 0.0;
+            if (j < n) {
+                const double *col = p.ypart + j;
+#pragma unroll 4
+                for (int b = grp; b < p.parts; b += kFinGroups) s += col[(int64_t)b * p.ypart_ld];
+            }
+            gsum[grp][lane] = s;
+            __syncthreads();
+            active = (grp == 0) && (j < n);
+            if (active) {
+                yj = gsum[0][lane];
+#pragma unroll
+                for (int q = 1; q < kFinGroups; ++q) yj += gsum[q][lane];
+            }
+        } else {
+            j = j0 + tid;
+            active = j < n;
+            if (active) {
+                if (!reduce) {
+                    yj = p.xsrc[j];
                 } else if (SRC == SRC_YW) {
                     yj = p.yw[j];
-                } else {
+                } else if (SRC == SRC_PEER) {
                     for (int r = 0; r < p.pv.world; ++r) yj += __ldcg(p.pv.buf[r] + slot_off + j);  // rank order
                 }
+            }
+        }
+        if (active) {
+            const double *Vj = p.V + j * p.ldv;
+            if (reduce) {
                 double corr = 0.0;  // (V (S w))_j: the 2nd / 4th terms of Eq. 2 in factored form
-                for (int i = 0; i < l; ++i) corr += p.V[(int64_t)j * p.ldv + i] * g[i];
+                for (int i = 0; i < l; ++i) corr += Vj[i] * g[i];
                 yj -= corr;
                 if (mode == FIN_ITERATE) vj = ycur[j] / ny;
-            } else {
-                yj = p.xsrc[j];
             }
             ynew[j] = yj;
+            a_yy += yj * yj;
+            a_vy += vj * yj;
+#pragma unroll
+            for (int i = 0; i < kVtReg; ++i)
+                if (i < l) acc[i] += Vj[i] * yj;
         }
-        ys[lane] = yj;
-        const double a = warp_sum(yj * yj), b = warp_sum(vj * yj);
-        if (lane == 0 && mode != FIN_APPLY) {
-            double *out = p.part + (int64_t)blockIdx.x * p.part_ld;
-            out[0] = a;
-            out[1] = b;
+        if (lx > 0) {  // components >= 16: shared tile of this chunk's y, coalesced over i
+            if (narrow) {
+                if (grp == 0) ys[lane] = active ? yj : 0.0;
+            } else {
+                ys[tid] = active ? yj : 0.0;
+            }
+            __syncthreads();
+            const int jn = (int)((n - j0) < cols ? (n - j0) : cols);
+            for (int i = kVtReg + tid; i < l; i += kFinThreads) {
+                double s = 0.0;
+                for (int jj = 0; jj < jn; ++jj) s += p.V[(j0 + jj) * p.ldv + i] * ys[jj];
+                vtx[i - kVtReg] += s;
+            }
+        }
+        __syncthreads();
+    }
+    // ---- block partials: { sum y^2, sum v y, (V^T y)_0..l-1 } (warp shuffles, then warps in order)
+    const int lr = l < kVtReg ? l : kVtReg;
+    {
+        double q = warp_sum(a_yy);
+        if (lane == 0) wred[grp][0] = q;
+        q = warp_sum(a_vy);
+        if (lane == 0) wred[grp][1] = q;
+        for (int i = 0; i < lr; ++i) {
+            q = warp_sum(acc[i]);
+            if (lane == 0) wred[grp][2 + i] = q;
         }
     }
     __syncthreads();
-    if (mode != FIN_APPLY) {
-        double *out = p.part + (int64_t)blockIdx.x * p.part_ld;
-        const int jn = (n - j0) < kFinCols ? (n - j0) : kFinCols;
-        for (int i = tid; i < l; i += kFinThreads) {  // (V^T y)_i over this block's 32 rows of V
-            double s = 0.0;
-            for (int jj = 0; jj < jn; ++jj) s += p.V[(int64_t)(j0 + jj) * p.ldv + i] * ys[jj];
-            out[2 + i] = s;
-        }
+    double *out = p.part + (int64_t)blockIdx.x * p.part_ld;
+    if (tid < 2 + lr) {
+        double s = 0.0;
+        for (int w = 0; w < kFinThreads / 32; ++w) s += wred[w][tid];
+        out[tid] = s;
     }
+    for (int i = tid; i < lx; i += kFinThreads) out[2 + kVtReg + i] = vtx[i];
     // ---- the last block to arrive takes the scalar decisions (fixed-order sums: deterministic)
     __threadfence();
     __syncthreads();

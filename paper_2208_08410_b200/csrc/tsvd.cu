@@ -22,6 +22,7 @@
 #include "../../include/tsvd.h"
 #include "fin_kernels.cuh"
 #include "gram_kernels.cuh"
+#include "sparse_kernels.cuh"
 
 using namespace tsvd;
 
@@ -111,6 +112,13 @@ struct tsvd_s {
     cudaStream_t copy_stream = nullptr;
     int64_t streamed_bytes = 0, streamed_batches = 0;
     double stream_pass_ms = 0.0;
+    // sparse CSR slab + its CSC (built once on the device)
+    bool sparse = false, csr_owned = false;
+    int64_t nnz_g = 0;
+    int64_t *row_ptr_d = nullptr, *col_ptr_d = nullptr;
+    int32_t *col_d = nullptr, *row_idx_d = nullptr;
+    float *val_d = nullptr, *cval_d = nullptr;
+    double csc_build_ms = 0.0;
     // factors (device)
     float *U32 = nullptr;   // m_g x kpad
     double *V64 = nullptr;  // n x k
@@ -174,11 +182,30 @@ struct tsvd_s {
 
 static thread_local std::string g_err;
 
-static int fin_src(tsvd_t h) { return h->coll == COLL_NONE ? SRC_PARTS : (h->coll == COLL_PEER ? SRC_PEER : SRC_YW); }
+static int fin_src(tsvd_t h) {
+    if (h->sparse) return SRC_YW;  // N3 writes y straight into yw (then NCCL if world > 1)
+    return h->coll == COLL_NONE ? SRC_PARTS : (h->coll == COLL_PEER ? SRC_PEER : SRC_YW);
+}
+
+static tsvd_status set_fin_attrs(tsvd_t h) {
+    const int fin_dyn = (2 * h->k + 2 + std::max(0, h->k - kVtReg) + kFinThreads) * (int)sizeof(double);
+    CK(cudaFuncSetAttribute(fin_iter<SRC_PARTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_dyn));
+    CK(cudaFuncSetAttribute(fin_iter<SRC_YW>, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_dyn));
+    CK(cudaFuncSetAttribute(fin_iter<SRC_PEER>, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_dyn));
+    return TSVD_OK;
+}
 
 // ------------------------------------------------------------------------------------ planning
 static tsvd_status plan(tsvd_t h) {
     const int64_t n = h->n;
+    if (h->sparse) {  // N2/N3: persistent grid of 256-thread blocks, warp per row / column
+        const int dyn = kSpWarps * std::max(h->k, 1) * (int)sizeof(double);
+        if (dyn > 200 * 1024) return h->fail(TSVD_ERR_UNSUPPORTED, "sparse path supports k <= 3200");
+        CK(cudaFuncSetAttribute(csr_spmv<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+        h->grid = h->sms * 8;
+        h->T = kSpThreads;
+        return set_fin_attrs(h);
+    }
     int T = 32;
     while ((int64_t)4 * T * 8 < n && T < kMaxThreadsPerCta) T *= 2;
     if ((int64_t)4 * T * 8 < n)
@@ -205,10 +232,7 @@ static tsvd_status plan(tsvd_t h) {
     h->gv_ex = pick_gv<true>(T, NV);
     CK(cudaFuncSetAttribute(h->gv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem));
     CK(cudaFuncSetAttribute(h->gv_ex, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem));
-    const int fin_dyn = (2 * h->k + 2) * (int)sizeof(double);
-    CK(cudaFuncSetAttribute(fin_iter<SRC_PARTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_dyn));
-    CK(cudaFuncSetAttribute(fin_iter<SRC_YW>, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_dyn));
-    CK(cudaFuncSetAttribute(fin_iter<SRC_PEER>, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_dyn));
+    TRY(set_fin_attrs(h));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->gv, T, h->smem));
     if (occ < 1) return h->fail(TSVD_ERR_UNSUPPORTED, "fused kernel does not fit on an SM (T=%d smem=%zu)", T, h->smem);
@@ -241,7 +265,7 @@ static tsvd_status ensure_alloc(tsvd_t h) {
     h->ystride = round_up(n, 32);
     h->wofs = round_up(n, 32);
     h->ypart_ld = round_up(n, 4);
-    h->fin_blocks = (int)((n + kFinCols - 1) / kFinCols);
+    h->fin_blocks = (int)std::min<int64_t>((n + kFinCols - 1) / kFinCols, (int64_t)h->sms * 8);
     h->part_ld = 2 + h->kpad;
     auto dm = [&](void **p, size_t bytes) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(bytes, 16)); };
     cudaError_t e = cudaSuccess;
@@ -252,7 +276,7 @@ static tsvd_status ensure_alloc(tsvd_t h) {
     if (!e) e = dm((void **)&h->yw, (size_t)(h->wofs + h->kpad) * sizeof(double));
     if (!e) e = dm((void **)&h->V0d, (size_t)h->k * n * sizeof(double));
     if (!e) e = dm((void **)&h->c64, (size_t)h->kpad * sizeof(double));
-    if (!e) e = dm((void **)&h->ypart, (size_t)h->grid * h->ypart_ld * sizeof(double));
+    if (!e && !h->sparse) e = dm((void **)&h->ypart, (size_t)h->grid * h->ypart_ld * sizeof(double));
     if (!e) e = dm((void **)&h->wpart, (size_t)h->grid * h->kpad * sizeof(double));
     if (!e) e = dm((void **)&h->part, (size_t)h->fin_blocks * h->part_ld * sizeof(double));
     if (!e) e = dm((void **)&h->u64, (size_t)mg * sizeof(double));
@@ -337,6 +361,7 @@ static void free_ring(tsvd_t h) {
 // run (H2D copy, counted in e2e timing).  Degree 0: the whole slab.  Degree 1: rows [0, m_res)
 // resident, rows [m_res, m_g) streamed each pass through the ring (launch_pass).
 static tsvd_status stage_A(tsvd_t h) {
+    if (h->sparse) return TSVD_OK;  // CSR/CSC staged (and validated) by tsvd_set_csr
     if (h->mem == TSVD_MEM_DEVICE) {
         h->streaming = false;
         h->m_res = h->m_g;
@@ -456,7 +481,49 @@ static GvParams gv_params(tsvd_t h, int l, bool extract) {
 // launch over the resident prefix, then row batches copied host->device on the copy stream into a
 // q_s-slot ring (slot reuse gated by events) and consumed by N1 launches that accumulate into the
 // same per-CTA partials, so the H2D of batch b+1.. overlaps the kernel on batch b.
+static SpParams sp_params(tsvd_t h, int l) {
+    SpParams p{};
+    p.row_ptr = h->row_ptr_d;
+    p.col = h->col_d;
+    p.val = h->val_d;
+    p.rows = h->m_g;
+    p.col_ptr = h->col_ptr_d;
+    p.row_idx = h->row_idx_d;
+    p.cval = h->cval_d;
+    p.n = h->n;
+    p.U = h->U32;
+    p.ldu = h->kpad;
+    p.l = l;
+    p.c = h->c64;
+    p.ybuf = h->ybuf;
+    p.ystride = h->ystride;
+    p.st = h->st;
+    p.t = h->u64;
+    p.wpart = h->wpart;
+    p.wpart_ld = h->kpad;
+    p.sq_part = h->sq_part;
+    p.yw = h->yw;
+    p.wofs = h->wofs;
+    p.parts = h->grid;
+    return p;
+}
+
+// Sparse pass: N2 (rows) then N3 (columns) for an iteration; N2 alone for the extraction.
+static tsvd_status launch_sparse(tsvd_t h, cudaStream_t s, int l, bool extract) {
+    const SpParams p = sp_params(h, l);
+    if (extract) {
+        csr_spmv<true><<<h->grid, kSpThreads, 0, s>>>(p);
+    } else {
+        csr_spmv<false><<<h->grid, kSpThreads, (size_t)kSpWarps * std::max(l, 1) * sizeof(double), s>>>(p);
+        CK(cudaGetLastError());
+        csc_spmvT<<<h->grid, kSpThreads, 0, s>>>(p);
+    }
+    CK(cudaGetLastError());
+    return TSVD_OK;
+}
+
 static tsvd_status launch_gv(tsvd_t h, cudaStream_t s, int l, bool extract) {
+    if (h->sparse) return launch_sparse(h, s, l, extract);
     GvFn fn = extract ? h->gv_ex : h->gv;
     GvParams p = gv_params(h, l, extract);
     if (!h->streaming || h->m_res > 0) {
@@ -522,7 +589,7 @@ static FinParams fin_params(tsvd_t h, int mode, int l, const double *xsrc, unsig
 }
 
 static tsvd_status launch_fin(tsvd_t h, cudaStream_t s, const FinParams &p, int src) {
-    const size_t dyn = (size_t)(2 * p.l + 2) * sizeof(double);
+    const size_t dyn = (size_t)(2 * p.l + 2 + std::max(0, p.l - kVtReg) + kFinThreads) * sizeof(double);
     switch (src) {
     case SRC_PARTS: fin_iter<SRC_PARTS><<<h->fin_blocks, kFinThreads, dyn, s>>>(p); break;
     case SRC_YW: fin_iter<SRC_YW><<<h->fin_blocks, kFinThreads, dyn, s>>>(p); break;
@@ -550,6 +617,10 @@ static PubParams pub_params(tsvd_t h, int mode, int l) {
 
 // The cross-rank part of an iteration before fin_iter: nothing / publish / local sum + NCCL.
 static tsvd_status launch_exchange(tsvd_t h, cudaStream_t s, int l) {
+    if (h->sparse) {  // N3 already wrote [y_g | w_g]; the length-n sum is bandwidth-bound: NCCL
+        if (h->world > 1) NK(ncclAllReduce(h->yw, h->yw, (size_t)(h->wofs + h->kpad), ncclDouble, ncclSum, h->comm, s));
+        return TSVD_OK;
+    }
     if (h->coll == COLL_PEER) {
         publish<<<h->fin_blocks, kFinThreads, 0, s>>>(pub_params(h, 0, l));
         CK(cudaGetLastError());
@@ -902,8 +973,9 @@ tsvd_status tsvd_set_dense(tsvd_t h, const float *A, int64_t ld, int64_t row_beg
     if (mem != TSVD_MEM_DEVICE && mem != TSVD_MEM_HOST_PINNED && mem != TSVD_MEM_HOST_PAGEABLE)
         return h->fail(TSVD_ERR_ARG, "bad mem kind");
     CK(cudaSetDevice(h->dev));
-    if (h->allocated && (row_end - row_begin) != h->m_g)
-        return h->fail(TSVD_ERR_STATE, "row slab size cannot change after the first run");
+    if (h->allocated && ((row_end - row_begin) != h->m_g || h->sparse))
+        return h->fail(TSVD_ERR_STATE, "the input kind / slab size cannot change after the first run");
+    h->sparse = false;
     h->row_begin = row_begin;
     h->row_end = row_end;
     h->m_g = row_end - row_begin;
@@ -936,10 +1008,108 @@ tsvd_status tsvd_set_dense(tsvd_t h, const float *A, int64_t ld, int64_t row_beg
     return TSVD_OK;
 }
 
-tsvd_status tsvd_set_csr(tsvd_t h, const int64_t *, const int32_t *, const float *, int64_t, int64_t, int64_t,
-                         tsvd_mem) {
+static void free_sparse(tsvd_t h) {
+    if (h->csr_owned) {
+        cudaFree(h->row_ptr_d);
+        cudaFree(h->col_d);
+        cudaFree(h->val_d);
+    }
+    cudaFree(h->col_ptr_d);
+    cudaFree(h->row_idx_d);
+    cudaFree(h->cval_d);
+    h->row_ptr_d = h->col_ptr_d = nullptr;
+    h->col_d = h->row_idx_d = nullptr;
+    h->val_d = h->cval_d = nullptr;
+    h->csr_owned = false;
+}
+
+tsvd_status tsvd_set_csr(tsvd_t h, const int64_t *row_ptr, const int32_t *col_idx, const float *val, int64_t nnz,
+                         int64_t row_begin, int64_t row_end, tsvd_mem mem) {
     if (!h) return TSVD_ERR_ARG;
-    return h->fail(TSVD_ERR_UNSUPPORTED, "sparse CSR path is not in this version");
+    if (!row_ptr || nnz < 0 || (nnz > 0 && (!col_idx || !val))) return h->fail(TSVD_ERR_ARG, "NULL CSR array");
+    if (row_begin < 0 || row_end > h->m || row_end <= row_begin)
+        return h->fail(TSVD_ERR_SHAPE, "row range [%lld, %lld) outside [0, %lld)", (long long)row_begin,
+                       (long long)row_end, (long long)h->m);
+    if (h->n > INT32_MAX || (row_end - row_begin) > INT32_MAX)
+        return h->fail(TSVD_ERR_UNSUPPORTED, "int32 column / local row indices");
+    if (mem != TSVD_MEM_DEVICE && mem != TSVD_MEM_HOST_PINNED && mem != TSVD_MEM_HOST_PAGEABLE)
+        return h->fail(TSVD_ERR_ARG, "bad mem kind");
+    if (h->allocated && ((row_end - row_begin) != h->m_g || !h->sparse))
+        return h->fail(TSVD_ERR_STATE, "the input kind / slab size cannot change after the first run");
+    CK(cudaSetDevice(h->dev));
+    const int64_t mg = row_end - row_begin, n = h->n;
+    if (mem != TSVD_MEM_DEVICE && (row_ptr[0] != 0 || row_ptr[mg] != nnz))
+        return h->fail(TSVD_ERR_ARG, "row_ptr[0] must be 0 and row_ptr[rows] == nnz");
+    free_sparse(h);
+    h->sparse = true;
+    h->row_begin = row_begin;
+    h->row_end = row_end;
+    h->m_g = mg;
+    h->nnz_g = nnz;
+    h->have_A = true;
+    h->graph_l0 = -1;
+    h->streaming = false;
+    h->m_res = mg;
+    if (h->world > 1) h->coll = COLL_NCCL;
+    auto t0 = std::chrono::steady_clock::now();
+    if (mem == TSVD_MEM_DEVICE) {
+        h->row_ptr_d = const_cast<int64_t *>(row_ptr);
+        h->col_d = const_cast<int32_t *>(col_idx);
+        h->val_d = const_cast<float *>(val);
+    } else {
+        h->csr_owned = true;
+        CK(cudaMalloc((void **)&h->row_ptr_d, (size_t)(mg + 1) * sizeof(int64_t)));
+        CK(cudaMalloc((void **)&h->col_d, std::max<size_t>((size_t)nnz * sizeof(int32_t), 16)));
+        CK(cudaMalloc((void **)&h->val_d, std::max<size_t>((size_t)nnz * sizeof(float), 16)));
+        CK(cudaMemcpyAsync(h->row_ptr_d, row_ptr, (size_t)(mg + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
+        if (nnz) {
+            CK(cudaMemcpyAsync(h->col_d, col_idx, (size_t)nnz * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+            CK(cudaMemcpyAsync(h->val_d, val, (size_t)nnz * sizeof(float), cudaMemcpyHostToDevice, h->stream));
+        }
+    }
+    // validate the CSR contract on the device (sorted unique columns in range)
+    unsigned long long *bad = nullptr, bad_h = 0;
+    CK(cudaMalloc((void **)&bad, sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(bad, 0, sizeof(unsigned long long), h->stream));
+    csr_check<<<h->sms * 8, 256, 0, h->stream>>>(h->row_ptr_d, h->col_d, mg, n, bad);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&bad_h, bad, sizeof(bad_h), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(bad);
+    if (bad_h) {
+        free_sparse(h);
+        h->have_A = false;
+        return h->fail(TSVD_ERR_ARG, "CSR has %llu entries with a column out of range or not strictly increasing",
+                       bad_h);
+    }
+    // N4: CSC of the slab (histogram, scan, scatter, per-column sort)
+    unsigned *cnt = nullptr;
+    int64_t *bsum = nullptr;
+    const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
+    CK(cudaMalloc((void **)&h->col_ptr_d, (size_t)(n + 1) * sizeof(int64_t)));
+    CK(cudaMalloc((void **)&h->row_idx_d, std::max<size_t>((size_t)nnz * sizeof(int32_t), 16)));
+    CK(cudaMalloc((void **)&h->cval_d, std::max<size_t>((size_t)nnz * sizeof(float), 16)));
+    CK(cudaMalloc((void **)&cnt, (size_t)n * sizeof(unsigned)));
+    CK(cudaMalloc((void **)&bsum, (size_t)ntiles * sizeof(int64_t)));
+    CK(cudaMemsetAsync(cnt, 0, (size_t)n * sizeof(unsigned), h->stream));
+    const int blocks = h->sms * 8;
+    if (nnz) csc_count<<<blocks, 256, 0, h->stream>>>(h->col_d, nnz, cnt);
+    scan_tiles<<<(int)ntiles, kScanThreads, 0, h->stream>>>(cnt, n, h->col_ptr_d, bsum);
+    scan_totals<<<1, kScanThreads, 0, h->stream>>>(bsum, ntiles, h->col_ptr_d + n);
+    scan_add<<<blocks, 256, 0, h->stream>>>(h->col_ptr_d, n, bsum);
+    CK(cudaGetLastError());
+    CK(cudaMemsetAsync(cnt, 0, (size_t)n * sizeof(unsigned), h->stream));
+    if (nnz) {
+        csc_scatter<<<blocks, 256, 0, h->stream>>>(h->row_ptr_d, h->col_d, h->val_d, mg, h->col_ptr_d, cnt,
+                                                   h->row_idx_d, h->cval_d);
+        csc_sort<<<blocks, 256, 0, h->stream>>>(h->col_ptr_d, n, h->row_idx_d, h->cval_d);
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(cnt);
+    cudaFree(bsum);
+    h->csc_build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return TSVD_OK;
 }
 
 tsvd_status tsvd_set_factors(tsvd_t h, int32_t l, const float *U, const double *S, const double *V) {
@@ -1031,7 +1201,12 @@ tsvd_status tsvd_run(tsvd_t h) {
     CK(cudaStreamSynchronize(h->stream));
     if (h->st_host->status == -6) return h->fail(TSVD_ERR_NCCL, "peer all-reduce timed out (a rank did not arrive)");
     tsvd_status result = TSVD_OK;
-    const int per_iter = h->coll == COLL_NONE ? 2 : 3, per_ext = h->coll == COLL_NONE ? 2 : 3;
+    // our kernels per iteration / extraction (NCCL calls not counted)
+    int64_t per_pass = 1;
+    if (h->streaming) per_pass = (h->m_res > 0 ? 1 : 0) + (h->m_g - h->m_res + h->batch_rows - 1) / h->batch_rows;
+    if (h->sparse) per_pass = 2;
+    const int64_t per_iter = per_pass + (h->coll == COLL_NONE || h->sparse ? 1 : 2);
+    const int64_t per_ext = (h->sparse ? 1 : per_pass) + (h->coll == COLL_NONE ? 1 : 2);
     for (int l = l0; l < h->k; ++l) {
         const CompStat &cs = h->stats_host[l];
         h->launches += 1 + per_iter * (int64_t)cs.it + per_ext;
@@ -1110,6 +1285,9 @@ tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
              h->streaming ? "true" : "false", (long long)h->m_res, (long long)h->batch_rows, h->qdepth,
              (long long)h->streamed_bytes, (long long)h->streamed_batches);
     s += tmp;
+    snprintf(tmp, sizeof tmp, "\"sparse\": {\"enabled\": %s, \"nnz\": %lld, \"csc_build_ms\": %.3f}, ",
+             h->sparse ? "true" : "false", (long long)h->nnz_g, h->csc_build_ms);
+    s += tmp;
     std::string ge = h->graph_error + (h->peer_error.empty() ? "" : " | " + h->peer_error);
     for (char &c : ge)
         if (c == '"' || c == '\\') c = '\'';
@@ -1166,6 +1344,7 @@ void tsvd_destroy(tsvd_t h) {
     drop_graph(h);
     if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
     free_ring(h);
+    free_sparse(h);
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
     if (h->host_registered) cudaHostUnregister((void *)h->A_user);
     for (int r = 0; r < kMaxRanks; ++r)

@@ -213,6 +213,23 @@ class TSVD:
         self.row_begin, self.row_end = row_begin, row_end
         tsvd_set_dense(self.h, A, ld, row_begin, row_end, mem)
 
+    def set_csr(self, row_ptr, col_idx, val, row_begin=0, row_end=None, mem=None):
+        """This rank's CSR row slab (row_ptr[0] == 0): numpy arrays (host) or torch CUDA tensors."""
+        row_end = self.m if row_end is None else row_end
+        if isinstance(row_ptr, np.ndarray):
+            row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+            col_idx = np.ascontiguousarray(col_idx, dtype=np.int32)
+            val = np.ascontiguousarray(val, dtype=np.float32)
+            mem = MEM_HOST_PAGEABLE if mem is None else mem
+        else:
+            import torch
+            assert row_ptr.dtype == torch.int64 and col_idx.dtype == torch.int32 and val.dtype == torch.float32
+            if mem is None:
+                mem = MEM_DEVICE if row_ptr.is_cuda else MEM_HOST_PAGEABLE
+        self._keep = [row_ptr, col_idx, val]
+        self.row_begin, self.row_end = row_begin, row_end
+        tsvd_set_csr(self.h, row_ptr, col_idx, val, len(col_idx), row_begin, row_end, mem)
+
     def set_factors(self, U, S, V):
         l = 0 if S is None else len(S)
         U = np.ascontiguousarray(U, dtype=np.float32) if l else None

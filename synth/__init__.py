@@ -100,15 +100,66 @@ def v0_normal(n: int, k: int, seed: int = 2) -> np.ndarray:
     return rng.standard_normal((k, n))
 
 
-def random_csr(m: int, n: int, nnz_per_row: int, seed: int = 1):
+def random_csr(m: int, n: int, nnz_per_row: int, seed: int = 1, rows: tuple[int, int] | None = None,
+               chunk: int = 1 << 16):
     """Paper-like sparse CSR ("randomly generated with a density"): exactly
-    ``nnz_per_row`` distinct sorted random columns per row, values U(0,1] fp32.
-    Returns (row_ptr int64[m+1], col_idx int32[nnz], val float32[nnz])."""
-    rng = np.random.Generator(np.random.PCG64(seed))
+    ``nnz_per_row`` distinct sorted random columns per row, values U(0,1] fp32 (nonnegative like
+    P:68).  Rows are drawn in fixed chunks seeded by (seed, chunk index), so any row slab
+    ``rows=(r0, r1)`` has the same content as the full matrix's rows (independent of the GPU count).
+    Returns (row_ptr int64[rows+1] starting at 0, col_idx int32[nnz], val float32[nnz])."""
     d = min(nnz_per_row, n)
-    cols = np.empty((m, d), dtype=np.int64)
-    for i in range(m):
-        cols[i] = np.sort(rng.choice(n, size=d, replace=False))
-    row_ptr = np.arange(0, m * d + 1, d, dtype=np.int64)
-    val = (1.0 - rng.random(m * d, dtype=np.float32)).astype(np.float32)
-    return row_ptr, cols.reshape(-1).astype(np.int32), val
+    g0, g1 = (0, m) if rows is None else rows
+    cols_out = np.empty((g1 - g0, d), dtype=np.int32)
+    vals_out = np.empty((g1 - g0, d), dtype=np.float32)
+    for c in range(g0 // chunk, (g1 + chunk - 1) // chunk):
+        c0, c1 = c * chunk, min(m, (c + 1) * chunk)
+        rng = np.random.Generator(np.random.PCG64([seed, c]))
+        cols = np.sort(rng.integers(0, n, size=(c1 - c0, d), dtype=np.int64), axis=1)
+        while True:  # redraw rows that hit a duplicate column
+            bad = np.nonzero(np.any(np.diff(cols, axis=1) == 0, axis=1))[0] if d > 1 else np.array([], int)
+            if bad.size == 0:
+                break
+            cols[bad] = np.sort(rng.integers(0, n, size=(bad.size, d), dtype=np.int64), axis=1)
+        vals = (1.0 - rng.random((c1 - c0, d), dtype=np.float32)).astype(np.float32)
+        a0, a1 = max(c0, g0), min(c1, g1)
+        cols_out[a0 - g0:a1 - g0] = cols[a0 - c0:a1 - c0]
+        vals_out[a0 - g0:a1 - g0] = vals[a0 - c0:a1 - c0]
+    row_ptr = np.arange(0, (g1 - g0) * d + 1, d, dtype=np.int64)
+    return row_ptr, cols_out.reshape(-1), vals_out.reshape(-1)
+
+
+def block_diag_csr(nblocks: int, b: int, s: np.ndarray, seed: int = 1, noise: float | None = None):
+    """Known-spectrum sparse family: a row/column-permuted block diagonal of
+    ``nblocks`` dense b x b blocks.  Block 0 = Q1 diag(s) Q2^T (len(s) = b); every other block is
+    U(0, a) with a = 0.8 * min(s) / b, so by the Frobenius bound its singular values are below
+    0.8 * min(s): the top len(s) singular values of the whole matrix are exactly s (before fp32
+    rounding).  Returns (row_ptr, col_idx, val, m) with m = n = nblocks * b."""
+    s = np.asarray(s, dtype=np.float64)
+    assert s.shape[0] == b
+    rng = np.random.Generator(np.random.PCG64(seed))
+    m = nblocks * b
+    a = 0.8 * float(s.min()) / b if noise is None else noise
+    q1, _ = np.linalg.qr(rng.standard_normal((b, b)))
+    q2, _ = np.linalg.qr(rng.standard_normal((b, b)))
+    blocks = rng.uniform(0.0, a, size=(nblocks, b, b))
+    blocks[0] = (q1 * s) @ q2.T
+    prow = rng.permutation(m)   # new row index of old row i
+    pcol = rng.permutation(m)   # new column index of old column j
+    cols = np.empty((m, b), dtype=np.int64)
+    vals = np.empty((m, b), dtype=np.float32)
+    for blk in range(nblocks):
+        old_rows = np.arange(blk * b, (blk + 1) * b)
+        new_cols = pcol[blk * b:(blk + 1) * b]
+        order = np.argsort(new_cols)
+        cols[prow[old_rows]] = new_cols[order]
+        vals[prow[old_rows]] = blocks[blk][:, order].astype(np.float32)
+    row_ptr = np.arange(0, m * b + 1, b, dtype=np.int64)
+    return row_ptr, cols.reshape(-1).astype(np.int32), vals.reshape(-1), m
+
+
+def csr_to_dense(row_ptr, col_idx, val, n):
+    m = len(row_ptr) - 1
+    A = np.zeros((m, n), dtype=np.float32)
+    for r in range(m):
+        A[r, col_idx[row_ptr[r]:row_ptr[r + 1]]] = val[row_ptr[r]:row_ptr[r + 1]]
+    return A

@@ -34,16 +34,26 @@ def main():
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    m, n, k, eps = 3001, 517, 5, 1e-8
-    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(64, 5.0, 0.75), seed=11)
+    sparse = os.environ.get("TSVD_SPARSE", "0") == "1"
+    if sparse:
+        m, n, k, eps = 6007, 4001, 4, 1e-8
+        full = synth.random_csr(m, n, 9, seed=21, chunk=512)
+    else:
+        m, n, k, eps = 3001, 517, 5, 1e-8
+        A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(64, 5.0, 0.75), seed=11)
     V0 = synth.v0_normal(n, k, seed=12)
     r0, r1 = slab(world, rank, m)
     obj = [P.tsvd_get_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     t = P.TSVD(m, n, k, eps, rank=rank, world=world, uid=obj[0], device=local)
     t.set_option(P.OPT_COLLECTIVE, int(os.environ.get("TSVD_COLLECTIVE", "0")))
+    if sparse:
+        t.set_option(P.OPT_FIXED_ITERS, 12)  # paper-like spectrum: fixed iterations
     t.set_init(V0)
-    t.set_dense(torch.from_numpy(np.ascontiguousarray(A[r0:r1])).cuda(), r0, r1)
+    if sparse:
+        t.set_csr(*synth.random_csr(m, n, 9, seed=21, rows=(r0, r1), chunk=512), row_begin=r0, row_end=r1)
+    else:
+        t.set_dense(torch.from_numpy(np.ascontiguousarray(A[r0:r1])).cuda(), r0, r1)
     # one Gram-vector product with the all-reduce
     v = synth.v0_normal(n, 1, seed=13)[0]
     y = t.gram_apply(v)
@@ -59,8 +69,12 @@ def main():
         ok &= np.array_equal(o[3], S) and np.array_equal(o[4], V) and np.array_equal(o[7], y)
     if rank == 0:
         import oracle
-        ref = oracle.tsvd(A, k, eps, V0)
-        yref = oracle.gram_apply(A, None, None, None, v)
+        if sparse:
+            ref = oracle.tsvd_csr(*full, n, k, eps, V0, fixed_T=12)
+            yref = oracle.gram_apply_csr(*full, n, None, None, None, v)
+        else:
+            ref = oracle.tsvd(A, k, eps, V0)
+            yref = oracle.gram_apply(A, None, None, None, v)
         Ufull = np.concatenate([o[2] for o in sorted(outs, key=lambda o: o[0])], axis=0)
         err_y = np.linalg.norm(y - yref) / np.linalg.norm(yref)
         rel = np.max(np.abs(S - ref.S) / ref.S)

@@ -27,3 +27,18 @@ def test_row_partition_parity(world, collective):
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "replicated_equal=True" in r.stdout
     assert ("graph-while/peer-nvlink" if collective == 0 else "host/nccl") in r.stdout
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sparse_row_partition_parity(world):
+    """Sparse CSR slabs per rank, length-n partial y summed by ncclAllReduce each iteration."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + world),
+           os.path.join(ROOT, "tests", "mgpu_worker.py")]
+    env = dict(os.environ, TSVD_SPARSE="1")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "replicated_equal=True" in r.stdout and "host/nccl" in r.stdout
