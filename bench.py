@@ -49,6 +49,12 @@ CONFIGS = {
                          "BASELINE configs[2] (256 GiB does not fit the box's 196 GB host RAM)",
                 m=1048576, n=16384, k=2, eps=1e-6, family="hadamard", rank=32, rho=0.8, s0=1.0,
                 stream=True, resident_bytes=0, fixed_T=3),
+    # the paper's per-node sparse matrix: 2^25 x 2^25, density ~1e-6 (32 nnz per row,
+    # 1.07e9 nnz), randomly generated, k=8 (BASELINE configs[3]); its near-degenerate spectrum never
+    # converges, so iterations are fixed as in the paper's OOM runs (100; here 10 per component)
+    "c4n": dict(workload="sparse CSR 33554432x33554432, 32 nnz/row (density 9.5e-7, 1.07e9 nnz), U(0,1] values, "
+                         "k=8, fixed T=10 (P:380 per-node sparse shape; BASELINE configs[3] family)",
+                m=1 << 25, n=1 << 25, k=8, eps=1e-6, family="sparse", d=32, fixed_T=10, rho=0.0, s0=0.0, rank=0),
 }
 METRIC = "seconds to top-k triplets; Gram-vector effective GB/s vs HBM/H2D peak @1/2/4/8"
 
@@ -147,19 +153,28 @@ def ncu_traffic(cfg_name):
 
 
 def cpu_baseline(A, cfg, budget_s=15.0):
-    """The oracle (as it stands) on a bounded sample: component 1 with a fixed iteration count."""
+    """The oracle (as it stands) on a bounded sample: component 1 with a fixed iteration count.
+    A: dense fp32 array, or a CSR tuple for the sparse configs; value in the bench's own unit."""
     import oracle
-    m_s, n = A.shape
+    n = cfg["n"]
     V0 = synth.v0_normal(n, 1, seed=2)
+    if isinstance(A, tuple):
+        m_s = len(A[0]) - 1
+        nnz = len(A[1])
+        run = lambda T: oracle.tsvd_csr(*A, n, 1, cfg["eps"], V0, fixed_T=T)  # noqa: E731
+        per_iter_b, per_ext_b = 16.0 * nnz + 8.0 * (m_s + 1) + 8.0 * (n + 1), 8.0 * nnz + 8.0 * (m_s + 1)
+    else:
+        m_s = A.shape[0]
+        run = lambda T: oracle.tsvd(A, 1, cfg["eps"], V0, fixed_T=T)  # noqa: E731
+        per_iter_b = per_ext_b = 4.0 * m_s * n
     t0 = time.perf_counter()
-    oracle.tsvd(A, 1, cfg["eps"], V0, fixed_T=1)       # 1 Gram pass + 1 extraction pass
+    run(1)                                               # 1 Gram pass + 1 extraction pass
     per_pass = (time.perf_counter() - t0) / 2.0
     T = int(max(1, min(50, budget_s / max(per_pass, 1e-9) - 1)))
     t0 = time.perf_counter()
-    oracle.tsvd(A, 1, cfg["eps"], V0, fixed_T=T)
+    run(T)
     dt = time.perf_counter() - t0
-    passes = T + 1
-    return {"value": 4.0 * m_s * n * passes / dt / 1e9, "unit": "GB/s", "cores": oracle.num_threads(),
+    return {"value": (T * per_iter_b + per_ext_b) / dt / 1e9, "unit": "GB/s", "cores": oracle.num_threads(),
             "kind": "oracle",
             "sample": f"component 1 of {cfg['m']}x{n} (rows {m_s}), fixed T={T} Gram passes + 1 extraction, "
                       f"fp64 plain C, {dt:.2f} s"}
@@ -224,11 +239,15 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     m, n, k, eps = cfg["m"], cfg["n"], cfg["k"], cfg["eps"]
     stream_cfg = cfg.get("stream", False)
+    sparse = cfg["family"] == "sparse"
     r0, r1 = slab(world, rank, m)
     if stream_cfg:  # out-of-memory degree 1: A lives in pinned host memory, streamed every pass
         A_pin = torch.empty((r1 - r0, n), dtype=torch.float32, pin_memory=True)
         A_host = make_A(cfg, r0, r1, out=A_pin.numpy())
         A_dev = A_pin
+    elif sparse:  # paper-like CSR slab; same rows whatever the GPU count
+        A_host = synth.random_csr(m, n, cfg["d"], seed=1, rows=(r0, r1))
+        A_dev = tuple(torch.from_numpy(x).cuda() for x in A_host)
     else:
         A_host = make_A(cfg, r0, r1)
         A_dev = torch.from_numpy(A_host).cuda()
@@ -246,7 +265,10 @@ def main():
         t.set_option(P.OPT_RESIDENT_BYTES, cfg.get("resident_bytes", 0))
     if cfg.get("fixed_T"):
         t.set_option(P.OPT_FIXED_ITERS, cfg["fixed_T"])
-    t.set_dense(A_dev, r0, r1)
+    if sparse:
+        t.set_csr(*A_dev, row_begin=r0, row_end=r1)
+    else:
+        t.set_dense(A_dev, r0, r1)
     if args.loop == "host":
         t.set_option(P.OPT_GRAPH, 0)
     stream = torch.cuda.ExternalStream(t.stream())
@@ -286,9 +308,15 @@ def main():
     kf, iters, dots = t.info()
     U, S, V = t.result()
     passes = int(np.sum(iters[:kf])) + kf
-    bytes_step = 4.0 * m * n * passes
+    if sparse:  # compulsory bytes: CSR + CSC per iteration, CSR per extraction
+        nnz = m * cfg["d"]
+        bytes_step = (int(np.sum(iters[:kf])) * (16.0 * nnz + 8.0 * (m + 1) + 8.0 * (n + 1))
+                      + kf * (8.0 * nnz + 8.0 * (m + 1)))
+    else:
+        bytes_step = 4.0 * m * n * passes
     value = bytes_step * args.steps / (ms / 1e3) / 1e9
-    sig_err = float(np.max(np.abs(S[:kf] - planted(cfg)[:kf]) / planted(cfg)[:kf])) if kf else None
+    sig_err = (float(np.max(np.abs(S[:kf] - planted(cfg)[:kf]) / planted(cfg)[:kf]))
+               if kf and not sparse else None)
 
     # ---- roofline of the dominant kernel (N1): per-launch CUDA events, same workload, one step
     t.set_option(P.OPT_TIMING, 1)
@@ -297,15 +325,22 @@ def main():
     rt = t.report()
     t.set_option(P.OPT_TIMING, 0)
     mg = r1 - r0
-    alg_bytes = sum(int(iters[l]) * (4.0 * mg * n + 4.0 * mg * (l if l % 4 == 0 else (l + 3) // 4 * 4) + 4.0 * n)
-                    for l in range(kf))
+    if sparse:  # N2 + N3: CSR + CSC streams, t written and read once, y_cur read and y written once
+        nnz_g = mg * cfg["d"]
+        alg_bytes = sum(int(iters[l]) * (16.0 * nnz_g + 8.0 * (mg + 1) + 8.0 * (n + 1) + 16.0 * mg + 16.0 * n
+                                         + 4.0 * mg * (l if l % 4 == 0 else (l + 3) // 4 * 4))
+                        for l in range(kf))
+    else:
+        alg_bytes = sum(int(iters[l]) * (4.0 * mg * n + 4.0 * mg * (l if l % 4 == 0 else (l + 3) // 4 * 4) + 4.0 * n)
+                        for l in range(kf))
     n1_ms_per_launch = rt["n1_ms"] / max(rt["n1_launches"], 1)
     per_launch_bytes = alg_bytes / max(rt["n1_launches"], 1)
     achieved = per_launch_bytes / (n1_ms_per_launch / 1e3) / 1e9
     peak, peak_src = measured_peak()
     traffic = ncu_traffic(args.config) if world == 1 else None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": "gv_fused (N1)", "per_launch_ms": n1_ms_per_launch,
+            "traffic": traffic, "kernel": "csr_spmv + csc_spmvT (N2+N3)" if sparse else "gv_fused (N1)",
+            "per_launch_ms": n1_ms_per_launch,
             "alg_bytes_per_launch": per_launch_bytes,
             "share_of_step": rt["n1_ms"] / rt["run_ms"] if rt["run_ms"] else None,
             "peak_source": peak_src, "rank0_rows": mg}
@@ -329,11 +364,20 @@ def main():
                "d2h_bytes_per_step": 4 * mg * k + 8 * k + 8 * n * k + k * 64,
                "note": "streamed config: value is already host-to-host (U, S, V read back after the timed region)"}
     elif not args.no_e2e:
-        A_pin = torch.from_numpy(A_host).pin_memory()
         t2 = P.TSVD(m, n, k, eps, rank=rank, world=world, uid=None, device=local) if world == 1 else None
         te = t2 if t2 is not None else t
         te.set_init(V0)
-        te.set_dense(A_pin, r0, r1)
+        if cfg.get("fixed_T"):
+            te.set_option(P.OPT_FIXED_ITERS, cfg["fixed_T"])
+        if sparse:  # host CSR: every step copies it and rebuilds the CSC on the device
+            def stage():
+                te.set_csr(*A_host, row_begin=r0, row_end=r1)
+        else:
+            A_pin = torch.from_numpy(A_host).pin_memory()
+
+            def stage():
+                te.set_dense(A_pin, r0, r1)
+        stage()
         s2 = torch.cuda.ExternalStream(te.stream())
         te.set_factors(None, None, None)
         te.run()
@@ -343,6 +387,7 @@ def main():
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record(s2)
         for _ in range(args.steps):
+            stage()
             te.set_factors(None, None, None)
             te.run()
             te.result()
@@ -350,7 +395,7 @@ def main():
         f1.synchronize()
         barrier()
         ems = max_over_ranks(f0.elapsed_time(f1))
-        h2d = 4 * mg * n + 8 * k * n
+        h2d = (16 * mg * cfg["d"] + 8 * (mg + 1) if sparse else 4 * mg * n) + 8 * k * n
         d2h = 4 * mg * k + 8 * k + 8 * n * k + k * 64
         e2e = {"value": bytes_step * args.steps / (ems / 1e3) / 1e9, "unit": "GB/s",
                "seconds_to_topk": ems / args.steps / 1e3, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
@@ -368,7 +413,8 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": cfg["workload"], "m": m, "n": n, "k": k, "eps": eps,
-                       "parallelism": f"row-partition x{world}", "l2": "no flush: A (4 GiB) > L2 (126 MB)"},
+                       "parallelism": f"row-partition x{world}",
+                       "l2": "no flush: the matrix read every pass is larger than L2 (126 MB)"},
             "iterations": [int(x) for x in iters[:kf]], "k_found": kf, "status": rc,
             "check": {"sigma_max_rel_err_vs_planted": sig_err},
             "roofline": roof,
