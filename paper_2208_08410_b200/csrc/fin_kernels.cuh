@@ -22,35 +22,11 @@
 
 namespace tsvd {
 
-constexpr int kMaxRanks = 8;
 constexpr int kFinCols = 32;                       // columns per fin block
 constexpr int kFinGroups = kFinThreads / kFinCols;  // partial groups per column
 
 enum FinMode { FIN_ITERATE = 0, FIN_INIT = 1, FIN_LOAD_RAW = 2, FIN_APPLY = 3 };
 enum FinSrc { SRC_PARTS = 0, SRC_YW = 1, SRC_PEER = 2 };
-
-struct PeerView {
-    double *buf[kMaxRanks];       // each rank's symmetric buffer (IPC-mapped); buf[rank] is local
-    unsigned *flags;              // local flag array: flags[q] = last epoch published by rank q
-    unsigned *rflags[kMaxRanks];  // &(rank r's flags)[my rank]
-    int world, rank;
-    int64_t slot_stride;          // doubles per slot; slot (epoch & 1)
-    int64_t wofs, sofs;           // offsets of w and of ||u||^2 inside a slot
-};
-
-__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned *p) {
-    unsigned v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_sys(unsigned *p, unsigned v) {
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 
 // Called by one thread per block: wait until every rank has published epoch `target`.
 // Gives up after 30 s (a dead peer) with status -6 instead of hanging the GPU.

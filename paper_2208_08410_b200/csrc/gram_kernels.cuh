@@ -42,6 +42,56 @@ struct LoopState {
     int32_t pad;
 };
 
+constexpr int kMaxRanks = 8;
+
+// Peer view of the symmetric reduction buffers (multi-GPU, NVLink peer memory).
+struct PeerView {
+    double *buf[kMaxRanks];       // each rank's symmetric buffer (IPC-mapped); buf[rank] is local
+    unsigned *flags;              // local flag array: flags[q] = last epoch published by rank q
+    unsigned *rflags[kMaxRanks];  // &(rank r's flags)[my rank]
+    int world, rank;
+    int64_t slot_stride;          // doubles per slot; slot (epoch & 1)
+    int64_t wofs, sofs;           // offsets of w and of ||u||^2 inside a slot
+};
+
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned *p, unsigned v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Grid-wide barrier for a cooperative launch (all CTAs co-resident): sense reversal on
+// bar[0] = arrivals, bar[1] = generation.  Used once per N1 launch.
+__device__ __forceinline__ void grid_sync(unsigned *bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned gen = ld_acquire_gpu(bar + 1);
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (ld_acquire_gpu(bar + 1) == gen) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 struct CompStat {  // per component, written by ext_finish
     double d;
     double sigma;
@@ -77,8 +127,67 @@ struct GvParams {
     double *sq_part;         // EXTRACT: [gridDim.x] fp64 sum of (A v)_r^2
     int32_t accumulate;      // 1: add into the partials of an earlier launch of the same pass
                              //    (out-of-memory streaming: resident prefix, then ring batches)
-    int32_t pad_;
+    int32_t reduce_mode;     // 0: per-CTA partials only (fin_iter<SRC_PARTS> sums them)
+                             // 1: cooperative launch; after a grid barrier each CTA sums a column
+                             //    slice of the partials into yw = [y | w] (fin_iter<SRC_YW>)
+                             // 2: as 1, into this rank's symmetric slot, then raise the peer flags
+    double *yw;              // reduce_mode 1 target
+    int64_t wofs;
+    unsigned *gbar;          // grid barrier state (2 words)
+    PeerView pv;             // reduce_mode 2
 };
+
+// Column-slice reduction of the per-CTA partials at the end of N1 (reduce_mode 1/2).  CTA c owns
+// columns [c*per, (c+1)*per); warp w sums partials b = w, w+NW, ... of 32 columns and the warp sums
+// are added in warp order (fixed order).  Partials written by other CTAs are read with ld.cg.
+__device__ __forceinline__ double warp_sum(double x);
+
+template <int T>
+__device__ __forceinline__ void reduce_tail(const GvParams &p) {
+    constexpr int NW = T / 32;
+    __shared__ double red2[NW][32];
+    grid_sync(p.gbar);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x;
+    LoopState *st = const_cast<LoopState *>(p.st);
+    const unsigned e = st->epoch;
+    double *yout = p.reduce_mode == 1 ? p.yw : p.pv.buf[p.pv.rank] + (int64_t)(e & 1u) * p.pv.slot_stride;
+    const int64_t wofs = p.reduce_mode == 1 ? p.wofs : p.pv.wofs;
+    const int64_t per = ((p.n + G - 1) / G + 31) / 32 * 32;
+    const int64_t j0 = (int64_t)blockIdx.x * per;
+    const int64_t j1 = (j0 + per) < (int64_t)p.n ? (j0 + per) : (int64_t)p.n;
+    for (int64_t c0 = j0; c0 < j1; c0 += 32) {
+        const int64_t j = c0 + lane;
+        double s = 0.0;
+        if (j < j1)
+            for (int b = warp; b < G; b += NW) s += __ldcg(p.ypart + (int64_t)b * p.ypart_ld + j);
+        red2[warp][lane] = s;
+        __syncthreads();
+        if (warp == 0 && j < j1) {
+            double y = red2[0][lane];
+#pragma unroll
+            for (int q = 1; q < NW; ++q) y += red2[q][lane];
+            yout[j] = y;
+        }
+        __syncthreads();
+    }
+    if (blockIdx.x == 0)
+        for (int i = warp; i < p.l; i += NW) {
+            double w = 0.0;
+            for (int b = lane; b < G; b += 32) w += __ldcg(p.wpart + (int64_t)b * p.wpart_ld + i);
+            w = warp_sum(w);
+            if (lane == 0) yout[wofs + i] = w;
+        }
+    if (p.reduce_mode == 2) {  // publish: last CTA raises flag = epoch + 1 on every rank
+        __threadfence_system();
+        __syncthreads();
+        if (tid == 0 && atomicAdd(&st->pub_counter, 1u) == (unsigned)G - 1) {
+            st->pub_counter = 0;
+            __threadfence_system();
+            for (int r = 0; r < p.pv.world; ++r) st_release_sys(p.pv.rflags[r], e + 1u);
+        }
+    }
+}
 
 // ---------------------------------------------------------------- PTX helpers (mbarrier + TMA)
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -281,6 +390,7 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
             double *wp = p.wpart + (int64_t)blockIdx.x * p.wpart_ld + tid;
             *wp = p.accumulate ? *wp + wacc : wacc;
         }
+        if (p.reduce_mode) reduce_tail<T>(p);
     }
 }
 

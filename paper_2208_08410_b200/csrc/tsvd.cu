@@ -119,6 +119,9 @@ struct tsvd_s {
     int32_t *col_d = nullptr, *row_idx_d = nullptr;
     float *val_d = nullptr, *cval_d = nullptr;
     double csc_build_ms = 0.0;
+    // in-kernel column-slice reduction of the N1 partials (cooperative launch), option 13
+    int fused_opt = 1;
+    unsigned *gbar = nullptr;
     // factors (device)
     float *U32 = nullptr;   // m_g x kpad
     double *V64 = nullptr;  // n x k
@@ -182,9 +185,15 @@ struct tsvd_s {
 
 static thread_local std::string g_err;
 
+// N1 reduces its own partials (grid barrier + column slices) unless the pass is split into
+// several launches (streaming) or the input is sparse (N3 writes y directly).
+static bool fused_reduce(tsvd_t h) { return h->fused_opt && !h->sparse && !h->streaming; }
+
 static int fin_src(tsvd_t h) {
     if (h->sparse) return SRC_YW;  // N3 writes y straight into yw (then NCCL if world > 1)
-    return h->coll == COLL_NONE ? SRC_PARTS : (h->coll == COLL_PEER ? SRC_PEER : SRC_YW);
+    if (h->coll == COLL_PEER) return SRC_PEER;
+    if (h->coll == COLL_NCCL) return SRC_YW;
+    return fused_reduce(h) ? SRC_YW : SRC_PARTS;
 }
 
 static tsvd_status set_fin_attrs(tsvd_t h) {
@@ -284,6 +293,8 @@ static tsvd_status ensure_alloc(tsvd_t h) {
     if (!e) e = dm((void **)&h->sig2, sizeof(double));
     if (!e) e = dm((void **)&h->st, sizeof(LoopState));
     if (!e) e = dm((void **)&h->stats, (size_t)h->k * sizeof(CompStat));
+    if (!e) e = dm((void **)&h->gbar, 2 * sizeof(unsigned));
+    if (!e) e = cudaMemsetAsync(h->gbar, 0, 2 * sizeof(unsigned), h->stream);
     if (!e) e = cudaMallocHost((void **)&h->st_host, sizeof(LoopState));
     if (!e) e = cudaMallocHost((void **)&h->stats_host, (size_t)h->k * sizeof(CompStat));
     if (!e) e = cudaMallocHost((void **)&h->vec_host, (size_t)n * sizeof(double));
@@ -474,6 +485,11 @@ static GvParams gv_params(tsvd_t h, int l, bool extract) {
     p.run_rows = h->run_rows;
     p.u_out = h->u64;
     p.sq_part = h->sq_part;
+    p.reduce_mode = (!extract && fused_reduce(h)) ? (h->coll == COLL_PEER ? 2 : 1) : 0;
+    p.yw = h->yw;
+    p.wofs = h->wofs;
+    p.gbar = h->gbar;
+    p.pv = h->pv;
     return p;
 }
 
@@ -526,6 +542,20 @@ static tsvd_status launch_gv(tsvd_t h, cudaStream_t s, int l, bool extract) {
     if (h->sparse) return launch_sparse(h, s, l, extract);
     GvFn fn = extract ? h->gv_ex : h->gv;
     GvParams p = gv_params(h, l, extract);
+    if (p.reduce_mode) {  // grid barrier inside: cooperative launch guarantees co-residency
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.gridDim = dim3(h->grid);
+        cfg.blockDim = dim3(h->T);
+        cfg.dynamicSmemBytes = h->smem;
+        cfg.stream = s;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, fn, p));
+        return TSVD_OK;
+    }
     if (!h->streaming || h->m_res > 0) {
         fn<<<h->grid, h->T, h->smem, s>>>(p);
         CK(cudaGetLastError());
@@ -619,6 +649,11 @@ static PubParams pub_params(tsvd_t h, int mode, int l) {
 static tsvd_status launch_exchange(tsvd_t h, cudaStream_t s, int l) {
     if (h->sparse) {  // N3 already wrote [y_g | w_g]; the length-n sum is bandwidth-bound: NCCL
         if (h->world > 1) NK(ncclAllReduce(h->yw, h->yw, (size_t)(h->wofs + h->kpad), ncclDouble, ncclSum, h->comm, s));
+        return TSVD_OK;
+    }
+    if (fused_reduce(h)) {  // N1 already summed its partials into yw / the symmetric slot
+        if (h->coll == COLL_NCCL)
+            NK(ncclAllReduce(h->yw, h->yw, (size_t)(h->wofs + h->kpad), ncclDouble, ncclSum, h->comm, s));
         return TSVD_OK;
     }
     if (h->coll == COLL_PEER) {
@@ -932,6 +967,9 @@ tsvd_status tsvd_set_option(tsvd_t h, int32_t key, int64_t value) {
         h->coll_opt = (int)value;
         if (h->world > 1) h->coll = (value == 1 || !h->sym || !h->pv.flags) ? COLL_NCCL : COLL_PEER;
         break;
+    case TSVD_OPT_FUSED_REDUCE:
+        h->fused_opt = value != 0;
+        break;
     case TSVD_OPT_PLACEMENT:
     case TSVD_OPT_RESIDENT_BYTES:
     case TSVD_OPT_BATCH_ROWS:
@@ -1205,7 +1243,7 @@ tsvd_status tsvd_run(tsvd_t h) {
     int64_t per_pass = 1;
     if (h->streaming) per_pass = (h->m_res > 0 ? 1 : 0) + (h->m_g - h->m_res + h->batch_rows - 1) / h->batch_rows;
     if (h->sparse) per_pass = 2;
-    const int64_t per_iter = per_pass + (h->coll == COLL_NONE || h->sparse ? 1 : 2);
+    const int64_t per_iter = per_pass + (h->coll == COLL_NONE || h->sparse || fused_reduce(h) ? 1 : 2);
     const int64_t per_ext = (h->sparse ? 1 : per_pass) + (h->coll == COLL_NONE ? 1 : 2);
     for (int l = l0; l < h->k; ++l) {
         const CompStat &cs = h->stats_host[l];
@@ -1350,7 +1388,7 @@ void tsvd_destroy(tsvd_t h) {
     for (int r = 0; r < kMaxRanks; ++r)
         if (h->peer_map[r]) cudaIpcCloseMemHandle(h->peer_map[r]);
     void *dev_ptrs[] = {h->A_own, h->U32, h->V64, h->S64, h->ybuf, h->yw, h->V0d, h->c64, h->ypart,
-                        h->wpart, h->part, h->u64, h->sq_part, h->sig2, h->st, h->stats, h->sym};
+                        h->wpart, h->part, h->u64, h->sq_part, h->sig2, h->st, h->stats, h->sym, h->gbar};
     for (void *p : dev_ptrs)
         if (p) cudaFree(p);
     if (h->st_host) cudaFreeHost(h->st_host);
