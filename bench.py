@@ -222,6 +222,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--loop", default="graph", choices=["graph", "host"],
                     help="host: host-driven iteration loop (ncu cannot profile kernels inside conditional graphs)")
+    ap.add_argument("--fused-reduce", type=int, default=None, choices=[0, 1],
+                    help="TSVD_OPT_FUSED_REDUCE (default: the library's default)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -271,6 +273,8 @@ def main():
         t.set_dense(A_dev, r0, r1)
     if args.loop == "host":
         t.set_option(P.OPT_GRAPH, 0)
+    if args.fused_reduce is not None:
+        t.set_option(P.OPT_FUSED_REDUCE, args.fused_reduce)
     stream = torch.cuda.ExternalStream(t.stream())
 
     def barrier():
