@@ -135,6 +135,8 @@ struct GvParams {
     int64_t wofs;
     unsigned *gbar;          // grid barrier state (2 words)
     PeerView pv;             // reduce_mode 2
+    unsigned long long *trace;  // debug (TSVD_TRACE): per CTA %globaltimer at entry, first row,
+                                // end of the row loop, exit
 };
 
 // Column-slice reduction of the per-CTA partials at the end of N1 (reduce_mode 1/2).  CTA c owns
@@ -245,6 +247,7 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     constexpr int NW = T / 32;
     const LoopState *st = p.st;
     if (st->stop || (!EXTRACT && st->done)) return;
+    if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 4 + 0] = globaltimer_ns();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (size_t)p.stages * p.stage_bytes);
     double *red = reinterpret_cast<double *>(bars + kMaxStages);  // [2][NW]
@@ -321,6 +324,7 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     for (int i = 0; i < nr; ++i) {
         const int s = i % S;
         mbar_wait(&bars[s], (uint32_t)((i / S) & 1));
+        if (i == 0 && p.trace && tid == 0) p.trace[blockIdx.x * 4 + 1] = globaltimer_ns();
         const unsigned char *slot = smem + (size_t)s * p.stage_bytes;
         const float4 *row = reinterpret_cast<const float4 *>(slot);
 
@@ -382,6 +386,7 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
             }
         }
     }
+    if (p.trace && tid == 0) p.trace[blockIdx.x * 4 + 2] = globaltimer_ns();
     if (EXTRACT) {
         if (tid == 0) p.sq_part[blockIdx.x] = p.accumulate ? p.sq_part[blockIdx.x] + sq : sq;
     } else {
@@ -391,6 +396,10 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
             *wp = p.accumulate ? *wp + wacc : wacc;
         }
         if (p.reduce_mode) reduce_tail<T>(p);
+    }
+    if (p.trace) {
+        __syncthreads();
+        if (tid == 0) p.trace[blockIdx.x * 4 + 3] = globaltimer_ns();
     }
 }
 

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -122,6 +123,10 @@ struct tsvd_s {
     // in-kernel column-slice reduction of the N1 partials (cooperative launch), option 13
     int fused_opt = 1;
     unsigned *gbar = nullptr;
+    // debug: TSVD_TRACE=<file> appends per-CTA N1 timestamps of host-loop iterations
+    unsigned long long *trace_d = nullptr;
+    FILE *trace_f = nullptr;
+    int64_t trace_launch = 0;
     // factors (device)
     float *U32 = nullptr;   // m_g x kpad
     double *V64 = nullptr;  // n x k
@@ -295,6 +300,10 @@ static tsvd_status ensure_alloc(tsvd_t h) {
     if (!e) e = dm((void **)&h->stats, (size_t)h->k * sizeof(CompStat));
     if (!e) e = dm((void **)&h->gbar, 2 * sizeof(unsigned));
     if (!e) e = cudaMemsetAsync(h->gbar, 0, 2 * sizeof(unsigned), h->stream);
+    if (!e && getenv("TSVD_TRACE")) {
+        e = dm((void **)&h->trace_d, (size_t)h->grid * 4 * sizeof(unsigned long long));
+        h->trace_f = fopen(getenv("TSVD_TRACE"), "a");
+    }
     if (!e) e = cudaMallocHost((void **)&h->st_host, sizeof(LoopState));
     if (!e) e = cudaMallocHost((void **)&h->stats_host, (size_t)h->k * sizeof(CompStat));
     if (!e) e = cudaMallocHost((void **)&h->vec_host, (size_t)n * sizeof(double));
@@ -490,6 +499,7 @@ static GvParams gv_params(tsvd_t h, int l, bool extract) {
     p.wofs = h->wofs;
     p.gbar = h->gbar;
     p.pv = h->pv;
+    p.trace = extract ? nullptr : h->trace_d;
     return p;
 }
 
@@ -831,6 +841,17 @@ static tsvd_status run_host_loop(tsvd_t h, int l0) {
                 CK(cudaEventElapsedTime(&ms, e0, e1));
                 h->n1_ms += ms;
                 h->n1_launches += 1;
+            }
+            if (h->trace_d && h->trace_f) {  // debug: per-CTA timestamps of this N1 launch
+                std::vector<unsigned long long> tr((size_t)h->grid * 4);
+                CK(cudaMemcpy(tr.data(), h->trace_d, tr.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+                unsigned long long t0 = tr[0];
+                for (int b = 0; b < h->grid; ++b) t0 = std::min(t0, tr[b * 4]);
+                for (int b = 0; b < h->grid; ++b)
+                    fprintf(h->trace_f, "%d,%lld,%d,%lld,%lld,%lld,%lld\n", h->rank, (long long)h->trace_launch, b,
+                            (long long)(tr[b * 4] - t0), (long long)(tr[b * 4 + 1] - t0),
+                            (long long)(tr[b * 4 + 2] - t0), (long long)(tr[b * 4 + 3] - t0));
+                h->trace_launch++;
             }
             if (h->st_host->done || h->st_host->stop) break;
         }
@@ -1388,7 +1409,9 @@ void tsvd_destroy(tsvd_t h) {
     for (int r = 0; r < kMaxRanks; ++r)
         if (h->peer_map[r]) cudaIpcCloseMemHandle(h->peer_map[r]);
     void *dev_ptrs[] = {h->A_own, h->U32, h->V64, h->S64, h->ybuf, h->yw, h->V0d, h->c64, h->ypart,
-                        h->wpart, h->part, h->u64, h->sq_part, h->sig2, h->st, h->stats, h->sym, h->gbar};
+                        h->wpart, h->part, h->u64, h->sq_part, h->sig2, h->st, h->stats, h->sym, h->gbar,
+                        h->trace_d};
+    if (h->trace_f) fclose(h->trace_f);
     for (void *p : dev_ptrs)
         if (p) cudaFree(p);
     if (h->st_host) cudaFreeHost(h->st_host);
