@@ -80,9 +80,13 @@ typedef enum {
                                     fits; 0 = stream every row)                                       */
     TSVD_OPT_BATCH_ROWS = 11,    /* stream mode: rows per H2D batch (0 = ~256 MiB batches)            */
     TSVD_OPT_QUEUE_DEPTH = 12,   /* stream mode: device ring slots q_s, 2..8, def. 3   */
-    TSVD_OPT_FUSED_REDUCE = 13   /* 1 (default): the fused kernel sums its per-CTA partials itself
-                                    (cooperative launch, grid barrier, column slices) and, multi-GPU,
-                                    publishes them to the peers; 0: separate reduction kernels       */
+    TSVD_OPT_FUSED_REDUCE = 13,  /* 1: the fused kernel sums its per-CTA partials itself (cooperative
+                                    launch, grid barrier, column slices) and, multi-GPU, publishes them
+                                    to the peers; 0 (default): separate reduction kernel (measured
+                                    faster)                                                */
+    TSVD_OPT_DETERMINISTIC = 14  /* 0 (default): N1 CTAs claim row chunks dynamically (no tail behind
+                                    the slowest SM; sums are reproducible only to rounding);
+                                    1: static contiguous row split, bitwise-reproducible results      */
 } tsvd_option;
 
 /*

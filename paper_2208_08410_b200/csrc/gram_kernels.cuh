@@ -137,6 +137,9 @@ struct GvParams {
     PeerView pv;             // reduce_mode 2
     unsigned long long *trace;  // debug (TSVD_TRACE): per CTA %globaltimer at entry, first row,
                                 // end of the row loop, exit
+    int32_t dynamic;            // 1: CTAs claim chunk_rows rows at a time from work[0]
+    int32_t chunk_rows;
+    unsigned long long *work;   // [0] next unclaimed row, [1] CTAs finished (reset by the last)
 };
 
 // Column-slice reduction of the per-CTA partials at the end of N1 (reduce_mode 1/2).  CTA c owns
@@ -211,6 +214,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void fence_barrier_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -252,42 +258,67 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (size_t)p.stages * p.stage_bytes);
     double *red = reinterpret_cast<double *>(bars + kMaxStages);  // [2][NW]
 
-    const int64_t r0 = p.rows * blockIdx.x / gridDim.x;
-    const int64_t r1 = p.rows * (blockIdx.x + 1) / gridDim.x;
-    const int nr = (int)(r1 - r0);
+    __shared__ int64_t slot_row[kMaxStages];  // row held by each ring slot (-1: no more rows)
     const int S = p.stages;
     const int l = EXTRACT ? 0 : p.l;
     const uint32_t tx_bytes = (uint32_t)(p.row_bytes + (EXTRACT ? 0 : p.u_bytes));
+
+    // Row schedule (producer thread only).  Dynamic: claim chunks of chunk_rows rows from a
+    // per-launch counter, so SMs that get less HBM bandwidth simply take fewer rows (the static
+    // split left a ~50 us tail behind the slowest SM).  Static: contiguous range per CTA
+    // (bitwise-reproducible sums for a fixed grid).
+    int64_t cur = p.dynamic ? 0 : p.rows * blockIdx.x / gridDim.x;
+    int64_t cur_end = p.dynamic ? 0 : p.rows * (blockIdx.x + 1) / gridDim.x;
+    auto next_row = [&]() -> int64_t {
+        if (cur >= cur_end) {
+            if (!p.dynamic) return -1;
+            const unsigned long long base = atomicAdd(p.work, (unsigned long long)p.chunk_rows);
+            if (base >= (unsigned long long)p.rows) return -1;
+            cur = (int64_t)base;
+            cur_end = cur + p.chunk_rows < p.rows ? cur + p.chunk_rows : p.rows;
+        }
+        return cur++;
+    };
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_barrier_init();
     }
     __syncthreads();
-    auto issue = [&](int slot, int64_t row) {
-        unsigned char *dst = smem + (size_t)slot * p.stage_bytes;
-        mbar_arrive_expect_tx(&bars[slot], tx_bytes);
-        tma_load_1d(dst, p.A + row * p.ld, (uint32_t)p.row_bytes, &bars[slot]);
-        if (!EXTRACT && p.u_bytes > 0)
-            tma_load_1d(dst + p.row_bytes, p.U + row * p.ldu, (uint32_t)p.u_bytes, &bars[slot]);
+    auto feed = [&](int slot) {  // producer: next row into `slot`, or close the slot
+        const int64_t row = next_row();
+        slot_row[slot] = row;
+        if (row >= 0) {
+            unsigned char *dst = smem + (size_t)slot * p.stage_bytes;
+            mbar_arrive_expect_tx(&bars[slot], tx_bytes);
+            tma_load_1d(dst, p.A + row * p.ld, (uint32_t)p.row_bytes, &bars[slot]);
+            if (!EXTRACT && p.u_bytes > 0)
+                tma_load_1d(dst + p.row_bytes, p.U + row * p.ldu, (uint32_t)p.u_bytes, &bars[slot]);
+        } else {
+            mbar_arrive(&bars[slot]);
+        }
     };
-    if (tid == 0) {
-        const int pre = nr < S ? nr : S;
-        for (int s = 0; s < pre; ++s) issue(s, r0 + s);
-    }
+    if (tid == 0)
+        for (int s = 0; s < S; ++s) feed(s);
 
     // this thread's slice of v = y_cur / ||y_cur|| (fp64 master -> fp32), while the ring fills
     float4 vr[NV];
     {
-        const double ny = st->ny;
+        const double inv = 1.0 / st->ny;
         const double *ycur = p.ybuf + (int64_t)(st->it & 1) * p.ystride;
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
             const int j = 4 * (k * T + tid);
-            vr[k].x = j + 0 < p.n ? (float)(ycur[j + 0] / ny) : 0.f;
-            vr[k].y = j + 1 < p.n ? (float)(ycur[j + 1] / ny) : 0.f;
-            vr[k].z = j + 2 < p.n ? (float)(ycur[j + 2] / ny) : 0.f;
-            vr[k].w = j + 3 < p.n ? (float)(ycur[j + 3] / ny) : 0.f;
+            if (j + 3 < p.n) {
+                const double2 lo = *reinterpret_cast<const double2 *>(ycur + j);
+                const double2 hi = *reinterpret_cast<const double2 *>(ycur + j + 2);
+                vr[k] = make_float4((float)(lo.x * inv), (float)(lo.y * inv), (float)(hi.x * inv), (float)(hi.y * inv));
+            } else {
+                vr[k].x = j + 0 < p.n ? (float)(ycur[j + 0] * inv) : 0.f;
+                vr[k].y = j + 1 < p.n ? (float)(ycur[j + 1] * inv) : 0.f;
+                vr[k].z = j + 2 < p.n ? (float)(ycur[j + 2] * inv) : 0.f;
+                vr[k].w = 0.f;
+            }
         }
     }
     double cval = 0.0;
@@ -321,10 +352,12 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     };
 
     int run = 0;
-    for (int i = 0; i < nr; ++i) {
+    for (int i = 0;; ++i) {
         const int s = i % S;
         mbar_wait(&bars[s], (uint32_t)((i / S) & 1));
         if (i == 0 && p.trace && tid == 0) p.trace[blockIdx.x * 4 + 1] = globaltimer_ns();
+        const int64_t grow = slot_row[s];  // same value in every thread: uniform exit
+        if (grow < 0) break;
         const unsigned char *slot = smem + (size_t)s * p.stage_bytes;
         const float4 *row = reinterpret_cast<const float4 *>(slot);
 
@@ -357,9 +390,9 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
         part = warp_sum(part);
         if (lane == 0) red[(i & 1) * NW + warp] = part;
         __syncthreads();  // (a) partial dots visible, (b) every thread is done reading slot s
-        if (tid == 0 && i + S < nr) {
+        if (tid == 0) {
             fence_proxy_async_smem();
-            issue(s, r0 + i + S);
+            feed(s);
         }
         double t = 0.0;
 #pragma unroll
@@ -367,7 +400,7 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
 
         if (EXTRACT) {
             if (tid == 0) {
-                p.u_out[r0 + i] = t;
+                p.u_out[grow] = t;
                 sq += t * t;
             }
         } else {
@@ -380,7 +413,7 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
                 ya[k].w = fmaf(tf, a[k].w, ya[k].w);
             }
             if (tid < l) wacc += t * (double)ur;
-            if (++run == p.run_rows && i + 1 < nr) {
+            if (++run == p.run_rows) {
                 flush();
                 run = 0;
             }
@@ -400,6 +433,14 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     if (p.trace) {
         __syncthreads();
         if (tid == 0) p.trace[blockIdx.x * 4 + 3] = globaltimer_ns();
+    }
+    if (p.dynamic && tid == 0) {  // last CTA out resets the row counter for the next launch
+        __threadfence();
+        if (atomicAdd(p.work + 1, 1ull) == gridDim.x - 1) {
+            p.work[0] = 0;
+            p.work[1] = 0;
+            __threadfence();
+        }
     }
 }
 

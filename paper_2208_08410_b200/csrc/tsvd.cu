@@ -121,8 +121,11 @@ struct tsvd_s {
     float *val_d = nullptr, *cval_d = nullptr;
     double csc_build_ms = 0.0;
     // in-kernel column-slice reduction of the N1 partials (cooperative launch), option 13
-    int fused_opt = 1;
+    int fused_opt = 0;
     unsigned *gbar = nullptr;
+    // dynamic row scheduling in N1 (option 14 DETERMINISTIC = 1 switches to a static split)
+    int dynamic_opt = 1;
+    unsigned long long *work = nullptr;
     // debug: TSVD_TRACE=<file> appends per-CTA N1 timestamps of host-loop iterations
     unsigned long long *trace_d = nullptr;
     FILE *trace_f = nullptr;
@@ -300,9 +303,13 @@ static tsvd_status ensure_alloc(tsvd_t h) {
     if (!e) e = dm((void **)&h->stats, (size_t)h->k * sizeof(CompStat));
     if (!e) e = dm((void **)&h->gbar, 2 * sizeof(unsigned));
     if (!e) e = cudaMemsetAsync(h->gbar, 0, 2 * sizeof(unsigned), h->stream);
+    if (!e) e = dm((void **)&h->work, 2 * sizeof(unsigned long long));
+    if (!e) e = cudaMemsetAsync(h->work, 0, 2 * sizeof(unsigned long long), h->stream);
     if (!e && getenv("TSVD_TRACE")) {
         e = dm((void **)&h->trace_d, (size_t)h->grid * 4 * sizeof(unsigned long long));
-        h->trace_f = fopen(getenv("TSVD_TRACE"), "a");
+        char name[1024];
+        snprintf(name, sizeof name, "%s.rank%d", getenv("TSVD_TRACE"), h->rank);
+        h->trace_f = fopen(name, "a");
     }
     if (!e) e = cudaMallocHost((void **)&h->st_host, sizeof(LoopState));
     if (!e) e = cudaMallocHost((void **)&h->stats_host, (size_t)h->k * sizeof(CompStat));
@@ -500,6 +507,9 @@ static GvParams gv_params(tsvd_t h, int l, bool extract) {
     p.gbar = h->gbar;
     p.pv = h->pv;
     p.trace = extract ? nullptr : h->trace_d;
+    p.dynamic = h->dynamic_opt;
+    p.chunk_rows = (int32_t)std::max<int64_t>(1, (256 << 10) / h->row_bytes);
+    p.work = h->work;
     return p;
 }
 
@@ -991,6 +1001,9 @@ tsvd_status tsvd_set_option(tsvd_t h, int32_t key, int64_t value) {
     case TSVD_OPT_FUSED_REDUCE:
         h->fused_opt = value != 0;
         break;
+    case TSVD_OPT_DETERMINISTIC:
+        h->dynamic_opt = value == 0;
+        break;
     case TSVD_OPT_PLACEMENT:
     case TSVD_OPT_RESIDENT_BYTES:
     case TSVD_OPT_BATCH_ROWS:
@@ -1410,7 +1423,7 @@ void tsvd_destroy(tsvd_t h) {
         if (h->peer_map[r]) cudaIpcCloseMemHandle(h->peer_map[r]);
     void *dev_ptrs[] = {h->A_own, h->U32, h->V64, h->S64, h->ybuf, h->yw, h->V0d, h->c64, h->ypart,
                         h->wpart, h->part, h->u64, h->sq_part, h->sig2, h->st, h->stats, h->sym, h->gbar,
-                        h->trace_d};
+                        h->trace_d, h->work};
     if (h->trace_f) fclose(h->trace_f);
     for (void *p : dev_ptrs)
         if (p) cudaFree(p);

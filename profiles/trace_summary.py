@@ -9,7 +9,10 @@ import numpy as np
 def main(path):
     L = defaultdict(list)
     for line in open(path):
-        r, launch, b, t0, t1, t2, t3 = (int(x) for x in line.strip().split(","))
+        f = line.strip().split(",")
+        if len(f) != 7 or not all(x.lstrip("-").isdigit() for x in f):  # interleaved appends
+            continue
+        r, launch, b, t0, t1, t2, t3 = (int(x) for x in f)
         L[(r, launch)].append((t0, t1, t2, t3))
     rows = []
     for key, v in sorted(L.items()):

@@ -144,9 +144,9 @@ def test_graph_and_host_loops_bitwise_equal():
     m, n, k = 900, 200, 4
     A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(n, 3.0, 0.7), seed=4)
     V0 = synth.v0_normal(n, k, seed=4)
-    a = _gpu_tsvd(A, k, 1e-8, V0, graph=1)
-    b = _gpu_tsvd(A, k, 1e-8, V0, graph=0)
-    c = _gpu_tsvd(A, k, 1e-8, V0, timing=1)
+    a = _gpu_tsvd(A, k, 1e-8, V0, graph=1, deterministic=1)
+    b = _gpu_tsvd(A, k, 1e-8, V0, graph=0, deterministic=1)
+    c = _gpu_tsvd(A, k, 1e-8, V0, timing=1, deterministic=1)
     for x in (b, c):
         np.testing.assert_array_equal(a[1], x[1])
         np.testing.assert_array_equal(a[2], x[2])
@@ -189,8 +189,8 @@ def test_host_input_equals_device_input():
     m, n, k = 600, 100, 3
     A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(n, 4.0, 0.6), seed=2)
     V0 = synth.v0_normal(n, k, seed=3)
-    a = _gpu_tsvd(A, k, 1e-6, V0, device=True)
-    b = _gpu_tsvd(A, k, 1e-6, V0, device=False)
+    a = _gpu_tsvd(A, k, 1e-6, V0, device=True, deterministic=1)
+    b = _gpu_tsvd(A, k, 1e-6, V0, device=False, deterministic=1)
     np.testing.assert_array_equal(a[2], b[2])
     np.testing.assert_array_equal(a[1], b[1])
 
@@ -253,6 +253,7 @@ def test_internal_generator_is_seeded():
     for _ in range(2):
         t = P.TSVD(m, n, k, 1e-8)
         t.set_option(P.OPT_SEED, 42)
+        t.set_option(P.OPT_DETERMINISTIC, 1)
         t.set_dense(torch.from_numpy(A).cuda())
         t.run()
         outs.append(t.result()[1])
