@@ -224,6 +224,8 @@ def main():
                     help="host: host-driven iteration loop (ncu cannot profile kernels inside conditional graphs)")
     ap.add_argument("--fused-reduce", type=int, default=None, choices=[0, 1],
                     help="TSVD_OPT_FUSED_REDUCE (default: the library's default)")
+    ap.add_argument("--deterministic", type=int, default=None, choices=[0, 1],
+                    help="TSVD_OPT_DETERMINISTIC (default: the library's default)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -275,6 +277,8 @@ def main():
         t.set_option(P.OPT_GRAPH, 0)
     if args.fused_reduce is not None:
         t.set_option(P.OPT_FUSED_REDUCE, args.fused_reduce)
+    if args.deterministic is not None:
+        t.set_option(P.OPT_DETERMINISTIC, args.deterministic)
     stream = torch.cuda.ExternalStream(t.stream())
 
     def barrier():
