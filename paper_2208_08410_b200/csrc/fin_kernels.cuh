@@ -163,6 +163,7 @@ struct FinParams {
     int fixed_T, max_iter;
     unsigned long long cond;
     int use_cond;
+    unsigned long long *tl;   // debug timeline (TSVD_TIMELINE)
 };
 
 // FIN_ITERATE : y_new = sum(partials) - V (S w) -> ybuf[(it+1)&1]; stop test; it += 1
@@ -401,6 +402,7 @@ __global__ void __launch_bounds__(kFinThreads) fin_iter(const FinParams p) {
             }
             inv_s = (nyn > 0.0 && isfinite(nyn)) ? nyn : 1.0;
             set_cond(p.cond, p.use_cond, (st->done || st->stop) ? 0u : 1u);
+            if (p.tl) p.tl[2 + 3 * ((p.tl[0] - 1) % 4096) + 2] = globaltimer_ns();  // debug timeline
         }
     }
     __syncthreads();

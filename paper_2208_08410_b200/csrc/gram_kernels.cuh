@@ -140,6 +140,7 @@ struct GvParams {
     int32_t dynamic;            // 1: CTAs claim chunk_rows rows at a time from work[0]
     int32_t chunk_rows;
     unsigned long long *work;   // [0] next unclaimed row, [1] CTAs finished (reset by the last)
+    unsigned long long *tl;     // debug timeline: [0] iterations, [1] exit count, then 3 per iteration
 };
 
 // Column-slice reduction of the per-CTA partials at the end of N1 (reduce_mode 1/2).  CTA c owns
@@ -254,6 +255,10 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     const LoopState *st = p.st;
     if (st->stop || (!EXTRACT && st->done)) return;
     if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 4 + 0] = globaltimer_ns();
+    if (!EXTRACT && p.tl && blockIdx.x == 0 && threadIdx.x == 0) {  // debug timeline (TSVD_TIMELINE)
+        const unsigned long long idx = atomicAdd(p.tl, 1ull) % 4096;
+        p.tl[2 + 3 * idx] = globaltimer_ns();
+    }
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (size_t)p.stages * p.stage_bytes);
     double *red = reinterpret_cast<double *>(bars + kMaxStages);  // [2][NW]
@@ -433,6 +438,13 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     if (p.trace) {
         __syncthreads();
         if (tid == 0) p.trace[blockIdx.x * 4 + 3] = globaltimer_ns();
+    }
+    if (!EXTRACT && p.tl && tid == 0) {
+        __threadfence();
+        if (atomicAdd(p.tl + 1, 1ull) == gridDim.x - 1) {
+            p.tl[1] = 0;
+            p.tl[2 + 3 * ((p.tl[0] - 1) % 4096) + 1] = globaltimer_ns();
+        }
     }
     if (p.dynamic && tid == 0) {  // last CTA out resets the row counter for the next launch
         __threadfence();

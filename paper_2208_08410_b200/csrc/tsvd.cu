@@ -126,6 +126,7 @@ struct tsvd_s {
     // dynamic row scheduling in N1 (option 14 DETERMINISTIC = 1 switches to a static split)
     int dynamic_opt = 1;
     unsigned long long *work = nullptr;
+    unsigned long long *tl_d = nullptr;  // debug: TSVD_TIMELINE=<file> (N1 start/end, fin end per iteration)
     // debug: TSVD_TRACE=<file> appends per-CTA N1 timestamps of host-loop iterations
     unsigned long long *trace_d = nullptr;
     FILE *trace_f = nullptr;
@@ -310,6 +311,10 @@ static tsvd_status ensure_alloc(tsvd_t h) {
         char name[1024];
         snprintf(name, sizeof name, "%s.rank%d", getenv("TSVD_TRACE"), h->rank);
         h->trace_f = fopen(name, "a");
+    }
+    if (!e && getenv("TSVD_TIMELINE")) {
+        e = dm((void **)&h->tl_d, (2 + 3 * 4096) * sizeof(unsigned long long));
+        if (!e) e = cudaMemsetAsync(h->tl_d, 0, (2 + 3 * 4096) * sizeof(unsigned long long), h->stream);
     }
     if (!e) e = cudaMallocHost((void **)&h->st_host, sizeof(LoopState));
     if (!e) e = cudaMallocHost((void **)&h->stats_host, (size_t)h->k * sizeof(CompStat));
@@ -510,6 +515,7 @@ static GvParams gv_params(tsvd_t h, int l, bool extract) {
     p.dynamic = h->dynamic_opt;
     p.chunk_rows = (int32_t)std::max<int64_t>(1, (256 << 10) / h->row_bytes);
     p.work = h->work;
+    p.tl = extract ? nullptr : h->tl_d;
     return p;
 }
 
@@ -635,6 +641,7 @@ static FinParams fin_params(tsvd_t h, int mode, int l, const double *xsrc, unsig
     p.max_iter = h->max_iter;
     p.cond = cond;
     p.use_cond = use_cond;
+    p.tl = h->tl_d;
     return p;
 }
 
@@ -1294,6 +1301,21 @@ tsvd_status tsvd_run(tsvd_t h) {
         h->l_found = l + 1;
         h->k_found = l + 1;
     }
+    if (h->tl_d) {  // debug timeline dump: iteration, N1 start, N1 end, fin end (ns, relative)
+        std::vector<unsigned long long> tl(2 + 3 * 4096);
+        CK(cudaMemcpy(tl.data(), h->tl_d, tl.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        char name[1024];
+        snprintf(name, sizeof name, "%s.rank%d", getenv("TSVD_TIMELINE"), h->rank);
+        if (FILE *f = fopen(name, "a")) {
+            const int64_t cnt = std::min<int64_t>((int64_t)tl[0], 4096);
+            const unsigned long long base = cnt ? tl[2] : 0;
+            for (int64_t i = 0; i < cnt; ++i)
+                fprintf(f, "%lld,%lld,%lld,%lld\n", (long long)i, (long long)(tl[2 + 3 * i] - base),
+                        (long long)(tl[3 + 3 * i] - base), (long long)(tl[4 + 3 * i] - base));
+            fclose(f);
+        }
+        CK(cudaMemsetAsync(h->tl_d, 0, tl.size() * sizeof(unsigned long long), h->stream));
+    }
     TRY(unstage_A(h));
     h->run_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (result == TSVD_WARN_RANK_EXHAUSTED) h->err = "rank exhausted before k components";
@@ -1423,7 +1445,7 @@ void tsvd_destroy(tsvd_t h) {
         if (h->peer_map[r]) cudaIpcCloseMemHandle(h->peer_map[r]);
     void *dev_ptrs[] = {h->A_own, h->U32, h->V64, h->S64, h->ybuf, h->yw, h->V0d, h->c64, h->ypart,
                         h->wpart, h->part, h->u64, h->sq_part, h->sig2, h->st, h->stats, h->sym, h->gbar,
-                        h->trace_d, h->work};
+                        h->trace_d, h->work, h->tl_d};
     if (h->trace_f) fclose(h->trace_f);
     for (void *p : dev_ptrs)
         if (p) cudaFree(p);
