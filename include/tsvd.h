@@ -84,9 +84,11 @@ typedef enum {
                                     launch, grid barrier, column slices) and, multi-GPU, publishes them
                                     to the peers; 0 (default): separate reduction kernel (measured
                                     faster)                                                */
-    TSVD_OPT_DETERMINISTIC = 14  /* 0 (default): N1 CTAs claim row chunks dynamically (no tail behind
-                                    the slowest SM; sums are reproducible only to rounding);
-                                    1: static contiguous row split, bitwise-reproducible results      */
+    TSVD_OPT_DETERMINISTIC = 14, /* 1 (default): static contiguous row split per CTA, bitwise-
+                                    reproducible results; 0: CTAs claim row chunks dynamically (sums
+                                    reproducible only to rounding; measured slower on dense C2)        */
+    TSVD_OPT_GRAPH_UNROLL = 15   /* iterations per CUDA-graph WHILE body (1..8, default 2): later ones
+                                    are no-ops once the component has stopped                        */
 } tsvd_option;
 
 /*

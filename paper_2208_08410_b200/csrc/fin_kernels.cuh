@@ -180,7 +180,7 @@ struct FinParams {
 constexpr int kVtReg = 16;
 
 template <int SRC>
-__global__ void __launch_bounds__(kFinThreads) fin_iter(const FinParams p) {
+__global__ void __launch_bounds__(kFinThreads, 4) fin_iter(const FinParams p) {
     __shared__ double gsum[kFinGroups][kFinCols];
     __shared__ double wred[kFinThreads / 32][2 + kVtReg];
     __shared__ int am_last, peer_ok;
@@ -317,9 +317,12 @@ __global__ void __launch_bounds__(kFinThreads) fin_iter(const FinParams p) {
         if (lane == 0) wred[grp][0] = q;
         q = warp_sum(a_vy);
         if (lane == 0) wred[grp][1] = q;
-        for (int i = 0; i < lr; ++i) {
-            q = warp_sum(acc[i]);
-            if (lane == 0) wred[grp][2 + i] = q;
+#pragma unroll
+        for (int i = 0; i < kVtReg; ++i) {  // static indices: acc stays in registers
+            if (i < lr) {
+                q = warp_sum(acc[i]);
+                if (lane == 0) wred[grp][2 + i] = q;
+            }
         }
     }
     __syncthreads();

@@ -88,7 +88,7 @@ struct tsvd_s {
     PeerView pv{};
     std::string peer_error;
     // options
-    int max_iter = 10000, fixed_T = 0, use_graph = 1, timing = 0, run_rows = 1024, cps_opt = 0;
+    int max_iter = 10000, fixed_T = 0, use_graph = 1, timing = 0, run_rows = 1024, cps_opt = 0, unroll = 2;
     uint64_t seed = 0;
     // input
     int64_t row_begin = 0, row_end = 0, m_g = 0;
@@ -124,7 +124,7 @@ struct tsvd_s {
     int fused_opt = 0;
     unsigned *gbar = nullptr;
     // dynamic row scheduling in N1 (option 14 DETERMINISTIC = 1 switches to a static split)
-    int dynamic_opt = 1;
+    int dynamic_opt = 0;  // measured: the static split is faster on the dense C2 pass
     unsigned long long *work = nullptr;
     unsigned long long *tl_d = nullptr;  // debug: TSVD_TIMELINE=<file> (N1 start/end, fin end per iteration)
     // debug: TSVD_TRACE=<file> appends per-CTA N1 timestamps of host-loop iterations
@@ -283,7 +283,7 @@ static tsvd_status ensure_alloc(tsvd_t h) {
     h->ystride = round_up(n, 32);
     h->wofs = round_up(n, 32);
     h->ypart_ld = round_up(n, 4);
-    h->fin_blocks = (int)std::min<int64_t>((n + kFinCols - 1) / kFinCols, (int64_t)h->sms * 8);
+    h->fin_blocks = (int)std::min<int64_t>((n + kFinCols - 1) / kFinCols, (int64_t)h->sms * 4);  // one wave
     h->part_ld = 2 + h->kpad;
     auto dm = [&](void **p, size_t bytes) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(bytes, 16)); };
     cudaError_t e = cudaSuccess;
@@ -815,7 +815,10 @@ static tsvd_status build_graph(tsvd_t h, int l0) {
         cudaGraph_t body = cp.conditional.phGraph_out[0];
         ce = cudaStreamBeginCaptureToGraph(h->body_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
         if (ce) break;
-        s = launch_iteration(h, h->body_stream, l, (unsigned long long)ch, 1);
+        // the body holds `unroll` iterations: every kernel of an iteration is a no-op once the
+        // component is done, so this only saves WHILE-node turnarounds (~8 us each, measured)
+        for (int u = 0; u < h->unroll && s >= 0; ++u)
+            s = launch_iteration(h, h->body_stream, l, (unsigned long long)ch, 1);
         cudaGraph_t body_out = nullptr;
         cudaError_t ce2 = cudaStreamEndCapture(h->body_stream, &body_out);
         if (s < 0) break;
@@ -1010,6 +1013,10 @@ tsvd_status tsvd_set_option(tsvd_t h, int32_t key, int64_t value) {
         break;
     case TSVD_OPT_DETERMINISTIC:
         h->dynamic_opt = value == 0;
+        break;
+    case TSVD_OPT_GRAPH_UNROLL:
+        if (value < 1 || value > 8) return h->fail(TSVD_ERR_ARG, "GRAPH_UNROLL in 1..8");
+        h->unroll = (int)value;
         break;
     case TSVD_OPT_PLACEMENT:
     case TSVD_OPT_RESIDENT_BYTES:
@@ -1288,7 +1295,8 @@ tsvd_status tsvd_run(tsvd_t h) {
     const int64_t per_ext = (h->sparse ? 1 : per_pass) + (h->coll == COLL_NONE ? 1 : 2);
     for (int l = l0; l < h->k; ++l) {
         const CompStat &cs = h->stats_host[l];
-        h->launches += 1 + per_iter * (int64_t)cs.it + per_ext;
+        const int64_t issued = h->loop_mode == "graph-while" ? (cs.it + h->unroll - 1) / h->unroll * h->unroll : cs.it;
+        h->launches += 1 + per_iter * issued + per_ext;
         if (cs.status == -7) return h->fail(TSVD_ERR_NUMERIC, "non-finite value or zero initial vector at component %d", l);
         if (!cs.valid || cs.status == 2) {
             result = TSVD_WARN_RANK_EXHAUSTED;

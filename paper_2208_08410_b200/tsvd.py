@@ -27,7 +27,8 @@ OPT_COLLECTIVE = 8  # world > 1: 0 = in-kernel NVLink peer all-reduce (default),
 OPT_PLACEMENT, OPT_RESIDENT_BYTES, OPT_BATCH_ROWS, OPT_QUEUE_DEPTH = 9, 10, 11, 12  # out-of-memory streaming
 PLACEMENT_AUTO, PLACEMENT_RESIDENT, PLACEMENT_STREAM = 0, 1, 2
 OPT_FUSED_REDUCE = 13  # 1: N1 reduces its own partials (cooperative launch); 0: separate kernels
-OPT_DETERMINISTIC = 14  # 1: static row split (bitwise reproducible); 0: dynamic row chunks (default)
+OPT_DETERMINISTIC = 14  # 1: static row split, bitwise reproducible (default); 0: dynamic row chunks
+OPT_GRAPH_UNROLL = 15  # iterations per CUDA-graph WHILE body (default 2)
 F32, ROW_MAJOR = 0, 0
 
 _lib = None
