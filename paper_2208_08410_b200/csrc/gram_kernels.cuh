@@ -218,6 +218,35 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// ---- 2-CTA cluster helpers (row split for n > 16384): DSMEM exchange of the half dot products
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t smem_addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_f64(uint32_t addr, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_remote_arrive(uint32_t addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "TSVD_CWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra TSVD_CWAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
 __device__ __forceinline__ void fence_barrier_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -248,7 +277,11 @@ __device__ __forceinline__ void set_cond(unsigned long long h, int use, unsigned
 // ---------------------------------------------------------------- N1: fused Gram-vector pass
 // Grid: one persistent CTA per (SM x CTAs/SM), each owning a contiguous row range.
 // Block: T threads; thread `tid` owns float4 columns {k*T + tid : k < NV} of every row.
-template <int T, int NV, bool EXTRACT>
+// SPLIT = 2 (n > 4*T*NV, up to 32768): a 2-CTA cluster shares each row range, CTA rank q staging
+// and owning the q-th half of every row; the two half dot products are exchanged through
+// distributed shared memory (remote store + remote mbarrier arrive) and added in rank order,
+// so both CTAs use the same t_r.  Rank 0 alone handles the U (deflation) columns.
+template <int T, int NV, bool EXTRACT, int SPLIT>
 __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int NW = T / 32;
@@ -264,19 +297,28 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     double *red = reinterpret_cast<double *>(bars + kMaxStages);  // [2][NW]
 
     __shared__ int64_t slot_row[kMaxStages];  // row held by each ring slot (-1: no more rows)
+    __shared__ double xch[2];                  // SPLIT: the partner's half dot product
+    __shared__ __align__(8) uint64_t xbar[2];  // SPLIT: arrivals of the partner's value
+    const int crank = SPLIT == 2 ? (int)cluster_ctarank() : 0;
+    const int part_id = blockIdx.x / SPLIT;
+    const int nparts = gridDim.x / SPLIT;
+    const int half4 = (p.n4 + SPLIT - 1) / SPLIT;    // float4 columns per CTA (row_bytes = half4*16)
+    const int c4_0 = crank * half4;                  // first float4 column of this CTA
+    const int my_n4 = (p.n4 - c4_0) < half4 ? (p.n4 - c4_0) : half4;
+    const bool owner = crank == 0;                   // handles U rows, w, u_out, sq
     const int S = p.stages;
-    const int l = EXTRACT ? 0 : p.l;
-    const uint32_t tx_bytes = (uint32_t)(p.row_bytes + (EXTRACT ? 0 : p.u_bytes));
+    const int l = (EXTRACT || !owner) ? 0 : p.l;
+    const uint32_t tx_bytes = (uint32_t)(my_n4 * 16 + (l > 0 ? p.u_bytes : 0));
 
     // Row schedule (producer thread only).  Dynamic: claim chunks of chunk_rows rows from a
-    // per-launch counter, so SMs that get less HBM bandwidth simply take fewer rows (the static
-    // split left a ~50 us tail behind the slowest SM).  Static: contiguous range per CTA
-    // (bitwise-reproducible sums for a fixed grid).
-    int64_t cur = p.dynamic ? 0 : p.rows * blockIdx.x / gridDim.x;
-    int64_t cur_end = p.dynamic ? 0 : p.rows * (blockIdx.x + 1) / gridDim.x;
+    // per-launch counter, so SMs that get less HBM bandwidth simply take fewer rows.  Static:
+    // contiguous range per CTA (per cluster when SPLIT = 2), bitwise-reproducible sums.
+    const bool dyn = p.dynamic && SPLIT == 1;
+    int64_t cur = dyn ? 0 : p.rows * part_id / nparts;
+    int64_t cur_end = dyn ? 0 : p.rows * (part_id + 1) / nparts;
     auto next_row = [&]() -> int64_t {
         if (cur >= cur_end) {
-            if (!p.dynamic) return -1;
+            if (!dyn) return -1;
             const unsigned long long base = atomicAdd(p.work, (unsigned long long)p.chunk_rows);
             if (base >= (unsigned long long)p.rows) return -1;
             cur = (int64_t)base;
@@ -287,17 +329,24 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        if (SPLIT == 2) {
+            mbar_init(&xbar[0], 1);
+            mbar_init(&xbar[1], 1);
+        }
         fence_barrier_init();
     }
     __syncthreads();
+    if (SPLIT == 2) cluster_sync_all();  // the partner's exchange barriers exist before any arrive
+    const uint32_t peer_xch = SPLIT == 2 ? map_to_rank(smem_u32(&xch[0]), crank ^ 1) : 0;
+    const uint32_t peer_xbar = SPLIT == 2 ? map_to_rank(smem_u32(&xbar[0]), crank ^ 1) : 0;
     auto feed = [&](int slot) {  // producer: next row into `slot`, or close the slot
         const int64_t row = next_row();
         slot_row[slot] = row;
         if (row >= 0) {
             unsigned char *dst = smem + (size_t)slot * p.stage_bytes;
             mbar_arrive_expect_tx(&bars[slot], tx_bytes);
-            tma_load_1d(dst, p.A + row * p.ld, (uint32_t)p.row_bytes, &bars[slot]);
-            if (!EXTRACT && p.u_bytes > 0)
+            tma_load_1d(dst, p.A + row * p.ld + (int64_t)c4_0 * 4, (uint32_t)(my_n4 * 16), &bars[slot]);
+            if (l > 0 && p.u_bytes > 0)
                 tma_load_1d(dst + p.row_bytes, p.U + row * p.ldu, (uint32_t)p.u_bytes, &bars[slot]);
         } else {
             mbar_arrive(&bars[slot]);
@@ -313,8 +362,10 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
         const double *ycur = p.ybuf + (int64_t)(st->it & 1) * p.ystride;
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
-            const int j = 4 * (k * T + tid);
-            if (j + 3 < p.n) {
+            const int j = 4 * (c4_0 + k * T + tid);
+            if (k * T + tid >= my_n4) {
+                vr[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            } else if (j + 3 < p.n) {
                 const double2 lo = *reinterpret_cast<const double2 *>(ycur + j);
                 const double2 hi = *reinterpret_cast<const double2 *>(ycur + j + 2);
                 vr[k] = make_float4((float)(lo.x * inv), (float)(lo.y * inv), (float)(hi.x * inv), (float)(hi.y * inv));
@@ -335,13 +386,13 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     for (int k = 0; k < NV; ++k) ya[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     double wacc = 0.0, sq = 0.0;
     bool flushed = p.accumulate != 0;
-    double *yp = p.ypart + (int64_t)blockIdx.x * p.ypart_ld;
+    double *yp = p.ypart + (int64_t)part_id * p.ypart_ld + (int64_t)c4_0 * 4;
 
     auto flush = [&]() {
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
             const int idx = k * T + tid;
-            if (idx < p.n4) {
+            if (idx < my_n4) {
                 double2 *dst = reinterpret_cast<double2 *>(yp + 4 * (int64_t)idx);
                 double2 lo = make_double2(ya[k].x, ya[k].y), hi = make_double2(ya[k].z, ya[k].w);
                 if (flushed) {
@@ -371,9 +422,9 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
             const int idx = k * T + tid;
-            if (idx < p.n4) {
+            if (idx < my_n4) {
                 a[k] = row[idx];
-                if (tail && idx == p.n4 - 1) {  // columns >= n of the last float4 may be garbage
+                if (tail && c4_0 + idx == p.n4 - 1) {  // columns >= n of the last float4 may be garbage
                     if (tail < 2) a[k].y = 0.f;
                     if (tail < 3) a[k].z = 0.f;
                     a[k].w = 0.f;
@@ -402,9 +453,19 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
         double t = 0.0;
 #pragma unroll
         for (int w = 0; w < NW; ++w) t += red[(i & 1) * NW + w];  // same order in every thread
+        if (SPLIT == 2) {  // half dot products: send mine, wait for the partner's, add in rank order
+            const int b = i & 1;
+            if (tid == 0) {
+                st_cluster_f64(peer_xch + b * (uint32_t)sizeof(double), t);
+                mbar_remote_arrive(peer_xbar + b * (uint32_t)sizeof(uint64_t));
+            }
+            mbar_wait_cluster(&xbar[b], (uint32_t)((i >> 1) & 1));
+            const double other = *reinterpret_cast<volatile double *>(&xch[b]);
+            t = owner ? t + other : other + t;
+        }
 
         if (EXTRACT) {
-            if (tid == 0) {
+            if (tid == 0 && owner) {
                 p.u_out[grow] = t;
                 sq += t * t;
             }
@@ -426,15 +487,16 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     }
     if (p.trace && tid == 0) p.trace[blockIdx.x * 4 + 2] = globaltimer_ns();
     if (EXTRACT) {
-        if (tid == 0) p.sq_part[blockIdx.x] = p.accumulate ? p.sq_part[blockIdx.x] + sq : sq;
+        if (tid == 0 && owner) p.sq_part[part_id] = p.accumulate ? p.sq_part[part_id] + sq : sq;
     } else {
         flush();
         if (tid < l) {
-            double *wp = p.wpart + (int64_t)blockIdx.x * p.wpart_ld + tid;
+            double *wp = p.wpart + (int64_t)part_id * p.wpart_ld + tid;
             *wp = p.accumulate ? *wp + wacc : wacc;
         }
-        if (p.reduce_mode) reduce_tail<T>(p);
+        if (SPLIT == 1 && p.reduce_mode) reduce_tail<T>(p);
     }
+    if (SPLIT == 2) cluster_sync_all();  // no CTA leaves while its partner may still address it
     if (p.trace) {
         __syncthreads();
         if (tid == 0) p.trace[blockIdx.x * 4 + 3] = globaltimer_ns();

@@ -50,15 +50,16 @@ using GvFn = void (*)(const GvParams);
 template <int T, bool EX>
 GvFn pick_nv(int nv) {
     switch (nv) {
-    case 1: return gv_fused<T, 1, EX>;
-    case 2: return gv_fused<T, 2, EX>;
-    case 4: return gv_fused<T, 4, EX>;
-    case 8: return gv_fused<T, 8, EX>;
+    case 1: return gv_fused<T, 1, EX, 1>;
+    case 2: return gv_fused<T, 2, EX, 1>;
+    case 4: return gv_fused<T, 4, EX, 1>;
+    case 8: return gv_fused<T, 8, EX, 1>;
     default: return nullptr;
     }
 }
 template <bool EX>
-GvFn pick_gv(int T, int nv) {
+GvFn pick_gv(int T, int nv, int split = 1) {
+    if (split == 2) return (T == 512 && nv == 8) ? gv_fused<512, 8, EX, 2> : nullptr;
     switch (T) {
     case 32: return pick_nv<32, EX>(nv);
     case 64: return pick_nv<64, EX>(nv);
@@ -149,6 +150,7 @@ struct tsvd_s {
     bool allocated = false;
     // plan
     int T = 0, NV = 0, S = 0, grid = 0, cps = 0, stage_bytes = 0, row_bytes = 0;
+    int split = 1, parts = 0;  // CTAs per row range (2-CTA cluster for n > 16384); partial slots
     size_t smem = 0;
     GvFn gv = nullptr, gv_ex = nullptr;
     // run graph (cached by starting component)
@@ -196,7 +198,7 @@ static thread_local std::string g_err;
 
 // N1 reduces its own partials (grid barrier + column slices) unless the pass is split into
 // several launches (streaming) or the input is sparse (N3 writes y directly).
-static bool fused_reduce(tsvd_t h) { return h->fused_opt && !h->sparse && !h->streaming; }
+static bool fused_reduce(tsvd_t h) { return h->fused_opt && !h->sparse && !h->streaming && h->split == 1; }
 
 static int fin_src(tsvd_t h) {
     if (h->sparse) return SRC_YW;  // N3 writes y straight into yw (then NCCL if world > 1)
@@ -221,18 +223,21 @@ static tsvd_status plan(tsvd_t h) {
         if (dyn > 200 * 1024) return h->fail(TSVD_ERR_UNSUPPORTED, "sparse path supports k <= 3200");
         CK(cudaFuncSetAttribute(csr_spmv<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
         h->grid = h->sms * 8;
+        h->parts = h->grid;
         h->T = kSpThreads;
         return set_fin_attrs(h);
     }
     int T = 32;
     while ((int64_t)4 * T * 8 < n && T < kMaxThreadsPerCta) T *= 2;
-    if ((int64_t)4 * T * 8 < n)
-        return h->fail(TSVD_ERR_UNSUPPORTED, "n = %lld > 16384 needs the 2-CTA cluster variant (not in this version)",
-                       (long long)n);
+    int split = 1;
+    if ((int64_t)4 * T * 8 < n) split = 2;  // 2-CTA cluster: each CTA stages and owns half a row
+    if ((int64_t)4 * T * 8 * split < n)
+        return h->fail(TSVD_ERR_UNSUPPORTED, "n = %lld > 32768 is not supported by the dense kernel", (long long)n);
     int NV = 1;
-    while ((int64_t)4 * T * NV < n) NV *= 2;
+    while ((int64_t)4 * T * NV * split < n) NV *= 2;
     const int n4 = (int)((n + 3) / 4);
-    h->row_bytes = n4 * 16;
+    h->split = split;
+    h->row_bytes = ((n4 + split - 1) / split) * 16;
     h->stage_bytes = (int)round_up(h->row_bytes + h->kpad * 4, 128);
     int cps = h->cps_opt > 0 ? h->cps_opt : std::max(1, 512 / T);
     int S = (int)std::min<int64_t>(kMaxStages, std::max<int64_t>(2, (kRingTargetBytes + (int64_t)h->stage_bytes * cps - 1) /
@@ -246,17 +251,40 @@ static tsvd_status plan(tsvd_t h) {
     h->NV = NV;
     h->S = S;
     h->smem = (size_t)S * h->stage_bytes + kMaxStages * sizeof(uint64_t) + 2 * (T / 32) * sizeof(double);
-    h->gv = pick_gv<false>(T, NV);
-    h->gv_ex = pick_gv<true>(T, NV);
+    h->gv = pick_gv<false>(T, NV, split);
+    h->gv_ex = pick_gv<true>(T, NV, split);
     CK(cudaFuncSetAttribute(h->gv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem));
     CK(cudaFuncSetAttribute(h->gv_ex, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem));
+    if (split == 2) {
+        CK(cudaFuncSetAttribute(h->gv, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+        CK(cudaFuncSetAttribute(h->gv_ex, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+    }
     TRY(set_fin_attrs(h));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->gv, T, h->smem));
     if (occ < 1) return h->fail(TSVD_ERR_UNSUPPORTED, "fused kernel does not fit on an SM (T=%d smem=%zu)", T, h->smem);
     h->cps = std::min(cps, occ);
-    h->grid = (int)std::min<int64_t>((int64_t)h->sms * h->cps, h->m_g);
+    // one row range per CTA (per 2-CTA cluster when split): at most one range per row
+    h->grid = (int)std::min<int64_t>((int64_t)h->sms * h->cps / split, h->m_g) * split;
+    h->parts = h->grid / split;
     return TSVD_OK;
+}
+
+// cluster launch of the split kernel (2 CTAs per row range)
+static cudaError_t launch_split(tsvd_t h, GvFn fn, const GvParams &p, cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(h->grid);
+    cfg.blockDim = dim3(h->T);
+    cfg.dynamicSmemBytes = h->smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fn, p);
 }
 
 // Fresh loop state; the peer-collective epoch is kept (flags in peer memory are monotone).
@@ -294,11 +322,11 @@ static tsvd_status ensure_alloc(tsvd_t h) {
     if (!e) e = dm((void **)&h->yw, (size_t)(h->wofs + h->kpad) * sizeof(double));
     if (!e) e = dm((void **)&h->V0d, (size_t)h->k * n * sizeof(double));
     if (!e) e = dm((void **)&h->c64, (size_t)h->kpad * sizeof(double));
-    if (!e && !h->sparse) e = dm((void **)&h->ypart, (size_t)h->grid * h->ypart_ld * sizeof(double));
-    if (!e) e = dm((void **)&h->wpart, (size_t)h->grid * h->kpad * sizeof(double));
+    if (!e && !h->sparse) e = dm((void **)&h->ypart, (size_t)h->parts * h->ypart_ld * sizeof(double));
+    if (!e) e = dm((void **)&h->wpart, (size_t)h->parts * h->kpad * sizeof(double));
     if (!e) e = dm((void **)&h->part, (size_t)h->fin_blocks * h->part_ld * sizeof(double));
     if (!e) e = dm((void **)&h->u64, (size_t)mg * sizeof(double));
-    if (!e) e = dm((void **)&h->sq_part, (size_t)h->grid * sizeof(double));
+    if (!e) e = dm((void **)&h->sq_part, (size_t)h->parts * sizeof(double));
     if (!e) e = dm((void **)&h->sig2, sizeof(double));
     if (!e) e = dm((void **)&h->st, sizeof(LoopState));
     if (!e) e = dm((void **)&h->stats, (size_t)h->k * sizeof(CompStat));
@@ -546,7 +574,7 @@ static SpParams sp_params(tsvd_t h, int l) {
     p.sq_part = h->sq_part;
     p.yw = h->yw;
     p.wofs = h->wofs;
-    p.parts = h->grid;
+    p.parts = h->parts;
     return p;
 }
 
@@ -583,7 +611,8 @@ static tsvd_status launch_gv(tsvd_t h, cudaStream_t s, int l, bool extract) {
         return TSVD_OK;
     }
     if (!h->streaming || h->m_res > 0) {
-        fn<<<h->grid, h->T, h->smem, s>>>(p);
+        if (h->split == 2) CK(launch_split(h, fn, p, s));
+        else fn<<<h->grid, h->T, h->smem, s>>>(p);
         CK(cudaGetLastError());
     }
     if (!h->streaming) return TSVD_OK;
@@ -604,7 +633,8 @@ static tsvd_status launch_gv(tsvd_t h, cudaStream_t s, int l, bool extract) {
         q.U = h->U32 + r0 * h->kpad;
         q.u_out = h->u64 + r0;
         q.accumulate = (r0 > 0 || h->m_res > 0) ? 1 : 0;
-        fn<<<h->grid, h->T, h->smem, s>>>(q);
+        if (h->split == 2) CK(launch_split(h, fn, q, s));
+        else fn<<<h->grid, h->T, h->smem, s>>>(q);
         CK(cudaGetLastError());
         CK(cudaEventRecord(h->ev_free[slot], s));
         h->streamed_bytes += rows * h->n * (int64_t)sizeof(float);
@@ -622,7 +652,7 @@ static FinParams fin_params(tsvd_t h, int mode, int l, const double *xsrc, unsig
     p.V = h->V64;
     p.ldv = h->k;
     p.ypart = h->ypart;
-    p.parts = h->grid;
+    p.parts = h->parts;
     p.ypart_ld = h->ypart_ld;
     p.wpart = h->wpart;
     p.wpart_ld = h->kpad;
@@ -660,7 +690,7 @@ static PubParams pub_params(tsvd_t h, int mode, int l) {
     PubParams p{};
     p.mode = mode;
     p.ypart = h->ypart;
-    p.parts = h->grid;
+    p.parts = h->parts;
     p.ypart_ld = h->ypart_ld;
     p.wpart = h->wpart;
     p.wpart_ld = h->kpad;
@@ -687,7 +717,7 @@ static tsvd_status launch_exchange(tsvd_t h, cudaStream_t s, int l) {
         publish<<<h->fin_blocks, kFinThreads, 0, s>>>(pub_params(h, 0, l));
         CK(cudaGetLastError());
     } else if (h->coll == COLL_NCCL) {
-        reduce_partials<<<h->fin_blocks, kFinThreads, 0, s>>>(h->ypart, h->grid, h->ypart_ld, (int)h->n, h->wpart,
+        reduce_partials<<<h->fin_blocks, kFinThreads, 0, s>>>(h->ypart, h->parts, h->ypart_ld, (int)h->n, h->wpart,
                                                               h->kpad, l, h->yw, h->wofs, h->st);
         CK(cudaGetLastError());
         NK(ncclAllReduce(h->yw, h->yw, (size_t)(h->wofs + h->kpad), ncclDouble, ncclSum, h->comm, s));
@@ -718,7 +748,7 @@ static tsvd_status launch_extract(tsvd_t h, cudaStream_t s, int l) {
     p.l = l;
     p.u = h->u64;
     p.sq_part = h->sq_part;
-    p.parts = h->grid;
+    p.parts = h->parts;
     p.sig2 = h->sig2;
     p.pv = h->pv;
     p.ybuf = h->ybuf;
@@ -739,7 +769,7 @@ static tsvd_status launch_extract(tsvd_t h, cudaStream_t s, int l) {
         CK(cudaGetLastError());
         ext_finish<SRC_PEER><<<blocks, 256, 0, s>>>(p);
     } else {
-        ext_reduce<<<1, 32, 0, s>>>(h->sq_part, h->grid, h->sig2, h->st);
+        ext_reduce<<<1, 32, 0, s>>>(h->sq_part, h->parts, h->sig2, h->st);
         CK(cudaGetLastError());
         NK(ncclAllReduce(h->sig2, h->sig2, 1, ncclDouble, ncclSum, h->comm, s));
         ext_finish<SRC_YW><<<blocks, 256, 0, s>>>(p);

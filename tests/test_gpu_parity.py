@@ -62,7 +62,9 @@ def _assert_parity(A, ref, U, S, V, kf, k):
 
 @pytest.mark.parametrize("m,n,l", [
     (513, 256, 0), (513, 256, 3), (777, 129, 1), (300, 37, 5), (1000, 1000, 2),
-    (4200, 4099, 4), (8300, 8192, 0), (16500, 16384, 6), (40, 3, 2), (9, 1, 0)])
+    (4200, 4099, 4), (8300, 8192, 0), (16500, 16384, 6), (40, 3, 2), (9, 1, 0),
+    # n > 16384: rows split across a 2-CTA cluster (DSMEM exchange of the half dot products)
+    (20001, 20000, 3), (24000, 16387, 2), (33000, 32768, 0), (32770, 32768, 5)])
 def test_gram_apply_vs_oracle(m, n, l):
     rng = np.random.default_rng(m + 7 * n + l)
     A = rng.standard_normal((m, n)).astype(np.float32)
@@ -126,6 +128,17 @@ def test_ragged_parity(m, n, k, fam):
     ref = oracle.tsvd(A, k, eps, V0)
     rc, U, S, V, kf, *_ = _gpu_tsvd(A, k, eps, V0)
     assert rc == P.OK
+    _assert_parity(A, ref, U, S, V, kf, k)
+
+
+def test_split_rows_full_tsvd():
+    """n = 24577 (> 16384): 2-CTA cluster kernel through a whole run, fixed iterations, vs the oracle."""
+    m, n, k, T = 25000, 24577, 2, 5
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(40, 5.0, 0.7), seed=41)
+    V0 = synth.v0_normal(n, k, seed=42)
+    ref = oracle.tsvd(A, k, 1e-6, V0, fixed_T=T)
+    rc, U, S, V, kf, iters, dots, rep = _gpu_tsvd(A, k, 1e-6, V0, fixed_iters=T)
+    assert rep["plan"]["grid"] % 2 == 0
     _assert_parity(A, ref, U, S, V, kf, k)
 
 
