@@ -246,9 +246,9 @@ def test_argument_errors():
         P.tsvd_create(5, 10, 2, 1e-6)
     assert ei.value.status == P.ERR_UNSUPPORTED
     # n > 16384 needs the cluster variant (not in this version)
-    t = P.TSVD(20000, 20000, 1, 1e-6)
+    t = P.TSVD(40000, 40000, 1, 1e-6)
     with pytest.raises(P.TsvdError) as ei:
-        t.set_dense(torch.zeros((20000, 20000), dtype=torch.float32, device="cuda"))
+        t.set_dense(torch.zeros((40000, 40000), dtype=torch.float32, device="cuda"))
         t.run()
     assert ei.value.status == P.ERR_UNSUPPORTED
     t.close()
