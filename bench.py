@@ -49,6 +49,11 @@ CONFIGS = {
                          "BASELINE configs[2] (256 GiB does not fit the box's 196 GB host RAM)",
                 m=1048576, n=16384, k=2, eps=1e-6, family="hadamard", rank=32, rho=0.8, s0=1.0,
                 stream=True, resident_bytes=0, fixed_T=3),
+    # configs[4] is 8M x 32768 (1 TiB) over 8 GPUs: one GPU's 1M-row slab (128 GiB, in HBM), generated
+    # on the device; n = 32768 runs the 2-CTA cluster row split
+    "c5s": dict(workload="dense fp32 1048576x32768 (128 GiB, one GPU's row slab of BASELINE configs[4] "
+                         "8Mx32768 = 1 TiB) in HBM, k=8, eps=1e-6, Hadamard known spectrum rank 32, s_i=0.8^i",
+                m=1048576, n=32768, k=8, eps=1e-6, family="hadamard_device", rank=32, rho=0.8, s0=1.0),
     # the paper's per-node sparse matrix: 2^25 x 2^25, density ~1e-6 (32 nnz per row,
     # 1.07e9 nnz), randomly generated, k=8 (BASELINE configs[3]); its near-degenerate spectrum never
     # converges, so iterations are fixed as in the paper's OOM runs (100; here 10 per component)
@@ -249,6 +254,10 @@ def main():
         A_pin = torch.empty((r1 - r0, n), dtype=torch.float32, pin_memory=True)
         A_host = make_A(cfg, r0, r1, out=A_pin.numpy())
         A_dev = A_pin
+    elif cfg["family"] == "hadamard_device":  # slab generated in HBM (larger than useful on the host)
+        s_pl = cfg["s0"] * cfg["rho"] ** np.arange(cfg["rank"])
+        A_dev = synth.hadamard_lowrank_device(m, n, s_pl, seed=1, rows=(r0, r1), device=f"cuda:{local}")
+        A_host = None
     elif sparse:  # paper-like CSR slab; same rows whatever the GPU count
         A_host = synth.random_csr(m, n, cfg["d"], seed=1, rows=(r0, r1))
         A_dev = tuple(torch.from_numpy(x).cuda() for x in A_host)
@@ -371,6 +380,9 @@ def main():
                "h2d_bytes_per_step": rep["placement"]["streamed_bytes"] + 8 * k * n,
                "d2h_bytes_per_step": 4 * mg * k + 8 * k + 8 * n * k + k * 64,
                "note": "streamed config: value is already host-to-host (U, S, V read back after the timed region)"}
+    elif A_host is None and not args.no_e2e:
+        e2e = {"value": None, "unit": "GB/s", "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+               "note": "slab generated on the device; a host copy of it would not fit the box's host RAM"}
     elif not args.no_e2e:
         t2 = P.TSVD(m, n, k, eps, rank=rank, world=world, uid=None, device=local) if world == 1 else None
         te = t2 if t2 is not None else t
@@ -412,7 +424,8 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(A_host, cfg)
+        # device-generated slabs: the oracle runs on a 65536-row sample copied to the host
+        cpu = cpu_baseline(A_host if A_host is not None else A_dev[:65536].cpu().numpy(), cfg)
 
     if rank == 0:
         line = {

@@ -88,6 +88,31 @@ def hadamard_lowrank(m: int, n: int, s: np.ndarray, seed: int = 1, out: np.ndarr
     return out
 
 
+def hadamard_lowrank_device(m: int, n: int, s: np.ndarray, seed: int = 1, rows: tuple[int, int] | None = None,
+                            device="cuda", row_chunk: int = 16384):
+    """``hadamard_lowrank`` materialised directly in GPU memory (torch tensor), for slabs larger than
+    host RAM: the rank-r factors come from the same seeded draws; the r-term product runs as an fp64
+    torch matmul on the device per row chunk, then is rounded to fp32.  (Input synthesis only: the
+    last bit may differ from the host version because the matmul sums in another order.)"""
+    import torch
+    s = np.asarray(s, dtype=np.float64)
+    r = s.shape[0]
+    rng = np.random.Generator(np.random.PCG64(seed))
+    a = rng.choice(m, size=r, replace=False)
+    b = rng.choice(n, size=r, replace=False)
+    d1 = rng.choice(np.array([-1.0, 1.0]), size=m)
+    d2 = rng.choice(np.array([-1.0, 1.0]), size=n)
+    right = _walsh_factor(n, b, d2, slice(None)) / np.sqrt(n)
+    rs = torch.from_numpy((right * s).T.copy()).to(device)             # r x n fp64
+    g0, g1 = (0, m) if rows is None else rows
+    out = torch.empty((g1 - g0, n), dtype=torch.float32, device=device)
+    for r0 in range(g0, g1, row_chunk):
+        r1 = min(g1, r0 + row_chunk)
+        left = torch.from_numpy(_walsh_factor(m, a, d1, slice(r0, r1)) / np.sqrt(m)).to(device)
+        out[r0 - g0:r1 - g0] = (left @ rs).to(torch.float32)
+    return out
+
+
 def uniform_dense(m: int, n: int, seed: int = 1) -> np.ndarray:
     """Paper-like nonnegative U[0,1) fp32 matrix."""
     rng = np.random.Generator(np.random.PCG64(seed))
