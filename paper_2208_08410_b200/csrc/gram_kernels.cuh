@@ -238,6 +238,13 @@ __device__ __forceinline__ void st_cluster_f64(uint32_t addr, double v) {
 __device__ __forceinline__ void mbar_remote_arrive(uint32_t addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
 }
+// asynchronous 8-byte store into the partner CTA's shared memory that completes 8 tx-bytes on the
+// partner's mbarrier (DSMEM message passing: one hop, no separate release/arrive)
+__device__ __forceinline__ void st_async_f64(uint32_t remote_addr, double v, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(remote_addr),
+                 "d"(v), "r"(remote_bar)
+                 : "memory");
+}
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -456,10 +463,11 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
         if (SPLIT == 2) {  // half dot products: send mine, wait for the partner's, add in rank order
             const int b = i & 1;
             if (tid == 0) {
-                st_cluster_f64(peer_xch + b * (uint32_t)sizeof(double), t);
-                mbar_remote_arrive(peer_xbar + b * (uint32_t)sizeof(uint64_t));
+                mbar_arrive_expect_tx(&xbar[b], (uint32_t)sizeof(double));  // my arrival + 8 bytes due
+                st_async_f64(peer_xch + b * (uint32_t)sizeof(double), t, peer_xbar + b * (uint32_t)sizeof(uint64_t));
+                mbar_wait_cluster(&xbar[b], (uint32_t)((i >> 1) & 1));
             }
-            mbar_wait_cluster(&xbar[b], (uint32_t)((i >> 1) & 1));
+            __syncthreads();
             const double other = *reinterpret_cast<volatile double *>(&xch[b]);
             t = owner ? t + other : other + t;
         }
