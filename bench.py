@@ -231,6 +231,8 @@ def main():
                     help="TSVD_OPT_FUSED_REDUCE (default: the library's default)")
     ap.add_argument("--deterministic", type=int, default=None, choices=[0, 1],
                     help="TSVD_OPT_DETERMINISTIC (default: the library's default)")
+    ap.add_argument("--fused-extract", type=int, default=None, choices=[0, 1],
+                    help="TSVD_OPT_FUSED_EXTRACT (default: the library's default)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -288,6 +290,8 @@ def main():
         t.set_option(P.OPT_FUSED_REDUCE, args.fused_reduce)
     if args.deterministic is not None:
         t.set_option(P.OPT_DETERMINISTIC, args.deterministic)
+    if args.fused_extract is not None:
+        t.set_option(P.OPT_FUSED_EXTRACT, args.fused_extract)
     stream = torch.cuda.ExternalStream(t.stream())
 
     def barrier():

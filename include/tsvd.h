@@ -87,8 +87,13 @@ typedef enum {
     TSVD_OPT_DETERMINISTIC = 14, /* 1 (default): static contiguous row split per CTA, bitwise-
                                     reproducible results; 0: CTAs claim row chunks dynamically (sums
                                     reproducible only to rounding; measured slower on dense C2)        */
-    TSVD_OPT_GRAPH_UNROLL = 15   /* iterations per CUDA-graph WHILE body (1..8, default 2): later ones
+    TSVD_OPT_GRAPH_UNROLL = 15,  /* iterations per CUDA-graph WHILE body (1..8, default 2): later ones
                                     are no-ops once the component has stopped                        */
+    TSVD_OPT_FUSED_EXTRACT = 16  /* dense resident input: 1 (default) = the extraction u = A v (Alg. 2
+                                    line 10) of component l-1 rides in the same pass over A
+                                    as the first iteration of component l (one read of A saved per
+                                    component); 0 = separate extraction pass. Same results to
+                                    rounding (DESIGN R21)                                             */
 } tsvd_option;
 
 /*

@@ -25,7 +25,7 @@ namespace tsvd {
 constexpr int kFinCols = 32;                       // columns per fin block
 constexpr int kFinGroups = kFinThreads / kFinCols;  // partial groups per column
 
-enum FinMode { FIN_ITERATE = 0, FIN_INIT = 1, FIN_LOAD_RAW = 2, FIN_APPLY = 3 };
+enum FinMode { FIN_ITERATE = 0, FIN_INIT = 1, FIN_LOAD_RAW = 2, FIN_APPLY = 3, FIN_INIT_EXT = 4, FIN_ITERATE_EXT = 5 };
 enum FinSrc { SRC_PARTS = 0, SRC_YW = 1, SRC_PEER = 2 };
 
 // Called by one thread per block: wait until every rank has published epoch `target`.
@@ -90,6 +90,7 @@ struct PubParams {
     const double *sq_part;
     PeerView pv;
     LoopState *st;
+    int with_sq;  // mode 0 after a fused-extraction pass: also publish sum(u_r^2)
 };
 
 __global__ void __launch_bounds__(kFinThreads) publish(const PubParams p) {
@@ -122,6 +123,11 @@ __global__ void __launch_bounds__(kFinThreads) publish(const PubParams p) {
                 w = warp_sum(w);
                 if (lane == 0) slot[p.pv.wofs + i] = w;
             }
+        if (p.with_sq && blockIdx.x == 0 && tid == 0) {
+            double s = 0.0;
+            for (int b = 0; b < p.parts; ++b) s += p.sq_part[b];
+            slot[p.pv.sofs] = s;
+        }
     } else if (blockIdx.x == 0 && tid == 0) {
         double s = 0.0;
         for (int b = 0; b < p.parts; ++b) s += p.sq_part[b];
@@ -164,6 +170,18 @@ struct FinParams {
     unsigned long long cond;
     int use_cond;
     unsigned long long *tl;   // debug timeline (TSVD_TIMELINE)
+    // fused extraction (FIN_INIT_EXT / FIN_ITERATE_EXT): component `fresh` = l-1 was extracted by
+    // the same N1 pass that ran the first iteration of component l; its sigma is only known here
+    int fresh;                // -1 when unused
+    double *Vout;             // FIN_INIT_EXT: V[:, fresh] = previous iterate
+    float *vprev32;           // FIN_INIT_EXT: fp32 copy of it, staged by the next N1<TWO>
+    CompStat *stat;           // stat[fresh]
+    const double *sq_part;    // FIN_ITERATE_EXT (SRC_PARTS): per-CTA sums of u_r^2
+    int sq_parts;
+    float *U;                 // FIN_ITERATE_EXT: U[:, fresh] = u / sigma
+    int ldu;
+    const double *u_out;
+    int64_t rows;
 };
 
 // FIN_ITERATE : y_new = sum(partials) - V (S w) -> ybuf[(it+1)&1]; stop test; it += 1
@@ -192,21 +210,25 @@ __global__ void __launch_bounds__(kFinThreads, 4) fin_iter(const FinParams p) {
     double *tot = g + l;
     double *vtx = tot + 2 + l;
     double *ys = vtx + lx;
+    __shared__ double sigma_s;
     LoopState *st = p.st;
     const int tid = threadIdx.x, lane = tid & 31, grp = tid >> 5;
-    if (st->stop || (p.mode == FIN_ITERATE && st->done)) {
+    const int mode = p.mode;
+    const bool iterate = (mode == FIN_ITERATE || mode == FIN_ITERATE_EXT);
+    if (st->stop || (iterate && st->done)) {
         if (blockIdx.x == 0 && tid == 0) set_cond(p.cond, p.use_cond, 0u);
         return;
     }
-    const int mode = p.mode;
     const int64_t n = p.n;
     const int it = st->it;
     const double ny = st->ny;
     const unsigned e = st->epoch;
     const double *ycur = p.ybuf + (int64_t)(it & 1) * p.ystride;
-    double *ynew = p.ybuf + (int64_t)(mode == FIN_ITERATE ? ((it + 1) & 1) : (mode == FIN_APPLY ? 1 : 0)) * p.ystride;
-    const bool reduce = (mode == FIN_ITERATE || mode == FIN_APPLY);
+    double *ynew = p.ybuf + (int64_t)(iterate ? ((it + 1) & 1) : (mode == FIN_APPLY ? 1 : 0)) * p.ystride;
+    const bool reduce = (iterate || mode == FIN_APPLY);
     const int64_t slot_off = (int64_t)(e & 1u) * p.pv.slot_stride;
+    // the fresh component's sigma is unknown until FIN_ITERATE_EXT: weight 1 in g and c meanwhile
+    const int fresh = (mode == FIN_INIT_EXT || mode == FIN_ITERATE_EXT) ? p.fresh : -1;
 
     if (reduce) {
         if (SRC == SRC_PEER) {
@@ -222,16 +244,33 @@ __global__ void __launch_bounds__(kFinThreads, 4) fin_iter(const FinParams p) {
                 double w = 0.0;
                 for (int b = lane; b < p.parts; b += 32) w += p.wpart[(int64_t)b * p.wpart_ld + i];
                 w = warp_sum(w);
-                if (lane == 0) g[i] = p.S[i] * w;
+                if (lane == 0) g[i] = (i == fresh ? 1.0 : p.S[i]) * w;
             }
         } else if (SRC == SRC_YW) {
-            for (int i = tid; i < l; i += kFinThreads) g[i] = p.S[i] * p.yw[p.wofs + i];
+            for (int i = tid; i < l; i += kFinThreads) g[i] = (i == fresh ? 1.0 : p.S[i]) * p.yw[p.wofs + i];
         } else {
             for (int i = tid; i < l; i += kFinThreads) {
                 double w = 0.0;
                 for (int r = 0; r < p.pv.world; ++r) w += __ldcg(p.pv.buf[r] + slot_off + p.pv.wofs + i);
-                g[i] = p.S[i] * w;
+                g[i] = (i == fresh ? 1.0 : p.S[i]) * w;
             }
+        }
+        if (mode == FIN_ITERATE_EXT) {  // sigma_fresh = ||A v_prev||, sums in a fixed order
+            if (tid == 0) {
+                double s2 = 0.0;
+                if (SRC == SRC_PEER) {
+                    for (int r = 0; r < p.pv.world; ++r) s2 += __ldcg(p.pv.buf[r] + slot_off + p.pv.sofs);
+                } else {
+                    for (int b = 0; b < p.sq_parts; ++b) s2 += p.sq_part[b];
+                }
+                sigma_s = sqrt(s2);
+            }
+            __syncthreads();
+            const double sg = sigma_s;
+            if (sg > 0.0 && isfinite(sg))  // U[:, fresh] = u / sigma, all blocks share the rows
+                for (int64_t r = (int64_t)blockIdx.x * kFinThreads + tid; r < p.rows;
+                     r += (int64_t)gridDim.x * kFinThreads)
+                    p.U[r * p.ldu + fresh] = (float)(p.u_out[r] / sg);
         }
     }
     for (int i = tid; i < lx; i += kFinThreads) vtx[i] = 0.0;
@@ -281,18 +320,23 @@ __global__ void __launch_bounds__(kFinThreads, 4) fin_iter(const FinParams p) {
         }
         if (active) {
             const double *Vj = p.V + j * p.ldv;
+            double vold = 0.0;
             if (reduce) {
                 double corr = 0.0;  // (V (S w))_j: the 2nd / 4th terms of Eq. 2 in factored form
                 for (int i = 0; i < l; ++i) corr += Vj[i] * g[i];
                 yj -= corr;
-                if (mode == FIN_ITERATE) vj = ycur[j] / ny;
+                if (iterate) vj = ycur[j] / ny;
+            } else if (mode == FIN_INIT_EXT) {  // the finished component's v becomes V[:, fresh]
+                vold = ycur[j] / ny;
+                p.Vout[j * p.ldv + fresh] = vold;
+                p.vprev32[j] = (float)vold;
             }
             ynew[j] = yj;
             a_yy += yj * yj;
             a_vy += vj * yj;
 #pragma unroll
             for (int i = 0; i < kVtReg; ++i)
-                if (i < l) acc[i] += Vj[i] * yj;
+                if (i < l) acc[i] += (i == fresh && mode == FIN_INIT_EXT ? vold : Vj[i]) * yj;
         }
         if (lx > 0) {  // components >= 16: shared tile of this chunk's y, coalesced over i
             if (narrow) {
@@ -355,17 +399,42 @@ __global__ void __launch_bounds__(kFinThreads, 4) fin_iter(const FinParams p) {
         if (lane == 0) tot[q] = s;
     }
     __syncthreads();
+    __shared__ double c_fresh_scale;  // S of the fresh column in c: 1 (INIT_EXT) or sigma (ITERATE_EXT)
     if (tid == 0) {
         st->counter = 0;
         const double yy = tot[0];
         const double nyn = sqrt(yy);
+        c_fresh_scale = 1.0;
+        if (mode == FIN_INIT_EXT) {  // close the finished component's record (sigma comes next pass)
+            CompStat cs = p.stat[fresh];
+            cs.it = it;
+            cs.d = st->d;
+            cs.status = st->status;
+            p.stat[fresh] = cs;
+        }
+        if (mode == FIN_ITERATE_EXT) {
+            const double sg = sigma_s;
+            CompStat cs = p.stat[fresh];
+            cs.sigma = sg;
+            if (sg > 0.0 && isfinite(sg)) {
+                const_cast<double *>(p.S)[fresh] = sg;  // (S is read-only elsewhere in this launch)
+                cs.valid = 1;
+                c_fresh_scale = sg;
+            } else {  // the extracted component had no energy: rank exhausted (R14) / non-finite
+                cs.status = isfinite(sg) ? 2 : -7;
+                st->status = cs.status;
+                st->stop = 1;
+                st->done = 1;
+            }
+            p.stat[fresh] = cs;
+        }
         if (mode == FIN_LOAD_RAW) {
             st->ny = 1.0;
             st->it = 0;
             st->done = 0;
             st->status = 0;
             inv_s = 1.0;
-        } else if (mode == FIN_INIT) {
+        } else if (mode == FIN_INIT || mode == FIN_INIT_EXT) {
             st->ny = nyn;
             st->it = 0;
             st->done = 0;
@@ -378,11 +447,13 @@ __global__ void __launch_bounds__(kFinThreads, 4) fin_iter(const FinParams p) {
                 st->status = 0;
             }
             inv_s = (nyn > 0.0 && isfinite(nyn)) ? nyn : 1.0;
-        } else {  // FIN_ITERATE
+        } else {  // FIN_ITERATE / FIN_ITERATE_EXT
             if (SRC == SRC_PEER) st->epoch = e + 1u;
             const int itn = it + 1;
             st->it = itn;
-            if (!isfinite(nyn)) {
+            if (st->stop) {
+                // the fused extraction found sigma == 0: nothing more to decide
+            } else if (!isfinite(nyn)) {
                 st->status = -7;
                 st->stop = 1;
                 st->done = 1;
@@ -409,7 +480,8 @@ __global__ void __launch_bounds__(kFinThreads, 4) fin_iter(const FinParams p) {
         }
     }
     __syncthreads();
-    for (int i = tid; i < l; i += kFinThreads) p.c[i] = p.S[i] * (tot[2 + i] / inv_s);  // c = S V^T v1
+    for (int i = tid; i < l; i += kFinThreads)  // c = S V^T v1
+        p.c[i] = (i == fresh ? c_fresh_scale : p.S[i]) * (tot[2 + i] / inv_s);
 }
 
 // ---------------------------------------------------------------- N6: extraction tail

@@ -141,6 +141,9 @@ struct GvParams {
     int32_t chunk_rows;
     unsigned long long *work;   // [0] next unclaimed row, [1] CTAs finished (reset by the last)
     unsigned long long *tl;     // debug timeline: [0] iterations, [1] exit count, then 3 per iteration
+    const float *vprev;         // TWO: previous component's v (fp32, n4*4 floats, zero padded)
+    int32_t vp_bytes;           // TWO: shared memory reserved for vprev (0 otherwise)
+    int32_t pad2_;
 };
 
 // Column-slice reduction of the per-CTA partials at the end of N1 (reduce_mode 1/2).  CTA c owns
@@ -288,7 +291,7 @@ __device__ __forceinline__ void set_cond(unsigned long long h, int use, unsigned
 // and owning the q-th half of every row; the two half dot products are exchanged through
 // distributed shared memory (remote store + remote mbarrier arrive) and added in rank order,
 // so both CTAs use the same t_r.  Rank 0 alone handles the U (deflation) columns.
-template <int T, int NV, bool EXTRACT, int SPLIT>
+template <int T, int NV, bool EXTRACT, int SPLIT, bool TWO>
 __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int NW = T / 32;
@@ -300,8 +303,9 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
         p.tl[2 + 3 * idx] = globaltimer_ns();
     }
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (size_t)p.stages * p.stage_bytes);
-    double *red = reinterpret_cast<double *>(bars + kMaxStages);  // [2][NW]
+    float4 *vps = reinterpret_cast<float4 *>(smem + (size_t)p.stages * p.stage_bytes);  // TWO: v_prev
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (size_t)p.stages * p.stage_bytes + p.vp_bytes);
+    double *red = reinterpret_cast<double *>(bars + kMaxStages);  // [2][NR][NW]
 
     __shared__ int64_t slot_row[kMaxStages];  // row held by each ring slot (-1: no more rows)
     __shared__ double xch[2];                  // SPLIT: the partner's half dot product
@@ -314,7 +318,12 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     const int my_n4 = (p.n4 - c4_0) < half4 ? (p.n4 - c4_0) : half4;
     const bool owner = crank == 0;                   // handles U rows, w, u_out, sq
     const int S = p.stages;
-    const int l = (EXTRACT || !owner) ? 0 : p.l;
+    // TWO: the U column p.l-1 ("fresh") is not stored yet: its entries are u_r = A_r . v_prev,
+    // computed in this same pass (the extraction of component p.l-1), with c_fresh = v_prev . v
+    // (sigma cancels: U_r,f sigma_f (V_f . v) = (A_r . v_prev)(v_prev . v)).
+    const int l = (EXTRACT || !owner) ? 0 : (TWO ? p.l - 1 : p.l);  // staged U columns
+    const double c_fresh = TWO ? p.c[p.l - 1] : 0.0;
+    constexpr int NR = TWO ? 2 : 1;                  // dot products per row
     const uint32_t tx_bytes = (uint32_t)(my_n4 * 16 + (l > 0 ? p.u_bytes : 0));
 
     // Row schedule (producer thread only).  Dynamic: claim chunks of chunk_rows rows from a
@@ -387,6 +396,13 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     double cval = 0.0;
     if (!EXTRACT && tid < l) cval = p.c[tid];
     const int tail = p.n & 3;  // valid lanes of the last float4 (0 = full)
+    if (TWO) {  // stage v_prev (fp32, zero padded to n4 float4) once; read per row from smem
+        const float4 *src = reinterpret_cast<const float4 *>(p.vprev);
+        for (int idx = tid; idx < p.n4; idx += T) vps[idx] = src[idx];
+        __syncthreads();
+    }
+    const int tf_thread = TWO ? ((p.l - 1) & (T - 1)) : 0;  // accumulates w of the fresh column
+    double wfresh = 0.0;
 
     float4 ya[NV];
 #pragma unroll
@@ -426,6 +442,7 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
 
         float4 a[NV];
         float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
+        float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;  // TWO: dot with v_prev
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
             const int idx = k * T + tid;
@@ -443,6 +460,13 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
             q1 = fmaf(a[k].y, vr[k].y, q1);
             q2 = fmaf(a[k].z, vr[k].z, q2);
             q3 = fmaf(a[k].w, vr[k].w, q3);
+            if (TWO && idx < my_n4) {
+                const float4 vp = vps[idx];
+                p0 = fmaf(a[k].x, vp.x, p0);
+                p1 = fmaf(a[k].y, vp.y, p1);
+                p2 = fmaf(a[k].z, vp.z, p2);
+                p3 = fmaf(a[k].w, vp.w, p3);
+            }
         }
         double part = (double)((q0 + q1) + (q2 + q3));
         float ur = 0.f;
@@ -451,15 +475,28 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
             part -= (double)ur * cval;  // - U_r . c  (deflation, never forming X')
         }
         part = warp_sum(part);
-        if (lane == 0) red[(i & 1) * NW + warp] = part;
+        if (lane == 0) red[((i & 1) * NR) * NW + warp] = part;
+        if (TWO) {
+            const double pu = warp_sum((double)((p0 + p1) + (p2 + p3)));
+            if (lane == 0) red[((i & 1) * NR + 1) * NW + warp] = pu;
+        }
         __syncthreads();  // (a) partial dots visible, (b) every thread is done reading slot s
         if (tid == 0) {
             fence_proxy_async_smem();
             feed(s);
         }
-        double t = 0.0;
+        double t = 0.0, u = 0.0;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) t += red[(i & 1) * NW + w];  // same order in every thread
+        for (int w = 0; w < NW; ++w) t += red[((i & 1) * NR) * NW + w];  // same order in every thread
+        if (TWO) {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) u += red[((i & 1) * NR + 1) * NW + w];
+            t -= u * c_fresh;  // - U_r,fresh sigma_f (V_f . v) = - u_r (v_prev . v)
+            if (tid == 0) {
+                p.u_out[grow] = u;
+                sq += u * u;
+            }
+        }
         if (SPLIT == 2) {  // half dot products: send mine, wait for the partner's, add in rank order
             const int b = i & 1;
             if (tid == 0) {
@@ -487,6 +524,7 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
                 ya[k].w = fmaf(tf, a[k].w, ya[k].w);
             }
             if (tid < l) wacc += t * (double)ur;
+            if (TWO && tid == tf_thread) wfresh += t * u;  // sigma_f U_f^T t = u^T t
             if (++run == p.run_rows) {
                 flush();
                 run = 0;
@@ -501,6 +539,13 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
         if (tid < l) {
             double *wp = p.wpart + (int64_t)part_id * p.wpart_ld + tid;
             *wp = p.accumulate ? *wp + wacc : wacc;
+        }
+        if (TWO) {
+            if (tid == tf_thread) {
+                double *wp = p.wpart + (int64_t)part_id * p.wpart_ld + (p.l - 1);
+                *wp = p.accumulate ? *wp + wfresh : wfresh;
+            }
+            if (tid == 0) p.sq_part[part_id] = p.accumulate ? p.sq_part[part_id] + sq : sq;
         }
         if (SPLIT == 1 && p.reduce_mode) reduce_tail<T>(p);
     }

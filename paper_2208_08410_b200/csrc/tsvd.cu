@@ -47,25 +47,27 @@ uint64_t splitmix64(uint64_t x) {
 
 using GvFn = void (*)(const GvParams);
 
-template <int T, bool EX>
+template <int T, bool EX, bool TWO>
 GvFn pick_nv(int nv) {
     switch (nv) {
-    case 1: return gv_fused<T, 1, EX, 1>;
-    case 2: return gv_fused<T, 2, EX, 1>;
-    case 4: return gv_fused<T, 4, EX, 1>;
-    case 8: return gv_fused<T, 8, EX, 1>;
+    case 1: return gv_fused<T, 1, EX, 1, TWO>;
+    case 2: return gv_fused<T, 2, EX, 1, TWO>;
+    case 4: return gv_fused<T, 4, EX, 1, TWO>;
+    case 8: return gv_fused<T, 8, EX, 1, TWO>;
     default: return nullptr;
     }
 }
-template <bool EX>
+// EX: extraction (dot only); TWO: extraction of the previous component fused into the first
+// iteration of the next (split-free kernels only)
+template <bool EX, bool TWO = false>
 GvFn pick_gv(int T, int nv, int split = 1) {
-    if (split == 2) return (T == 512 && nv == 8) ? gv_fused<512, 8, EX, 2> : nullptr;
+    if (split == 2) return (!TWO && T == 512 && nv == 8) ? gv_fused<512, 8, EX, 2, false> : nullptr;
     switch (T) {
-    case 32: return pick_nv<32, EX>(nv);
-    case 64: return pick_nv<64, EX>(nv);
-    case 128: return pick_nv<128, EX>(nv);
-    case 256: return pick_nv<256, EX>(nv);
-    case 512: return pick_nv<512, EX>(nv);
+    case 32: return pick_nv<32, EX, TWO>(nv);
+    case 64: return pick_nv<64, EX, TWO>(nv);
+    case 128: return pick_nv<128, EX, TWO>(nv);
+    case 256: return pick_nv<256, EX, TWO>(nv);
+    case 512: return pick_nv<512, EX, TWO>(nv);
     default: return nullptr;
     }
 }
@@ -151,6 +153,12 @@ struct tsvd_s {
     // plan
     int T = 0, NV = 0, S = 0, grid = 0, cps = 0, stage_bytes = 0, row_bytes = 0;
     int split = 1, parts = 0;  // CTAs per row range (2-CTA cluster for n > 16384); partial slots
+    // fused extraction (option 16): N1<TWO> = first iteration of component l + extraction of l-1
+    int fuse_ext_opt = 1, S_two = 0, vp_bytes = 0;
+    size_t smem_two = 0;
+    GvFn gv_two = nullptr;
+    float *vprev32 = nullptr;
+    bool fused_ext_used = false;
     size_t smem = 0;
     GvFn gv = nullptr, gv_ex = nullptr;
     // run graph (cached by starting component)
@@ -267,6 +275,20 @@ static tsvd_status plan(tsvd_t h) {
     // one row range per CTA (per 2-CTA cluster when split): at most one range per row
     h->grid = (int)std::min<int64_t>((int64_t)h->sms * h->cps / split, h->m_g) * split;
     h->parts = h->grid / split;
+    // fused-extraction variant: v_prev staged in shared memory, so fewer ring stages
+    h->gv_two = nullptr;
+    if (split == 1) {
+        h->vp_bytes = (int)round_up((int64_t)n4 * 16, 128);
+        const int64_t fixed = h->vp_bytes + kMaxStages * sizeof(uint64_t) + 4 * (T / 32) * sizeof(double) + 1024;
+        int S2 = (int)std::min<int64_t>(S, (kSmemBudget / h->cps - fixed) / h->stage_bytes);
+        if (S2 >= 2) {
+            h->S_two = S2;
+            h->smem_two = (size_t)S2 * h->stage_bytes + h->vp_bytes + kMaxStages * sizeof(uint64_t) +
+                          4 * (T / 32) * sizeof(double);
+            h->gv_two = pick_gv<false, true>(T, NV);
+            CK(cudaFuncSetAttribute(h->gv_two, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_two));
+        }
+    }
     return TSVD_OK;
 }
 
@@ -333,6 +355,10 @@ static tsvd_status ensure_alloc(tsvd_t h) {
     if (!e) e = dm((void **)&h->gbar, 2 * sizeof(unsigned));
     if (!e) e = cudaMemsetAsync(h->gbar, 0, 2 * sizeof(unsigned), h->stream);
     if (!e) e = dm((void **)&h->work, 2 * sizeof(unsigned long long));
+    if (!e && !h->sparse) {
+        e = dm((void **)&h->vprev32, (size_t)round_up(n, 4) * sizeof(float));
+        if (!e) e = cudaMemsetAsync(h->vprev32, 0, (size_t)round_up(n, 4) * sizeof(float), h->stream);
+    }
     if (!e) e = cudaMemsetAsync(h->work, 0, 2 * sizeof(unsigned long long), h->stream);
     if (!e && getenv("TSVD_TRACE")) {
         e = dm((void **)&h->trace_d, (size_t)h->grid * 4 * sizeof(unsigned long long));
@@ -672,6 +698,16 @@ static FinParams fin_params(tsvd_t h, int mode, int l, const double *xsrc, unsig
     p.cond = cond;
     p.use_cond = use_cond;
     p.tl = h->tl_d;
+    p.fresh = l - 1;  // only read by the *_EXT modes
+    p.Vout = h->V64;
+    p.vprev32 = h->vprev32;
+    p.stat = h->stats;
+    p.sq_part = h->sq_part;
+    p.sq_parts = h->parts;
+    p.U = h->U32;
+    p.ldu = h->kpad;
+    p.u_out = h->u64;
+    p.rows = h->m_g;
     return p;
 }
 
@@ -738,6 +774,44 @@ static tsvd_status launch_iteration(tsvd_t h, cudaStream_t s, int l, unsigned lo
 // x_l (device, fp64) -> y_cur = x, ||x||, c = S V^T (x / ||x||)
 static tsvd_status launch_init(tsvd_t h, cudaStream_t s, int l) {
     return launch_fin(h, s, fin_params(h, FIN_INIT, l, h->V0d + (size_t)l * h->n, 0ull, 0), SRC_PARTS);
+}
+
+// Fused extraction is used for dense, resident, unsplit slabs with an in-kernel reduction path.
+static bool fuse_ext(tsvd_t h) {
+    return h->fuse_ext_opt && h->gv_two && !h->sparse && !h->streaming && h->split == 1 && h->coll != COLL_NCCL &&
+           !fused_reduce(h);
+}
+
+// Component l >= 1 with fused extraction.  FIN_INIT_EXT: V[:, l-1] = v_{l-1} (+ fp32 copy), load
+// x_l, c = (S V^T x / ||x||) with weight 1 on column l-1.  Then ONE pass over A (N1<TWO>) does the
+// first iteration of component l and u = A v_{l-1}; FIN_ITERATE_EXT finishes both:
+// sigma_{l-1} = ||u||, U[:, l-1] = u / sigma_{l-1}, and the iterate of component l.
+static tsvd_status launch_init_ext(tsvd_t h, cudaStream_t s, int l) {
+    return launch_fin(h, s, fin_params(h, FIN_INIT_EXT, l, h->V0d + (size_t)l * h->n, 0ull, 0), SRC_PARTS);
+}
+
+static tsvd_status launch_fused_first(tsvd_t h, cudaStream_t s, int l, cudaEvent_t e0 = nullptr,
+                                      cudaEvent_t e1 = nullptr) {
+    if (e0) CK(cudaEventRecord(e0, s));
+    GvParams p = gv_params(h, l, false);
+    p.l = l;
+    p.u_bytes = l - 1 > 0 ? (int32_t)(round_up(l - 1, 4) * 4) : 0;
+    p.stages = h->S_two;
+    p.vprev = h->vprev32;
+    p.vp_bytes = h->vp_bytes;
+    p.reduce_mode = 0;
+    p.tl = nullptr;
+    p.trace = nullptr;
+    h->gv_two<<<h->grid, h->T, h->smem_two, s>>>(p);
+    CK(cudaGetLastError());
+    if (e1) CK(cudaEventRecord(e1, s));
+    if (h->coll == COLL_PEER) {
+        PubParams q = pub_params(h, 0, l);
+        q.with_sq = 1;
+        publish<<<h->fin_blocks, kFinThreads, 0, s>>>(q);
+        CK(cudaGetLastError());
+    }
+    return launch_fin(h, s, fin_params(h, FIN_ITERATE_EXT, l, nullptr, 0ull, 0), fin_src(h));
 }
 
 static tsvd_status launch_extract(tsvd_t h, cudaStream_t s, int l) {
@@ -820,8 +894,14 @@ static tsvd_status build_graph(tsvd_t h, int l0) {
     CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
     tsvd_status s = TSVD_OK;
     cudaError_t ce = cudaSuccess;
+    const bool fx = fuse_ext(h);
     for (int l = l0; l < h->k && s >= 0 && ce == cudaSuccess; ++l) {
-        s = launch_init(h, h->stream, l);
+        if (fx && l > l0) {  // extraction of l-1 rides on the first iteration of l
+            s = launch_init_ext(h, h->stream, l);
+            if (s >= 0) s = launch_fused_first(h, h->stream, l);
+        } else {
+            s = launch_init(h, h->stream, l);
+        }
         if (s < 0) break;
         cudaStreamCaptureStatus cs;
         cudaGraph_t g = nullptr;
@@ -854,7 +934,7 @@ static tsvd_status build_graph(tsvd_t h, int l0) {
         if (s < 0) break;
         ce = ce2;
         if (ce) break;
-        s = launch_extract(h, h->stream, l);
+        if (!fx || l == h->k - 1) s = launch_extract(h, h->stream, l);
     }
     cudaGraph_t graph = nullptr;
     cudaError_t ce3 = cudaStreamEndCapture(h->stream, &graph);
@@ -880,10 +960,14 @@ static tsvd_status run_host_loop(tsvd_t h, int l0) {
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
     }
+    const bool fx = fuse_ext(h);
     for (int l = l0; l < h->k; ++l) {
-        TRY(launch_init(h, h->stream, l));
-        for (;;) {
-            TRY(launch_iteration(h, h->stream, l, 0ull, 0, e0, e1));
+        const bool fused_first = fx && l > l0;
+        if (fused_first) TRY(launch_init_ext(h, h->stream, l));
+        else TRY(launch_init(h, h->stream, l));
+        for (int pass = 0;; ++pass) {
+            if (fused_first && pass == 0) TRY(launch_fused_first(h, h->stream, l, e0, e1));
+            else TRY(launch_iteration(h, h->stream, l, 0ull, 0, e0, e1));
             CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
             CK(cudaStreamSynchronize(h->stream));
             if (h->timing && !h->st_host->stop) {
@@ -905,7 +989,7 @@ static tsvd_status run_host_loop(tsvd_t h, int l0) {
             }
             if (h->st_host->done || h->st_host->stop) break;
         }
-        TRY(launch_extract(h, h->stream, l));
+        if (!fx || l == h->k - 1) TRY(launch_extract(h, h->stream, l));
         CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
         if (h->st_host->stop) break;
@@ -1047,6 +1131,9 @@ tsvd_status tsvd_set_option(tsvd_t h, int32_t key, int64_t value) {
     case TSVD_OPT_GRAPH_UNROLL:
         if (value < 1 || value > 8) return h->fail(TSVD_ERR_ARG, "GRAPH_UNROLL in 1..8");
         h->unroll = (int)value;
+        break;
+    case TSVD_OPT_FUSED_EXTRACT:
+        h->fuse_ext_opt = value != 0;
         break;
     case TSVD_OPT_PLACEMENT:
     case TSVD_OPT_RESIDENT_BYTES:
@@ -1316,7 +1403,10 @@ tsvd_status tsvd_run(tsvd_t h) {
     CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     if (h->st_host->status == -6) return h->fail(TSVD_ERR_NCCL, "peer all-reduce timed out (a rank did not arrive)");
+    if (h->st_host->status == -7 && h->st_host->stop)
+        return h->fail(TSVD_ERR_NUMERIC, "non-finite value or zero initial vector");
     tsvd_status result = TSVD_OK;
+    h->fused_ext_used = fuse_ext(h) && h->k - l0 > 1;
     // our kernels per iteration / extraction (NCCL calls not counted)
     int64_t per_pass = 1;
     if (h->streaming) per_pass = (h->m_res > 0 ? 1 : 0) + (h->m_g - h->m_res + h->batch_rows - 1) / h->batch_rows;
@@ -1325,8 +1415,15 @@ tsvd_status tsvd_run(tsvd_t h) {
     const int64_t per_ext = (h->sparse ? 1 : per_pass) + (h->coll == COLL_NONE ? 1 : 2);
     for (int l = l0; l < h->k; ++l) {
         const CompStat &cs = h->stats_host[l];
-        const int64_t issued = h->loop_mode == "graph-while" ? (cs.it + h->unroll - 1) / h->unroll * h->unroll : cs.it;
-        h->launches += 1 + per_iter * issued + per_ext;
+        // fused extraction: component l > l0 starts with init_ext + the fused first iteration (which
+        // also extracts l-1); only the last component keeps a separate extraction
+        const bool ff = h->fused_ext_used && l > l0;
+        const int64_t body_it = ff ? std::max<int64_t>(cs.it - 1, 0) : cs.it;
+        const int64_t issued = h->loop_mode == "graph-while"
+                                   ? std::max<int64_t>(1, (body_it + h->unroll - 1) / h->unroll) * h->unroll
+                                   : body_it;
+        h->launches += 1 + (ff ? per_iter : 0) + per_iter * issued +
+                       (!h->fused_ext_used || l == h->k - 1 ? per_ext : 0);
         if (cs.status == -7) return h->fail(TSVD_ERR_NUMERIC, "non-finite value or zero initial vector at component %d", l);
         if (!cs.valid || cs.status == 2) {
             result = TSVD_WARN_RANK_EXHAUSTED;
@@ -1408,8 +1505,9 @@ tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
     s += tmp;
     snprintf(tmp, sizeof tmp,
              "\"plan\": {\"T\": %d, \"NV\": %d, \"stages\": %d, \"ctas_per_sm\": %d, \"grid\": %d, \"smem\": %zu, "
-             "\"stage_bytes\": %d, \"run_rows\": %d}, ",
-             h->T, h->NV, h->S, h->cps, h->grid, h->smem, h->stage_bytes, h->run_rows);
+             "\"stage_bytes\": %d, \"run_rows\": %d, \"split\": %d, \"fused_extract\": %s}, ",
+             h->T, h->NV, h->S, h->cps, h->grid, h->smem, h->stage_bytes, h->run_rows, h->split,
+             h->fused_ext_used ? "true" : "false");
     s += tmp;
     snprintf(tmp, sizeof tmp,
              "\"placement\": {\"streaming\": %s, \"resident_rows\": %lld, \"batch_rows\": %lld, \"queue_depth\": %d, "

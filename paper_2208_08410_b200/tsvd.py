@@ -29,6 +29,7 @@ PLACEMENT_AUTO, PLACEMENT_RESIDENT, PLACEMENT_STREAM = 0, 1, 2
 OPT_FUSED_REDUCE = 13  # 1: N1 reduces its own partials (cooperative launch); 0: separate kernels
 OPT_DETERMINISTIC = 14  # 1: static row split, bitwise reproducible (default); 0: dynamic row chunks
 OPT_GRAPH_UNROLL = 15  # iterations per CUDA-graph WHILE body (default 2)
+OPT_FUSED_EXTRACT = 16  # 1 (default): extraction of l-1 fused into the first pass of component l
 F32, ROW_MAJOR = 0, 0
 
 _lib = None

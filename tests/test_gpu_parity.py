@@ -153,6 +153,53 @@ def test_paper_like_uniform_fixed_iterations():
     _assert_parity(A, ref, U, S, V, kf, k)
 
 
+@pytest.mark.parametrize("m,n,k,T", [(2000, 500, 5, 0), (1500, 400, 3, 1), (1500, 400, 3, 2),
+                                     (4200, 4099, 3, 0), (700, 64, 1, 0), (16500, 16384, 2, 3)])
+def test_fused_extraction_matches_separate(m, n, k, T):
+    """FUSED_EXTRACT=1 (u = A v_{l-1} in the same pass as the first iteration of l, reading R21)
+    against the separate extraction pass and against the oracle; includes fixed T = 1 (every
+    component is a single fused pass) and the graph and host loops."""
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(min(n, 48), 5.0, 0.75), seed=m + k)
+    V0 = synth.v0_normal(n, k, seed=k + 1)
+    opts = {"fixed_iters": T} if T else {}
+    ref = oracle.tsvd(A, k, 1e-6, V0, fixed_T=T)
+    on = _gpu_tsvd(A, k, 1e-6, V0, fused_extract=1, **opts)
+    off = _gpu_tsvd(A, k, 1e-6, V0, fused_extract=0, **opts)
+    host = _gpu_tsvd(A, k, 1e-6, V0, fused_extract=1, graph=0, **opts)
+    assert on[7]["plan"]["fused_extract"] == (k > 1)
+    assert off[7]["plan"]["fused_extract"] is False
+    for r in (on, off, host):
+        assert r[0] == P.OK
+        _assert_parity(A, ref, *r[1:5], k)
+    assert np.all(np.abs(on[5] - off[5]) <= 1), (on[5], off[5])
+    np.testing.assert_allclose(on[2], off[2], rtol=2e-6)
+    np.testing.assert_array_equal(on[1], host[1])
+    np.testing.assert_array_equal(on[2], host[2])
+    np.testing.assert_array_equal(on[3], host[3])
+
+
+def test_fused_extraction_resume():
+    """Resume from l0 = 2 factors with fused extraction (the first fused pass is at l = 3)."""
+    m, n, k = 800, 160, 5
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(n, 4.0, 0.7), seed=13)
+    V0 = synth.v0_normal(n, k, seed=13)
+    _, U, S, V, *_ = _gpu_tsvd(A, k, 1e-8, V0, fused_extract=0)
+    t = P.TSVD(m, n, k, 1e-8)
+    t.set_init(V0)
+    t.set_dense(torch.from_numpy(A).cuda())
+    t.set_factors(U[:, :2], S[:2], V[:, :2].astype(np.float64))
+    t.run()
+    U2, S2, V2 = t.result()
+    kf, iters, _ = t.info()
+    assert t.report()["plan"]["fused_extract"] is True
+    t.close()
+    assert kf == k and iters[0] == 0 and iters[1] == 0
+    np.testing.assert_allclose(S2[2:], S[2:], rtol=1e-6)
+    for i in range(2, k):
+        assert 1 - _cos(V2[:, i], V[:, i]) <= 1e-8
+        assert 1 - _cos(U2[:, i], U[:, i]) <= 1e-8
+
+
 def test_graph_and_host_loops_bitwise_equal():
     m, n, k = 900, 200, 4
     A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(n, 3.0, 0.7), seed=4)
