@@ -233,6 +233,10 @@ def main():
                     help="TSVD_OPT_DETERMINISTIC (default: the library's default)")
     ap.add_argument("--fused-extract", type=int, default=None, choices=[0, 1],
                     help="TSVD_OPT_FUSED_EXTRACT (default: the library's default)")
+    ap.add_argument("--pdl", type=int, default=None, choices=[0, 1],
+                    help="TSVD_OPT_PDL (default: the library's default)")
+    ap.add_argument("--row-order", type=int, default=None, choices=[0, 1],
+                    help="TSVD_OPT_ROW_ORDER (default: the library's default)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -292,6 +296,10 @@ def main():
         t.set_option(P.OPT_DETERMINISTIC, args.deterministic)
     if args.fused_extract is not None:
         t.set_option(P.OPT_FUSED_EXTRACT, args.fused_extract)
+    if args.pdl is not None:
+        t.set_option(P.OPT_PDL, args.pdl)
+    if args.row_order is not None:
+        t.set_option(P.OPT_ROW_ORDER, args.row_order)
     stream = torch.cuda.ExternalStream(t.stream())
 
     def barrier():
@@ -356,15 +364,34 @@ def main():
                         for l in range(kf))
     n1_ms_per_launch = rt["n1_ms"] / max(rt["n1_launches"], 1)
     per_launch_bytes = alg_bytes / max(rt["n1_launches"], 1)
+    kern_ms, kernel = rt["n1_ms"], "csr_spmv + csc_spmvT (N2+N3)" if sparse else "gv_fused (N1)"
+    ps = rt.get("persistent", {})
+    ps_passes = None
+    if ps.get("enabled") and ps.get("launches"):
+        # N7: one launch per component runs all its passes after the (fused) first one; the
+        # algorithmic bytes are those of the passes it ran, the time its whole launch (grid
+        # barriers, in-kernel reduction and stop test included)
+        ff = rt["plan"].get("fused_extract", False)
+        body = [int(iters[l]) - (1 if ff and l > 0 else 0) for l in range(kf)]
+        ps_passes = sum(body)
+        alg_bytes = sum(body[l] * (4.0 * mg * n + 4.0 * mg * (l if l % 4 == 0 else (l + 3) // 4 * 4) + 4.0 * n)
+                        for l in range(kf))
+        kern_ms, kernel = ps["ms"], "gv_persist (N7: a component's passes + in-kernel reduction)"
+        n1_ms_per_launch = kern_ms / ps["launches"]
+        per_launch_bytes = alg_bytes / ps["launches"]
     achieved = per_launch_bytes / (n1_ms_per_launch / 1e3) / 1e9
     peak, peak_src = measured_peak()
     traffic = ncu_traffic(args.config) if world == 1 else None
+    if traffic is not None and ps_passes:  # the ncu figure is per pass: scale to a launch
+        traffic = traffic * ps_passes / ps["launches"]
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": "csr_spmv + csc_spmvT (N2+N3)" if sparse else "gv_fused (N1)",
+            "traffic": traffic, "kernel": kernel,
             "per_launch_ms": n1_ms_per_launch,
             "alg_bytes_per_launch": per_launch_bytes,
-            "share_of_step": rt["n1_ms"] / rt["run_ms"] if rt["run_ms"] else None,
+            "share_of_step": kern_ms / rt["run_ms"] if rt["run_ms"] else None,
             "peak_source": peak_src, "rank0_rows": mg}
+    if ps_passes:
+        roof["passes_per_launch"] = ps_passes / ps["launches"]
     if stream_cfg:  # the pass is host-link bound: streamed bytes per pass over the H2D peak
         pl = rep["placement"]
         h2d_peak = measure_h2d_peak(torch, local)

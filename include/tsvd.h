@@ -89,11 +89,24 @@ typedef enum {
                                     reproducible only to rounding; measured slower on dense C2)        */
     TSVD_OPT_GRAPH_UNROLL = 15,  /* iterations per CUDA-graph WHILE body (1..8, default 2): later ones
                                     are no-ops once the component has stopped                        */
-    TSVD_OPT_FUSED_EXTRACT = 16  /* dense resident input: 1 (default) = the extraction u = A v (Alg. 2
+    TSVD_OPT_FUSED_EXTRACT = 16, /* dense resident input: 1 (default) = the extraction u = A v (Alg. 2
                                     line 10) of component l-1 rides in the same pass over A
                                     as the first iteration of component l (one read of A saved per
                                     component); 0 = separate extraction pass. Same results to
                                     rounding (DESIGN R21)                                             */
+    TSVD_OPT_PDL = 17,           /* 1 (default): kernels of the loop are launched with programmatic
+                                    dependent launch (each waits for its predecessor in-kernel, so
+                                    launch latency overlaps the predecessor's drain); 0: plain
+                                    stream order. Bitwise-identical results either way             */
+    TSVD_OPT_ROW_ORDER = 18,     /* resident input: 1 (default) = serpentine, each CTA walks its row
+                                    range backwards on odd iterations so the rows last read by the
+                                    previous pass (still in the 126 MB L2) are read first; 0 = always
+                                    forward. Changes only the fp32 summation order (rounding)       */
+    TSVD_OPT_PERSISTENT = 19     /* single GPU, dense resident, n <= 16384: 1 (default) = the
+                                    iterations of a component run inside ONE cooperative kernel
+                                    (grid barriers, in-kernel reduction and stop test; no per-
+                                    iteration kernel boundaries); 0 = one fused pass + finalize
+                                    kernel per iteration (needed to profile single passes)          */
 } tsvd_option;
 
 /*

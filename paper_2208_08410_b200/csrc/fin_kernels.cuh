@@ -52,6 +52,8 @@ __global__ void __launch_bounds__(kFinThreads)
                     const double *__restrict__ wpart, int wpart_ld, int l, double *__restrict__ yw, int64_t wofs,
                     const LoopState *st) {
     __shared__ double gsum[kFinGroups][kFinCols];
+    griddep_launch();
+    griddep_wait();
     if (st->stop || st->done) return;
     const int tid = threadIdx.x, lane = tid & 31, grp = tid >> 5;
     for (int64_t ch = blockIdx.x; ch * kFinCols < n; ch += gridDim.x) {
@@ -97,6 +99,8 @@ __global__ void __launch_bounds__(kFinThreads) publish(const PubParams p) {
     __shared__ double gsum[kFinGroups][kFinCols];
     __shared__ int am_last;
     LoopState *st = p.st;
+    griddep_launch();
+    griddep_wait();
     if (st->stop || (p.mode == 0 && st->done)) return;  // identical decision on every rank
     const int tid = threadIdx.x, lane = tid & 31, grp = tid >> 5;
     const unsigned e = st->epoch;
@@ -215,6 +219,8 @@ __global__ void __launch_bounds__(kFinThreads, 4) fin_iter(const FinParams p) {
     const int tid = threadIdx.x, lane = tid & 31, grp = tid >> 5;
     const int mode = p.mode;
     const bool iterate = (mode == FIN_ITERATE || mode == FIN_ITERATE_EXT);
+    griddep_launch();
+    griddep_wait();
     if (st->stop || (iterate && st->done)) {
         if (blockIdx.x == 0 && tid == 0) set_cond(p.cond, p.use_cond, 0u);
         return;
@@ -224,6 +230,7 @@ __global__ void __launch_bounds__(kFinThreads, 4) fin_iter(const FinParams p) {
     const double ny = st->ny;
     const unsigned e = st->epoch;
     const double *ycur = p.ybuf + (int64_t)(it & 1) * p.ystride;
+    if (p.tl && iterate && blockIdx.x == 0 && tid == 0) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 3] = globaltimer_ns();
     double *ynew = p.ybuf + (int64_t)(iterate ? ((it + 1) & 1) : (mode == FIN_APPLY ? 1 : 0)) * p.ystride;
     const bool reduce = (iterate || mode == FIN_APPLY);
     const int64_t slot_off = (int64_t)(e & 1u) * p.pv.slot_stride;
@@ -384,6 +391,7 @@ __global__ void __launch_bounds__(kFinThreads, 4) fin_iter(const FinParams p) {
     __syncthreads();
     if (!am_last) return;
     __threadfence();
+    if (p.tl && iterate && tid == 0) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 4] = globaltimer_ns();
     if (mode == FIN_APPLY) {
         if (tid == 0) {
             st->counter = 0;
@@ -476,7 +484,7 @@ __global__ void __launch_bounds__(kFinThreads, 4) fin_iter(const FinParams p) {
             }
             inv_s = (nyn > 0.0 && isfinite(nyn)) ? nyn : 1.0;
             set_cond(p.cond, p.use_cond, (st->done || st->stop) ? 0u : 1u);
-            if (p.tl) p.tl[2 + 3 * ((p.tl[0] - 1) % 4096) + 2] = globaltimer_ns();  // debug timeline
+            if (p.tl) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 2] = globaltimer_ns();  // debug timeline
         }
     }
     __syncthreads();
@@ -488,6 +496,8 @@ __global__ void __launch_bounds__(kFinThreads, 4) fin_iter(const FinParams p) {
 // NCCL path: local sum of the per-CTA ||u||^2 partials (then ncclAllReduce).
 __global__ void ext_reduce(const double *__restrict__ sq_part, int parts, double *__restrict__ sig2,
                            const LoopState *st) {
+    griddep_launch();
+    griddep_wait();
     if (st->stop) return;
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         double s = 0.0;
@@ -520,6 +530,8 @@ template <int SRC>
 __global__ void ext_finish(const ExtParams p) {
     __shared__ int am_last, peer_ok;
     LoopState *st = p.st;
+    griddep_launch();
+    griddep_wait();
     if (st->stop) {  // a previous step hit rank exhaustion / non-finite: record and skip
         if (blockIdx.x == 0 && threadIdx.x == 0 && !p.stat[p.l].valid) {
             p.stat[p.l].status = st->status;

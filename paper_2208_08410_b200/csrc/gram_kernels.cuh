@@ -143,7 +143,8 @@ struct GvParams {
     unsigned long long *tl;     // debug timeline: [0] iterations, [1] exit count, then 3 per iteration
     const float *vprev;         // TWO: previous component's v (fp32, n4*4 floats, zero padded)
     int32_t vp_bytes;           // TWO: shared memory reserved for vprev (0 otherwise)
-    int32_t pad2_;
+    int32_t serpentine;         // 1: odd iterations walk each CTA's row range backwards, so the
+                                // rows the previous pass read last (still in L2) are read first
 };
 
 // Column-slice reduction of the per-CTA partials at the end of N1 (reduce_mode 1/2).  CTA c owns
@@ -278,6 +279,17 @@ __device__ __forceinline__ double warp_sum(double x) {
     return x;
 }
 
+// debug timeline record per iteration: N1 start (block 0), N1 end (last CTA), fin end, fin start
+// (block 0), fin tail start (last block), first N1 CTA out
+constexpr int kTl = 6;
+
+// Programmatic dependent launch: a kernel launched with the PDL attribute may start while its
+// predecessor in the stream is still running; griddep_wait() blocks until that predecessor has
+// completed and its memory is visible (a no-op without the attribute).  griddep_launch() lets the
+// successor launch early; the successor still waits for this grid's completion before it reads.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void set_cond(unsigned long long h, int use, unsigned v) {
 #if CUDART_VERSION >= 12040
     if (use) cudaGraphSetConditional((cudaGraphConditionalHandle)h, v);
@@ -296,11 +308,13 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int NW = T / 32;
     const LoopState *st = p.st;
+    griddep_launch();
+    griddep_wait();
     if (st->stop || (!EXTRACT && st->done)) return;
     if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 4 + 0] = globaltimer_ns();
     if (!EXTRACT && p.tl && blockIdx.x == 0 && threadIdx.x == 0) {  // debug timeline (TSVD_TIMELINE)
         const unsigned long long idx = atomicAdd(p.tl, 1ull) % 4096;
-        p.tl[2 + 3 * idx] = globaltimer_ns();
+        p.tl[2 + kTl * idx] = globaltimer_ns();
     }
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     float4 *vps = reinterpret_cast<float4 *>(smem + (size_t)p.stages * p.stage_bytes);  // TWO: v_prev
@@ -332,6 +346,8 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     const bool dyn = p.dynamic && SPLIT == 1;
     int64_t cur = dyn ? 0 : p.rows * part_id / nparts;
     int64_t cur_end = dyn ? 0 : p.rows * (part_id + 1) / nparts;
+    // serpentine order (static split): the row range is walked backwards on odd iterations
+    const int64_t mirror = (!dyn && p.serpentine && (st->it & 1)) ? cur + cur_end - 1 : -1;
     auto next_row = [&]() -> int64_t {
         if (cur >= cur_end) {
             if (!dyn) return -1;
@@ -340,7 +356,8 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
             cur = (int64_t)base;
             cur_end = cur + p.chunk_rows < p.rows ? cur + p.chunk_rows : p.rows;
         }
-        return cur++;
+        const int64_t r = cur++;
+        return mirror >= 0 ? mirror - r : r;
     };
 
     if (tid == 0) {
@@ -556,9 +573,13 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     }
     if (!EXTRACT && p.tl && tid == 0) {
         __threadfence();
-        if (atomicAdd(p.tl + 1, 1ull) == gridDim.x - 1) {
+        const unsigned long long now = globaltimer_ns();
+        unsigned long long *rec = p.tl + 2 + kTl * ((p.tl[0] - 1) % 4096);
+        const unsigned long long old = atomicAdd(p.tl + 1, 1ull);
+        if (old == 0) rec[5] = now;  // first CTA out
+        if (old == gridDim.x - 1) {
             p.tl[1] = 0;
-            p.tl[2 + 3 * ((p.tl[0] - 1) % 4096) + 1] = globaltimer_ns();
+            rec[1] = now;
         }
     }
     if (p.dynamic && tid == 0) {  // last CTA out resets the row counter for the next launch

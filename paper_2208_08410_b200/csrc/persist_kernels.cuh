@@ -1,0 +1,410 @@
+// persist_kernels.cuh — N7: the whole SVD_1D loop of one component in ONE persistent kernel.
+//
+// Alg. 2 lines 5-9: repeat { y = X'^T X' v (Eq. 2, factored form F2);
+// v1 = y / ||y||; stop when |v0 . v1| >= 1 - eps }.  The separate-kernel path (N1 gv_fused +
+// N5 fin_iter per iteration) pays two kernel boundaries per iteration (measured ~30 us of
+// transition + ~20 us of finalize on a ~620 us pass).  Here a cooperative grid (one
+// CTA per SM slot, all co-resident) runs every pass of the component:
+//
+//   pass:   stream the CTA's row range through the TMA ring exactly as N1 does (t_r, y += t_r A_r,
+//           w += t_r U_r), flush the per-CTA fp64 partials ypart[b], wpart[b]
+//   sync 1: grid barrier
+//   reduce: CTA b sums a 32-aligned column slice of the partials over all CTAs in a fixed order,
+//           applies the V (S w) correction (every CTA reduces w itself), writes y_new, and its
+//           slice's partial scalars { sum y^2, sum v y, (V^T y)_0..l-1 } -> part[b]
+//   sync 2: grid barrier
+//   decide: every CTA sums part[0..G) in the same fixed order (so every CTA takes the same
+//           decision bit for bit), ||y||, d = |v . y| / ||y||, stop test, c = S V^T v1 for the
+//           next pass; CTA 0 publishes the loop state
+//
+// The producer keeps feeding the ring across pass boundaries (A and the U rows do not change
+// during a component), so the next pass's first S rows are in flight while the grid reduces.
+// The row ranges are walked serpentine (odd passes backwards) when p.serpentine is set.
+// Summation orders are fixed: the result is bitwise reproducible run to run.
+#pragma once
+#include "gram_kernels.cuh"
+
+namespace tsvd {
+
+struct PsParams {
+    const float *A;          // row slab, ld floats per row
+    int64_t ld;
+    int64_t rows;
+    int32_t n, n4;
+    const float *U;          // rows x ldu fp32 (deflation rows staged with every A row)
+    int32_t ldu;
+    int32_t l;               // components already found
+    int32_t u_bytes;         // round4(l) * 4, 0 if l == 0
+    int32_t stages, stage_bytes, row_bytes, run_rows;
+    double *ybuf;            // [2][ystride] fp64 iterates
+    int64_t ystride;
+    LoopState *st;
+    double *c;               // c = S V^T v (in: from the init kernel; out: last value)
+    const double *S;         // sigma[0..l)
+    const double *V;         // n x ldv fp64
+    int32_t ldv;
+    double *ypart;           // [G][ypart_ld]
+    int64_t ypart_ld;
+    double *wpart;           // [G][wpart_ld]
+    int32_t wpart_ld;
+    double *part;            // [G][part_ld] slice scalars
+    int32_t part_ld;
+    unsigned *gbar;          // grid barrier state (2 words, zero-initialised)
+    double eps;
+    int32_t fixed_T, max_iter;
+    int32_t serpentine;
+    unsigned long long *tl;  // debug timeline (TSVD_TIMELINE), same record layout as N1 + N5
+};
+
+constexpr int kPsLanesV = 4;  // (V^T y) accumulators per lane: components l <= 128
+
+template <int T, int NV>
+__global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    constexpr int NW = T / 32;
+    griddep_launch();
+    griddep_wait();
+    LoopState *st = p.st;
+    if (st->stop || st->done) return;  // every CTA reads the same state: uniform exit
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x, b = blockIdx.x;
+    const int S = p.stages, l = p.l;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (size_t)S * p.stage_bytes);
+    double *red = reinterpret_cast<double *>(bars + kMaxStages);  // [2][NW] row dot partials
+    double *cvec = red + 2 * NW;                                   // [l] c = S V^T v
+    double *gvec = cvec + p.wpart_ld;                              // [l] S w
+    double *tot = gvec + p.wpart_ld;                               // [2 + l] decision sums
+    double *gred = tot + 2 + p.wpart_ld;                           // [NW][32] slice reduction
+    double *ys = gred + NW * 32;                                   // [128] y of the column block
+    __shared__ int64_t slot_row[kMaxStages];
+    __shared__ double ny_s;
+    __shared__ int done_s;
+    __shared__ double sred[2][32];
+    // producer state (thread 0 only; kept in shared memory to leave the registers to the row loop):
+    // next row index pk within pass pp of the range [plo, plo + pnr), next ring slot pslot
+    __shared__ int64_t plo, pnr, pk;
+    __shared__ int pp, pslot, pit0;
+
+    const int64_t nr = p.rows * (b + 1) / G - p.rows * b / G;
+    const int it0 = st->it;
+    int it = it0;
+
+    auto feed = [&]() {  // thread 0: next row of the (endless) serpentine sequence into the ring
+        const int64_t k = pk;
+        const int64_t row = (p.serpentine && ((pit0 + pp) & 1)) ? plo + pnr - 1 - k : plo + k;
+        if (k + 1 == pnr) {
+            pk = 0;
+            pp = pp + 1;
+        } else {
+            pk = k + 1;
+        }
+        const int slot = pslot;
+        pslot = slot + 1 == S ? 0 : slot + 1;
+        slot_row[slot] = row;
+        unsigned char *dst = smem + (size_t)slot * p.stage_bytes;
+        mbar_arrive_expect_tx(&bars[slot], (uint32_t)(p.n4 * 16 + (l > 0 ? p.u_bytes : 0)));
+        tma_load_1d(dst, p.A + row * p.ld, (uint32_t)(p.n4 * 16), &bars[slot]);
+        if (l > 0) tma_load_1d(dst + p.row_bytes, p.U + row * p.ldu, (uint32_t)p.u_bytes, &bars[slot]);
+    };
+    if (tid == 0) {
+        plo = p.rows * b / G;
+        pnr = nr;
+        pk = 0;
+        pp = 0;
+        pslot = 0;
+        pit0 = it0;
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        fence_barrier_init();
+        if (nr > 0)
+            for (int s = 0; s < S; ++s) feed();
+    }
+    for (int i = tid; i < l; i += T) cvec[i] = p.c[i];
+    if (tid == 0) ny_s = st->ny;
+    __syncthreads();
+
+    const int tail = p.n & 3;
+    int cs = 0;         // consumer: ring slot of the next row
+    uint32_t cph = 0;   // and the phase to wait for
+    int rb = 0;         // parity of the dot-product scratch
+    double *yp = p.ypart + (int64_t)b * p.ypart_ld;
+    for (;;) {
+        // ---- v = y_cur / ||y_cur|| in registers (fp64 master -> fp32), c for this pass
+        float4 vr[NV];
+        {
+            const double inv = 1.0 / ny_s;
+            const double *ycur = p.ybuf + (int64_t)(it & 1) * p.ystride;
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                const int idx = k * T + tid;
+                const int j = 4 * idx;
+                if (idx >= p.n4) {
+                    vr[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                } else if (j + 3 < p.n) {
+                    const double2 lo2 = __ldcg(reinterpret_cast<const double2 *>(ycur + j));
+                    const double2 hi2 = __ldcg(reinterpret_cast<const double2 *>(ycur + j + 2));
+                    vr[k] = make_float4((float)(lo2.x * inv), (float)(lo2.y * inv), (float)(hi2.x * inv),
+                                        (float)(hi2.y * inv));
+                } else {
+                    vr[k].x = j + 0 < p.n ? (float)(__ldcg(ycur + j + 0) * inv) : 0.f;
+                    vr[k].y = j + 1 < p.n ? (float)(__ldcg(ycur + j + 1) * inv) : 0.f;
+                    vr[k].z = j + 2 < p.n ? (float)(__ldcg(ycur + j + 2) * inv) : 0.f;
+                    vr[k].w = 0.f;
+                }
+            }
+        }
+        const double cval = tid < l ? cvec[tid] : 0.0;
+        if (p.tl && b == 0 && tid == 0) {
+            const unsigned long long idx = atomicAdd(p.tl, 1ull) % 4096;
+            p.tl[2 + kTl * idx] = globaltimer_ns();
+        }
+
+        // ---- the pass over this CTA's rows (N1 body)
+        float4 ya[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) ya[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        double wacc = 0.0;
+        bool flushed = false;
+        auto flush = [&]() {
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                const int idx = k * T + tid;
+                if (idx < p.n4) {
+                    double2 *dst = reinterpret_cast<double2 *>(yp + 4 * (int64_t)idx);
+                    double2 lo2 = make_double2(ya[k].x, ya[k].y), hi2 = make_double2(ya[k].z, ya[k].w);
+                    if (flushed) {
+                        const double2 olo = dst[0], ohi = dst[1];
+                        lo2.x += olo.x; lo2.y += olo.y; hi2.x += ohi.x; hi2.y += ohi.y;
+                    }
+                    dst[0] = lo2;
+                    dst[1] = hi2;
+                }
+                ya[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            flushed = true;
+        };
+        int run = 0;
+        for (int64_t k = 0; k < nr; ++k) {
+            mbar_wait(&bars[cs], cph);
+            const unsigned char *slot = smem + (size_t)cs * p.stage_bytes;
+            const float4 *row = reinterpret_cast<const float4 *>(slot);
+            float4 a[NV];
+            float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
+#pragma unroll
+            for (int kk = 0; kk < NV; ++kk) {
+                const int idx = kk * T + tid;
+                if (idx < p.n4) {
+                    a[kk] = row[idx];
+                    if (tail && idx == p.n4 - 1) {
+                        if (tail < 2) a[kk].y = 0.f;
+                        if (tail < 3) a[kk].z = 0.f;
+                        a[kk].w = 0.f;
+                    }
+                } else {
+                    a[kk] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                q0 = fmaf(a[kk].x, vr[kk].x, q0);
+                q1 = fmaf(a[kk].y, vr[kk].y, q1);
+                q2 = fmaf(a[kk].z, vr[kk].z, q2);
+                q3 = fmaf(a[kk].w, vr[kk].w, q3);
+            }
+            double part = (double)((q0 + q1) + (q2 + q3));
+            float ur = 0.f;
+            if (tid < l) {
+                ur = reinterpret_cast<const float *>(slot + p.row_bytes)[tid];
+                part -= (double)ur * cval;  // - U_r . c
+            }
+            part = warp_sum(part);
+            if (lane == 0) red[rb * NW + warp] = part;
+            __syncthreads();  // dots visible; every thread is done reading the slot
+            if (tid == 0) {
+                fence_proxy_async_smem();
+                feed();  // keeps S rows in flight, across the pass boundary too
+            }
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) t += red[rb * NW + w];
+            rb ^= 1;
+            if (++cs == S) {
+                cs = 0;
+                cph ^= 1u;
+            }
+            const float tf = (float)t;
+#pragma unroll
+            for (int kk = 0; kk < NV; ++kk) {
+                ya[kk].x = fmaf(tf, a[kk].x, ya[kk].x);
+                ya[kk].y = fmaf(tf, a[kk].y, ya[kk].y);
+                ya[kk].z = fmaf(tf, a[kk].z, ya[kk].z);
+                ya[kk].w = fmaf(tf, a[kk].w, ya[kk].w);
+            }
+            if (tid < l) wacc += t * (double)ur;
+            if (++run == p.run_rows) {
+                flush();
+                run = 0;
+            }
+        }
+        flush();
+        if (tid < l) p.wpart[(int64_t)b * p.wpart_ld + tid] = wacc;
+        __threadfence();
+        grid_sync(p.gbar);  // sync 1: every partial is written
+        if (p.tl && b == 0 && tid == 0) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 1] = globaltimer_ns();
+
+        // ---- g = S w (every CTA, fixed order), then this CTA's column slice of y_new
+        for (int i = warp; i < l; i += NW) {
+            double w = 0.0;
+            for (int bb = lane; bb < G; bb += 32) w += __ldcg(p.wpart + (int64_t)bb * p.wpart_ld + i);
+            w = warp_sum(w);
+            if (lane == 0) gvec[i] = p.S[i] * w;
+        }
+        __syncthreads();
+        const double *ycur = p.ybuf + (int64_t)(it & 1) * p.ystride;
+        double *ynew = p.ybuf + (int64_t)((it + 1) & 1) * p.ystride;
+        const double inv = 1.0 / ny_s;
+        const int64_t per = ((p.n + G - 1) / G + 31) / 32 * 32;
+        const int64_t j0 = (int64_t)b * per;
+        const int64_t j1 = (j0 + per) < (int64_t)p.n ? (j0 + per) : (int64_t)p.n;
+        // column blocks of CW columns: PG thread groups sum interleaved subsets of the G partials of
+        // one column each (independent loads, unrolled), group sums added in group order
+        constexpr int CW = T < 128 ? T : 128;
+        constexpr int PG = T / CW;
+        const int cc = tid % CW, cg = tid / CW;
+        double a_yy = 0.0, a_vy = 0.0;
+        double vacc[kPsLanesV];  // (V^T y)_i, i = lane + 32 q, partial over the columns of this warp
+#pragma unroll
+        for (int q = 0; q < kPsLanesV; ++q) vacc[q] = 0.0;
+        for (int64_t c0 = j0; c0 < j1; c0 += CW) {
+            const int64_t j = c0 + cc;
+            double sacc = 0.0;
+            if (j < j1) {
+                const double *col = p.ypart + j;
+#pragma unroll 8
+                for (int bb = cg; bb < G; bb += PG) sacc += __ldcg(col + (int64_t)bb * p.ypart_ld);
+            }
+            gred[cg * CW + cc] = sacc;
+            __syncthreads();
+            if (tid < CW) {
+                double y = 0.0;
+                if (j < j1) {
+                    y = gred[tid];
+#pragma unroll
+                    for (int q = 1; q < PG; ++q) y += gred[q * CW + tid];
+                    const double *Vj = p.V + j * p.ldv;
+                    double corr = 0.0;  // (V (S w))_j
+#pragma unroll 4
+                    for (int i = 0; i < l; ++i) corr += Vj[i] * gvec[i];
+                    y -= corr;
+                    __stcg(ynew + j, y);
+                    a_yy += y * y;
+                    a_vy += (__ldcg(ycur + j) * inv) * y;
+                }
+                ys[tid] = y;
+            }
+            __syncthreads();
+            if (l > 0) {  // warp w: columns w, w + NW, ... of the block; lane: components lane + 32 q
+                const int jn = (int)((j1 - c0) < CW ? (j1 - c0) : CW);
+                for (int jj = warp; jj < jn; jj += NW) {
+                    const double *Vr = p.V + (c0 + jj) * p.ldv;
+                    const double yj = ys[jj];
+#pragma unroll
+                    for (int q = 0; q < kPsLanesV; ++q)
+                        if (lane + 32 * q < l) vacc[q] += Vr[lane + 32 * q] * yj;
+                }
+            }
+            __syncthreads();
+        }
+        double *pp = p.part + (int64_t)b * p.part_ld;
+        {  // block sums in a fixed order: warps (of the CW column threads), then lanes
+            const double yy = warp_sum(a_yy), vy = warp_sum(a_vy);
+            if (lane == 0 && warp < CW / 32) {
+                sred[0][warp] = yy;
+                sred[1][warp] = vy;
+            }
+            __syncthreads();
+            if (tid < 2) {
+                double acc = 0.0;
+                for (int w = 0; w < CW / 32; ++w) acc += sred[tid][w];
+                pp[tid] = acc;
+            }
+#pragma unroll
+            for (int q = 0; q < kPsLanesV; ++q) {
+                if (32 * q >= l) break;
+                __syncthreads();
+                gred[warp * 32 + lane] = vacc[q];
+                __syncthreads();
+                if (tid < 32 && 32 * q + tid < l) {
+                    double acc = 0.0;
+                    for (int w = 0; w < NW; ++w) acc += gred[w * 32 + tid];
+                    pp[2 + 32 * q + tid] = acc;
+                }
+            }
+        }
+        __threadfence();
+        grid_sync(p.gbar);  // sync 2: every slice is written
+
+        // ---- decision: identical in every CTA (same data, same fixed order)
+        for (int q = warp; q < 2 + l; q += NW) {
+            double sq = 0.0;
+            for (int bb = lane; bb < G; bb += 32) sq += __ldcg(p.part + (int64_t)bb * p.part_ld + q);
+            sq = warp_sum(sq);
+            if (lane == 0) tot[q] = sq;
+        }
+        __syncthreads();
+        const int itn = it + 1;
+        if (tid == 0) {
+            const double nyn = sqrt(tot[0]);
+            int done = 0, status = 0;
+            double d = 0.0;
+            if (!isfinite(nyn)) {
+                status = -7;
+                done = 2;
+            } else if (nyn == 0.0) {  // X'^T X' v = 0: rank exhausted (reading R14)
+                status = 2;
+                done = 2;
+            } else {
+                d = fabs(tot[1]) / nyn;  // |v0 . v1| with v1 = y / ||y||
+                if (p.fixed_T > 0) {
+                    if (itn >= p.fixed_T) done = 1;
+                } else if (d >= 1.0 - p.eps) {
+                    done = 1;
+                } else if (itn >= p.max_iter) {
+                    done = 1;
+                    status = 1;
+                }
+            }
+            ny_s = (nyn > 0.0 && isfinite(nyn)) ? nyn : 1.0;
+            done_s = done;
+            if (b == 0) {
+                st->it = itn;
+                if (done < 2) {
+                    st->ny = nyn;
+                    st->d = d;
+                }
+                if (done) {
+                    st->status = status;
+                    st->done = 1;
+                    if (done == 2) st->stop = 1;
+                }
+                if (p.tl) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 2] = globaltimer_ns();
+            }
+        }
+        __syncthreads();
+        for (int i = tid; i < l; i += T) {  // c = S V^T v1 for the next pass
+            cvec[i] = p.S[i] * (tot[2 + i] / ny_s);
+            if (b == 0) p.c[i] = cvec[i];
+        }
+        it = itn;
+        const int done = done_s;
+        __syncthreads();
+        if (done) break;
+    }
+    // drain the S rows fed ahead for a pass that will not run (no bulk copy may outlive the CTA)
+    if (tid == 0 && nr > 0)
+        for (int j = 0; j < S; ++j) {
+            mbar_wait(&bars[cs], cph);
+            if (++cs == S) {
+                cs = 0;
+                cph ^= 1u;
+            }
+        }
+}
+
+}  // namespace tsvd

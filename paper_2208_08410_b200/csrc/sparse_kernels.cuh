@@ -52,6 +52,8 @@ __global__ void __launch_bounds__(kSpThreads) csr_spmv(const SpParams p) {
     extern __shared__ double wsm[];
     __shared__ double sqw[kSpWarps];
     const LoopState *st = p.st;
+    griddep_launch();
+    griddep_wait();
     if (st->stop || (!EXTRACT && st->done)) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int l = EXTRACT ? 0 : p.l;
@@ -98,6 +100,8 @@ __global__ void __launch_bounds__(kSpThreads) csr_spmv(const SpParams p) {
 // N3.
 __global__ void __launch_bounds__(kSpThreads) csc_spmvT(const SpParams p) {
     const LoopState *st = p.st;
+    griddep_launch();
+    griddep_wait();
     if (st->stop || st->done) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t nwarps = (int64_t)gridDim.x * kSpWarps;

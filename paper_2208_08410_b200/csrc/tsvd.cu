@@ -24,6 +24,7 @@
 #include "fin_kernels.cuh"
 #include "gram_kernels.cuh"
 #include "sparse_kernels.cuh"
+#include "persist_kernels.cuh"
 
 using namespace tsvd;
 
@@ -68,6 +69,29 @@ GvFn pick_gv(int T, int nv, int split = 1) {
     case 128: return pick_nv<128, EX, TWO>(nv);
     case 256: return pick_nv<256, EX, TWO>(nv);
     case 512: return pick_nv<512, EX, TWO>(nv);
+    default: return nullptr;
+    }
+}
+
+using PsFn = void (*)(const PsParams);
+
+template <int T>
+PsFn pick_ps_nv(int nv) {
+    switch (nv) {
+    case 1: return gv_persist<T, 1>;
+    case 2: return gv_persist<T, 2>;
+    case 4: return gv_persist<T, 4>;
+    case 8: return gv_persist<T, 8>;
+    default: return nullptr;
+    }
+}
+PsFn pick_ps(int T, int nv) {
+    switch (T) {
+    case 32: return pick_ps_nv<32>(nv);
+    case 64: return pick_ps_nv<64>(nv);
+    case 128: return pick_ps_nv<128>(nv);
+    case 256: return pick_ps_nv<256>(nv);
+    case 512: return pick_ps_nv<512>(nv);
     default: return nullptr;
     }
 }
@@ -159,6 +183,15 @@ struct tsvd_s {
     GvFn gv_two = nullptr;
     float *vprev32 = nullptr;
     bool fused_ext_used = false;
+    int carveout_opt = 1;
+    int pdl_opt = 1;       // TSVD_OPT_PDL
+    int serp_opt = 1;      // TSVD_OPT_ROW_ORDER
+    int persist_opt = 1;   // TSVD_OPT_PERSISTENT
+    PsFn gv_ps = nullptr;  // N7: one persistent cooperative kernel per component (null: unsupported)
+    int S_ps = 0;
+    size_t smem_ps = 0;
+    double ps_ms = 0.0;    // TIMING: event time of the persistent launches, and the passes they ran
+    int64_t ps_passes = 0, ps_launches = 0;  // debug knob TSVD_CARVEOUT=0: leave the driver's per-kernel L1/shared split
     size_t smem = 0;
     GvFn gv = nullptr, gv_ex = nullptr;
     // run graph (cached by starting component)
@@ -215,11 +248,34 @@ static int fin_src(tsvd_t h) {
     return fused_reduce(h) ? SRC_YW : SRC_PARTS;
 }
 
+// Every kernel of the loop asks for the same L1/shared split (maximum shared), so consecutive
+// launches never wait for an SM to drain and re-partition its L1 (measured: the gap between the
+// finalize kernel and the next fused pass).
+template <class F>
+static cudaError_t max_carveout(F *fn) {
+    return cudaFuncSetAttribute((const void *)fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                (int)cudaSharedmemCarveoutMaxShared);
+}
+
 static tsvd_status set_fin_attrs(tsvd_t h) {
     const int fin_dyn = (2 * h->k + 2 + std::max(0, h->k - kVtReg) + kFinThreads) * (int)sizeof(double);
     CK(cudaFuncSetAttribute(fin_iter<SRC_PARTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_dyn));
     CK(cudaFuncSetAttribute(fin_iter<SRC_YW>, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_dyn));
     CK(cudaFuncSetAttribute(fin_iter<SRC_PEER>, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_dyn));
+    if (h->carveout_opt) {
+        CK(max_carveout(fin_iter<SRC_PARTS>));
+        CK(max_carveout(fin_iter<SRC_YW>));
+        CK(max_carveout(fin_iter<SRC_PEER>));
+        CK(max_carveout(publish));
+        CK(max_carveout(reduce_partials));
+        CK(max_carveout(ext_reduce));
+        CK(max_carveout(ext_finish<SRC_PARTS>));
+        CK(max_carveout(ext_finish<SRC_YW>));
+        CK(max_carveout(ext_finish<SRC_PEER>));
+        CK(max_carveout(csr_spmv<false>));
+        CK(max_carveout(csr_spmv<true>));
+        CK(max_carveout(csc_spmvT));
+    }
     return TSVD_OK;
 }
 
@@ -263,6 +319,10 @@ static tsvd_status plan(tsvd_t h) {
     h->gv_ex = pick_gv<true>(T, NV, split);
     CK(cudaFuncSetAttribute(h->gv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem));
     CK(cudaFuncSetAttribute(h->gv_ex, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem));
+    if (h->carveout_opt) {
+        CK(max_carveout(h->gv));
+        CK(max_carveout(h->gv_ex));
+    }
     if (split == 2) {
         CK(cudaFuncSetAttribute(h->gv, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
         CK(cudaFuncSetAttribute(h->gv_ex, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
@@ -287,26 +347,67 @@ static tsvd_status plan(tsvd_t h) {
                           4 * (T / 32) * sizeof(double);
             h->gv_two = pick_gv<false, true>(T, NV);
             CK(cudaFuncSetAttribute(h->gv_two, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_two));
+            if (h->carveout_opt) CK(max_carveout(h->gv_two));
+        }
+    }
+    // persistent per-component kernel: same ring, plus the reduction scratch; every CTA of the grid
+    // must be co-resident (cooperative launch), and (V^T y)_i is owned by thread i (k <= T + 1)
+    h->gv_ps = nullptr;
+    if (split == 1 && h->k <= 32 * kPsLanesV + 1) {
+        const int64_t extra = kMaxStages * 8 + (int64_t)(2 * (T / 32) + 3 * h->kpad + 2 + (T / 32) * 32 + 128) * 8;
+        int Sp = S;
+        while (Sp > 2 && ((int64_t)Sp * h->stage_bytes + extra) * h->cps > kSmemBudget) --Sp;
+        PsFn fn = pick_ps(T, NV);
+        if (fn && ((int64_t)Sp * h->stage_bytes + extra) * h->cps <= kSmemBudget) {
+            const size_t sm = (size_t)Sp * h->stage_bytes + (size_t)extra;
+            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            if (h->carveout_opt) CK(max_carveout(fn));
+            int occ_ps = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_ps, fn, T, sm));
+            if (occ_ps * h->sms >= h->grid) {
+                h->gv_ps = fn;
+                h->S_ps = Sp;
+                h->smem_ps = sm;
+            }
         }
     }
     return TSVD_OK;
 }
 
-// cluster launch of the split kernel (2 CTAs per row range)
-static cudaError_t launch_split(tsvd_t h, GvFn fn, const GvParams &p, cudaStream_t s) {
+// Kernel launch with programmatic dependent launch (PDL) when enabled: the kernel may be scheduled
+// while its predecessor drains (every kernel of the loop calls griddep_wait() before it reads
+// anything), which hides the launch latency between the fused pass and the finalize kernel.
+// cluster > 1: thread-block cluster of that many CTAs (the split kernel).
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(tsvd_t h, void (*fn)(KArgs...), int grid, int block, size_t smem, cudaStream_t s,
+                            int cluster, Args &&...args) {
     cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(h->grid);
-    cfg.blockDim = dim3(h->T);
-    cfg.dynamicSmemBytes = h->smem;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (h->pdl_opt) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (cluster > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = cluster;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, fn, p);
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, fn, std::forward<Args>(args)...);
+}
+
+// the fused pass: one CTA per row range, or a 2-CTA cluster per row range (split)
+static cudaError_t launch_n1(tsvd_t h, GvFn fn, const GvParams &p, cudaStream_t s) {
+    return launch_k(h, fn, h->grid, h->T, h->smem, s, h->split, p);
 }
 
 // Fresh loop state; the peer-collective epoch is kept (flags in peer memory are monotone).
@@ -346,7 +447,7 @@ static tsvd_status ensure_alloc(tsvd_t h) {
     if (!e) e = dm((void **)&h->c64, (size_t)h->kpad * sizeof(double));
     if (!e && !h->sparse) e = dm((void **)&h->ypart, (size_t)h->parts * h->ypart_ld * sizeof(double));
     if (!e) e = dm((void **)&h->wpart, (size_t)h->parts * h->kpad * sizeof(double));
-    if (!e) e = dm((void **)&h->part, (size_t)h->fin_blocks * h->part_ld * sizeof(double));
+    if (!e) e = dm((void **)&h->part, (size_t)std::max(h->fin_blocks, h->grid) * h->part_ld * sizeof(double));
     if (!e) e = dm((void **)&h->u64, (size_t)mg * sizeof(double));
     if (!e) e = dm((void **)&h->sq_part, (size_t)h->parts * sizeof(double));
     if (!e) e = dm((void **)&h->sig2, sizeof(double));
@@ -367,8 +468,8 @@ static tsvd_status ensure_alloc(tsvd_t h) {
         h->trace_f = fopen(name, "a");
     }
     if (!e && getenv("TSVD_TIMELINE")) {
-        e = dm((void **)&h->tl_d, (2 + 3 * 4096) * sizeof(unsigned long long));
-        if (!e) e = cudaMemsetAsync(h->tl_d, 0, (2 + 3 * 4096) * sizeof(unsigned long long), h->stream);
+        e = dm((void **)&h->tl_d, (2 + kTl * 4096) * sizeof(unsigned long long));
+        if (!e) e = cudaMemsetAsync(h->tl_d, 0, (2 + kTl * 4096) * sizeof(unsigned long long), h->stream);
     }
     if (!e) e = cudaMallocHost((void **)&h->st_host, sizeof(LoopState));
     if (!e) e = cudaMallocHost((void **)&h->stats_host, (size_t)h->k * sizeof(CompStat));
@@ -568,6 +669,7 @@ static GvParams gv_params(tsvd_t h, int l, bool extract) {
     p.trace = extract ? nullptr : h->trace_d;
     p.dynamic = h->dynamic_opt;
     p.chunk_rows = (int32_t)std::max<int64_t>(1, (256 << 10) / h->row_bytes);
+    p.serpentine = h->serp_opt && !h->streaming;
     p.work = h->work;
     p.tl = extract ? nullptr : h->tl_d;
     return p;
@@ -608,11 +710,11 @@ static SpParams sp_params(tsvd_t h, int l) {
 static tsvd_status launch_sparse(tsvd_t h, cudaStream_t s, int l, bool extract) {
     const SpParams p = sp_params(h, l);
     if (extract) {
-        csr_spmv<true><<<h->grid, kSpThreads, 0, s>>>(p);
+        CK(launch_k(h, csr_spmv<true>, h->grid, kSpThreads, 0, s, 1, p));
     } else {
-        csr_spmv<false><<<h->grid, kSpThreads, (size_t)kSpWarps * std::max(l, 1) * sizeof(double), s>>>(p);
-        CK(cudaGetLastError());
-        csc_spmvT<<<h->grid, kSpThreads, 0, s>>>(p);
+        CK(launch_k(h, csr_spmv<false>, h->grid, kSpThreads, (size_t)kSpWarps * std::max(l, 1) * sizeof(double), s, 1,
+                    p));
+        CK(launch_k(h, csc_spmvT, h->grid, kSpThreads, 0, s, 1, p));
     }
     CK(cudaGetLastError());
     return TSVD_OK;
@@ -636,11 +738,7 @@ static tsvd_status launch_gv(tsvd_t h, cudaStream_t s, int l, bool extract) {
         CK(cudaLaunchKernelEx(&cfg, fn, p));
         return TSVD_OK;
     }
-    if (!h->streaming || h->m_res > 0) {
-        if (h->split == 2) CK(launch_split(h, fn, p, s));
-        else fn<<<h->grid, h->T, h->smem, s>>>(p);
-        CK(cudaGetLastError());
-    }
+    if (!h->streaming || h->m_res > 0) CK(launch_n1(h, fn, p, s));
     if (!h->streaming) return TSVD_OK;
     const int64_t row_bytes = (int64_t)h->row_bytes;
     int b = 0;
@@ -659,9 +757,7 @@ static tsvd_status launch_gv(tsvd_t h, cudaStream_t s, int l, bool extract) {
         q.U = h->U32 + r0 * h->kpad;
         q.u_out = h->u64 + r0;
         q.accumulate = (r0 > 0 || h->m_res > 0) ? 1 : 0;
-        if (h->split == 2) CK(launch_split(h, fn, q, s));
-        else fn<<<h->grid, h->T, h->smem, s>>>(q);
-        CK(cudaGetLastError());
+        CK(launch_n1(h, fn, q, s));
         CK(cudaEventRecord(h->ev_free[slot], s));
         h->streamed_bytes += rows * h->n * (int64_t)sizeof(float);
         h->streamed_batches += 1;
@@ -714,9 +810,9 @@ static FinParams fin_params(tsvd_t h, int mode, int l, const double *xsrc, unsig
 static tsvd_status launch_fin(tsvd_t h, cudaStream_t s, const FinParams &p, int src) {
     const size_t dyn = (size_t)(2 * p.l + 2 + std::max(0, p.l - kVtReg) + kFinThreads) * sizeof(double);
     switch (src) {
-    case SRC_PARTS: fin_iter<SRC_PARTS><<<h->fin_blocks, kFinThreads, dyn, s>>>(p); break;
-    case SRC_YW: fin_iter<SRC_YW><<<h->fin_blocks, kFinThreads, dyn, s>>>(p); break;
-    default: fin_iter<SRC_PEER><<<h->fin_blocks, kFinThreads, dyn, s>>>(p); break;
+    case SRC_PARTS: CK(launch_k(h, fin_iter<SRC_PARTS>, h->fin_blocks, kFinThreads, dyn, s, 1, p)); break;
+    case SRC_YW: CK(launch_k(h, fin_iter<SRC_YW>, h->fin_blocks, kFinThreads, dyn, s, 1, p)); break;
+    default: CK(launch_k(h, fin_iter<SRC_PEER>, h->fin_blocks, kFinThreads, dyn, s, 1, p)); break;
     }
     CK(cudaGetLastError());
     return TSVD_OK;
@@ -750,12 +846,11 @@ static tsvd_status launch_exchange(tsvd_t h, cudaStream_t s, int l) {
         return TSVD_OK;
     }
     if (h->coll == COLL_PEER) {
-        publish<<<h->fin_blocks, kFinThreads, 0, s>>>(pub_params(h, 0, l));
-        CK(cudaGetLastError());
+        CK(launch_k(h, publish, h->fin_blocks, kFinThreads, 0, s, 1, pub_params(h, 0, l)));
     } else if (h->coll == COLL_NCCL) {
-        reduce_partials<<<h->fin_blocks, kFinThreads, 0, s>>>(h->ypart, h->parts, h->ypart_ld, (int)h->n, h->wpart,
-                                                              h->kpad, l, h->yw, h->wofs, h->st);
-        CK(cudaGetLastError());
+        CK(launch_k(h, reduce_partials, h->fin_blocks, kFinThreads, 0, s, 1, (const double *)h->ypart, h->parts,
+                    h->ypart_ld, (int)h->n, (const double *)h->wpart, (int)h->kpad, l, h->yw, h->wofs,
+                    (const LoopState *)h->st));
         NK(ncclAllReduce(h->yw, h->yw, (size_t)(h->wofs + h->kpad), ncclDouble, ncclSum, h->comm, s));
     }
     return TSVD_OK;
@@ -802,16 +897,71 @@ static tsvd_status launch_fused_first(tsvd_t h, cudaStream_t s, int l, cudaEvent
     p.reduce_mode = 0;
     p.tl = nullptr;
     p.trace = nullptr;
-    h->gv_two<<<h->grid, h->T, h->smem_two, s>>>(p);
-    CK(cudaGetLastError());
+    CK(launch_k(h, h->gv_two, h->grid, h->T, h->smem_two, s, 1, p));
     if (e1) CK(cudaEventRecord(e1, s));
     if (h->coll == COLL_PEER) {
         PubParams q = pub_params(h, 0, l);
         q.with_sq = 1;
-        publish<<<h->fin_blocks, kFinThreads, 0, s>>>(q);
-        CK(cudaGetLastError());
+        CK(launch_k(h, publish, h->fin_blocks, kFinThreads, 0, s, 1, q));
     }
     return launch_fin(h, s, fin_params(h, FIN_ITERATE_EXT, l, nullptr, 0ull, 0), fin_src(h));
+}
+
+// N7: the iterations of component l after the first (or all of them), in one cooperative launch.
+static bool use_persist(tsvd_t h) {
+    return h->persist_opt && h->gv_ps && !h->sparse && !h->streaming && h->split == 1 && h->coll == COLL_NONE &&
+           !fused_reduce(h) && h->dynamic_opt == 0;
+}
+
+static tsvd_status launch_persist(tsvd_t h, cudaStream_t s, int l, cudaEvent_t e0 = nullptr,
+                                  cudaEvent_t e1 = nullptr) {
+    PsParams p{};
+    p.A = h->A_use;
+    p.ld = h->ld_use;
+    p.rows = h->m_res;
+    p.n = (int32_t)h->n;
+    p.n4 = (int32_t)((h->n + 3) / 4);
+    p.U = h->U32;
+    p.ldu = h->kpad;
+    p.l = l;
+    p.u_bytes = l == 0 ? 0 : (int32_t)(round_up(l, 4) * 4);
+    p.stages = h->S_ps;
+    p.stage_bytes = h->stage_bytes;
+    p.row_bytes = h->row_bytes;
+    p.run_rows = h->run_rows;
+    p.ybuf = h->ybuf;
+    p.ystride = h->ystride;
+    p.st = h->st;
+    p.c = h->c64;
+    p.S = h->S64;
+    p.V = h->V64;
+    p.ldv = h->k;
+    p.ypart = h->ypart;
+    p.ypart_ld = h->ypart_ld;
+    p.wpart = h->wpart;
+    p.wpart_ld = h->kpad;
+    p.part = h->part;
+    p.part_ld = h->part_ld;
+    p.gbar = h->gbar;
+    p.eps = h->eps;
+    p.fixed_T = h->fixed_T;
+    p.max_iter = h->max_iter;
+    p.serpentine = h->serp_opt;
+    p.tl = h->tl_d;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident: grid barriers inside
+    attr[0].val.cooperative = 1;
+    cfg.gridDim = dim3(h->grid);
+    cfg.blockDim = dim3(h->T);
+    cfg.dynamicSmemBytes = h->smem_ps;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (e0) CK(cudaEventRecord(e0, s));
+    CK(cudaLaunchKernelEx(&cfg, h->gv_ps, p));
+    if (e1) CK(cudaEventRecord(e1, s));
+    return TSVD_OK;
 }
 
 static tsvd_status launch_extract(tsvd_t h, cudaStream_t s, int l) {
@@ -837,14 +987,13 @@ static tsvd_status launch_extract(tsvd_t h, cudaStream_t s, int l) {
     const int64_t work = std::max<int64_t>(h->m_g, h->n);
     const int blocks = (int)std::min<int64_t>((work + 255) / 256, (int64_t)h->sms * 8);
     if (h->coll == COLL_NONE) {
-        ext_finish<SRC_PARTS><<<blocks, 256, 0, s>>>(p);
+        CK(launch_k(h, ext_finish<SRC_PARTS>, blocks, 256, 0, s, 1, p));
     } else if (h->coll == COLL_PEER) {
-        publish<<<1, kFinThreads, 0, s>>>(pub_params(h, 1, l));
-        CK(cudaGetLastError());
-        ext_finish<SRC_PEER><<<blocks, 256, 0, s>>>(p);
+        CK(launch_k(h, publish, 1, kFinThreads, 0, s, 1, pub_params(h, 1, l)));
+        CK(launch_k(h, ext_finish<SRC_PEER>, blocks, 256, 0, s, 1, p));
     } else {
-        ext_reduce<<<1, 32, 0, s>>>(h->sq_part, h->parts, h->sig2, h->st);
-        CK(cudaGetLastError());
+        CK(launch_k(h, ext_reduce, 1, 32, 0, s, 1, (const double *)h->sq_part, h->parts, h->sig2,
+                    (const LoopState *)h->st));
         NK(ncclAllReduce(h->sig2, h->sig2, 1, ncclDouble, ncclSum, h->comm, s));
         ext_finish<SRC_YW><<<blocks, 256, 0, s>>>(p);
     }
@@ -895,6 +1044,7 @@ static tsvd_status build_graph(tsvd_t h, int l0) {
     tsvd_status s = TSVD_OK;
     cudaError_t ce = cudaSuccess;
     const bool fx = fuse_ext(h);
+    const bool ps = use_persist(h);
     for (int l = l0; l < h->k && s >= 0 && ce == cudaSuccess; ++l) {
         if (fx && l > l0) {  // extraction of l-1 rides on the first iteration of l
             s = launch_init_ext(h, h->stream, l);
@@ -903,6 +1053,12 @@ static tsvd_status build_graph(tsvd_t h, int l0) {
             s = launch_init(h, h->stream, l);
         }
         if (s < 0) break;
+        if (ps) {  // the iteration loop is one persistent kernel: no conditional node needed
+            s = launch_persist(h, h->stream, l);
+            if (s < 0) break;
+            if (!fx || l == h->k - 1) s = launch_extract(h, h->stream, l);
+            continue;
+        }
         cudaStreamCaptureStatus cs;
         cudaGraph_t g = nullptr;
         const cudaGraphNode_t *deps = nullptr;
@@ -961,10 +1117,28 @@ static tsvd_status run_host_loop(tsvd_t h, int l0) {
         CK(cudaEventCreate(&e1));
     }
     const bool fx = fuse_ext(h);
+    const bool ps = use_persist(h);
     for (int l = l0; l < h->k; ++l) {
         const bool fused_first = fx && l > l0;
         if (fused_first) TRY(launch_init_ext(h, h->stream, l));
         else TRY(launch_init(h, h->stream, l));
+        if (ps) {  // fused first pass (if any), then the remaining iterations in one launch
+            if (fused_first) TRY(launch_fused_first(h, h->stream, l));
+            TRY(launch_persist(h, h->stream, l, e0, e1));
+            CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            if (h->timing) {
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, e0, e1));
+                h->ps_ms += ms;
+                h->ps_launches += 1;
+            }
+            if (!fx || l == h->k - 1) TRY(launch_extract(h, h->stream, l));
+            CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            if (h->st_host->stop) break;
+            continue;
+        }
         for (int pass = 0;; ++pass) {
             if (fused_first && pass == 0) TRY(launch_fused_first(h, h->stream, l, e0, e1));
             else TRY(launch_iteration(h, h->stream, l, 0ull, 0, e0, e1));
@@ -1035,6 +1209,7 @@ tsvd_status tsvd_create(tsvd_t *out, int64_t m, int64_t n, int32_t k, double eps
     h->m_g = m;
     h->iters.assign(h->k, 0);
     h->dots.assign(h->k, 0.0);
+    if (const char *c = getenv("TSVD_CARVEOUT")) h->carveout_opt = atoi(c);
     cudaError_t e = cudaGetDevice(&h->dev);
     if (!e) e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->dev);
     if (!e) e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
@@ -1134,6 +1309,15 @@ tsvd_status tsvd_set_option(tsvd_t h, int32_t key, int64_t value) {
         break;
     case TSVD_OPT_FUSED_EXTRACT:
         h->fuse_ext_opt = value != 0;
+        break;
+    case TSVD_OPT_PDL:
+        h->pdl_opt = value != 0;
+        break;
+    case TSVD_OPT_ROW_ORDER:
+        h->serp_opt = value != 0;
+        break;
+    case TSVD_OPT_PERSISTENT:
+        h->persist_opt = value != 0;
         break;
     case TSVD_OPT_PLACEMENT:
     case TSVD_OPT_RESIDENT_BYTES:
@@ -1374,6 +1558,9 @@ tsvd_status tsvd_run(tsvd_t h) {
     TRY(upload_v0(h));
     h->n1_ms = 0.0;
     h->n1_launches = 0;
+    h->ps_ms = 0.0;
+    h->ps_launches = 0;
+    h->ps_passes = 0;
     h->total_iters = 0;
     h->launches = 0;
     const int l0 = h->l_found;
@@ -1391,7 +1578,7 @@ tsvd_status tsvd_run(tsvd_t h) {
         if (!h->exec || h->graph_l0 != l0) gs = build_graph(h, l0);
         if (gs >= 0) {
             CK(cudaGraphLaunch(h->exec, h->stream));
-            h->loop_mode = "graph-while";
+            h->loop_mode = use_persist(h) ? "graph-persistent" : "graph-while";
             ran = true;
         } else {
             h->graph_error = h->err;  // fall back to the host loop, keep the reason for the report
@@ -1399,6 +1586,7 @@ tsvd_status tsvd_run(tsvd_t h) {
         }
     }
     if (!ran) TRY(run_host_loop(h, l0));
+    if (!ran && use_persist(h)) h->loop_mode = h->timing ? "host-persistent+events" : "host-persistent";
     CK(cudaMemcpyAsync(h->stats_host, h->stats, (size_t)h->k * sizeof(CompStat), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
@@ -1422,7 +1610,9 @@ tsvd_status tsvd_run(tsvd_t h) {
         const int64_t issued = h->loop_mode == "graph-while"
                                    ? std::max<int64_t>(1, (body_it + h->unroll - 1) / h->unroll) * h->unroll
                                    : body_it;
-        h->launches += 1 + (ff ? per_iter : 0) + per_iter * issued +
+        const bool ps = use_persist(h);
+        if (ps) h->ps_passes += body_it;
+        h->launches += 1 + (ff ? per_iter : 0) + (ps ? 1 : per_iter * issued) +
                        (!h->fused_ext_used || l == h->k - 1 ? per_ext : 0);
         if (cs.status == -7) return h->fail(TSVD_ERR_NUMERIC, "non-finite value or zero initial vector at component %d", l);
         if (!cs.valid || cs.status == 2) {
@@ -1436,8 +1626,9 @@ tsvd_status tsvd_run(tsvd_t h) {
         h->l_found = l + 1;
         h->k_found = l + 1;
     }
-    if (h->tl_d) {  // debug timeline dump: iteration, N1 start, N1 end, fin end (ns, relative)
-        std::vector<unsigned long long> tl(2 + 3 * 4096);
+    if (h->tl_d) {  // debug timeline dump: iteration, N1 start, N1 end, fin end, fin start, fin tail,
+                    // first N1 CTA out (ns, relative; -1 = not recorded)
+        std::vector<unsigned long long> tl(2 + kTl * 4096);
         CK(cudaMemcpy(tl.data(), h->tl_d, tl.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
         char name[1024];
         snprintf(name, sizeof name, "%s.rank%d", getenv("TSVD_TIMELINE"), h->rank);
@@ -1445,8 +1636,12 @@ tsvd_status tsvd_run(tsvd_t h) {
             const int64_t cnt = std::min<int64_t>((int64_t)tl[0], 4096);
             const unsigned long long base = cnt ? tl[2] : 0;
             for (int64_t i = 0; i < cnt; ++i)
-                fprintf(f, "%lld,%lld,%lld,%lld\n", (long long)i, (long long)(tl[2 + 3 * i] - base),
-                        (long long)(tl[3 + 3 * i] - base), (long long)(tl[4 + 3 * i] - base));
+            {
+                const unsigned long long *r = tl.data() + 2 + kTl * i;
+                auto rel = [&](unsigned long long t) { return t ? (long long)(t - base) : -1ll; };
+                fprintf(f, "%lld,%lld,%lld,%lld,%lld,%lld,%lld\n", (long long)i, rel(r[0]), rel(r[1]), rel(r[2]),
+                        rel(r[3]), rel(r[4]), rel(r[5]));
+            }
             fclose(f);
         }
         CK(cudaMemsetAsync(h->tl_d, 0, tl.size() * sizeof(unsigned long long), h->stream));
@@ -1504,10 +1699,17 @@ tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
              (long long)h->n1_launches, (long long)h->launches, h->loop_mode.c_str(), colls[h->coll]);
     s += tmp;
     snprintf(tmp, sizeof tmp,
+             "\"persistent\": {\"enabled\": %s, \"stages\": %d, \"smem\": %zu, \"ms\": %.6f, \"launches\": %lld, "
+             "\"passes\": %lld}, ",
+             use_persist(h) ? "true" : "false", h->S_ps, h->smem_ps, h->ps_ms, (long long)h->ps_launches,
+             (long long)h->ps_passes);
+    s += tmp;
+    snprintf(tmp, sizeof tmp,
              "\"plan\": {\"T\": %d, \"NV\": %d, \"stages\": %d, \"ctas_per_sm\": %d, \"grid\": %d, \"smem\": %zu, "
-             "\"stage_bytes\": %d, \"run_rows\": %d, \"split\": %d, \"fused_extract\": %s}, ",
+             "\"stage_bytes\": %d, \"run_rows\": %d, \"split\": %d, \"fused_extract\": %s, \"pdl\": %s, \"serpentine\": %s}, ",
              h->T, h->NV, h->S, h->cps, h->grid, h->smem, h->stage_bytes, h->run_rows, h->split,
-             h->fused_ext_used ? "true" : "false");
+             h->fused_ext_used ? "true" : "false", h->pdl_opt ? "true" : "false",
+             h->serp_opt && !h->streaming ? "true" : "false");
     s += tmp;
     snprintf(tmp, sizeof tmp,
              "\"placement\": {\"streaming\": %s, \"resident_rows\": %lld, \"batch_rows\": %lld, \"queue_depth\": %d, "

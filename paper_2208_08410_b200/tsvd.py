@@ -30,6 +30,9 @@ OPT_FUSED_REDUCE = 13  # 1: N1 reduces its own partials (cooperative launch); 0:
 OPT_DETERMINISTIC = 14  # 1: static row split, bitwise reproducible (default); 0: dynamic row chunks
 OPT_GRAPH_UNROLL = 15  # iterations per CUDA-graph WHILE body (default 2)
 OPT_FUSED_EXTRACT = 16  # 1 (default): extraction of l-1 fused into the first pass of component l
+OPT_PDL = 17  # 1 (default): programmatic dependent launch between the loop's kernels
+OPT_ROW_ORDER = 18  # 1 (default): serpentine row order (odd iterations backwards, L2 reuse); 0 forward
+OPT_PERSISTENT = 19  # 1 (default): a component's iterations in one cooperative kernel (single GPU)
 F32, ROW_MAJOR = 0, 0
 
 _lib = None

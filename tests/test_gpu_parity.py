@@ -112,7 +112,7 @@ def test_c1_parity():
     assert rc == P.OK
     _assert_parity(A, ref, U, S, V, kf, k)
     assert np.all(np.abs(iters - ref.iters) <= 1), (iters, ref.iters)
-    assert rep["loop"] == "graph-while"
+    assert rep["loop"] == "graph-persistent" and rep["persistent"]["enabled"]
 
 
 @pytest.mark.parametrize("m,n,k,fam", [(1000, 300, 5, "qr"), (333, 333, 4, "qr"), (5000, 4099, 3, "qr"),
@@ -211,7 +211,57 @@ def test_graph_and_host_loops_bitwise_equal():
         np.testing.assert_array_equal(a[1], x[1])
         np.testing.assert_array_equal(a[2], x[2])
         np.testing.assert_array_equal(a[3], x[3])
-    assert c[7]["n1_launches"] == int(np.sum(c[5]))
+    # TIMING: events around every persistent launch (one per component); its passes are the
+    # iterations after each component's fused first pass
+    assert c[7]["persistent"]["launches"] == k
+    assert c[7]["persistent"]["passes"] == int(np.sum(c[5])) - (k - 1)
+
+
+@pytest.mark.parametrize("m,n,k,T", [(2000, 500, 5, 0), (1500, 400, 3, 1), (1500, 400, 3, 2), (4200, 4099, 3, 0),
+                                     (700, 64, 1, 0), (5, 3, 2, 0), (100, 37, 4, 3), (16500, 16384, 2, 3)])
+def test_persistent_matches_per_iteration_kernels(m, n, k, T):
+    """PERSISTENT=1 (all iterations of a component in one cooperative kernel: grid barriers, in-kernel
+    column-slice reduction and stop test) against PERSISTENT=0 (one fused pass + finalize kernel per
+    iteration) and the oracle: same iteration counts (+-1 where the stop test is near its threshold),
+    sigma to summation-order rounding; host loop and graph bitwise equal.  (5, 3): fewer rows than
+    CTAs, most CTAs own no row and only take part in the barriers."""
+    fam = min(n, 48)
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(fam, 5.0, 0.75), seed=m + 3 * k)
+    V0 = synth.v0_normal(n, k, seed=k + 5)
+    opts = {"fixed_iters": T} if T else {}
+    ref = oracle.tsvd(A, k, 1e-6, V0, fixed_T=T)
+    on = _gpu_tsvd(A, k, 1e-6, V0, persistent=1, **opts)
+    off = _gpu_tsvd(A, k, 1e-6, V0, persistent=0, **opts)
+    host = _gpu_tsvd(A, k, 1e-6, V0, persistent=1, graph=0, **opts)
+    assert on[7]["persistent"]["enabled"] and not off[7]["persistent"]["enabled"]
+    for r in (on, off, host):
+        assert r[0] == P.OK
+        _assert_parity(A, ref, *r[1:5], k)
+    assert np.all(np.abs(on[5] - off[5]) <= 1), (on[5], off[5])
+    if T:
+        assert list(on[5]) == [T] * k
+    np.testing.assert_allclose(on[2], off[2], rtol=2e-6)
+    for i in (1, 2, 3):
+        np.testing.assert_array_equal(on[i], host[i])
+
+
+def test_persistent_bitwise_reproducible_and_resume():
+    m, n, k = 3000, 700, 4
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(64, 3.0, 0.8), seed=77)
+    V0 = synth.v0_normal(n, k, seed=77)
+    a = _gpu_tsvd(A, k, 1e-8, V0)
+    b = _gpu_tsvd(A, k, 1e-8, V0)
+    for i in (1, 2, 3, 5):
+        np.testing.assert_array_equal(a[i], b[i])
+    t = P.TSVD(m, n, k, 1e-8)
+    t.set_init(V0)
+    t.set_dense(torch.from_numpy(A).cuda())
+    t.set_factors(a[1][:, :1], a[2][:1], a[3][:, :1].astype(np.float64))
+    t.run()
+    U2, S2, V2 = t.result()
+    assert t.report()["persistent"]["enabled"]
+    t.close()
+    np.testing.assert_allclose(S2[1:], a[2][1:], rtol=1e-6)
 
 
 def test_run_rows_flush_and_ctas():
