@@ -39,10 +39,22 @@ struct LoopState {
     uint32_t counter;      // arrivals of the last-block-done reductions (returns to 0 after use)
     uint32_t epoch;        // peer-collective epoch: identical on all ranks, monotone across runs
     uint32_t pub_counter;  // arrivals of publish_partials
-    int32_t pad;
+    uint32_t xepoch;       // persistent kernel's peer exchange: passes exchanged so far (identical
+                           // on all ranks, monotone across runs)
 };
 
 constexpr int kMaxRanks = 8;
+
+// Persistent kernel's cross-rank exchange (N7, world > 1): every rank owns a receive area
+// [2 parity][world src][G slices][SL elements]; an element is one double sent with the
+// low-latency protocol (two 8-byte words, each half of the value + the pass stamp).  CTA b pushes
+// its local column-slice sums (and the local w) into slice b of every rank.
+struct PxView {
+    ulonglong2 *rbuf[kMaxRanks];  // rank r's receive area (IPC-mapped; [rank] is local)
+    const ulonglong2 *lbuf;       // this rank's receive area
+    int world, rank, G;
+    int per, SL;                  // slice width (columns), slice stride (per + w slots, elements)
+};
 
 // Peer view of the symmetric reduction buffers (multi-GPU, NVLink peer memory).
 struct PeerView {

@@ -54,9 +54,52 @@ struct PsParams {
     int32_t fixed_T, max_iter;
     int32_t serpentine;
     unsigned long long *tl;  // debug timeline (TSVD_TIMELINE), same record layout as N1 + N5
+    PxView px;               // world > 1: NVLink peer exchange of the column slices (one block)
 };
 
 constexpr int kPsLanesV = 4;  // (V^T y) accumulators per lane: components l <= 128
+
+// sum_{b = first, first + step, ... < count} base[b * ld], in that order, with U loads in flight at a
+// time (these reductions are L2-latency bound: one round trip per batch instead of per element)
+template <int U>
+__device__ __forceinline__ double strided_sum(const double *base, int64_t ld, int first, int step, int count) {
+    double acc = 0.0;
+    for (int b0 = first; b0 < count; b0 += U * step) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int bb = b0 + u * step;
+            v[u] = bb < count ? __ldcg(base + (int64_t)bb * ld) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (b0 + u * step < count) acc += v[u];
+    }
+    return acc;
+}
+
+// Low-latency exchange word pair: {lo32 | stamp << 32, hi32 | stamp << 32}.  Each 8-byte word is
+// written and read single-copy atomically, so a word whose stamp matches carries the right half.
+__device__ __forceinline__ void ll_send(ulonglong2 *dst, unsigned stamp, double x) {
+    const unsigned long long s = (unsigned long long)stamp << 32;
+    const unsigned long long a = s | (unsigned)__double2loint(x), b = s | (unsigned)__double2hiint(x);
+    asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(dst), "l"(a), "l"(b) : "memory");
+}
+// Poll until both words carry `stamp`; after 30 s mark the run failed (status -6) and return 0.
+__device__ __forceinline__ double ll_recv(const ulonglong2 *src, unsigned stamp, unsigned long long t0,
+                                         LoopState *st) {
+    for (unsigned spin = 0;; ++spin) {
+        unsigned long long a, b;
+        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(src) : "memory");
+        if ((unsigned)(a >> 32) == stamp && (unsigned)(b >> 32) == stamp)
+            return __hiloint2double((int)(unsigned)b, (int)(unsigned)a);
+        if ((spin & 1023) == 1023 && globaltimer_ns() - t0 > 30000000000ull) {  // a rank did not arrive
+            st->status = -6;
+            st->stop = 1;
+            return 0.0;
+        }
+    }
+}
 
 template <int T, int NV>
 __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
@@ -88,6 +131,7 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
     const int64_t nr = p.rows * (b + 1) / G - p.rows * b / G;
     const int it0 = st->it;
     int it = it0;
+    unsigned xe = st->xepoch;  // world > 1: exchanges done so far (flag values are xe + 1)
 
     auto feed = [&]() {  // thread 0: next row of the (endless) serpentine sequence into the ring
         const int64_t k = pk;
@@ -248,19 +292,22 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
         grid_sync(p.gbar);  // sync 1: every partial is written
         if (p.tl && b == 0 && tid == 0) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 1] = globaltimer_ns();
 
-        // ---- g = S w (every CTA, fixed order), then this CTA's column slice of y_new
+        // ---- g = S w (every CTA, fixed order), then this CTA's column slice of y_new.  world > 1:
+        // gvec holds the local w until the exchange has delivered every rank's
+        const bool multi = p.px.world > 1;
         for (int i = warp; i < l; i += NW) {
-            double w = 0.0;
-            for (int bb = lane; bb < G; bb += 32) w += __ldcg(p.wpart + (int64_t)bb * p.wpart_ld + i);
-            w = warp_sum(w);
-            if (lane == 0) gvec[i] = p.S[i] * w;
+            const double w = warp_sum(strided_sum<8>(p.wpart + i, p.wpart_ld, lane, 32, G));
+            if (lane == 0) gvec[i] = multi ? w : p.S[i] * w;
         }
         __syncthreads();
         const double *ycur = p.ybuf + (int64_t)(it & 1) * p.ystride;
         double *ynew = p.ybuf + (int64_t)((it + 1) & 1) * p.ystride;
         const double inv = 1.0 / ny_s;
-        const int64_t per = ((p.n + G - 1) / G + 31) / 32 * 32;
-        const int64_t j0 = (int64_t)b * per;
+        // column slices: G of them (world > 1: px.G, the smallest grid of any rank, so that every
+        // rank cuts the columns the same way)
+        const int Gs = multi ? p.px.G : G;
+        const int64_t per = ((p.n + Gs - 1) / Gs + 31) / 32 * 32;
+        const int64_t j0 = b < Gs ? (int64_t)b * per : (int64_t)p.n;
         const int64_t j1 = (j0 + per) < (int64_t)p.n ? (j0 + per) : (int64_t)p.n;
         // column blocks of CW columns: PG thread groups sum interleaved subsets of the G partials of
         // one column each (independent loads, unrolled), group sums added in group order
@@ -274,19 +321,45 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
         for (int64_t c0 = j0; c0 < j1; c0 += CW) {
             const int64_t j = c0 + cc;
             double sacc = 0.0;
-            if (j < j1) {
-                const double *col = p.ypart + j;
-#pragma unroll 8
-                for (int bb = cg; bb < G; bb += PG) sacc += __ldcg(col + (int64_t)bb * p.ypart_ld);
-            }
+            if (j < j1) sacc = strided_sum<20>(p.ypart + j, p.ypart_ld, cg, PG, G);
             gred[cg * CW + cc] = sacc;
             __syncthreads();
-            if (tid < CW) {
-                double y = 0.0;
-                if (j < j1) {
-                    y = gred[tid];
+            if (p.tl && b == 0 && tid == 0 && c0 == j0) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 3] = globaltimer_ns();
+            double y = 0.0;
+            if (tid < CW && j < j1) {
+                y = gred[tid];
 #pragma unroll
-                    for (int q = 1; q < PG; ++q) y += gred[q * CW + tid];
+                for (int q = 1; q < PG; ++q) y += gred[q * CW + tid];
+            }
+            if (multi) {  // push my slice (+ local w) to every rank, wait for every rank's, sum in rank order
+                // low-latency protocol: every 8-byte word carries half of the value and the pass
+                // stamp, so a receiver polls the data itself (no fence, no separate flag)
+                const unsigned target = xe + 1u;
+                const int64_t so = ((int64_t)(target & 1u) * p.px.world * Gs + b) * p.px.SL;  // + src * Gs * SL
+                const int64_t mine = so + (int64_t)p.px.rank * Gs * p.px.SL;
+                for (int r = 0; r < p.px.world; ++r) {
+                    ulonglong2 *dst = p.px.rbuf[r] + mine;
+                    if (tid < CW && j < j1) ll_send(dst + tid, target, y);
+                    if (tid < l) ll_send(dst + p.px.per + tid, target, gvec[tid]);
+                }
+                const ulonglong2 *src = p.px.lbuf + so;
+                const unsigned long long t0 = globaltimer_ns();
+                if (tid < CW && j < j1) {
+                    y = 0.0;
+                    for (int r = 0; r < p.px.world; ++r) y += ll_recv(src + (int64_t)r * Gs * p.px.SL + tid, target, t0, st);
+                }
+                __syncthreads();  // every thread is done with gvec (local w)
+                if (tid < l) {
+                    double w = 0.0;
+                    for (int r = 0; r < p.px.world; ++r)
+                        w += ll_recv(src + (int64_t)r * Gs * p.px.SL + p.px.per + tid, target, t0, st);
+                    gvec[tid] = p.S[tid] * w;
+                }
+                __syncthreads();
+                if (p.tl && b == 0 && tid == 0 && c0 == j0) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 4] = globaltimer_ns();
+            }
+            if (tid < CW) {
+                if (j < j1) {
                     const double *Vj = p.V + j * p.ldv;
                     double corr = 0.0;  // (V (S w))_j
 #pragma unroll 4
@@ -311,6 +384,7 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
             }
             __syncthreads();
         }
+        if (p.tl && b == 0 && tid == 0) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 5] = globaltimer_ns();
         double *pp = p.part + (int64_t)b * p.part_ld;
         {  // block sums in a fixed order: warps (of the CW column threads), then lanes
             const double yy = warp_sum(a_yy), vy = warp_sum(a_vy);
@@ -342,18 +416,21 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
 
         // ---- decision: identical in every CTA (same data, same fixed order)
         for (int q = warp; q < 2 + l; q += NW) {
-            double sq = 0.0;
-            for (int bb = lane; bb < G; bb += 32) sq += __ldcg(p.part + (int64_t)bb * p.part_ld + q);
-            sq = warp_sum(sq);
+            const double sq = warp_sum(strided_sum<8>(p.part + q, p.part_ld, lane, 32, G));
             if (lane == 0) tot[q] = sq;
         }
         __syncthreads();
         const int itn = it + 1;
+        if (multi) ++xe;
         if (tid == 0) {
             const double nyn = sqrt(tot[0]);
             int done = 0, status = 0;
             double d = 0.0;
-            if (!isfinite(nyn)) {
+            // a CTA whose exchange timed out raised st->stop before sync 2: every CTA leaves
+            const int peer_fail = multi ? *reinterpret_cast<volatile int32_t *>(&st->stop) : 0;
+            if (peer_fail) {
+                done = 3;
+            } else if (!isfinite(nyn)) {
                 status = -7;
                 done = 2;
             } else if (nyn == 0.0) {  // X'^T X' v = 0: rank exhausted (reading R14)
@@ -378,11 +455,13 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
                     st->ny = nyn;
                     st->d = d;
                 }
-                if (done) {
+                if (done == 3) st->done = 1;  // status -6 / stop already set by the timed-out CTA
+                if (done == 1 || done == 2) {
                     st->status = status;
                     st->done = 1;
                     if (done == 2) st->stop = 1;
                 }
+                if (multi) st->xepoch = xe;
                 if (p.tl) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 2] = globaltimer_ns();
             }
         }

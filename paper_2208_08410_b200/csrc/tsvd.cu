@@ -112,6 +112,10 @@ struct tsvd_s {
     int coll_opt = 0;
     double *sym = nullptr;                  // this rank's symmetric buffer (peer path)
     void *peer_map[kMaxRanks] = {};         // IPC-opened peer buffers
+    void *px_map[kMaxRanks] = {};           // IPC-opened peer receive areas of the persistent kernel
+    char *px_mem = nullptr;                 // this rank's receive area + flags (N7, world > 1)
+    PxView px{};
+    bool px_ok = false;
     PeerView pv{};
     std::string peer_error;
     // options
@@ -412,18 +416,92 @@ static cudaError_t launch_n1(tsvd_t h, GvFn fn, const GvParams &p, cudaStream_t 
 
 // Fresh loop state; the peer-collective epoch is kept (flags in peer memory are monotone).
 static tsvd_status reset_state(tsvd_t h) {
-    uint32_t epoch = 0;
+    uint32_t epoch = 0, xepoch = 0;
     if (h->allocated) {
         CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
         epoch = h->st_host->epoch;
+        xepoch = h->st_host->xepoch;
     }
     LoopState s{};
     s.ny = 1.0;
     s.epoch = epoch;
+    s.xepoch = xepoch;
     *h->st_host = s;
     CK(cudaMemcpyAsync(h->st, h->st_host, sizeof(LoopState), cudaMemcpyHostToDevice, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    return TSVD_OK;
+}
+
+// Receive areas of the persistent kernel's exchange (N7, world > 1): [2][world][G][SL] doubles +
+// flags [world][G] per rank, IPC handles all-gathered with NCCL.  Needs one column block per CTA
+// (slice width <= 128 columns); otherwise the multi-GPU run keeps the per-iteration kernels.
+static tsvd_status setup_px(tsvd_t h) {
+    // the column slices must be the same on every rank: slice by the smallest grid of any rank
+    // (a rank with fewer rows than CTA slots runs a smaller grid)
+    int G = h->grid;
+    {
+        int *dg = nullptr;
+        CK(cudaMalloc((void **)&dg, sizeof(int)));
+        CK(cudaMemcpy(dg, &G, sizeof(int), cudaMemcpyHostToDevice));
+        NK(ncclAllReduce(dg, dg, 1, ncclInt, ncclMin, h->comm, h->stream));
+        CK(cudaMemcpyAsync(&G, dg, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        cudaFree(dg);
+    }
+    const int CW = std::min(h->T, 128);
+    const int per = (int)(((h->n + G - 1) / G + 31) / 32 * 32);
+    if (per > CW || h->world > kMaxRanks) return TSVD_OK;
+    const int SL = (int)round_up(per + h->kpad, 4);
+    const size_t bytes = (size_t)2 * h->world * G * SL * sizeof(ulonglong2);
+    CK(cudaMalloc((void **)&h->px_mem, bytes));
+    CK(cudaMemset(h->px_mem, 0, bytes));
+    cudaIpcMemHandle_t mine;
+    CK(cudaIpcGetMemHandle(&mine, h->px_mem));
+    char *dbuf = nullptr;
+    CK(cudaMalloc((void **)&dbuf, sizeof(cudaIpcMemHandle_t) * (h->world + 1)));
+    CK(cudaMemcpy(dbuf, &mine, sizeof(mine), cudaMemcpyHostToDevice));
+    NK(ncclAllGather(dbuf, dbuf + sizeof(mine), sizeof(mine), ncclUint8, h->comm, h->stream));
+    std::vector<cudaIpcMemHandle_t> all(h->world);
+    CK(cudaMemcpyAsync(all.data(), dbuf + sizeof(mine), sizeof(mine) * h->world, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(dbuf);
+    PxView px{};
+    px.world = h->world;
+    px.rank = h->rank;
+    px.G = G;
+    px.per = per;
+    px.SL = SL;
+    bool ok = true;
+    for (int r = 0; r < h->world; ++r) {
+        char *base = h->px_mem;
+        if (r != h->rank) {
+            void *q = nullptr;
+            cudaError_t e = cudaIpcOpenMemHandle(&q, all[r], cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                h->peer_error = std::string("persistent exchange: cudaIpcOpenMemHandle: ") + cudaGetErrorString(e);
+                ok = false;
+                continue;
+            }
+            h->px_map[r] = q;
+            base = (char *)q;
+        }
+        px.rbuf[r] = (ulonglong2 *)base;
+    }
+    px.lbuf = (const ulonglong2 *)h->px_mem;
+    // every rank must agree, or none uses the persistent exchange
+    int *dflag = nullptr;
+    CK(cudaMalloc((void **)&dflag, sizeof(int)));
+    const int okv = ok ? 1 : 0;
+    CK(cudaMemcpy(dflag, &okv, sizeof(int), cudaMemcpyHostToDevice));
+    NK(ncclAllReduce(dflag, dflag, 1, ncclInt, ncclMin, h->comm, h->stream));
+    int agreed = 0;
+    CK(cudaMemcpyAsync(&agreed, dflag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(dflag);
+    h->px = px;
+    h->px_ok = agreed == 1;
     return TSVD_OK;
 }
 
@@ -484,6 +562,7 @@ static tsvd_status ensure_alloc(tsvd_t h) {
     CK(cudaMemsetAsync(h->yw, 0, (size_t)(h->wofs + h->kpad) * sizeof(double), h->stream));
     TRY(reset_state(h));
     h->allocated = true;
+    if (h->world > 1 && h->coll == COLL_PEER && h->gv_ps && !h->sparse) TRY(setup_px(h));
     return TSVD_OK;
 }
 
@@ -909,8 +988,8 @@ static tsvd_status launch_fused_first(tsvd_t h, cudaStream_t s, int l, cudaEvent
 
 // N7: the iterations of component l after the first (or all of them), in one cooperative launch.
 static bool use_persist(tsvd_t h) {
-    return h->persist_opt && h->gv_ps && !h->sparse && !h->streaming && h->split == 1 && h->coll == COLL_NONE &&
-           !fused_reduce(h) && h->dynamic_opt == 0;
+    return h->persist_opt && h->gv_ps && !h->sparse && !h->streaming && h->split == 1 &&
+           (h->coll == COLL_NONE || (h->coll == COLL_PEER && h->px_ok)) && !fused_reduce(h) && h->dynamic_opt == 0;
 }
 
 static tsvd_status launch_persist(tsvd_t h, cudaStream_t s, int l, cudaEvent_t e0 = nullptr,
@@ -948,6 +1027,8 @@ static tsvd_status launch_persist(tsvd_t h, cudaStream_t s, int l, cudaEvent_t e
     p.max_iter = h->max_iter;
     p.serpentine = h->serp_opt;
     p.tl = h->tl_d;
+    p.px.world = 1;
+    if (h->world > 1) p.px = h->px;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident: grid barriers inside
@@ -1779,11 +1860,13 @@ void tsvd_destroy(tsvd_t h) {
     free_sparse(h);
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
     if (h->host_registered) cudaHostUnregister((void *)h->A_user);
-    for (int r = 0; r < kMaxRanks; ++r)
+    for (int r = 0; r < kMaxRanks; ++r) {
         if (h->peer_map[r]) cudaIpcCloseMemHandle(h->peer_map[r]);
+        if (h->px_map[r]) cudaIpcCloseMemHandle(h->px_map[r]);
+    }
     void *dev_ptrs[] = {h->A_own, h->U32, h->V64, h->S64, h->ybuf, h->yw, h->V0d, h->c64, h->ypart,
                         h->wpart, h->part, h->u64, h->sq_part, h->sig2, h->st, h->stats, h->sym, h->gbar,
-                        h->trace_d, h->work, h->tl_d};
+                        h->trace_d, h->work, h->tl_d, h->vprev32, h->px_mem};
     if (h->trace_f) fclose(h->trace_f);
     for (void *p : dev_ptrs)
         if (p) cudaFree(p);

@@ -47,6 +47,7 @@ def main():
     dist.broadcast_object_list(obj, src=0)
     t = P.TSVD(m, n, k, eps, rank=rank, world=world, uid=obj[0], device=local)
     t.set_option(P.OPT_COLLECTIVE, int(os.environ.get("TSVD_COLLECTIVE", "0")))
+    t.set_option(P.OPT_PERSISTENT, int(os.environ.get("TSVD_PERSISTENT", "1")))
     if sparse:
         t.set_option(P.OPT_FIXED_ITERS, 12)  # paper-like spectrum: fixed iterations
     t.set_init(V0)

@@ -12,21 +12,24 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("world,collective", [(2, 0), (2, 1), (4, 0), (8, 0)])
-def test_row_partition_parity(world, collective):
-    """collective 0: all-reduce fused into fin_iter over NVLink peer memory (graph mode);
-    collective 1: ncclAllReduce with the host-driven loop."""
+@pytest.mark.parametrize("world,collective,persistent", [(2, 0, 1), (2, 0, 0), (2, 1, 1), (4, 0, 1), (4, 0, 0),
+                                                      (8, 0, 1)])
+def test_row_partition_parity(world, collective, persistent):
+    """collective 0: NVLink peer memory — persistent 1: the persistent kernel exchanges column
+    slices between ranks inside the kernel; persistent 0: all-reduce fused into fin_iter (graph
+    WHILE loop).  collective 1: ncclAllReduce with the host-driven loop."""
     if not torch.cuda.is_available() or torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29400 + 10 * world + collective),
+           "--master-addr", "127.0.0.1", "--master-port", str(29400 + 10 * world + 2 * collective + persistent),
            os.path.join(ROOT, "tests", "mgpu_worker.py")]
-    env = dict(os.environ, TSVD_COLLECTIVE=str(collective))
+    env = dict(os.environ, TSVD_COLLECTIVE=str(collective), TSVD_PERSISTENT=str(persistent))
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "replicated_equal=True" in r.stdout
-    assert ("graph-while/peer-nvlink" if collective == 0 else "host/nccl") in r.stdout
+    want = "host/nccl" if collective else ("graph-persistent" if persistent else "graph-while") + "/peer-nvlink"
+    assert want in r.stdout
 
 
 @pytest.mark.parametrize("world", [2, 4])
