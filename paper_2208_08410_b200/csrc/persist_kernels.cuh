@@ -295,11 +295,6 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
         // ---- g = S w (every CTA, fixed order), then this CTA's column slice of y_new.  world > 1:
         // gvec holds the local w until the exchange has delivered every rank's
         const bool multi = p.px.world > 1;
-        for (int i = warp; i < l; i += NW) {
-            const double w = warp_sum(strided_sum<8>(p.wpart + i, p.wpart_ld, lane, 32, G));
-            if (lane == 0) gvec[i] = multi ? w : p.S[i] * w;
-        }
-        __syncthreads();
         const double *ycur = p.ybuf + (int64_t)(it & 1) * p.ystride;
         double *ynew = p.ybuf + (int64_t)((it + 1) & 1) * p.ystride;
         const double inv = 1.0 / ny_s;
@@ -321,8 +316,13 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
         for (int64_t c0 = j0; c0 < j1; c0 += CW) {
             const int64_t j = c0 + cc;
             double sacc = 0.0;
-            if (j < j1) sacc = strided_sum<20>(p.ypart + j, p.ypart_ld, cg, PG, G);
+            if (j < j1) sacc = strided_sum<40>(p.ypart + j, p.ypart_ld, cg, PG, G);
             gred[cg * CW + cc] = sacc;
+            if (c0 == j0)  // w = U^T t summed over the CTAs (issued after the slice loads: one more round)
+                for (int i = warp; i < l; i += NW) {
+                    const double w = warp_sum(strided_sum<8>(p.wpart + i, p.wpart_ld, lane, 32, G));
+                    if (lane == 0) gvec[i] = multi ? w : p.S[i] * w;
+                }
             __syncthreads();
             if (p.tl && b == 0 && tid == 0 && c0 == j0) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 3] = globaltimer_ns();
             double y = 0.0;
@@ -415,9 +415,15 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
         grid_sync(p.gbar);  // sync 2: every slice is written
 
         // ---- decision: identical in every CTA (same data, same fixed order)
-        for (int q = warp; q < 2 + l; q += NW) {
-            const double sq = warp_sum(strided_sum<8>(p.part + q, p.part_ld, lane, 32, G));
-            if (lane == 0) tot[q] = sq;
+        {  // half-warp per quantity, 16 lanes striding the CTAs: one round of loads for 2 + l <= 2 NW
+            const int hl = lane & 15;
+            for (int q0 = 2 * warp; q0 < 2 + l; q0 += 2 * NW) {  // warp-uniform trip count
+                const int q = q0 + (lane >> 4);
+                double sq = q < 2 + l ? strided_sum<10>(p.part + q, p.part_ld, hl, 16, G) : 0.0;
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+                if (hl == 0 && q < 2 + l) tot[q] = sq;
+            }
         }
         __syncthreads();
         const int itn = it + 1;

@@ -15,7 +15,7 @@ def main(path):
         if len(r) <= vi:
             continue
         v = float(r[vi].replace(",", ""))
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
         name = r[ki]
         tot[name] += v
         cnt[name] += 1
