@@ -425,7 +425,44 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     double cval = 0.0;
     if (!EXTRACT && tid < l) cval = p.c[tid];
     const int tail = p.n & 3;  // valid lanes of the last float4 (0 = full)
-    if (TWO) {  // stage v_prev (fp32, zero padded to n4 float4) once; read per row from smem
+    // TWO: v_prev is read with every row.  Small n: staged once in shared memory.  n > 8192 (T = 512):
+    // shared memory is taken by the ring, so each thread keeps its 4*NV floats of v_prev in tensor
+    // memory (TMEM, 128 columns: lane quarter = warp % 4, column group = warp / 4) and reloads
+    // them per row with tcgen05.ld — TMEM is otherwise unused by this memory-bound kernel.
+    constexpr bool kTmemV = TWO && T == 512 && NV == 8 && SPLIT == 1;
+    __shared__ uint32_t tm_base;
+    uint32_t tm_addr = 0;
+    if (kTmemV) {
+        if (warp == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tm_base))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        tm_addr = tm_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(32 * (warp >> 2));
+        const float4 *src = reinterpret_cast<const float4 *>(p.vprev);
+        uint32_t r[32];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int idx = k * T + tid;
+            const float4 v = idx < p.n4 ? src[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
+            r[4 * k + 0] = __float_as_uint(v.x);
+            r[4 * k + 1] = __float_as_uint(v.y);
+            r[4 * k + 2] = __float_as_uint(v.z);
+            r[4 * k + 3] = __float_as_uint(v.w);
+        }
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+            "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(tm_addr),
+            "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+            "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+            "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+            "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+            : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    } else if (TWO) {  // stage v_prev (fp32, zero padded to n4 float4) once; read per row from smem
         const float4 *src = reinterpret_cast<const float4 *>(p.vprev);
         for (int idx = tid; idx < p.n4; idx += T) vps[idx] = src[idx];
         __syncthreads();
@@ -472,6 +509,7 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
         float4 a[NV];
         float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
         float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;  // TWO: dot with v_prev
+        uint32_t vt8[8];                                // kTmemV: two float4 of v_prev from TMEM
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
             const int idx = k * T + tid;
@@ -489,7 +527,22 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
             q1 = fmaf(a[k].y, vr[k].y, q1);
             q2 = fmaf(a[k].z, vr[k].z, q2);
             q3 = fmaf(a[k].w, vr[k].w, q3);
-            if (TWO && idx < my_n4) {
+            if (kTmemV) {  // columns 4k..4k+3 of this thread's v_prev, two float4 per TMEM load
+                if ((k & 1) == 0) {
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t"
+                        "tcgen05.wait::ld.sync.aligned;"
+                        : "=r"(vt8[0]), "=r"(vt8[1]), "=r"(vt8[2]), "=r"(vt8[3]), "=r"(vt8[4]), "=r"(vt8[5]),
+                          "=r"(vt8[6]), "=r"(vt8[7])
+                        : "r"(tm_addr + (uint32_t)(4 * k))
+                        : "memory");
+                }
+                const int o = 4 * (k & 1);
+                p0 = fmaf(a[k].x, __uint_as_float(vt8[o + 0]), p0);
+                p1 = fmaf(a[k].y, __uint_as_float(vt8[o + 1]), p1);
+                p2 = fmaf(a[k].z, __uint_as_float(vt8[o + 2]), p2);
+                p3 = fmaf(a[k].w, __uint_as_float(vt8[o + 3]), p3);
+            } else if (TWO && idx < my_n4) {
                 const float4 vp = vps[idx];
                 p0 = fmaf(a[k].x, vp.x, p0);
                 p1 = fmaf(a[k].y, vp.y, p1);
@@ -579,6 +632,12 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
         if (SPLIT == 1 && p.reduce_mode) reduce_tail<T>(p);
     }
     if (SPLIT == 2) cluster_sync_all();  // no CTA leaves while its partner may still address it
+    if (kTmemV) {  // every warp is done with its TMEM columns
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tm_base) : "memory");
+    }
     if (p.trace) {
         __syncthreads();
         if (tid == 0) p.trace[blockIdx.x * 4 + 3] = globaltimer_ns();

@@ -342,7 +342,8 @@ static tsvd_status plan(tsvd_t h) {
     // fused-extraction variant: v_prev staged in shared memory, so fewer ring stages
     h->gv_two = nullptr;
     if (split == 1) {
-        h->vp_bytes = (int)round_up((int64_t)n4 * 16, 128);
+        // T = 512 (n > 8192): v_prev lives in tensor memory, the ring keeps all its stages
+        h->vp_bytes = (T == 512 && NV == 8) ? 0 : (int)round_up((int64_t)n4 * 16, 128);
         const int64_t fixed = h->vp_bytes + kMaxStages * sizeof(uint64_t) + 4 * (T / 32) * sizeof(double) + 1024;
         int S2 = (int)std::min<int64_t>(S, (kSmemBudget / h->cps - fixed) / h->stage_bytes);
         if (S2 >= 2) {
