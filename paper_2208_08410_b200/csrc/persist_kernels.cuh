@@ -53,23 +53,27 @@ struct PsParams {
     double eps;
     int32_t fixed_T, max_iter;
     int32_t serpentine;
+    int32_t part32;          // every CTA's range is a single fp32 run (rows <= run_rows): fp32 partials
     unsigned long long *tl;  // debug timeline (TSVD_TIMELINE), same record layout as N1 + N5
     PxView px;               // world > 1: NVLink peer exchange of the column slices (one block)
 };
 
 constexpr int kPsLanesV = 4;  // (V^T y) accumulators per lane: components l <= 128
+// doubles of slice-reduction scratch: T (one per thread) or, for T >= 128, [T/32 warps][128 columns]
+// (fp32 partials are read as float4: a warp covers a 128-column block of one partial row)
+__host__ __device__ constexpr int kPsGred(int T) { return T >= 128 ? 4 * T : T; }
 
 // sum_{b = first, first + step, ... < count} base[b * ld], in that order, with U loads in flight at a
 // time (these reductions are L2-latency bound: one round trip per batch instead of per element)
-template <int U>
-__device__ __forceinline__ double strided_sum(const double *base, int64_t ld, int first, int step, int count) {
+template <int U, typename E>
+__device__ __forceinline__ double strided_sum(const E *base, int64_t ld, int first, int step, int count) {
     double acc = 0.0;
     for (int b0 = first; b0 < count; b0 += U * step) {
         double v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int bb = b0 + u * step;
-            v[u] = bb < count ? __ldcg(base + (int64_t)bb * ld) : 0.0;
+            v[u] = bb < count ? (double)__ldcg(base + (int64_t)bb * ld) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -117,8 +121,8 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
     double *cvec = red + 2 * NW;                                   // [l] c = S V^T v
     double *gvec = cvec + p.wpart_ld;                              // [l] S w
     double *tot = gvec + p.wpart_ld;                               // [2 + l] decision sums
-    double *gred = tot + 2 + p.wpart_ld;                           // [NW][32] slice reduction
-    double *ys = gred + NW * 32;                                   // [128] y of the column block
+    double *gred = tot + 2 + p.wpart_ld;                           // [kPsGred(T)] slice reduction
+    double *ys = gred + kPsGred(T);                                // [128] y of the column block
     __shared__ int64_t slot_row[kMaxStages];
     __shared__ double ny_s;
     __shared__ int done_s;
@@ -209,6 +213,15 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
         double wacc = 0.0;
         bool flushed = false;
         auto flush = [&]() {
+            if (p.part32) {  // one fp32 run per pass: the partial IS an fp32 sum, store it as such
+#pragma unroll
+                for (int k = 0; k < NV; ++k) {
+                    const int idx = k * T + tid;
+                    if (idx < p.n4) reinterpret_cast<float4 *>(yp)[idx] = ya[k];
+                    ya[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                return;
+            }
 #pragma unroll
             for (int k = 0; k < NV; ++k) {
                 const int idx = k * T + tid;
@@ -281,7 +294,7 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
                 ya[kk].w = fmaf(tf, a[kk].w, ya[kk].w);
             }
             if (tid < l) wacc += t * (double)ur;
-            if (++run == p.run_rows) {
+            if (++run == p.run_rows && !p.part32) {  // part32: the single run is flushed after the loop
                 flush();
                 run = 0;
             }
@@ -315,9 +328,45 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
         for (int q = 0; q < kPsLanesV; ++q) vacc[q] = 0.0;
         for (int64_t c0 = j0; c0 < j1; c0 += CW) {
             const int64_t j = c0 + cc;
-            double sacc = 0.0;
-            if (j < j1) sacc = strided_sum<40>(p.ypart + j, p.ypart_ld, cg, PG, G);
-            gred[cg * CW + cc] = sacc;
+            constexpr bool kVec = CW == 128;  // fp32 partials as float4: warp w sums partials w, w+NW, ...
+            const bool vec = kVec && p.part32;
+            if (vec) {
+                const int64_t jv = c0 + 4 * lane;
+                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                if (jv < j1) {
+                    const float *col = reinterpret_cast<const float *>(p.ypart) + jv;
+                    const int64_t ld32 = 2 * p.ypart_ld;
+                    constexpr int U = 12;
+                    for (int b0 = warp; b0 < G; b0 += U * NW) {
+                        float4 v[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const int bb = b0 + u * NW;
+                            v[u] = bb < G ? __ldcg(reinterpret_cast<const float4 *>(col + (int64_t)bb * ld32))
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+                            if (b0 + u * NW < G) {
+                                s0 += (double)v[u].x;
+                                s1 += (double)v[u].y;
+                                s2 += (double)v[u].z;
+                                s3 += (double)v[u].w;
+                            }
+                    }
+                }
+                double *gw = gred + warp * 128 + 4 * lane;
+                gw[0] = s0;
+                gw[1] = s1;
+                gw[2] = s2;
+                gw[3] = s3;
+            } else {
+                double sacc = 0.0;
+                if (j < j1)
+                    sacc = p.part32 ? strided_sum<40>(reinterpret_cast<const float *>(p.ypart) + j, 2 * p.ypart_ld, cg, PG, G)
+                                    : strided_sum<40>(p.ypart + j, p.ypart_ld, cg, PG, G);
+                gred[cg * CW + cc] = sacc;
+            }
             if (c0 == j0)  // w = U^T t summed over the CTAs (issued after the slice loads: one more round)
                 for (int i = warp; i < l; i += NW) {
                     const double w = warp_sum(strided_sum<8>(p.wpart + i, p.wpart_ld, lane, 32, G));
@@ -327,9 +376,15 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
             if (p.tl && b == 0 && tid == 0 && c0 == j0) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 3] = globaltimer_ns();
             double y = 0.0;
             if (tid < CW && j < j1) {
-                y = gred[tid];
+                if (vec) {
+                    y = gred[tid];
 #pragma unroll
-                for (int q = 1; q < PG; ++q) y += gred[q * CW + tid];
+                    for (int q = 1; q < NW; ++q) y += gred[q * 128 + tid];
+                } else {
+                    y = gred[tid];
+#pragma unroll
+                    for (int q = 1; q < PG; ++q) y += gred[q * CW + tid];
+                }
             }
             if (multi) {  // push my slice (+ local w) to every rank, wait for every rank's, sum in rank order
                 // low-latency protocol: every 8-byte word carries half of the value and the pass

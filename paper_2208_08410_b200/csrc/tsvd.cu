@@ -359,7 +359,7 @@ static tsvd_status plan(tsvd_t h) {
     // must be co-resident (cooperative launch), and (V^T y)_i is owned by thread i (k <= T + 1)
     h->gv_ps = nullptr;
     if (split == 1 && h->k <= 32 * kPsLanesV + 1) {
-        const int64_t extra = kMaxStages * 8 + (int64_t)(2 * (T / 32) + 3 * h->kpad + 2 + (T / 32) * 32 + 128) * 8;
+        const int64_t extra = kMaxStages * 8 + (int64_t)(2 * (T / 32) + 3 * h->kpad + 2 + kPsGred(T) + 128) * 8;
         int Sp = S;
         while (Sp > 2 && ((int64_t)Sp * h->stage_bytes + extra) * h->cps > kSmemBudget) --Sp;
         PsFn fn = pick_ps(T, NV);
@@ -512,7 +512,8 @@ static tsvd_status ensure_alloc(tsvd_t h) {
     const int64_t n = h->n, mg = h->m_g;
     h->ystride = round_up(n, 32);
     h->wofs = round_up(n, 32);
-    h->ypart_ld = round_up(n, 4);
+    // per-CTA partial rows: padded so the rows of different CTAs do not sit a power of two apart
+    h->ypart_ld = round_up(n, 4) + (getenv("TSVD_NOPAD") ? 0 : 40);
     h->fin_blocks = (int)std::min<int64_t>((n + kFinCols - 1) / kFinCols, (int64_t)h->sms * 4);  // one wave
     h->part_ld = 2 + h->kpad;
     auto dm = [&](void **p, size_t bytes) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(bytes, 16)); };
@@ -1027,6 +1028,10 @@ static tsvd_status launch_persist(tsvd_t h, cudaStream_t s, int l, cudaEvent_t e
     p.fixed_T = h->fixed_T;
     p.max_iter = h->max_iter;
     p.serpentine = h->serp_opt;
+    // rows per CTA <= RUN_ROWS: each CTA's partial is one fp32 run, stored as fp32 (half the bytes;
+    // the reduction widens to fp64 exactly as the fp64 store did)
+    p.part32 = (h->m_res + h->grid - 1) / h->grid <= h->run_rows ? 1 : 0;
+    if (const char *e = getenv("TSVD_PART32")) p.part32 &= atoi(e);  // debug A/B knob
     p.tl = h->tl_d;
     p.px.world = 1;
     if (h->world > 1) p.px = h->px;
