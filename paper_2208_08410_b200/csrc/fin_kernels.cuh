@@ -186,6 +186,7 @@ struct FinParams {
     int ldu;
     const double *u_out;
     int64_t rows;
+    float *y32;               // sparse path: fp32 copy of every vector written to ybuf (else null)
 };
 
 // FIN_ITERATE : y_new = sum(partials) - V (S w) -> ybuf[(it+1)&1]; stop test; it += 1
@@ -339,6 +340,7 @@ __global__ void __launch_bounds__(kFinThreads, 4) fin_iter(const FinParams p) {
                 p.vprev32[j] = (float)vold;
             }
             ynew[j] = yj;
+            if (p.y32) p.y32[j] = (float)yj;  // sparse path: fp32 copy for N2's gathers
             a_yy += yj * yj;
             a_vy += vj * yj;
 #pragma unroll

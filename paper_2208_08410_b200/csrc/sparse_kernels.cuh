@@ -1,9 +1,9 @@
 // sparse_kernels.cuh — the Gram-vector product for a CSR row slab (Alg. 4).
 //
-//   N2 csr_spmv   warp per row: t_r = (sum_k val_k y_cur[col_k]) / ||y_cur|| - U_r . c   (= (X' v)_r,
-//                 v = y_cur / ||y_cur|| folded in; gathers of the fp64 iterate cost the same 32-B
-//                 sector as fp32 ones); per-block partials of w = U^T t.  EXTRACT: u_r = (A v)_r and
-//                 per-block sum u_r^2.
+//   N2 csr_spmv   warp per row: t_r = (sum_k val_k y32[col_k]) / ||y_cur|| - U_r . c   (= (X' v)_r,
+//                 v = y_cur / ||y_cur|| folded in, y32 = fp32 copy of the fp64 iterate written by the
+//                 finalize kernel: reading R23); per-block partials of w = U^T t.  EXTRACT: u_r =
+//                 (A v)_r and per-block sum u_r^2.
 //   N3 csc_spmvT  warp per column over the slab's CSC: y_j = sum_k cval_k t[row_k] — the transpose
 //                 product with no atomics and a fixed summation order; block 0 also sums the w
 //                 partials.  y and w land in yw = [y | w] (then the all-reduce across ranks, if any,
@@ -11,8 +11,8 @@
 //   N4 csc_*      one-time CSR -> CSC of the slab on the device: column histogram, exclusive scan,
 //                 scatter, per-column sort by row index (so the CSC, and every result, is
 //                 deterministic).
-// Products and sums are fp64 (the path is bound by the index/value stream and the gathers, not by
-// arithmetic).
+// Products and sums are fp64; the gathered vectors are fp32 copies (the path is bound by the random
+// gathers' DRAM traffic, not by arithmetic).
 #pragma once
 #include "fin_kernels.cuh"
 
@@ -37,7 +37,9 @@ struct SpParams {
     const double *ybuf;
     int64_t ystride;
     const LoopState *st;
-    double *t;        // [rows] t_r (EXTRACT: u_r)
+    double *t;        // [rows] EXTRACT: u_r (fp64)
+    float *t32;       // [rows] iteration: t_r rounded to fp32, gathered by N3
+    const float *y32; // [n] y_cur rounded to fp32 (written by fin_iter), gathered by N2
     double *wpart;    // [gridDim.x][wpart_ld]
     int wpart_ld;
     double *sq_part;  // [gridDim.x] (EXTRACT)
@@ -45,6 +47,63 @@ struct SpParams {
     int64_t wofs;
     int parts;        // gridDim.x of N2 (rows of wpart)
 };
+
+// Memory-level parallelism: each warp works on kSpRows consecutive rows (columns) at once.  Per lane,
+// the index/value loads of all of them are issued together (streaming, evict-first: they are read
+// once per pass), then all their gathers, so a warp has kSpRows dependent chains in flight instead
+// of one.  Lane `lane` of row q still sums k = k0 + lane, k0 + lane + 32, ... and the warp tree is
+// the same, so every result is bitwise what one row per warp gives.
+constexpr int kSpRows = 4;
+
+// row (column) pointers of kSpRows consecutive rows starting at r0: lanes 0..kSpRows load
+// ptr[min(r0 + lane, rows)], the bounds are broadcast; rows past the end are empty
+__device__ __forceinline__ void sp_bounds(const int64_t *ptr, int64_t r0, int64_t rows, int lane, int64_t (&kb)[kSpRows],
+                                          int64_t (&ke)[kSpRows]) {
+    int64_t v = 0;
+    if (lane <= kSpRows) v = __ldcs(ptr + (r0 + lane < rows ? r0 + lane : rows));
+#pragma unroll
+    for (int q = 0; q < kSpRows; ++q) {
+        kb[q] = __shfl_sync(0xffffffffu, v, q);
+        ke[q] = __shfl_sync(0xffffffffu, v, q + 1);
+    }
+}
+
+// sum_k val[k] x[idx[k]] over [kb[q], ke[q]) for every q, lane-strided, fp64 products and sums.
+// x is an fp32 copy of the gathered vector: a random gather costs a whole L2 sector (or line) of
+// DRAM traffic whatever its width, and the fp32 copy is half the footprint, so most of it stays in
+// the 126 MB L2 (measured: L2 hit rate 10 % with the fp64 vector at n = 2^25).
+__device__ __forceinline__ void sp_rows_dot(const int64_t (&kb)[kSpRows], const int64_t (&ke)[kSpRows],
+                                            const int32_t *idx, const float *val, const float *x, int lane,
+                                            double (&s)[kSpRows]) {
+    int64_t maxlen = 0;
+#pragma unroll
+    for (int q = 0; q < kSpRows; ++q) {
+        s[q] = 0.0;
+        maxlen = (ke[q] - kb[q]) > maxlen ? (ke[q] - kb[q]) : maxlen;
+    }
+    for (int64_t off = lane; off < maxlen; off += 32) {
+        int32_t ci[kSpRows];
+        float vv[kSpRows];
+#pragma unroll
+        for (int q = 0; q < kSpRows; ++q) {
+            const int64_t k = kb[q] + off;
+            ci[q] = -1;
+            vv[q] = 0.f;
+            if (k < ke[q]) {
+                ci[q] = __ldcs(idx + k);
+                vv[q] = __ldcs(val + k);
+            }
+        }
+        double g[kSpRows];
+#pragma unroll
+        for (int q = 0; q < kSpRows; ++q) g[q] = ci[q] >= 0 ? (double)__ldg(x + ci[q]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < kSpRows; ++q)
+            if (ci[q] >= 0) s[q] += (double)vv[q] * g[q];
+    }
+#pragma unroll
+    for (int q = 0; q < kSpRows; ++q) s[q] = warp_sum(s[q]);
+}
 
 // N2.  Dynamic shared memory: kSpWarps * l doubles (per-warp w accumulators, lane-owned entries).
 template <bool EXTRACT>
@@ -58,26 +117,32 @@ __global__ void __launch_bounds__(kSpThreads) csr_spmv(const SpParams p) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int l = EXTRACT ? 0 : p.l;
     const double inv = 1.0 / st->ny;
-    const double *ycur = p.ybuf + (int64_t)(st->it & 1) * p.ystride;
     double *wme = wsm + warp * (l > 0 ? l : 1);
     for (int i = lane; i < l; i += 32) wme[i] = 0.0;
     double sq = 0.0;
     const int64_t nwarps = (int64_t)gridDim.x * kSpWarps;
-    for (int64_t r = (int64_t)blockIdx.x * kSpWarps + warp; r < p.rows; r += nwarps) {
-        const int64_t k0 = p.row_ptr[r], k1 = p.row_ptr[r + 1];
-        double s = 0.0;
-        for (int64_t k = k0 + lane; k < k1; k += 32) s += (double)p.val[k] * ycur[p.col[k]];
-        s = warp_sum(s) * inv;
-        if (!EXTRACT && l > 0) {
-            const float *Ur = p.U + r * p.ldu;
-            double corr = 0.0;  // U_r . c: deflation without forming X' (Eq. 2, factored)
-            for (int i = lane; i < l; i += 32) corr += (double)Ur[i] * p.c[i];
-            s -= warp_sum(corr);
-            for (int i = lane; i < l; i += 32) wme[i] += s * (double)Ur[i];
-        }
-        if (lane == 0) {
-            p.t[r] = s;
-            sq += s * s;
+    for (int64_t r0 = ((int64_t)blockIdx.x * kSpWarps + warp) * kSpRows; r0 < p.rows; r0 += nwarps * kSpRows) {
+        int64_t kb[kSpRows], ke[kSpRows];
+        sp_bounds(p.row_ptr, r0, p.rows, lane, kb, ke);
+        double sr[kSpRows];
+        sp_rows_dot(kb, ke, p.col, p.val, p.y32, lane, sr);
+#pragma unroll
+        for (int q = 0; q < kSpRows; ++q) {
+            const int64_t r = r0 + q;
+            if (r >= p.rows) break;
+            double s = sr[q] * inv;
+            if (!EXTRACT && l > 0) {
+                const float *Ur = p.U + r * p.ldu;
+                double corr = 0.0;  // U_r . c: deflation without forming X' (Eq. 2, factored)
+                for (int i = lane; i < l; i += 32) corr += (double)Ur[i] * p.c[i];
+                s -= warp_sum(corr);
+                for (int i = lane; i < l; i += 32) wme[i] += s * (double)Ur[i];
+            }
+            if (lane == 0) {
+                if (EXTRACT) p.t[r] = s;
+                else p.t32[r] = (float)s;
+                sq += s * s;
+            }
         }
     }
     if (lane == 0) sqw[warp] = sq;
@@ -105,12 +170,18 @@ __global__ void __launch_bounds__(kSpThreads) csc_spmvT(const SpParams p) {
     if (st->stop || st->done) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t nwarps = (int64_t)gridDim.x * kSpWarps;
-    for (int64_t j = (int64_t)blockIdx.x * kSpWarps + warp; j < p.n; j += nwarps) {
-        const int64_t k0 = p.col_ptr[j], k1 = p.col_ptr[j + 1];
-        double s = 0.0;
-        for (int64_t k = k0 + lane; k < k1; k += 32) s += (double)p.cval[k] * p.t[p.row_idx[k]];
-        s = warp_sum(s);
-        if (lane == 0) p.yw[j] = s;
+    for (int64_t j0 = ((int64_t)blockIdx.x * kSpWarps + warp) * kSpRows; j0 < p.n; j0 += nwarps * kSpRows) {
+        int64_t kb[kSpRows], ke[kSpRows];
+        sp_bounds(p.col_ptr, j0, p.n, lane, kb, ke);
+        double sc[kSpRows];
+        sp_rows_dot(kb, ke, p.row_idx, p.cval, p.t32, lane, sc);
+        if (lane < kSpRows && j0 + lane < p.n) {
+            double v = sc[0];
+#pragma unroll
+            for (int q = 1; q < kSpRows; ++q)
+                if (lane == q) v = sc[q];
+            p.yw[j0 + lane] = v;
+        }
     }
     if (blockIdx.x == 0)
         for (int i = warp; i < p.l; i += kSpWarps) {

@@ -170,6 +170,7 @@ struct tsvd_s {
     // vectors / workspaces (device)
     double *ybuf = nullptr, *yw = nullptr, *V0d = nullptr, *c64 = nullptr, *ypart = nullptr, *wpart = nullptr;
     double *part = nullptr, *u64 = nullptr, *sq_part = nullptr, *sig2 = nullptr;
+    float *y32 = nullptr, *t32 = nullptr;  // sparse: fp32 copies of y_cur and t for the gathers
     LoopState *st = nullptr;
     CompStat *stats = nullptr;
     LoopState *st_host = nullptr;      // pinned
@@ -529,6 +530,8 @@ static tsvd_status ensure_alloc(tsvd_t h) {
     if (!e) e = dm((void **)&h->wpart, (size_t)h->parts * h->kpad * sizeof(double));
     if (!e) e = dm((void **)&h->part, (size_t)std::max(h->fin_blocks, h->grid) * h->part_ld * sizeof(double));
     if (!e) e = dm((void **)&h->u64, (size_t)mg * sizeof(double));
+    if (!e && h->sparse) e = dm((void **)&h->y32, (size_t)round_up(n, 4) * sizeof(float));
+    if (!e && h->sparse) e = dm((void **)&h->t32, (size_t)mg * sizeof(float));
     if (!e) e = dm((void **)&h->sq_part, (size_t)h->parts * sizeof(double));
     if (!e) e = dm((void **)&h->sig2, sizeof(double));
     if (!e) e = dm((void **)&h->st, sizeof(LoopState));
@@ -778,6 +781,8 @@ static SpParams sp_params(tsvd_t h, int l) {
     p.ystride = h->ystride;
     p.st = h->st;
     p.t = h->u64;
+    p.t32 = h->t32;
+    p.y32 = h->y32;
     p.wpart = h->wpart;
     p.wpart_ld = h->kpad;
     p.sq_part = h->sq_part;
@@ -876,6 +881,7 @@ static FinParams fin_params(tsvd_t h, int mode, int l, const double *xsrc, unsig
     p.use_cond = use_cond;
     p.tl = h->tl_d;
     p.fresh = l - 1;  // only read by the *_EXT modes
+    p.y32 = h->sparse ? h->y32 : nullptr;
     p.Vout = h->V64;
     p.vprev32 = h->vprev32;
     p.stat = h->stats;
@@ -1659,6 +1665,13 @@ tsvd_status tsvd_run(tsvd_t h) {
     h->streamed_batches = 0;
     // the graph needs every step to be a device kernel: no NCCL call, no host->device streaming
     const bool graph = h->use_graph && !h->timing && h->coll != COLL_NCCL && !h->streaming;
+    // debug A/B knob: L2 fetch granularity (bytes) while the run's kernels execute
+    size_t l2_fetch_old = 0;
+    const char *l2f = getenv("TSVD_L2FETCH");
+    if (l2f) {
+        CK(cudaDeviceGetLimit(&l2_fetch_old, cudaLimitMaxL2FetchGranularity));
+        CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(l2f)));
+    }
     bool ran = false;
     if (graph) {
         tsvd_status gs = TSVD_OK;
@@ -1673,6 +1686,10 @@ tsvd_status tsvd_run(tsvd_t h) {
         }
     }
     if (!ran) TRY(run_host_loop(h, l0));
+    if (l2f) {
+        CK(cudaStreamSynchronize(h->stream));
+        CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, l2_fetch_old));
+    }
     if (!ran && use_persist(h)) h->loop_mode = h->timing ? "host-persistent+events" : "host-persistent";
     CK(cudaMemcpyAsync(h->stats_host, h->stats, (size_t)h->k * sizeof(CompStat), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
@@ -1872,7 +1889,7 @@ void tsvd_destroy(tsvd_t h) {
     }
     void *dev_ptrs[] = {h->A_own, h->U32, h->V64, h->S64, h->ybuf, h->yw, h->V0d, h->c64, h->ypart,
                         h->wpart, h->part, h->u64, h->sq_part, h->sig2, h->st, h->stats, h->sym, h->gbar,
-                        h->trace_d, h->work, h->tl_d, h->vprev32, h->px_mem};
+                        h->trace_d, h->work, h->tl_d, h->vprev32, h->px_mem, h->y32, h->t32};
     if (h->trace_f) fclose(h->trace_f);
     for (void *p : dev_ptrs)
         if (p) cudaFree(p);
