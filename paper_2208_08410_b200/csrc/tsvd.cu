@@ -1665,13 +1665,6 @@ tsvd_status tsvd_run(tsvd_t h) {
     h->streamed_batches = 0;
     // the graph needs every step to be a device kernel: no NCCL call, no host->device streaming
     const bool graph = h->use_graph && !h->timing && h->coll != COLL_NCCL && !h->streaming;
-    // debug A/B knob: L2 fetch granularity (bytes) while the run's kernels execute
-    size_t l2_fetch_old = 0;
-    const char *l2f = getenv("TSVD_L2FETCH");
-    if (l2f) {
-        CK(cudaDeviceGetLimit(&l2_fetch_old, cudaLimitMaxL2FetchGranularity));
-        CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(l2f)));
-    }
     bool ran = false;
     if (graph) {
         tsvd_status gs = TSVD_OK;
@@ -1686,10 +1679,6 @@ tsvd_status tsvd_run(tsvd_t h) {
         }
     }
     if (!ran) TRY(run_host_loop(h, l0));
-    if (l2f) {
-        CK(cudaStreamSynchronize(h->stream));
-        CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, l2_fetch_old));
-    }
     if (!ran && use_persist(h)) h->loop_mode = h->timing ? "host-persistent+events" : "host-persistent";
     CK(cudaMemcpyAsync(h->stats_host, h->stats, (size_t)h->k * sizeof(CompStat), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
