@@ -87,7 +87,7 @@ __device__ __forceinline__ double strided_sum(const E *base, int64_t ld, int fir
 __device__ __forceinline__ void ll_send(ulonglong2 *dst, unsigned stamp, double x) {
     const unsigned long long s = (unsigned long long)stamp << 32;
     const unsigned long long a = s | (unsigned)__double2loint(x), b = s | (unsigned)__double2hiint(x);
-    asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(dst), "l"(a), "l"(b) : "memory");
+    asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(dst), "l"(a), "l"(b) : "memory");
 }
 // Poll until both words carry `stamp`; after 30 s mark the run failed (status -6) and return 0.
 __device__ __forceinline__ double ll_recv(const ulonglong2 *src, unsigned stamp, unsigned long long t0,
@@ -399,16 +399,39 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
                 }
                 const ulonglong2 *src = p.px.lbuf + so;
                 const unsigned long long t0 = globaltimer_ns();
-                if (tid < CW && j < j1) {
-                    y = 0.0;
-                    for (int r = 0; r < p.px.world; ++r) y += ll_recv(src + (int64_t)r * Gs * p.px.SL + tid, target, t0, st);
-                }
-                __syncthreads();  // every thread is done with gvec (local w)
-                if (tid < l) {
-                    double w = 0.0;
-                    for (int r = 0; r < p.px.world; ++r)
-                        w += ll_recv(src + (int64_t)r * Gs * p.px.SL + p.px.per + tid, target, t0, st);
-                    gvec[tid] = p.S[tid] * w;
+                const int E = p.px.world * (CW + l);  // elements to receive: [rank][CW slice values | l w]
+                if (E <= kPsGred(T)) {  // one element per thread: all polls in flight at once
+                    __syncthreads();    // gred (the local sums) and gvec (local w) have been read
+                    for (int e = tid; e < E; e += T) {
+                        const int r = e / (CW + l), c = e - r * (CW + l);
+                        double v = 0.0;
+                        if (c >= CW) v = ll_recv(src + (int64_t)r * Gs * p.px.SL + p.px.per + (c - CW), target, t0, st);
+                        else if (c0 + c < j1) v = ll_recv(src + (int64_t)r * Gs * p.px.SL + c, target, t0, st);
+                        gred[e] = v;
+                    }
+                    __syncthreads();
+                    if (tid < CW && j < j1) {  // ranks in order
+                        y = 0.0;
+                        for (int r = 0; r < p.px.world; ++r) y += gred[r * (CW + l) + tid];
+                    }
+                    if (tid < l) {
+                        double w = 0.0;
+                        for (int r = 0; r < p.px.world; ++r) w += gred[r * (CW + l) + CW + tid];
+                        gvec[tid] = p.S[tid] * w;
+                    }
+                } else {
+                    if (tid < CW && j < j1) {
+                        y = 0.0;
+                        for (int r = 0; r < p.px.world; ++r)
+                            y += ll_recv(src + (int64_t)r * Gs * p.px.SL + tid, target, t0, st);
+                    }
+                    __syncthreads();  // every thread is done with gvec (local w)
+                    if (tid < l) {
+                        double w = 0.0;
+                        for (int r = 0; r < p.px.world; ++r)
+                            w += ll_recv(src + (int64_t)r * Gs * p.px.SL + p.px.per + tid, target, t0, st);
+                        gvec[tid] = p.S[tid] * w;
+                    }
                 }
                 __syncthreads();
                 if (p.tl && b == 0 && tid == 0 && c0 == j0) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 4] = globaltimer_ns();
