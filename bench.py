@@ -237,6 +237,8 @@ def main():
                     help="TSVD_OPT_PDL (default: the library's default)")
     ap.add_argument("--row-order", type=int, default=None, choices=[0, 1],
                     help="TSVD_OPT_ROW_ORDER (default: the library's default)")
+    ap.add_argument("--sparse-block", type=int, default=None,
+                    help="TSVD_OPT_SPARSE_BLOCK: index-block width in elements (default: the library's)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -285,6 +287,8 @@ def main():
     if cfg.get("fixed_T"):
         t.set_option(P.OPT_FIXED_ITERS, cfg["fixed_T"])
     if sparse:
+        if args.sparse_block is not None:
+            t.set_option(P.OPT_SPARSE_BLOCK, args.sparse_block)
         t.set_csr(*A_dev, row_begin=r0, row_end=r1)
     else:
         t.set_dense(A_dev, r0, r1)

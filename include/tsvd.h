@@ -102,11 +102,15 @@ typedef enum {
                                     range backwards on odd iterations so the rows last read by the
                                     previous pass (still in the 126 MB L2) are read first; 0 = always
                                     forward. Changes only the fp32 summation order (rounding)       */
-    TSVD_OPT_PERSISTENT = 19     /* single GPU, dense resident, n <= 16384: 1 (default) = the
+    TSVD_OPT_PERSISTENT = 19,    /* single GPU, dense resident, n <= 16384: 1 (default) = the
                                     iterations of a component run inside ONE cooperative kernel
                                     (grid barriers, in-kernel reduction and stop test; no per-
                                     iteration kernel boundaries); 0 = one fused pass + finalize
                                     kernel per iteration (needed to profile single passes)          */
+    TSVD_OPT_SPARSE_BLOCK = 20   /* sparse: width (elements) of the index blocks the gathers are
+                                    split into so that each launch's block of the fp32 gathered
+                                    vector stays in L2; 0 (default) = 32 MiB of fp32 (n > 8M
+                                    columns / rows => several blocks). Read by tsvd_set_csr          */
 } tsvd_option;
 
 /*

@@ -19,6 +19,7 @@
 namespace tsvd {
 
 constexpr int kSpThreads = 256;
+constexpr size_t kSpL2BlockBytes = 32u << 20;  // fp32 gather block that stays L2-resident (126 MB L2)
 constexpr int kSpWarps = kSpThreads / 32;
 
 struct SpParams {
@@ -46,6 +47,13 @@ struct SpParams {
     double *yw;       // N3 output: y (n) | w (l) at wofs
     int64_t wofs;
     int parts;        // gridDim.x of N2 (rows of wpart)
+    // index blocking (an L2-sized block of the gathered vector per launch): launch `phase` of
+    // `nphase` covers the entries whose gathered index lies in block `phase`; the per-row (column)
+    // partial sums are carried across launches in fp64 and finished by the last launch.  The
+    // blocked pointers of phase b start at row_ptr + b * rows (col_ptr + b * n): one exclusive scan
+    // over [block][segment] counts.
+    int phase, nphase;
+    double *acc;      // [rows] (N2) or [n] (N3) carried partial sums when nphase > 1
 };
 
 // Memory-level parallelism: each warp works on kSpRows consecutive rows (columns) at once.  Per lane,
@@ -55,25 +63,41 @@ struct SpParams {
 // the same, so every result is bitwise what one row per warp gives.
 constexpr int kSpRows = 4;
 
-// row (column) pointers of kSpRows consecutive rows starting at r0: lanes 0..kSpRows load
-// ptr[min(r0 + lane, rows)], the bounds are broadcast; rows past the end are empty
-__device__ __forceinline__ void sp_bounds(const int64_t *ptr, int64_t r0, int64_t rows, int lane, int64_t (&kb)[kSpRows],
+// Lanes per segment: L (8, 16 or 32) lanes share a row (column), so a warp holds 32 / L groups of
+// kSpRows consecutive segments.  The host picks L from the mean segment length (nnz per row per
+// index block): short segments (blocked, or sparse rows) would otherwise leave most lanes idle.
+
+// bounds of the group's kSpRows segments starting at rb: group lanes 0..kSpRows load
+// ptr[min(rb + lane, segs)], broadcast within the group; segments past the end are empty
+template <int L>
+__device__ __forceinline__ void sp_bounds(const int64_t *ptr, int64_t rb, int64_t segs, int sl, int64_t (&kb)[kSpRows],
                                           int64_t (&ke)[kSpRows]) {
     int64_t v = 0;
-    if (lane <= kSpRows) v = __ldcs(ptr + (r0 + lane < rows ? r0 + lane : rows));
+    if (sl <= kSpRows) v = __ldcs(ptr + (rb + sl < segs ? rb + sl : segs));
 #pragma unroll
     for (int q = 0; q < kSpRows; ++q) {
-        kb[q] = __shfl_sync(0xffffffffu, v, q);
-        ke[q] = __shfl_sync(0xffffffffu, v, q + 1);
+        kb[q] = __shfl_sync(0xffffffffu, v, q, L);
+        ke[q] = __shfl_sync(0xffffffffu, v, q + 1, L);
     }
 }
 
-// sum_k val[k] x[idx[k]] over [kb[q], ke[q]) for every q, lane-strided, fp64 products and sums.
-// x is an fp32 copy of the gathered vector: a random gather costs a whole L2 sector (or line) of
-// DRAM traffic whatever its width, and the fp32 copy is half the footprint, so most of it stays in
-// the 126 MB L2 (measured: L2 hit rate 10 % with the fp64 vector at n = 2^25).
+// fp64 sum over the L lanes of a group (butterfly inside the group: every lane gets the total)
+template <int L>
+__device__ __forceinline__ double group_sum(double x) {
+#pragma unroll
+    for (int o = L / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+// sum_k val[k] x[idx[k]] over [kb[q], ke[q]) for every q: group lane sl takes k = kb + sl, kb + sl
+// + L, ...; fp64 products and sums; the index/value loads of all kSpRows segments are issued
+// together (streaming, evict-first: read once per pass), then all their gathers.  x is an fp32
+// copy of the gathered vector: a random gather costs a whole L2 sector (or line) of DRAM traffic
+// whatever its width, and the fp32 copy is half the footprint, so more of it stays in L2
+// (measured: L2 hit rate 10 % with the fp64 vector at n = 2^25, 24 % fp32, 72 % fp32 + blocks).
+template <int L>
 __device__ __forceinline__ void sp_rows_dot(const int64_t (&kb)[kSpRows], const int64_t (&ke)[kSpRows],
-                                            const int32_t *idx, const float *val, const float *x, int lane,
+                                            const int32_t *idx, const float *val, const float *x, int sl,
                                             double (&s)[kSpRows]) {
     int64_t maxlen = 0;
 #pragma unroll
@@ -81,7 +105,7 @@ __device__ __forceinline__ void sp_rows_dot(const int64_t (&kb)[kSpRows], const 
         s[q] = 0.0;
         maxlen = (ke[q] - kb[q]) > maxlen ? (ke[q] - kb[q]) : maxlen;
     }
-    for (int64_t off = lane; off < maxlen; off += 32) {
+    for (int64_t off = sl; off < maxlen; off += L) {
         int32_t ci[kSpRows];
         float vv[kSpRows];
 #pragma unroll
@@ -102,88 +126,124 @@ __device__ __forceinline__ void sp_rows_dot(const int64_t (&kb)[kSpRows], const 
             if (ci[q] >= 0) s[q] += (double)vv[q] * g[q];
     }
 #pragma unroll
-    for (int q = 0; q < kSpRows; ++q) s[q] = warp_sum(s[q]);
+    for (int q = 0; q < kSpRows; ++q) s[q] = group_sum<L>(s[q]);
 }
 
-// N2.  Dynamic shared memory: kSpWarps * l doubles (per-warp w accumulators, lane-owned entries).
-template <bool EXTRACT>
+// carry the kSpRows segment sums of a group across index blocks (fixed block order): group lane
+// q < kSpRows owns segment rb + q; on the last block the totals are broadcast back into s[]
+template <int L>
+__device__ __forceinline__ bool sp_carry(const SpParams &p, double *acc, int64_t rb, int64_t segs, int sl,
+                                         double (&s)[kSpRows]) {
+    double v = s[0];
+#pragma unroll
+    for (int q = 1; q < kSpRows; ++q)
+        if (sl == q) v = s[q];
+    if (sl < kSpRows && rb + sl < segs) {
+        if (p.phase > 0) v = acc[rb + sl] + v;
+        if (p.phase < p.nphase - 1) acc[rb + sl] = v;
+    }
+    if (p.phase < p.nphase - 1) return false;  // totals not complete yet
+#pragma unroll
+    for (int q = 0; q < kSpRows; ++q) s[q] = __shfl_sync(0xffffffffu, v, q, L);
+    return true;
+}
+
+// N2.  Dynamic shared memory: kSpWarps * (32 / L) * l doubles (per-group w accumulators).
+template <bool EXTRACT, int L>
 __global__ void __launch_bounds__(kSpThreads) csr_spmv(const SpParams p) {
+    constexpr int G = 32 / L;
     extern __shared__ double wsm[];
-    __shared__ double sqw[kSpWarps];
+    __shared__ double sqw[kSpWarps * G];
     const LoopState *st = p.st;
     griddep_launch();
     griddep_wait();
     if (st->stop || (!EXTRACT && st->done)) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int grp = lane / L, sl = lane % L;
     const int l = EXTRACT ? 0 : p.l;
     const double inv = 1.0 / st->ny;
-    double *wme = wsm + warp * (l > 0 ? l : 1);
-    for (int i = lane; i < l; i += 32) wme[i] = 0.0;
+    double *wme = wsm + (warp * G + grp) * (l > 0 ? l : 1);
+    for (int i = sl; i < l; i += L) wme[i] = 0.0;
     double sq = 0.0;
     const int64_t nwarps = (int64_t)gridDim.x * kSpWarps;
-    for (int64_t r0 = ((int64_t)blockIdx.x * kSpWarps + warp) * kSpRows; r0 < p.rows; r0 += nwarps * kSpRows) {
+    const int64_t *ptr = p.row_ptr + (int64_t)p.phase * p.rows;
+    for (int64_t r0 = ((int64_t)blockIdx.x * kSpWarps + warp) * (G * kSpRows); r0 < p.rows;
+         r0 += nwarps * (G * kSpRows)) {
+        const int64_t rb = r0 + grp * kSpRows;
         int64_t kb[kSpRows], ke[kSpRows];
-        sp_bounds(p.row_ptr, r0, p.rows, lane, kb, ke);
+        sp_bounds<L>(ptr, rb, p.rows, sl, kb, ke);
         double sr[kSpRows];
-        sp_rows_dot(kb, ke, p.col, p.val, p.y32, lane, sr);
+        sp_rows_dot<L>(kb, ke, p.col, p.val, p.y32, sl, sr);
+        if (p.nphase > 1 && !sp_carry<L>(p, p.acc, rb, p.rows, sl, sr)) continue;
 #pragma unroll
         for (int q = 0; q < kSpRows; ++q) {
-            const int64_t r = r0 + q;
-            if (r >= p.rows) break;
+            const int64_t r = rb + q;
+            const bool ok = r < p.rows;  // group-uniform; every lane still joins the shuffles
             double s = sr[q] * inv;
             if (!EXTRACT && l > 0) {
-                const float *Ur = p.U + r * p.ldu;
+                const float *Ur = p.U + (ok ? r : 0) * p.ldu;
                 double corr = 0.0;  // U_r . c: deflation without forming X' (Eq. 2, factored)
-                for (int i = lane; i < l; i += 32) corr += (double)Ur[i] * p.c[i];
-                s -= warp_sum(corr);
-                for (int i = lane; i < l; i += 32) wme[i] += s * (double)Ur[i];
+                if (ok)
+                    for (int i = sl; i < l; i += L) corr += (double)Ur[i] * p.c[i];
+                s -= group_sum<L>(corr);
+                if (ok)
+                    for (int i = sl; i < l; i += L) wme[i] += s * (double)Ur[i];
             }
-            if (lane == 0) {
+            if (ok && sl == 0) {
                 if (EXTRACT) p.t[r] = s;
                 else p.t32[r] = (float)s;
                 sq += s * s;
             }
         }
     }
-    if (lane == 0) sqw[warp] = sq;
+    if (p.phase < p.nphase - 1) return;  // not the last block: only the carried sums were written
+    if (sl == 0) sqw[warp * G + grp] = sq;
     __syncthreads();
     if (EXTRACT) {
         if (tid == 0) {
             double a = 0.0;
-            for (int w = 0; w < kSpWarps; ++w) a += sqw[w];
+            for (int w = 0; w < kSpWarps * G; ++w) a += sqw[w];
             p.sq_part[blockIdx.x] = a;
         }
     } else {
         for (int i = tid; i < l; i += kSpThreads) {
             double a = 0.0;
-            for (int w = 0; w < kSpWarps; ++w) a += wsm[w * l + i];  // warps in order
+            for (int w = 0; w < kSpWarps * G; ++w) a += wsm[w * l + i];  // groups in order
             p.wpart[(int64_t)blockIdx.x * p.wpart_ld + i] = a;
         }
     }
 }
 
 // N3.
+template <int L>
 __global__ void __launch_bounds__(kSpThreads) csc_spmvT(const SpParams p) {
+    constexpr int G = 32 / L;
     const LoopState *st = p.st;
     griddep_launch();
     griddep_wait();
     if (st->stop || st->done) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int grp = lane / L, sl = lane % L;
     const int64_t nwarps = (int64_t)gridDim.x * kSpWarps;
-    for (int64_t j0 = ((int64_t)blockIdx.x * kSpWarps + warp) * kSpRows; j0 < p.n; j0 += nwarps * kSpRows) {
+    const int64_t *ptr = p.col_ptr + (int64_t)p.phase * p.n;
+    for (int64_t j0 = ((int64_t)blockIdx.x * kSpWarps + warp) * (G * kSpRows); j0 < p.n;
+         j0 += nwarps * (G * kSpRows)) {
+        const int64_t jb = j0 + grp * kSpRows;
         int64_t kb[kSpRows], ke[kSpRows];
-        sp_bounds(p.col_ptr, j0, p.n, lane, kb, ke);
+        sp_bounds<L>(ptr, jb, p.n, sl, kb, ke);
         double sc[kSpRows];
-        sp_rows_dot(kb, ke, p.row_idx, p.cval, p.t32, lane, sc);
-        if (lane < kSpRows && j0 + lane < p.n) {
-            double v = sc[0];
+        sp_rows_dot<L>(kb, ke, p.row_idx, p.cval, p.t32, sl, sc);
+        double v = sc[0];
 #pragma unroll
-            for (int q = 1; q < kSpRows; ++q)
-                if (lane == q) v = sc[q];
-            p.yw[j0 + lane] = v;
+        for (int q = 1; q < kSpRows; ++q)
+            if (sl == q) v = sc[q];
+        if (sl < kSpRows && jb + sl < p.n) {
+            if (p.nphase > 1 && p.phase > 0) v = p.acc[jb + sl] + v;
+            if (p.phase < p.nphase - 1) p.acc[jb + sl] = v;
+            else p.yw[jb + sl] = v;
         }
     }
-    if (blockIdx.x == 0)
+    if (blockIdx.x == 0 && p.phase == p.nphase - 1)
         for (int i = warp; i < p.l; i += kSpWarps) {
             double w = 0.0;
             for (int b = lane; b < p.parts; b += 32) w += p.wpart[(int64_t)b * p.wpart_ld + i];
@@ -305,6 +365,45 @@ __global__ void csc_sort(const int64_t *__restrict__ col_ptr, int64_t n, int32_t
             }
             row_idx[b + 1] = key;
             cval[b + 1] = v;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- N4b: index blocking (one time)
+// Compressed segments (rows of the CSR, columns of the CSC) with sorted indices, split into K
+// blocks of width bw by index: thread per segment, binary search of the block boundaries.
+// cnt[b * segs + s] = entries of segment s in block b.
+__global__ void blk_count(const int64_t *__restrict__ ptr, const int32_t *__restrict__ idx, int64_t segs, int K,
+                          int64_t bw, unsigned *__restrict__ cnt) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < segs; s += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k0 = ptr[s], k1 = ptr[s + 1];
+        int64_t prev = k0;
+        for (int b = 0; b < K; ++b) {
+            int64_t lo = prev, hi = k1;  // first entry with idx >= (b + 1) bw
+            const int64_t lim = (int64_t)(b + 1) * bw;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if ((int64_t)idx[mid] < lim) lo = mid + 1;
+                else hi = mid;
+            }
+            cnt[(int64_t)b * segs + s] = (unsigned)(lo - prev);
+            prev = lo;
+        }
+    }
+}
+
+// scatter each segment's block pieces (order inside a piece kept) to the blocked layout
+__global__ void blk_scatter(const int64_t *__restrict__ ptr, const int32_t *__restrict__ idx,
+                            const float *__restrict__ val, int64_t segs, int K, const int64_t *__restrict__ bptr,
+                            int32_t *__restrict__ bidx, float *__restrict__ bval) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < segs; s += (int64_t)gridDim.x * blockDim.x) {
+        int64_t k = ptr[s];
+        for (int b = 0; b < K; ++b) {
+            const int64_t d0 = bptr[(int64_t)b * segs + s], d1 = bptr[(int64_t)b * segs + s + 1];
+            for (int64_t d = d0; d < d1; ++d, ++k) {
+                bidx[d] = idx[k];
+                bval[d] = val[k];
+            }
         }
     }
 }

@@ -73,6 +73,15 @@ GvFn pick_gv(int T, int nv, int split = 1) {
     }
 }
 
+using SpFn = void (*)(const SpParams);
+template <bool EX>
+SpFn pick_csr(int L) {
+    return L == 8 ? csr_spmv<EX, 8> : L == 16 ? csr_spmv<EX, 16> : csr_spmv<EX, 32>;
+}
+inline SpFn pick_csc(int L) { return L == 8 ? csc_spmvT<8> : L == 16 ? csc_spmvT<16> : csc_spmvT<32>; }
+// lanes per segment from the mean segment length (entries per row / column per index block)
+inline int pick_lanes(double mean_len) { return mean_len >= 24.0 ? 32 : mean_len >= 12.0 ? 16 : 8; }
+
 using PsFn = void (*)(const PsParams);
 
 template <int T>
@@ -171,6 +180,15 @@ struct tsvd_s {
     double *ybuf = nullptr, *yw = nullptr, *V0d = nullptr, *c64 = nullptr, *ypart = nullptr, *wpart = nullptr;
     double *part = nullptr, *u64 = nullptr, *sq_part = nullptr, *sig2 = nullptr;
     float *y32 = nullptr, *t32 = nullptr;  // sparse: fp32 copies of y_cur and t for the gathers
+    // sparse index blocking (L2-sized blocks of the gathered vectors): kc column blocks for N2,
+    // kr row blocks for N3; blocked copies of the CSR / CSC when > 1
+    int sp_kc = 1, sp_kr = 1;
+    int sp_lc = 32, sp_lr = 32;  // lanes per row (N2) / per column (N3)
+    int64_t sp_block_opt = 0;  // TSVD_OPT_SPARSE_BLOCK: block width in elements (0 = auto)
+    int64_t *bcsr_ptr = nullptr, *bcsc_ptr = nullptr;
+    int32_t *bcsr_idx = nullptr, *bcsc_idx = nullptr;
+    float *bcsr_val = nullptr, *bcsc_val = nullptr;
+    double *acc_r = nullptr, *acc_c = nullptr;
     LoopState *st = nullptr;
     CompStat *stats = nullptr;
     LoopState *st_host = nullptr;      // pinned
@@ -277,9 +295,11 @@ static tsvd_status set_fin_attrs(tsvd_t h) {
         CK(max_carveout(ext_finish<SRC_PARTS>));
         CK(max_carveout(ext_finish<SRC_YW>));
         CK(max_carveout(ext_finish<SRC_PEER>));
-        CK(max_carveout(csr_spmv<false>));
-        CK(max_carveout(csr_spmv<true>));
-        CK(max_carveout(csc_spmvT));
+        for (int L : {8, 16, 32}) {
+            CK(max_carveout(pick_csr<false>(L)));
+            CK(max_carveout(pick_csr<true>(L)));
+            CK(max_carveout(pick_csc(L)));
+        }
     }
     return TSVD_OK;
 }
@@ -287,10 +307,15 @@ static tsvd_status set_fin_attrs(tsvd_t h) {
 // ------------------------------------------------------------------------------------ planning
 static tsvd_status plan(tsvd_t h) {
     const int64_t n = h->n;
-    if (h->sparse) {  // N2/N3: persistent grid of 256-thread blocks, warp per row / column
-        const int dyn = kSpWarps * std::max(h->k, 1) * (int)sizeof(double);
-        if (dyn > 200 * 1024) return h->fail(TSVD_ERR_UNSUPPORTED, "sparse path supports k <= 3200");
-        CK(cudaFuncSetAttribute(csr_spmv<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    if (h->sparse) {  // N2/N3: persistent grid of 256-thread blocks, L lanes per row / column
+        for (int L : {8, 16, 32}) {
+            const int dyn = kSpWarps * (32 / L) * std::max(h->k, 1) * (int)sizeof(double);
+            if (dyn > 200 * 1024) {
+                if (L == h->sp_lc) return h->fail(TSVD_ERR_UNSUPPORTED, "sparse path: k too large for the w accumulators");
+                continue;
+            }
+            CK(cudaFuncSetAttribute(pick_csr<false>(L), cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+        }
         h->grid = h->sms * 8;
         h->parts = h->grid;
         h->T = kSpThreads;
@@ -765,13 +790,16 @@ static GvParams gv_params(tsvd_t h, int l, bool extract) {
 // same per-CTA partials, so the H2D of batch b+1.. overlaps the kernel on batch b.
 static SpParams sp_params(tsvd_t h, int l) {
     SpParams p{};
-    p.row_ptr = h->row_ptr_d;
-    p.col = h->col_d;
-    p.val = h->val_d;
+    const bool bc = h->sp_kc > 1, br = h->sp_kr > 1;
+    p.phase = 0;
+    p.nphase = 1;
+    p.row_ptr = bc ? h->bcsr_ptr : h->row_ptr_d;
+    p.col = bc ? h->bcsr_idx : h->col_d;
+    p.val = bc ? h->bcsr_val : h->val_d;
     p.rows = h->m_g;
-    p.col_ptr = h->col_ptr_d;
-    p.row_idx = h->row_idx_d;
-    p.cval = h->cval_d;
+    p.col_ptr = br ? h->bcsc_ptr : h->col_ptr_d;
+    p.row_idx = br ? h->bcsc_idx : h->row_idx_d;
+    p.cval = br ? h->bcsc_val : h->cval_d;
     p.n = h->n;
     p.U = h->U32;
     p.ldu = h->kpad;
@@ -795,12 +823,23 @@ static SpParams sp_params(tsvd_t h, int l) {
 // Sparse pass: N2 (rows) then N3 (columns) for an iteration; N2 alone for the extraction.
 static tsvd_status launch_sparse(tsvd_t h, cudaStream_t s, int l, bool extract) {
     const SpParams p = sp_params(h, l);
-    if (extract) {
-        CK(launch_k(h, csr_spmv<true>, h->grid, kSpThreads, 0, s, 1, p));
-    } else {
-        CK(launch_k(h, csr_spmv<false>, h->grid, kSpThreads, (size_t)kSpWarps * std::max(l, 1) * sizeof(double), s, 1,
-                    p));
-        CK(launch_k(h, csc_spmvT, h->grid, kSpThreads, 0, s, 1, p));
+    SpParams q = p;  // one launch per index block (phase), partial sums carried in acc
+    q.nphase = h->sp_kc;
+    q.acc = h->acc_r;
+    for (int b = 0; b < h->sp_kc; ++b) {
+        q.phase = b;
+        if (extract) CK(launch_k(h, pick_csr<true>(h->sp_lc), h->grid, kSpThreads, 0, s, 1, q));
+        else
+            CK(launch_k(h, pick_csr<false>(h->sp_lc), h->grid, kSpThreads,
+                        (size_t)kSpWarps * (32 / h->sp_lc) * std::max(l, 1) * sizeof(double), s, 1, q));
+    }
+    if (!extract) {
+        q.nphase = h->sp_kr;
+        q.acc = h->acc_c;
+        for (int b = 0; b < h->sp_kr; ++b) {
+            q.phase = b;
+            CK(launch_k(h, pick_csc(h->sp_lr), h->grid, kSpThreads, 0, s, 1, q));
+        }
     }
     CK(cudaGetLastError());
     return TSVD_OK;
@@ -1412,6 +1451,10 @@ tsvd_status tsvd_set_option(tsvd_t h, int32_t key, int64_t value) {
     case TSVD_OPT_PERSISTENT:
         h->persist_opt = value != 0;
         break;
+    case TSVD_OPT_SPARSE_BLOCK:
+        if (value < 0) return h->fail(TSVD_ERR_ARG, "SPARSE_BLOCK >= 0");
+        h->sp_block_opt = value;
+        break;
     case TSVD_OPT_PLACEMENT:
     case TSVD_OPT_RESIDENT_BYTES:
     case TSVD_OPT_BATCH_ROWS:
@@ -1488,6 +1531,32 @@ tsvd_status tsvd_set_dense(tsvd_t h, const float *A, int64_t ld, int64_t row_beg
     return TSVD_OK;
 }
 
+// Blocked copy of a compressed matrix (segments with sorted indices) split into K index blocks of
+// width bw: counts per [block][segment], one exclusive scan, scatter (N4b).
+static tsvd_status build_blocked(tsvd_t h, const int64_t *ptr, const int32_t *idx, const float *val, int64_t segs,
+                                 int64_t nnz, int K, int64_t bw, int64_t **bptr, int32_t **bidx, float **bval) {
+    const int64_t len = (int64_t)K * segs;
+    const int64_t ntiles = (len + kScanTile - 1) / kScanTile;
+    unsigned *cnt = nullptr;
+    int64_t *bsum = nullptr;
+    CK(cudaMalloc((void **)bptr, (size_t)(len + 1) * sizeof(int64_t)));
+    CK(cudaMalloc((void **)bidx, (size_t)nnz * sizeof(int32_t)));
+    CK(cudaMalloc((void **)bval, (size_t)nnz * sizeof(float)));
+    CK(cudaMalloc((void **)&cnt, (size_t)len * sizeof(unsigned)));
+    CK(cudaMalloc((void **)&bsum, (size_t)ntiles * sizeof(int64_t)));
+    const int blocks = h->sms * 8;
+    blk_count<<<blocks, 256, 0, h->stream>>>(ptr, idx, segs, K, bw, cnt);
+    scan_tiles<<<(int)ntiles, kScanThreads, 0, h->stream>>>(cnt, len, *bptr, bsum);
+    scan_totals<<<1, kScanThreads, 0, h->stream>>>(bsum, ntiles, *bptr + len);
+    scan_add<<<blocks, 256, 0, h->stream>>>(*bptr, len, bsum);
+    blk_scatter<<<blocks, 256, 0, h->stream>>>(ptr, idx, val, segs, K, *bptr, *bidx, *bval);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(cnt);
+    cudaFree(bsum);
+    return TSVD_OK;
+}
+
 static void free_sparse(tsvd_t h) {
     if (h->csr_owned) {
         cudaFree(h->row_ptr_d);
@@ -1497,6 +1566,15 @@ static void free_sparse(tsvd_t h) {
     cudaFree(h->col_ptr_d);
     cudaFree(h->row_idx_d);
     cudaFree(h->cval_d);
+    for (void *q : {(void *)h->bcsr_ptr, (void *)h->bcsc_ptr, (void *)h->bcsr_idx, (void *)h->bcsc_idx,
+                    (void *)h->bcsr_val, (void *)h->bcsc_val, (void *)h->acc_r, (void *)h->acc_c})
+        if (q) cudaFree(q);
+    h->bcsr_ptr = h->bcsc_ptr = nullptr;
+    h->bcsr_idx = h->bcsc_idx = nullptr;
+    h->bcsr_val = h->bcsc_val = nullptr;
+    h->acc_r = h->acc_c = nullptr;
+    h->sp_kc = h->sp_kr = 1;
+    h->sp_lc = h->sp_lr = 32;
     h->row_ptr_d = h->col_ptr_d = nullptr;
     h->col_d = h->row_idx_d = nullptr;
     h->val_d = h->cval_d = nullptr;
@@ -1588,6 +1666,30 @@ tsvd_status tsvd_set_csr(tsvd_t h, const int64_t *row_ptr, const int32_t *col_id
     CK(cudaStreamSynchronize(h->stream));
     cudaFree(cnt);
     cudaFree(bsum);
+    // N4b: index blocking, so that each launch's gathers hit an L2-resident block of the fp32
+    // vector (y32 for N2 by column, t32 for N3 by row)
+    const int64_t bw_auto = (int64_t)kSpL2BlockBytes / (int64_t)sizeof(float);
+    const int64_t bwc = h->sp_block_opt > 0 ? h->sp_block_opt : bw_auto;
+    const int64_t bwr = h->sp_block_opt > 0 ? h->sp_block_opt : bw_auto;
+    const int kc = (int)std::min<int64_t>(64, (n + bwc - 1) / bwc), kr = (int)std::min<int64_t>(64, (mg + bwr - 1) / bwr);
+    if (kc > 1 && nnz) {
+        TRY(build_blocked(h, h->row_ptr_d, h->col_d, h->val_d, mg, nnz, kc, (n + kc - 1) / kc, &h->bcsr_ptr,
+                          &h->bcsr_idx, &h->bcsr_val));
+        CK(cudaMalloc((void **)&h->acc_r, (size_t)mg * sizeof(double)));
+        h->sp_kc = kc;
+    }
+    if (kr > 1 && nnz) {
+        TRY(build_blocked(h, h->col_ptr_d, h->row_idx_d, h->cval_d, n, nnz, kr, (mg + kr - 1) / kr, &h->bcsc_ptr,
+                          &h->bcsc_idx, &h->bcsc_val));
+        CK(cudaMalloc((void **)&h->acc_c, (size_t)n * sizeof(double)));
+        h->sp_kr = kr;
+        cudaFree(h->row_idx_d);  // the blocked CSC replaces the plain one (col_ptr kept for the report)
+        cudaFree(h->cval_d);
+        h->row_idx_d = nullptr;
+        h->cval_d = nullptr;
+    }
+    h->sp_lc = pick_lanes((double)nnz / std::max<double>(1.0, (double)mg * h->sp_kc));
+    h->sp_lr = pick_lanes((double)nnz / std::max<double>(1.0, (double)n * h->sp_kr));
     h->csc_build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return TSVD_OK;
 }
@@ -1691,9 +1793,9 @@ tsvd_status tsvd_run(tsvd_t h) {
     // our kernels per iteration / extraction (NCCL calls not counted)
     int64_t per_pass = 1;
     if (h->streaming) per_pass = (h->m_res > 0 ? 1 : 0) + (h->m_g - h->m_res + h->batch_rows - 1) / h->batch_rows;
-    if (h->sparse) per_pass = 2;
+    if (h->sparse) per_pass = h->sp_kc + h->sp_kr;
     const int64_t per_iter = per_pass + (h->coll == COLL_NONE || h->sparse || fused_reduce(h) ? 1 : 2);
-    const int64_t per_ext = (h->sparse ? 1 : per_pass) + (h->coll == COLL_NONE ? 1 : 2);
+    const int64_t per_ext = (h->sparse ? h->sp_kc : per_pass) + (h->coll == COLL_NONE ? 1 : 2);
     for (int l = l0; l < h->k; ++l) {
         const CompStat &cs = h->stats_host[l];
         // fused extraction: component l > l0 starts with init_ext + the fused first iteration (which
@@ -1810,8 +1912,10 @@ tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
              h->streaming ? "true" : "false", (long long)h->m_res, (long long)h->batch_rows, h->qdepth,
              (long long)h->streamed_bytes, (long long)h->streamed_batches);
     s += tmp;
-    snprintf(tmp, sizeof tmp, "\"sparse\": {\"enabled\": %s, \"nnz\": %lld, \"csc_build_ms\": %.3f}, ",
-             h->sparse ? "true" : "false", (long long)h->nnz_g, h->csc_build_ms);
+    snprintf(tmp, sizeof tmp,
+             "\"sparse\": {\"enabled\": %s, \"nnz\": %lld, \"csc_build_ms\": %.3f, \"col_blocks\": %d, \"row_blocks\": %d, "
+             "\"lanes_row\": %d, \"lanes_col\": %d}, ",
+             h->sparse ? "true" : "false", (long long)h->nnz_g, h->csc_build_ms, h->sp_kc, h->sp_kr, h->sp_lc, h->sp_lr);
     s += tmp;
     std::string ge = h->graph_error + (h->peer_error.empty() ? "" : " | " + h->peer_error);
     for (char &c : ge)

@@ -33,6 +33,7 @@ OPT_FUSED_EXTRACT = 16  # 1 (default): extraction of l-1 fused into the first pa
 OPT_PDL = 17  # 1 (default): programmatic dependent launch between the loop's kernels
 OPT_ROW_ORDER = 18  # 1 (default): serpentine row order (odd iterations backwards, L2 reuse); 0 forward
 OPT_PERSISTENT = 19  # 1 (default): a component's iterations in one cooperative kernel (single GPU)
+OPT_SPARSE_BLOCK = 20  # sparse: index-block width (elements) for L2-resident gathers; 0 = auto (set before set_csr)
 F32, ROW_MAJOR = 0, 0
 
 _lib = None

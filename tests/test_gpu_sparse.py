@@ -110,6 +110,39 @@ def test_sparse_empty_rows_and_columns_and_graph_vs_host():
     np.testing.assert_allclose(a[2], ref.S, rtol=1e-6)
 
 
+@pytest.mark.parametrize("blk", [300, 1024, 64])
+def test_sparse_index_blocking(blk):
+    """SPARSE_BLOCK forces the L2 index blocking (several launches per product, row / column sums
+    carried in fp64 across them) at a small size: same products and t-SVD as the unblocked path
+    to summation-order rounding, and the oracle to the sparse tolerance."""
+    m, n, d, k, T = 3000, 2000, 13, 3, 6
+    rp, ci, va = synth.random_csr(m, n, d, seed=31)
+    V0 = synth.v0_normal(n, k, seed=32)
+    rng = np.random.default_rng(5)
+    v = rng.standard_normal(n)
+    want = oracle.gram_apply_csr(rp, ci, va, n, None, None, None, v)
+    got = []
+    for b in (0, blk):
+        t = P.TSVD(m, n, k, 1e-6)
+        t.set_option(P.OPT_SPARSE_BLOCK, b)
+        t.set_csr(rp, ci, va)
+        rep = t.report()
+        got.append(t.gram_apply(v))
+        t.close()
+        if b:
+            assert rep["sparse"]["col_blocks"] == -(-n // b) and rep["sparse"]["row_blocks"] == -(-m // b)
+    for g in got:
+        assert np.linalg.norm(g - want) / np.linalg.norm(want) <= 1e-6
+    np.testing.assert_allclose(got[1], got[0], rtol=1e-12, atol=1e-12 * np.abs(got[0]).max())
+    ref = oracle.tsvd_csr(rp, ci, va, n, k, 1e-6, V0, fixed_T=T)
+    a = _run((rp, ci, va), m, n, k, 1e-6, V0, fixed_iters=T)
+    bl = _run((rp, ci, va), m, n, k, 1e-6, V0, fixed_iters=T, sparse_block=blk)
+    np.testing.assert_allclose(bl[2], a[2], rtol=1e-10)
+    np.testing.assert_allclose(bl[2], ref.S, rtol=1e-6)
+    for i in range(k):
+        assert 1 - _cos(bl[3][:, i], ref.V[:, i]) <= 1e-5
+
+
 def test_sparse_invalid_and_zero():
     t = P.TSVD(4, 4, 1, 1e-6)
     with pytest.raises(P.TsvdError) as ei:  # unsorted columns in row 0
