@@ -56,6 +56,22 @@ struct PsParams {
     int32_t part32;          // every CTA's range is a single fp32 run (rows <= run_rows): fp32 partials
     unsigned long long *tl;  // debug timeline (TSVD_TIMELINE), same record layout as N1 + N5
     PxView px;               // world > 1: NVLink peer exchange of the column slices (one block)
+    // component transitions inside the kernel (two-vector path, R21):
+    // head_ext: the launch starts by reducing the partials of the two-vector pass (gv_fused<TWO>,
+    //   fp64 partials, sq_part, u_out) that began this component: sigma_fresh = ||u||, U[:, fresh] =
+    //   u / sigma, S[fresh], stat[fresh]; weight 1 on the fresh column in g, sigma in c
+    // tail_init: after the stop decision, initialise component l + 1: V[:, l] = v, vprev32 = v,
+    //   y_cur = x_{l+1} (V0n), ||x||, c = S V^T x / ||x|| (weight 1 on column l), stat[l]
+    int32_t head_ext, tail_init;
+    int32_t fresh;           // head_ext: the component being extracted (l - 1)
+    double *Sw;              // writable S (head_ext)
+    double *Vw;              // writable V (tail_init)
+    float *Uw;               // writable U (head_ext)
+    const double *u_out;     // head_ext: (A v_fresh)_r of this rank's rows, fp64
+    const double *sq_part;   // head_ext: per-CTA sums of u_r^2 of the two-vector pass
+    CompStat *stat;
+    const double *V0n;       // tail_init: x_{l+1}
+    float *vprev32;          // tail_init: fp32 copy of v_l for the next two-vector pass
 };
 
 constexpr int kPsLanesV = 4;  // (V^T y) accumulators per lane: components l <= 128
@@ -160,10 +176,11 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
         pk = 0;
         pp = 0;
         pslot = 0;
-        pit0 = it0;
+        pit0 = it0 + (p.head_ext ? 1 : 0);  // head: the first pass run here is iteration it0 + 1
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_barrier_init();
-        if (nr > 0)
+        // head: the first rows are fed after the U column of the fresh component is written
+        if (nr > 0 && !p.head_ext)
             for (int s = 0; s < S; ++s) feed();
     }
     for (int i = tid; i < l; i += T) cvec[i] = p.c[i];
@@ -175,7 +192,10 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
     uint32_t cph = 0;   // and the phase to wait for
     int rb = 0;         // parity of the dot-product scratch
     double *yp = p.ypart + (int64_t)b * p.ypart_ld;
+    __shared__ double sigma_s;
+    bool head = p.head_ext != 0;
     for (;;) {
+      if (!head) {
         // ---- v = y_cur / ||y_cur|| in registers (fp64 master -> fp32), c for this pass
         float4 vr[NV];
         {
@@ -304,6 +324,12 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
         __threadfence();
         grid_sync(p.gbar);  // sync 1: every partial is written
         if (p.tl && b == 0 && tid == 0) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 1] = globaltimer_ns();
+      }
+        // head: the partials are those of the two-vector pass (an earlier kernel: fp64, visible)
+        const bool ext = head;
+        const bool p32 = p.part32 && !ext;
+        const int fresh = ext ? p.fresh : -1;
+        const bool xsq = ext && b == 0;  // CTA 0 (column slice 0 on every rank) carries ||u||^2
 
         // ---- g = S w (every CTA, fixed order), then this CTA's column slice of y_new.  world > 1:
         // gvec holds the local w until the exchange has delivered every rank's
@@ -329,7 +355,7 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
         for (int64_t c0 = j0; c0 < j1; c0 += CW) {
             const int64_t j = c0 + cc;
             constexpr bool kVec = CW == 128;  // fp32 partials as float4: warp w sums partials w, w+NW, ...
-            const bool vec = kVec && p.part32;
+            const bool vec = kVec && p32;
             if (vec) {
                 const int64_t jv = c0 + 4 * lane;
                 double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -363,15 +389,20 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
             } else {
                 double sacc = 0.0;
                 if (j < j1)
-                    sacc = p.part32 ? strided_sum<40>(reinterpret_cast<const float *>(p.ypart) + j, 2 * p.ypart_ld, cg, PG, G)
-                                    : strided_sum<40>(p.ypart + j, p.ypart_ld, cg, PG, G);
+                    sacc = p32 ? strided_sum<40>(reinterpret_cast<const float *>(p.ypart) + j, 2 * p.ypart_ld, cg, PG, G)
+                               : strided_sum<40>(p.ypart + j, p.ypart_ld, cg, PG, G);
                 gred[cg * CW + cc] = sacc;
             }
-            if (c0 == j0)  // w = U^T t summed over the CTAs (issued after the slice loads: one more round)
+            if (c0 == j0) {  // w = U^T t summed over the CTAs (issued after the slice loads: one more round)
                 for (int i = warp; i < l; i += NW) {
                     const double w = warp_sum(strided_sum<8>(p.wpart + i, p.wpart_ld, lane, 32, G));
-                    if (lane == 0) gvec[i] = multi ? w : p.S[i] * w;
+                    if (lane == 0) gvec[i] = multi ? w : (i == fresh ? 1.0 : p.S[i]) * w;
                 }
+                if (xsq && warp == NW - 1) {  // ||u||^2 of this rank (sigma of the fresh component)
+                    const double q = warp_sum(strided_sum<8>(p.sq_part, 1, lane, 32, G));
+                    if (lane == 0) sigma_s = q;
+                }
+            }
             __syncthreads();
             if (p.tl && b == 0 && tid == 0 && c0 == j0) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 3] = globaltimer_ns();
             double y = 0.0;
@@ -396,14 +427,17 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
                     ulonglong2 *dst = p.px.rbuf[r] + mine;
                     if (tid < CW && j < j1) ll_send(dst + tid, target, y);
                     if (tid < l) ll_send(dst + p.px.per + tid, target, gvec[tid]);
+                    if (xsq && tid == T - 1) ll_send(dst + p.px.per + l, target, sigma_s);
                 }
                 const ulonglong2 *src = p.px.lbuf + so;
                 const unsigned long long t0 = globaltimer_ns();
-                const int E = p.px.world * (CW + l);  // elements to receive: [rank][CW slice values | l w]
+                // elements to receive: [rank][CW slice values | l w | ||u||^2 (head)]
+                const int EL = CW + l + (xsq ? 1 : 0);
+                const int E = p.px.world * EL;
                 if (E <= kPsGred(T)) {  // one element per thread: all polls in flight at once
                     __syncthreads();    // gred (the local sums) and gvec (local w) have been read
                     for (int e = tid; e < E; e += T) {
-                        const int r = e / (CW + l), c = e - r * (CW + l);
+                        const int r = e / EL, c = e - r * EL;
                         double v = 0.0;
                         if (c >= CW) v = ll_recv(src + (int64_t)r * Gs * p.px.SL + p.px.per + (c - CW), target, t0, st);
                         else if (c0 + c < j1) v = ll_recv(src + (int64_t)r * Gs * p.px.SL + c, target, t0, st);
@@ -412,12 +446,17 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
                     __syncthreads();
                     if (tid < CW && j < j1) {  // ranks in order
                         y = 0.0;
-                        for (int r = 0; r < p.px.world; ++r) y += gred[r * (CW + l) + tid];
+                        for (int r = 0; r < p.px.world; ++r) y += gred[r * EL + tid];
                     }
                     if (tid < l) {
                         double w = 0.0;
-                        for (int r = 0; r < p.px.world; ++r) w += gred[r * (CW + l) + CW + tid];
-                        gvec[tid] = p.S[tid] * w;
+                        for (int r = 0; r < p.px.world; ++r) w += gred[r * EL + CW + tid];
+                        gvec[tid] = (tid == fresh ? 1.0 : p.S[tid]) * w;
+                    }
+                    if (xsq && tid == T - 1) {
+                        double q = 0.0;
+                        for (int r = 0; r < p.px.world; ++r) q += gred[r * EL + CW + l];
+                        sigma_s = q;
                     }
                 } else {
                     if (tid < CW && j < j1) {
@@ -425,12 +464,18 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
                         for (int r = 0; r < p.px.world; ++r)
                             y += ll_recv(src + (int64_t)r * Gs * p.px.SL + tid, target, t0, st);
                     }
-                    __syncthreads();  // every thread is done with gvec (local w)
+                    __syncthreads();  // every thread is done with gvec (local w) and sigma_s
                     if (tid < l) {
                         double w = 0.0;
                         for (int r = 0; r < p.px.world; ++r)
                             w += ll_recv(src + (int64_t)r * Gs * p.px.SL + p.px.per + tid, target, t0, st);
-                        gvec[tid] = p.S[tid] * w;
+                        gvec[tid] = (tid == fresh ? 1.0 : p.S[tid]) * w;
+                    }
+                    if (xsq && tid == T - 1) {
+                        double q = 0.0;
+                        for (int r = 0; r < p.px.world; ++r)
+                            q += ll_recv(src + (int64_t)r * Gs * p.px.SL + p.px.per + l, target, t0, st);
+                        sigma_s = q;
                     }
                 }
                 __syncthreads();
@@ -476,6 +521,7 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
                 for (int w = 0; w < CW / 32; ++w) acc += sred[tid][w];
                 pp[tid] = acc;
             }
+            if (ext && tid == 2) pp[2 + l] = xsq ? sigma_s : 0.0;  // ||u||^2 rides with the slice scalars
 #pragma unroll
             for (int q = 0; q < kPsLanesV; ++q) {
                 if (32 * q >= l) break;
@@ -495,12 +541,13 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
         // ---- decision: identical in every CTA (same data, same fixed order)
         {  // half-warp per quantity, 16 lanes striding the CTAs: one round of loads for 2 + l <= 2 NW
             const int hl = lane & 15;
-            for (int q0 = 2 * warp; q0 < 2 + l; q0 += 2 * NW) {  // warp-uniform trip count
+            const int nq = 2 + l + (ext ? 1 : 0);
+            for (int q0 = 2 * warp; q0 < nq; q0 += 2 * NW) {  // warp-uniform trip count
                 const int q = q0 + (lane >> 4);
-                double sq = q < 2 + l ? strided_sum<10>(p.part + q, p.part_ld, hl, 16, G) : 0.0;
+                double sq = q < nq ? strided_sum<10>(p.part + q, p.part_ld, hl, 16, G) : 0.0;
 #pragma unroll
                 for (int o = 8; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-                if (hl == 0 && q < 2 + l) tot[q] = sq;
+                if (hl == 0 && q < nq) tot[q] = sq;
             }
         }
         __syncthreads();
@@ -512,8 +559,13 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
             double d = 0.0;
             // a CTA whose exchange timed out raised st->stop before sync 2: every CTA leaves
             const int peer_fail = multi ? *reinterpret_cast<volatile int32_t *>(&st->stop) : 0;
+            const double sg = ext ? sqrt(tot[2 + l]) : 1.0;  // sigma of the fresh component
+            sigma_s = sg;
             if (peer_fail) {
                 done = 3;
+            } else if (ext && !(sg > 0.0 && isfinite(sg))) {  // the extracted component had no energy
+                status = isfinite(sg) ? 2 : -7;
+                done = 2;
             } else if (!isfinite(nyn)) {
                 status = -7;
                 done = 2;
@@ -546,18 +598,140 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
                     if (done == 2) st->stop = 1;
                 }
                 if (multi) st->xepoch = xe;
+                if (ext) {  // the fresh component's sigma; its it/d/status came with tail_init
+                    CompStat cs = p.stat[fresh];
+                    cs.sigma = sg;
+                    if (sg > 0.0 && isfinite(sg)) {
+                        p.Sw[fresh] = sg;
+                        cs.valid = 1;
+                    } else {
+                        cs.status = status;
+                    }
+                    p.stat[fresh] = cs;
+                }
                 if (p.tl) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 2] = globaltimer_ns();
             }
         }
         __syncthreads();
-        for (int i = tid; i < l; i += T) {  // c = S V^T v1 for the next pass
-            cvec[i] = p.S[i] * (tot[2 + i] / ny_s);
+        for (int i = tid; i < l; i += T) {  // c = S V^T v1 for the next pass (sigma for the fresh column)
+            cvec[i] = (i == fresh ? sigma_s : p.S[i]) * (tot[2 + i] / ny_s);
             if (b == 0) p.c[i] = cvec[i];
         }
+        if (ext) {  // U[:, fresh] = u / sigma on this CTA's rows, then start the row stream
+            const double sg = sigma_s;
+            const int64_t r0 = p.rows * b / G;
+            if (sg > 0.0 && isfinite(sg))
+                for (int64_t r = r0 + tid; r < r0 + nr; r += T) p.Uw[r * p.ldu + fresh] = (float)(p.u_out[r] / sg);
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // U rows are read by TMA next
+            __syncthreads();
+            if (tid == 0 && nr > 0)
+                for (int s2 = 0; s2 < S; ++s2) feed();
+        }
+        head = false;
         it = itn;
         const int done = done_s;
         __syncthreads();
         if (done) break;
+    }
+    if (p.tail_init && done_s == 1) {
+        // ---- component l + 1: V[:, l] = v, the fp32 copy for the next two-vector
+        // pass, y_cur = x, ||x||, c = S V^T x / ||x|| with weight 1 on column l (its sigma comes with
+        // the next pass, R21).  Same column slices as the reduction; V and x are replicated, so every
+        // rank computes the same values without an exchange.
+        constexpr int CW = T < 128 ? T : 128;
+        const int Gs = p.px.world > 1 ? p.px.G : G;
+        const int64_t per = ((p.n + Gs - 1) / Gs + 31) / 32 * 32;
+        const int64_t j0 = b < Gs ? (int64_t)b * per : (int64_t)p.n;
+        const int64_t j1 = (j0 + per) < (int64_t)p.n ? (j0 + per) : (int64_t)p.n;
+        const double *yfin = p.ybuf + (int64_t)(it & 1) * p.ystride;
+        double *x0 = p.ybuf;  // the next component starts at it = 0
+        const double inv = 1.0 / ny_s;
+        const int l1 = l + 1;
+        double a_xx = 0.0;
+        double vacc[kPsLanesV];
+#pragma unroll
+        for (int q = 0; q < kPsLanesV; ++q) vacc[q] = 0.0;
+        for (int64_t c0 = j0; c0 < j1; c0 += CW) {
+            if (tid < CW) {
+                const int64_t j = c0 + tid;
+                double x = 0.0;
+                if (j < j1) {
+                    const double v = __ldcg(yfin + j) * inv;  // read before x0 (maybe the same buffer) is written
+                    p.Vw[j * p.ldv + l] = v;
+                    p.vprev32[j] = (float)v;
+                    x = p.V0n[j];
+                    __stcg(x0 + j, x);
+                    a_xx += x * x;
+                }
+                ys[tid] = x;
+            }
+            __syncthreads();
+            const int jn = (int)((j1 - c0) < CW ? (j1 - c0) : CW);
+            for (int jj = warp; jj < jn; jj += NW) {  // (V^T x)_i, columns 0..l (column l written above)
+                const double *Vr = p.V + (c0 + jj) * p.ldv;
+                const double xj = ys[jj];
+#pragma unroll
+                for (int q = 0; q < kPsLanesV; ++q)
+                    if (lane + 32 * q < l1) vacc[q] += Vr[lane + 32 * q] * xj;
+            }
+            __syncthreads();
+        }
+        double *pp = p.part + (int64_t)b * p.part_ld;
+        {
+            const double xx = warp_sum(a_xx);
+            if (lane == 0 && warp < CW / 32) sred[0][warp] = xx;
+            __syncthreads();
+            if (tid == 0) {
+                double acc = 0.0;
+                for (int w = 0; w < CW / 32; ++w) acc += sred[0][w];
+                pp[0] = acc;
+            }
+#pragma unroll
+            for (int q = 0; q < kPsLanesV; ++q) {
+                if (32 * q >= l1) break;
+                __syncthreads();
+                gred[warp * 32 + lane] = vacc[q];
+                __syncthreads();
+                if (tid < 32 && 32 * q + tid < l1) {
+                    double acc = 0.0;
+                    for (int w = 0; w < NW; ++w) acc += gred[w * 32 + tid];
+                    pp[2 + 32 * q + tid] = acc;
+                }
+            }
+        }
+        __threadfence();
+        grid_sync(p.gbar);
+        {
+            const int hl = lane & 15;
+            const int nq = 2 + l1;
+            for (int q0 = 2 * warp; q0 < nq; q0 += 2 * NW) {
+                const int q = q0 + (lane >> 4);
+                double sq = (q < nq && q != 1) ? strided_sum<10>(p.part + q, p.part_ld, hl, 16, G) : 0.0;
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+                if (hl == 0 && q < nq) tot[q] = sq;
+            }
+        }
+        __syncthreads();
+        const double nyx = sqrt(tot[0]);
+        const bool okx = nyx > 0.0 && isfinite(nyx);
+        if (b == 0) {
+            if (tid == 0) {
+                CompStat cs = p.stat[l];  // the finished component (sigma comes with the next pass)
+                cs.it = it;
+                cs.d = st->d;
+                cs.status = st->status;
+                p.stat[l] = cs;
+                st->it = 0;
+                st->ny = okx ? nyx : 1.0;
+                st->d = 0.0;
+                st->done = okx ? 0 : 1;
+                st->status = okx ? 0 : -7;
+                if (!okx) st->stop = 1;
+            }
+            for (int i = tid; i < l1; i += T)
+                p.c[i] = (i == l ? 1.0 : p.S[i]) * (tot[2 + i] / (okx ? nyx : 1.0));
+        }
     }
     // drain the S rows fed ahead for a pass that will not run (no bulk copy may outlive the CTA)
     if (tid == 0 && nr > 0)

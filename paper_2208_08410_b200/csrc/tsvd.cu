@@ -1011,6 +1011,21 @@ static tsvd_status launch_init_ext(tsvd_t h, cudaStream_t s, int l) {
     return launch_fin(h, s, fin_params(h, FIN_INIT_EXT, l, h->V0d + (size_t)l * h->n, 0ull, 0), SRC_PARTS);
 }
 
+// the two-vector pass alone (its partials are reduced by the next kernel)
+static tsvd_status launch_two(tsvd_t h, cudaStream_t s, int l) {
+    GvParams p = gv_params(h, l, false);
+    p.l = l;
+    p.u_bytes = l - 1 > 0 ? (int32_t)(round_up(l - 1, 4) * 4) : 0;
+    p.stages = h->S_two;
+    p.vprev = h->vprev32;
+    p.vp_bytes = h->vp_bytes;
+    p.reduce_mode = 0;
+    p.tl = nullptr;
+    p.trace = nullptr;
+    CK(launch_k(h, h->gv_two, h->grid, h->T, h->smem_two, s, 1, p));
+    return TSVD_OK;
+}
+
 static tsvd_status launch_fused_first(tsvd_t h, cudaStream_t s, int l, cudaEvent_t e0 = nullptr,
                                       cudaEvent_t e1 = nullptr) {
     if (e0) CK(cudaEventRecord(e0, s));
@@ -1039,9 +1054,22 @@ static bool use_persist(tsvd_t h) {
            (h->coll == COLL_NONE || (h->coll == COLL_PEER && h->px_ok)) && !fused_reduce(h) && h->dynamic_opt == 0;
 }
 
+// head: the launch first reduces the two-vector pass of component l (extraction of l - 1);
+// tail: after component l stops, it initialises component l + 1 (R21, DESIGN §6 N7)
 static tsvd_status launch_persist(tsvd_t h, cudaStream_t s, int l, cudaEvent_t e0 = nullptr,
-                                  cudaEvent_t e1 = nullptr) {
+                                  cudaEvent_t e1 = nullptr, int head = 0, int tail = 0) {
     PsParams p{};
+    p.head_ext = head;
+    p.tail_init = tail;
+    p.fresh = l - 1;
+    p.Sw = h->S64;
+    p.Vw = h->V64;
+    p.Uw = h->U32;
+    p.u_out = h->u64;
+    p.sq_part = h->sq_part;
+    p.stat = h->stats;
+    p.V0n = tail ? h->V0d + (size_t)(l + 1) * h->n : nullptr;
+    p.vprev32 = h->vprev32;
     p.A = h->A_use;
     p.ld = h->ld_use;
     p.rows = h->m_res;
@@ -1177,7 +1205,14 @@ static tsvd_status build_graph(tsvd_t h, int l0) {
     cudaError_t ce = cudaSuccess;
     const bool fx = fuse_ext(h);
     const bool ps = use_persist(h);
-    for (int l = l0; l < h->k && s >= 0 && ce == cudaSuccess; ++l) {
+    if (fx && ps) {  // chain: init, then per component [two-vector pass] + one persistent launch
+        for (int l = l0; l < h->k && s >= 0; ++l) {
+            s = l == l0 ? launch_init(h, h->stream, l) : launch_two(h, h->stream, l);
+            if (s >= 0) s = launch_persist(h, h->stream, l, nullptr, nullptr, l > l0, l + 1 < h->k);
+        }
+        if (s >= 0) s = launch_extract(h, h->stream, h->k - 1);
+    }
+    for (int l = l0; l < h->k && s >= 0 && ce == cudaSuccess && !(fx && ps); ++l) {
         if (fx && l > l0) {  // extraction of l-1 rides on the first iteration of l
             s = launch_init_ext(h, h->stream, l);
             if (s >= 0) s = launch_fused_first(h, h->stream, l);
@@ -1250,6 +1285,27 @@ static tsvd_status run_host_loop(tsvd_t h, int l0) {
     }
     const bool fx = fuse_ext(h);
     const bool ps = use_persist(h);
+    if (fx && ps) {  // chain (as in the graph): one synchronisation per component
+        for (int l = l0; l < h->k; ++l) {
+            if (l == l0) TRY(launch_init(h, h->stream, l));
+            else TRY(launch_two(h, h->stream, l));
+            TRY(launch_persist(h, h->stream, l, e0, e1, l > l0, l + 1 < h->k));
+            CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            if (h->timing) {
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, e0, e1));
+                h->ps_ms += ms;
+                h->ps_launches += 1;
+            }
+            if (h->st_host->stop) break;
+        }
+        if (!h->st_host->stop) TRY(launch_extract(h, h->stream, h->k - 1));
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+        h->loop_mode = h->timing ? "host+events" : "host";
+        return TSVD_OK;
+    }
     for (int l = l0; l < h->k; ++l) {
         const bool fused_first = fx && l > l0;
         if (fused_first) TRY(launch_init_ext(h, h->stream, l));
@@ -1807,8 +1863,11 @@ tsvd_status tsvd_run(tsvd_t h) {
                                    : body_it;
         const bool ps = use_persist(h);
         if (ps) h->ps_passes += body_it;
-        h->launches += 1 + (ff ? per_iter : 0) + (ps ? 1 : per_iter * issued) +
-                       (!h->fused_ext_used || l == h->k - 1 ? per_ext : 0);
+        if (ps && h->fused_ext_used)  // chain: [init | two-vector pass] + one persistent launch
+            h->launches += 2 + (l == h->k - 1 ? per_ext : 0);
+        else
+            h->launches += 1 + (ff ? per_iter : 0) + (ps ? 1 : per_iter * issued) +
+                           (!h->fused_ext_used || l == h->k - 1 ? per_ext : 0);
         if (cs.status == -7) return h->fail(TSVD_ERR_NUMERIC, "non-finite value or zero initial vector at component %d", l);
         if (!cs.valid || cs.status == 2) {
             result = TSVD_WARN_RANK_EXHAUSTED;
