@@ -59,3 +59,18 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "oracle.c" not in txt, f
+
+
+def test_binding_option_and_status_values_match_the_header():
+    """Every TSVD_OPT_* / TSVD_* enum value in include/tsvd.h has the same value in the binding."""
+    import paper_2208_08410_b200.tsvd as b
+    src = open(os.path.join(ROOT, "include", "tsvd.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    pairs = dict((k, int(v)) for k, v in re.findall(r"\b(TSVD_[A-Z0-9_]+)\s*=\s*(-?\d+)", src))
+    opts = {k[len("TSVD_OPT_"):]: v for k, v in pairs.items() if k.startswith("TSVD_OPT_")}
+    assert len(opts) >= 20
+    for name, val in opts.items():
+        assert getattr(b, "OPT_" + name) == val, name
+    for name in ("OK", "WARN_NOT_CONVERGED", "WARN_RANK_EXHAUSTED", "ERR_ARG", "ERR_SHAPE", "ERR_UNSUPPORTED",
+                 "ERR_NOMEM", "ERR_CUDA", "ERR_NCCL", "ERR_NUMERIC", "ERR_STATE"):
+        assert getattr(b, name) == pairs["TSVD_" + name], name
