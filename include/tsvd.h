@@ -79,7 +79,8 @@ typedef enum {
     TSVD_OPT_RESIDENT_BYTES = 10,/* stream mode: cap on the HBM-resident prefix of A (-1 = as much as
                                     fits; 0 = stream every row)                                       */
     TSVD_OPT_BATCH_ROWS = 11,    /* stream mode: rows per H2D batch (0 = ~256 MiB batches)            */
-    TSVD_OPT_QUEUE_DEPTH = 12,   /* stream mode: device ring slots q_s, 2..8, def. 3   */
+    TSVD_OPT_QUEUE_DEPTH = 12,   /* stream mode: device ring slots q_s, 1..8, def. 3
+                                    (1: copy and compute of consecutive batches serialise)            */
     TSVD_OPT_FUSED_REDUCE = 13,  /* 1: the fused kernel sums its per-CTA partials itself (cooperative
                                     launch, grid barrier, column slices) and, multi-GPU, publishes them
                                     to the peers; 0 (default): separate reduction kernel (measured

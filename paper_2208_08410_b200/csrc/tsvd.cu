@@ -145,6 +145,7 @@ struct tsvd_s {
     int64_t v0_version = 1, v0_uploaded = 0;
     // out-of-memory degree 1 (host input): resident prefix [0, m_res) + streamed batches
     int placement = 0, qdepth = 3;
+    int64_t work_bytes = 0;  // device workspace allocated by ensure_alloc (report: peak device bytes)
     int64_t resident_cap = -1, batch_rows_opt = 0;
     int64_t m_res = 0, batch_rows = 0, own_rows = 0;
     bool streaming = false, host_registered = false;
@@ -542,7 +543,10 @@ static tsvd_status ensure_alloc(tsvd_t h) {
     h->ypart_ld = round_up(n, 4) + (getenv("TSVD_NOPAD") ? 0 : 40);
     h->fin_blocks = (int)std::min<int64_t>((n + kFinCols - 1) / kFinCols, (int64_t)h->sms * 4);  // one wave
     h->part_ld = 2 + h->kpad;
-    auto dm = [&](void **p, size_t bytes) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(bytes, 16)); };
+    auto dm = [&](void **p, size_t bytes) -> cudaError_t {
+        h->work_bytes += (int64_t)std::max<size_t>(bytes, 16);
+        return cudaMalloc(p, std::max<size_t>(bytes, 16));
+    };
     cudaError_t e = cudaSuccess;
     if (!e) e = dm((void **)&h->U32, (size_t)mg * h->kpad * sizeof(float));
     if (!e) e = dm((void **)&h->V64, (size_t)n * h->k * sizeof(double));
@@ -1518,7 +1522,7 @@ tsvd_status tsvd_set_option(tsvd_t h, int32_t key, int64_t value) {
         if (key == TSVD_OPT_PLACEMENT && (value < 0 || value > 2)) return h->fail(TSVD_ERR_ARG, "PLACEMENT in 0..2");
         if (key == TSVD_OPT_RESIDENT_BYTES && value < -1) return h->fail(TSVD_ERR_ARG, "RESIDENT_BYTES >= -1");
         if (key == TSVD_OPT_BATCH_ROWS && value < 0) return h->fail(TSVD_ERR_ARG, "BATCH_ROWS >= 0");
-        if (key == TSVD_OPT_QUEUE_DEPTH && (value < 2 || value > 8)) return h->fail(TSVD_ERR_ARG, "QUEUE_DEPTH in 2..8");
+        if (key == TSVD_OPT_QUEUE_DEPTH && (value < 1 || value > 8)) return h->fail(TSVD_ERR_ARG, "QUEUE_DEPTH in 1..8");
         if (key == TSVD_OPT_PLACEMENT) h->placement = (int)value;
         if (key == TSVD_OPT_RESIDENT_BYTES) h->resident_cap = value;
         if (key == TSVD_OPT_BATCH_ROWS) h->batch_rows_opt = value;
@@ -1967,9 +1971,11 @@ tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
     s += tmp;
     snprintf(tmp, sizeof tmp,
              "\"placement\": {\"streaming\": %s, \"resident_rows\": %lld, \"batch_rows\": %lld, \"queue_depth\": %d, "
-             "\"streamed_bytes\": %lld, \"streamed_batches\": %lld}, ",
+             "\"streamed_bytes\": %lld, \"streamed_batches\": %lld, \"device_bytes\": %lld}, ",
              h->streaming ? "true" : "false", (long long)h->m_res, (long long)h->batch_rows, h->qdepth,
-             (long long)h->streamed_bytes, (long long)h->streamed_batches);
+             (long long)h->streamed_bytes, (long long)h->streamed_batches,
+             (long long)(h->work_bytes + (h->mem == TSVD_MEM_DEVICE ? 0 : h->m_res * ((h->n + 3) / 4) * 16) +
+                         (h->streaming ? (int64_t)h->qdepth * h->batch_rows * ((h->n + 3) / 4) * 16 : 0)));
     s += tmp;
     snprintf(tmp, sizeof tmp,
              "\"sparse\": {\"enabled\": %s, \"nnz\": %lld, \"csc_build_ms\": %.3f, \"col_blocks\": %d, \"row_blocks\": %d, "

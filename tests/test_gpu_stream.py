@@ -37,7 +37,8 @@ def _run(A, k, eps, V0, src, **opts):
     return rc, U, S, V, kf, iters, rep
 
 
-@pytest.mark.parametrize("resident_rows,batch_rows,depth", [(0, 97, 2), (500, 211, 3), (1999, 64, 4), (0, 5000, 2)])
+@pytest.mark.parametrize("resident_rows,batch_rows,depth", [(0, 97, 2), (500, 211, 3), (1999, 64, 4), (0, 5000, 2),
+                                                         (0, 211, 1)])
 def test_streamed_equals_oracle_and_resident(resident_rows, batch_rows, depth):
     m, n, k, eps = 2000, 384, 4, 1e-8
     A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(96, 6.0, 0.7), seed=31)
@@ -87,7 +88,7 @@ def test_streamed_pageable_gram_apply():
 
 def test_stream_options_validated():
     t = P.TSVD(100, 10, 2, 1e-6)
-    for key, bad in ((P.OPT_PLACEMENT, 3), (P.OPT_QUEUE_DEPTH, 1), (P.OPT_QUEUE_DEPTH, 9), (P.OPT_RESIDENT_BYTES, -2)):
+    for key, bad in ((P.OPT_PLACEMENT, 3), (P.OPT_QUEUE_DEPTH, 0), (P.OPT_QUEUE_DEPTH, 9), (P.OPT_RESIDENT_BYTES, -2)):
         with pytest.raises(P.TsvdError) as ei:
             t.set_option(key, bad)
         assert ei.value.status == P.ERR_ARG
