@@ -54,6 +54,11 @@ CONFIGS = {
     "c5s": dict(workload="dense fp32 1048576x32768 (128 GiB, one GPU's row slab of BASELINE configs[4] "
                          "8Mx32768 = 1 TiB) in HBM, k=8, eps=1e-6, Hadamard known spectrum rank 32, s_i=0.8^i",
                 m=1048576, n=32768, k=8, eps=1e-6, family="hadamard_device", rank=32, rho=0.8, s0=1.0),
+    # NEXT#2: the wide orientation (m < n, Alg. 1 else-branch P:88-92) on C2's transpose; one GPU
+    "c2w": dict(workload="dense fp32 16384x65536 (C2 transposed, m < n: U-first branch) in HBM, k=16, eps=1e-6, "
+                         "Hadamard known spectrum rank 32, s_i=0.8^i; run as the tall problem on a transposed "
+                         "device copy made at set_dense (outside the timed step)",
+                m=16384, n=65536, k=16, eps=1e-6, family="hadamard", rank=32, rho=0.8, s0=1.0),
     # the paper's per-node sparse matrix: 2^25 x 2^25, density ~1e-6 (32 nnz per row,
     # 1.07e9 nnz), randomly generated, k=8 (BASELINE configs[3]); its near-degenerate spectrum never
     # converges, so iterations are fixed as in the paper's OOM runs (100; here 10 per component)
@@ -162,7 +167,7 @@ def cpu_baseline(A, cfg, budget_s=15.0):
     A: dense fp32 array, or a CSR tuple for the sparse configs; value in the bench's own unit."""
     import oracle
     n = cfg["n"]
-    V0 = synth.v0_normal(n, 1, seed=2)
+    V0 = synth.v0_normal(min(cfg["m"], n), 1, seed=2)  # the iterate has length min(m, n)
     if isinstance(A, tuple):
         m_s = len(A[0]) - 1
         nnz = len(A[1])
@@ -191,7 +196,7 @@ def run_reference(args, cfg):
         return 0
     A = make_A(cfg, 0, cfg["m"])
     import oracle
-    V0 = synth.v0_normal(cfg["n"], 1, seed=2)
+    V0 = synth.v0_normal(min(cfg["m"], cfg["n"]), 1, seed=2)
     t0 = time.perf_counter()
     oracle.tsvd(A, 1, cfg["eps"], V0, fixed_T=1)
     per_pass = (time.perf_counter() - t0) / 2.0
@@ -272,7 +277,7 @@ def main():
     else:
         A_host = make_A(cfg, r0, r1)
         A_dev = torch.from_numpy(A_host).cuda()
-    V0 = synth.v0_normal(n, k, seed=2)
+    V0 = synth.v0_normal(min(m, n), k, seed=2)
 
     uid = None
     if world > 1:

@@ -117,8 +117,11 @@ typedef enum {
 /*
  * tsvd_create — new handle for an m x n fp32 problem, k components (k == -1 -> min(m, n),
  * P:71-72), stop rule |v0 . v1| >= 1 - eps.  Binds the current CUDA device.
+ * m < n (wide, Alg. 1 else-branch P:88-92, Eq. 3): the U-first branch, run as the tall
+ * problem on a transposed device copy of A (single GPU; the whole matrix is passed to
+ * tsvd_set_dense); the iterate and V0 have length m, U and V keep their meaning for A.
  * Errors: TSVD_ERR_ARG (m, n < 1; k < -1 or 0 or > min(m,n); eps not in (0,1); out == NULL),
- *         TSVD_ERR_UNSUPPORTED (dtype != F32, layout != ROW_MAJOR, m < n), TSVD_ERR_CUDA.
+ *         TSVD_ERR_UNSUPPORTED (dtype != F32, layout != ROW_MAJOR), TSVD_ERR_CUDA.
  */
 tsvd_status tsvd_create(tsvd_t *out, int64_t m, int64_t n, int32_t k, double eps, tsvd_dtype dtype,
                         tsvd_layout layout);
@@ -184,7 +187,8 @@ tsvd_status tsvd_set_factors(tsvd_t h, int32_t l, const float *U, const double *
 /*
  * tsvd_gram_apply — ONE implicit Gram-vector product y = X'^T (X' v) for the current l
  * factors (Eq. 2 in exact factored form; includes the cross-rank all-reduce).  v, y: host
- * fp64[n] (v is used as given, not normalised).  Blocking.  Errors: TSVD_ERR_STATE, CUDA/NCCL.
+ * fp64[min(m, n)] (m < n: y = X' X'^T v, Eq. 3; v is used as given, not normalised).  Blocking.
+ * Errors: TSVD_ERR_STATE, CUDA/NCCL.
  */
 tsvd_status tsvd_gram_apply(tsvd_t h, const double *v, double *y);
 

@@ -144,6 +144,11 @@ struct tsvd_s {
     bool have_V0 = false;
     int64_t v0_version = 1, v0_uploaded = 0;
     // out-of-memory degree 1 (host input): resident prefix [0, m_res) + streamed batches
+    // wide input (m < n): the handle runs the tall problem on A^T (a transposed device copy);
+    // U and V swap roles at the boundary
+    bool wide = false;
+    int64_t m_user = 0, n_user = 0;
+    float *At = nullptr;
     int placement = 0, qdepth = 3;
     int64_t work_bytes = 0;  // device workspace allocated by ensure_alloc (report: peak device bytes)
     int64_t resident_cap = -1, batch_rows_opt = 0;
@@ -1381,8 +1386,8 @@ tsvd_status tsvd_create(tsvd_t *out, int64_t m, int64_t n, int32_t k, double eps
         g_err = "bad arguments: need m,n >= 1, k in [1, min(m,n)] or -1, 0 < eps < 1";
         return TSVD_ERR_ARG;
     }
-    if (dtype != TSVD_F32 || layout != TSVD_ROW_MAJOR || m < n) {
-        g_err = "only fp32 row-major with m >= n in this version";
+    if (dtype != TSVD_F32 || layout != TSVD_ROW_MAJOR) {
+        g_err = "only fp32 row-major in this version";
         return TSVD_ERR_UNSUPPORTED;
     }
     const int64_t kk = k == -1 ? mn : k;
@@ -1391,6 +1396,10 @@ tsvd_status tsvd_create(tsvd_t *out, int64_t m, int64_t n, int32_t k, double eps
         return TSVD_ERR_UNSUPPORTED;
     }
     tsvd_t h = new tsvd_s();
+    h->m_user = m;
+    h->n_user = n;
+    h->wide = m < n;
+    if (h->wide) std::swap(m, n);  // internal tall problem: A^T, n x m
     h->m = m;
     h->n = n;
     h->k = (int32_t)kk;
@@ -1428,6 +1437,8 @@ tsvd_status tsvd_set_comm(tsvd_t h, int32_t rank, int32_t world, const void *uid
     if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world || (world > 1 && !uid))
         return h->fail(TSVD_ERR_ARG, "bad rank/world (world <= %d)", kMaxRanks);
     if (h->allocated || h->have_A) return h->fail(TSVD_ERR_STATE, "set_comm must precede set_dense");
+    if (h->wide && world > 1)
+        return h->fail(TSVD_ERR_UNSUPPORTED, "wide inputs (m < n) run on one GPU in this version (NEXT#2)");
     if (device != h->dev) {
         CK(cudaSetDevice(device));
         if (h->stream) cudaStreamDestroy(h->stream);
@@ -1547,8 +1558,65 @@ tsvd_status tsvd_set_init(tsvd_t h, const double *V0) {
     return TSVD_OK;
 }
 
+static tsvd_status set_dense_impl(tsvd_t h, const float *A, int64_t ld, int64_t row_begin, int64_t row_end,
+                                  tsvd_mem mem);
+
+// A^T into the handle's own buffer (n_user x round4(m_user)), from device or host A
+__global__ void transpose_f32(const float *__restrict__ in, int64_t rows, int64_t cols, int64_t ldi,
+                              float *__restrict__ out, int64_t ldo) {
+    __shared__ float tile[32][33];
+    const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t r = r0 + i, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * ldi + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t c = c0 + i, r = r0 + threadIdx.x;  // out row = input column
+        if (r < rows && c < cols) out[c * ldo + r] = tile[threadIdx.x][i];
+    }
+}
+
 tsvd_status tsvd_set_dense(tsvd_t h, const float *A, int64_t ld, int64_t row_begin, int64_t row_end, tsvd_mem mem) {
     if (!h) return TSVD_ERR_ARG;
+    if (!h->wide) return set_dense_impl(h, A, ld, row_begin, row_end, mem);
+    // wide: A is m_user x n_user (m < n); the tall solver runs on A^T (NEXT#2)
+    if (!A || ld < h->n_user) return h->fail(TSVD_ERR_ARG, "A == NULL or ld < n");
+    if (row_begin != 0 || row_end != h->m_user)
+        return h->fail(TSVD_ERR_SHAPE, "wide inputs are passed whole (rows [0, m))");
+    if (mem != TSVD_MEM_DEVICE && mem != TSVD_MEM_HOST_PINNED && mem != TSVD_MEM_HOST_PAGEABLE)
+        return h->fail(TSVD_ERR_ARG, "bad mem kind");
+    if (h->sparse) return h->fail(TSVD_ERR_STATE, "the input kind cannot change");
+    CK(cudaSetDevice(h->dev));
+    const int64_t mu = h->m_user, nu = h->n_user, ldt = round_up(mu, 4);
+    if (!h->At) {
+        cudaError_t e = cudaMalloc((void **)&h->At, (size_t)nu * ldt * sizeof(float));
+        if (e == cudaErrorMemoryAllocation) return h->fail(TSVD_ERR_NOMEM, "no room for the transposed copy of A");
+        CK(e);
+        CK(cudaMemsetAsync(h->At, 0, (size_t)nu * ldt * sizeof(float), h->stream));
+    }
+    const float *src = A;
+    float *tmp = nullptr;
+    int64_t lds = ld;
+    if (mem != TSVD_MEM_DEVICE) {  // stage the host matrix once, then transpose on the device
+        cudaError_t e = cudaMalloc((void **)&tmp, (size_t)mu * nu * sizeof(float));
+        if (e == cudaErrorMemoryAllocation) return h->fail(TSVD_ERR_NOMEM, "no room to stage the wide input");
+        CK(e);
+        CK(cudaMemcpy2DAsync(tmp, nu * sizeof(float), A, ld * sizeof(float), nu * sizeof(float), mu,
+                             cudaMemcpyHostToDevice, h->stream));
+        src = tmp;
+        lds = nu;
+    }
+    dim3 grid((unsigned)((nu + 31) / 32), (unsigned)((mu + 31) / 32));
+    transpose_f32<<<grid, dim3(32, 8), 0, h->stream>>>(src, mu, nu, lds, h->At, ldt);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
+    if (tmp) cudaFree(tmp);
+    return set_dense_impl(h, h->At, ldt, 0, nu, TSVD_MEM_DEVICE);
+}
+
+static tsvd_status set_dense_impl(tsvd_t h, const float *A, int64_t ld, int64_t row_begin, int64_t row_end,
+                                  tsvd_mem mem) {
     if (!A || ld < h->n) return h->fail(TSVD_ERR_ARG, "A == NULL or ld < n");
     if (row_begin < 0 || row_end > h->m || row_end <= row_begin)
         return h->fail(TSVD_ERR_SHAPE, "row range [%lld, %lld) outside [0, %lld)", (long long)row_begin,
@@ -1760,6 +1828,16 @@ tsvd_status tsvd_set_factors(tsvd_t h, int32_t l, const float *U, const double *
     if (!h->have_A) return h->fail(TSVD_ERR_STATE, "set_dense first");
     CK(cudaSetDevice(h->dev));
     TRY(ensure_alloc(h));
+    std::vector<float> uw;
+    std::vector<double> vw;
+    if (h->wide && l > 0) {  // the caller's U (m_user x l) is the tall V, its V (n_user x l) the tall U
+        uw.resize((size_t)h->m_g * l);
+        vw.resize((size_t)h->n * l);
+        for (size_t i = 0; i < uw.size(); ++i) uw[i] = (float)V[i];
+        for (size_t i = 0; i < vw.size(); ++i) vw[i] = (double)U[i];
+        U = uw.data();
+        V = vw.data();
+    }
     if (l > 0) {
         CK(cudaMemcpy2DAsync(h->U32, h->kpad * sizeof(float), U, l * sizeof(float), l * sizeof(float), h->m_g,
                              cudaMemcpyHostToDevice, h->stream));
@@ -1914,6 +1992,20 @@ tsvd_status tsvd_get_U_S_V(tsvd_t h, float *U, double *S, float *V) {
     if (!h) return TSVD_ERR_ARG;
     if (!h->allocated) return h->fail(TSVD_ERR_STATE, "nothing computed yet");
     CK(cudaSetDevice(h->dev));
+    if (h->wide) {  // A^T = V S U^T: the caller's U is the tall V (m_user x k), its V the tall U
+        std::vector<double> vt((size_t)h->n * h->k);
+        std::vector<float> ut((size_t)h->m_g * h->kpad);
+        CK(cudaMemcpyAsync(vt.data(), h->V64, vt.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(ut.data(), h->U32, ut.size() * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
+        if (S) CK(cudaMemcpyAsync(S, h->S64, h->k * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        for (int64_t r = 0; U && r < h->n; ++r)
+            for (int c = 0; c < h->k; ++c) U[r * h->k + c] = c < h->k_found ? (float)vt[r * h->k + c] : 0.f;
+        for (int64_t r = 0; V && r < h->m_g; ++r)
+            for (int c = 0; c < h->k; ++c) V[r * h->k + c] = c < h->k_found ? ut[r * h->kpad + c] : 0.f;
+        for (int c = h->k_found; S && c < h->k; ++c) S[c] = 0.0;
+        return TSVD_OK;
+    }
     if (U)
         CK(cudaMemcpy2DAsync(U, h->k * sizeof(float), h->U32, h->kpad * sizeof(float), h->k * sizeof(float), h->m_g,
                              cudaMemcpyDeviceToHost, h->stream));
@@ -1950,10 +2042,11 @@ tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
     static const char *colls[] = {"none", "peer-nvlink", "nccl"};
     snprintf(tmp, sizeof tmp,
              "\"m\": %lld, \"n\": %lld, \"k\": %d, \"eps\": %.3g, \"rank\": %d, \"world\": %d, \"rows\": [%lld, %lld], "
-             "\"k_found\": %d, \"total_iters\": %lld, \"run_ms\": %.4f, \"h2d_ms\": %.4f, \"n1_ms\": %.6f, "
+             "\"wide\": %s, \"k_found\": %d, \"total_iters\": %lld, \"run_ms\": %.4f, \"h2d_ms\": %.4f, \"n1_ms\": %.6f, "
              "\"n1_launches\": %lld, \"kernel_launches\": %lld, \"loop\": \"%s\", \"collective\": \"%s\", ",
-             (long long)h->m, (long long)h->n, h->k, h->eps, h->rank, h->world, (long long)h->row_begin,
-             (long long)h->row_end, h->k_found, (long long)h->total_iters, h->run_ms, h->h2d_ms, h->n1_ms,
+             (long long)h->m_user, (long long)h->n_user, h->k, h->eps, h->rank, h->world, (long long)h->row_begin,
+             (long long)h->row_end, h->wide ? "true" : "false", h->k_found, (long long)h->total_iters, h->run_ms, h->h2d_ms,
+             h->n1_ms,
              (long long)h->n1_launches, (long long)h->launches, h->loop_mode.c_str(), colls[h->coll]);
     s += tmp;
     snprintf(tmp, sizeof tmp,
@@ -2047,7 +2140,7 @@ void tsvd_destroy(tsvd_t h) {
     }
     void *dev_ptrs[] = {h->A_own, h->U32, h->V64, h->S64, h->ybuf, h->yw, h->V0d, h->c64, h->ypart,
                         h->wpart, h->part, h->u64, h->sq_part, h->sig2, h->st, h->stats, h->sym, h->gbar,
-                        h->trace_d, h->work, h->tl_d, h->vprev32, h->px_mem, h->y32, h->t32};
+                        h->trace_d, h->work, h->tl_d, h->vprev32, h->px_mem, h->y32, h->t32, h->At};
     if (h->trace_f) fclose(h->trace_f);
     for (void *p : dev_ptrs)
         if (p) cudaFree(p);

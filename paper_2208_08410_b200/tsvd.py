@@ -247,7 +247,7 @@ class TSVD:
 
     def gram_apply(self, v):
         v = np.ascontiguousarray(v, dtype=np.float64)
-        y = np.empty(self.n, dtype=np.float64)
+        y = np.empty(min(self.m, self.n), dtype=np.float64)  # wide (m < n): the U-first mirror
         tsvd_gram_apply(self.h, v, y)
         return y
 

@@ -339,9 +339,14 @@ def test_argument_errors():
     with pytest.raises(P.TsvdError) as ei:
         P.tsvd_create(10, 5, 2, 1.5)
     assert ei.value.status == P.ERR_ARG
+    h = P.tsvd_create(5, 10, 2, 1e-6)  # wide: single GPU only, the whole matrix at once
     with pytest.raises(P.TsvdError) as ei:
-        P.tsvd_create(5, 10, 2, 1e-6)
+        P.tsvd_set_comm(h, 0, 2, b"\0" * 128, 0)
     assert ei.value.status == P.ERR_UNSUPPORTED
+    with pytest.raises(P.TsvdError) as ei:
+        P.tsvd_set_dense(h, np.zeros((5, 10), np.float32), 10, 0, 3, P.MEM_HOST_PAGEABLE)
+    assert ei.value.status == P.ERR_SHAPE
+    P.tsvd_destroy(h)
     # n > 16384 needs the cluster variant (not in this version)
     t = P.TSVD(40000, 40000, 1, 1e-6)
     with pytest.raises(P.TsvdError) as ei:
@@ -370,3 +375,36 @@ def test_internal_generator_is_seeded():
         t.close()
     np.testing.assert_array_equal(outs[0], outs[1])
     np.testing.assert_allclose(outs[0], 4.0 * 0.6 ** np.arange(k), rtol=1e-5)
+
+
+@pytest.mark.parametrize("m,n,k,src", [(256, 700, 4, "device"), (300, 4099, 3, "pinned"), (61, 1000, 5, "pageable"),
+                                       (1000, 16385, 2, "device")])
+def test_wide_matrix_parity(m, n, k, src):
+    """m < n (NEXT#2, Alg. 1 else-branch P:88-92): the U-first mirror, run as the tall problem on a
+    transposed copy of A; the oracle runs the mirrored branch (V0 of length m)."""
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(min(m, 48), 5.0, 0.75), seed=m + n)
+    V0 = synth.v0_normal(m, k, seed=k + 11)
+    ref = oracle.tsvd(A, k, 1e-6, V0)
+    t = P.TSVD(m, n, k, 1e-6)
+    t.set_init(V0)
+    if src == "device":
+        t.set_dense(torch.from_numpy(A).cuda())
+    elif src == "pinned":
+        t.set_dense(torch.from_numpy(A).pin_memory())
+    else:
+        t.set_dense(A)
+    rc = t.run()
+    U, S, V = t.result()
+    kf, iters, _ = t.info()
+    rep = t.report()
+    rng = np.random.default_rng(3)
+    u = rng.standard_normal(m)
+    y = t.gram_apply(u)
+    t.close()
+    assert rc == P.OK and rep["wide"] is True and rep["m"] == m and rep["n"] == n
+    assert U.shape == (m, k) and V.shape == (n, k)
+    _assert_parity(A, ref, U, S, V, kf, k)
+    assert np.all(np.abs(iters - ref.iters) <= 1), (iters, ref.iters)
+    # the product with the run's own factors (exported U is the fp32 copy of the fp64 iterate)
+    want = oracle.gram_apply_wide(A, U.astype(np.float64), S, V.astype(np.float64), u)
+    assert np.linalg.norm(y - want) / np.linalg.norm(want) <= 1e-4
