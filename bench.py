@@ -242,6 +242,11 @@ def main():
                     help="TSVD_OPT_PDL (default: the library's default)")
     ap.add_argument("--row-order", type=int, default=None, choices=[0, 1],
                     help="TSVD_OPT_ROW_ORDER (default: the library's default)")
+    ap.add_argument("--method", type=int, default=0, choices=[0, 1],
+                    help="TSVD_OPT_METHOD: 0 implicit Gram-vector (default), 1 explicit Gram (NEXT#1; the Gram is "
+                         "rebuilt inside every timed step)")
+    ap.add_argument("--fixed-iters", type=int, default=None,
+                    help="override the config's iteration rule with a fixed count (the paper's benchmark mode, P:404)")
     ap.add_argument("--sparse-block", type=int, default=None,
                     help="TSVD_OPT_SPARSE_BLOCK: index-block width in elements (default: the library's)")
     args = ap.parse_args()
@@ -309,6 +314,10 @@ def main():
         t.set_option(P.OPT_PDL, args.pdl)
     if args.row_order is not None:
         t.set_option(P.OPT_ROW_ORDER, args.row_order)
+    if args.method:
+        t.set_option(P.OPT_METHOD, args.method)
+    if args.fixed_iters:
+        t.set_option(P.OPT_FIXED_ITERS, args.fixed_iters)
     stream = torch.cuda.ExternalStream(t.stream())
 
     def barrier():
@@ -324,6 +333,8 @@ def main():
         return float(tt.item())
 
     def one_step():
+        if args.method == 1 and not sparse and not stream_cfg:
+            t.set_dense(A_dev, r0, r1)  # explicit Gram: B0 = A^T A is rebuilt inside every step
         t.set_factors(None, None, None)  # restart from component 0
         return t.run()
 
@@ -386,6 +397,11 @@ def main():
         alg_bytes = sum(body[l] * (4.0 * mg * n + 4.0 * mg * (l if l % 4 == 0 else (l + 3) // 4 * 4) + 4.0 * n)
                         for l in range(kf))
         kern_ms, kernel = ps["ms"], "gv_persist (N7: a component's passes + in-kernel reduction)"
+        if rt.get("method") == "explicit-gram":  # gb_persist streams the n x n Gram B0 each iteration
+            body = [int(iters[l]) for l in range(kf)]
+            ps_passes = sum(body)
+            alg_bytes = sum(body[l] * (4.0 * n * n + 12.0 * n * l + 8.0 * n) for l in range(kf))
+            kernel = "gb_persist (explicit Gram: B0 = A^T A streamed per iteration)"
         n1_ms_per_launch = kern_ms / ps["launches"]
         per_launch_bytes = alg_bytes / ps["launches"]
     achieved = per_launch_bytes / (n1_ms_per_launch / 1e3) / 1e9
@@ -480,8 +496,10 @@ def main():
             "check": {"sigma_max_rel_err_vs_planted": sig_err},
             "roofline": roof,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks.summary(),
-            "plan": rep["plan"], "loop": rep["loop"],
+            "plan": rep["plan"], "loop": rep["loop"], "method": rep.get("method", "gram-vector"),
         }
+        if rep.get("method") == "explicit-gram":
+            line["gram_ms_per_step"] = rep.get("gram_ms")
         print(json.dumps(line), flush=True)
     t.close()
     if world > 1:

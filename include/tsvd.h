@@ -108,10 +108,16 @@ typedef enum {
                                     (grid barriers, in-kernel reduction and stop test; no per-
                                     iteration kernel boundaries); 0 = one fused pass + finalize
                                     kernel per iteration (needed to profile single passes)          */
-    TSVD_OPT_SPARSE_BLOCK = 20   /* sparse: width (elements) of the index blocks the gathers are
+    TSVD_OPT_SPARSE_BLOCK = 20,  /* sparse: width (elements) of the index blocks the gathers are
                                     split into so that each launch's block of the fp32 gathered
                                     vector stays in L2; 0 (default) = 32 MiB of fp32 (n > 8M
                                     columns / rows => several blocks). Read by tsvd_set_csr          */
+    TSVD_OPT_METHOD = 21         /* 0 (default): implicit Gram-vector products (Eq. 2, the north star);
+                                    1: explicit Gram (Alg. 2 lines 6-9 with Alg. 3's Gram, P:114-121,
+                                    P:220-249): B0 = A^T A once (TF32x3 tensor-core GEMMs), then per
+                                    iteration y = B0 v - P c - V g with P = A^T U, Q = U^T U (exact
+                                    deflation, no U^T U = I assumption); dense, resident, one GPU,
+                                    n <= 16384; pays off when iterations per component are many    */
 } tsvd_option;
 
 /*

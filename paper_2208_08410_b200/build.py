@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtsvd.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("tsvd.cu",)]
-DEPS = SOURCES + [os.path.join(CSRC, "gram_kernels.cuh"), os.path.join(CSRC, "fin_kernels.cuh"), os.path.join(CSRC, "sparse_kernels.cuh"), os.path.join(CSRC, "persist_kernels.cuh"), os.path.join(ROOT, "include", "tsvd.h")]
+DEPS = SOURCES + [os.path.join(CSRC, "gram_kernels.cuh"), os.path.join(CSRC, "fin_kernels.cuh"), os.path.join(CSRC, "sparse_kernels.cuh"), os.path.join(CSRC, "persist_kernels.cuh"), os.path.join(CSRC, "explicit_kernels.cuh"), os.path.join(ROOT, "include", "tsvd.h")]
 
 
 def nccl_dir() -> str:
@@ -20,6 +20,15 @@ def nccl_dir() -> str:
         if os.path.exists(os.path.join(p, "include", "nccl.h")):
             return p
     raise RuntimeError("pip NCCL headers not found")
+
+
+def cublas_dir() -> str:
+    """The cuBLAS torch loads (pip nvidia-cublas): the explicit-Gram path's B0 = A^T A GEMMs."""
+    import nvidia.cublas  # noqa: F401
+    for p in nvidia.cublas.__path__:
+        if os.path.exists(os.path.join(p, "include", "cublas_v2.h")):
+            return p
+    raise RuntimeError("pip cuBLAS headers not found")
 
 
 def nvcc() -> str:
@@ -33,12 +42,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in DEPS):
         return LIB
     nd = nccl_dir()
+    cb = cublas_dir()
     tmp = LIB + f".{os.getpid()}.tmp"
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
+           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"), "-I", os.path.join(cb, "include"),
            *SOURCES, "-o", tmp,
-           "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(nd, "lib")]
+           "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(nd, "lib"),
+           "-L", os.path.join(cb, "lib"), "-l:libcublas.so.12", "-Xlinker", "-rpath," + os.path.join(cb, "lib")]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -157,6 +157,7 @@ struct GvParams {
     int32_t vp_bytes;           // TWO: shared memory reserved for vprev (0 otherwise)
     int32_t serpentine;         // 1: odd iterations walk each CTA's row range backwards, so the
                                 // rows the previous pass read last (still in L2) are read first
+    int32_t store_t;            // explicit-Gram extraction: also store t_r in u_out and sum t_r^2
 };
 
 // Column-slice reduction of the per-CTA partials at the end of N1 (reduce_mode 1/2).  CTA c owns
@@ -322,7 +323,8 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     const LoopState *st = p.st;
     griddep_launch();
     griddep_wait();
-    if (st->stop || (!EXTRACT && st->done)) return;
+    // (store_t: the explicit path's extraction pass runs after its component is done)
+    if (st->stop || (!EXTRACT && st->done && !p.store_t)) return;
     if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 4 + 0] = globaltimer_ns();
     if (!EXTRACT && p.tl && blockIdx.x == 0 && threadIdx.x == 0) {  // debug timeline (TSVD_TIMELINE)
         const unsigned long long idx = atomicAdd(p.tl, 1ull) % 4096;
@@ -607,6 +609,10 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
             }
             if (tid < l) wacc += t * (double)ur;
             if (TWO && tid == tf_thread) wfresh += t * u;  // sigma_f U_f^T t = u^T t
+            if (!TWO && p.store_t && tid == 0 && owner) {
+                p.u_out[grow] = t;
+                sq += t * t;
+            }
             if (++run == p.run_rows) {
                 flush();
                 run = 0;
@@ -622,6 +628,7 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
             double *wp = p.wpart + (int64_t)part_id * p.wpart_ld + tid;
             *wp = p.accumulate ? *wp + wacc : wacc;
         }
+        if (!TWO && p.store_t && tid == 0 && owner) p.sq_part[part_id] = p.accumulate ? p.sq_part[part_id] + sq : sq;
         if (TWO) {
             if (tid == tf_thread) {
                 double *wp = p.wpart + (int64_t)part_id * p.wpart_ld + (p.l - 1);

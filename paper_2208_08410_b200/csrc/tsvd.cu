@@ -25,6 +25,8 @@
 #include "gram_kernels.cuh"
 #include "sparse_kernels.cuh"
 #include "persist_kernels.cuh"
+#include "explicit_kernels.cuh"
+#include <cublas_v2.h>
 
 using namespace tsvd;
 
@@ -81,6 +83,21 @@ SpFn pick_csr(int L) {
 inline SpFn pick_csc(int L) { return L == 8 ? csc_spmvT<8> : L == 16 ? csc_spmvT<16> : csc_spmvT<32>; }
 // lanes per segment from the mean segment length (entries per row / column per index block)
 inline int pick_lanes(double mean_len) { return mean_len >= 24.0 ? 32 : mean_len >= 12.0 ? 16 : 8; }
+
+using GbFn = void (*)(const GbParams);
+template <int T>
+GbFn pick_gb_nv(int nv) {
+    return nv == 1 ? gb_persist<T, 1> : nv == 2 ? gb_persist<T, 2> : nv == 4 ? gb_persist<T, 4> : gb_persist<T, 8>;
+}
+inline GbFn pick_gb(int T, int nv) {
+    switch (T) {
+    case 32: return pick_gb_nv<32>(nv);
+    case 64: return pick_gb_nv<64>(nv);
+    case 128: return pick_gb_nv<128>(nv);
+    case 256: return pick_gb_nv<256>(nv);
+    default: return pick_gb_nv<512>(nv);
+    }
+}
 
 using PsFn = void (*)(const PsParams);
 
@@ -216,6 +233,18 @@ struct tsvd_s {
     int pdl_opt = 1;       // TSVD_OPT_PDL
     int serp_opt = 1;      // TSVD_OPT_ROW_ORDER
     int persist_opt = 1;   // TSVD_OPT_PERSISTENT
+    // explicit-Gram path (TSVD_OPT_METHOD = 1, NEXT#1): B0 = A^T A, P = A^T U, Q = U^T U
+    int method = 0;
+    GbFn gb = nullptr;
+    int S_gb = 0;
+    size_t smem_gb = 0;
+    float *B0 = nullptr, *Pm = nullptr, *g_hi = nullptr, *g_lo = nullptr;  // Gram, A^T U, TF32 split of A
+    double *Qm = nullptr, *gpart = nullptr, *zero64 = nullptr;
+    int64_t ldb0 = 0;
+    bool B0_ok = false;
+    int pq_l = 0;          // components whose P / Q columns are valid
+    double gram_ms = 0.0;  // B0 build time of the last build
+    cublasHandle_t cublas = nullptr;
     PsFn gv_ps = nullptr;  // N7: one persistent cooperative kernel per component (null: unsupported)
     int S_ps = 0;
     size_t smem_ps = 0;
@@ -405,6 +434,25 @@ static tsvd_status plan(tsvd_t h) {
                 h->gv_ps = fn;
                 h->S_ps = Sp;
                 h->smem_ps = sm;
+            }
+        }
+    }
+    // explicit-Gram iteration kernel: the same ring over rows of B0 (n x n)
+    h->gb = nullptr;
+    if (split == 1) {
+        const int64_t extra = kMaxStages * 8 + (int64_t)(2 * (T / 32) + 4 * h->kpad + 2) * 8;
+        int Sg = S;
+        while (Sg > 2 && ((int64_t)Sg * h->stage_bytes + extra) * h->cps > kSmemBudget) --Sg;
+        GbFn fn = pick_gb(T, NV);
+        const size_t sm = (size_t)Sg * h->stage_bytes + (size_t)extra;
+        if (((int64_t)Sg * h->stage_bytes + extra) * h->cps <= kSmemBudget) {
+            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            int occ = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, T, sm));
+            if (occ * h->sms >= h->grid) {
+                h->gb = fn;
+                h->S_gb = Sg;
+                h->smem_gb = sm;
             }
         }
     }
@@ -1286,6 +1334,169 @@ static tsvd_status build_graph(tsvd_t h, int l0) {
 }
 
 // Host-driven loop: one pinned D2H state read per iteration; optional CUDA events around N1.
+// ---------------------------------------------------------------- explicit-Gram path (NEXT#1)
+#define CB(x)                                                                                  \
+    do {                                                                                       \
+        cublasStatus_t cb_ = (x);                                                              \
+        if (cb_ != CUBLAS_STATUS_SUCCESS) return h->fail(TSVD_ERR_CUDA, "cuBLAS error %d", (int)cb_); \
+    } while (0)
+
+// B0 = A^T A (Alg. 3's Gram) with three TF32 tensor-core GEMMs of the hi/lo split of A:
+// A^T A ~= Ah^T Ah + Ah^T Al + Al^T Ah (fp32-level products; cuBLAS for the plain library GEMM).
+static tsvd_status build_gram(tsvd_t h) {
+    auto t0 = std::chrono::steady_clock::now();
+    const int64_t m = h->m_g, n = h->n;
+    h->ldb0 = round_up(n, 4);
+    if (!h->B0) {
+        cudaError_t e = cudaMalloc((void **)&h->B0, (size_t)n * h->ldb0 * sizeof(float));
+        if (e == cudaErrorMemoryAllocation) return h->fail(TSVD_ERR_NOMEM, "no room for the n x n Gram");
+        CK(e);
+        CK(cudaMemsetAsync(h->B0, 0, (size_t)n * h->ldb0 * sizeof(float), h->stream));
+    }
+    if (!h->g_hi) {  // kept for later builds (a new A of the same shape)
+        cudaError_t e = cudaMalloc((void **)&h->g_hi, (size_t)m * n * sizeof(float));
+        if (!e) e = cudaMalloc((void **)&h->g_lo, (size_t)m * n * sizeof(float));
+        if (e) {
+            cudaFree(h->g_hi);
+            h->g_hi = h->g_lo = nullptr;
+            cudaGetLastError();
+            return h->fail(TSVD_ERR_NOMEM, "no room for the TF32 split of A");
+        }
+    }
+    float *hi = h->g_hi, *lo = h->g_lo;
+    split_tf32<<<h->sms * 8, 256, 0, h->stream>>>(h->A_use, m, n, h->ld_use, hi, lo);
+    CK(cudaGetLastError());
+    if (!h->cublas) CB(cublasCreate(&h->cublas));
+    CB(cublasSetStream(h->cublas, h->stream));
+    // column-major view: a row-major m x n slab is an n x m matrix (lda = n); A^T A = A' A'^T.
+    // Three TF32 GEMMs (measured: 162 ms at C2; cuBLAS SYRK + SYR2K in TF32 math mode took 785 ms)
+    const float one = 1.f, zero = 0.f;
+    const float *ops[3][2] = {{hi, hi}, {hi, lo}, {lo, hi}};
+    for (int g = 0; g < 3; ++g)
+        CB(cublasGemmEx(h->cublas, CUBLAS_OP_N, CUBLAS_OP_T, (int)n, (int)n, (int)m, &one, ops[g][0], CUDA_R_32F,
+                        (int)n, ops[g][1], CUDA_R_32F, (int)n, g == 0 ? &zero : &one, h->B0, CUDA_R_32F, (int)h->ldb0,
+                        CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT));
+    CK(cudaStreamSynchronize(h->stream));
+    h->B0_ok = true;
+    h->gram_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return TSVD_OK;
+}
+
+static tsvd_status run_explicit(tsvd_t h, int l0) {
+    if (h->sparse || h->streaming || h->world > 1 || h->split != 1 || !h->gb)
+        return h->fail(TSVD_ERR_UNSUPPORTED, "METHOD=1 (explicit Gram) needs a dense, HBM-resident, single-GPU input "
+                                             "with n <= 16384");
+    if (l0 > h->pq_l)
+        return h->fail(TSVD_ERR_UNSUPPORTED, "METHOD=1 resumes only from factors it computed itself");
+    const int64_t n = h->n;
+    if (!h->Pm) {
+        CK(cudaMalloc((void **)&h->Pm, (size_t)n * h->kpad * sizeof(float)));
+        CK(cudaMalloc((void **)&h->Qm, (size_t)h->k * h->k * sizeof(double)));
+        CK(cudaMalloc((void **)&h->gpart, (size_t)2 * h->grid * (2 + 2 * h->kpad) * sizeof(double)));
+        CK(cudaMalloc((void **)&h->zero64, (size_t)h->kpad * sizeof(double)));
+        CK(cudaMemsetAsync(h->Pm, 0, (size_t)n * h->kpad * sizeof(float), h->stream));
+        CK(cudaMemsetAsync(h->Qm, 0, (size_t)h->k * h->k * sizeof(double), h->stream));
+        CK(cudaMemsetAsync(h->zero64, 0, (size_t)h->kpad * sizeof(double), h->stream));
+    }
+    if (!h->B0_ok) TRY(build_gram(h));
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (h->timing) {
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+    }
+    for (int l = l0; l < h->k; ++l) {
+        TRY(launch_init(h, h->stream, l));  // x -> y_cur, ||x||
+        GbParams g{};
+        g.B = h->B0;
+        g.ldb = h->ldb0;
+        g.rows = n;
+        g.n = (int32_t)n;
+        g.n4 = (int32_t)((n + 3) / 4);
+        g.P = h->Pm;
+        g.ldp = h->kpad;
+        g.V = h->V64;
+        g.ldv = h->k;
+        g.S = h->S64;
+        g.Q = h->Qm;
+        g.ldq = h->k;
+        g.l = l;
+        g.stages = h->S_gb;
+        g.stage_bytes = h->stage_bytes;
+        g.row_bytes = h->row_bytes;
+        g.ybuf = h->ybuf;
+        g.ystride = h->ystride;
+        g.st = h->st;
+        g.c = h->c64;
+        g.part = h->gpart;
+        g.part_ld = 2 + 2 * h->kpad;
+        g.gbar = h->gbar;
+        g.eps = h->eps;
+        g.fixed_T = h->fixed_T;
+        g.max_iter = h->max_iter;
+        g.serpentine = h->serp_opt;
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.gridDim = dim3(h->grid);
+        cfg.blockDim = dim3(h->T);
+        cfg.dynamicSmemBytes = h->smem_gb;
+        cfg.stream = h->stream;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (e0) CK(cudaEventRecord(e0, h->stream));
+        CK(cudaLaunchKernelEx(&cfg, h->gb, g));
+        if (e1) CK(cudaEventRecord(e1, h->stream));
+        // extraction + the new columns of P = A^T U and Q = U^T U: one fused pass, c = 0
+        GvParams q = gv_params(h, l, false);
+        q.c = h->zero64;
+        q.store_t = 1;
+        q.tl = nullptr;
+        q.trace = nullptr;
+        CK(launch_n1(h, h->gv, q, h->stream));
+        GxParams x{};
+        x.rows = h->m_g;
+        x.n = n;
+        x.l = l;
+        x.parts = h->parts;
+        x.ldu = h->kpad;
+        x.ldp = h->kpad;
+        x.ldv = h->k;
+        x.ldq = h->k;
+        x.u_out = h->u64;
+        x.ypart = h->ypart;
+        x.wpart = h->wpart;
+        x.sq_part = h->sq_part;
+        x.ypart_ld = h->ypart_ld;
+        x.wpart_ld = h->kpad;
+        x.ybuf = h->ybuf;
+        x.ystride = h->ystride;
+        x.U = h->U32;
+        x.P = h->Pm;
+        x.V = h->V64;
+        x.S = h->S64;
+        x.Q = h->Qm;
+        x.stat = h->stats;
+        x.st = h->st;
+        const int blocks = (int)std::min<int64_t>((std::max(h->m_g, n) + 255) / 256, (int64_t)h->sms * 8);
+        CK(launch_k(h, gram_ext_finish, blocks, 256, 0, h->stream, 1, x));
+        CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        if (h->timing) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            h->ps_ms += ms;
+            h->ps_launches += 1;
+        }
+        if (h->st_host->stop) break;
+        h->pq_l = l + 1;
+    }
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    h->loop_mode = h->timing ? "explicit-gram+events" : "explicit-gram";
+    return TSVD_OK;
+}
+
 static tsvd_status run_host_loop(tsvd_t h, int l0) {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (h->timing) {
@@ -1522,6 +1733,10 @@ tsvd_status tsvd_set_option(tsvd_t h, int32_t key, int64_t value) {
     case TSVD_OPT_PERSISTENT:
         h->persist_opt = value != 0;
         break;
+    case TSVD_OPT_METHOD:
+        if (value < 0 || value > 1) return h->fail(TSVD_ERR_ARG, "METHOD in 0..1");
+        h->method = (int)value;
+        break;
     case TSVD_OPT_SPARSE_BLOCK:
         if (value < 0) return h->fail(TSVD_ERR_ARG, "SPARSE_BLOCK >= 0");
         h->sp_block_opt = value;
@@ -1635,6 +1850,8 @@ static tsvd_status set_dense_impl(tsvd_t h, const float *A, int64_t ld, int64_t 
     h->mem = mem;
     h->have_A = true;
     h->graph_l0 = -1;
+    h->B0_ok = false;  // explicit path: the Gram of the new A is built at the next run
+    h->pq_l = 0;
     if (mem == TSVD_MEM_DEVICE) {
         const bool aligned = ((uintptr_t)A % 16 == 0) && (ld % 4 == 0);
         if (aligned) {
@@ -1904,8 +2121,13 @@ tsvd_status tsvd_run(tsvd_t h) {
     h->streamed_bytes = 0;
     h->streamed_batches = 0;
     // the graph needs every step to be a device kernel: no NCCL call, no host->device streaming
-    const bool graph = h->use_graph && !h->timing && h->coll != COLL_NCCL && !h->streaming;
+    const bool explicit_gram = h->method == 1;
+    const bool graph = !explicit_gram && h->use_graph && !h->timing && h->coll != COLL_NCCL && !h->streaming;
     bool ran = false;
+    if (explicit_gram) {
+        TRY(run_explicit(h, l0));
+        ran = true;
+    }
     if (graph) {
         tsvd_status gs = TSVD_OK;
         if (!h->exec || h->graph_l0 != l0) gs = build_graph(h, l0);
@@ -1927,7 +2149,7 @@ tsvd_status tsvd_run(tsvd_t h) {
     if (h->st_host->status == -7 && h->st_host->stop)
         return h->fail(TSVD_ERR_NUMERIC, "non-finite value or zero initial vector");
     tsvd_status result = TSVD_OK;
-    h->fused_ext_used = fuse_ext(h) && h->k - l0 > 1;
+    h->fused_ext_used = !explicit_gram && fuse_ext(h) && h->k - l0 > 1;
     // our kernels per iteration / extraction (NCCL calls not counted)
     int64_t per_pass = 1;
     if (h->streaming) per_pass = (h->m_res > 0 ? 1 : 0) + (h->m_g - h->m_res + h->batch_rows - 1) / h->batch_rows;
@@ -1943,9 +2165,11 @@ tsvd_status tsvd_run(tsvd_t h) {
         const int64_t issued = h->loop_mode == "graph-while"
                                    ? std::max<int64_t>(1, (body_it + h->unroll - 1) / h->unroll) * h->unroll
                                    : body_it;
-        const bool ps = use_persist(h);
-        if (ps) h->ps_passes += body_it;
-        if (ps && h->fused_ext_used)  // chain: [init | two-vector pass] + one persistent launch
+        const bool ps = !explicit_gram && use_persist(h);
+        if (ps || explicit_gram) h->ps_passes += body_it;
+        if (explicit_gram)  // init + the B0 iteration kernel + the extraction pass + its finish
+            h->launches += 4;
+        else if (ps && h->fused_ext_used)  // chain: [init | two-vector pass] + one persistent launch
             h->launches += 2 + (l == h->k - 1 ? per_ext : 0);
         else
             h->launches += 1 + (ff ? per_iter : 0) + (ps ? 1 : per_iter * issued) +
@@ -2051,9 +2275,10 @@ tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
     s += tmp;
     snprintf(tmp, sizeof tmp,
              "\"persistent\": {\"enabled\": %s, \"stages\": %d, \"smem\": %zu, \"ms\": %.6f, \"launches\": %lld, "
-             "\"passes\": %lld}, ",
-             use_persist(h) ? "true" : "false", h->S_ps, h->smem_ps, h->ps_ms, (long long)h->ps_launches,
-             (long long)h->ps_passes);
+             "\"passes\": %lld}, \"method\": \"%s\", \"gram_ms\": %.3f, ",
+             (use_persist(h) || h->method == 1) ? "true" : "false", h->method == 1 ? h->S_gb : h->S_ps,
+             h->method == 1 ? h->smem_gb : h->smem_ps, h->ps_ms, (long long)h->ps_launches, (long long)h->ps_passes,
+             h->method == 1 ? "explicit-gram" : "gram-vector", h->gram_ms);
     s += tmp;
     snprintf(tmp, sizeof tmp,
              "\"plan\": {\"T\": %d, \"NV\": %d, \"stages\": %d, \"ctas_per_sm\": %d, \"grid\": %d, \"smem\": %zu, "
@@ -2140,7 +2365,9 @@ void tsvd_destroy(tsvd_t h) {
     }
     void *dev_ptrs[] = {h->A_own, h->U32, h->V64, h->S64, h->ybuf, h->yw, h->V0d, h->c64, h->ypart,
                         h->wpart, h->part, h->u64, h->sq_part, h->sig2, h->st, h->stats, h->sym, h->gbar,
-                        h->trace_d, h->work, h->tl_d, h->vprev32, h->px_mem, h->y32, h->t32, h->At};
+                        h->trace_d, h->work, h->tl_d, h->vprev32, h->px_mem, h->y32, h->t32, h->At,
+                        h->B0, h->Pm, h->Qm, h->gpart, h->zero64, h->g_hi, h->g_lo};
+    if (h->cublas) cublasDestroy(h->cublas);
     if (h->trace_f) fclose(h->trace_f);
     for (void *p : dev_ptrs)
         if (p) cudaFree(p);

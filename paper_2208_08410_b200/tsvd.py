@@ -34,6 +34,7 @@ OPT_PDL = 17  # 1 (default): programmatic dependent launch between the loop's ke
 OPT_ROW_ORDER = 18  # 1 (default): serpentine row order (odd iterations backwards, L2 reuse); 0 forward
 OPT_PERSISTENT = 19  # 1 (default): a component's iterations in one cooperative kernel (single GPU)
 OPT_SPARSE_BLOCK = 20  # sparse: index-block width (elements) for L2-resident gathers; 0 = auto (set before set_csr)
+OPT_METHOD = 21  # 0 (default): implicit Gram-vector path; 1: explicit Gram (B0 = A^T A once, NEXT#1)
 F32, ROW_MAJOR = 0, 0
 
 _lib = None

@@ -408,3 +408,35 @@ def test_wide_matrix_parity(m, n, k, src):
     # the product with the run's own factors (exported U is the fp32 copy of the fp64 iterate)
     want = oracle.gram_apply_wide(A, U.astype(np.float64), S, V.astype(np.float64), u)
     assert np.linalg.norm(y - want) / np.linalg.norm(want) <= 1e-4
+
+
+@pytest.mark.parametrize("m,n,k,T", [(2000, 500, 5, 0), (4200, 4099, 3, 0), (1500, 400, 3, 12), (700, 64, 4, 0),
+                                     (16500, 16384, 2, 3)])
+def test_explicit_gram_parity(m, n, k, T):
+    """METHOD=1 (NEXT#1, Alg. 2 lines 6-9 with Alg. 3's Gram): B0 = A^T A once (TF32x3 GEMMs), then
+    y = B0 v - P c - V g with P = A^T U, Q = U^T U (exact deflation) — against the oracle and the
+    implicit path."""
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(min(n, 48), 5.0, 0.75), seed=m + n + k)
+    V0 = synth.v0_normal(n, k, seed=k + 21)
+    opts = {"fixed_iters": T} if T else {}
+    ref = oracle.tsvd(A, k, 1e-6, V0, fixed_T=T)
+    ex = _gpu_tsvd(A, k, 1e-6, V0, method=1, **opts)
+    im = _gpu_tsvd(A, k, 1e-6, V0, **opts)
+    assert ex[0] == P.OK and ex[7]["method"] == "explicit-gram" and ex[7]["loop"].startswith("explicit")
+    _assert_parity(A, ref, *ex[1:5], k)
+    assert np.all(np.abs(ex[5] - ref.iters) <= 1), (ex[5], ref.iters)
+    np.testing.assert_allclose(ex[2], im[2], rtol=1e-5)
+    # run twice on one handle: the Gram is built once and reused
+    t = P.TSVD(m, n, k, 1e-6)
+    t.set_option(P.OPT_METHOD, 1)
+    for key, val in opts.items():
+        t.set_option(getattr(P, "OPT_" + key.upper()), val)
+    t.set_init(V0)
+    t.set_dense(torch.from_numpy(A).cuda())
+    t.run()
+    S1 = t.result()[1]
+    t.set_factors(None, None, None)
+    t.run()
+    S2 = t.result()[1]
+    t.close()
+    np.testing.assert_array_equal(S1, S2)
