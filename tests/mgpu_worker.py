@@ -50,6 +50,7 @@ def main():
     t.set_option(P.OPT_PERSISTENT, int(os.environ.get("TSVD_PERSISTENT", "1")))
     if sparse:
         t.set_option(P.OPT_FIXED_ITERS, 12)  # paper-like spectrum: fixed iterations
+        t.set_option(P.OPT_SPARSE_BLOCK, int(os.environ.get("TSVD_SPARSE_BLOCK", "0")))
     t.set_init(V0)
     if sparse:
         t.set_csr(*synth.random_csr(m, n, 9, seed=21, rows=(r0, r1), chunk=512), row_begin=r0, row_end=r1)

@@ -32,15 +32,16 @@ def test_row_partition_parity(world, collective, persistent):
     assert want in r.stdout
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_sparse_row_partition_parity(world):
-    """Sparse CSR slabs per rank, length-n partial y summed by ncclAllReduce each iteration."""
+@pytest.mark.parametrize("world,block", [(2, 0), (4, 0), (2, 700)])
+def test_sparse_row_partition_parity(world, block):
+    """Sparse CSR slabs per rank, length-n partial y summed by ncclAllReduce each iteration
+    (block > 0: the L2 index blocking forced small, several launches per product on every rank)."""
     if not torch.cuda.is_available() or torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29500 + world),
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + world + (1 if block else 0)),
            os.path.join(ROOT, "tests", "mgpu_worker.py")]
-    env = dict(os.environ, TSVD_SPARSE="1")
+    env = dict(os.environ, TSVD_SPARSE="1", TSVD_SPARSE_BLOCK=str(block))
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
