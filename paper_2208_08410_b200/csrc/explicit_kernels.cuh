@@ -228,8 +228,7 @@ __global__ void __launch_bounds__(T) gb_persist(const GbParams p) {
                 feed();
             }
             double y = 0.0;
-#pragma unroll
-            for (int w = 0; w < NW; ++w) y += red[rb * NW + w];
+            y = sum_warps<NW>(red + rb * NW, lane);
             rb ^= 1;
             if (++cs == S) {
                 cs = 0;

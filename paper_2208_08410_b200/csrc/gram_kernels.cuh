@@ -303,6 +303,18 @@ constexpr int kTl = 6;
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Sum of the NW per-warp partials of a row, the same in every lane and every warp: lane i reads
+// partial i mod NW and a butterfly over NW lanes adds them (commutative pairings: bitwise identical
+// in all lanes).  One shared load + log2(NW) shuffle steps per warp instead of NW loads + NW - 1 adds
+// per thread (the row loop's fp64 reduction was its largest instruction cost).
+template <int NW>
+__device__ __forceinline__ double sum_warps(const double *part, int lane) {
+    double v = part[lane & (NW - 1)];
+#pragma unroll
+    for (int o = NW / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
 __device__ __forceinline__ void set_cond(unsigned long long h, int use, unsigned v) {
 #if CUDART_VERSION >= 12040
     if (use) cudaGraphSetConditional((cudaGraphConditionalHandle)h, v);
@@ -570,11 +582,9 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
             feed(s);
         }
         double t = 0.0, u = 0.0;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) t += red[((i & 1) * NR) * NW + w];  // same order in every thread
+        t = sum_warps<NW>(red + ((i & 1) * NR) * NW, lane);  // same value in every thread
         if (TWO) {
-#pragma unroll
-            for (int w = 0; w < NW; ++w) u += red[((i & 1) * NR + 1) * NW + w];
+            u = sum_warps<NW>(red + ((i & 1) * NR + 1) * NW, lane);
             t -= u * c_fresh;  // - U_r,fresh sigma_f (V_f . v) = - u_r (v_prev . v)
             if (tid == 0) {
                 p.u_out[grow] = u;

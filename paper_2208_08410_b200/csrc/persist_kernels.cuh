@@ -298,8 +298,7 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
                 feed();  // keeps S rows in flight, across the pass boundary too
             }
             double t = 0.0;
-#pragma unroll
-            for (int w = 0; w < NW; ++w) t += red[rb * NW + w];
+            t = sum_warps<NW>(red + rb * NW, lane);
             rb ^= 1;
             if (++cs == S) {
                 cs = 0;
