@@ -356,8 +356,11 @@ static tsvd_status plan(tsvd_t h) {
         h->T = kSpThreads;
         return set_fin_attrs(h);
     }
+    // thread tid owns deflation column tid of a staged U row (and its w / V^T y lane): T >= k
+    if (h->k > kMaxThreadsPerCta)
+        return h->fail(TSVD_ERR_UNSUPPORTED, "dense path: k = %d > %d components", h->k, kMaxThreadsPerCta);
     int T = 32;
-    while ((int64_t)4 * T * 8 < n && T < kMaxThreadsPerCta) T *= 2;
+    while (((int64_t)4 * T * 8 < n || T < h->k) && T < kMaxThreadsPerCta) T *= 2;
     int split = 1;
     if ((int64_t)4 * T * 8 < n) split = 2;  // 2-CTA cluster: each CTA stages and owns half a row
     if ((int64_t)4 * T * 8 * split < n)

@@ -440,3 +440,16 @@ def test_explicit_gram_parity(m, n, k, T):
     S2 = t.result()[1]
     t.close()
     np.testing.assert_array_equal(S1, S2)
+
+
+def test_many_components_fall_back_cleanly():
+    """k = 140 > 129: beyond the persistent kernel's (V^T y) lanes (32 x 4 per thread) the run takes
+    the per-iteration kernels; fixed T keeps it short.  Against the oracle."""
+    m, n, k, T = 900, 300, 140, 3
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(n, 3.0, 0.97), seed=5)
+    V0 = synth.v0_normal(n, k, seed=6)
+    ref = oracle.tsvd(A, k, 1e-6, V0, fixed_T=T)
+    rc, U, S, V, kf, iters, dots, rep = _gpu_tsvd(A, k, 1e-6, V0, fixed_iters=T)
+    assert rc == P.OK and kf == k and rep["persistent"]["enabled"] is False
+    rel = np.abs(S - ref.S) / ref.S
+    assert rel.max() <= 1e-4, rel.max()
