@@ -38,16 +38,18 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in DEPS):
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Compile libtsvd.so (or, for A/B experiments, a variant with extra -D defines at `out`)."""
+    lib = out or LIB
+    if not force and os.path.exists(lib) and all(os.path.getmtime(lib) >= os.path.getmtime(d) for d in DEPS):
         return LIB
     nd = nccl_dir()
     cb = cublas_dir()
-    tmp = LIB + f".{os.getpid()}.tmp"
+    tmp = lib + f".{os.getpid()}.tmp"
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"), "-I", os.path.join(cb, "include"),
-           *SOURCES, "-o", tmp,
+           *[f"-D{d}" for d in defines], *SOURCES, "-o", tmp,
            "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(nd, "lib"),
            "-L", os.path.join(cb, "lib"), "-l:libcublas.so.12", "-Xlinker", "-rpath," + os.path.join(cb, "lib")]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -56,9 +58,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building libtsvd.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python build.py [--force] [-v] [-o OUT -DNAME ...]   (variants for A/B timing)
+    a = sys.argv[1:]
+    out = a[a.index("-o") + 1] if "-o" in a else None
+    print(build(force="--force" in a or out is not None, verbose="-v" in a, out=out,
+                defines=[x[2:] for x in a if x.startswith("-D")]))

@@ -85,11 +85,13 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     return t;
 }
 
-// Grid-wide barrier for a cooperative launch (all CTAs co-resident): sense reversal on
-// bar[0] = arrivals, bar[1] = generation.  Used once per N1 launch.
+// Grid-wide barrier for a cooperative launch (all CTAs co-resident).  One arrival word: CTA 0 adds
+// 2^31 - (G - 1), every other CTA adds 1, so bit 31 flips exactly when the last CTA arrives and the
+// low bits return to zero (no reset, no generation read: one atomic round trip + the poll).
 __device__ __forceinline__ void grid_sync(unsigned *bar) {
     __syncthreads();
     if (threadIdx.x == 0) {
+#ifdef TSVD_GBAR_LEGACY
         const unsigned gen = ld_acquire_gpu(bar + 1);
         __threadfence();
         if (atomicAdd(bar, 1u) == gridDim.x - 1) {
@@ -99,6 +101,13 @@ __device__ __forceinline__ void grid_sync(unsigned *bar) {
         } else {
             while (ld_acquire_gpu(bar + 1) == gen) __nanosleep(32);
         }
+#else
+        const unsigned nb = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+        __threadfence();
+        const unsigned old = atomicAdd(bar, nb);
+        while (((old ^ ld_acquire_gpu(bar)) & 0x80000000u) == 0u) {
+        }
+#endif
         __threadfence();
     }
     __syncthreads();
@@ -294,7 +303,7 @@ __device__ __forceinline__ double warp_sum(double x) {
 
 // debug timeline record per iteration: N1 start (block 0), N1 end (last CTA), fin end, fin start
 // (block 0), fin tail start (last block), first N1 CTA out
-constexpr int kTl = 6;
+constexpr int kTl = 8;
 
 // Programmatic dependent launch: a kernel launched with the PDL attribute may start while its
 // predecessor in the stream is still running; griddep_wait() blocks until that predecessor has

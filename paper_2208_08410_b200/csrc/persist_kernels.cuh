@@ -12,10 +12,11 @@
 //   reduce: CTA b sums a 32-aligned column slice of the partials over all CTAs in a fixed order,
 //           applies the V (S w) correction (every CTA reduces w itself), writes y_new, and its
 //           slice's partial scalars { sum y^2, sum v y, (V^T y)_0..l-1 } -> part[b]
-//   sync 2: grid barrier
-//   decide: every CTA sums part[0..G) in the same fixed order (so every CTA takes the same
-//           decision bit for bit), ||y||, d = |v . y| / ||y||, stop test, c = S V^T v1 for the
-//           next pass; CTA 0 publishes the loop state
+//   publish: the slice of y_new (fp32) and the slice scalars as stamped words (value + pass stamp)
+//   decide: every CTA polls the G slice scalars and sums them in the same fixed order (so every CTA
+//           takes the same decision bit for bit), ||y||, d = |v . y| / ||y||, stop test, c = S V^T v1
+//           for the next pass; CTA 0 publishes the loop state; the next pass polls the y_new words
+//           it needs for v.  No second grid barrier: a stamped word carries its own readiness.
 //
 // The producer keeps feeding the ring across pass boundaries (A and the U rows do not change
 // during a component), so the next pass's first S rows are in flight while the grid reduces.
@@ -47,8 +48,10 @@ struct PsParams {
     int64_t ypart_ld;
     double *wpart;           // [G][wpart_ld]
     int32_t wpart_ld;
-    double *part;            // [G][part_ld] slice scalars
+    double *part;            // [G][part_ld] slice scalars (tail_init)
     int32_t part_ld;
+    ulonglong2 *pub;         // [G][part_ld] stamped slice scalars of every pass (ll_send words)
+    unsigned long long *puby;  // [round4(n)] stamped fp32 y_new words {float bits | stamp << 32}
     unsigned *gbar;          // grid barrier state (2 words, zero-initialised)
     double eps;
     int32_t fixed_T, max_iter;
@@ -105,6 +108,16 @@ __device__ __forceinline__ void ll_send(ulonglong2 *dst, unsigned stamp, double 
     const unsigned long long a = s | (unsigned)__double2loint(x), b = s | (unsigned)__double2hiint(x);
     asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(dst), "l"(a), "l"(b) : "memory");
 }
+__device__ __forceinline__ void ll_send_gpu(ulonglong2 *dst, unsigned stamp, double x) {
+    const unsigned long long s = (unsigned long long)stamp << 32;
+    const unsigned long long a = s | (unsigned)__double2loint(x), b = s | (unsigned)__double2hiint(x);
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(dst), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ ulonglong2 ld_volatile_u2(const void *src) {
+    ulonglong2 v;
+    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(src) : "memory");
+    return v;
+}
 // Poll until both words carry `stamp`; after 30 s mark the run failed (status -6) and return 0.
 __device__ __forceinline__ double ll_recv(const ulonglong2 *src, unsigned stamp, unsigned long long t0,
                                          LoopState *st) {
@@ -119,6 +132,29 @@ __device__ __forceinline__ double ll_recv(const ulonglong2 *src, unsigned stamp,
             return 0.0;
         }
     }
+}
+
+// strided_sum over stamped words, one attempt: U loads in flight per batch, `ok` cleared if any
+// word is not yet current (the caller waits and retries); the summation order is that of strided_sum
+template <int U>
+__device__ __forceinline__ double ll_try_sum(const ulonglong2 *base, int64_t ld, int first, int step, int count,
+                                             unsigned stamp, bool &ok) {
+    double acc = 0.0;
+    for (int b0 = first; b0 < count; b0 += U * step) {
+        ulonglong2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int bb = b0 + u * step;
+            v[u] = bb < count ? ld_volatile_u2(base + (int64_t)bb * ld) : make_ulonglong2(0ull, 0ull);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (b0 + u * step < count) {
+                ok &= (unsigned)(v[u].x >> 32) == stamp && (unsigned)(v[u].y >> 32) == stamp;
+                acc += __hiloint2double((int)(unsigned)v[u].y, (int)(unsigned)v[u].x);
+            }
+    }
+    return acc;
 }
 
 template <int T, int NV>
@@ -142,16 +178,21 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
     __shared__ int64_t slot_row[kMaxStages];
     __shared__ double ny_s;
     __shared__ int done_s;
+    __shared__ int xfail_s;  // world > 1: an exchange timed out (st->stop raised) before publication
     __shared__ double sred[2][32];
     // producer state (thread 0 only; kept in shared memory to leave the registers to the row loop):
     // next row index pk within pass pp of the range [plo, plo + pnr), next ring slot pslot
     __shared__ int64_t plo, pnr, pk;
     __shared__ int pp, pslot, pit0;
+    // pass stamps (monotone across launches and runs: a stamp never repeats): the words published by
+    // iteration `it` carry xeb_s + it + 1; kept in shared memory with it0_s to spare the row loop's
+    // registers
+    __shared__ unsigned xeb_s;
+    __shared__ int it0_s;
 
     const int64_t nr = p.rows * (b + 1) / G - p.rows * b / G;
     const int it0 = st->it;
     int it = it0;
-    unsigned xe = st->xepoch;  // world > 1: exchanges done so far (flag values are xe + 1)
 
     auto feed = [&]() {  // thread 0: next row of the (endless) serpentine sequence into the ring
         const int64_t k = pk;
@@ -177,6 +218,8 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
         pp = 0;
         pslot = 0;
         pit0 = it0 + (p.head_ext ? 1 : 0);  // head: the first pass run here is iteration it0 + 1
+        xeb_s = st->xepoch - (unsigned)it0;
+        it0_s = it0;
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_barrier_init();
         // head: the first rows are fed after the U column of the fresh component is written
@@ -201,23 +244,48 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
         {
             const double inv = 1.0 / ny_s;
             const double *ycur = p.ybuf + (int64_t)(it & 1) * p.ystride;
+            // y_new of the previous pass of this launch: the stamped fp32 words published by the slice
+            // owners (p.puby); the first pass of a launch reads the fp64 ybuf of a prior kernel.  Both
+            // are 8 bytes per column: one load sequence, the interpretation selected per word
+            const bool pub = it != it0_s;
+            const unsigned xe = xeb_s + (unsigned)it;
+            const unsigned long long *src =
+                pub ? p.puby : reinterpret_cast<const unsigned long long *>(ycur);
+            auto build = [&]() -> bool {  // straight-line: loads, stamp checks, v; false if a word is stale
+                bool ok = true;
 #pragma unroll
-            for (int k = 0; k < NV; ++k) {
-                const int idx = k * T + tid;
-                const int j = 4 * idx;
-                if (idx >= p.n4) {
-                    vr[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-                } else if (j + 3 < p.n) {
-                    const double2 lo2 = __ldcg(reinterpret_cast<const double2 *>(ycur + j));
-                    const double2 hi2 = __ldcg(reinterpret_cast<const double2 *>(ycur + j + 2));
-                    vr[k] = make_float4((float)(lo2.x * inv), (float)(lo2.y * inv), (float)(hi2.x * inv),
-                                        (float)(hi2.y * inv));
-                } else {
-                    vr[k].x = j + 0 < p.n ? (float)(__ldcg(ycur + j + 0) * inv) : 0.f;
-                    vr[k].y = j + 1 < p.n ? (float)(__ldcg(ycur + j + 1) * inv) : 0.f;
-                    vr[k].z = j + 2 < p.n ? (float)(__ldcg(ycur + j + 2) * inv) : 0.f;
-                    vr[k].w = 0.f;
+                for (int k = 0; k < NV; ++k) {
+                    const int idx = k * T + tid;
+                    const int j = 4 * idx;
+                    float f[4] = {0.f, 0.f, 0.f, 0.f};
+                    if (idx < p.n4) {  // (both buffers hold round4(n) words)
+                        // L2 loads (ld.cg: never a stale L1 line); a stale stamped word is re-polled
+                        const ulonglong2 w0 = __ldcg(reinterpret_cast<const ulonglong2 *>(src) + 2 * (int64_t)idx);
+                        const ulonglong2 w1 = __ldcg(reinterpret_cast<const ulonglong2 *>(src) + 2 * (int64_t)idx + 1);
+                        const unsigned long long wd[4] = {w0.x, w0.y, w1.x, w1.y};
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+                            if (j + c < p.n) {
+                                ok &= !pub || (unsigned)(wd[c] >> 32) == xe;
+                                const double y = pub ? (double)__uint_as_float((unsigned)wd[c])
+                                                     : __longlong_as_double((long long)wd[c]);
+                                f[c] = (float)(y * inv);
+                            }
+                    }
+                    vr[k] = make_float4(f[0], f[1], f[2], f[3]);
                 }
+                return ok;
+            };
+            // a stale word (its owner's y stores and scalar stores come from different threads, so the
+            // scalars can be seen first) costs one more round of the same parallel loads
+            const unsigned long long t0 = globaltimer_ns();
+            for (unsigned spin = 1; !build(); ++spin) {
+                if ((spin & 255) == 0 && globaltimer_ns() - t0 > 30000000000ull) {
+                    st->status = -6;
+                    st->stop = 1;
+                    break;
+                }
+                __nanosleep(128);
             }
         }
         const double cval = tid < l ? cvec[tid] : 0.0;
@@ -320,7 +388,6 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
         }
         flush();
         if (tid < l) p.wpart[(int64_t)b * p.wpart_ld + tid] = wacc;
-        __threadfence();
         grid_sync(p.gbar);  // sync 1: every partial is written
         if (p.tl && b == 0 && tid == 0) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 1] = globaltimer_ns();
       }
@@ -419,7 +486,7 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
             if (multi) {  // push my slice (+ local w) to every rank, wait for every rank's, sum in rank order
                 // low-latency protocol: every 8-byte word carries half of the value and the pass
                 // stamp, so a receiver polls the data itself (no fence, no separate flag)
-                const unsigned target = xe + 1u;
+                const unsigned target = xeb_s + (unsigned)it + 1u;
                 const int64_t so = ((int64_t)(target & 1u) * p.px.world * Gs + b) * p.px.SL;  // + src * Gs * SL
                 const int64_t mine = so + (int64_t)p.px.rank * Gs * p.px.SL;
                 for (int r = 0; r < p.px.world; ++r) {
@@ -488,6 +555,7 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
                     for (int i = 0; i < l; ++i) corr += Vj[i] * gvec[i];
                     y -= corr;
                     __stcg(ynew + j, y);
+                    __stcg(p.puby + j, ((unsigned long long)(xeb_s + (unsigned)it + 1u) << 32) | __float_as_uint((float)y));
                     a_yy += y * y;
                     a_vy += (__ldcg(ycur + j) * inv) * y;
                 }
@@ -507,8 +575,11 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
             __syncthreads();
         }
         if (p.tl && b == 0 && tid == 0) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 5] = globaltimer_ns();
-        double *pp = p.part + (int64_t)b * p.part_ld;
-        {  // block sums in a fixed order: warps (of the CW column threads), then lanes
+        const unsigned pst = xeb_s + (unsigned)it + 1u;  // this pass's stamp
+        if (tid == 0) xfail_s = multi ? *reinterpret_cast<volatile int32_t *>(&st->stop) : 0;
+        ulonglong2 *pb = p.pub + (int64_t)b * p.part_ld;
+        {  // block sums in a fixed order: warps (of the CW column threads), then lanes; published as
+           // stamped words (a CTA whose exchange timed out publishes -inf for ||y||^2)
             const double yy = warp_sum(a_yy), vy = warp_sum(a_vy);
             if (lane == 0 && warp < CW / 32) {
                 sred[0][warp] = yy;
@@ -518,9 +589,10 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
             if (tid < 2) {
                 double acc = 0.0;
                 for (int w = 0; w < CW / 32; ++w) acc += sred[tid][w];
-                pp[tid] = acc;
+                if (tid == 0 && xfail_s) acc = -INFINITY;
+                ll_send_gpu(pb + tid, pst, acc);
             }
-            if (ext && tid == 2) pp[2 + l] = xsq ? sigma_s : 0.0;  // ||u||^2 rides with the slice scalars
+            if (ext && tid == 2) ll_send_gpu(pb + 2 + l, pst, xsq ? sigma_s : 0.0);  // ||u||^2 rides along
 #pragma unroll
             for (int q = 0; q < kPsLanesV; ++q) {
                 if (32 * q >= l) break;
@@ -530,34 +602,59 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
                 if (tid < 32 && 32 * q + tid < l) {
                     double acc = 0.0;
                     for (int w = 0; w < NW; ++w) acc += gred[w * 32 + tid];
-                    pp[2 + 32 * q + tid] = acc;
+                    ll_send_gpu(pb + 2 + 32 * q + tid, pst, acc);
                 }
             }
         }
-        __threadfence();
-        grid_sync(p.gbar);  // sync 2: every slice is written
+        if (p.tl && b == 0 && tid == 0) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 6] = globaltimer_ns();
 
-        // ---- decision: identical in every CTA (same data, same fixed order)
-        {  // half-warp per quantity, 16 lanes striding the CTAs: one round of loads for 2 + l <= 2 NW
+        // ---- decision: identical in every CTA (same data, same fixed order).  Polling every CTA's
+        // stamped scalars is also the grid-wide ordering point: a CTA that has them all knows every
+        // CTA has finished reading this pass's partials (its next flush may overwrite them)
+        {  // half-warp per quantity, 16 lanes striding the CTAs: one round of loads for 2 + l <= 2 NW.
+           // A CTA that finds a stale word (its peers are still reducing) does not keep the whole
+           // block polling (that load storm slows the late CTAs down): warp 0 alone polls, with a
+           // back-off, the word each CTA writes last, then the block loads everything again
             const int hl = lane & 15;
             const int nq = 2 + l + (ext ? 1 : 0);
-            for (int q0 = 2 * warp; q0 < nq; q0 += 2 * NW) {  // warp-uniform trip count
-                const int q = q0 + (lane >> 4);
-                double sq = q < nq ? strided_sum<10>(p.part + q, p.part_ld, hl, 16, G) : 0.0;
+            const int qlast = l > 0 ? 2 + l - 1 : 1;
+            const unsigned long long t0 = globaltimer_ns();
+            for (;;) {
+                bool ok = true;
+                for (int q0 = 2 * warp; q0 < nq; q0 += 2 * NW) {  // warp-uniform trip count
+                    const int q = q0 + (lane >> 4);
+                    double sq = q < nq ? ll_try_sum<10>(p.pub + q, p.part_ld, hl, 16, G, pst, ok) : 0.0;
 #pragma unroll
-                for (int o = 8; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-                if (hl == 0 && q < nq) tot[q] = sq;
+                    for (int o = 8; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+                    if (hl == 0 && q < nq) tot[q] = sq;
+                }
+                if (__syncthreads_and(ok)) break;
+                if (warp == 0) {
+                    for (int bb = lane; bb < G; bb += 32)
+                        for (unsigned spin = 0;; ++spin) {
+                            const ulonglong2 w = ld_volatile_u2(p.pub + (int64_t)bb * p.part_ld + qlast);
+                            if ((unsigned)(w.x >> 32) == pst && (unsigned)(w.y >> 32) == pst) break;
+                            if ((spin & 255) == 255 && globaltimer_ns() - t0 > 30000000000ull) {
+                                st->status = -6;  // a CTA never published: give up (the run fails)
+                                st->stop = 1;
+                                break;
+                            }
+                            __nanosleep(64);
+                        }
+                }
+                __syncthreads();
+                if (globaltimer_ns() - t0 > 30000000000ull) break;
             }
         }
         __syncthreads();
+        if (p.tl && b == 0 && tid == 0) p.tl[2 + kTl * ((p.tl[0] - 1) % 4096) + 7] = globaltimer_ns();
         const int itn = it + 1;
-        if (multi) ++xe;
         if (tid == 0) {
             const double nyn = sqrt(tot[0]);
             int done = 0, status = 0;
             double d = 0.0;
-            // a CTA whose exchange timed out raised st->stop before sync 2: every CTA leaves
-            const int peer_fail = multi ? *reinterpret_cast<volatile int32_t *>(&st->stop) : 0;
+            // a CTA whose exchange timed out (st->stop raised) published -inf: every CTA leaves
+            const int peer_fail = multi && tot[0] < 0.0;
             const double sg = ext ? sqrt(tot[2 + l]) : 1.0;  // sigma of the fresh component
             sigma_s = sg;
             if (peer_fail) {
@@ -596,7 +693,7 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
                     st->done = 1;
                     if (done == 2) st->stop = 1;
                 }
-                if (multi) st->xepoch = xe;
+                st->xepoch = xeb_s + (unsigned)itn;
                 if (ext) {  // the fresh component's sigma; its it/d/status came with tail_init
                     CompStat cs = p.stat[fresh];
                     cs.sigma = sg;

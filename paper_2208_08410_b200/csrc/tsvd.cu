@@ -215,6 +215,8 @@ struct tsvd_s {
     LoopState *st = nullptr;
     CompStat *stats = nullptr;
     LoopState *st_host = nullptr;      // pinned
+    ulonglong2 *pub = nullptr;         // persistent kernel: stamped slice scalars [grid][part_ld]
+    unsigned long long *puby = nullptr;  // persistent kernel: stamped fp32 y words [round4(n)]
     CompStat *stats_host = nullptr;    // pinned
     double *vec_host = nullptr;        // pinned staging (n doubles)
     int64_t ystride = 0, wofs = 0, ypart_ld = 0;
@@ -624,6 +626,12 @@ static tsvd_status ensure_alloc(tsvd_t h) {
     if (!e) e = dm((void **)&h->gbar, 2 * sizeof(unsigned));
     if (!e) e = cudaMemsetAsync(h->gbar, 0, 2 * sizeof(unsigned), h->stream);
     if (!e) e = dm((void **)&h->work, 2 * sizeof(unsigned long long));
+    if (!e && !h->sparse) {  // persistent kernel's stamped publication words (zero: no stamp matches)
+        e = dm((void **)&h->pub, (size_t)h->grid * h->part_ld * sizeof(ulonglong2));
+        if (!e) e = cudaMemsetAsync(h->pub, 0, (size_t)h->grid * h->part_ld * sizeof(ulonglong2), h->stream);
+        if (!e) e = dm((void **)&h->puby, (size_t)round_up(n, 4) * sizeof(unsigned long long));
+        if (!e) e = cudaMemsetAsync(h->puby, 0, (size_t)round_up(n, 4) * sizeof(unsigned long long), h->stream);
+    }
     if (!e && !h->sparse) {
         e = dm((void **)&h->vprev32, (size_t)round_up(n, 4) * sizeof(float));
         if (!e) e = cudaMemsetAsync(h->vprev32, 0, (size_t)round_up(n, 4) * sizeof(float), h->stream);
@@ -1156,6 +1164,8 @@ static tsvd_status launch_persist(tsvd_t h, cudaStream_t s, int l, cudaEvent_t e
     p.wpart_ld = h->kpad;
     p.part = h->part;
     p.part_ld = h->part_ld;
+    p.pub = h->pub;
+    p.puby = h->puby;
     p.gbar = h->gbar;
     p.eps = h->eps;
     p.fixed_T = h->fixed_T;
@@ -2202,8 +2212,9 @@ tsvd_status tsvd_run(tsvd_t h) {
             {
                 const unsigned long long *r = tl.data() + 2 + kTl * i;
                 auto rel = [&](unsigned long long t) { return t ? (long long)(t - base) : -1ll; };
-                fprintf(f, "%lld,%lld,%lld,%lld,%lld,%lld,%lld\n", (long long)i, rel(r[0]), rel(r[1]), rel(r[2]),
-                        rel(r[3]), rel(r[4]), rel(r[5]));
+                fprintf(f, "%lld", (long long)i);
+                for (int q = 0; q < kTl; ++q) fprintf(f, ",%lld", rel(r[q]));
+                fprintf(f, "\n");
             }
             fclose(f);
         }
@@ -2369,7 +2380,7 @@ void tsvd_destroy(tsvd_t h) {
     void *dev_ptrs[] = {h->A_own, h->U32, h->V64, h->S64, h->ybuf, h->yw, h->V0d, h->c64, h->ypart,
                         h->wpart, h->part, h->u64, h->sq_part, h->sig2, h->st, h->stats, h->sym, h->gbar,
                         h->trace_d, h->work, h->tl_d, h->vprev32, h->px_mem, h->y32, h->t32, h->At,
-                        h->B0, h->Pm, h->Qm, h->gpart, h->zero64, h->g_hi, h->g_lo};
+                        h->B0, h->Pm, h->Qm, h->gpart, h->zero64, h->g_hi, h->g_lo, h->pub, h->puby};
     if (h->cublas) cublasDestroy(h->cublas);
     if (h->trace_f) fclose(h->trace_f);
     for (void *p : dev_ptrs)

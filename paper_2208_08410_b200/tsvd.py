@@ -53,8 +53,8 @@ def lib():
     """Load libtsvd.so (building it in-tree with nvcc if it is missing or stale)."""
     global _lib
     if _lib is None:
-        path = _build.LIB
-        if not os.path.exists(path) or os.environ.get("TSVD_REBUILD"):
+        path = os.environ.get("TSVD_LIB") or _build.LIB  # TSVD_LIB: an A/B variant built by build.py -o
+        if path == _build.LIB and (not os.path.exists(path) or os.environ.get("TSVD_REBUILD")):
             _build.build()
         L = ctypes.CDLL(path)
         L.tsvd_create.argtypes = [ctypes.POINTER(_vp), _i64, _i64, _i32, ctypes.c_double, ctypes.c_int, ctypes.c_int]
