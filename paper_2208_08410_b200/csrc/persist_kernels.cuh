@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
     double *tot = gvec + p.wpart_ld;                               // [2 + l] decision sums
     double *gred = tot + 2 + p.wpart_ld;                           // [kPsGred(T)] slice reduction
     double *ys = gred + kPsGred(T);                                // [128] y of the column block
+    double *Ssm = ys + 128;  // [l] sigma (the per-pass reductions read it twice: no L2 round trip)
     __shared__ int64_t slot_row[kMaxStages];
     __shared__ double ny_s;
     __shared__ int done_s;
@@ -226,7 +227,10 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
         if (nr > 0 && !p.head_ext)
             for (int s = 0; s < S; ++s) feed();
     }
-    for (int i = tid; i < l; i += T) cvec[i] = p.c[i];
+    for (int i = tid; i < l; i += T) {
+        cvec[i] = p.c[i];
+        Ssm[i] = p.S[i];  // (head: entry `fresh` is not final yet; it is never read, see below)
+    }
     if (tid == 0) ny_s = st->ny;
     __syncthreads();
 
@@ -462,7 +466,7 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
             if (c0 == j0) {  // w = U^T t summed over the CTAs (issued after the slice loads: one more round)
                 for (int i = warp; i < l; i += NW) {
                     const double w = warp_sum(strided_sum<8>(p.wpart + i, p.wpart_ld, lane, 32, G));
-                    if (lane == 0) gvec[i] = multi ? w : (i == fresh ? 1.0 : p.S[i]) * w;
+                    if (lane == 0) gvec[i] = multi ? w : (i == fresh ? 1.0 : Ssm[i]) * w;
                 }
                 if (xsq && warp == NW - 1) {  // ||u||^2 of this rank (sigma of the fresh component)
                     const double q = warp_sum(strided_sum<8>(p.sq_part, 1, lane, 32, G));
@@ -517,7 +521,7 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
                     if (tid < l) {
                         double w = 0.0;
                         for (int r = 0; r < p.px.world; ++r) w += gred[r * EL + CW + tid];
-                        gvec[tid] = (tid == fresh ? 1.0 : p.S[tid]) * w;
+                        gvec[tid] = (tid == fresh ? 1.0 : Ssm[tid]) * w;
                     }
                     if (xsq && tid == T - 1) {
                         double q = 0.0;
@@ -535,7 +539,7 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
                         double w = 0.0;
                         for (int r = 0; r < p.px.world; ++r)
                             w += ll_recv(src + (int64_t)r * Gs * p.px.SL + p.px.per + tid, target, t0, st);
-                        gvec[tid] = (tid == fresh ? 1.0 : p.S[tid]) * w;
+                        gvec[tid] = (tid == fresh ? 1.0 : Ssm[tid]) * w;
                     }
                     if (xsq && tid == T - 1) {
                         double q = 0.0;
@@ -710,7 +714,7 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
         }
         __syncthreads();
         for (int i = tid; i < l; i += T) {  // c = S V^T v1 for the next pass (sigma for the fresh column)
-            cvec[i] = (i == fresh ? sigma_s : p.S[i]) * (tot[2 + i] / ny_s);
+            cvec[i] = (i == fresh ? sigma_s : Ssm[i]) * (tot[2 + i] / ny_s);
             if (b == 0) p.c[i] = cvec[i];
         }
         if (ext) {  // U[:, fresh] = u / sigma on this CTA's rows, then start the row stream

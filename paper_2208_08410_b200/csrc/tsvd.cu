@@ -425,7 +425,7 @@ static tsvd_status plan(tsvd_t h) {
     // must be co-resident (cooperative launch), and (V^T y)_i is owned by thread i (k <= T + 1)
     h->gv_ps = nullptr;
     if (split == 1 && h->k <= 32 * kPsLanesV + 1) {
-        const int64_t extra = kMaxStages * 8 + (int64_t)(2 * (T / 32) + 3 * h->kpad + 2 + kPsGred(T) + 128) * 8;
+        const int64_t extra = kMaxStages * 8 + (int64_t)(2 * (T / 32) + 4 * h->kpad + 2 + kPsGred(T) + 128) * 8;
         int Sp = S;
         while (Sp > 2 && ((int64_t)Sp * h->stage_bytes + extra) * h->cps > kSmemBudget) --Sp;
         PsFn fn = pick_ps(T, NV);
