@@ -35,6 +35,26 @@ __global__ void split_tf32(const float *__restrict__ A, int64_t rows, int64_t co
     }
 }
 
+// Symmetric task schedule of the Gram (n_b(n_b+1)/2 block tasks instead of n_b^2): only the
+// blocks (I <= J) are multiplied; this kernel fills the strictly-lower blocks by transposition.
+// M[c][r] = B[r + c*ldb] (column-major as cuBLAS wrote it): blocks with blk(c) < blk(r) were not
+// computed; they take M[r][c].  32x32 tiles through shared memory (both sides coalesced).
+__global__ void gram_mirror(float *__restrict__ B, int64_t n, int64_t ldb, int64_t bs) {
+    __shared__ float tile[32][33];
+    const int64_t c0 = (int64_t)blockIdx.y * 32, r0 = (int64_t)blockIdx.x * 32;
+    if (c0 / bs >= r0 / bs) return;  // (bs is a multiple of 32: one block row and column per tile)
+    const int tx = threadIdx.x, ty = threadIdx.y;                   // 32 x 8
+    for (int k = ty; k < 32; k += 8) {                              // read M[r][c] (contiguous in c)
+        const int64_t r = r0 + k, c = c0 + tx;
+        if (r < n && c < n) tile[k][tx] = B[c + r * ldb];
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {  // write M[c][r] (contiguous in r) where blk(c) < blk(r)
+        const int64_t c = c0 + k, r = r0 + tx;
+        if (r < n && c < n && c / bs < r / bs) B[r + c * ldb] = tile[tx][k];
+    }
+}
+
 struct GbParams {
     const float *B;          // n x ldb fp32 (B0 = A^T A)
     int64_t ldb;

@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
     }
     for (int i = tid; i < l; i += T) {
         cvec[i] = p.c[i];
-        Ssm[i] = p.S[i];  // (head: entry `fresh` is not final yet; it is never read, see below)
+        Ssm[i] = p.S[i];  // (head: entry `fresh` is set from the head's own sigma below)
     }
     if (tid == 0) ny_s = st->ny;
     __syncthreads();
@@ -719,6 +719,7 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
         }
         if (ext) {  // U[:, fresh] = u / sigma on this CTA's rows, then start the row stream
             const double sg = sigma_s;
+            if (tid == 0) Ssm[fresh] = sg;  // the cached sigma of the column extracted just now
             const int64_t r0 = p.rows * b / G;
             if (sg > 0.0 && isfinite(sg))
                 for (int64_t r = r0 + tid; r < r0 + nr; r += T) p.Uw[r * p.ldu + fresh] = (float)(p.u_out[r] / sg);

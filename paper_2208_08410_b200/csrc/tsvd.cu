@@ -246,6 +246,7 @@ struct tsvd_s {
     bool B0_ok = false;
     int pq_l = 0;          // components whose P / Q columns are valid
     double gram_ms = 0.0;  // B0 build time of the last build
+    int gram_blocks = 0;   // n_b of the symmetric task schedule of the last build
     cublasHandle_t cublas = nullptr;
     PsFn gv_ps = nullptr;  // N7: one persistent cooperative kernel per component (null: unsupported)
     int S_ps = 0;
@@ -1381,14 +1382,32 @@ static tsvd_status build_gram(tsvd_t h) {
     CK(cudaGetLastError());
     if (!h->cublas) CB(cublasCreate(&h->cublas));
     CB(cublasSetStream(h->cublas, h->stream));
-    // column-major view: a row-major m x n slab is an n x m matrix (lda = n); A^T A = A' A'^T.
-    // Three TF32 GEMMs (measured: 162 ms at C2; cuBLAS SYRK + SYR2K in TF32 math mode took 785 ms)
+    // column-major view: a row-major m x n slab is an n x m matrix A' (lda = n); A^T A = A' A'^T.
+    // Symmetric task schedule: n_b column blocks of A', only the n_b(n_b + 1)/2 block
+    // products (I <= J) are formed — each as three TF32 GEMMs of the hi/lo split — and the
+    // strictly-lower blocks are mirrored.  n_b is the largest of 1..8 that keeps blocks >= 2048
+    // wide (cuBLAS stays efficient).  (Full three GEMMs: 150-162 ms at C2; cuBLAS SYRK + SYR2K in
+    // TF32 math mode: 785 ms.)  TSVD_GRAM_NB overrides n_b (A/B experiments).
     const float one = 1.f, zero = 0.f;
     const float *ops[3][2] = {{hi, hi}, {hi, lo}, {lo, hi}};
-    for (int g = 0; g < 3; ++g)
-        CB(cublasGemmEx(h->cublas, CUBLAS_OP_N, CUBLAS_OP_T, (int)n, (int)n, (int)m, &one, ops[g][0], CUDA_R_32F,
-                        (int)n, ops[g][1], CUDA_R_32F, (int)n, g == 0 ? &zero : &one, h->B0, CUDA_R_32F, (int)h->ldb0,
-                        CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT));
+    int nb = (int)std::max<int64_t>(1, std::min<int64_t>(8, n / 2048));
+    if (const char *e = getenv("TSVD_GRAM_NB")) nb = std::max(1, atoi(e));
+    const int64_t bs = round_up((n + nb - 1) / nb, 32);
+    h->gram_blocks = nb;
+    for (int64_t I0 = 0; I0 < n; I0 += bs)
+        for (int64_t J0 = I0; J0 < n; J0 += bs) {
+            const int64_t bi = std::min(bs, n - I0), bj = std::min(bs, n - J0);
+            for (int g = 0; g < 3; ++g)
+                CB(cublasGemmEx(h->cublas, CUBLAS_OP_N, CUBLAS_OP_T, (int)bi, (int)bj, (int)m, &one, ops[g][0] + I0,
+                                CUDA_R_32F, (int)n, ops[g][1] + J0, CUDA_R_32F, (int)n, g == 0 ? &zero : &one,
+                                h->B0 + I0 + J0 * h->ldb0, CUDA_R_32F, (int)h->ldb0, CUBLAS_COMPUTE_32F_FAST_TF32,
+                                CUBLAS_GEMM_DEFAULT));
+        }
+    if (bs < n) {
+        const dim3 grid((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32));
+        gram_mirror<<<grid, dim3(32, 8), 0, h->stream>>>(h->B0, n, h->ldb0, bs);
+        CK(cudaGetLastError());
+    }
     CK(cudaStreamSynchronize(h->stream));
     h->B0_ok = true;
     h->gram_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -2289,10 +2308,10 @@ tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
     s += tmp;
     snprintf(tmp, sizeof tmp,
              "\"persistent\": {\"enabled\": %s, \"stages\": %d, \"smem\": %zu, \"ms\": %.6f, \"launches\": %lld, "
-             "\"passes\": %lld}, \"method\": \"%s\", \"gram_ms\": %.3f, ",
+             "\"passes\": %lld}, \"method\": \"%s\", \"gram_ms\": %.3f, \"gram_blocks\": %d, ",
              (use_persist(h) || h->method == 1) ? "true" : "false", h->method == 1 ? h->S_gb : h->S_ps,
              h->method == 1 ? h->smem_gb : h->smem_ps, h->ps_ms, (long long)h->ps_launches, (long long)h->ps_passes,
-             h->method == 1 ? "explicit-gram" : "gram-vector", h->gram_ms);
+             h->method == 1 ? "explicit-gram" : "gram-vector", h->gram_ms, h->gram_blocks);
     s += tmp;
     snprintf(tmp, sizeof tmp,
              "\"plan\": {\"T\": %d, \"NV\": %d, \"stages\": %d, \"ctas_per_sm\": %d, \"grid\": %d, \"smem\": %zu, "

@@ -442,6 +442,24 @@ def test_explicit_gram_parity(m, n, k, T):
     np.testing.assert_array_equal(S1, S2)
 
 
+@pytest.mark.parametrize("nb", [3, 5])
+def test_explicit_gram_symmetric_schedule(nb, monkeypatch):
+    """The Gram's symmetric task schedule (n_b(n_b+1)/2 block products, the strictly-lower
+    blocks mirrored) with ragged blocks: against the oracle and the unblocked Gram."""
+    m, n, k = 1800, 700, 4
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(48, 5.0, 0.75), seed=77)
+    V0 = synth.v0_normal(n, k, seed=78)
+    ref = oracle.tsvd(A, k, 1e-6, V0)
+    monkeypatch.setenv("TSVD_GRAM_NB", str(nb))
+    ex = _gpu_tsvd(A, k, 1e-6, V0, method=1)
+    assert ex[0] == P.OK and ex[7]["gram_blocks"] == nb
+    _assert_parity(A, ref, *ex[1:5], k)
+    monkeypatch.setenv("TSVD_GRAM_NB", "1")  # the unblocked Gram: the same spectrum
+    one = _gpu_tsvd(A, k, 1e-6, V0, method=1)
+    assert one[7]["gram_blocks"] == 1
+    np.testing.assert_allclose(ex[2], one[2], rtol=1e-6)
+
+
 def test_many_components_fall_back_cleanly():
     """k = 140 > 129: beyond the persistent kernel's (V^T y) lanes (32 x 4 per thread) the run takes
     the per-iteration kernels; fixed T keeps it short.  Against the oracle."""
