@@ -347,6 +347,29 @@ struct GxParams {
     LoopState *st;
 };
 
+// World > 1: the extraction pass's per-CTA partials reduced in CTA order into one rank vector
+// out = [A_g^T u_g (n) | U_g^T u_g (l) | ||u_g||^2] for the cross-rank all-reduce; gram_ext_finish
+// then runs on it with parts = 1.
+__global__ void gx_reduce(const GxParams p, double *__restrict__ out, int64_t wofs) {
+    griddep_launch();
+    griddep_wait();
+    const int64_t total = p.n + p.l + 1;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += (int64_t)gridDim.x * blockDim.x) {
+        double a = 0.0;
+        if (j < p.n) {
+            for (int b = 0; b < p.parts; ++b) a += p.ypart[(int64_t)b * p.ypart_ld + j];
+            out[j] = a;
+        } else if (j < p.n + p.l) {
+            const int i = (int)(j - p.n);
+            for (int b = 0; b < p.parts; ++b) a += p.wpart[(int64_t)b * p.wpart_ld + i];
+            out[wofs + i] = a;
+        } else {
+            for (int b = 0; b < p.parts; ++b) a += p.sq_part[b];
+            out[wofs + p.l] = a;
+        }
+    }
+}
+
 __global__ void gram_ext_finish(const GxParams p) {
     __shared__ double sig_s;
     LoopState *st = p.st;

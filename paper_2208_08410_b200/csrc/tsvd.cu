@@ -251,6 +251,7 @@ struct tsvd_s {
     PsFn gv_ps = nullptr;  // N7: one persistent cooperative kernel per component (null: unsupported)
     int S_ps = 0;
     size_t smem_ps = 0;
+    int grid_gb = 0;  // explicit-Gram iteration grid (from n, identical on every rank)
     double ps_ms = 0.0;    // TIMING: event time of the persistent launches, and the passes they ran
     int64_t ps_passes = 0, ps_launches = 0;  // debug knob TSVD_CARVEOUT=0: leave the driver's per-kernel L1/shared split
     size_t smem = 0;
@@ -455,10 +456,14 @@ static tsvd_status plan(tsvd_t h) {
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             int occ = 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, T, sm));
-            if (occ * h->sms >= h->grid) {
+            // grid from n and the device only (not from this rank's rows): with a row-partitioned A
+            // every rank iterates on the same B0 with the same grid, so the results agree bit for bit
+            const int64_t gg = std::min<int64_t>((int64_t)h->sms * std::min(h->cps, occ), h->n);
+            if (occ > 0 && gg >= 1) {
                 h->gb = fn;
                 h->S_gb = Sg;
                 h->smem_gb = sm;
+                h->grid_gb = (int)gg;
             }
         }
     }
@@ -1408,6 +1413,9 @@ static tsvd_status build_gram(tsvd_t h) {
         gram_mirror<<<grid, dim3(32, 8), 0, h->stream>>>(h->B0, n, h->ldb0, bs);
         CK(cudaGetLastError());
     }
+    // row-partitioned A (world > 1): B0 = sum_g A_g^T A_g, one all-reduce over NVLink (Alg. 3's
+    // Reduce_sum, as an all-reduce so that every rank iterates on the same B0)
+    if (h->world > 1) NK(ncclAllReduce(h->B0, h->B0, (size_t)n * h->ldb0, ncclFloat, ncclSum, h->comm, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     h->B0_ok = true;
     h->gram_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1415,8 +1423,8 @@ static tsvd_status build_gram(tsvd_t h) {
 }
 
 static tsvd_status run_explicit(tsvd_t h, int l0) {
-    if (h->sparse || h->streaming || h->world > 1 || h->split != 1 || !h->gb)
-        return h->fail(TSVD_ERR_UNSUPPORTED, "METHOD=1 (explicit Gram) needs a dense, HBM-resident, single-GPU input "
+    if (h->sparse || h->streaming || h->split != 1 || !h->gb)
+        return h->fail(TSVD_ERR_UNSUPPORTED, "METHOD=1 (explicit Gram) needs a dense, HBM-resident input "
                                              "with n <= 16384");
     if (l0 > h->pq_l)
         return h->fail(TSVD_ERR_UNSUPPORTED, "METHOD=1 resumes only from factors it computed itself");
@@ -1424,7 +1432,7 @@ static tsvd_status run_explicit(tsvd_t h, int l0) {
     if (!h->Pm) {
         CK(cudaMalloc((void **)&h->Pm, (size_t)n * h->kpad * sizeof(float)));
         CK(cudaMalloc((void **)&h->Qm, (size_t)h->k * h->k * sizeof(double)));
-        CK(cudaMalloc((void **)&h->gpart, (size_t)2 * h->grid * (2 + 2 * h->kpad) * sizeof(double)));
+        CK(cudaMalloc((void **)&h->gpart, (size_t)2 * h->grid_gb * (2 + 2 * h->kpad) * sizeof(double)));
         CK(cudaMalloc((void **)&h->zero64, (size_t)h->kpad * sizeof(double)));
         CK(cudaMemsetAsync(h->Pm, 0, (size_t)n * h->kpad * sizeof(float), h->stream));
         CK(cudaMemsetAsync(h->Qm, 0, (size_t)h->k * h->k * sizeof(double), h->stream));
@@ -1470,7 +1478,7 @@ static tsvd_status run_explicit(tsvd_t h, int l0) {
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeCooperative;
         attr[0].val.cooperative = 1;
-        cfg.gridDim = dim3(h->grid);
+        cfg.gridDim = dim3(h->grid_gb);
         cfg.blockDim = dim3(h->T);
         cfg.dynamicSmemBytes = h->smem_gb;
         cfg.stream = h->stream;
@@ -1483,6 +1491,7 @@ static tsvd_status run_explicit(tsvd_t h, int l0) {
         GvParams q = gv_params(h, l, false);
         q.c = h->zero64;
         q.store_t = 1;
+        q.reduce_mode = 0;  // partials stay per CTA (world > 1: reduced and all-reduced below)
         q.tl = nullptr;
         q.trace = nullptr;
         CK(launch_n1(h, h->gv, q, h->stream));
@@ -1511,6 +1520,17 @@ static tsvd_status run_explicit(tsvd_t h, int l0) {
         x.stat = h->stats;
         x.st = h->st;
         const int blocks = (int)std::min<int64_t>((std::max(h->m_g, n) + 255) / 256, (int64_t)h->sms * 8);
+        if (h->world > 1) {  // [A_g^T u | U_g^T u | ||u_g||^2] summed over the ranks; identical on every rank
+            CK(launch_k(h, gx_reduce, (int)std::min<int64_t>((n + l + 256) / 256, (int64_t)h->sms * 8), 256, 0,
+                        h->stream, 1, x, h->yw, h->wofs));
+            NK(ncclAllReduce(h->yw, h->yw, (size_t)(h->wofs + h->kpad), ncclDouble, ncclSum, h->comm, h->stream));
+            x.parts = 1;
+            x.ypart = h->yw;
+            x.ypart_ld = 0;
+            x.wpart = h->yw + h->wofs;
+            x.wpart_ld = 0;
+            x.sq_part = h->yw + h->wofs + l;
+        }
         CK(launch_k(h, gram_ext_finish, blocks, 256, 0, h->stream, 1, x));
         CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));

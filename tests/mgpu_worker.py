@@ -48,6 +48,7 @@ def main():
     t = P.TSVD(m, n, k, eps, rank=rank, world=world, uid=obj[0], device=local)
     t.set_option(P.OPT_COLLECTIVE, int(os.environ.get("TSVD_COLLECTIVE", "0")))
     t.set_option(P.OPT_PERSISTENT, int(os.environ.get("TSVD_PERSISTENT", "1")))
+    t.set_option(P.OPT_METHOD, int(os.environ.get("TSVD_METHOD", "0")))  # 1: explicit Gram (NEXT#1)
     if sparse:
         t.set_option(P.OPT_FIXED_ITERS, 12)  # paper-like spectrum: fixed iterations
         t.set_option(P.OPT_SPARSE_BLOCK, int(os.environ.get("TSVD_SPARSE_BLOCK", "0")))

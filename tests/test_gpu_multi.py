@@ -46,3 +46,20 @@ def test_sparse_row_partition_parity(world, block):
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "replicated_equal=True" in r.stdout and "host/nccl" in r.stdout
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_explicit_gram_row_partition_parity(world):
+    """METHOD=1 on row slabs: B0 = sum_g A_g^T A_g by one NCCL all-reduce (Alg. 3's Reduce_sum,
+    P:242), the iterations on B0 replicated on every rank, the per-component extraction sums
+    [A^T u | U^T u | ||u||^2] all-reduced — against the oracle, bitwise equal S and V on all ranks."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + world),
+           os.path.join(ROOT, "tests", "mgpu_worker.py")]
+    env = dict(os.environ, TSVD_METHOD="1")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "replicated_equal=True" in r.stdout and "explicit-gram" in r.stdout
