@@ -114,10 +114,12 @@ typedef enum {
                                     columns / rows => several blocks). Read by tsvd_set_csr          */
     TSVD_OPT_METHOD = 21         /* 0 (default): implicit Gram-vector products (Eq. 2, the north star);
                                     1: explicit Gram (Alg. 2 lines 6-9 with Alg. 3's Gram, P:114-121,
-                                    P:220-249): B0 = A^T A once (TF32x3 tensor-core GEMMs), then per
-                                    iteration y = B0 v - P c - V g with P = A^T U, Q = U^T U (exact
-                                    deflation, no U^T U = I assumption); dense, resident, one GPU,
-                                    n <= 16384; pays off when iterations per component are many    */
+                                    P:220-249): B0 = A^T A once (TF32x3 tensor-core GEMMs over the
+                                    symmetric block schedule of P:348), then per iteration
+                                    y = B0 v - P c - V g with P = A^T U, Q = U^T U (exact deflation,
+                                    no U^T U = I assumption); dense, resident, n <= 16384.  World > 1:
+                                    B0 all-reduced once, iterations replicated on every rank.  Pays
+                                    off when iterations per component are many                     */
 } tsvd_option;
 
 /*
