@@ -81,7 +81,48 @@ struct GbParams {
     double eps;
     int32_t fixed_T, max_iter;
     int32_t serpentine;
+    // world > 1: this rank iterates on rows [row0, row0 + rows) of B0 only; every iteration's y rows
+    // and per-CTA sums go to every rank as stamped words (value halves + exchange stamp, as N7):
+    // yx[r] = rank r's y area [2 parity][n], sx[r] = its sums area [2][world][G][2 + 2 l]
+    int64_t row0;
+    int32_t world, rank;
+    ulonglong2 *yx[kMaxRanks];
+    ulonglong2 *sx[kMaxRanks];
 };
+
+// world > 1: sums of the per-CTA quantities over [rank][CTA] in that fixed order, from the stamped
+// sums area (half-warp per quantity); a stale first read leaves warp 0 polling with a back-off
+__device__ __forceinline__ void gx_totals(const ulonglong2 *area, int E, int nqx, unsigned stamp, double *tot_c,
+                                          LoopState *st) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    const int hl = lane & 15;
+    const unsigned long long t0 = globaltimer_ns();
+    for (;;) {
+        bool ok = true;
+        for (int q0 = 2 * warp; q0 < nqx; q0 += 2 * NW) {
+            const int q = q0 + (lane >> 4);
+            double v = q < nqx ? ll_try_sum<10>(area + q, nqx, hl, 16, E, stamp, ok) : 0.0;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (hl == 0 && q < nqx) tot_c[q] = v;
+        }
+        if (__syncthreads_and(ok)) return;
+        if (warp == 0)
+            for (int e = lane; e < E; e += 32)
+                for (unsigned spin = 0;; ++spin) {
+                    const ulonglong2 w = ld_volatile_u2(area + (int64_t)e * nqx + nqx - 1);
+                    if ((unsigned)(w.x >> 32) == stamp && (unsigned)(w.y >> 32) == stamp) break;
+                    if ((spin & 255) == 255 && globaltimer_ns() - t0 > 30000000000ull) {
+                        st->status = -6;
+                        st->stop = 1;
+                        break;
+                    }
+                    __nanosleep(64);
+                }
+        __syncthreads();
+        if (globaltimer_ns() - t0 > 30000000000ull) return;
+    }
+}
 
 template <int T, int NV>
 __global__ void __launch_bounds__(T) gb_persist(const GbParams p) {
@@ -105,9 +146,13 @@ __global__ void __launch_bounds__(T) gb_persist(const GbParams p) {
     __shared__ int done_s;
     __shared__ int64_t plo, pnr, pk;
     __shared__ int pp, pslot, pit0;
-    const int64_t lo = p.rows * b / G;
-    const int nr = (int)(p.rows * (b + 1) / G - lo);
+    const int64_t lo = p.row0 + p.rows * b / G;  // global rows of B0 (row0 = 0 on one GPU)
+    const int nr = (int)(p.row0 + p.rows * (b + 1) / G - lo);
     int it = st->it;
+    const bool mx = p.world > 1;
+    unsigned xe = st->xepoch;  // world > 1: exchanges so far (monotone: a stale stamp never matches)
+    const int nqx = 2 + 2 * l;  // exchanged sums: yy, vy, V^T y (l), P^T y (l)
+    __shared__ double totc[2 + 2 * 128];
 
     auto feed = [&]() {
         const int64_t k = pk;
@@ -178,15 +223,36 @@ __global__ void __launch_bounds__(T) gb_persist(const GbParams p) {
                 vt += p.V[r * p.ldv + tid] * yr;
                 pt += (double)p.P[r * p.ldp + tid] * yr;
             }
-        double *pr = my_part();
-        if (tid == 0) pr[0] = pr[1] = 0.0;
-        if (tid < l) {
-            pr[2 + tid] = vt;
-            pr[2 + kp + tid] = pt;
+        if (mx) {
+            const unsigned sx = ++xe;
+            for (int r = 0; r < p.world; ++r) {
+                ulonglong2 *dst = p.sx[r] + (((int64_t)(sx & 1u) * p.world + p.rank) * G + b) * nqx;
+                if (tid == 0) {
+                    ll_send(dst + 0, sx, 0.0);
+                    ll_send(dst + 1, sx, 0.0);
+                }
+                if (tid < l) {
+                    ll_send(dst + 2 + tid, sx, vt);
+                    ll_send(dst + 2 + l + tid, sx, pt);
+                }
+            }
+            gx_totals(p.sx[p.rank] + (int64_t)(sx & 1u) * p.world * G * nqx, p.world * G, nqx, sx, totc, st);
+            for (int i = tid; i < l; i += T) {
+                tot[2 + i] = totc[2 + i];
+                tot[2 + kp + i] = totc[2 + l + i];
+            }
+            __syncthreads();
+        } else {
+            double *pr = my_part();
+            if (tid == 0) pr[0] = pr[1] = 0.0;
+            if (tid < l) {
+                pr[2 + tid] = vt;
+                pr[2 + kp + tid] = pt;
+            }
+            __threadfence();
+            grid_sync(p.gbar);
+            grid_totals(2 + kp + l);
         }
-        __threadfence();
-        grid_sync(p.gbar);
-        grid_totals(2 + kp + l);
         make_cg(ny_s);
     }
 
@@ -198,6 +264,34 @@ __global__ void __launch_bounds__(T) gb_persist(const GbParams p) {
         const double *ycur = p.ybuf + (int64_t)(it & 1) * p.ystride;
         double *ynew = p.ybuf + (int64_t)((it + 1) & 1) * p.ystride;
         float4 vr[NV];
+        if (mx && it != pit0) {  // the previous iteration's y rows of every rank, stamped
+            const ulonglong2 *ya = p.yx[p.rank] + (int64_t)(xe & 1u) * p.n;
+            const unsigned long long t0 = globaltimer_ns();
+            for (unsigned spin = 0;; ++spin) {
+                bool ok = true;
+#pragma unroll
+                for (int k = 0; k < NV; ++k) {
+                    const int idx = k * T + tid;
+                    double y4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        if (idx < p.n4 && 4 * idx + c < p.n) {
+                            const ulonglong2 w = ld_volatile_u2(ya + 4 * (int64_t)idx + c);
+                            ok &= (unsigned)(w.x >> 32) == xe && (unsigned)(w.y >> 32) == xe;
+                            y4[c] = __hiloint2double((int)(unsigned)w.y, (int)(unsigned)w.x);
+                        }
+                    vr[k] = make_float4((float)(y4[0] * inv), (float)(y4[1] * inv), (float)(y4[2] * inv),
+                                        (float)(y4[3] * inv));
+                }
+                if (ok) break;
+                if ((spin & 255) == 255 && globaltimer_ns() - t0 > 30000000000ull) {
+                    st->status = -6;
+                    st->stop = 1;
+                    break;
+                }
+                __nanosleep(64);
+            }
+        } else {
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
             const int idx = k * T + tid;
@@ -208,6 +302,8 @@ __global__ void __launch_bounds__(T) gb_persist(const GbParams p) {
             }
             vr[k] = make_float4((float)(lo2.x * inv), (float)(lo2.y * inv), (float)(hi2.x * inv), (float)(hi2.y * inv));
         }
+        }
+        const unsigned sxn = xe + 1u;  // world > 1: this iteration's exchange stamp
         const double cv = tid < l ? cvec[tid] : 0.0, gv = tid < l ? gvec[tid] : 0.0;
         double a_yy = 0.0, a_vy = 0.0, a_vt = 0.0, a_pt = 0.0;
         for (int k = 0; k < nr; ++k) {
@@ -259,23 +355,47 @@ __global__ void __launch_bounds__(T) gb_persist(const GbParams p) {
                 a_yy += y * y;
                 a_vy += (__ldcg(ycur + r) * inv) * y;
             }
+            if (mx && tid < p.world)  // y_r to every rank (one thread per destination rank)
+                ll_send(p.yx[tid] + (int64_t)(sxn & 1u) * p.n + r, sxn, y);
             if (tid < l) {
                 a_vt += vri * y;
                 a_pt += pri * y;
             }
         }
-        double *pr = my_part();
-        if (tid == 0) {
-            pr[0] = a_yy;
-            pr[1] = a_vy;
+        if (mx) {
+            xe = sxn;
+            for (int r = 0; r < p.world; ++r) {
+                ulonglong2 *dst = p.sx[r] + (((int64_t)(sxn & 1u) * p.world + p.rank) * G + b) * nqx;
+                if (tid == 0) {
+                    ll_send(dst + 0, sxn, a_yy);
+                    ll_send(dst + 1, sxn, a_vy);
+                }
+                if (tid < l) {
+                    ll_send(dst + 2 + tid, sxn, a_vt);
+                    ll_send(dst + 2 + l + tid, sxn, a_pt);
+                }
+            }
+            gx_totals(p.sx[p.rank] + (int64_t)(sxn & 1u) * p.world * G * nqx, p.world * G, nqx, sxn, totc, st);
+            if (tid < 2) tot[tid] = totc[tid];
+            for (int i = tid; i < l; i += T) {
+                tot[2 + i] = totc[2 + i];
+                tot[2 + kp + i] = totc[2 + l + i];
+            }
+            __syncthreads();
+        } else {
+            double *pr = my_part();
+            if (tid == 0) {
+                pr[0] = a_yy;
+                pr[1] = a_vy;
+            }
+            if (tid < l) {
+                pr[2 + tid] = a_vt;
+                pr[2 + kp + tid] = a_pt;
+            }
+            __threadfence();
+            grid_sync(p.gbar);
+            grid_totals(2 + kp + l);
         }
-        if (tid < l) {
-            pr[2 + tid] = a_vt;
-            pr[2 + kp + tid] = a_pt;
-        }
-        __threadfence();
-        grid_sync(p.gbar);
-        grid_totals(2 + kp + l);
         const int itn = it + 1;
         if (tid == 0) {
             const double nyn = sqrt(tot[0]);
@@ -302,6 +422,7 @@ __global__ void __launch_bounds__(T) gb_persist(const GbParams p) {
             done_s = done;
             if (b == 0) {
                 st->it = itn;
+                if (mx) st->xepoch = xe;
                 if (done < 2) {
                     st->ny = nyn;
                     st->d = d;
@@ -316,7 +437,16 @@ __global__ void __launch_bounds__(T) gb_persist(const GbParams p) {
         __syncthreads();
         it = itn;
         const int done = done_s;
-        if (done) break;
+        if (done) {
+            if (mx) {  // the full final y (every rank's rows) into this rank's ybuf for the extraction
+                const ulonglong2 *ya = p.yx[p.rank] + (int64_t)(xe & 1u) * p.n;
+                double *yfin = p.ybuf + (int64_t)(it & 1) * p.ystride;
+                const unsigned long long t0 = globaltimer_ns();
+                for (int64_t j = (int64_t)b * T + tid; j < p.n; j += (int64_t)G * T)
+                    yfin[j] = ll_recv(ya + j, xe, t0, st);
+            }
+            break;
+        }
         make_cg(ny_s);
     }
     if (tid == 0 && nr > 0)  // drain the rows fed ahead

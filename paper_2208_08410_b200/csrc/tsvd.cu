@@ -252,6 +252,10 @@ struct tsvd_s {
     int S_ps = 0;
     size_t smem_ps = 0;
     int grid_gb = 0;  // explicit-Gram iteration grid (from n, identical on every rank)
+    char *gx_mem = nullptr;             // explicit Gram, world > 1: [y area 2n | sums area] (IPC)
+    void *gx_map[kMaxRanks] = {};
+    ulonglong2 *gx_y[kMaxRanks] = {}, *gx_s[kMaxRanks] = {};
+    bool gx_ok = false;
     double ps_ms = 0.0;    // TIMING: event time of the persistent launches, and the passes they ran
     int64_t ps_passes = 0, ps_launches = 0;  // debug knob TSVD_CARVEOUT=0: leave the driver's per-kernel L1/shared split
     size_t smem = 0;
@@ -1422,6 +1426,54 @@ static tsvd_status build_gram(tsvd_t h) {
     return TSVD_OK;
 }
 
+// Explicit Gram, world > 1: exchange areas of the row-partitioned iterations (gb_persist): every
+// rank's [2][n] stamped y words + [2][world][G][2 + 2k] stamped sums, IPC handles all-gathered with
+// NCCL (as setup_px).  On any failure every rank falls back to replicated iterations.
+static tsvd_status setup_gx(tsvd_t h) {
+    if (h->gx_mem || h->world > kMaxRanks || h->k > 129) return TSVD_OK;
+    const size_t ny = (size_t)2 * h->n, ns = (size_t)2 * h->world * h->grid_gb * (2 + 2 * h->k);
+    CK(cudaMalloc((void **)&h->gx_mem, (ny + ns) * sizeof(ulonglong2)));
+    CK(cudaMemset(h->gx_mem, 0, (ny + ns) * sizeof(ulonglong2)));
+    cudaIpcMemHandle_t mine;
+    CK(cudaIpcGetMemHandle(&mine, h->gx_mem));
+    char *dbuf = nullptr;
+    CK(cudaMalloc((void **)&dbuf, sizeof(cudaIpcMemHandle_t) * (h->world + 1)));
+    CK(cudaMemcpy(dbuf, &mine, sizeof(mine), cudaMemcpyHostToDevice));
+    NK(ncclAllGather(dbuf, dbuf + sizeof(mine), sizeof(mine), ncclUint8, h->comm, h->stream));
+    std::vector<cudaIpcMemHandle_t> all(h->world);
+    CK(cudaMemcpyAsync(all.data(), dbuf + sizeof(mine), sizeof(mine) * h->world, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(dbuf);
+    bool ok = true;
+    for (int r = 0; r < h->world; ++r) {
+        char *base = h->gx_mem;
+        if (r != h->rank) {
+            void *q = nullptr;
+            cudaError_t e = cudaIpcOpenMemHandle(&q, all[r], cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                ok = false;
+                continue;
+            }
+            h->gx_map[r] = q;
+            base = (char *)q;
+        }
+        h->gx_y[r] = (ulonglong2 *)base;
+        h->gx_s[r] = (ulonglong2 *)base + ny;
+    }
+    int *dflag = nullptr;
+    CK(cudaMalloc((void **)&dflag, sizeof(int)));
+    const int okv = ok ? 1 : 0;
+    CK(cudaMemcpy(dflag, &okv, sizeof(int), cudaMemcpyHostToDevice));
+    NK(ncclAllReduce(dflag, dflag, 1, ncclInt, ncclMin, h->comm, h->stream));
+    int agreed = 0;
+    CK(cudaMemcpyAsync(&agreed, dflag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(dflag);
+    h->gx_ok = agreed == 1 && !getenv("TSVD_GX_REPLICATED");  // env: A/B against replicated iterations
+    return TSVD_OK;
+}
+
 static tsvd_status run_explicit(tsvd_t h, int l0) {
     if (h->sparse || h->streaming || h->split != 1 || !h->gb)
         return h->fail(TSVD_ERR_UNSUPPORTED, "METHOD=1 (explicit Gram) needs a dense, HBM-resident input "
@@ -1439,6 +1491,7 @@ static tsvd_status run_explicit(tsvd_t h, int l0) {
         CK(cudaMemsetAsync(h->zero64, 0, (size_t)h->kpad * sizeof(double), h->stream));
     }
     if (!h->B0_ok) TRY(build_gram(h));
+    if (h->world > 1) TRY(setup_gx(h));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (h->timing) {
         CK(cudaEventCreate(&e0));
@@ -1450,6 +1503,18 @@ static tsvd_status run_explicit(tsvd_t h, int l0) {
         g.B = h->B0;
         g.ldb = h->ldb0;
         g.rows = n;
+        g.row0 = 0;
+        g.world = 1;
+        if (h->world > 1 && h->gx_ok) {  // rows [n r / W, n (r + 1) / W) of B0 on rank r
+            g.row0 = n * h->rank / h->world;
+            g.rows = n * (h->rank + 1) / h->world - g.row0;
+            g.world = h->world;
+            g.rank = h->rank;
+            for (int r = 0; r < h->world; ++r) {
+                g.yx[r] = h->gx_y[r];
+                g.sx[r] = h->gx_s[r];
+            }
+        }
         g.n = (int32_t)n;
         g.n4 = (int32_t)((n + 3) / 4);
         g.P = h->Pm;
@@ -2415,11 +2480,12 @@ void tsvd_destroy(tsvd_t h) {
     for (int r = 0; r < kMaxRanks; ++r) {
         if (h->peer_map[r]) cudaIpcCloseMemHandle(h->peer_map[r]);
         if (h->px_map[r]) cudaIpcCloseMemHandle(h->px_map[r]);
+        if (h->gx_map[r]) cudaIpcCloseMemHandle(h->gx_map[r]);
     }
     void *dev_ptrs[] = {h->A_own, h->U32, h->V64, h->S64, h->ybuf, h->yw, h->V0d, h->c64, h->ypart,
                         h->wpart, h->part, h->u64, h->sq_part, h->sig2, h->st, h->stats, h->sym, h->gbar,
                         h->trace_d, h->work, h->tl_d, h->vprev32, h->px_mem, h->y32, h->t32, h->At,
-                        h->B0, h->Pm, h->Qm, h->gpart, h->zero64, h->g_hi, h->g_lo, h->pub, h->puby};
+                        h->B0, h->Pm, h->Qm, h->gpart, h->zero64, h->g_hi, h->g_lo, h->pub, h->puby, h->gx_mem};
     if (h->cublas) cublasDestroy(h->cublas);
     if (h->trace_f) fclose(h->trace_f);
     for (void *p : dev_ptrs)

@@ -51,8 +51,9 @@ def test_sparse_row_partition_parity(world, block):
 @pytest.mark.parametrize("world", [2, 4])
 def test_explicit_gram_row_partition_parity(world):
     """METHOD=1 on row slabs: B0 = sum_g A_g^T A_g by one NCCL all-reduce (Alg. 3's Reduce_sum,
-    P:242), the iterations on B0 replicated on every rank, the per-component extraction sums
-    [A^T u | U^T u | ||u||^2] all-reduced — against the oracle, bitwise equal S and V on all ranks."""
+    P:242), the iterations row-partitioned over B0 with an in-kernel stamped-word exchange of the y
+    rows and sums, the per-component extraction sums [A^T u | U^T u | ||u||^2] all-reduced —
+    against the oracle, bitwise equal S and V on all ranks."""
     if not torch.cuda.is_available() or torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
