@@ -118,8 +118,9 @@ typedef enum {
                                     symmetric block schedule of P:348), then per iteration
                                     y = B0 v - P c - V g with P = A^T U, Q = U^T U (exact deflation,
                                     no U^T U = I assumption); dense, resident, n <= 16384.  World > 1:
-                                    B0 all-reduced once, iterations replicated on every rank.  Pays
-                                    off when iterations per component are many                     */
+                                    B0 all-reduced once, iterations row-partitioned over B0 (y rows
+                                    exchanged over NVLink inside the kernel; k <= 129, else
+                                    replicated).  Pays off when iterations per component are many */
 } tsvd_option;
 
 /*
