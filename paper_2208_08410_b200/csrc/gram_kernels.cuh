@@ -91,23 +91,11 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 __device__ __forceinline__ void grid_sync(unsigned *bar) {
     __syncthreads();
     if (threadIdx.x == 0) {
-#ifdef TSVD_GBAR_LEGACY
-        const unsigned gen = ld_acquire_gpu(bar + 1);
-        __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            bar[0] = 0;
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (ld_acquire_gpu(bar + 1) == gen) __nanosleep(32);
-        }
-#else
         const unsigned nb = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
         __threadfence();
         const unsigned old = atomicAdd(bar, nb);
         while (((old ^ ld_acquire_gpu(bar)) & 0x80000000u) == 0u) {
         }
-#endif
         __threadfence();
     }
     __syncthreads();
