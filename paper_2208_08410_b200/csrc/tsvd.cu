@@ -111,7 +111,9 @@ PsFn pick_ps_nv(int nv) {
     default: return nullptr;
     }
 }
-PsFn pick_ps(int T, int nv) {
+PsFn pick_ps(int T, int nv, bool full = false) {
+    if (full && T == 512 && nv == 8) return gv_persist<512, 8, true>;  // n = 16384
+    if (full && T == 512 && nv == 4) return gv_persist<512, 4, true>;  // n = 8192
     switch (T) {
     case 32: return pick_ps_nv<32>(nv);
     case 64: return pick_ps_nv<64>(nv);
@@ -434,7 +436,7 @@ static tsvd_status plan(tsvd_t h) {
         const int64_t extra = kMaxStages * 8 + (int64_t)(2 * (T / 32) + 4 * h->kpad + 2 + kPsGred(T) + 128) * 8;
         int Sp = S;
         while (Sp > 2 && ((int64_t)Sp * h->stage_bytes + extra) * h->cps > kSmemBudget) --Sp;
-        PsFn fn = pick_ps(T, NV);
+        PsFn fn = pick_ps(T, NV, n == (int64_t)4 * NV * T && !getenv("TSVD_NO_FULL"));
         if (fn && ((int64_t)Sp * h->stage_bytes + extra) * h->cps <= kSmemBudget) {
             const size_t sm = (size_t)Sp * h->stage_bytes + (size_t)extra;
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
