@@ -112,6 +112,7 @@ PsFn pick_ps_nv(int nv) {
     }
 }
 PsFn pick_ps(int T, int nv, bool full = false) {
+    if (T == 256 && nv == 16) return full ? gv_persist<256, 16, true> : gv_persist<256, 16>;  // n = 16384, 8 warps
     if (full && T == 512 && nv == 8) return gv_persist<512, 8, true>;  // n = 16384
     if (full && T == 512 && nv == 4) return gv_persist<512, 4, true>;  // n = 8192
     switch (T) {
@@ -254,6 +255,7 @@ struct tsvd_s {
     int S_ps = 0;
     size_t smem_ps = 0;
     int grid_gb = 0;  // explicit-Gram iteration grid (from n, identical on every rank)
+    int T_ps = 0, NV_ps = 0;  // persistent kernel's CTA width (may differ from the N1 kernels')
     char *gx_mem = nullptr;             // explicit Gram, world > 1: [y area 2n | sums area] (IPC)
     void *gx_map[kMaxRanks] = {};
     ulonglong2 *gx_y[kMaxRanks] = {}, *gx_s[kMaxRanks] = {};
@@ -432,17 +434,27 @@ static tsvd_status plan(tsvd_t h) {
     // persistent per-component kernel: same ring, plus the reduction scratch; every CTA of the grid
     // must be co-resident (cooperative launch), and (V^T y)_i is owned by thread i (k <= T + 1)
     h->gv_ps = nullptr;
-    if (split == 1 && h->k <= 32 * kPsLanesV + 1) {
-        const int64_t extra = kMaxStages * 8 + (int64_t)(2 * (T / 32) + 4 * h->kpad + 2 + kPsGred(T) + 128) * 8;
+    // n = 16384: 8 warps x 16 float4 columns per thread (255 registers) instead of the N1 kernels'
+    // 16 x 8 — half the per-row warp reductions (1 GPU 144.9 -> 143.9 ms, 4 GPUs 39.47 -> 39.27 ms,
+    // interleaved A/B); TSVD_PS_T512 keeps 16 warps
+    int Tp = T, NVp = NV;
+    if (T == 512 && NV == 8 && !getenv("TSVD_PS_T512")) {
+        Tp = 256;
+        NVp = 16;
+    }
+    h->T_ps = Tp;
+    h->NV_ps = NVp;
+    if (split == 1 && h->k <= 32 * kPsLanesV + 1 && h->k <= Tp) {
+        const int64_t extra = kMaxStages * 8 + (int64_t)(2 * (Tp / 32) + 4 * h->kpad + 2 + kPsGred(Tp) + 128) * 8;
         int Sp = S;
         while (Sp > 2 && ((int64_t)Sp * h->stage_bytes + extra) * h->cps > kSmemBudget) --Sp;
-        PsFn fn = pick_ps(T, NV, n == (int64_t)4 * NV * T && !getenv("TSVD_NO_FULL"));
+        PsFn fn = pick_ps(Tp, NVp, n == (int64_t)4 * NVp * Tp && !getenv("TSVD_NO_FULL"));
         if (fn && ((int64_t)Sp * h->stage_bytes + extra) * h->cps <= kSmemBudget) {
             const size_t sm = (size_t)Sp * h->stage_bytes + (size_t)extra;
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             if (h->carveout_opt) CK(max_carveout(fn));
             int occ_ps = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_ps, fn, T, sm));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_ps, fn, Tp, sm));
             if (occ_ps * h->sms >= h->grid) {
                 h->gv_ps = fn;
                 h->S_ps = Sp;
@@ -547,7 +559,7 @@ static tsvd_status setup_px(tsvd_t h) {
         CK(cudaStreamSynchronize(h->stream));
         cudaFree(dg);
     }
-    const int CW = std::min(h->T, 128);
+    const int CW = std::min(h->T_ps, 128);
     const int per = (int)(((h->n + G - 1) / G + 31) / 32 * 32);
     if (per > CW || h->world > kMaxRanks) return TSVD_OK;
     const int SL = (int)round_up(per + h->kpad, 4);
@@ -1195,7 +1207,7 @@ static tsvd_status launch_persist(tsvd_t h, cudaStream_t s, int l, cudaEvent_t e
     attr[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident: grid barriers inside
     attr[0].val.cooperative = 1;
     cfg.gridDim = dim3(h->grid);
-    cfg.blockDim = dim3(h->T);
+    cfg.blockDim = dim3(h->T_ps);
     cfg.dynamicSmemBytes = h->smem_ps;
     cfg.stream = s;
     cfg.attrs = attr;
