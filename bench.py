@@ -497,6 +497,7 @@ def main():
             "roofline": roof,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks.summary(),
             "plan": rep["plan"], "loop": rep["loop"], "method": rep.get("method", "gram-vector"),
+            "persistent_plan": {key: rep.get("persistent", {}).get(key) for key in ("enabled", "T", "NV", "stages")},
         }
         if rep.get("method") == "explicit-gram":
             line["gram_ms_per_step"] = rep.get("gram_ms")

@@ -2406,9 +2406,10 @@ tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
              (long long)h->n1_launches, (long long)h->launches, h->loop_mode.c_str(), colls[h->coll]);
     s += tmp;
     snprintf(tmp, sizeof tmp,
-             "\"persistent\": {\"enabled\": %s, \"stages\": %d, \"smem\": %zu, \"ms\": %.6f, \"launches\": %lld, "
-             "\"passes\": %lld}, \"method\": \"%s\", \"gram_ms\": %.3f, \"gram_blocks\": %d, ",
-             (use_persist(h) || h->method == 1) ? "true" : "false", h->method == 1 ? h->S_gb : h->S_ps,
+             "\"persistent\": {\"enabled\": %s, \"T\": %d, \"NV\": %d, \"stages\": %d, \"smem\": %zu, \"ms\": %.6f, "
+             "\"launches\": %lld, \"passes\": %lld}, \"method\": \"%s\", \"gram_ms\": %.3f, \"gram_blocks\": %d, ",
+             (use_persist(h) || h->method == 1) ? "true" : "false", h->method == 1 ? h->T : h->T_ps,
+             h->method == 1 ? h->NV : h->NV_ps, h->method == 1 ? h->S_gb : h->S_ps,
              h->method == 1 ? h->smem_gb : h->smem_ps, h->ps_ms, (long long)h->ps_launches, (long long)h->ps_passes,
              h->method == 1 ? "explicit-gram" : "gram-vector", h->gram_ms, h->gram_blocks);
     s += tmp;
