@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
                 if (jv < j1) {
                     const float *col = reinterpret_cast<const float *>(p.ypart) + jv;
                     const int64_t ld32 = 2 * p.ypart_ld;
-                    constexpr int U = 12;
+                    constexpr int U = NW >= 16 ? 12 : 20;  // one round of loads for G <= U NW (148 CTAs)
                     for (int b0 = warp; b0 < G; b0 += U * NW) {
                         float4 v[U];
 #pragma unroll
