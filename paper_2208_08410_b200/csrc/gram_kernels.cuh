@@ -440,7 +440,8 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     // shared memory is taken by the ring, so each thread keeps its 4*NV floats of v_prev in tensor
     // memory (TMEM, 128 columns: lane quarter = warp % 4, column group = warp / 4) and reloads
     // them per row with tcgen05.ld — TMEM is otherwise unused by this memory-bound kernel.
-    constexpr bool kTmemV = TWO && T == 512 && NV == 8 && SPLIT == 1;
+    constexpr bool kTmemV = TWO && SPLIT == 1 && ((T == 512 && NV == 8) || (T == 256 && NV == 16));
+    constexpr int kCpt = 4 * NV;  // TMEM columns per thread (32 or 64; 128 allocated per CTA)
     __shared__ uint32_t tm_base;
     uint32_t tm_addr = 0;
     if (kTmemV) {
@@ -452,26 +453,29 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        tm_addr = tm_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(32 * (warp >> 2));
+        tm_addr = tm_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(kCpt * (warp >> 2));
         const float4 *src = reinterpret_cast<const float4 *>(p.vprev);
+#pragma unroll
+        for (int c = 0; c < kCpt / 32; ++c) {  // 8 float4 (32 columns) per tcgen05.st
         uint32_t r[32];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int idx = k * T + tid;
+        for (int k8 = 0; k8 < 8; ++k8) {
+            const int idx = (8 * c + k8) * T + tid;
             const float4 v = idx < p.n4 ? src[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
-            r[4 * k + 0] = __float_as_uint(v.x);
-            r[4 * k + 1] = __float_as_uint(v.y);
-            r[4 * k + 2] = __float_as_uint(v.z);
-            r[4 * k + 3] = __float_as_uint(v.w);
+            r[4 * k8 + 0] = __float_as_uint(v.x);
+            r[4 * k8 + 1] = __float_as_uint(v.y);
+            r[4 * k8 + 2] = __float_as_uint(v.z);
+            r[4 * k8 + 3] = __float_as_uint(v.w);
         }
         asm volatile(
             "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-            "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(tm_addr),
+            "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(tm_addr + (uint32_t)(32 * c)),
             "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
             "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
             "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
             "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
             : "memory");
+        }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     } else if (TWO) {  // stage v_prev (fp32, zero padded to n4 float4) once; read per row from smem
         const float4 *src = reinterpret_cast<const float4 *>(p.vprev);

@@ -57,6 +57,9 @@ GvFn pick_nv(int nv) {
     case 2: return gv_fused<T, 2, EX, 1, TWO>;
     case 4: return gv_fused<T, 4, EX, 1, TWO>;
     case 8: return gv_fused<T, 8, EX, 1, TWO>;
+    case 16:
+        if constexpr (T == 256 && TWO && !EX) return gv_fused<256, 16, false, 1, true>;  // n = 16384, 8 warps
+        return nullptr;
     default: return nullptr;
     }
 }
@@ -229,7 +232,7 @@ struct tsvd_s {
     int T = 0, NV = 0, S = 0, grid = 0, cps = 0, stage_bytes = 0, row_bytes = 0;
     int split = 1, parts = 0;  // CTAs per row range (2-CTA cluster for n > 16384); partial slots
     // fused extraction (option 16): N1<TWO> = first iteration of component l + extraction of l-1
-    int fuse_ext_opt = 1, S_two = 0, vp_bytes = 0;
+    int fuse_ext_opt = 1, S_two = 0, vp_bytes = 0, T_two = 0;
     size_t smem_two = 0;
     GvFn gv_two = nullptr;
     float *vprev32 = nullptr;
@@ -418,15 +421,22 @@ static tsvd_status plan(tsvd_t h) {
     // fused-extraction variant: v_prev staged in shared memory, so fewer ring stages
     h->gv_two = nullptr;
     if (split == 1) {
-        // T = 512 (n > 8192): v_prev lives in tensor memory, the ring keeps all its stages
+        // n > 8192: v_prev lives in tensor memory, the ring keeps all its stages.  n = 16384: 256
+        // threads x 16 float4 columns (as the persistent kernel; TSVD_TWO_T512 keeps 512 x 8)
+        int Tt = T, NVt = NV;
+        if (T == 512 && NV == 8 && !getenv("TSVD_TWO_T512")) {
+            Tt = 256;
+            NVt = 16;
+        }
+        h->T_two = Tt;
         h->vp_bytes = (T == 512 && NV == 8) ? 0 : (int)round_up((int64_t)n4 * 16, 128);
-        const int64_t fixed = h->vp_bytes + kMaxStages * sizeof(uint64_t) + 4 * (T / 32) * sizeof(double) + 1024;
+        const int64_t fixed = h->vp_bytes + kMaxStages * sizeof(uint64_t) + 4 * (Tt / 32) * sizeof(double) + 1024;
         int S2 = (int)std::min<int64_t>(S, (kSmemBudget / h->cps - fixed) / h->stage_bytes);
         if (S2 >= 2) {
             h->S_two = S2;
             h->smem_two = (size_t)S2 * h->stage_bytes + h->vp_bytes + kMaxStages * sizeof(uint64_t) +
-                          4 * (T / 32) * sizeof(double);
-            h->gv_two = pick_gv<false, true>(T, NV);
+                          4 * (Tt / 32) * sizeof(double);
+            h->gv_two = pick_gv<false, true>(Tt, NVt);
             CK(cudaFuncSetAttribute(h->gv_two, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_two));
             if (h->carveout_opt) CK(max_carveout(h->gv_two));
         }
@@ -1114,7 +1124,7 @@ static tsvd_status launch_two(tsvd_t h, cudaStream_t s, int l) {
     p.reduce_mode = 0;
     p.tl = nullptr;
     p.trace = nullptr;
-    CK(launch_k(h, h->gv_two, h->grid, h->T, h->smem_two, s, 1, p));
+    CK(launch_k(h, h->gv_two, h->grid, h->T_two, h->smem_two, s, 1, p));
     return TSVD_OK;
 }
 
@@ -1130,7 +1140,7 @@ static tsvd_status launch_fused_first(tsvd_t h, cudaStream_t s, int l, cudaEvent
     p.reduce_mode = 0;
     p.tl = nullptr;
     p.trace = nullptr;
-    CK(launch_k(h, h->gv_two, h->grid, h->T, h->smem_two, s, 1, p));
+    CK(launch_k(h, h->gv_two, h->grid, h->T_two, h->smem_two, s, 1, p));
     if (e1) CK(cudaEventRecord(e1, s));
     if (h->coll == COLL_PEER) {
         PubParams q = pub_params(h, 0, l);
@@ -2415,8 +2425,9 @@ tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
     s += tmp;
     snprintf(tmp, sizeof tmp,
              "\"plan\": {\"T\": %d, \"NV\": %d, \"stages\": %d, \"ctas_per_sm\": %d, \"grid\": %d, \"smem\": %zu, "
-             "\"stage_bytes\": %d, \"run_rows\": %d, \"split\": %d, \"fused_extract\": %s, \"pdl\": %s, \"serpentine\": %s}, ",
-             h->T, h->NV, h->S, h->cps, h->grid, h->smem, h->stage_bytes, h->run_rows, h->split,
+             "\"stage_bytes\": %d, \"run_rows\": %d, \"split\": %d, \"two_T\": %d, \"fused_extract\": %s, \"pdl\": %s, "
+             "\"serpentine\": %s}, ",
+             h->T, h->NV, h->S, h->cps, h->grid, h->smem, h->stage_bytes, h->run_rows, h->split, h->T_two,
              h->fused_ext_used ? "true" : "false", h->pdl_opt ? "true" : "false",
              h->serp_opt && !h->streaming ? "true" : "false");
     s += tmp;
