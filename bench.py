@@ -7,15 +7,19 @@ u = A v / sigma extraction, on the BASELINE.json configs[1] workload (65536 x 16
 k = 16, in HBM) with a known (Hadamard, rank 32, s_i = 0.8^i) spectrum.  A (4 GiB) is larger
 than L2 (126 MB), so no L2 flush is needed between steps.
 
-  value      = whole-job bytes of A streamed (4 m n per Gram pass and per extraction pass)
+  value      = whole-job bytes of A actually streamed per step (4 m n per pass over A: every Gram
+               pass, plus the separate extraction passes — with the fused two-vector pass only the
+               last component's; the others ride inside the next component's first Gram pass)
                / device time of the K timed steps (CUDA events on the library's stream, max over ranks)
   e2e        = the same metric through the public API with A in pinned HOST memory: every step
                copies A host->device and reads U, S, V back
   roofline   = the fused kernel N1: algorithmic bytes per launch / its CUDA-event duration
   cpu_baseline = the fp64 oracle (oracle/) on a bounded sample of the same workload
 
-Multi-GPU (torchrun): rows split across ranks, one NCCL all-reduce per iteration,
-strong scaling (total work fixed).  `--impl reference` times the CPU oracle as the reference arm.
+Multi-GPU: `--gpus N` without torchrun re-launches this script under torch.distributed.run with N
+processes (one per GPU); under torchrun WORLD_SIZE must equal N.  Rows split across ranks
+(P:323-325), one cross-rank reduction per iteration, strong scaling (total work fixed).
+`--impl reference` times the CPU oracle as the reference arm.
 """
 from __future__ import annotations
 
@@ -162,6 +166,25 @@ def ncu_traffic(cfg_name):
         return None
 
 
+def host_info():
+    """CPU model, sockets, threads and RAM of the box the oracle runs on."""
+    info = {"threads_available": len(os.sched_getaffinity(0))}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            key, _, val = line.partition(":")
+            if key.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                info[key.strip().lower().replace("(s)", "s").replace(" ", "_")] = val.strip()
+    except Exception:
+        pass
+    try:
+        with open("/proc/meminfo") as f:
+            info["ram_gib"] = round(int(f.readline().split()[1]) / 2**20, 1)
+    except Exception:
+        pass
+    return info
+
+
 def cpu_baseline(A, cfg, budget_s=15.0):
     """The oracle (as it stands) on a bounded sample: component 1 with a fixed iteration count.
     A: dense fp32 array, or a CSR tuple for the sparse configs; value in the bench's own unit."""
@@ -185,7 +208,7 @@ def cpu_baseline(A, cfg, budget_s=15.0):
     run(T)
     dt = time.perf_counter() - t0
     return {"value": (T * per_iter_b + per_ext_b) / dt / 1e9, "unit": "GB/s", "cores": oracle.num_threads(),
-            "kind": "oracle",
+            "kind": "oracle", "host": host_info(),
             "sample": f"component 1 of {cfg['m']}x{n} (rows {m_s}), fixed T={T} Gram passes + 1 extraction, "
                       f"fp64 plain C, {dt:.2f} s"}
 
@@ -215,7 +238,7 @@ def run_reference(args, cfg):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["workload"], "m": cfg["m"], "n": cfg["n"], "k": cfg["k"]},
             "cpu_baseline": {"value": val, "unit": "GB/s", "cores": oracle.num_threads(), "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "host": host_info()},
             "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -254,11 +277,24 @@ def main():
     if args.impl == "reference":
         return run_reference(args, cfg)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch under torch.distributed.run (the driver may call us directly)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        return subprocess.call(cmd)
+
     import torch
     import torch.distributed as dist
     import paper_2208_08410_b200 as P
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        return 2
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -356,7 +392,12 @@ def main():
     rep = t.report()
     kf, iters, dots = t.info()
     U, S, V = t.result()
-    passes = int(np.sum(iters[:kf])) + kf
+    # passes over A actually streamed in one step: every Gram pass, plus the separate extraction
+    # passes — with the fused two-vector pass (plan.fused_extract) the extraction of components
+    # 0..k-2 rides inside the next component's first Gram pass, so only the last one reads A again
+    fused_ext = bool(rep["plan"].get("fused_extract"))
+    ext_passes = (1 if kf else 0) if fused_ext else kf
+    passes = int(np.sum(iters[:kf])) + ext_passes
     if sparse:  # compulsory bytes: CSR + CSC per iteration, CSR per extraction
         nnz = m * cfg["d"]
         bytes_step = (int(np.sum(iters[:kf])) * (16.0 * nnz + 8.0 * (m + 1) + 8.0 * (n + 1))
@@ -364,8 +405,21 @@ def main():
     else:
         bytes_step = 4.0 * m * n * passes
     value = bytes_step * args.steps / (ms / 1e3) / 1e9
+    # the same step credited with k extraction passes (the algorithmic work of Alg. 1 as written)
+    alg_bytes_step = 4.0 * m * n * (int(np.sum(iters[:kf])) + kf) if not sparse else bytes_step
     sig_err = (float(np.max(np.abs(S[:kf] - planted(cfg)[:kf]) / planted(cfg)[:kf]))
                if kf and not sparse else None)
+    v_err = None
+    if kf and cfg["family"] in ("hadamard", "hadamard_device") and m >= n:
+        # V against the planted right Walsh factor (closed form, synth.hadamard_lowrank's own draws)
+        rng = np.random.Generator(np.random.PCG64(1))
+        rng.choice(m, size=cfg["rank"], replace=False)
+        b_idx = rng.choice(n, size=cfg["rank"], replace=False)
+        rng.choice(np.array([-1.0, 1.0]), size=m)
+        d2 = rng.choice(np.array([-1.0, 1.0]), size=n)
+        right = synth._walsh_factor(n, b_idx, d2, slice(None)) / np.sqrt(n)
+        v_err = float(max(1.0 - abs(float(V[:, i].astype(np.float64) @ right[:, i]))
+                          / float(np.linalg.norm(V[:, i].astype(np.float64))) for i in range(kf)))
 
     # ---- roofline of the dominant kernel (N1): per-launch CUDA events, same workload, one step
     t.set_option(P.OPT_TIMING, 1)
@@ -493,7 +547,11 @@ def main():
                        "parallelism": f"row-partition x{world}",
                        "l2": "no flush: the matrix read every pass is larger than L2 (126 MB)"},
             "iterations": [int(x) for x in iters[:kf]], "k_found": kf, "status": rc,
-            "check": {"sigma_max_rel_err_vs_planted": sig_err},
+            "check": {"sigma_max_rel_err_vs_planted": sig_err, "v_max_1_minus_cos_vs_planted": v_err},
+            "passes_over_A_per_step": passes if not sparse else None,
+            "value_counting_k_extraction_passes": alg_bytes_step * args.steps / (ms / 1e3) / 1e9,
+            "gbps_eff_per_iteration": roof.get("achieved") if roof.get("bound") == "hbm" else None,
+            "comm_world": rep.get("world"), "collective": rep.get("collective"),
             "roofline": roof,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks.summary(),
             "plan": rep["plan"], "loop": rep["loop"], "method": rep.get("method", "gram-vector"),

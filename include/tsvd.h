@@ -14,8 +14,11 @@
  *   until |v . v1| >= 1 - eps, then extracts u = A v1 / sigma, sigma = ||A v1||
  *   with the ORIGINAL A.
  *
- * Orientation: m >= n runs the V-first (X'^T X') branch.  m < n is
- * not in this version (TSVD_ERR_UNSUPPORTED).
+ * Orientation (Alg. 1): m >= n runs the V-first (X'^T X') branch (square inputs too);
+ * m < n runs the U-first (X' X'^T) branch of P:88-92 / Eq. 3 as the V-first branch of
+ * A^T, with U and V swapped at the boundary.  Layout (tsvd_create): a row-major tall A and a
+ * column-major wide A (= A^T row-major) are used in place; a row-major wide A or a column-major
+ * tall A is transposed once into a device copy (one GPU).
  *
  * Conventions for every function:
  *   - No exceptions cross the ABI.  Every call returns a tsvd_status (warnings > 0, errors < 0)
@@ -24,10 +27,14 @@
  *     consumes them (tsvd_run / tsvd_gram_apply) returns.  Outputs are copied into caller-owned
  *     buffers.  The handle owns every device buffer, stream, graph and communicator it creates.
  *   - A handle is not thread-safe; one host thread per handle.  One handle per GPU per process.
- *   - Multi-GPU (row partition): each rank owns rows [row_begin, row_end) of A and
- *     of U; S and V are replicated.  Every rank calls every function with the same (m, n, k, eps)
- *     and options.  One NCCL all-reduce of [y_g | w_g] per iteration (Alg. 4 lines 6, 8, 16,
- *     P:269-279, merged into one).
+ *   - Multi-GPU, one process per GPU.  Row partition (RSVD/HSVD, row-major tall A):
+ *     each rank owns rows [row_begin, row_end) of A and of U; S and V are replicated.  Column
+ *     partition (CSVD, column-major wide A): each rank owns columns [row_begin, row_end)
+ *     of A and those rows of V; S and U are replicated.  Every rank calls every function with
+ *     the same (m, n, k, eps) and options.  Per iteration ONE reduction of [y_g | w_g] across ranks
+ *     (Alg. 4 lines 6, 8, 16, merged): by default inside the kernels over NVLink peer
+ *     memory (CUDA IPC-mapped buffers, stamped words, no library call; TSVD_OPT_COLLECTIVE = 0);
+ *     ncclAllReduce with TSVD_OPT_COLLECTIVE = 1 and for sparse inputs.
  */
 #ifndef TSVD_H
 #define TSVD_H
@@ -42,7 +49,10 @@ extern "C" {
 typedef struct tsvd_s *tsvd_t; /* opaque handle */
 
 typedef enum { TSVD_F32 = 0 /* A, U stored fp32, all cross-thread sums fp64 */, TSVD_F64 = 1 /* reserved */ } tsvd_dtype;
-typedef enum { TSVD_ROW_MAJOR = 0, TSVD_COL_MAJOR = 1 /* reserved */ } tsvd_layout;
+typedef enum {
+    TSVD_ROW_MAJOR = 0,  /* A[i, j] at A[i * ld + j]; range arguments count rows                       */
+    TSVD_COL_MAJOR = 1   /* A[i, j] at A[i + j * ld]; range arguments count columns (the major dim.)    */
+} tsvd_layout;
 typedef enum { TSVD_MEM_DEVICE = 0, TSVD_MEM_HOST_PINNED = 1, TSVD_MEM_HOST_PAGEABLE = 2 } tsvd_mem;
 
 typedef enum {
@@ -90,8 +100,8 @@ typedef enum {
                                     reproducible only to rounding; measured slower on dense C2)        */
     TSVD_OPT_GRAPH_UNROLL = 15,  /* iterations per CUDA-graph WHILE body (1..8, default 2): later ones
                                     are no-ops once the component has stopped                        */
-    TSVD_OPT_FUSED_EXTRACT = 16, /* dense resident input: 1 (default) = the extraction u = A v (Alg. 2
-                                    line 10) of component l-1 rides in the same pass over A
+    TSVD_OPT_FUSED_EXTRACT = 16, /* dense resident input: 1 (default) = the extraction u = A v (Alg. 1
+                                    lines 12-14) of component l-1 rides in the same pass over A
                                     as the first iteration of component l (one read of A saved per
                                     component); 0 = separate extraction pass. Same results to
                                     rounding (DESIGN R21)                                             */
@@ -103,11 +113,11 @@ typedef enum {
                                     range backwards on odd iterations so the rows last read by the
                                     previous pass (still in the 126 MB L2) are read first; 0 = always
                                     forward. Changes only the fp32 summation order (rounding)       */
-    TSVD_OPT_PERSISTENT = 19,    /* single GPU, dense resident, n <= 16384: 1 (default) = the
-                                    iterations of a component run inside ONE cooperative kernel
-                                    (grid barriers, in-kernel reduction and stop test; no per-
-                                    iteration kernel boundaries); 0 = one fused pass + finalize
-                                    kernel per iteration (needed to profile single passes)          */
+    TSVD_OPT_PERSISTENT = 19,    /* dense resident, n <= 16384, one GPU or several with the peer
+                                    collective: 1 (default) = the iterations of a component run inside
+                                    ONE cooperative kernel (grid barrier, in-kernel reduction, cross-
+                                    rank exchange and stop test; no per-iteration kernel boundaries);
+                                    0 = one fused pass + finalize kernel per iteration                */
     TSVD_OPT_SPARSE_BLOCK = 20,  /* sparse: width (elements) of the index blocks the gathers are
                                     split into so that each launch's block of the fp32 gathered
                                     vector stays in L2; 0 (default) = 32 MiB of fp32 (n > 8M
@@ -127,10 +137,13 @@ typedef enum {
  * tsvd_create — new handle for an m x n fp32 problem, k components (k == -1 -> min(m, n),
  * P:71-72), stop rule |v0 . v1| >= 1 - eps.  Binds the current CUDA device.
  * m < n (wide, Alg. 1 else-branch P:88-92, Eq. 3): the U-first branch, run as the tall
- * problem on a transposed device copy of A (single GPU; the whole matrix is passed to
- * tsvd_set_dense); the iterate and V0 have length m, U and V keep their meaning for A.
- * Errors: TSVD_ERR_ARG (m, n < 1; k < -1 or 0 or > min(m,n); eps not in (0,1); out == NULL),
- *         TSVD_ERR_UNSUPPORTED (dtype != F32, layout != ROW_MAJOR), TSVD_ERR_CUDA.
+ * (V-first) problem on A^T; the iterate and V0 have length m, U and V keep their meaning for A.
+ * layout = TSVD_COL_MAJOR with m < n: A^T is the caller's buffer read row-major, used in place, and
+ * may be column-partitioned across ranks (CSVD).  layout = TSVD_ROW_MAJOR with m < n, or
+ * TSVD_COL_MAJOR with m >= n: the whole matrix is passed to tsvd_set_dense and transposed once into
+ * a device copy (single GPU; the copy doubles the footprint).
+ * Errors: TSVD_ERR_ARG (m, n < 1; k < -1 or 0 or > min(m,n); eps not in (0,1); out == NULL; unknown
+ *         layout), TSVD_ERR_UNSUPPORTED (dtype != F32; k > 4096), TSVD_ERR_CUDA.
  */
 tsvd_status tsvd_create(tsvd_t *out, int64_t m, int64_t n, int32_t k, double eps, tsvd_dtype dtype,
                         tsvd_layout layout);
@@ -156,8 +169,11 @@ tsvd_status tsvd_set_option(tsvd_t h, int32_t key, int64_t value);
 tsvd_status tsvd_set_init(tsvd_t h, const double *V0);
 
 /*
- * tsvd_set_dense — this rank's row slab A[row_begin:row_end, 0:n], fp32 row-major with
- * leading dimension ld >= n (elements).  mem = DEVICE: the pointer is used in place when it
+ * tsvd_set_dense — this rank's slab of A, fp32.  ROW_MAJOR: rows A[row_begin:row_end, 0:n] with
+ * leading dimension ld >= n (elements between rows).  COL_MAJOR: columns A[0:m, row_begin:row_end]
+ * (the range counts columns) with ld >= m (elements between columns).  Layouts that need the
+ * transposed copy (see tsvd_create) take the whole matrix (range [0, major dimension)).
+ * mem = DEVICE: the pointer is used in place when it
  * is 16-byte aligned and ld % 4 == 0, otherwise copied once into a padded device buffer.
  * mem = HOST_*: copied host->device inside every tsvd_run (end-to-end semantics).  If the slab
  * does not fit in HBM (or TSVD_OPT_PLACEMENT = 2) the run is out of memory of degree 1:
@@ -165,8 +181,9 @@ tsvd_status tsvd_set_init(tsvd_t h, const double *V0);
  * (collinear batching) through a q_s-slot device ring on a copy stream, overlapped with
  * the fused kernel.  Pageable input is page-locked (cudaHostRegister) for the
  * duration of a streamed run.
- * The union of all ranks' slabs must be [0, m) with contiguous, disjoint ranges.
- * Errors: TSVD_ERR_ARG (NULL, ld < n), TSVD_ERR_SHAPE (range outside [0, m) or empty),
+ * The union of all ranks' slabs must be [0, m) ([0, n) for COL_MAJOR) with contiguous, disjoint
+ * ranges.
+ * Errors: TSVD_ERR_ARG (NULL, ld too small), TSVD_ERR_SHAPE (range outside the major dimension or empty),
  *         TSVD_ERR_NOMEM (device input that is unaligned and has no room for an aligned copy).
  */
 tsvd_status tsvd_set_dense(tsvd_t h, const float *A, int64_t ld, int64_t row_begin, int64_t row_end, tsvd_mem mem);
@@ -179,8 +196,11 @@ tsvd_status tsvd_set_dense(tsvd_t h, const float *A, int64_t ld, int64_t row_beg
  * (histogram, scan, scatter, per-column sort: deterministic), so every iteration runs the
  * row-wise product t = A v - U c and the column-wise, atomics-free y = A^T t.  The CSC doubles
  * the slab's footprint.  Multi-GPU: the length-n partial y is summed with ncclAllReduce.
- * Errors: TSVD_ERR_ARG (NULL arrays, bad row_ptr ends, columns out of range or unsorted),
- *         TSVD_ERR_SHAPE, TSVD_ERR_UNSUPPORTED (n or rows > 2^31 - 1), TSVD_ERR_CUDA / NOMEM.
+ * row_ptr's ends are read back and checked for device input too (two 8-byte copies) before any
+ * kernel indexes col_idx / val with them.
+ * Errors: TSVD_ERR_ARG (NULL arrays, row_ptr[0] != 0 or row_ptr[rows] != nnz, decreasing row_ptr,
+ *         columns out of range or unsorted), TSVD_ERR_SHAPE, TSVD_ERR_UNSUPPORTED (m < n; n or rows >
+ *         2^31 - 1), TSVD_ERR_CUDA / NOMEM.
  */
 tsvd_status tsvd_set_csr(tsvd_t h, const int64_t *row_ptr, const int32_t *col_idx, const float *val, int64_t nnz,
                          int64_t row_begin, int64_t row_end, tsvd_mem mem);
@@ -188,8 +208,11 @@ tsvd_status tsvd_set_csr(tsvd_t h, const int64_t *row_ptr, const int32_t *col_id
 /*
  * tsvd_set_factors — resume / inject the deflation state: the first l components
  * (checkpoint after component l).  Host buffers: U this rank's slab, (row_end -
- * row_begin) x l fp32 row-major; S fp64[l]; V n x l fp64 row-major.  A later tsvd_run starts at
- * component l.  Errors: TSVD_ERR_ARG (l < 0 or > k, NULL with l > 0), TSVD_ERR_STATE.
+ * row_begin) x l fp32 row-major; S fp64[l]; V n x l fp64 row-major (m < n: U is m x l fp32,
+ * replicated, and V this rank's slab of rows, fp64).  A later tsvd_run starts at component l.
+ * With l > 0 the explicit-Gram state (TSVD_OPT_METHOD = 1: P = A^T U, Q = U^T U) is invalidated,
+ * so a METHOD = 1 run after an injection fails with TSVD_ERR_UNSUPPORTED unless it restarts from
+ * l = 0.  Errors: TSVD_ERR_ARG (l < 0 or > k, NULL with l > 0), TSVD_ERR_STATE.
  */
 tsvd_status tsvd_set_factors(tsvd_t h, int32_t l, const float *U, const double *S, const double *V);
 
@@ -209,7 +232,8 @@ tsvd_status tsvd_run(tsvd_t h);
 
 /* tsvd_get_U_S_V — copy results to caller-owned host buffers (any may be NULL):
  * U: (row_end-row_begin) x k fp32 row-major (this rank's slab), S: fp64[k], V: n x k fp32
- * row-major.  Columns >= k_found are zero. */
+ * row-major.  m < n: U is m x k (replicated) and V is this rank's slab, (row_end-row_begin) x k.
+ * Columns >= k_found are zero. */
 tsvd_status tsvd_get_U_S_V(tsvd_t h, float *U, double *S, float *V);
 
 /* tsvd_get_info — k_found, per-component iteration counts iters[k] and final |v0 . v1| dots[k]

@@ -120,7 +120,10 @@ __device__ __forceinline__ void gx_totals(const ulonglong2 *area, int E, int nqx
                     __nanosleep(64);
                 }
         __syncthreads();
-        if (globaltimer_ns() - t0 > 30000000000ull) return;
+        __shared__ int tout_s;  // give-up decision taken once and shared: the whole block returns
+        if (threadIdx.x == 0) tout_s = globaltimer_ns() - t0 > 30000000000ull;
+        __syncthreads();
+        if (tout_s) return;
     }
 }
 

@@ -181,7 +181,8 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
     __shared__ int64_t slot_row[kMaxStages];
     __shared__ double ny_s;
     __shared__ int done_s;
-    __shared__ int xfail_s;  // world > 1: an exchange timed out (st->stop raised) before publication
+    __shared__ int xfail_s;
+    __shared__ int tout_s;   // the decision poll gave up (30 s): block-uniform exit flag  // world > 1: an exchange timed out (st->stop raised) before publication
     __shared__ double sred[2][32];
     // producer state (thread 0 only; kept in shared memory to leave the registers to the row loop):
     // next row index pk within pass pp of the range [plo, plo + pnr), next ring slot pslot
@@ -648,8 +649,13 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
                             __nanosleep(64);
                         }
                 }
+                // the give-up decision is taken once (thread 0) and shared, so every thread of the
+                // block leaves the poll loop together (a per-thread clock read could split the block
+                // between the __syncthreads_and above and the barrier below)
                 __syncthreads();
-                if (globaltimer_ns() - t0 > 30000000000ull) break;
+                if (tid == 0) tout_s = globaltimer_ns() - t0 > 30000000000ull;
+                __syncthreads();
+                if (tout_s) break;
             }
         }
         __syncthreads();
@@ -686,6 +692,8 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
                 }
             }
             ny_s = (nyn > 0.0 && isfinite(nyn)) ? nyn : 1.0;
+            // a CTA that gave up waiting (30 s) has already set status -6 and stop: keep them
+            if (*reinterpret_cast<volatile int32_t *>(&st->status) == -6) done = 3;
             done_s = done;
             if (b == 0) {
                 st->it = itn;

@@ -1,18 +1,22 @@
 // sparse_kernels.cuh — the Gram-vector product for a CSR row slab (Alg. 4).
 //
-//   N2 csr_spmv   warp per row: t_r = (sum_k val_k y32[col_k]) / ||y_cur|| - U_r . c   (= (X' v)_r,
-//                 v = y_cur / ||y_cur|| folded in, y32 = fp32 copy of the fp64 iterate written by the
-//                 finalize kernel: reading R23); per-block partials of w = U^T t.  EXTRACT: u_r =
-//                 (A v)_r and per-block sum u_r^2.
-//   N3 csc_spmvT  warp per column over the slab's CSC: y_j = sum_k cval_k t[row_k] — the transpose
-//                 product with no atomics and a fixed summation order; block 0 also sums the w
-//                 partials.  y and w land in yw = [y | w] (then the all-reduce across ranks, if any,
-//                 and fin_iter<SRC_YW>).
-//   N4 csc_*      one-time CSR -> CSC of the slab on the device: column histogram, exclusive scan,
-//                 scatter, per-column sort by row index (so the CSC, and every result, is
-//                 deterministic).
-// Products and sums are fp64; the gathered vectors are fp32 copies (the path is bound by the random
-// gathers' DRAM traffic, not by arithmetic).
+// Both products of an iteration are one kernel over "segments" (rows of the CSR for N2, columns of
+// the slab's CSC for N3) — the gathered vector is read through an fp32 copy (reading R23) and every
+// product and sum is fp64:
+//   N2 (MODE_T)  t_r = (sum_k val_k y32[col_k]) / ||y_cur|| - U_r . c   (= (X' v)_r, v = y_cur/||y_cur||
+//                folded in; deflation in the factored form of Eq. 2), t32[r] = fp32(t_r), per-thread
+//                partials of w = U^T t;
+//   N2 (MODE_U)  extraction u_r = (A v)_r and per-block sum u_r^2;
+//   N3 (MODE_Y)  y_j = sum_k cval_k t32[row_k] over the CSC — the transpose product without atomics and
+//                in a fixed order; block 0 also sums the w partials.  y and w land in yw = [y | w].
+// Layout (N4b, built once by tsvd_set_csr): the entries are split into K index blocks so that one
+// launch's gathers stay inside an L2-resident block of the gathered vector (32 MiB of fp32); block b
+// of a direction is a compressed matrix of its own with int32 block-local offsets off[b][0..segs] and
+// an int64 base[b] into the shared idx / val arrays.  The per-segment fp64 sums are carried across the
+// K launches in block order (acc), so every result is deterministic.
+// One THREAD per segment (a CSR row piece of a block holds ~nnz/row/K entries: 8 at c4n): the entry
+// loads of a batch of 8 are issued together, then the 8 gathers, then the fp64 products in entry
+// order — 8 independent L2 gathers in flight per thread, no shuffles, no shared partial sums.
 #pragma once
 #include "fin_kernels.cuh"
 
@@ -21,241 +25,161 @@ namespace tsvd {
 constexpr int kSpThreads = 256;
 constexpr size_t kSpL2BlockBytes = 32u << 20;  // fp32 gather block that stays L2-resident (126 MB L2)
 constexpr int kSpWarps = kSpThreads / 32;
+constexpr int kSpBatch = 8;                     // entries (gathers) in flight per thread
+constexpr int kSpMaxL = 96;                     // deflation columns the per-thread w partials can hold
+
+enum SpMode { MODE_T = 0, MODE_U = 1, MODE_Y = 2 };
+
+// One direction of the product: K blocks of `segs` segments over shared entry arrays.
+struct SpView {
+    const int32_t *off;   // [K][segs + 1] block-local offsets (off[b][0] == 0)
+    const int64_t *base;  // [K + 1] first entry of each block
+    const int32_t *idx;   // gathered indices (columns for the CSR, local rows for the CSC)
+    const float *val;
+    int64_t segs;
+};
 
 struct SpParams {
-    const int64_t *row_ptr;  // CSR of the slab, rows + 1 entries, row_ptr[0] == 0
-    const int32_t *col;
-    const float *val;
+    SpView csr;       // rows of the slab by column block (N2)
+    SpView csc;       // columns of the slab by row block (N3)
     int64_t rows;
-    const int64_t *col_ptr;  // CSC of the same slab, n + 1 entries
-    const int32_t *row_idx;
-    const float *cval;
     int64_t n;
-    const float *U;  // rows x ldu fp32
+    const float *U;   // rows x ldu fp32
     int ldu;
     int l;
     const double *c;
     const double *ybuf;
     int64_t ystride;
     const LoopState *st;
-    double *t;        // [rows] EXTRACT: u_r (fp64)
-    float *t32;       // [rows] iteration: t_r rounded to fp32, gathered by N3
+    double *t;        // [rows] MODE_U: u_r (fp64)
+    float *t32;       // [rows] MODE_T: t_r rounded to fp32, gathered by N3
     const float *y32; // [n] y_cur rounded to fp32 (written by fin_iter), gathered by N2
     double *wpart;    // [gridDim.x][wpart_ld]
     int wpart_ld;
-    double *sq_part;  // [gridDim.x] (EXTRACT)
+    double *sq_part;  // [gridDim.x] (MODE_U)
     double *yw;       // N3 output: y (n) | w (l) at wofs
     int64_t wofs;
     int parts;        // gridDim.x of N2 (rows of wpart)
-    // index blocking (an L2-sized block of the gathered vector per launch): launch `phase` of
-    // `nphase` covers the entries whose gathered index lies in block `phase`; the per-row (column)
-    // partial sums are carried across launches in fp64 and finished by the last launch.  The
-    // blocked pointers of phase b start at row_ptr + b * rows (col_ptr + b * n): one exclusive scan
-    // over [block][segment] counts.
-    int phase, nphase;
-    double *acc;      // [rows] (N2) or [n] (N3) carried partial sums when nphase > 1
+    int phase, nphase;  // launch `phase` of `nphase` covers index block `phase`
+    double *acc;      // [segs] carried fp64 partial sums when nphase > 1
+    int64_t seg0, seg1;  // segments [seg0, seg1) of this launch (N3 last block: column chunks)
 };
 
-// Memory-level parallelism: each warp works on kSpRows consecutive rows (columns) at once.  Per lane,
-// the index/value loads of all of them are issued together (streaming, evict-first: they are read
-// once per pass), then all their gathers, so a warp has kSpRows dependent chains in flight instead
-// of one.  Lane `lane` of row q still sums k = k0 + lane, k0 + lane + 32, ... and the warp tree is
-// the same, so every result is bitwise what one row per warp gives.
-constexpr int kSpRows = 4;
-
-// Lanes per segment: L (8, 16 or 32) lanes share a row (column), so a warp holds 32 / L groups of
-// kSpRows consecutive segments.  The host picks L from the mean segment length (nnz per row per
-// index block): short segments (blocked, or sparse rows) would otherwise leave most lanes idle.
-
-// bounds of the group's kSpRows segments starting at rb: group lanes 0..kSpRows load
-// ptr[min(rb + lane, segs)], broadcast within the group; segments past the end are empty
-template <int L>
-__device__ __forceinline__ void sp_bounds(const int64_t *ptr, int64_t rb, int64_t segs, int sl, int64_t (&kb)[kSpRows],
-                                          int64_t (&ke)[kSpRows]) {
-    int64_t v = 0;
-    if (sl <= kSpRows) v = __ldcs(ptr + (rb + sl < segs ? rb + sl : segs));
+// sum_k val[k] x[idx[k]] over [k0, k1), entry order, fp64
+__device__ __forceinline__ double sp_segment_dot(const int32_t *__restrict__ ip, const float *__restrict__ vp,
+                                                 const float *__restrict__ x, int32_t k0, int32_t k1) {
+    double sum = 0.0;
+    for (int32_t k = k0; k < k1; k += kSpBatch) {
+        int32_t c[kSpBatch];
+        float v[kSpBatch], g[kSpBatch];
 #pragma unroll
-    for (int q = 0; q < kSpRows; ++q) {
-        kb[q] = __shfl_sync(0xffffffffu, v, q, L);
-        ke[q] = __shfl_sync(0xffffffffu, v, q + 1, L);
-    }
-}
-
-// fp64 sum over the L lanes of a group (butterfly inside the group: every lane gets the total)
-template <int L>
-__device__ __forceinline__ double group_sum(double x) {
-#pragma unroll
-    for (int o = L / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    return x;
-}
-
-// sum_k val[k] x[idx[k]] over [kb[q], ke[q]) for every q: group lane sl takes k = kb + sl, kb + sl
-// + L, ...; fp64 products and sums; the index/value loads of all kSpRows segments are issued
-// together (streaming, evict-first: read once per pass), then all their gathers.  x is an fp32
-// copy of the gathered vector: a random gather costs a whole L2 sector (or line) of DRAM traffic
-// whatever its width, and the fp32 copy is half the footprint, so more of it stays in L2
-// (measured: L2 hit rate 10 % with the fp64 vector at n = 2^25, 24 % fp32, 72 % fp32 + blocks).
-template <int L>
-__device__ __forceinline__ void sp_rows_dot(const int64_t (&kb)[kSpRows], const int64_t (&ke)[kSpRows],
-                                            const int32_t *idx, const float *val, const float *x, int sl,
-                                            double (&s)[kSpRows]) {
-    int64_t maxlen = 0;
-#pragma unroll
-    for (int q = 0; q < kSpRows; ++q) {
-        s[q] = 0.0;
-        maxlen = (ke[q] - kb[q]) > maxlen ? (ke[q] - kb[q]) : maxlen;
-    }
-    for (int64_t off = sl; off < maxlen; off += L) {
-        int32_t ci[kSpRows];
-        float vv[kSpRows];
-#pragma unroll
-        for (int q = 0; q < kSpRows; ++q) {
-            const int64_t k = kb[q] + off;
-            ci[q] = -1;
-            vv[q] = 0.f;
-            if (k < ke[q]) {
-                ci[q] = __ldcs(idx + k);
-                vv[q] = __ldcs(val + k);
-            }
+        for (int u = 0; u < kSpBatch; ++u) {
+            const bool ok = k + u < k1;
+            c[u] = ok ? __ldcs(ip + k + u) : 0;  // streaming: read once per pass
+            v[u] = ok ? __ldcs(vp + k + u) : 0.f;
         }
-        double g[kSpRows];
 #pragma unroll
-        for (int q = 0; q < kSpRows; ++q) g[q] = ci[q] >= 0 ? (double)__ldg(x + ci[q]) : 0.0;
+        for (int u = 0; u < kSpBatch; ++u) g[u] = (k + u < k1) ? __ldg(x + c[u]) : 0.f;
 #pragma unroll
-        for (int q = 0; q < kSpRows; ++q)
-            if (ci[q] >= 0) s[q] += (double)vv[q] * g[q];
+        for (int u = 0; u < kSpBatch; ++u)
+            if (k + u < k1) sum += (double)v[u] * (double)g[u];
     }
-#pragma unroll
-    for (int q = 0; q < kSpRows; ++q) s[q] = group_sum<L>(s[q]);
+    return sum;
 }
 
-// carry the kSpRows segment sums of a group across index blocks (fixed block order): group lane
-// q < kSpRows owns segment rb + q; on the last block the totals are broadcast back into s[]
-template <int L>
-__device__ __forceinline__ bool sp_carry(const SpParams &p, double *acc, int64_t rb, int64_t segs, int sl,
-                                         double (&s)[kSpRows]) {
-    double v = s[0];
-#pragma unroll
-    for (int q = 1; q < kSpRows; ++q)
-        if (sl == q) v = s[q];
-    if (sl < kSpRows && rb + sl < segs) {
-        if (p.phase > 0) v = acc[rb + sl] + v;
-        if (p.phase < p.nphase - 1) acc[rb + sl] = v;
-    }
-    if (p.phase < p.nphase - 1) return false;  // totals not complete yet
-#pragma unroll
-    for (int q = 0; q < kSpRows; ++q) s[q] = __shfl_sync(0xffffffffu, v, q, L);
-    return true;
-}
-
-// N2.  Dynamic shared memory: kSpWarps * (32 / L) * l doubles (per-group w accumulators).
-template <bool EXTRACT, int L>
-__global__ void __launch_bounds__(kSpThreads) csr_spmv(const SpParams p) {
-    constexpr int G = 32 / L;
+// N2 / N3.  Dynamic shared memory (MODE_T): l * (kSpThreads + 1) doubles (per-thread w partials, c).
+template <int MODE>
+__global__ void __launch_bounds__(kSpThreads) sp_pass(const SpParams p) {
     extern __shared__ double wsm[];
-    __shared__ double sqw[kSpWarps * G];
+    __shared__ double red[kSpWarps];
     const LoopState *st = p.st;
     griddep_launch();
     griddep_wait();
-    if (st->stop || (!EXTRACT && st->done)) return;
+    if (st->stop || (MODE != MODE_U && st->done)) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int grp = lane / L, sl = lane % L;
-    const int l = EXTRACT ? 0 : p.l;
-    const double inv = 1.0 / st->ny;
-    double *wme = wsm + (warp * G + grp) * (l > 0 ? l : 1);
-    for (int i = sl; i < l; i += L) wme[i] = 0.0;
+    const SpView &V = MODE == MODE_Y ? p.csc : p.csr;
+    const float *__restrict__ x = MODE == MODE_Y ? p.t32 : p.y32;
+    const int l = MODE == MODE_T ? p.l : 0;
+    const bool last = p.phase == p.nphase - 1;
+    const bool carry_in = p.nphase > 1 && p.phase > 0;
+    double *csm = wsm + (int64_t)l * kSpThreads;
+    if (MODE == MODE_T && last) {
+        for (int i = 0; i < l; ++i) wsm[i * kSpThreads + tid] = 0.0;
+        for (int i = tid; i < l; i += kSpThreads) csm[i] = p.c[i];
+        __syncthreads();
+    }
+    const double inv = MODE == MODE_Y ? 1.0 : 1.0 / st->ny;
+    const int32_t *__restrict__ off = V.off + (int64_t)p.phase * (V.segs + 1);
+    const int64_t b0 = V.base[p.phase];
+    const int32_t *__restrict__ ip = V.idx + b0;
+    const float *__restrict__ vp = V.val + b0;
     double sq = 0.0;
-    const int64_t nwarps = (int64_t)gridDim.x * kSpWarps;
-    const int64_t *ptr = p.row_ptr + (int64_t)p.phase * p.rows;
-    for (int64_t r0 = ((int64_t)blockIdx.x * kSpWarps + warp) * (G * kSpRows); r0 < p.rows;
-         r0 += nwarps * (G * kSpRows)) {
-        const int64_t rb = r0 + grp * kSpRows;
-        int64_t kb[kSpRows], ke[kSpRows];
-        sp_bounds<L>(ptr, rb, p.rows, sl, kb, ke);
-        double sr[kSpRows];
-        sp_rows_dot<L>(kb, ke, p.col, p.val, p.y32, sl, sr);
-        if (p.nphase > 1 && !sp_carry<L>(p, p.acc, rb, p.rows, sl, sr)) continue;
-#pragma unroll
-        for (int q = 0; q < kSpRows; ++q) {
-            const int64_t r = rb + q;
-            const bool ok = r < p.rows;  // group-uniform; every lane still joins the shuffles
-            double s = sr[q] * inv;
-            if (!EXTRACT && l > 0) {
-                const float *Ur = p.U + (ok ? r : 0) * p.ldu;
-                double corr = 0.0;  // U_r . c: deflation without forming X' (Eq. 2, factored)
-                if (ok)
-                    for (int i = sl; i < l; i += L) corr += (double)Ur[i] * p.c[i];
-                s -= group_sum<L>(corr);
-                if (ok)
-                    for (int i = sl; i < l; i += L) wme[i] += s * (double)Ur[i];
+    const int64_t stride = (int64_t)gridDim.x * kSpThreads;
+    for (int64_t s = p.seg0 + (int64_t)blockIdx.x * kSpThreads + tid; s < p.seg1; s += stride) {
+        const double carried = carry_in ? __ldcg(p.acc + s) : 0.0;  // issued before the gathers
+        const int32_t k0 = __ldcs(off + s), k1 = __ldcs(off + s + 1);
+        double sum = sp_segment_dot(ip, vp, x, k0, k1);
+        if (carry_in) sum = carried + sum;  // blocks in order
+        if (!last) {
+            p.acc[s] = sum;
+            continue;
+        }
+        if (MODE == MODE_Y) {
+            p.yw[s] = sum;
+        } else if (MODE == MODE_U) {
+            const double u = sum * inv;
+            p.t[s] = u;
+            sq += u * u;
+        } else {
+            double t = sum * inv;
+            if (l > 0) {  // U_r . c: deflation without forming X' (Eq. 2, factored); w += t U_r
+                const float *Ur = p.U + s * p.ldu;
+                double corr = 0.0;
+                for (int i = 0; i < l; ++i) corr += (double)Ur[i] * csm[i];
+                t -= corr;
+                for (int i = 0; i < l; ++i) wsm[i * kSpThreads + tid] += t * (double)Ur[i];
             }
-            if (ok && sl == 0) {
-                if (EXTRACT) p.t[r] = s;
-                else p.t32[r] = (float)s;
-                sq += s * s;
-            }
+            p.t32[s] = (float)t;
         }
     }
-    if (p.phase < p.nphase - 1) return;  // not the last block: only the carried sums were written
-    if (sl == 0) sqw[warp * G + grp] = sq;
-    __syncthreads();
-    if (EXTRACT) {
+    if (!last) return;  // not the last block: only the carried sums were written
+    if (MODE == MODE_U) {
+        sq = warp_sum(sq);
+        if (lane == 0) red[warp] = sq;
+        __syncthreads();
         if (tid == 0) {
             double a = 0.0;
-            for (int w = 0; w < kSpWarps * G; ++w) a += sqw[w];
+            for (int w = 0; w < kSpWarps; ++w) a += red[w];
             p.sq_part[blockIdx.x] = a;
         }
-    } else {
-        for (int i = tid; i < l; i += kSpThreads) {
+    } else if (MODE == MODE_T) {
+        __syncthreads();
+        for (int i = warp; i < l; i += kSpWarps) {  // threads' partials in thread order
             double a = 0.0;
-            for (int w = 0; w < kSpWarps * G; ++w) a += wsm[w * l + i];  // groups in order
-            p.wpart[(int64_t)blockIdx.x * p.wpart_ld + i] = a;
+            for (int j = lane; j < kSpThreads; j += 32) a += wsm[i * kSpThreads + j];
+            a = warp_sum(a);
+            if (lane == 0) p.wpart[(int64_t)blockIdx.x * p.wpart_ld + i] = a;
         }
-    }
-}
-
-// N3.
-template <int L>
-__global__ void __launch_bounds__(kSpThreads) csc_spmvT(const SpParams p) {
-    constexpr int G = 32 / L;
-    const LoopState *st = p.st;
-    griddep_launch();
-    griddep_wait();
-    if (st->stop || st->done) return;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int grp = lane / L, sl = lane % L;
-    const int64_t nwarps = (int64_t)gridDim.x * kSpWarps;
-    const int64_t *ptr = p.col_ptr + (int64_t)p.phase * p.n;
-    for (int64_t j0 = ((int64_t)blockIdx.x * kSpWarps + warp) * (G * kSpRows); j0 < p.n;
-         j0 += nwarps * (G * kSpRows)) {
-        const int64_t jb = j0 + grp * kSpRows;
-        int64_t kb[kSpRows], ke[kSpRows];
-        sp_bounds<L>(ptr, jb, p.n, sl, kb, ke);
-        double sc[kSpRows];
-        sp_rows_dot<L>(kb, ke, p.row_idx, p.cval, p.t32, sl, sc);
-        double v = sc[0];
-#pragma unroll
-        for (int q = 1; q < kSpRows; ++q)
-            if (sl == q) v = sc[q];
-        if (sl < kSpRows && jb + sl < p.n) {
-            if (p.nphase > 1 && p.phase > 0) v = p.acc[jb + sl] + v;
-            if (p.phase < p.nphase - 1) p.acc[jb + sl] = v;
-            else p.yw[jb + sl] = v;
-        }
-    }
-    if (blockIdx.x == 0 && p.phase == p.nphase - 1)
+    } else if (blockIdx.x == 0 && p.seg1 == V.segs) {  // the launch that finishes y also finishes w
         for (int i = warp; i < p.l; i += kSpWarps) {
             double w = 0.0;
             for (int b = lane; b < p.parts; b += 32) w += p.wpart[(int64_t)b * p.wpart_ld + i];
             w = warp_sum(w);
             if (lane == 0) p.yw[p.wofs + i] = w;
         }
+    }
 }
 
 // ---------------------------------------------------------------- N4: CSR -> CSC (one time)
-__global__ void csc_count(const int32_t *__restrict__ col, int64_t nnz, unsigned *__restrict__ cnt) {
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(&cnt[col[k]], 1u);
+// blocked CSC (row block b = r / bwr): entries per [block][column]
+__global__ void csc_blk_count(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col, int64_t rows,
+                              int64_t n, int64_t bwr, unsigned *__restrict__ cnt) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x / 32);
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; r < rows; r += nwarps) {
+        unsigned *cb = cnt + (r / bwr) * n;
+        for (int64_t k = row_ptr[r] + lane; k < row_ptr[r + 1]; k += 32) atomicAdd(&cb[col[k]], 1u);
+    }
 }
 
 constexpr int kScanThreads = 1024, kScanItems = 4, kScanTile = kScanThreads * kScanItems;
@@ -333,19 +257,36 @@ __global__ void scan_add(int64_t *__restrict__ out, int64_t n, const int64_t *__
         out[i] += bsum[i / kScanTile];
 }
 
-// warp per row: claim a slot in each entry's column (order inside a column fixed by csc_sort)
-__global__ void csc_scatter(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                            const float *__restrict__ val, int64_t rows, const int64_t *__restrict__ col_ptr,
-                            unsigned *__restrict__ fill, int32_t *__restrict__ row_idx, float *__restrict__ cval) {
+// warp per row: claim a slot in each entry's [row block][column] segment (order inside a segment fixed
+// afterwards by csc_sort); the stored row index is local to the slab
+__global__ void csc_blk_scatter(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                const float *__restrict__ val, int64_t rows, int64_t n, int64_t bwr,
+                                const int64_t *__restrict__ flat, unsigned *__restrict__ fill,
+                                int32_t *__restrict__ row_idx, float *__restrict__ cval) {
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x / 32);
-    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; r < rows; r += nwarps)
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; r < rows; r += nwarps) {
+        const int64_t sb = (r / bwr) * n;
         for (int64_t k = row_ptr[r] + lane; k < row_ptr[r + 1]; k += 32) {
-            const int32_t j = col[k];
-            const int64_t pos = col_ptr[j] + atomicAdd(&fill[j], 1u);
+            const int64_t seg = sb + col[k];
+            const int64_t pos = flat[seg] + atomicAdd(&fill[seg], 1u);
             row_idx[pos] = (int32_t)r;
             cval[pos] = val[k];
         }
+    }
+}
+
+// flat exclusive scan over [K][segs] (+ total) -> block bases and int32 block-local offsets
+__global__ void flat_to_off(const int64_t *__restrict__ flat, int K, int64_t segs, int32_t *__restrict__ off,
+                            int64_t *__restrict__ base) {
+    const int64_t total = (int64_t)K * (segs + 1);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i / (segs + 1), s = i - b * (segs + 1);
+        const int64_t b0 = flat[b * segs];
+        off[i] = (int32_t)(flat[b * segs + s] - b0);  // s == segs: the next block's first entry (or the total)
+        if (s == 0) base[b] = b0;
+        if (i == 0) base[K] = flat[(int64_t)K * segs];
+    }
 }
 
 // thread per column: insertion sort of the column segment by row index (CSR has unique columns
@@ -411,13 +352,16 @@ __global__ void blk_scatter(const int64_t *__restrict__ ptr, const int32_t *__re
 // host-input validation helper on the device: count entries with a column outside [0, n) or a
 // non-increasing column inside a row (CSR contract: sorted, unique columns)
 __global__ void csr_check(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col, int64_t rows,
-                          int64_t n, unsigned long long *__restrict__ bad) {
+                          int64_t n, int64_t nnz, unsigned long long *__restrict__ bad) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     unsigned long long nb = 0;
     for (int64_t r = i; r < rows; r += stride) {
         const int64_t k0 = row_ptr[r], k1 = row_ptr[r + 1];
-        if (k1 < k0) ++nb;
+        if (k1 < k0 || k0 < 0 || k1 > nnz) {  // decreasing or out of [0, nnz]: never index col with it
+            ++nb;
+            continue;
+        }
         for (int64_t k = k0; k < k1; ++k) {
             const int32_t c = col[k];
             if (c < 0 || c >= n || (k > k0 && c <= col[k - 1])) ++nb;

@@ -78,14 +78,6 @@ GvFn pick_gv(int T, int nv, int split = 1) {
     }
 }
 
-using SpFn = void (*)(const SpParams);
-template <bool EX>
-SpFn pick_csr(int L) {
-    return L == 8 ? csr_spmv<EX, 8> : L == 16 ? csr_spmv<EX, 16> : csr_spmv<EX, 32>;
-}
-inline SpFn pick_csc(int L) { return L == 8 ? csc_spmvT<8> : L == 16 ? csc_spmvT<16> : csc_spmvT<32>; }
-// lanes per segment from the mean segment length (entries per row / column per index block)
-inline int pick_lanes(double mean_len) { return mean_len >= 24.0 ? 32 : mean_len >= 12.0 ? 16 : 8; }
 
 using GbFn = void (*)(const GbParams);
 template <int T>
@@ -167,9 +159,12 @@ struct tsvd_s {
     bool have_V0 = false;
     int64_t v0_version = 1, v0_uploaded = 0;
     // out-of-memory degree 1 (host input): resident prefix [0, m_res) + streamed batches
-    // wide input (m < n): the handle runs the tall problem on A^T (a transposed device copy);
-    // U and V swap roles at the boundary
-    bool wide = false;
+    // wide input (m < n): the handle runs the tall problem on A^T; U and V swap roles at the
+    // boundary.  The user's buffer is A^T row-major in place when it is column-major (the CSVD column
+    // partition across ranks: a rank's column slab of A is a row slab of A^T); a row-major wide A
+    // (or a column-major tall one) is transposed once into a device copy (tcopy, single GPU)
+    bool wide = false, tcopy = false;
+    tsvd_layout layout = TSVD_ROW_MAJOR;
     int64_t m_user = 0, n_user = 0;
     float *At = nullptr;
     int placement = 0, qdepth = 3;
@@ -182,12 +177,17 @@ struct tsvd_s {
     cudaStream_t copy_stream = nullptr;
     int64_t streamed_bytes = 0, streamed_batches = 0;
     double stream_pass_ms = 0.0;
-    // sparse CSR slab + its CSC (built once on the device)
+    // sparse CSR slab: the input arrays (borrowed device arrays, or an owned copy of host
+    // arrays, freed once the blocked views replace them) and the two blocked views built once on
+    // the device (N4/N4b): spc = the CSR by column block (N2), spr = the CSC by row block (N3)
     bool sparse = false, csr_owned = false;
     int64_t nnz_g = 0;
-    int64_t *row_ptr_d = nullptr, *col_ptr_d = nullptr;
-    int32_t *col_d = nullptr, *row_idx_d = nullptr;
-    float *val_d = nullptr, *cval_d = nullptr;
+    int64_t *row_ptr_d = nullptr;
+    int32_t *col_d = nullptr;
+    float *val_d = nullptr;
+    SpView spc{}, spr{};
+    std::vector<void *> sp_mem;  // device arrays owned by the blocked views
+    int64_t sp_bytes = 0;        // their size (report)
     double csc_build_ms = 0.0;
     // in-kernel column-slice reduction of the N1 partials (cooperative launch), option 13
     int fused_opt = 0;
@@ -210,14 +210,13 @@ struct tsvd_s {
     double *part = nullptr, *u64 = nullptr, *sq_part = nullptr, *sig2 = nullptr;
     float *y32 = nullptr, *t32 = nullptr;  // sparse: fp32 copies of y_cur and t for the gathers
     // sparse index blocking (L2-sized blocks of the gathered vectors): kc column blocks for N2,
-    // kr row blocks for N3; blocked copies of the CSR / CSC when > 1
+    // kr row blocks for N3
     int sp_kc = 1, sp_kr = 1;
-    int sp_lc = 32, sp_lr = 32;  // lanes per row (N2) / per column (N3)
     int64_t sp_block_opt = 0;  // TSVD_OPT_SPARSE_BLOCK: block width in elements (0 = auto)
-    int64_t *bcsr_ptr = nullptr, *bcsc_ptr = nullptr;
-    int32_t *bcsr_idx = nullptr, *bcsc_idx = nullptr;
-    float *bcsr_val = nullptr, *bcsc_val = nullptr;
+    int sp_chunks = 4;         // world > 1: N3's last block in column chunks, each all-reduced at once
     double *acc_r = nullptr, *acc_c = nullptr;
+    cudaStream_t sp_comm_stream = nullptr;
+    std::vector<cudaEvent_t> sp_ev;
     LoopState *st = nullptr;
     CompStat *stats = nullptr;
     LoopState *st_host = nullptr;      // pinned
@@ -345,11 +344,8 @@ static tsvd_status set_fin_attrs(tsvd_t h) {
         CK(max_carveout(ext_finish<SRC_PARTS>));
         CK(max_carveout(ext_finish<SRC_YW>));
         CK(max_carveout(ext_finish<SRC_PEER>));
-        for (int L : {8, 16, 32}) {
-            CK(max_carveout(pick_csr<false>(L)));
-            CK(max_carveout(pick_csr<true>(L)));
-            CK(max_carveout(pick_csc(L)));
-        }
+        // (the sparse kernels keep the driver's L1 / shared split: a thread's entry loads of a batch
+        // hit the L1 lines its warp's neighbours brought in)
     }
     return TSVD_OK;
 }
@@ -357,16 +353,15 @@ static tsvd_status set_fin_attrs(tsvd_t h) {
 // ------------------------------------------------------------------------------------ planning
 static tsvd_status plan(tsvd_t h) {
     const int64_t n = h->n;
-    if (h->sparse) {  // N2/N3: persistent grid of 256-thread blocks, L lanes per row / column
-        for (int L : {8, 16, 32}) {
-            const int dyn = kSpWarps * (32 / L) * std::max(h->k, 1) * (int)sizeof(double);
-            if (dyn > 200 * 1024) {
-                if (L == h->sp_lc) return h->fail(TSVD_ERR_UNSUPPORTED, "sparse path: k too large for the w accumulators");
-                continue;
-            }
-            CK(cudaFuncSetAttribute(pick_csr<false>(L), cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
-        }
-        h->grid = h->sms * 8;
+    if (h->sparse) {  // N2/N3: one thread per segment, a grid of resident 256-thread blocks
+        // l <= k deflation columns (tsvd_gram_apply may run with l = k injected factors)
+        if (h->k > kSpMaxL)
+            return h->fail(TSVD_ERR_UNSUPPORTED, "sparse path: k = %d > %d (per-thread w partials)", h->k, kSpMaxL);
+        const int dyn = (int)((int64_t)std::max(h->k, 1) * (kSpThreads + 1) * sizeof(double));
+        CK(cudaFuncSetAttribute(sp_pass<MODE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sp_pass<MODE_Y>, kSpThreads, 0));
+        h->grid = h->sms * std::max(1, occ);
         h->parts = h->grid;
         h->T = kSpThreads;
         return set_fin_attrs(h);
@@ -892,16 +887,11 @@ static GvParams gv_params(tsvd_t h, int l, bool extract) {
 // same per-CTA partials, so the H2D of batch b+1.. overlaps the kernel on batch b.
 static SpParams sp_params(tsvd_t h, int l) {
     SpParams p{};
-    const bool bc = h->sp_kc > 1, br = h->sp_kr > 1;
     p.phase = 0;
     p.nphase = 1;
-    p.row_ptr = bc ? h->bcsr_ptr : h->row_ptr_d;
-    p.col = bc ? h->bcsr_idx : h->col_d;
-    p.val = bc ? h->bcsr_val : h->val_d;
+    p.csr = h->spc;
+    p.csc = h->spr;
     p.rows = h->m_g;
-    p.col_ptr = br ? h->bcsc_ptr : h->col_ptr_d;
-    p.row_idx = br ? h->bcsc_idx : h->row_idx_d;
-    p.cval = br ? h->bcsc_val : h->cval_d;
     p.n = h->n;
     p.U = h->U32;
     p.ldu = h->kpad;
@@ -922,25 +912,51 @@ static SpParams sp_params(tsvd_t h, int l) {
     return p;
 }
 
-// Sparse pass: N2 (rows) then N3 (columns) for an iteration; N2 alone for the extraction.
+// the sparse pass overlaps its cross-rank sum with N3 (column chunks of the last index block)
+static bool sp_overlap(tsvd_t h) { return h->sparse && h->world > 1 && h->coll == COLL_NCCL && h->sp_chunks > 1; }
+
+// Sparse pass: N2 (rows, one launch per column block) then N3 (columns, one launch per row block);
+// N2 alone for the extraction.  world > 1: N3's last block runs in column chunks and each chunk's
+// [y] (the last one with [w]) is all-reduced on a side stream while the next chunk computes.
 static tsvd_status launch_sparse(tsvd_t h, cudaStream_t s, int l, bool extract) {
-    const SpParams p = sp_params(h, l);
-    SpParams q = p;  // one launch per index block (phase), partial sums carried in acc
+    SpParams q = sp_params(h, l);  // one launch per index block (phase), partial sums carried in acc
     q.nphase = h->sp_kc;
     q.acc = h->acc_r;
+    q.seg0 = 0;
+    q.seg1 = h->m_g;
+    const size_t dyn = (size_t)std::max(l, 0) * (kSpThreads + 1) * sizeof(double);
     for (int b = 0; b < h->sp_kc; ++b) {
         q.phase = b;
-        if (extract) CK(launch_k(h, pick_csr<true>(h->sp_lc), h->grid, kSpThreads, 0, s, 1, q));
-        else
-            CK(launch_k(h, pick_csr<false>(h->sp_lc), h->grid, kSpThreads,
-                        (size_t)kSpWarps * (32 / h->sp_lc) * std::max(l, 1) * sizeof(double), s, 1, q));
+        if (extract) CK(launch_k(h, sp_pass<MODE_U>, h->grid, kSpThreads, 0, s, 1, q));
+        else CK(launch_k(h, sp_pass<MODE_T>, h->grid, kSpThreads, dyn, s, 1, q));
     }
     if (!extract) {
         q.nphase = h->sp_kr;
         q.acc = h->acc_c;
-        for (int b = 0; b < h->sp_kr; ++b) {
+        q.seg0 = 0;
+        q.seg1 = h->n;
+        for (int b = 0; b + 1 < h->sp_kr; ++b) {
             q.phase = b;
-            CK(launch_k(h, pick_csc(h->sp_lr), h->grid, kSpThreads, 0, s, 1, q));
+            CK(launch_k(h, sp_pass<MODE_Y>, h->grid, kSpThreads, 0, s, 1, q));
+        }
+        q.phase = h->sp_kr - 1;
+        if (!sp_overlap(h)) {
+            CK(launch_k(h, sp_pass<MODE_Y>, h->grid, kSpThreads, 0, s, 1, q));
+        } else {
+            const int C = h->sp_chunks;
+            for (int c = 0; c < C; ++c) {
+                const int64_t c0 = h->n * c / C / 32 * 32, c1 = c + 1 == C ? h->n : h->n * (c + 1) / C / 32 * 32;
+                q.seg0 = c0;
+                q.seg1 = c1;
+                CK(launch_k(h, sp_pass<MODE_Y>, h->grid, kSpThreads, 0, s, 1, q));
+                CK(cudaEventRecord(h->sp_ev[c], s));
+                CK(cudaStreamWaitEvent(h->sp_comm_stream, h->sp_ev[c], 0));
+                const int64_t e1 = c + 1 == C ? h->wofs + h->kpad : c1;  // the last chunk carries w
+                NK(ncclAllReduce(h->yw + c0, h->yw + c0, (size_t)(e1 - c0), ncclDouble, ncclSum, h->comm,
+                                 h->sp_comm_stream));
+            }
+            CK(cudaEventRecord(h->sp_ev[C], h->sp_comm_stream));
+            CK(cudaStreamWaitEvent(s, h->sp_ev[C], 0));
         }
     }
     CK(cudaGetLastError());
@@ -1065,7 +1081,8 @@ static PubParams pub_params(tsvd_t h, int mode, int l) {
 // The cross-rank part of an iteration before fin_iter: nothing / publish / local sum + NCCL.
 static tsvd_status launch_exchange(tsvd_t h, cudaStream_t s, int l) {
     if (h->sparse) {  // N3 already wrote [y_g | w_g]; the length-n sum is bandwidth-bound: NCCL
-        if (h->world > 1) NK(ncclAllReduce(h->yw, h->yw, (size_t)(h->wofs + h->kpad), ncclDouble, ncclSum, h->comm, s));
+        if (h->world > 1 && !sp_overlap(h))
+            NK(ncclAllReduce(h->yw, h->yw, (size_t)(h->wofs + h->kpad), ncclDouble, ncclSum, h->comm, s));
         return TSVD_OK;
     }
     if (fused_reduce(h)) {  // N1 already summed its partials into yw / the symmetric slot
@@ -1738,9 +1755,13 @@ tsvd_status tsvd_create(tsvd_t *out, int64_t m, int64_t n, int32_t k, double eps
         g_err = "bad arguments: need m,n >= 1, k in [1, min(m,n)] or -1, 0 < eps < 1";
         return TSVD_ERR_ARG;
     }
-    if (dtype != TSVD_F32 || layout != TSVD_ROW_MAJOR) {
-        g_err = "only fp32 row-major in this version";
+    if (dtype != TSVD_F32) {
+        g_err = "only fp32 in this version";
         return TSVD_ERR_UNSUPPORTED;
+    }
+    if (layout != TSVD_ROW_MAJOR && layout != TSVD_COL_MAJOR) {
+        g_err = "layout must be TSVD_ROW_MAJOR or TSVD_COL_MAJOR";
+        return TSVD_ERR_ARG;
     }
     const int64_t kk = k == -1 ? mn : k;
     if (kk > kMaxK) {
@@ -1751,6 +1772,10 @@ tsvd_status tsvd_create(tsvd_t *out, int64_t m, int64_t n, int32_t k, double eps
     h->m_user = m;
     h->n_user = n;
     h->wide = m < n;
+    h->layout = layout;
+    // the internal problem is always tall (rows >= columns, V-first); it is stored row-major in
+    // place when the user's major dimension is its row dimension, else through a transposed copy
+    h->tcopy = (layout == TSVD_ROW_MAJOR) == h->wide;
     if (h->wide) std::swap(m, n);  // internal tall problem: A^T, n x m
     h->m = m;
     h->n = n;
@@ -1789,8 +1814,9 @@ tsvd_status tsvd_set_comm(tsvd_t h, int32_t rank, int32_t world, const void *uid
     if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world || (world > 1 && !uid))
         return h->fail(TSVD_ERR_ARG, "bad rank/world (world <= %d)", kMaxRanks);
     if (h->allocated || h->have_A) return h->fail(TSVD_ERR_STATE, "set_comm must precede set_dense");
-    if (h->wide && world > 1)
-        return h->fail(TSVD_ERR_UNSUPPORTED, "wide inputs (m < n) run on one GPU in this version (NEXT#2)");
+    if (h->tcopy && world > 1)
+        return h->fail(TSVD_ERR_UNSUPPORTED, "row-major wide (or column-major tall) inputs run on one GPU; pass a "
+                                             "wide matrix column-major to partition its columns (CSVD, P:323)");
     if (device != h->dev) {
         CK(cudaSetDevice(device));
         if (h->stream) cudaStreamDestroy(h->stream);
@@ -1935,16 +1961,20 @@ __global__ void transpose_f32(const float *__restrict__ in, int64_t rows, int64_
 
 tsvd_status tsvd_set_dense(tsvd_t h, const float *A, int64_t ld, int64_t row_begin, int64_t row_end, tsvd_mem mem) {
     if (!h) return TSVD_ERR_ARG;
-    if (!h->wide) return set_dense_impl(h, A, ld, row_begin, row_end, mem);
-    // wide: A is m_user x n_user (m < n); the tall solver runs on A^T (NEXT#2)
-    if (!A || ld < h->n_user) return h->fail(TSVD_ERR_ARG, "A == NULL or ld < n");
-    if (row_begin != 0 || row_end != h->m_user)
-        return h->fail(TSVD_ERR_SHAPE, "wide inputs are passed whole (rows [0, m))");
+    // in place: the user's buffer IS the internal tall matrix, row-major (row-major tall A, or
+    // column-major wide A = row-major A^T whose rows are A's columns; ranges count the major dimension)
+    if (!h->tcopy) return set_dense_impl(h, A, ld, row_begin, row_end, mem);
+    // transposed copy: the user's buffer is mu x nu row-major (mu < nu: row-major wide A; mu > nu:
+    // column-major tall A viewed as its row-major transpose) and the tall solver runs on its transpose
+    const int64_t mu = h->wide ? h->m_user : h->n_user, nu = h->wide ? h->n_user : h->m_user;
+    if (!A || ld < nu) return h->fail(TSVD_ERR_ARG, "A == NULL or ld < the major dimension");
+    if (row_begin != 0 || row_end != mu)
+        return h->fail(TSVD_ERR_SHAPE, "this layout is passed whole (range [0, %lld))", (long long)mu);
     if (mem != TSVD_MEM_DEVICE && mem != TSVD_MEM_HOST_PINNED && mem != TSVD_MEM_HOST_PAGEABLE)
         return h->fail(TSVD_ERR_ARG, "bad mem kind");
     if (h->sparse) return h->fail(TSVD_ERR_STATE, "the input kind cannot change");
     CK(cudaSetDevice(h->dev));
-    const int64_t mu = h->m_user, nu = h->n_user, ldt = round_up(mu, 4);
+    const int64_t ldt = round_up(mu, 4);
     if (!h->At) {
         cudaError_t e = cudaMalloc((void **)&h->At, (size_t)nu * ldt * sizeof(float));
         if (e == cudaErrorMemoryAllocation) return h->fail(TSVD_ERR_NOMEM, "no room for the transposed copy of A");
@@ -2017,30 +2047,147 @@ static tsvd_status set_dense_impl(tsvd_t h, const float *A, int64_t ld, int64_t 
     return TSVD_OK;
 }
 
-// Blocked copy of a compressed matrix (segments with sorted indices) split into K index blocks of
-// width bw: counts per [block][segment], one exclusive scan, scatter (N4b).
-static tsvd_status build_blocked(tsvd_t h, const int64_t *ptr, const int32_t *idx, const float *val, int64_t segs,
-                                 int64_t nnz, int K, int64_t bw, int64_t **bptr, int32_t **bidx, float **bval) {
-    const int64_t len = (int64_t)K * segs;
+// device array owned by the sparse views (freed by free_sparse)
+static cudaError_t sp_alloc(tsvd_t h, void **p, size_t bytes) {
+    cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 16));
+    if (e == cudaSuccess) {
+        h->sp_mem.push_back(*p);
+        h->sp_bytes += (int64_t)bytes;
+    }
+    return e;
+}
+
+// exclusive scan of K x segs counts into flat[0 .. len] (flat[len] = total), int64
+static tsvd_status sp_scan(tsvd_t h, const unsigned *cnt, int64_t len, int64_t *flat) {
     const int64_t ntiles = (len + kScanTile - 1) / kScanTile;
-    unsigned *cnt = nullptr;
     int64_t *bsum = nullptr;
-    CK(cudaMalloc((void **)bptr, (size_t)(len + 1) * sizeof(int64_t)));
-    CK(cudaMalloc((void **)bidx, (size_t)nnz * sizeof(int32_t)));
-    CK(cudaMalloc((void **)bval, (size_t)nnz * sizeof(float)));
+    CK(cudaMalloc((void **)&bsum, (size_t)std::max<int64_t>(ntiles, 1) * sizeof(int64_t)));
+    if (len > 0) {
+        scan_tiles<<<(int)ntiles, kScanThreads, 0, h->stream>>>(cnt, len, flat, bsum);
+        scan_totals<<<1, kScanThreads, 0, h->stream>>>(bsum, ntiles, flat + len);
+        scan_add<<<h->sms * 8, 256, 0, h->stream>>>(flat, len, bsum);
+    } else {
+        CK(cudaMemsetAsync(flat, 0, sizeof(int64_t), h->stream));
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(bsum);
+    return TSVD_OK;
+}
+
+// flat [K][segs] offsets -> SpView (int32 block-local offsets + int64 bases); TSVD_ERR_UNSUPPORTED if
+// a block holds 2^31 or more entries (the caller retries with more blocks)
+static tsvd_status sp_view(tsvd_t h, const int64_t *flat, int K, int64_t segs, SpView *v) {
+    std::vector<int64_t> starts(K + 1);
+    for (int b = 0; b <= K; ++b)
+        CK(cudaMemcpy(&starts[b], flat + (int64_t)b * segs, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    for (int b = 0; b < K; ++b)
+        if (starts[b + 1] - starts[b] > (int64_t)INT32_MAX) return TSVD_ERR_UNSUPPORTED;
+    int32_t *off = nullptr;
+    int64_t *base = nullptr;
+    cudaError_t e = sp_alloc(h, (void **)&off, (size_t)K * (segs + 1) * sizeof(int32_t));
+    if (!e) e = sp_alloc(h, (void **)&base, (size_t)(K + 1) * sizeof(int64_t));
+    if (e == cudaErrorMemoryAllocation) return h->fail(TSVD_ERR_NOMEM, "sparse block offsets allocation failed");
+    CK(e);
+    flat_to_off<<<h->sms * 8, 256, 0, h->stream>>>(flat, K, segs, off, base);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
+    v->off = off;
+    v->base = base;
+    v->segs = segs;
+    return TSVD_OK;
+}
+
+// N4b (CSR by column block): K = 1 views the CSR itself (int32 offsets of row_ptr, entries in place);
+// K > 1 copies each row's entries of block b (columns [b bw, (b + 1) bw)) to block b's region
+static tsvd_status build_csr_view(tsvd_t h, int K, int64_t bw) {
+    const int64_t mg = h->m_g, nnz = h->nnz_g;
+    if (K == 1) {
+        TRY(sp_view(h, h->row_ptr_d, 1, mg, &h->spc));  // row_ptr is the flat scan of one block
+        h->spc.idx = h->col_d;
+        h->spc.val = h->val_d;
+        return TSVD_OK;
+    }
+    const int64_t len = (int64_t)K * mg;
+    unsigned *cnt = nullptr;
+    int64_t *flat = nullptr;
     CK(cudaMalloc((void **)&cnt, (size_t)len * sizeof(unsigned)));
-    CK(cudaMalloc((void **)&bsum, (size_t)ntiles * sizeof(int64_t)));
-    const int blocks = h->sms * 8;
-    blk_count<<<blocks, 256, 0, h->stream>>>(ptr, idx, segs, K, bw, cnt);
-    scan_tiles<<<(int)ntiles, kScanThreads, 0, h->stream>>>(cnt, len, *bptr, bsum);
-    scan_totals<<<1, kScanThreads, 0, h->stream>>>(bsum, ntiles, *bptr + len);
-    scan_add<<<blocks, 256, 0, h->stream>>>(*bptr, len, bsum);
-    blk_scatter<<<blocks, 256, 0, h->stream>>>(ptr, idx, val, segs, K, *bptr, *bidx, *bval);
+    CK(cudaMalloc((void **)&flat, (size_t)(len + 1) * sizeof(int64_t)));
+    blk_count<<<h->sms * 8, 256, 0, h->stream>>>(h->row_ptr_d, h->col_d, mg, K, bw, cnt);
+    tsvd_status st = sp_scan(h, cnt, len, flat);
+    cudaFree(cnt);
+    if (st == TSVD_OK) st = sp_view(h, flat, K, mg, &h->spc);
+    if (st != TSVD_OK) {
+        cudaFree(flat);
+        return st;
+    }
+    int32_t *idx = nullptr;
+    float *val = nullptr;
+    cudaError_t e = sp_alloc(h, (void **)&idx, (size_t)nnz * sizeof(int32_t));
+    if (!e) e = sp_alloc(h, (void **)&val, (size_t)nnz * sizeof(float));
+    if (e) {
+        cudaFree(flat);
+        cudaGetLastError();
+        return h->fail(TSVD_ERR_NOMEM, "no room for the column-blocked CSR");
+    }
+    blk_scatter<<<h->sms * 8, 256, 0, h->stream>>>(h->row_ptr_d, h->col_d, h->val_d, mg, K, flat, idx, val);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(flat);
+    h->spc.idx = idx;
+    h->spc.val = val;
+    return TSVD_OK;
+}
+
+// N4 (CSC by row block, straight from the CSR): counts per [row block][column], scan, scatter, then
+// each (block, column) segment sorted by row, so the layout — and every result — is deterministic
+static tsvd_status build_csc_view(tsvd_t h, int K, int64_t bw) {
+    const int64_t mg = h->m_g, n = h->n, nnz = h->nnz_g;
+    const int64_t len = (int64_t)K * n;
+    unsigned *cnt = nullptr;
+    int64_t *flat = nullptr;
+    CK(cudaMalloc((void **)&cnt, (size_t)len * sizeof(unsigned)));
+    CK(cudaMalloc((void **)&flat, (size_t)(len + 1) * sizeof(int64_t)));
+    CK(cudaMemsetAsync(cnt, 0, (size_t)len * sizeof(unsigned), h->stream));
+    if (nnz) csc_blk_count<<<h->sms * 8, 256, 0, h->stream>>>(h->row_ptr_d, h->col_d, mg, n, bw, cnt);
+    tsvd_status st = sp_scan(h, cnt, len, flat);
+    if (st == TSVD_OK) st = sp_view(h, flat, K, n, &h->spr);
+    if (st != TSVD_OK) {
+        cudaFree(cnt);
+        cudaFree(flat);
+        return st;
+    }
+    int32_t *idx = nullptr;
+    float *val = nullptr;
+    cudaError_t e = sp_alloc(h, (void **)&idx, (size_t)nnz * sizeof(int32_t));
+    if (!e) e = sp_alloc(h, (void **)&val, (size_t)nnz * sizeof(float));
+    if (e) {
+        cudaFree(cnt);
+        cudaFree(flat);
+        cudaGetLastError();
+        return h->fail(TSVD_ERR_NOMEM, "no room for the row-blocked CSC");
+    }
+    CK(cudaMemsetAsync(cnt, 0, (size_t)len * sizeof(unsigned), h->stream));
+    if (nnz) {
+        csc_blk_scatter<<<h->sms * 8, 256, 0, h->stream>>>(h->row_ptr_d, h->col_d, h->val_d, mg, n, bw, flat, cnt,
+                                                           idx, val);
+        csc_sort<<<h->sms * 8, 256, 0, h->stream>>>(flat, len, idx, val);
+    }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(h->stream));
     cudaFree(cnt);
-    cudaFree(bsum);
+    cudaFree(flat);
+    h->spr.idx = idx;
+    h->spr.val = val;
     return TSVD_OK;
+}
+
+static void free_sparse_views(tsvd_t h) {
+    for (void *q : h->sp_mem) cudaFree(q);
+    h->sp_mem.clear();
+    h->sp_bytes = 0;
+    h->spc = SpView{};
+    h->spr = SpView{};
 }
 
 static void free_sparse(tsvd_t h) {
@@ -2049,21 +2196,14 @@ static void free_sparse(tsvd_t h) {
         cudaFree(h->col_d);
         cudaFree(h->val_d);
     }
-    cudaFree(h->col_ptr_d);
-    cudaFree(h->row_idx_d);
-    cudaFree(h->cval_d);
-    for (void *q : {(void *)h->bcsr_ptr, (void *)h->bcsc_ptr, (void *)h->bcsr_idx, (void *)h->bcsc_idx,
-                    (void *)h->bcsr_val, (void *)h->bcsc_val, (void *)h->acc_r, (void *)h->acc_c})
+    free_sparse_views(h);
+    for (void *q : {(void *)h->acc_r, (void *)h->acc_c})
         if (q) cudaFree(q);
-    h->bcsr_ptr = h->bcsc_ptr = nullptr;
-    h->bcsr_idx = h->bcsc_idx = nullptr;
-    h->bcsr_val = h->bcsc_val = nullptr;
     h->acc_r = h->acc_c = nullptr;
     h->sp_kc = h->sp_kr = 1;
-    h->sp_lc = h->sp_lr = 32;
-    h->row_ptr_d = h->col_ptr_d = nullptr;
-    h->col_d = h->row_idx_d = nullptr;
-    h->val_d = h->cval_d = nullptr;
+    h->row_ptr_d = nullptr;
+    h->col_d = nullptr;
+    h->val_d = nullptr;
     h->csr_owned = false;
 }
 
@@ -2071,6 +2211,7 @@ tsvd_status tsvd_set_csr(tsvd_t h, const int64_t *row_ptr, const int32_t *col_id
                          int64_t row_begin, int64_t row_end, tsvd_mem mem) {
     if (!h) return TSVD_ERR_ARG;
     if (!row_ptr || nnz < 0 || (nnz > 0 && (!col_idx || !val))) return h->fail(TSVD_ERR_ARG, "NULL CSR array");
+    if (h->wide) return h->fail(TSVD_ERR_UNSUPPORTED, "sparse inputs must have m >= n (V-first branch) in this version");
     if (row_begin < 0 || row_end > h->m || row_end <= row_begin)
         return h->fail(TSVD_ERR_SHAPE, "row range [%lld, %lld) outside [0, %lld)", (long long)row_begin,
                        (long long)row_end, (long long)h->m);
@@ -2082,8 +2223,17 @@ tsvd_status tsvd_set_csr(tsvd_t h, const int64_t *row_ptr, const int32_t *col_id
         return h->fail(TSVD_ERR_STATE, "the input kind / slab size cannot change after the first run");
     CK(cudaSetDevice(h->dev));
     const int64_t mg = row_end - row_begin, n = h->n;
-    if (mem != TSVD_MEM_DEVICE && (row_ptr[0] != 0 || row_ptr[mg] != nnz))
-        return h->fail(TSVD_ERR_ARG, "row_ptr[0] must be 0 and row_ptr[rows] == nnz");
+    int64_t ends[2] = {0, nnz};
+    if (mem == TSVD_MEM_DEVICE) {  // two small reads: the CSC build trusts [row_ptr[0], row_ptr[rows])
+        CK(cudaMemcpy(&ends[0], row_ptr, sizeof(int64_t), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&ends[1], row_ptr + mg, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    } else {
+        ends[0] = row_ptr[0];
+        ends[1] = row_ptr[mg];
+    }
+    if (ends[0] != 0 || ends[1] != nnz)
+        return h->fail(TSVD_ERR_ARG, "row_ptr[0] must be 0 and row_ptr[rows] == nnz (got %lld, %lld; nnz %lld)",
+                       (long long)ends[0], (long long)ends[1], (long long)nnz);
     free_sparse(h);
     h->sparse = true;
     h->row_begin = row_begin;
@@ -2115,7 +2265,7 @@ tsvd_status tsvd_set_csr(tsvd_t h, const int64_t *row_ptr, const int32_t *col_id
     unsigned long long *bad = nullptr, bad_h = 0;
     CK(cudaMalloc((void **)&bad, sizeof(unsigned long long)));
     CK(cudaMemsetAsync(bad, 0, sizeof(unsigned long long), h->stream));
-    csr_check<<<h->sms * 8, 256, 0, h->stream>>>(h->row_ptr_d, h->col_d, mg, n, bad);
+    csr_check<<<h->sms * 8, 256, 0, h->stream>>>(h->row_ptr_d, h->col_d, mg, n, nnz, bad);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(&bad_h, bad, sizeof(bad_h), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
@@ -2123,59 +2273,58 @@ tsvd_status tsvd_set_csr(tsvd_t h, const int64_t *row_ptr, const int32_t *col_id
     if (bad_h) {
         free_sparse(h);
         h->have_A = false;
-        return h->fail(TSVD_ERR_ARG, "CSR has %llu entries with a column out of range or not strictly increasing",
+        return h->fail(TSVD_ERR_ARG, "CSR has %llu bad rows / entries (row_ptr decreasing or outside [0, nnz], column out of range or not strictly increasing)",
                        bad_h);
     }
-    // N4: CSC of the slab (histogram, scan, scatter, per-column sort)
-    unsigned *cnt = nullptr;
-    int64_t *bsum = nullptr;
-    const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
-    CK(cudaMalloc((void **)&h->col_ptr_d, (size_t)(n + 1) * sizeof(int64_t)));
-    CK(cudaMalloc((void **)&h->row_idx_d, std::max<size_t>((size_t)nnz * sizeof(int32_t), 16)));
-    CK(cudaMalloc((void **)&h->cval_d, std::max<size_t>((size_t)nnz * sizeof(float), 16)));
-    CK(cudaMalloc((void **)&cnt, (size_t)n * sizeof(unsigned)));
-    CK(cudaMalloc((void **)&bsum, (size_t)ntiles * sizeof(int64_t)));
-    CK(cudaMemsetAsync(cnt, 0, (size_t)n * sizeof(unsigned), h->stream));
-    const int blocks = h->sms * 8;
-    if (nnz) csc_count<<<blocks, 256, 0, h->stream>>>(h->col_d, nnz, cnt);
-    scan_tiles<<<(int)ntiles, kScanThreads, 0, h->stream>>>(cnt, n, h->col_ptr_d, bsum);
-    scan_totals<<<1, kScanThreads, 0, h->stream>>>(bsum, ntiles, h->col_ptr_d + n);
-    scan_add<<<blocks, 256, 0, h->stream>>>(h->col_ptr_d, n, bsum);
-    CK(cudaGetLastError());
-    CK(cudaMemsetAsync(cnt, 0, (size_t)n * sizeof(unsigned), h->stream));
-    if (nnz) {
-        csc_scatter<<<blocks, 256, 0, h->stream>>>(h->row_ptr_d, h->col_d, h->val_d, mg, h->col_ptr_d, cnt,
-                                                   h->row_idx_d, h->cval_d);
-        csc_sort<<<blocks, 256, 0, h->stream>>>(h->col_ptr_d, n, h->row_idx_d, h->cval_d);
-    }
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(h->stream));
-    cudaFree(cnt);
-    cudaFree(bsum);
-    // N4b: index blocking, so that each launch's gathers hit an L2-resident block of the fp32
-    // vector (y32 for N2 by column, t32 for N3 by row)
+    // N4 / N4b: the two blocked views.  Index blocks keep each launch's gathers inside an L2-resident
+    // block of the fp32 gathered vector (y32 for N2 by column, t32 for N3 by row); every block must
+    // hold < 2^31 entries (int32 block-local offsets): the block count doubles until it does.
     const int64_t bw_auto = (int64_t)kSpL2BlockBytes / (int64_t)sizeof(float);
     const int64_t bwc = h->sp_block_opt > 0 ? h->sp_block_opt : bw_auto;
     const int64_t bwr = h->sp_block_opt > 0 ? h->sp_block_opt : bw_auto;
-    const int kc = (int)std::min<int64_t>(64, (n + bwc - 1) / bwc), kr = (int)std::min<int64_t>(64, (mg + bwr - 1) / bwr);
-    if (kc > 1 && nnz) {
-        TRY(build_blocked(h, h->row_ptr_d, h->col_d, h->val_d, mg, nnz, kc, (n + kc - 1) / kc, &h->bcsr_ptr,
-                          &h->bcsr_idx, &h->bcsr_val));
-        CK(cudaMalloc((void **)&h->acc_r, (size_t)mg * sizeof(double)));
-        h->sp_kc = kc;
+    int kc = (int)std::min<int64_t>(64, (n + bwc - 1) / bwc), kr = (int)std::min<int64_t>(64, (mg + bwr - 1) / bwr);
+    tsvd_status bs = TSVD_OK;
+    for (;; kr *= 2) {  // the CSC first: it is built from the CSR, which the CSR view may replace
+        bs = build_csc_view(h, kr, (mg + kr - 1) / kr);
+        if (bs != TSVD_ERR_UNSUPPORTED || kr >= mg) break;
+        free_sparse_views(h);
     }
-    if (kr > 1 && nnz) {
-        TRY(build_blocked(h, h->col_ptr_d, h->row_idx_d, h->cval_d, n, nnz, kr, (mg + kr - 1) / kr, &h->bcsc_ptr,
-                          &h->bcsc_idx, &h->bcsc_val));
-        CK(cudaMalloc((void **)&h->acc_c, (size_t)n * sizeof(double)));
-        h->sp_kr = kr;
-        cudaFree(h->row_idx_d);  // the blocked CSC replaces the plain one (col_ptr kept for the report)
-        cudaFree(h->cval_d);
-        h->row_idx_d = nullptr;
-        h->cval_d = nullptr;
+    if (bs == TSVD_OK)
+        for (;; kc *= 2) {
+            bs = build_csr_view(h, kc, (n + kc - 1) / kc);
+            if (bs != TSVD_ERR_UNSUPPORTED || kc >= n) break;
+        }
+    if (bs != TSVD_OK) {
+        free_sparse(h);
+        h->have_A = false;
+        return bs == TSVD_ERR_UNSUPPORTED ? h->fail(bs, "sparse slab: an index block would exceed 2^31 entries") : bs;
     }
-    h->sp_lc = pick_lanes((double)nnz / std::max<double>(1.0, (double)mg * h->sp_kc));
-    h->sp_lr = pick_lanes((double)nnz / std::max<double>(1.0, (double)n * h->sp_kr));
+    h->sp_kc = kc;
+    h->sp_kr = kr;
+    if (kc > 1) CK(cudaMalloc((void **)&h->acc_r, (size_t)mg * sizeof(double)));
+    if (kr > 1) CK(cudaMalloc((void **)&h->acc_c, (size_t)n * sizeof(double)));
+    // the CSR view holds a blocked copy when kc > 1: an owned input copy is dropped (2 copies of the
+    // entries remain: the blocked CSR and the blocked CSC); borrowed device arrays are no longer read
+    if (kc > 1 && h->csr_owned) {
+        cudaFree(h->row_ptr_d);
+        cudaFree(h->col_d);
+        cudaFree(h->val_d);
+        h->row_ptr_d = nullptr;
+        h->col_d = nullptr;
+        h->val_d = nullptr;
+        h->csr_owned = false;
+    } else if (h->csr_owned) {  // kc == 1: the view reads col / val in place; row_ptr is replaced
+        cudaFree(h->row_ptr_d);
+        h->row_ptr_d = nullptr;
+    }
+    if (h->world > 1 && !h->sp_comm_stream) {
+        CK(cudaStreamCreateWithFlags(&h->sp_comm_stream, cudaStreamNonBlocking));
+        for (int c = 0; c <= h->sp_chunks; ++c) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            h->sp_ev.push_back(e);
+        }
+    }
     h->csc_build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return TSVD_OK;
 }
@@ -2210,6 +2359,9 @@ tsvd_status tsvd_set_factors(tsvd_t h, int32_t l, const float *U, const double *
     }
     h->l_found = l;
     h->k_found = l;
+    // explicit Gram (METHOD = 1): P = A^T U and Q = U^T U were built for the factors this handle
+    // computed; injected factors invalidate them (a METHOD = 1 run then restarts from l = 0 only)
+    if (l > 0) h->pq_l = 0;
     return TSVD_OK;
 }
 
@@ -2408,10 +2560,11 @@ tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
     static const char *colls[] = {"none", "peer-nvlink", "nccl"};
     snprintf(tmp, sizeof tmp,
              "\"m\": %lld, \"n\": %lld, \"k\": %d, \"eps\": %.3g, \"rank\": %d, \"world\": %d, \"rows\": [%lld, %lld], "
-             "\"wide\": %s, \"k_found\": %d, \"total_iters\": %lld, \"run_ms\": %.4f, \"h2d_ms\": %.4f, \"n1_ms\": %.6f, "
+             "\"wide\": %s, \"layout\": \"%s\", \"transposed_copy\": %s, \"k_found\": %d, \"total_iters\": %lld, \"run_ms\": %.4f, \"h2d_ms\": %.4f, \"n1_ms\": %.6f, "
              "\"n1_launches\": %lld, \"kernel_launches\": %lld, \"loop\": \"%s\", \"collective\": \"%s\", ",
              (long long)h->m_user, (long long)h->n_user, h->k, h->eps, h->rank, h->world, (long long)h->row_begin,
-             (long long)h->row_end, h->wide ? "true" : "false", h->k_found, (long long)h->total_iters, h->run_ms, h->h2d_ms,
+             (long long)h->row_end, h->wide ? "true" : "false", h->layout == TSVD_COL_MAJOR ? "col" : "row",
+             h->tcopy ? "true" : "false", h->k_found, (long long)h->total_iters, h->run_ms, h->h2d_ms,
              h->n1_ms,
              (long long)h->n1_launches, (long long)h->launches, h->loop_mode.c_str(), colls[h->coll]);
     s += tmp;
@@ -2441,8 +2594,9 @@ tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
     s += tmp;
     snprintf(tmp, sizeof tmp,
              "\"sparse\": {\"enabled\": %s, \"nnz\": %lld, \"csc_build_ms\": %.3f, \"col_blocks\": %d, \"row_blocks\": %d, "
-             "\"lanes_row\": %d, \"lanes_col\": %d}, ",
-             h->sparse ? "true" : "false", (long long)h->nnz_g, h->csc_build_ms, h->sp_kc, h->sp_kr, h->sp_lc, h->sp_lr);
+             "\"view_bytes\": %lld, \"input_kept\": %s, \"chunks\": %d}, ",
+             h->sparse ? "true" : "false", (long long)h->nnz_g, h->csc_build_ms, h->sp_kc, h->sp_kr,
+             (long long)h->sp_bytes, h->sparse && h->sp_kc == 1 ? "true" : "false", sp_overlap(h) ? h->sp_chunks : 1);
     s += tmp;
     std::string ge = h->graph_error + (h->peer_error.empty() ? "" : " | " + h->peer_error);
     for (char &c : ge)
@@ -2502,6 +2656,11 @@ void tsvd_destroy(tsvd_t h) {
     free_ring(h);
     free_sparse(h);
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+    if (h->sp_comm_stream) {
+        cudaStreamSynchronize(h->sp_comm_stream);
+        cudaStreamDestroy(h->sp_comm_stream);
+    }
+    for (cudaEvent_t e : h->sp_ev) cudaEventDestroy(e);
     if (h->host_registered) cudaHostUnregister((void *)h->A_user);
     for (int r = 0; r < kMaxRanks; ++r) {
         if (h->peer_map[r]) cudaIpcCloseMemHandle(h->peer_map[r]);

@@ -35,7 +35,7 @@ OPT_ROW_ORDER = 18  # 1 (default): serpentine row order (odd iterations backward
 OPT_PERSISTENT = 19  # 1 (default): a component's iterations in one cooperative kernel (single GPU)
 OPT_SPARSE_BLOCK = 20  # sparse: index-block width (elements) for L2-resident gathers; 0 = auto (set before set_csr)
 OPT_METHOD = 21  # 0 (default): implicit Gram-vector path; 1: explicit Gram (B0 = A^T A once, NEXT#1)
-F32, ROW_MAJOR = 0, 0
+F32, ROW_MAJOR, COL_MAJOR = 0, 0, 1
 
 _lib = None
 _vp = ctypes.c_void_p
@@ -185,18 +185,23 @@ def tsvd_destroy(h):
 
 # ---- object wrapper --------------------------------------------------------------------------
 class TSVD:
-    """Power-method truncated SVD of an m x n fp32 matrix (m >= n) on this process's GPU."""
+    """Power-method truncated SVD of an m x n fp32 matrix on this process's GPU.
 
-    def __init__(self, m, n, k, eps, rank=0, world=1, uid=None, device=None):
+    layout: ROW_MAJOR (slabs are row ranges) or COL_MAJOR (slabs are column ranges: a wide matrix
+    stored column-major is column-partitioned across ranks, CSVD P:323)."""
+
+    def __init__(self, m, n, k, eps, rank=0, world=1, uid=None, device=None, layout=ROW_MAJOR):
         self.m, self.n, self.eps = m, n, eps
         self.k = min(m, n) if k == -1 else k
+        self.layout = layout
+        self.wide = m < n
         if device is not None:
             import torch
             torch.cuda.set_device(device)
-        self.h = tsvd_create(m, n, k, eps)
+        self.h = tsvd_create(m, n, k, eps, F32, layout)
         if world > 1 or device is not None:
             tsvd_set_comm(self.h, rank, world, uid, 0 if device is None else device)
-        self.row_begin, self.row_end = 0, m
+        self.row_begin, self.row_end = 0, (m if layout == ROW_MAJOR else n)
         self._keep = []
 
     def set_option(self, key, value):
@@ -206,16 +211,20 @@ class TSVD:
         tsvd_set_init(self.h, V0)
 
     def set_dense(self, A, row_begin=0, row_end=None, mem=None):
-        """A: this rank's row slab — numpy (host) or torch tensor (device/host), fp32, unit column stride."""
-        row_end = self.m if row_end is None else row_end
+        """A: this rank's slab — numpy (host) or torch tensor (device/host), fp32.  ROW_MAJOR: rows
+        [row_begin, row_end) with unit column stride; COL_MAJOR: columns [row_begin, row_end) (an
+        (m, cols) array with unit row stride, e.g. numpy order='F' or torch ``X.t().contiguous().t()``)."""
+        cm = self.layout == COL_MAJOR
+        row_end = (self.n if cm else self.m) if row_end is None else row_end
+        minor, major = (0, 1) if cm else (1, 0)
         if isinstance(A, np.ndarray):
-            assert A.dtype == np.float32 and A.strides[1] == 4
-            ld = A.strides[0] // 4
+            assert A.dtype == np.float32 and A.strides[minor] == 4
+            ld = A.strides[major] // 4
             mem = MEM_HOST_PAGEABLE if mem is None else mem
         else:
             import torch
-            assert A.dtype == torch.float32 and A.stride(1) == 1
-            ld = A.stride(0)
+            assert A.dtype == torch.float32 and A.stride(minor) == 1
+            ld = A.stride(major)
             if mem is None:
                 mem = MEM_DEVICE if A.is_cuda else (MEM_HOST_PINNED if A.is_pinned() else MEM_HOST_PAGEABLE)
         self._keep = [A]
@@ -256,10 +265,13 @@ class TSVD:
         return tsvd_run(self.h)
 
     def result(self):
-        mg = self.row_end - self.row_begin
-        U = np.zeros((mg, self.k), dtype=np.float32)
+        """(U, S, V): U this rank's row slab and V replicated (m >= n); U replicated and V this rank's
+        slab (m < n)."""
+        r0, r1 = self.report()["rows"]  # the library's own slab: rows of the internal tall matrix
+        mg = r1 - r0
+        U = np.zeros((self.m if self.wide else mg, self.k), dtype=np.float32)
         S = np.zeros(self.k, dtype=np.float64)
-        V = np.zeros((self.n, self.k), dtype=np.float32)
+        V = np.zeros((mg if self.wide else self.n, self.k), dtype=np.float32)
         tsvd_get_U_S_V(self.h, U, S, V)
         return U, S, V
 

@@ -29,3 +29,12 @@ def test_reference_arm_other_ranks_exit_quietly():
                         "--steps", "1", "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=ROOT,
                        env=env)
     assert r.returncode == 0 and not [l for l in r.stdout.splitlines() if l.startswith("{")]
+
+
+def test_gpus_must_match_world_size():
+    """Under torchrun WORLD_SIZE must equal --gpus (a mismatch would time the wrong number of GPUs);
+    without torchrun, --gpus N > 1 re-launches bench.py under torch.distributed.run (GPU box only)."""
+    env = dict(os.environ, RANK="0", WORLD_SIZE="2", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--steps", "1", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 2 and "WORLD_SIZE=2" in r.stderr

@@ -24,6 +24,7 @@ if not torch.cuda.is_available():  # pragma: no cover - collected on the GPU box
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_2208_08410_b200 as P  # noqa: E402
+from _parity import assert_pair_close, assert_vec_close  # noqa: E402
 
 M, N, K, EPS, RANK = 65536, 16384, 16, 1e-6, 32
 SIG_TOL = 1e-4
@@ -86,8 +87,7 @@ def test_c2_sampled_u_rows_vs_definition(c2):
     for i in range(K):
         want = oracle.matvec(A_s, V[:, i]) / c2["S"][i]
         got = c2["U"][rows, i].astype(np.float64)
-        err = np.linalg.norm(got - want) / np.linalg.norm(want)
-        assert err <= 1e-5, (i, err)
+        assert_vec_close(got, want, 1e-5, f"u{i} rows")
 
 
 def test_c2_full_parity_vs_oracle(c2):
@@ -97,8 +97,8 @@ def test_c2_full_parity_vs_oracle(c2):
     rel = np.abs(c2["S"][:K] - ref.S[:K]) / ref.S[:K]
     assert rel.max() <= SIG_TOL, rel
     for i in range(K):
-        assert 1 - _cos(c2["V"][:, i], ref.V[:, i]) <= COS_TOL, i
-        assert 1 - _cos(c2["U"][:, i], ref.U[:, i]) <= COS_TOL, i
+        assert_pair_close(c2["V"][:, i], ref.V[:, i], f"v{i}")
+        assert_pair_close(c2["U"][:, i], ref.U[:, i], f"u{i}")
     assert np.all(np.abs(c2["iters"] - np.asarray(ref.iters)) <= 1), (c2["iters"], ref.iters)
 
 
@@ -117,5 +117,4 @@ def test_c2_single_gram_product_with_16_factors(c2):
     t.set_factors(U, S, V)
     got = t.gram_apply(v)
     t.close()
-    err = np.linalg.norm(got - want) / np.linalg.norm(want)
-    assert err <= 1e-5, err
+    assert_vec_close(got, want, 1e-5)

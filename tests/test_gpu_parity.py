@@ -20,9 +20,7 @@ if not torch.cuda.is_available():  # pragma: no cover - collected on the GPU box
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_2208_08410_b200 as P  # noqa: E402
-
-SIG_TOL = 1e-4
-COS_TOL = 1e-4
+from _parity import COS_TOL, SIG_TOL, assert_tsvd_close, assert_vec_close  # noqa: E402
 
 
 def _cos(a, b):
@@ -50,12 +48,9 @@ def _gpu_tsvd(A, k, eps, V0, device=True, **opts):
 
 
 def _assert_parity(A, ref, U, S, V, kf, k):
+    """sigma relative error, |cos| per u and v pair, and each vector elementwise (tests/_parity.py)."""
     assert kf == ref.k_found == k
-    rel = np.abs(S[:k] - ref.S[:k]) / ref.S[:k]
-    assert rel.max() <= SIG_TOL, rel
-    for i in range(k):
-        assert 1 - _cos(V[:, i], ref.V[:, i]) <= COS_TOL, (i, 1 - _cos(V[:, i], ref.V[:, i]))
-        assert 1 - _cos(U[:, i], ref.U[:, i]) <= COS_TOL, (i, 1 - _cos(U[:, i], ref.U[:, i]))
+    assert_tsvd_close(U, S, V, ref, k)
 
 
 # ------------------------------------------------------------------ one Gram-vector product
@@ -78,8 +73,7 @@ def test_gram_apply_vs_oracle(m, n, l):
     t.set_factors(U, S, V)
     got = t.gram_apply(v)
     t.close()
-    err = np.linalg.norm(got - want) / np.linalg.norm(want)
-    assert err <= 1e-5, err
+    assert_vec_close(got, want, 1e-5, f"gram_apply {m}x{n} l={l}")
 
 
 def test_gram_apply_ld_and_host_input():
@@ -96,7 +90,7 @@ def test_gram_apply_ld_and_host_input():
         outs.append(t.gram_apply(v))
         t.close()
     for got in outs:
-        assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-5
+        assert_vec_close(got, want, 1e-5)
     np.testing.assert_array_equal(outs[1], outs[2])
 
 
@@ -316,6 +310,7 @@ def test_tiny_shapes(m, n, k):
     rc, U, S, V, kf, *_ = _gpu_tsvd(A, k, 1e-6, V0)
     assert kf == ref.k_found
     np.testing.assert_allclose(S[:kf], ref.S[:kf], rtol=SIG_TOL)
+    assert_tsvd_close(U, S, V, ref, kf)  # the vectors too, not only sigma
 
 
 def test_zero_matrix_rank_exhausted():
@@ -407,7 +402,7 @@ def test_wide_matrix_parity(m, n, k, src):
     assert np.all(np.abs(iters - ref.iters) <= 1), (iters, ref.iters)
     # the product with the run's own factors (exported U is the fp32 copy of the fp64 iterate)
     want = oracle.gram_apply_wide(A, U.astype(np.float64), S, V.astype(np.float64), u)
-    assert np.linalg.norm(y - want) / np.linalg.norm(want) <= 1e-4
+    assert_vec_close(y, want, 1e-4)
 
 
 @pytest.mark.parametrize("m,n,k,T", [(2000, 500, 5, 0), (4200, 4099, 3, 0), (1500, 400, 3, 12), (700, 64, 4, 0),
@@ -471,3 +466,4 @@ def test_many_components_fall_back_cleanly():
     assert rc == P.OK and kf == k and rep["persistent"]["enabled"] is False
     rel = np.abs(S - ref.S) / ref.S
     assert rel.max() <= 1e-4, rel.max()
+    assert_tsvd_close(U, S, V, ref, k)  # all 140 u and v pairs, not only sigma

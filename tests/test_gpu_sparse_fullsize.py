@@ -24,6 +24,7 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_2208_08410_b200 as P  # noqa: E402
+from _parity import assert_pair_close, assert_vec_close  # noqa: E402
 
 M = N = 1 << 25
 D = 32
@@ -71,8 +72,7 @@ def test_c4n_bench_configuration_properties(c4n):
     for i in range(k):
         want = oracle.csr_matvec(sub_rp, sub_ci, sub_va, V[:, i].astype(np.float64)) / S[i]
         got = U[rows, i].astype(np.float64)
-        err = np.linalg.norm(got - want) / np.linalg.norm(want)
-        assert err <= 1e-6, (i, err)
+        assert_vec_close(got, want, 1e-6, f"u{i} rows")
 
 
 def test_c4n_gram_product_with_8_factors(c4n):
@@ -90,7 +90,7 @@ def test_c4n_gram_product_with_8_factors(c4n):
     t.close()
     torch.cuda.empty_cache()
     want = oracle.gram_apply_csr(rp, ci, va, N, U.astype(np.float64), S, V, v)
-    assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-6
+    assert_vec_close(got, want, 1e-6)
 
 
 def test_c4n_two_components_vs_oracle(c4n):

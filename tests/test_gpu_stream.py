@@ -14,6 +14,7 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_2208_08410_b200 as P  # noqa: E402
+from _parity import assert_pair_close, assert_vec_close  # noqa: E402
 
 
 def _cos(a, b):
@@ -59,8 +60,8 @@ def test_streamed_equals_oracle_and_resident(resident_rows, batch_rows, depth):
     ref = oracle.tsvd(A, k, eps, V0)
     np.testing.assert_allclose(S, ref.S, rtol=1e-4)
     for i in range(k):
-        assert 1 - _cos(U[:, i], ref.U[:, i]) <= 1e-4
-        assert 1 - _cos(V[:, i], ref.V[:, i]) <= 1e-4
+        assert_pair_close(U[:, i], ref.U[:, i], f"u{i}")
+        assert_pair_close(V[:, i], ref.V[:, i], f"v{i}")
 
 
 def test_streamed_pageable_gram_apply():
@@ -83,7 +84,7 @@ def test_streamed_pageable_gram_apply():
     rep = t.report()
     t.close()
     assert rep["placement"]["streaming"] and rep["placement"]["streamed_batches"] == (m + 332) // 333
-    assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-5
+    assert_vec_close(got, want, 1e-5)
 
 
 def test_stream_options_validated():

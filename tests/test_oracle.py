@@ -276,3 +276,55 @@ def test_wide_branch_mirrors_tall():
     np.testing.assert_allclose(rw.S, rt.S, rtol=1e-9)
     np.testing.assert_allclose(rw.U, rt.V, atol=1e-8)
     np.testing.assert_allclose(rw.V, rt.U, atol=1e-8)
+
+
+def _py_power_literal(a, b, x, eps, max_iter):
+    """Pure-Python Alg. 2 on A = diag(a, b) with the oracle's operation order written out: t = A v
+    (row dots in column order), y = A^T t (column sums in row order), ||y|| = sqrt(y0^2 + y1^2),
+    v1 = y / ||y||, stop on |v0 . v1| >= 1 - eps or at the cap (reading R5: P:119 has no cap).
+    Returns (iterations, v1, capped)."""
+    nx = math.sqrt(x[0] * x[0] + x[1] * x[1])
+    v0 = [x[0] / nx, x[1] / nx]
+    it = 0
+    while True:
+        t = [a * v0[0] + 0.0 * v0[1], 0.0 * v0[0] + b * v0[1]]
+        y = [a * t[0] + 0.0 * t[1], 0.0 * t[0] + b * t[1]]
+        ny = math.sqrt(y[0] * y[0] + y[1] * y[1])
+        v1 = [y[0] / ny, y[1] / ny]
+        it += 1
+        d = abs(v0[0] * v1[0] + v0[1] * v1[1])
+        if d >= 1 - eps:
+            return it, v1, False
+        if it >= max_iter:
+            return it, v1, True
+        v0 = v1
+
+
+@pytest.mark.parametrize("cap", [1, 2, 3, 7])
+def test_max_iter_branch_pure_python(cap):
+    """The MAX_ITER branch (oracle.c: it >= max_iter -> OR_NOT_CONVERGED): on the near-degenerate
+    diag(1, 0.999) no step meets eps = 1e-12, so the loop stops after exactly `cap` iterations with
+    status NOT_CONVERGED and the iterate of the pure-Python loop, bit for bit.  An off-by-one (> for
+    >=) or a dropped status fails here."""
+    a, b = 1.0, float(np.float32(0.999))
+    x = [0.6, 0.8]
+    want_it, want_v, capped = _py_power_literal(a, b, x, 1e-12, cap)
+    assert capped and want_it == cap
+    A = np.diag([a, b]).astype(np.float32)
+    r = oracle.tsvd(A, 1, 1e-12, np.array([x]), max_iter=cap)
+    assert r.status == oracle.NOT_CONVERGED and r.k_found == 1
+    assert r.iters[0] == cap
+    np.testing.assert_array_equal(r.V[:, 0], want_v)
+    # a converging component under the same cap keeps status OK: diag(3, 1) needs few iterations
+    r2 = oracle.tsvd(np.diag([3.0, 1.0]).astype(np.float32), 1, 1e-6, np.array([x]), max_iter=50)
+    assert r2.status == oracle.OK and r2.iters[0] < 50
+
+
+def test_max_iter_status_is_sticky_over_components():
+    """k = 2 on diag(1, 0.999, 0.5): component 0 hits the cap (status NOT_CONVERGED), component 1
+    is still computed (the warning is not fatal, include/tsvd.h) and k_found == 2."""
+    A = np.diag([1.0, 0.999, 0.5]).astype(np.float32)
+    V0 = np.array([[0.6, 0.8, 0.1], [0.3, -0.2, 0.9]])
+    r = oracle.tsvd(A, 2, 1e-12, V0, max_iter=4)
+    assert r.status == oracle.NOT_CONVERGED and r.k_found == 2
+    assert r.iters[0] == 4
