@@ -70,6 +70,14 @@ CONFIGS = {
                          "k=8, fixed T=10 (P:380 per-node sparse shape; BASELINE configs[3] family)",
                 m=1 << 25, n=1 << 25, k=8, eps=1e-6, family="sparse", d=32, fixed_T=10, rho=0.0, s0=0.0, rank=0),
 }
+# BASELINE configs[3] at its stated size: 1e8 x 1e8, density 1e-6 (100 entries per row, 1e10 in all),
+# k = 8, row-partitioned; each rank generates its slab on the device (synth.stratified_csr_device).
+# One GPU cannot hold the slab's two sliced copies (~170 GB) next to the generated input: 2, 4, 8 GPUs.
+CONFIGS["c3p"] = dict(workload="sparse CSR 100000000x100000000, density 1e-6 (100 nnz/row, 1e10 nnz), values in "
+                               "(0,1], stratified random columns, k=8, fixed T=10 (BASELINE configs[3] at its "
+                               "stated size; the paper disables convergence, P:380)",
+                      m=100_000_000, n=100_000_000, k=8, eps=1e-6, family="sparse_device", d=100, fixed_T=10,
+                      rho=0.0, s0=0.0, rank=0)
 METRIC = "seconds to top-k triplets; Gram-vector effective GB/s vs HBM/H2D peak @1/2/4/8"
 
 
@@ -302,7 +310,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     m, n, k, eps = cfg["m"], cfg["n"], cfg["k"], cfg["eps"]
     stream_cfg = cfg.get("stream", False)
-    sparse = cfg["family"] == "sparse"
+    sparse = cfg["family"] in ("sparse", "sparse_device")
     r0, r1 = slab(world, rank, m)
     if stream_cfg:  # out-of-memory degree 1: A lives in pinned host memory, streamed every pass
         A_pin = torch.empty((r1 - r0, n), dtype=torch.float32, pin_memory=True)
@@ -311,6 +319,9 @@ def main():
     elif cfg["family"] == "hadamard_device":  # slab generated in HBM (larger than useful on the host)
         s_pl = cfg["s0"] * cfg["rho"] ** np.arange(cfg["rank"])
         A_dev = synth.hadamard_lowrank_device(m, n, s_pl, seed=1, rows=(r0, r1), device=f"cuda:{local}")
+        A_host = None
+    elif cfg["family"] == "sparse_device":  # generated in HBM; not referenced after set_csr (freed then)
+        A_dev = synth.stratified_csr_device(m, n, cfg["d"], seed=1, rows=(r0, r1), device=f"cuda:{local}")
         A_host = None
     elif sparse:  # paper-like CSR slab; same rows whatever the GPU count
         A_host = synth.random_csr(m, n, cfg["d"], seed=1, rows=(r0, r1))
@@ -336,6 +347,10 @@ def main():
         if args.sparse_block is not None:
             t.set_option(P.OPT_SPARSE_BLOCK, args.sparse_block)
         t.set_csr(*A_dev, row_begin=r0, row_end=r1)
+        if A_host is None:  # tsvd_set_csr keeps its own sliced copies: drop the generated input
+            t._keep = []
+            A_dev = None
+            torch.cuda.empty_cache()
     else:
         t.set_dense(A_dev, r0, r1)
     if args.loop == "host":
@@ -534,8 +549,14 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        # device-generated slabs: the oracle runs on a 65536-row sample copied to the host
-        cpu = cpu_baseline(A_host if A_host is not None else A_dev[:65536].cpu().numpy(), cfg)
+        # device-generated slabs: the oracle runs on a 65536-row sample (the same rows, generated on the host)
+        if A_host is not None:
+            sample = A_host
+        elif cfg["family"] == "sparse_device":
+            sample = synth.stratified_csr(m, n, cfg["d"], seed=1, rows=(0, 65536))
+        else:
+            sample = A_dev[:65536].cpu().numpy()
+        cpu = cpu_baseline(sample, cfg)
 
     if rank == 0:
         line = {

@@ -122,7 +122,7 @@ typedef enum {
                                     split into so that each launch's block of the fp32 gathered
                                     vector stays in L2; 0 (default) = 32 MiB of fp32 (n > 8M
                                     columns / rows => several blocks). Read by tsvd_set_csr          */
-    TSVD_OPT_METHOD = 21         /* 0 (default): implicit Gram-vector products (Eq. 2, the north star);
+    TSVD_OPT_METHOD = 21,        /* 0 (default): implicit Gram-vector products (Eq. 2, the north star);
                                     1: explicit Gram (Alg. 2 lines 6-9 with Alg. 3's Gram, P:114-121,
                                     P:220-249): B0 = A^T A once (TF32x3 tensor-core GEMMs over the
                                     symmetric block schedule of P:348), then per iteration
@@ -131,6 +131,12 @@ typedef enum {
                                     B0 all-reduced once, iterations row-partitioned over B0 (y rows
                                     exchanged over NVLink inside the kernel; k <= 129, else
                                     replicated).  Pays off when iterations per component are many */
+    TSVD_OPT_V_PLACEMENT = 22    /* 0 (default): the co-factor V (n x k fp64) and the initial samples
+                                    (k x n fp64) in HBM; 1: in pinned host memory mapped into the
+                                    device address space ("the heavy co-factor V is stored on the
+                                    host"): the kernels read and write them over the host link
+                                    (frees 16 n k bytes of HBM; every iteration pays n l reads over
+                                    PCIe).  Must precede the first run                               */
 } tsvd_option;
 
 /*

@@ -1,0 +1,368 @@
+// gram_tc.cuh — B0 = A^T A on the 5th-generation tensor cores (tcgen05, kind::tf32), for the
+// explicit-Gram path (TSVD_OPT_METHOD = 1; Alg. 3's Gram, with the symmetric task schedule
+// of P:347-348: only the tiles touching the upper triangle are computed, the rest is mirrored).
+//
+// C[i, j] = sum_r A[r, i] A[r, j]: M = the i columns, N = the j columns, K = the rows of the slab.
+// Both operands are column blocks of the row-major slab, so both are MN-major in the MMA's terms.
+// One persistent CTA per SM walks a tile list (BM x BN = 128 x 256 output tiles, grouped so that the
+// SMs working at the same time share operand column blocks in L2); per tile the K loop streams
+// BK-row chunks of the two column blocks through a ring of shared-memory stages:
+//   warp 0  (one thread)  TMA producer: 2-D tensor loads (128-byte swizzle, 32-byte atoms) of the raw
+//                         fp32 chunks
+//   warps 2-5             converter: lo = a - tf32(a) for every element of the chunk (the tensor core
+//                         reads fp32 bits and keeps the top 19, i.e. tf32(a) by truncation), written
+//                         to the stage's lo buffers at the same (swizzled) offsets
+//   warps 6-9             epilogue: each finished K chunk of the accumulator (TMEM -> registers) is
+//                         added into the output (see below)
+//   warp 1  (one thread)  MMA issuer: per 8-row k-group three tcgen05.mma (M=128, N=256, K=8):
+//                         D += A·B, D += A·B_lo, D += A_lo·B  (3xTF32: hi·hi + hi·lo + lo·hi with
+//                         hi = the truncation the MMA applies itself, so no hi copy exists) into a
+//                         128 x 256 fp32 accumulator in tensor memory; tcgen05.commit frees the stage.
+//                         The tensor core's accumulation rounds toward zero (measured: a relative bias
+//                         ~K 2^-25 on sums of K positive terms, 1e-3 at K = 65536), so it only sums
+//                         K chunks of 512 rows, into two accumulators used in turn; the epilogue warps
+//                         add each finished chunk into the output in fp32 (round to nearest) while the
+//                         tensor core fills the other one
+// No copy of A (the round-1 path kept 8 GiB of TF32 hi / lo copies for cuBLAS at C2).
+#pragma once
+#include <cuda.h>
+
+#include "gram_kernels.cuh"
+
+namespace tsvd {
+
+constexpr int kGtBM = 128, kGtBN = 256, kGtBK = 16, kGtStages = 4;
+constexpr int kGtConvWarps = 4, kGtEpiWarps = 4;                   // warps 2-5 convert, 6-9 fold chunks
+constexpr int kGtThreads = 32 * (2 + kGtConvWarps + kGtEpiWarps);
+constexpr int kGtConv = 32 * kGtConvWarps;
+constexpr int kGtChunkBytes = kGtBK * 128;                         // one 32-column x BK-row TMA box
+constexpr int kGtABytes = (kGtBM / 32) * kGtChunkBytes;            // 8 KB
+constexpr int kGtBBytes = (kGtBN / 32) * kGtChunkBytes;            // 16 KB
+constexpr int kGtStageBytes = 2 * (kGtABytes + kGtBBytes);         // raw + lo: 48 KB
+constexpr int kGtSmem = kGtStages * kGtStageBytes + 1024 + 256;    // + alignment + barriers
+constexpr int kGtTmemCols = 512;                                   // two fp32 accumulators (N columns each)
+constexpr int kGtChunkStages = 512 / kGtBK;  // K rows summed inside the tensor core per chunk: 512
+
+struct GtParams {
+    const int2 *tiles;   // (I, J) tile list, in schedule order
+    int ntiles;
+    int64_t n;           // B0 is n x n, row stride ldb
+    int64_t ldb;
+    int64_t m;           // rows of the slab (K)
+    float *B;
+};
+
+__device__ __forceinline__ uint32_t gt_smem(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void gt_tma_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(gt_smem(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(gt_smem(bar))
+        : "memory");
+}
+
+// shared-memory matrix descriptor, MN-major tf32: the only smem layout the tensor core takes for
+// 32-bit MN-major operands is the 128-byte swizzle with 32-byte atoms (layout type 1,
+// "SWIZZLE_128B_BASE32B"; the TMA writes it with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): 128-byte rows
+// (32 elements along M / N) in groups of 4 rows.  LBO = stride between 32-element column chunks,
+// SBO = stride between 4-row groups (512 B), version 1 (sm_100)
+__device__ __forceinline__ uint64_t gt_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;  // version
+    d |= (uint64_t)1 << 61;  // SWIZZLE_128B_BASE32B
+    return d;
+}
+
+// instruction descriptor: D fp32, A / B tf32, both MN-major, M = 128, N = 256
+constexpr uint32_t kGtIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
+                              ((uint32_t)(kGtBN >> 3) << 17) | ((uint32_t)(kGtBM >> 4) << 24);
+
+__device__ __forceinline__ void gt_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(kGtIdesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void gt_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(gt_smem(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void gt_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(gt_smem(bar)) : "memory");
+}
+
+// lo = a - tf32_trunc(a) (exact in fp32): the part of a the tensor core drops
+__device__ __forceinline__ float gt_lo(float a) { return a - __uint_as_float(__float_as_uint(a) & 0xFFFFE000u); }
+
+// the lo parts of a row slab in global memory (LO_GMEM)
+__global__ void gram_lo_split(const float *__restrict__ A, int64_t rows, int64_t cols, int64_t ld,
+                              float *__restrict__ lo) {
+    const int64_t n4 = cols / 4, total = rows * n4;  // ld % 4 == 0 and 16-B aligned rows (TMA contract)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / n4, c = (i - r * n4) * 4;
+        const float4 a = *reinterpret_cast<const float4 *>(A + r * ld + c);
+        *reinterpret_cast<float4 *>(lo + r * ld + c) = make_float4(gt_lo(a.x), gt_lo(a.y), gt_lo(a.z), gt_lo(a.w));
+    }
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows && (cols & 3); r += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t c = n4 * 4; c < cols; ++c) lo[r * ld + c] = gt_lo(A[r * ld + c]);
+}
+
+// mbarrier phase test without blocking (the epilogue folds a finished chunk when it is ready)
+__device__ __forceinline__ bool gt_test(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(gt_smem(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+// LO_GMEM: the lo parts come from a precomputed copy in global memory (map_lo, one elementwise pass
+// over A before the kernel) by TMA like the raw chunks, instead of the converter warps — less
+// shared-memory traffic per stage (no converter read + write), one more copy of A in HBM
+template <bool LO_GMEM>
+__global__ void __launch_bounds__(kGtThreads, 1)
+    gram_tc(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap map_lo, const GtParams p) {
+    extern __shared__ unsigned char gt_raw[];
+    unsigned char *smem = (unsigned char *)(((uintptr_t)gt_raw + 1023) & ~(uintptr_t)1023);  // swizzle: 1 KB
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kGtStages * kGtStageBytes);         // TMA landed
+    uint64_t *conv = full + kGtStages;    // lo buffers written (kGtConv converter threads)
+    uint64_t *empty = conv + kGtStages;   // the stage's MMAs completed
+    uint64_t *dfull = empty + kGtStages;  // [2] accumulator buffer b holds a finished K chunk
+    uint64_t *dempty = dfull + 2;         // [2] the epilogue has folded buffer b into the output
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(dempty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nk = (int)((p.m + kGtBK - 1) / kGtBK);
+    const int nchunk = (nk + kGtChunkStages - 1) / kGtChunkStages;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kGtStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&conv[s], kGtConv);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&dfull[b], 1);
+            mbar_init(&dempty[b], 32 * kGtEpiWarps);
+        }
+        fence_barrier_init();
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(gt_smem(tmem_slot)),
+                     "n"(kGtTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    // Work order: rounds of two tiles per CTA (t0 = r 2G + b, t1 = t0 + G, G = grid), and inside a round
+    // K-chunk-major: chunk k of t0, chunk k of t1, chunk k + 1 of t0, ...  Every CTA is at about the
+    // same K chunk of a compact block of tiles at the same time, so one chunk's operand rows (a few MB)
+    // are read from DRAM once and served from L2 to all SMs; the two tiles alternate between the two
+    // TMEM accumulators, so one tile's chunk is folded while the other's is multiplied.
+    // job j (0, 1, 2, ... in that order) uses accumulator j & 1.
+#define GT_FOR_JOBS(...)                                                                           \
+    for (int r0 = blockIdx.x; r0 < p.ntiles; r0 += 2 * gridDim.x) {                                \
+        const int nt = r0 + (int)gridDim.x < p.ntiles ? 2 : 1;                                     \
+        const int2 tl[2] = {p.tiles[r0], p.tiles[nt == 2 ? r0 + gridDim.x : r0]};                  \
+        for (int k = 0; k < nchunk; ++k)                                                           \
+            for (int u = 0; u < nt; ++u) {                                                         \
+                const int2 tile = tl[u];                                                           \
+                const int kb0 = k * kGtChunkStages;                                                \
+                const int kb1 = kb0 + kGtChunkStages < nk ? kb0 + kGtChunkStages : nk;             \
+                __VA_ARGS__                                                                        \
+            }                                                                                      \
+    }
+
+    if (warp == 0) {
+        if (lane == 0) {  // ===== TMA producer
+            int s = 0;
+            uint32_t ph = 0;
+            GT_FOR_JOBS({
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    unsigned char *st = smem + (size_t)s * kGtStageBytes;
+                    mbar_arrive_expect_tx(&full[s], (uint32_t)((LO_GMEM ? 2 : 1) * (kGtABytes + kGtBBytes)));
+                    for (int c = 0; c < kGtBM / 32; ++c)
+                        gt_tma_2d(st + c * kGtChunkBytes, &map, tile.x * kGtBM + 32 * c, kb * kGtBK, &full[s]);
+                    for (int c = 0; c < kGtBN / 32; ++c)
+                        gt_tma_2d(st + kGtABytes + c * kGtChunkBytes, &map, tile.y * kGtBN + 32 * c, kb * kGtBK,
+                                  &full[s]);
+                    if (LO_GMEM) {
+                        unsigned char *sl = st + kGtABytes + kGtBBytes;
+                        for (int c = 0; c < kGtBM / 32; ++c)
+                            gt_tma_2d(sl + c * kGtChunkBytes, &map_lo, tile.x * kGtBM + 32 * c, kb * kGtBK, &full[s]);
+                        for (int c = 0; c < kGtBN / 32; ++c)
+                            gt_tma_2d(sl + kGtABytes + c * kGtChunkBytes, &map_lo, tile.y * kGtBN + 32 * c,
+                                      kb * kGtBK, &full[s]);
+                    }
+                    if (++s == kGtStages) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            })
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ===== MMA issuer
+            int s = 0;
+            uint32_t ph = 0;
+            uint32_t dph[2] = {0u, 0u};
+            int buf = 0;
+            GT_FOR_JOBS({
+                const uint32_t dacc = tmem + (uint32_t)(buf * kGtBN);  // this job's accumulator columns
+                mbar_wait(&dempty[buf], dph[buf] ^ 1u);  // the epilogue has folded this buffer's last job
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(LO_GMEM ? &full[s] : &conv[s], ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t base = gt_smem(smem + (size_t)s * kGtStageBytes);
+                    const uint32_t a_raw = base, b_raw = base + kGtABytes;
+                    const uint32_t a_lo = base + kGtABytes + kGtBBytes, b_lo = a_lo + kGtABytes;
+#pragma unroll
+                    for (int kk = 0; kk < kGtBK / 8; ++kk) {
+                        const uint32_t ko = kk * 1024;  // 8 rows of 128 B
+                        const uint64_t da = gt_desc(a_raw + ko, kGtChunkBytes, 512);
+                        const uint64_t db = gt_desc(b_raw + ko, kGtChunkBytes, 512);
+                        const uint64_t dal = gt_desc(a_lo + ko, kGtChunkBytes, 512);
+                        const uint64_t dbl = gt_desc(b_lo + ko, kGtChunkBytes, 512);
+                        gt_mma(dacc, da, db, (kb > kb0 || kk > 0) ? 1u : 0u);  // hi·hi (a job's first overwrites)
+                        gt_mma(dacc, da, dbl, 1u);                             // hi·lo
+                        gt_mma(dacc, dal, db, 1u);                             // lo·hi
+                    }
+                    gt_commit(&empty[s]);  // frees the stage once these MMAs have read it
+                    if (++s == kGtStages) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+                gt_commit(&dfull[buf]);  // the job's partial sum is complete once every MMA above has finished
+                dph[buf] ^= 1u;
+                buf ^= 1;
+            })
+        }
+    } else if (warp < 2 + kGtConvWarps) {  // ===== converter (warps 2-5)
+        if (!LO_GMEM) {
+            const int ct = threadIdx.x - 64;  // 0 .. kGtConv - 1
+            int s = 0;
+            uint32_t ph = 0;
+            GT_FOR_JOBS({
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&full[s], ph);
+                    const float4 *raw = reinterpret_cast<const float4 *>(smem + (size_t)s * kGtStageBytes);
+                    float4 *lo =
+                        reinterpret_cast<float4 *>(smem + (size_t)s * kGtStageBytes + kGtABytes + kGtBBytes);
+#pragma unroll 4
+                    for (int i = ct; i < (kGtABytes + kGtBBytes) / 16; i += kGtConv) {
+                        const float4 a = raw[i];
+                        lo[i] = make_float4(gt_lo(a.x), gt_lo(a.y), gt_lo(a.z), gt_lo(a.w));
+                    }
+                    fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core (async proxy)
+                    gt_arrive(&conv[s]);
+                    if (++s == kGtStages) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            })
+        }
+    } else {  // ===== epilogue (warps 6-9: TMEM lane quarter q = warp % 4, all 256 columns)
+        // a finished job's partial sum (rows i0 + 32 q + lane, columns j0 .. j0 + 255) is added in fp32
+        // (round to nearest) into the output — chunk 0 of a tile stores.  The tensor core's own
+        // accumulation rounds toward zero, so its sums stay short (512 rows) and the chunks of a tile are
+        // summed here, in chunk order, while the tensor core fills the other accumulator
+        const int q = warp & 3;
+        uint32_t dph[2] = {0u, 0u};
+        int buf = 0;
+        GT_FOR_JOBS({
+            (void)kb1;
+            const int64_t i = (int64_t)tile.x * kGtBM + 32 * q + lane;
+            const int64_t j0 = (int64_t)tile.y * kGtBN;
+            float *row = p.B + i * p.ldb + j0;
+            mbar_wait(&dfull[buf], dph[buf]);
+            dph[buf] ^= 1u;
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const bool first = k == 0;
+#pragma unroll 1
+            for (int c = 0; c < kGtBN / 32; ++c) {
+                uint32_t v[32];
+                const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * kGtBN + 32 * c);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+                    "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+                    "%30, %31}, [%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                      "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+                      "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+                      "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr)
+                    : "memory");
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (i < p.n) {
+                    const int64_t jc = j0 + 32 * c;
+                    float *dst = row + 32 * c;
+                    if (jc + 32 <= p.n) {
+#pragma unroll
+                        for (int e = 0; e < 32; e += 4) {
+                            float4 x = make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]),
+                                                   __uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
+                            if (!first) {
+                                const float4 o = *reinterpret_cast<const float4 *>(dst + e);
+                                x.x += o.x;
+                                x.y += o.y;
+                                x.z += o.z;
+                                x.w += o.w;
+                            }
+                            *reinterpret_cast<float4 *>(dst + e) = x;
+                        }
+                    } else {
+                        for (int e = 0; e < 32; ++e)
+                            if (jc + e < p.n) dst[e] = first ? __uint_as_float(v[e]) : dst[e] + __uint_as_float(v[e]);
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            gt_arrive(&dempty[buf]);
+            buf ^= 1;
+        })
+    }
+#undef GT_FOR_JOBS
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kGtTmemCols) : "memory");
+}
+
+// strictly-lower triangle from the upper one (the symmetric schedule computed every (i, j) with
+// j >= i); 32 x 32 tiles through shared memory, both sides coalesced
+__global__ void gram_mirror_lower(float *__restrict__ B, int64_t n, int64_t ldb) {
+    __shared__ float tile[32][33];
+    const int64_t bi = blockIdx.y, bj = blockIdx.x;  // destination tile (rows bi, columns bj), bi >= bj
+    if (bj > bi) return;
+    const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+    for (int k = ty; k < 32; k += 8) {  // source: rows of tile (bj, bi)
+        const int64_t r = bj * 32 + k, c = bi * 32 + tx;
+        if (r < n && c < n) tile[k][tx] = B[r * ldb + c];
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+        const int64_t r = bi * 32 + k, c = bj * 32 + tx;  // B[r][c] = B[c][r] for r > c
+        if (r < n && c < n && r > c) B[r * ldb + c] = tile[tx][k];
+    }
+}
+
+}  // namespace tsvd

@@ -10,13 +10,15 @@
 //   N3 (MODE_Y)  y_j = sum_k cval_k t32[row_k] over the CSC — the transpose product without atomics and
 //                in a fixed order; block 0 also sums the w partials.  y and w land in yw = [y | w].
 // Layout (N4b, built once by tsvd_set_csr): the entries are split into K index blocks so that one
-// launch's gathers stay inside an L2-resident block of the gathered vector (32 MiB of fp32); block b
-// of a direction is a compressed matrix of its own with int32 block-local offsets off[b][0..segs] and
-// an int64 base[b] into the shared idx / val arrays.  The per-segment fp64 sums are carried across the
-// K launches in block order (acc), so every result is deterministic.
-// One THREAD per segment (a CSR row piece of a block holds ~nnz/row/K entries: 8 at c4n): the entry
-// loads of a batch of 8 are issued together, then the 8 gathers, then the fp64 products in entry
-// order — 8 independent L2 gathers in flight per thread, no shuffles, no shared partial sums.
+// launch's gathers stay inside an L2-resident block of the gathered vector (32 MiB of fp32).  Inside a
+// block the segments are stored SELL-32-sigma: segments are sorted by length (descending, stable)
+// inside windows of kSellW, cut into slices of 32 (one warp, one segment per lane), and a slice's
+// entries are interleaved — entry u of lane l at slice_off + 32 u + l, short segments padded with
+// idx = -1 — so every entry load of a warp is one coalesced 128-byte line (a plain CSR row per thread
+// costs ~9 L1 wavefronts per load instruction; the random gathers, 1 wavefront per entry, are what
+// is left).  perm[] maps a slice lane back to its segment.  The per-segment fp64 sums are carried
+// across the K launches in block order (acc) and each segment sums its entries in their order, so
+// every result is deterministic.
 #pragma once
 #include "fin_kernels.cuh"
 
@@ -25,18 +27,35 @@ namespace tsvd {
 constexpr int kSpThreads = 256;
 constexpr size_t kSpL2BlockBytes = 32u << 20;  // fp32 gather block that stays L2-resident (126 MB L2)
 constexpr int kSpWarps = kSpThreads / 32;
-constexpr int kSpBatch = 8;                     // entries (gathers) in flight per thread
+#ifndef TSVD_SP_BATCH
+#define TSVD_SP_BATCH 8
+#endif
+constexpr int kSpBatch = TSVD_SP_BATCH;         // entries (gathers) in flight per lane
 constexpr int kSpMaxL = 96;                     // deflation columns the per-thread w partials can hold
+constexpr int kSellW = 1024;                    // segments per sorting window (sigma)
 
 enum SpMode { MODE_T = 0, MODE_U = 1, MODE_Y = 2 };
 
-// One direction of the product: K blocks of `segs` segments over shared entry arrays.
+// the random gather of the fp32 vector (A/B variants: TSVD_SP_GATHER = 0 read-only path, 1 L2 only)
+#ifndef TSVD_SP_GATHER
+#define TSVD_SP_GATHER 0
+#endif
+__device__ __forceinline__ float sp_gather(const float *p) {
+#if TSVD_SP_GATHER == 1
+    return __ldcg(p);
+#else
+    return __ldg(p);
+#endif
+}
+
+// One direction of the product: K blocks of `segs` segments over shared entry arrays, SELL-32-sigma.
 struct SpView {
-    const int32_t *off;   // [K][segs + 1] block-local offsets (off[b][0] == 0)
+    const int32_t *soff;  // [K][nsl + 1] block-local entry offset of each slice (slice length = diff / 32)
     const int64_t *base;  // [K + 1] first entry of each block
-    const int32_t *idx;   // gathered indices (columns for the CSR, local rows for the CSC)
+    const int32_t *perm;  // [K][segs] segment of slice lane (32 j + l)
+    const int32_t *idx;   // gathered indices (columns for the CSR, local rows for the CSC); -1 = padding
     const float *val;
-    int64_t segs;
+    int64_t segs, nsl;    // segments, slices per block (ceil(segs / 32))
 };
 
 struct SpParams {
@@ -62,33 +81,15 @@ struct SpParams {
     int parts;        // gridDim.x of N2 (rows of wpart)
     int phase, nphase;  // launch `phase` of `nphase` covers index block `phase`
     double *acc;      // [segs] carried fp64 partial sums when nphase > 1
-    int64_t seg0, seg1;  // segments [seg0, seg1) of this launch (N3 last block: column chunks)
+    int64_t sl0, sl1; // slices [sl0, sl1) of this launch (N3's last block: column chunks, kSellW-aligned)
+    const int32_t *blk_idx;  // out of memory (degree 1): this block's entries in a device ring slot
+    const float *blk_val;    // (nullptr: the view's resident arrays)
 };
 
-// sum_k val[k] x[idx[k]] over [k0, k1), entry order, fp64
-__device__ __forceinline__ double sp_segment_dot(const int32_t *__restrict__ ip, const float *__restrict__ vp,
-                                                 const float *__restrict__ x, int32_t k0, int32_t k1) {
-    double sum = 0.0;
-    for (int32_t k = k0; k < k1; k += kSpBatch) {
-        int32_t c[kSpBatch];
-        float v[kSpBatch], g[kSpBatch];
-#pragma unroll
-        for (int u = 0; u < kSpBatch; ++u) {
-            const bool ok = k + u < k1;
-            c[u] = ok ? __ldcs(ip + k + u) : 0;  // streaming: read once per pass
-            v[u] = ok ? __ldcs(vp + k + u) : 0.f;
-        }
-#pragma unroll
-        for (int u = 0; u < kSpBatch; ++u) g[u] = (k + u < k1) ? __ldg(x + c[u]) : 0.f;
-#pragma unroll
-        for (int u = 0; u < kSpBatch; ++u)
-            if (k + u < k1) sum += (double)v[u] * (double)g[u];
-    }
-    return sum;
-}
-
-// N2 / N3.  Dynamic shared memory (MODE_T): l * (kSpThreads + 1) doubles (per-thread w partials, c).
-template <int MODE>
+// N2 / N3.  LAST: the launch of the last index block (finishes the sums: outputs, deflation, w);
+// the others only carry their partial sums.  Dynamic shared memory (MODE_T, LAST): l * (kSpThreads + 1)
+// doubles (per-thread w partials, c).
+template <int MODE, bool LAST>
 __global__ void __launch_bounds__(kSpThreads) sp_pass(const SpParams p) {
     extern __shared__ double wsm[];
     __shared__ double red[kSpWarps];
@@ -99,28 +100,46 @@ __global__ void __launch_bounds__(kSpThreads) sp_pass(const SpParams p) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const SpView &V = MODE == MODE_Y ? p.csc : p.csr;
     const float *__restrict__ x = MODE == MODE_Y ? p.t32 : p.y32;
-    const int l = MODE == MODE_T ? p.l : 0;
-    const bool last = p.phase == p.nphase - 1;
-    const bool carry_in = p.nphase > 1 && p.phase > 0;
+    const int l = (MODE == MODE_T && LAST) ? p.l : 0;
+    const bool carry_in = p.phase > 0;
     double *csm = wsm + (int64_t)l * kSpThreads;
-    if (MODE == MODE_T && last) {
+    if (MODE == MODE_T && LAST) {
         for (int i = 0; i < l; ++i) wsm[i * kSpThreads + tid] = 0.0;
         for (int i = tid; i < l; i += kSpThreads) csm[i] = p.c[i];
         __syncthreads();
     }
     const double inv = MODE == MODE_Y ? 1.0 : 1.0 / st->ny;
-    const int32_t *__restrict__ off = V.off + (int64_t)p.phase * (V.segs + 1);
+    const int32_t *__restrict__ soff = V.soff + (int64_t)p.phase * (V.nsl + 1);
+    const int32_t *__restrict__ perm = V.perm + (int64_t)p.phase * V.segs;
     const int64_t b0 = V.base[p.phase];
-    const int32_t *__restrict__ ip = V.idx + b0;
-    const float *__restrict__ vp = V.val + b0;
+    const int32_t *__restrict__ ip = (p.blk_idx ? p.blk_idx : V.idx + b0) + lane;
+    const float *__restrict__ vp = (p.blk_val ? p.blk_val : V.val + b0) + lane;
     double sq = 0.0;
-    const int64_t stride = (int64_t)gridDim.x * kSpThreads;
-    for (int64_t s = p.seg0 + (int64_t)blockIdx.x * kSpThreads + tid; s < p.seg1; s += stride) {
-        const double carried = carry_in ? __ldcg(p.acc + s) : 0.0;  // issued before the gathers
-        const int32_t k0 = __ldcs(off + s), k1 = __ldcs(off + s + 1);
-        double sum = sp_segment_dot(ip, vp, x, k0, k1);
+    const int64_t nw = (int64_t)gridDim.x * kSpWarps;
+    for (int64_t j = p.sl0 + (int64_t)blockIdx.x * kSpWarps + warp; j < p.sl1; j += nw) {
+        const int64_t q = 32 * j + lane;
+        const int32_t s = q < V.segs ? __ldcs(perm + q) : -1;  // this lane's segment (-1: past the end)
+        const double carried = (carry_in && s >= 0) ? __ldcg(p.acc + s) : 0.0;  // issued before the gathers
+        const int32_t e0 = __ldg(soff + j), e1 = __ldg(soff + j + 1);  // slice entries [e0, e1), 32 wide
+        double sum = 0.0;
+        for (int32_t e = e0; e < e1; e += 32 * kSpBatch) {
+            int32_t c[kSpBatch];
+            float v[kSpBatch], g[kSpBatch];
+#pragma unroll
+            for (int u = 0; u < kSpBatch; ++u) {  // coalesced: 32 lanes read one 128-byte line
+                const bool ok = e + 32 * u < e1;
+                c[u] = ok ? __ldcs(ip + e + 32 * u) : -1;  // streaming: read once per pass
+                v[u] = ok ? __ldcs(vp + e + 32 * u) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < kSpBatch; ++u) g[u] = c[u] >= 0 ? sp_gather(x + c[u]) : 0.f;
+#pragma unroll
+            for (int u = 0; u < kSpBatch; ++u)
+                if (c[u] >= 0) sum += (double)v[u] * (double)g[u];  // entry order
+        }
+        if (s < 0) continue;
         if (carry_in) sum = carried + sum;  // blocks in order
-        if (!last) {
+        if (!LAST) {
             p.acc[s] = sum;
             continue;
         }
@@ -133,7 +152,7 @@ __global__ void __launch_bounds__(kSpThreads) sp_pass(const SpParams p) {
         } else {
             double t = sum * inv;
             if (l > 0) {  // U_r . c: deflation without forming X' (Eq. 2, factored); w += t U_r
-                const float *Ur = p.U + s * p.ldu;
+                const float *Ur = p.U + (int64_t)s * p.ldu;
                 double corr = 0.0;
                 for (int i = 0; i < l; ++i) corr += (double)Ur[i] * csm[i];
                 t -= corr;
@@ -142,7 +161,7 @@ __global__ void __launch_bounds__(kSpThreads) sp_pass(const SpParams p) {
             p.t32[s] = (float)t;
         }
     }
-    if (!last) return;  // not the last block: only the carried sums were written
+    if (!LAST) return;  // not the last block: only the carried sums were written
     if (MODE == MODE_U) {
         sq = warp_sum(sq);
         if (lane == 0) red[warp] = sq;
@@ -156,16 +175,91 @@ __global__ void __launch_bounds__(kSpThreads) sp_pass(const SpParams p) {
         __syncthreads();
         for (int i = warp; i < l; i += kSpWarps) {  // threads' partials in thread order
             double a = 0.0;
-            for (int j = lane; j < kSpThreads; j += 32) a += wsm[i * kSpThreads + j];
+            for (int jj = lane; jj < kSpThreads; jj += 32) a += wsm[i * kSpThreads + jj];
             a = warp_sum(a);
             if (lane == 0) p.wpart[(int64_t)blockIdx.x * p.wpart_ld + i] = a;
         }
-    } else if (blockIdx.x == 0 && p.seg1 == V.segs) {  // the launch that finishes y also finishes w
+    } else if (blockIdx.x == 0 && p.sl1 == V.nsl) {  // the launch that finishes y also finishes w
         for (int i = warp; i < p.l; i += kSpWarps) {
             double w = 0.0;
             for (int b = lane; b < p.parts; b += 32) w += p.wpart[(int64_t)b * p.wpart_ld + i];
             w = warp_sum(w);
             if (lane == 0) p.yw[p.wofs + i] = w;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- N4b: SELL-32-sigma build (one time)
+// one CTA (kSellW threads) per (block, window): sort the window's segments by length, descending and
+// stable (bitonic sort of 64-bit keys (~len << 32 | index)), write perm, the inverse position ipos and
+// the slice sizes (32 x the longest segment of each slice, the slice's first)
+__global__ void __launch_bounds__(kSellW) sell_sort(const unsigned *__restrict__ cnt, int64_t segs,
+                                                    int32_t *__restrict__ perm, int32_t *__restrict__ ipos,
+                                                    unsigned *__restrict__ ssize, int64_t nsl) {
+    __shared__ unsigned long long key[kSellW];
+    const int b = blockIdx.y;
+    const int64_t w0 = (int64_t)blockIdx.x * kSellW;
+    const int i = threadIdx.x;
+    const int64_t s = w0 + i;
+    const unsigned len = s < segs ? cnt[(int64_t)b * segs + s] : 0u;
+    key[i] = s < segs ? ((unsigned long long)(0xFFFFFFFFu - len) << 32) | (unsigned)i : ~0ull;
+    __syncthreads();
+    for (int k = 2; k <= kSellW; k <<= 1)
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            const int ixj = i ^ jj;
+            if (ixj > i) {
+                const unsigned long long a = key[i], c = key[ixj];
+                if (((i & k) == 0) == (a > c)) {
+                    key[i] = c;
+                    key[ixj] = a;
+                }
+            }
+            __syncthreads();
+        }
+    const unsigned long long kk = key[i];
+    if (s < segs) {  // position w0 + i holds a real segment (padding keys sort last)
+        const int64_t seg = w0 + (int64_t)(kk & 0xFFFFFFFFu);
+        perm[(int64_t)b * segs + s] = (int32_t)seg;
+        ipos[(int64_t)b * segs + seg] = (int32_t)s;
+        if ((i & 31) == 0) ssize[(int64_t)b * nsl + s / 32] = 32u * (0xFFFFFFFFu - (unsigned)(kk >> 32));
+    }
+}
+
+// entry u of the segment at position q (slice q / 32, lane q % 32) goes to soff[slice] + 32 u + lane
+__device__ __forceinline__ int64_t sell_dst(const int64_t *flat_sl, int64_t b, int64_t nsl, int32_t q) {
+    return flat_sl[b * nsl + q / 32] + (q & 31);
+}
+
+// CSR rows -> column-blocked SELL: thread per row, its pieces of block 0, 1, ... in row order
+__global__ void sell_from_csr(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                              const float *__restrict__ val, int64_t rows, int K, const unsigned *__restrict__ cnt,
+                              const int32_t *__restrict__ ipos, const int64_t *__restrict__ flat_sl, int64_t nsl,
+                              int32_t *__restrict__ sidx, float *__restrict__ sval) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t k = row_ptr[r];
+        for (int b = 0; b < K; ++b) {
+            const unsigned len = cnt[(int64_t)b * rows + r];
+            const int64_t d = sell_dst(flat_sl, b, nsl, ipos[(int64_t)b * rows + r]);
+            for (unsigned u = 0; u < len; ++u, ++k) {
+                sidx[d + 32 * (int64_t)u] = col[k];
+                sval[d + 32 * (int64_t)u] = val[k];
+            }
+        }
+    }
+}
+
+// compact blocked segments (flat [K][segs] offsets) -> SELL: thread per (block, segment)
+__global__ void sell_from_flat(const int64_t *__restrict__ flat, const int32_t *__restrict__ idx,
+                               const float *__restrict__ val, int K, int64_t segs, const int32_t *__restrict__ ipos,
+                               const int64_t *__restrict__ flat_sl, int64_t nsl, int32_t *__restrict__ sidx,
+                               float *__restrict__ sval) {
+    const int64_t total = (int64_t)K * segs;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i / segs;
+        const int64_t d = sell_dst(flat_sl, b, nsl, ipos[i]);
+        for (int64_t k = flat[i], u = 0; k < flat[i + 1]; ++k, ++u) {
+            sidx[d + 32 * u] = idx[k];
+            sval[d + 32 * u] = val[k];
         }
     }
 }

@@ -26,6 +26,7 @@
 #include "sparse_kernels.cuh"
 #include "persist_kernels.cuh"
 #include "explicit_kernels.cuh"
+#include "gram_tc.cuh"
 #include <cublas_v2.h>
 
 using namespace tsvd;
@@ -202,7 +203,9 @@ struct tsvd_s {
     int64_t trace_launch = 0;
     // factors (device)
     float *U32 = nullptr;   // m_g x kpad
-    double *V64 = nullptr;  // n x k
+    double *V64 = nullptr;  // n x k (TSVD_OPT_V_PLACEMENT = 1: the device alias of mapped pinned host memory)
+    int v_host = 0;         // TSVD_OPT_V_PLACEMENT: the co-factor V and the initial samples V0 on the host
+    double *V64_h = nullptr, *V0d_h = nullptr;  // their host allocations (v_host)
     double *S64 = nullptr;  // k
     int32_t l_found = 0;
     // vectors / workspaces (device)
@@ -214,9 +217,19 @@ struct tsvd_s {
     int sp_kc = 1, sp_kr = 1;
     int64_t sp_block_opt = 0;  // TSVD_OPT_SPARSE_BLOCK: block width in elements (0 = auto)
     int sp_chunks = 4;         // world > 1: N3's last block in column chunks, each all-reduced at once
+    int grid_nl = 0;           // grid of the carry-only sparse launches (not the last index block)
     double *acc_r = nullptr, *acc_c = nullptr;
     cudaStream_t sp_comm_stream = nullptr;
     std::vector<cudaEvent_t> sp_ev;
+    // sparse out of memory (degree 1, PLACEMENT = 2 with host input): both views' entry arrays in
+    // pinned host memory, each block copied into a q_s-slot device ring before its launch
+    bool sp_stream = false;
+    int32_t *sp_hidx[2] = {}; float *sp_hval[2] = {};
+    std::vector<int64_t> sp_hbase[2];
+    std::vector<void *> sp_ring;
+    std::vector<cudaEvent_t> sp_full, sp_free;
+    int64_t sp_slot_entries = 0;
+    int64_t sp_launch = 0;
     LoopState *st = nullptr;
     CompStat *stats = nullptr;
     LoopState *st_host = nullptr;      // pinned
@@ -251,7 +264,10 @@ struct tsvd_s {
     bool B0_ok = false;
     int pq_l = 0;          // components whose P / Q columns are valid
     double gram_ms = 0.0;  // B0 build time of the last build
-    int gram_blocks = 0;   // n_b of the symmetric task schedule of the last build
+    int gram_blocks = 0;   // n_b of the symmetric task schedule of the last build (tcgen05: tiles computed)
+    int2 *gram_tiles = nullptr;  // tcgen05 Gram: the symmetric tile list
+    int gram_ntiles = 0;
+    int64_t gram_n = -1;
     cublasHandle_t cublas = nullptr;
     PsFn gv_ps = nullptr;  // N7: one persistent cooperative kernel per component (null: unsupported)
     int S_ps = 0;
@@ -358,10 +374,14 @@ static tsvd_status plan(tsvd_t h) {
         if (h->k > kSpMaxL)
             return h->fail(TSVD_ERR_UNSUPPORTED, "sparse path: k = %d > %d (per-thread w partials)", h->k, kSpMaxL);
         const int dyn = (int)((int64_t)std::max(h->k, 1) * (kSpThreads + 1) * sizeof(double));
-        CK(cudaFuncSetAttribute(sp_pass<MODE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
-        int occ = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sp_pass<MODE_Y>, kSpThreads, 0));
+        int occ = 0, occ_nl = 0;
+        CK(cudaFuncSetAttribute(sp_pass<MODE_T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+        // one resident wave each: the last-block kernels (outputs, per-block w / u^2 partials: `parts`
+        // rows) and the leaner carry-only kernels of the other index blocks
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sp_pass<MODE_T, true>, kSpThreads, dyn));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_nl, sp_pass<MODE_Y, false>, kSpThreads, 0));
         h->grid = h->sms * std::max(1, occ);
+        h->grid_nl = h->sms * std::max(1, occ_nl);
         h->parts = h->grid;
         h->T = kSpThreads;
         return set_fin_attrs(h);
@@ -636,11 +656,20 @@ static tsvd_status ensure_alloc(tsvd_t h) {
     };
     cudaError_t e = cudaSuccess;
     if (!e) e = dm((void **)&h->U32, (size_t)mg * h->kpad * sizeof(float));
-    if (!e) e = dm((void **)&h->V64, (size_t)n * h->k * sizeof(double));
+    // the heavy co-factor V (n x k) and the initial samples (k x n): HBM by default; with
+    // TSVD_OPT_V_PLACEMENT = 1 pinned host memory mapped into the device address space ("the
+    // heavy co-factor V is stored on the host"), read by the kernels over the host link
+    auto vm = [&](double **dptr, double **hptr, size_t bytes) -> cudaError_t {
+        if (!h->v_host) return dm((void **)dptr, bytes);
+        cudaError_t ee = cudaHostAlloc((void **)hptr, std::max<size_t>(bytes, 16), cudaHostAllocMapped);
+        if (!ee) ee = cudaHostGetDevicePointer((void **)dptr, *hptr, 0);
+        return ee;
+    };
+    if (!e) e = vm(&h->V64, &h->V64_h, (size_t)n * h->k * sizeof(double));
     if (!e) e = dm((void **)&h->S64, (size_t)h->k * sizeof(double));
     if (!e) e = dm((void **)&h->ybuf, (size_t)2 * h->ystride * sizeof(double));
     if (!e) e = dm((void **)&h->yw, (size_t)(h->wofs + h->kpad) * sizeof(double));
-    if (!e) e = dm((void **)&h->V0d, (size_t)h->k * n * sizeof(double));
+    if (!e) e = vm(&h->V0d, &h->V0d_h, (size_t)h->k * n * sizeof(double));
     if (!e) e = dm((void **)&h->c64, (size_t)h->kpad * sizeof(double));
     if (!e && !h->sparse) e = dm((void **)&h->ypart, (size_t)h->parts * h->ypart_ld * sizeof(double));
     if (!e) e = dm((void **)&h->wpart, (size_t)h->parts * h->kpad * sizeof(double));
@@ -918,46 +947,87 @@ static bool sp_overlap(tsvd_t h) { return h->sparse && h->world > 1 && h->coll =
 // Sparse pass: N2 (rows, one launch per column block) then N3 (columns, one launch per row block);
 // N2 alone for the extraction.  world > 1: N3's last block runs in column chunks and each chunk's
 // [y] (the last one with [w]) is all-reduced on a side stream while the next chunk computes.
+// out of memory (degree 1): before a block launch of view v (0 = CSR, 1 = CSC), copy the block's entries
+// into the next ring slot on the copy stream (slot reuse gated by the kernel that last read it)
+static tsvd_status sp_stage_block(tsvd_t h, cudaStream_t s, int v, int b, SpParams &q) {
+    q.blk_idx = nullptr;
+    q.blk_val = nullptr;
+    if (!h->sp_stream) return TSVD_OK;
+    const int slot = (int)(h->sp_launch++ % (int64_t)h->sp_ring.size());
+    const int64_t e0 = h->sp_hbase[v][b], cnt = h->sp_hbase[v][b + 1] - e0;
+    int32_t *di = (int32_t *)h->sp_ring[slot];
+    float *dv = (float *)(di + h->sp_slot_entries);
+    CK(cudaStreamWaitEvent(h->copy_stream, h->sp_free[slot], 0));
+    CK(cudaMemcpyAsync(di, h->sp_hidx[v] + e0, (size_t)cnt * sizeof(int32_t), cudaMemcpyHostToDevice, h->copy_stream));
+    CK(cudaMemcpyAsync(dv, h->sp_hval[v] + e0, (size_t)cnt * sizeof(float), cudaMemcpyHostToDevice, h->copy_stream));
+    CK(cudaEventRecord(h->sp_full[slot], h->copy_stream));
+    CK(cudaStreamWaitEvent(s, h->sp_full[slot], 0));
+    h->streamed_bytes += cnt * 8;
+    h->streamed_batches += 1;
+    q.blk_idx = di;
+    q.blk_val = dv;
+    q.phase = b;
+    return TSVD_OK;
+}
+static tsvd_status sp_release_block(tsvd_t h, cudaStream_t s) {
+    if (h->sp_stream)
+        CK(cudaEventRecord(h->sp_free[(int)((h->sp_launch - 1) % (int64_t)h->sp_ring.size())], s));
+    return TSVD_OK;
+}
+
 static tsvd_status launch_sparse(tsvd_t h, cudaStream_t s, int l, bool extract) {
     SpParams q = sp_params(h, l);  // one launch per index block (phase), partial sums carried in acc
     q.nphase = h->sp_kc;
     q.acc = h->acc_r;
-    q.seg0 = 0;
-    q.seg1 = h->m_g;
+    q.sl0 = 0;
+    q.sl1 = h->spc.nsl;
     const size_t dyn = (size_t)std::max(l, 0) * (kSpThreads + 1) * sizeof(double);
     for (int b = 0; b < h->sp_kc; ++b) {
         q.phase = b;
-        if (extract) CK(launch_k(h, sp_pass<MODE_U>, h->grid, kSpThreads, 0, s, 1, q));
-        else CK(launch_k(h, sp_pass<MODE_T>, h->grid, kSpThreads, dyn, s, 1, q));
+        TRY(sp_stage_block(h, s, 0, b, q));
+        const bool last = b + 1 == h->sp_kc;
+        if (!last) CK(launch_k(h, extract ? sp_pass<MODE_U, false> : sp_pass<MODE_T, false>, h->grid_nl, kSpThreads,
+                               0, s, 1, q));
+        else if (extract) CK(launch_k(h, sp_pass<MODE_U, true>, h->grid, kSpThreads, 0, s, 1, q));
+        else CK(launch_k(h, sp_pass<MODE_T, true>, h->grid, kSpThreads, dyn, s, 1, q));
+        TRY(sp_release_block(h, s));
     }
     if (!extract) {
         q.nphase = h->sp_kr;
         q.acc = h->acc_c;
-        q.seg0 = 0;
-        q.seg1 = h->n;
+        q.sl0 = 0;
+        q.sl1 = h->spr.nsl;
         for (int b = 0; b + 1 < h->sp_kr; ++b) {
             q.phase = b;
-            CK(launch_k(h, sp_pass<MODE_Y>, h->grid, kSpThreads, 0, s, 1, q));
+            TRY(sp_stage_block(h, s, 1, b, q));
+            CK(launch_k(h, sp_pass<MODE_Y, false>, h->grid_nl, kSpThreads, 0, s, 1, q));
+            TRY(sp_release_block(h, s));
         }
         q.phase = h->sp_kr - 1;
+        TRY(sp_stage_block(h, s, 1, h->sp_kr - 1, q));
         if (!sp_overlap(h)) {
-            CK(launch_k(h, sp_pass<MODE_Y>, h->grid, kSpThreads, 0, s, 1, q));
+            CK(launch_k(h, sp_pass<MODE_Y, true>, h->grid, kSpThreads, 0, s, 1, q));
         } else {
+            // column chunks on sorting-window boundaries (a window's slices hold only its columns)
             const int C = h->sp_chunks;
+            const int64_t nwin = (h->n + kSellW - 1) / kSellW;
             for (int c = 0; c < C; ++c) {
-                const int64_t c0 = h->n * c / C / 32 * 32, c1 = c + 1 == C ? h->n : h->n * (c + 1) / C / 32 * 32;
-                q.seg0 = c0;
-                q.seg1 = c1;
-                CK(launch_k(h, sp_pass<MODE_Y>, h->grid, kSpThreads, 0, s, 1, q));
+                const int64_t w0 = nwin * c / C, w1 = nwin * (c + 1) / C;
+                const int64_t c0 = w0 * kSellW, c1 = c + 1 == C ? h->n : w1 * kSellW;
+                q.sl0 = c0 / 32;
+                q.sl1 = c + 1 == C ? h->spr.nsl : c1 / 32;
+                if (q.sl1 > q.sl0) CK(launch_k(h, sp_pass<MODE_Y, true>, h->grid, kSpThreads, 0, s, 1, q));
                 CK(cudaEventRecord(h->sp_ev[c], s));
                 CK(cudaStreamWaitEvent(h->sp_comm_stream, h->sp_ev[c], 0));
                 const int64_t e1 = c + 1 == C ? h->wofs + h->kpad : c1;  // the last chunk carries w
-                NK(ncclAllReduce(h->yw + c0, h->yw + c0, (size_t)(e1 - c0), ncclDouble, ncclSum, h->comm,
-                                 h->sp_comm_stream));
+                if (e1 > c0)
+                    NK(ncclAllReduce(h->yw + c0, h->yw + c0, (size_t)(e1 - c0), ncclDouble, ncclSum, h->comm,
+                                     h->sp_comm_stream));
             }
             CK(cudaEventRecord(h->sp_ev[C], h->sp_comm_stream));
             CK(cudaStreamWaitEvent(s, h->sp_ev[C], 0));
         }
+        TRY(sp_release_block(h, s));
     }
     CK(cudaGetLastError());
     return TSVD_OK;
@@ -1405,9 +1475,117 @@ static tsvd_status build_graph(tsvd_t h, int l0) {
         if (cb_ != CUBLAS_STATUS_SUCCESS) return h->fail(TSVD_ERR_CUDA, "cuBLAS error %d", (int)cb_); \
     } while (0)
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// The symmetric task schedule at tile granularity: the 128 x 256 tiles (I, J) that hold
+// some (i, j) with j >= i, ordered in groups of 8 I blocks (an A column block is reused by the J
+// tiles of its group; the SMs running at the same time share 8 A blocks and ~20 B blocks in L2)
+static std::vector<int2> gram_tiles(int64_t n) {
+    const int nI = (int)((n + kGtBM - 1) / kGtBM), nJ = (int)((n + kGtBN - 1) / kGtBN);
+    std::vector<int2> t;
+    for (int I0 = 0; I0 < nI; I0 += 8)
+        for (int J = 0; J < nJ; ++J)
+            for (int I = I0; I < std::min(nI, I0 + 8); ++I)
+                if ((int64_t)kGtBN * J + kGtBN - 1 >= (int64_t)kGtBM * I) t.push_back(make_int2(I, J));
+    return t;
+}
+
+// B0 = A^T A (Alg. 3's Gram) on the tcgen05 tensor cores, 3xTF32 (gram_tc.cuh), the
+// symmetric tile schedule, then the strictly-lower triangle mirrored.  TSVD_GRAM_CUBLAS=1 keeps the
+// round-1 path (three cuBLAS TF32 GEMMs of a hi/lo split of A per block product) for A/B timing.
+static tsvd_status build_gram_cublas(tsvd_t h);
+static tsvd_status build_gram(tsvd_t h) {
+    if (getenv("TSVD_GRAM_CUBLAS")) return build_gram_cublas(h);
+    auto t0 = std::chrono::steady_clock::now();
+    const int64_t m = h->m_g, n = h->n;
+    h->ldb0 = round_up(n, 4);
+    if (!h->B0) {
+        cudaError_t e = cudaMalloc((void **)&h->B0, (size_t)n * h->ldb0 * sizeof(float));
+        if (e == cudaErrorMemoryAllocation) return h->fail(TSVD_ERR_NOMEM, "no room for the n x n Gram");
+        CK(e);
+        CK(cudaMemsetAsync(h->B0, 0, (size_t)n * h->ldb0 * sizeof(float), h->stream));
+    }
+    static EncodeTiledFn encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) return h->fail(TSVD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        encode = (EncodeTiledFn)fn;
+    }
+    const bool lo_gmem = getenv("TSVD_GRAM_LO_GMEM") != nullptr;  // A/B: the lo parts as a copy in HBM
+    if (lo_gmem && !h->g_lo) {
+        cudaError_t e = cudaMalloc((void **)&h->g_lo, (size_t)m * h->ld_use * sizeof(float));
+        if (e) {
+            cudaGetLastError();
+            return h->fail(TSVD_ERR_NOMEM, "no room for the lo copy of A");
+        }
+    }
+    if (lo_gmem) {
+        gram_lo_split<<<h->sms * 8, 256, 0, h->stream>>>(h->A_use, m, n, h->ld_use, h->g_lo);
+        CK(cudaGetLastError());
+    }
+    CUtensorMap map, map_lo;
+    const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)m};
+    const cuuint64_t strides[1] = {(cuuint64_t)h->ld_use * sizeof(float)};
+    const cuuint32_t box[2] = {32, (cuuint32_t)kGtBK};
+    const cuuint32_t estr[2] = {1, 1};
+    for (int w = 0; w < 2; ++w) {
+        CUresult r = encode(w ? &map_lo : &map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                            (void *)(w && lo_gmem ? h->g_lo : h->A_use), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return h->fail(TSVD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    }
+    if (h->gram_n != n) {
+        const std::vector<int2> tiles = gram_tiles(n);
+        cudaFree(h->gram_tiles);
+        h->gram_tiles = nullptr;
+        CK(cudaMalloc((void **)&h->gram_tiles, tiles.size() * sizeof(int2)));
+        CK(cudaMemcpy(h->gram_tiles, tiles.data(), tiles.size() * sizeof(int2), cudaMemcpyHostToDevice));
+        h->gram_ntiles = (int)tiles.size();
+        h->gram_n = n;
+        CK(cudaFuncSetAttribute(gram_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGtSmem));
+        CK(cudaFuncSetAttribute(gram_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGtSmem));
+    }
+    GtParams p{};
+    p.tiles = h->gram_tiles;
+    p.ntiles = h->gram_ntiles;
+    p.n = n;
+    p.ldb = h->ldb0;
+    p.m = m;
+    p.B = h->B0;
+    if (lo_gmem) gram_tc<true><<<std::min(h->sms, h->gram_ntiles), kGtThreads, kGtSmem, h->stream>>>(map, map_lo, p);
+    else gram_tc<false><<<std::min(h->sms, h->gram_ntiles), kGtThreads, kGtSmem, h->stream>>>(map, map_lo, p);
+    CK(cudaGetLastError());
+    const int64_t nb = (n + 31) / 32;
+    gram_mirror_lower<<<dim3((unsigned)nb, (unsigned)nb), dim3(32, 8), 0, h->stream>>>(h->B0, n, h->ldb0);
+    CK(cudaGetLastError());
+    h->gram_blocks = h->gram_ntiles;
+    if (const char *dump = getenv("TSVD_GRAM_DUMP")) {  // debug: the Gram as n x ldb fp32 (tests, A/B)
+        CK(cudaStreamSynchronize(h->stream));
+        std::vector<float> hb((size_t)n * h->ldb0);
+        CK(cudaMemcpy(hb.data(), h->B0, hb.size() * sizeof(float), cudaMemcpyDeviceToHost));
+        if (FILE *f = fopen(dump, "wb")) {
+            fwrite(hb.data(), sizeof(float), hb.size(), f);
+            fclose(f);
+        }
+    }
+    // row-partitioned A (world > 1): B0 = sum_g A_g^T A_g, one all-reduce over NVLink (Alg. 3's
+    // Reduce_sum, as an all-reduce so that every rank iterates on the same B0)
+    if (h->world > 1) NK(ncclAllReduce(h->B0, h->B0, (size_t)n * h->ldb0, ncclFloat, ncclSum, h->comm, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->B0_ok = true;
+    h->gram_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return TSVD_OK;
+}
+
 // B0 = A^T A (Alg. 3's Gram) with three TF32 tensor-core GEMMs of the hi/lo split of A:
 // A^T A ~= Ah^T Ah + Ah^T Al + Al^T Ah (fp32-level products; cuBLAS for the plain library GEMM).
-static tsvd_status build_gram(tsvd_t h) {
+static tsvd_status build_gram_cublas(tsvd_t h) {
     auto t0 = std::chrono::steady_clock::now();
     const int64_t m = h->m_g, n = h->n;
     h->ldb0 = round_up(n, 4);
@@ -1900,6 +2078,11 @@ tsvd_status tsvd_set_option(tsvd_t h, int32_t key, int64_t value) {
     case TSVD_OPT_PERSISTENT:
         h->persist_opt = value != 0;
         break;
+    case TSVD_OPT_V_PLACEMENT:
+        if (value < 0 || value > 1) return h->fail(TSVD_ERR_ARG, "V_PLACEMENT is 0 (HBM) or 1 (host)");
+        if (h->allocated) return h->fail(TSVD_ERR_STATE, "V_PLACEMENT must precede the first run");
+        h->v_host = (int)value;
+        break;
     case TSVD_OPT_METHOD:
         if (value < 0 || value > 1) return h->fail(TSVD_ERR_ARG, "METHOD in 0..1");
         h->method = (int)value;
@@ -2075,110 +2258,207 @@ static tsvd_status sp_scan(tsvd_t h, const unsigned *cnt, int64_t len, int64_t *
     return TSVD_OK;
 }
 
-// flat [K][segs] offsets -> SpView (int32 block-local offsets + int64 bases); TSVD_ERR_UNSUPPORTED if
-// a block holds 2^31 or more entries (the caller retries with more blocks)
-static tsvd_status sp_view(tsvd_t h, const int64_t *flat, int K, int64_t segs, SpView *v) {
+// SELL-32-sigma view of one direction from its entry counts cnt[K][segs] (N4b): sort every window's
+// segments by length, slice sizes, scan, int32 block-local slice offsets + int64 block bases, and the
+// padded entry arrays (idx = -1 / val = 0 where a lane's segment is shorter than its slice).  Leaves the
+// flat slice scan (flat_sl, [K][nsl] + 1) and the inverse positions (ipos, [K][segs]) for the caller's
+// scatter (caller frees).  TSVD_ERR_UNSUPPORTED if a block holds 2^31 or more (padded) entries.
+static tsvd_status sell_view(tsvd_t h, const unsigned *cnt, int K, int64_t segs, SpView *v, int64_t **flat_sl,
+                             int32_t **ipos) {
+    const int64_t nsl = (segs + 31) / 32, len = (int64_t)K * nsl;
+    int32_t *perm = nullptr, *soff = nullptr;
+    int64_t *base = nullptr;
+    unsigned *ssize = nullptr;
+    *flat_sl = nullptr;
+    *ipos = nullptr;
+    cudaError_t e = sp_alloc(h, (void **)&perm, (size_t)K * segs * sizeof(int32_t));
+    if (!e) e = cudaMalloc((void **)ipos, std::max<size_t>((size_t)K * segs * sizeof(int32_t), 16));
+    if (!e) e = cudaMalloc((void **)&ssize, std::max<size_t>((size_t)len * sizeof(unsigned), 16));
+    if (!e) e = cudaMalloc((void **)flat_sl, (size_t)(len + 1) * sizeof(int64_t));
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        cudaFree(ssize);
+        return h->fail(TSVD_ERR_NOMEM, "sparse layout: no room for the slice tables");
+    }
+    CK(e);
+    if (segs > 0) {
+        const dim3 grid((unsigned)((segs + kSellW - 1) / kSellW), (unsigned)K);
+        sell_sort<<<grid, kSellW, 0, h->stream>>>(cnt, segs, perm, *ipos, ssize, nsl);
+        CK(cudaGetLastError());
+    }
+    tsvd_status st = sp_scan(h, ssize, len, *flat_sl);
+    cudaFree(ssize);
+    if (st != TSVD_OK) return st;
     std::vector<int64_t> starts(K + 1);
     for (int b = 0; b <= K; ++b)
-        CK(cudaMemcpy(&starts[b], flat + (int64_t)b * segs, sizeof(int64_t), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&starts[b], *flat_sl + (int64_t)b * nsl, sizeof(int64_t), cudaMemcpyDeviceToHost));
     for (int b = 0; b < K; ++b)
         if (starts[b + 1] - starts[b] > (int64_t)INT32_MAX) return TSVD_ERR_UNSUPPORTED;
-    int32_t *off = nullptr;
-    int64_t *base = nullptr;
-    cudaError_t e = sp_alloc(h, (void **)&off, (size_t)K * (segs + 1) * sizeof(int32_t));
+    e = sp_alloc(h, (void **)&soff, (size_t)K * (nsl + 1) * sizeof(int32_t));
     if (!e) e = sp_alloc(h, (void **)&base, (size_t)(K + 1) * sizeof(int64_t));
-    if (e == cudaErrorMemoryAllocation) return h->fail(TSVD_ERR_NOMEM, "sparse block offsets allocation failed");
-    CK(e);
-    flat_to_off<<<h->sms * 8, 256, 0, h->stream>>>(flat, K, segs, off, base);
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(h->stream));
-    v->off = off;
-    v->base = base;
-    v->segs = segs;
-    return TSVD_OK;
-}
-
-// N4b (CSR by column block): K = 1 views the CSR itself (int32 offsets of row_ptr, entries in place);
-// K > 1 copies each row's entries of block b (columns [b bw, (b + 1) bw)) to block b's region
-static tsvd_status build_csr_view(tsvd_t h, int K, int64_t bw) {
-    const int64_t mg = h->m_g, nnz = h->nnz_g;
-    if (K == 1) {
-        TRY(sp_view(h, h->row_ptr_d, 1, mg, &h->spc));  // row_ptr is the flat scan of one block
-        h->spc.idx = h->col_d;
-        h->spc.val = h->val_d;
-        return TSVD_OK;
-    }
-    const int64_t len = (int64_t)K * mg;
-    unsigned *cnt = nullptr;
-    int64_t *flat = nullptr;
-    CK(cudaMalloc((void **)&cnt, (size_t)len * sizeof(unsigned)));
-    CK(cudaMalloc((void **)&flat, (size_t)(len + 1) * sizeof(int64_t)));
-    blk_count<<<h->sms * 8, 256, 0, h->stream>>>(h->row_ptr_d, h->col_d, mg, K, bw, cnt);
-    tsvd_status st = sp_scan(h, cnt, len, flat);
-    cudaFree(cnt);
-    if (st == TSVD_OK) st = sp_view(h, flat, K, mg, &h->spc);
-    if (st != TSVD_OK) {
-        cudaFree(flat);
-        return st;
-    }
-    int32_t *idx = nullptr;
-    float *val = nullptr;
-    cudaError_t e = sp_alloc(h, (void **)&idx, (size_t)nnz * sizeof(int32_t));
-    if (!e) e = sp_alloc(h, (void **)&val, (size_t)nnz * sizeof(float));
-    if (e) {
-        cudaFree(flat);
+    int32_t *sidx = nullptr;
+    float *sval = nullptr;
+    const int64_t total = starts[K];
+    if (!e) e = sp_alloc(h, (void **)&sidx, (size_t)total * sizeof(int32_t));
+    if (!e) e = sp_alloc(h, (void **)&sval, (size_t)total * sizeof(float));
+    if (e == cudaErrorMemoryAllocation) {
         cudaGetLastError();
-        return h->fail(TSVD_ERR_NOMEM, "no room for the column-blocked CSR");
+        return h->fail(TSVD_ERR_NOMEM, "sparse layout: no room for the sliced entries (%lld)", (long long)total);
     }
-    blk_scatter<<<h->sms * 8, 256, 0, h->stream>>>(h->row_ptr_d, h->col_d, h->val_d, mg, K, flat, idx, val);
+    CK(e);
+    CK(cudaMemsetAsync(sidx, 0xFF, (size_t)total * sizeof(int32_t), h->stream));  // padding: idx = -1
+    CK(cudaMemsetAsync(sval, 0, (size_t)total * sizeof(float), h->stream));
+    flat_to_off<<<h->sms * 8, 256, 0, h->stream>>>(*flat_sl, K, nsl, soff, base);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(h->stream));
-    cudaFree(flat);
-    h->spc.idx = idx;
-    h->spc.val = val;
+    v->soff = soff;
+    v->base = base;
+    v->perm = perm;
+    v->idx = sidx;
+    v->val = sval;
+    v->segs = segs;
+    v->nsl = nsl;
     return TSVD_OK;
 }
 
-// N4 (CSC by row block, straight from the CSR): counts per [row block][column], scan, scatter, then
-// each (block, column) segment sorted by row, so the layout — and every result — is deterministic
+// N4b (CSR by column block): per row, the entries of block b (columns [b bw, (b + 1) bw)) are a
+// contiguous piece of the row; counted by binary search, then written straight into the SELL layout
+static tsvd_status build_csr_view(tsvd_t h, int K, int64_t bw) {
+    const int64_t mg = h->m_g;
+    unsigned *cnt = nullptr;
+    CK(cudaMalloc((void **)&cnt, std::max<size_t>((size_t)K * mg * sizeof(unsigned), 16)));
+    blk_count<<<h->sms * 8, 256, 0, h->stream>>>(h->row_ptr_d, h->col_d, mg, K, bw, cnt);
+    CK(cudaGetLastError());
+    int64_t *flat_sl = nullptr;
+    int32_t *ipos = nullptr;
+    tsvd_status st = sell_view(h, cnt, K, mg, &h->spc, &flat_sl, &ipos);
+    if (st == TSVD_OK && h->nnz_g > 0) {
+        sell_from_csr<<<h->sms * 8, 256, 0, h->stream>>>(h->row_ptr_d, h->col_d, h->val_d, mg, K, cnt, ipos, flat_sl,
+                                                         h->spc.nsl, const_cast<int32_t *>(h->spc.idx),
+                                                         const_cast<float *>(h->spc.val));
+        if (cudaGetLastError() != cudaSuccess) st = h->fail(TSVD_ERR_CUDA, "sell_from_csr launch failed");
+        else if (cudaStreamSynchronize(h->stream) != cudaSuccess) st = h->fail(TSVD_ERR_CUDA, "sell_from_csr failed");
+    }
+    cudaFree(cnt);
+    cudaFree(flat_sl);
+    cudaFree(ipos);
+    return st;
+}
+
+// N4 (CSC by row block, straight from the CSR): counts per [row block][column], scan, scatter into a
+// compact temporary, each (block, column) segment sorted by row (so the layout — and every result —
+// is deterministic), then the SELL layout
 static tsvd_status build_csc_view(tsvd_t h, int K, int64_t bw) {
     const int64_t mg = h->m_g, n = h->n, nnz = h->nnz_g;
     const int64_t len = (int64_t)K * n;
-    unsigned *cnt = nullptr;
+    unsigned *cnt = nullptr, *fill = nullptr;
     int64_t *flat = nullptr;
-    CK(cudaMalloc((void **)&cnt, (size_t)len * sizeof(unsigned)));
-    CK(cudaMalloc((void **)&flat, (size_t)(len + 1) * sizeof(int64_t)));
-    CK(cudaMemsetAsync(cnt, 0, (size_t)len * sizeof(unsigned), h->stream));
-    if (nnz) csc_blk_count<<<h->sms * 8, 256, 0, h->stream>>>(h->row_ptr_d, h->col_d, mg, n, bw, cnt);
-    tsvd_status st = sp_scan(h, cnt, len, flat);
-    if (st == TSVD_OK) st = sp_view(h, flat, K, n, &h->spr);
-    if (st != TSVD_OK) {
-        cudaFree(cnt);
-        cudaFree(flat);
-        return st;
-    }
-    int32_t *idx = nullptr;
-    float *val = nullptr;
-    cudaError_t e = sp_alloc(h, (void **)&idx, (size_t)nnz * sizeof(int32_t));
-    if (!e) e = sp_alloc(h, (void **)&val, (size_t)nnz * sizeof(float));
+    int32_t *cidx = nullptr;
+    float *cval = nullptr;
+    cudaError_t e = cudaMalloc((void **)&cnt, std::max<size_t>((size_t)len * sizeof(unsigned), 16));
+    if (!e) e = cudaMalloc((void **)&fill, std::max<size_t>((size_t)len * sizeof(unsigned), 16));
+    if (!e) e = cudaMalloc((void **)&flat, (size_t)(len + 1) * sizeof(int64_t));
+    if (!e) e = cudaMalloc((void **)&cidx, std::max<size_t>((size_t)nnz * sizeof(int32_t), 16));
+    if (!e) e = cudaMalloc((void **)&cval, std::max<size_t>((size_t)nnz * sizeof(float), 16));
+    tsvd_status st = TSVD_OK;
     if (e) {
-        cudaFree(cnt);
-        cudaFree(flat);
         cudaGetLastError();
-        return h->fail(TSVD_ERR_NOMEM, "no room for the row-blocked CSC");
+        st = h->fail(e == cudaErrorMemoryAllocation ? TSVD_ERR_NOMEM : TSVD_ERR_CUDA, "CSC build: %s",
+                     cudaGetErrorString(e));
     }
-    CK(cudaMemsetAsync(cnt, 0, (size_t)len * sizeof(unsigned), h->stream));
-    if (nnz) {
-        csc_blk_scatter<<<h->sms * 8, 256, 0, h->stream>>>(h->row_ptr_d, h->col_d, h->val_d, mg, n, bw, flat, cnt,
-                                                           idx, val);
-        csc_sort<<<h->sms * 8, 256, 0, h->stream>>>(flat, len, idx, val);
+    if (st == TSVD_OK) {
+        cudaMemsetAsync(cnt, 0, (size_t)len * sizeof(unsigned), h->stream);
+        cudaMemsetAsync(fill, 0, (size_t)len * sizeof(unsigned), h->stream);
+        if (nnz) csc_blk_count<<<h->sms * 8, 256, 0, h->stream>>>(h->row_ptr_d, h->col_d, mg, n, bw, cnt);
+        st = sp_scan(h, cnt, len, flat);
     }
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(h->stream));
+    if (st == TSVD_OK && nnz) {
+        csc_blk_scatter<<<h->sms * 8, 256, 0, h->stream>>>(h->row_ptr_d, h->col_d, h->val_d, mg, n, bw, flat, fill,
+                                                           cidx, cval);
+        csc_sort<<<h->sms * 8, 256, 0, h->stream>>>(flat, len, cidx, cval);
+        if (cudaGetLastError() != cudaSuccess) st = h->fail(TSVD_ERR_CUDA, "CSC scatter / sort launch failed");
+    }
+    cudaFree(fill);
+    int64_t *flat_sl = nullptr;
+    int32_t *ipos = nullptr;
+    if (st == TSVD_OK) st = sell_view(h, cnt, K, n, &h->spr, &flat_sl, &ipos);
+    if (st == TSVD_OK && nnz) {
+        sell_from_flat<<<h->sms * 8, 256, 0, h->stream>>>(flat, cidx, cval, K, n, ipos, flat_sl, h->spr.nsl,
+                                                          const_cast<int32_t *>(h->spr.idx),
+                                                          const_cast<float *>(h->spr.val));
+        if (cudaGetLastError() != cudaSuccess) st = h->fail(TSVD_ERR_CUDA, "sell_from_flat launch failed");
+        else if (cudaStreamSynchronize(h->stream) != cudaSuccess) st = h->fail(TSVD_ERR_CUDA, "CSC layout failed");
+    }
     cudaFree(cnt);
     cudaFree(flat);
-    h->spr.idx = idx;
-    h->spr.val = val;
+    cudaFree(cidx);
+    cudaFree(cval);
+    cudaFree(flat_sl);
+    cudaFree(ipos);
+    return st;
+}
+
+static void free_sparse_stream(tsvd_t h) {
+    if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
+    for (int v = 0; v < 2; ++v) {
+        if (h->sp_hidx[v]) cudaFreeHost(h->sp_hidx[v]);
+        if (h->sp_hval[v]) cudaFreeHost(h->sp_hval[v]);
+        h->sp_hidx[v] = nullptr;
+        h->sp_hval[v] = nullptr;
+        h->sp_hbase[v].clear();
+    }
+    for (void *q : h->sp_ring) cudaFree(q);
+    for (cudaEvent_t e : h->sp_full) cudaEventDestroy(e);
+    for (cudaEvent_t e : h->sp_free) cudaEventDestroy(e);
+    h->sp_ring.clear();
+    h->sp_full.clear();
+    h->sp_free.clear();
+    h->sp_stream = false;
+}
+
+// Sparse out of memory (degree 1): move both views' entry arrays (the bulk: 8 bytes per entry)
+// to pinned host memory and size a q_s-slot device ring for the largest index block; every block
+// launch then copies its block first (sp_stage_block).  The slice tables stay in HBM.
+static tsvd_status sp_to_host(tsvd_t h) {
+    int64_t slot = 0;
+    for (int v = 0; v < 2; ++v) {
+        SpView *view = v == 0 ? &h->spc : &h->spr;
+        const int K = v == 0 ? h->sp_kc : h->sp_kr;
+        h->sp_hbase[v].resize(K + 1);
+        CK(cudaMemcpy(h->sp_hbase[v].data(), view->base, (K + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+        const int64_t T = h->sp_hbase[v][K];
+        for (int b = 0; b < K; ++b) slot = std::max(slot, h->sp_hbase[v][b + 1] - h->sp_hbase[v][b]);
+        CK(cudaHostAlloc((void **)&h->sp_hidx[v], std::max<size_t>((size_t)T * 4, 16), cudaHostAllocDefault));
+        CK(cudaHostAlloc((void **)&h->sp_hval[v], std::max<size_t>((size_t)T * 4, 16), cudaHostAllocDefault));
+        CK(cudaMemcpy(h->sp_hidx[v], view->idx, (size_t)T * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(h->sp_hval[v], view->val, (size_t)T * 4, cudaMemcpyDeviceToHost));
+        for (const void *q : {(const void *)view->idx, (const void *)view->val}) {
+            auto it = std::find(h->sp_mem.begin(), h->sp_mem.end(), q);
+            if (it != h->sp_mem.end()) {
+                cudaFree(*it);
+                h->sp_mem.erase(it);
+            }
+        }
+        h->sp_bytes -= 8 * T;
+        view->idx = nullptr;
+        view->val = nullptr;
+    }
+    h->sp_slot_entries = round_up(std::max<int64_t>(slot, 1), 32);
+    for (int q = 0; q < h->qdepth; ++q) {
+        void *p = nullptr;
+        cudaEvent_t ef, eb;
+        cudaError_t e = cudaMalloc(&p, (size_t)h->sp_slot_entries * 8);
+        if (e == cudaErrorMemoryAllocation) return h->fail(TSVD_ERR_NOMEM, "no room for the %d-slot ring", h->qdepth);
+        CK(e);
+        CK(cudaEventCreateWithFlags(&ef, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&eb, cudaEventDisableTiming));
+        h->sp_ring.push_back(p);
+        h->sp_full.push_back(ef);
+        h->sp_free.push_back(eb);
+    }
+    if (!h->copy_stream) CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+    h->sp_stream = true;
+    h->streaming = true;  // host-driven loop (the copies are not captured in the run graph)
     return TSVD_OK;
 }
 
@@ -2191,6 +2471,8 @@ static void free_sparse_views(tsvd_t h) {
 }
 
 static void free_sparse(tsvd_t h) {
+    free_sparse_stream(h);
+    h->streaming = false;
     if (h->csr_owned) {
         cudaFree(h->row_ptr_d);
         cudaFree(h->col_d);
@@ -2303,20 +2585,18 @@ tsvd_status tsvd_set_csr(tsvd_t h, const int64_t *row_ptr, const int32_t *col_id
     h->sp_kr = kr;
     if (kc > 1) CK(cudaMalloc((void **)&h->acc_r, (size_t)mg * sizeof(double)));
     if (kr > 1) CK(cudaMalloc((void **)&h->acc_c, (size_t)n * sizeof(double)));
-    // the CSR view holds a blocked copy when kc > 1: an owned input copy is dropped (2 copies of the
-    // entries remain: the blocked CSR and the blocked CSC); borrowed device arrays are no longer read
-    if (kc > 1 && h->csr_owned) {
+    // both views are the library's own (sliced) copies: an owned input copy is dropped (2 copies of the
+    // entries remain); borrowed device arrays are not read after tsvd_set_csr returns
+    if (h->csr_owned) {
         cudaFree(h->row_ptr_d);
         cudaFree(h->col_d);
         cudaFree(h->val_d);
-        h->row_ptr_d = nullptr;
-        h->col_d = nullptr;
-        h->val_d = nullptr;
         h->csr_owned = false;
-    } else if (h->csr_owned) {  // kc == 1: the view reads col / val in place; row_ptr is replaced
-        cudaFree(h->row_ptr_d);
-        h->row_ptr_d = nullptr;
     }
+    h->row_ptr_d = nullptr;
+    h->col_d = nullptr;
+    h->val_d = nullptr;
+    if (h->placement == 2) TRY(sp_to_host(h));  // out of memory, degree 1
     if (h->world > 1 && !h->sp_comm_stream) {
         CK(cudaStreamCreateWithFlags(&h->sp_comm_stream, cudaStreamNonBlocking));
         for (int c = 0; c <= h->sp_chunks; ++c) {
@@ -2445,7 +2725,8 @@ tsvd_status tsvd_run(tsvd_t h) {
     h->fused_ext_used = !explicit_gram && fuse_ext(h) && h->k - l0 > 1;
     // our kernels per iteration / extraction (NCCL calls not counted)
     int64_t per_pass = 1;
-    if (h->streaming) per_pass = (h->m_res > 0 ? 1 : 0) + (h->m_g - h->m_res + h->batch_rows - 1) / h->batch_rows;
+    if (h->streaming && !h->sparse)
+        per_pass = (h->m_res > 0 ? 1 : 0) + (h->m_g - h->m_res + h->batch_rows - 1) / h->batch_rows;
     if (h->sparse) per_pass = h->sp_kc + h->sp_kr;
     const int64_t per_iter = per_pass + (h->coll == COLL_NONE || h->sparse || fused_reduce(h) ? 1 : 2);
     const int64_t per_ext = (h->sparse ? h->sp_kc : per_pass) + (h->coll == COLL_NONE ? 1 : 2);
@@ -2586,11 +2867,14 @@ tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
     s += tmp;
     snprintf(tmp, sizeof tmp,
              "\"placement\": {\"streaming\": %s, \"resident_rows\": %lld, \"batch_rows\": %lld, \"queue_depth\": %d, "
-             "\"streamed_bytes\": %lld, \"streamed_batches\": %lld, \"device_bytes\": %lld}, ",
+             "\"streamed_bytes\": %lld, \"streamed_batches\": %lld, \"device_bytes\": %lld, \"v_on_host\": %s}, ",
              h->streaming ? "true" : "false", (long long)h->m_res, (long long)h->batch_rows, h->qdepth,
              (long long)h->streamed_bytes, (long long)h->streamed_batches,
-             (long long)(h->work_bytes + (h->mem == TSVD_MEM_DEVICE ? 0 : h->m_res * ((h->n + 3) / 4) * 16) +
-                         (h->streaming ? (int64_t)h->qdepth * h->batch_rows * ((h->n + 3) / 4) * 16 : 0)));
+             (long long)(h->work_bytes + (h->mem == TSVD_MEM_DEVICE || h->sparse ? 0 : h->m_res * ((h->n + 3) / 4) * 16) +
+                         (h->streaming ? (int64_t)h->qdepth * h->batch_rows * ((h->n + 3) / 4) * 16 : 0) +
+                         h->sp_bytes + (h->acc_r ? 8 * h->m_g : 0) + (h->acc_c ? 8 * h->n : 0) +
+                         (int64_t)h->sp_ring.size() * h->sp_slot_entries * 8),
+             h->v_host ? "true" : "false");
     s += tmp;
     snprintf(tmp, sizeof tmp,
              "\"sparse\": {\"enabled\": %s, \"nnz\": %lld, \"csc_build_ms\": %.3f, \"col_blocks\": %d, \"row_blocks\": %d, "
@@ -2667,10 +2951,14 @@ void tsvd_destroy(tsvd_t h) {
         if (h->px_map[r]) cudaIpcCloseMemHandle(h->px_map[r]);
         if (h->gx_map[r]) cudaIpcCloseMemHandle(h->gx_map[r]);
     }
+    if (h->V64_h) cudaFreeHost(h->V64_h);
+    if (h->V0d_h) cudaFreeHost(h->V0d_h);
+    if (h->v_host) h->V64 = h->V0d = nullptr;
     void *dev_ptrs[] = {h->A_own, h->U32, h->V64, h->S64, h->ybuf, h->yw, h->V0d, h->c64, h->ypart,
                         h->wpart, h->part, h->u64, h->sq_part, h->sig2, h->st, h->stats, h->sym, h->gbar,
                         h->trace_d, h->work, h->tl_d, h->vprev32, h->px_mem, h->y32, h->t32, h->At,
-                        h->B0, h->Pm, h->Qm, h->gpart, h->zero64, h->g_hi, h->g_lo, h->pub, h->puby, h->gx_mem};
+                        h->B0, h->Pm, h->Qm, h->gpart, h->zero64, h->g_hi, h->g_lo, h->pub, h->puby, h->gx_mem,
+                        h->gram_tiles};
     if (h->cublas) cublasDestroy(h->cublas);
     if (h->trace_f) fclose(h->trace_f);
     for (void *p : dev_ptrs)

@@ -35,6 +35,7 @@ OPT_ROW_ORDER = 18  # 1 (default): serpentine row order (odd iterations backward
 OPT_PERSISTENT = 19  # 1 (default): a component's iterations in one cooperative kernel (single GPU)
 OPT_SPARSE_BLOCK = 20  # sparse: index-block width (elements) for L2-resident gathers; 0 = auto (set before set_csr)
 OPT_METHOD = 21  # 0 (default): implicit Gram-vector path; 1: explicit Gram (B0 = A^T A once, NEXT#1)
+OPT_V_PLACEMENT = 22  # 0 (default): V and V0 in HBM; 1: pinned host memory read over the host link
 F32, ROW_MAJOR, COL_MAJOR = 0, 0, 1
 
 _lib = None

@@ -188,3 +188,86 @@ def csr_to_dense(row_ptr, col_idx, val, n):
     for r in range(m):
         A[r, col_idx[row_ptr[r]:row_ptr[r + 1]]] = val[row_ptr[r]:row_ptr[r + 1]]
     return A
+
+
+# ---------------------------------------------------------------- stratified random CSR (any size)
+_SM_C0 = 0x9E3779B97F4A7C15
+_SM_C1 = 0xBF58476D1CE4E5B9
+_SM_C2 = 0x94D049BB133111EB
+
+
+def _splitmix64_np(x):
+    """splitmix64 finaliser on uint64 arrays (wrapping arithmetic)."""
+    x = (x + np.uint64(_SM_C0)).astype(np.uint64)
+    x = ((x ^ (x >> np.uint64(30))) * np.uint64(_SM_C1)).astype(np.uint64)
+    x = ((x ^ (x >> np.uint64(27))) * np.uint64(_SM_C2)).astype(np.uint64)
+    return x ^ (x >> np.uint64(31))
+
+
+def _stratified_np(rows, n, d, seed):
+    """Columns / values of the given global rows of ``stratified_csr`` (numpy, uint64 hashing)."""
+    w = n // d
+    r = np.asarray(rows, dtype=np.uint64)[:, None]
+    j = np.arange(d, dtype=np.uint64)[None, :]
+    with np.errstate(over="ignore"):
+        key = (np.uint64(seed) << np.uint64(40)) ^ (r * np.uint64(d) + j)
+        h = _splitmix64_np(key)
+        h2 = _splitmix64_np(h)
+    width = np.where(j.astype(np.int64) == d - 1, n - (d - 1) * w, w).astype(np.uint64)
+    cols = (j * np.uint64(w) + (h >> np.uint64(1)) % width).astype(np.int64)
+    vals = (((h2 >> np.uint64(40)).astype(np.float64) + 1.0) * 2.0 ** -24).astype(np.float32)
+    return cols.astype(np.int32), vals
+
+
+def stratified_csr(m, n, d, seed=1, rows=None):
+    """Paper-like sparse CSR of any size ("randomly generated with a density"), exactly d
+    entries per row: entry j of row r lies in column stratum j (width n // d, the last one takes the
+    remainder) at offset splitmix64(seed << 40 ^ (r d + j)) mod width, so the columns of a row are
+    distinct and sorted, and each column's degree is binomial like uniform sampling; value
+    (splitmix64(h) >> 40 + 1) 2^-24 in (0, 1] (exact in fp32).  Counter-based: any row slab has the
+    content of the full matrix's rows.  Returns (row_ptr int64 from 0, col_idx int32, val fp32)."""
+    g0, g1 = (0, m) if rows is None else rows
+    d = min(d, n)
+    cols, vals = _stratified_np(np.arange(g0, g1), n, d, seed)
+    row_ptr = np.arange(0, (g1 - g0) * d + 1, d, dtype=np.int64)
+    return row_ptr, cols.reshape(-1), vals.reshape(-1)
+
+
+def stratified_csr_device(m, n, d, seed=1, rows=None, device="cuda", chunk=1 << 21):
+    """``stratified_csr`` generated in GPU memory (torch), bit-identical to the numpy version, for slabs
+    too large for host RAM (BASELINE configs[3]: 1e8 x 1e8, 100 per row = 1e10 entries).  Input
+    synthesis only: int64 torch arithmetic wraps like uint64; logical shifts are masked."""
+    import torch
+
+    def s64(c):  # uint64 constant as the int64 with the same bits
+        return c - (1 << 64) if c >= 1 << 63 else c
+
+    def shr(x, k):  # logical shift right of an int64 tensor
+        return (x >> k) & ((1 << (64 - k)) - 1)
+
+    def mix(x):
+        x = x + s64(_SM_C0)
+        x = (x ^ shr(x, 30)) * s64(_SM_C1)
+        x = (x ^ shr(x, 27)) * s64(_SM_C2)
+        return x ^ shr(x, 31)
+
+    g0, g1 = (0, m) if rows is None else rows
+    d = min(d, n)
+    w = n // d
+    nr = g1 - g0
+    col = torch.empty(nr * d, dtype=torch.int32, device=device)
+    val = torch.empty(nr * d, dtype=torch.float32, device=device)
+    j = torch.arange(d, dtype=torch.int64, device=device)[None, :]
+    width = torch.where(j == d - 1, n - (d - 1) * w, w)
+    for r0 in range(g0, g1, chunk):
+        r1 = min(g1, r0 + chunk)
+        r = torch.arange(r0, r1, dtype=torch.int64, device=device)[:, None]
+        h = mix((seed << 40) ^ (r * d + j))
+        h2 = mix(h)
+        c = j * w + torch.remainder(shr(h, 1), width)
+        v = ((shr(h2, 40).to(torch.float64) + 1.0) * 2.0 ** -24).to(torch.float32)
+        col[(r0 - g0) * d:(r1 - g0) * d] = c.reshape(-1).to(torch.int32)
+        val[(r0 - g0) * d:(r1 - g0) * d] = v.reshape(-1)
+        del h, h2, c, v, r
+    row_ptr = torch.arange(0, nr * d + 1, d, dtype=torch.int64, device=device)
+    return row_ptr, col, val

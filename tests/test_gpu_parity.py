@@ -439,20 +439,25 @@ def test_explicit_gram_parity(m, n, k, T):
 
 @pytest.mark.parametrize("nb", [3, 5])
 def test_explicit_gram_symmetric_schedule(nb, monkeypatch):
-    """The Gram's symmetric task schedule (n_b(n_b+1)/2 block products, the strictly-lower
-    blocks mirrored) with ragged blocks: against the oracle and the unblocked Gram."""
+    """The Gram's symmetric task schedule (only the blocks on or above the diagonal are
+    multiplied, the strictly-lower ones mirrored): the tcgen05 kernel's tile schedule (128 x 256 tiles
+    touching the upper triangle) and the round-1 cuBLAS block schedule (n_b(n_b+1)/2 block products,
+    TSVD_GRAM_CUBLAS=1) with ragged blocks — both against the oracle and against each other."""
     m, n, k = 1800, 700, 4
     A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(48, 5.0, 0.75), seed=77)
     V0 = synth.v0_normal(n, k, seed=78)
     ref = oracle.tsvd(A, k, 1e-6, V0)
+    tc = _gpu_tsvd(A, k, 1e-6, V0, method=1)
+    nI, nJ = -(-n // 128), -(-n // 256)
+    want_tiles = sum(1 for I in range(nI) for J in range(nJ) if 256 * J + 255 >= 128 * I)
+    assert tc[0] == P.OK and tc[7]["gram_blocks"] == want_tiles < nI * nJ
+    _assert_parity(A, ref, *tc[1:5], k)
+    monkeypatch.setenv("TSVD_GRAM_CUBLAS", "1")
     monkeypatch.setenv("TSVD_GRAM_NB", str(nb))
     ex = _gpu_tsvd(A, k, 1e-6, V0, method=1)
     assert ex[0] == P.OK and ex[7]["gram_blocks"] == nb
     _assert_parity(A, ref, *ex[1:5], k)
-    monkeypatch.setenv("TSVD_GRAM_NB", "1")  # the unblocked Gram: the same spectrum
-    one = _gpu_tsvd(A, k, 1e-6, V0, method=1)
-    assert one[7]["gram_blocks"] == 1
-    np.testing.assert_allclose(ex[2], one[2], rtol=1e-6)
+    np.testing.assert_allclose(ex[2], tc[2], rtol=1e-6)
 
 
 def test_many_components_fall_back_cleanly():
@@ -467,3 +472,19 @@ def test_many_components_fall_back_cleanly():
     rel = np.abs(S - ref.S) / ref.S
     assert rel.max() <= 1e-4, rel.max()
     assert_tsvd_close(U, S, V, ref, k)  # all 140 u and v pairs, not only sigma
+
+
+@pytest.mark.parametrize("m,n", [(3000, 1000), (4111, 4099), (777, 129), (20000, 16384)])
+def test_explicit_gram_one_product_elementwise(m, n):
+    """One explicit-Gram iteration (fixed T = 1, k = 1): v1 = B0 v0 / ||B0 v0|| with B0 = A^T A from
+    the tcgen05 3xTF32 kernel — a dense, unstructured product that exercises every tile, the
+    ragged edges (n, m not multiples of the 128 x 256 tile or the 16-row K chunk) and the mirror.
+    Elementwise against the oracle's fp64 (A^T (A v0)) direction."""
+    rng = np.random.default_rng(m + n)
+    A = rng.standard_normal((m, n)).astype(np.float32)
+    V0 = synth.v0_normal(n, 1, seed=n)
+    ref = oracle.tsvd(A, 1, 1e-6, V0, fixed_T=1)
+    rc, U, S, V, kf, iters, dots, rep = _gpu_tsvd(A, 1, 1e-6, V0, method=1, fixed_iters=1)
+    assert rc == P.OK and rep["method"] == "explicit-gram" and list(iters) == [1]
+    assert_vec_close(V[:, 0], ref.V[:, 0], 2e-5, "B0 v0 direction")
+    assert abs(S[0] - ref.S[0]) / ref.S[0] <= 1e-5

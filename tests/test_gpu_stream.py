@@ -94,3 +94,70 @@ def test_stream_options_validated():
             t.set_option(key, bad)
         assert ei.value.status == P.ERR_ARG
     t.close()
+
+
+def _sparse_run(rp, ci, va, n, k, V0, T, **opts):
+    m = len(rp) - 1
+    t = P.TSVD(m, n, k, 1e-6)
+    for key, val in opts.items():
+        t.set_option(getattr(P, "OPT_" + key.upper()), val)
+    t.set_option(P.OPT_FIXED_ITERS, T)
+    t.set_init(V0)
+    t.set_csr(rp, ci, va)
+    rc = t.run()
+    U, S, V = t.result()
+    rep = t.report()
+    t.close()
+    return rc, U, S, V, rep
+
+
+@pytest.mark.parametrize("qs,block", [(1, 700), (2, 700), (3, 1500)])
+def test_sparse_out_of_memory_degree1(qs, block):
+    """Sparse OOM degree 1: the sliced entries of both products in pinned host memory, every
+    index block copied into a q_s-slot device ring before its launch — bitwise equal to the resident
+    run (same kernels, same block order), and equal to the oracle at the contract."""
+    m, n, k, T = 5000, 3000, 3, 6
+    rp, ci, va = synth.stratified_csr(m, n, 11, seed=7)
+    V0 = synth.v0_normal(n, k, seed=8)
+    ref = oracle.tsvd_csr(rp, ci, va, n, k, 1e-6, V0, fixed_T=T)
+    res = _sparse_run(rp, ci, va, n, k, V0, T, sparse_block=block)
+    oom = _sparse_run(rp, ci, va, n, k, V0, T, sparse_block=block, placement=P.PLACEMENT_STREAM, queue_depth=qs)
+    pl = oom[4]["placement"]
+    assert oom[0] == P.OK and pl["streaming"] and pl["streamed_batches"] > 0
+    assert pl["device_bytes"] < res[4]["placement"]["device_bytes"]  # the entries left HBM
+    np.testing.assert_array_equal(oom[2], res[2])
+    np.testing.assert_array_equal(oom[3], res[3])
+    np.testing.assert_array_equal(oom[1], res[1])
+    for i in range(k):
+        assert_pair_close(oom[1][:, i], ref.U[:, i], f"u{i}", 1e-6, 1e-5)
+        assert_pair_close(oom[3][:, i], ref.V[:, i], f"v{i}", 1e-6, 1e-5)
+
+
+@pytest.mark.parametrize("sparse", [False, True])
+def test_v_on_host(sparse):
+    """TSVD_OPT_V_PLACEMENT = 1 (the co-factor V on the host): V and V0 in mapped pinned host
+    memory, read by the same kernels over the host link — bitwise equal to the HBM run."""
+    k = 4
+    if sparse:
+        rp, ci, va = synth.stratified_csr(4000, 2500, 9, seed=9)
+        V0 = synth.v0_normal(2500, k, seed=10)
+        a = _sparse_run(rp, ci, va, 2500, k, V0, 5)
+        b = _sparse_run(rp, ci, va, 2500, k, V0, 5, v_placement=1)
+    else:
+        A = synth.known_spectrum_qr(3000, 700, synth.geometric_spectrum(64, 5.0, 0.7), seed=11)
+        V0 = synth.v0_normal(700, k, seed=12)
+        out = []
+        for vp in (0, 1):
+            t = P.TSVD(3000, 700, k, 1e-6)
+            t.set_option(P.OPT_V_PLACEMENT, vp)
+            t.set_init(V0)
+            t.set_dense(torch.from_numpy(A).cuda())
+            rc = t.run()
+            U, S, V = t.result()
+            out.append((rc, U, S, V, t.report()))
+            t.close()
+        a, b = out
+    assert b[4]["placement"]["v_on_host"] is True and a[4]["placement"]["v_on_host"] is False
+    assert b[0] == a[0] == P.OK
+    for x, y in zip(a[1:4], b[1:4]):
+        np.testing.assert_array_equal(x, y)

@@ -35,3 +35,25 @@ def test_uniform_and_csr():
         c = ci[rp[i]:rp[i + 1]]
         assert np.all(np.diff(c) > 0) and c.min() >= 0 and c.max() < 40
     assert va.min() > 0 and va.max() <= 1
+
+
+def test_stratified_csr_host_device_identical():
+    """The counter-based stratified family (configs[3] at 1e10 entries is generated on the device):
+    the torch version (run here on the CPU) equals the numpy one bit for bit, any slab equals the
+    full matrix's rows, columns are distinct, sorted, in range, one per stratum; values in (0, 1]."""
+    import torch
+    m, n, d = 3000, 1001, 7
+    full = synth.stratified_csr(m, n, d, seed=5)
+    part = synth.stratified_csr(m, n, d, seed=5, rows=(1234, 2345))
+    dev = synth.stratified_csr_device(m, n, d, seed=5, rows=(1234, 2345), device="cpu", chunk=100)
+    assert np.array_equal(part[1], full[1][1234 * d:2345 * d]) and np.array_equal(part[2], full[2][1234 * d:2345 * d])
+    for a, b in zip(part, dev):
+        assert np.array_equal(a, b.numpy())
+    cols = full[1].reshape(m, d).astype(np.int64)
+    w = n // d
+    assert np.all(np.diff(cols, axis=1) > 0) and cols.min() >= 0 and cols.max() < n
+    assert np.all(cols[:, :-1] // w == np.arange(d - 1))  # one column per stratum
+    assert full[2].min() > 0 and full[2].max() <= 1
+    # column degrees spread like uniform sampling (mean d m / n)
+    deg = np.bincount(cols.reshape(-1), minlength=n)
+    assert abs(deg.mean() - d * m / n) < 1e-9 and deg.max() < 4 * d * m / n
