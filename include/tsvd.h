@@ -131,12 +131,16 @@ typedef enum {
                                     B0 all-reduced once, iterations row-partitioned over B0 (y rows
                                     exchanged over NVLink inside the kernel; k <= 129, else
                                     replicated).  Pays off when iterations per component are many */
-    TSVD_OPT_V_PLACEMENT = 22    /* 0 (default): the co-factor V (n x k fp64) and the initial samples
+    TSVD_OPT_V_PLACEMENT = 22,   /* 0 (default): the co-factor V (n x k fp64) and the initial samples
                                     (k x n fp64) in HBM; 1: in pinned host memory mapped into the
                                     device address space ("the heavy co-factor V is stored on the
                                     host"): the kernels read and write them over the host link
                                     (frees 16 n k bytes of HBM; every iteration pays n l reads over
                                     PCIe).  Must precede the first run                               */
+    TSVD_OPT_SM_LIMIT = 23       /* run on at most this many SMs (0, default: all).  Lets several
+                                    handles share one GPU at the same time — the in-process ranks of
+                                    tsvd_get_inproc_id, whose persistent grids must be co-resident.
+                                    Must precede tsvd_set_dense / tsvd_set_csr                        */
 } tsvd_option;
 
 /*
@@ -158,12 +162,25 @@ tsvd_status tsvd_create(tsvd_t *out, int64_t m, int64_t n, int32_t k, double eps
  * broadcasts the bytes, e.g. through torch.distributed).  Errors: TSVD_ERR_NCCL. */
 tsvd_status tsvd_get_unique_id(void *out128);
 
+/* tsvd_get_inproc_id — writes a 128-byte id of a NEW in-process rank group into out128: `world`
+ * handles of this one process, each driven from its own host thread (tsvd_run blocks), pass it to
+ * tsvd_set_comm instead of an NCCL id.  The setup-time agreements then use a host rendezvous and
+ * the exchange buffers are the other handles' device pointers; the data path is the multi-GPU
+ * peer path unchanged (row partition; one reduction per iteration, Alg. 4).
+ * Typical use: several ranks on ONE GPU (TSVD_OPT_SM_LIMIT = SMs / world each), which runs the
+ * multi-GPU exchange protocol where only one GPU exists.  Dense input and the peer collective only
+ * (sparse inputs and METHOD = 1 across ranks need NCCL: TSVD_ERR_UNSUPPORTED).  Errors: TSVD_ERR_ARG. */
+tsvd_status tsvd_get_inproc_id(void *out128);
+
 /* tsvd_set_comm — join an NCCL communicator of `world` ranks (this rank = `rank`, world <= 8, one
  * node) on CUDA device `device`, and map every rank's symmetric reduction buffer into this process
  * (CUDA IPC handles exchanged with ncclAllGather) for the in-kernel NVLink all-reduce.  Collective:
  * every rank must call it.  Optional; world == 1 needs no call.  Must precede tsvd_set_dense.
  * If the peer mapping fails the handle falls back to ncclAllReduce (TSVD_OPT_COLLECTIVE = 1).
- * Errors: TSVD_ERR_ARG (bad rank/world, world > 8), TSVD_ERR_NCCL, TSVD_ERR_CUDA. */
+ * With an id from tsvd_get_inproc_id the ranks are handles of this process (no NCCL, see above);
+ * a rank that does not arrive within 60 s fails the others with TSVD_ERR_NCCL.
+ * Errors: TSVD_ERR_ARG (bad rank/world, world > 8, group size mismatch), TSVD_ERR_NCCL,
+ * TSVD_ERR_CUDA, TSVD_ERR_UNSUPPORTED (in-process ranks with COLLECTIVE = 1). */
 tsvd_status tsvd_set_comm(tsvd_t h, int32_t rank, int32_t world, const void *nccl_unique_id, int32_t device);
 
 /* tsvd_set_option — see tsvd_option.  Errors: TSVD_ERR_ARG (unknown key / bad value). */

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtsvd.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("tsvd.cu",)]
-DEPS = SOURCES + [os.path.join(CSRC, "gram_kernels.cuh"), os.path.join(CSRC, "fin_kernels.cuh"), os.path.join(CSRC, "sparse_kernels.cuh"), os.path.join(CSRC, "persist_kernels.cuh"), os.path.join(CSRC, "explicit_kernels.cuh"), os.path.join(ROOT, "include", "tsvd.h")]
+DEPS = SOURCES + [os.path.join(CSRC, "gram_kernels.cuh"), os.path.join(CSRC, "fin_kernels.cuh"), os.path.join(CSRC, "sparse_kernels.cuh"), os.path.join(CSRC, "persist_kernels.cuh"), os.path.join(CSRC, "explicit_kernels.cuh"), os.path.join(CSRC, "gram_tc.cuh"), os.path.join(ROOT, "include", "tsvd.h")]
 
 
 def nccl_dir() -> str:

@@ -13,7 +13,7 @@
 //                         reads fp32 bits and keeps the top 19, i.e. tf32(a) by truncation), written
 //                         to the stage's lo buffers at the same (swizzled) offsets
 //   warps 6-9             epilogue: each finished K chunk of the accumulator (TMEM -> registers) is
-//                         added into the output (see below)
+//                         added into the output, transposed into the lower triangle (gt_fold_t)
 //   warp 1  (one thread)  MMA issuer: per 8-row k-group three tcgen05.mma (M=128, N=256, K=8):
 //                         D += A·B, D += A·B_lo, D += A_lo·B  (3xTF32: hi·hi + hi·lo + lo·hi with
 //                         hi = the truncation the MMA applies itself, so no hi copy exists) into a
@@ -123,6 +123,41 @@ __device__ __forceinline__ bool gt_test(uint64_t *bar, uint32_t parity) {
         : "r"(gt_smem(bar)), "r"(parity)
         : "memory");
     return ok != 0;
+}
+
+// 32 consecutive accumulator columns of this warp's TMEM lane quarter (lane = row), waited for
+__device__ __forceinline__ void gt_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+        "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+        "%30, %31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr)
+        : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Fold one 32-column group of a finished accumulator chunk into B, TRANSPOSED.  Lane = row i of the
+// tile (tcgen05.ld 32x32b: TMEM lane i, registers = columns jc .. jc + 31); it adds C[i][jc + e] into
+// B[jc + e][i] — B is symmetric, so the tile lands in the other triangle and gram_mirror_to_upper
+// completes B afterwards.  For each e the warp's 32 lanes touch 32 consecutive floats of one row of
+// B: one 128-byte line per instruction (the row-per-thread float4 RMW touched 32 lines per instruction
+// and was ~9 % of the single-CTA kernel's L1 wavefronts, ncu).  Each element is read, added (round to
+// nearest) and written by one thread, chunk after chunk in order: deterministic.
+__device__ __forceinline__ void gt_fold_t(float *__restrict__ B, int64_t ldb, int64_t n, int64_t i, int64_t jc,
+                                          const uint32_t (&v)[32], bool first) {
+    if (i >= n) return;
+    float old[32];
+    if (!first) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) old[e] = jc + e < n ? B[(jc + e) * ldb + i] : 0.f;
+    }
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+        if (jc + e < n) B[(jc + e) * ldb + i] = first ? __uint_as_float(v[e]) : old[e] + __uint_as_float(v[e]);
 }
 
 // LO_GMEM: the lo parts come from a precomputed copy in global memory (map_lo, one elementwise pass
@@ -280,7 +315,8 @@ __global__ void __launch_bounds__(kGtThreads, 1)
         }
     } else {  // ===== epilogue (warps 6-9: TMEM lane quarter q = warp % 4, all 256 columns)
         // a finished job's partial sum (rows i0 + 32 q + lane, columns j0 .. j0 + 255) is added in fp32
-        // (round to nearest) into the output — chunk 0 of a tile stores.  The tensor core's own
+        // (round to nearest) into the output, transposed (gt_fold_t) — chunk 0 of a tile stores.  The
+        // tensor core's own
         // accumulation rounds toward zero, so its sums stay short (512 rows) and the chunks of a tile are
         // summed here, in chunk order, while the tensor core fills the other accumulator
         const int q = warp & 3;
@@ -290,7 +326,6 @@ __global__ void __launch_bounds__(kGtThreads, 1)
             (void)kb1;
             const int64_t i = (int64_t)tile.x * kGtBM + 32 * q + lane;
             const int64_t j0 = (int64_t)tile.y * kGtBN;
-            float *row = p.B + i * p.ldb + j0;
             mbar_wait(&dfull[buf], dph[buf]);
             dph[buf] ^= 1u;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -299,40 +334,8 @@ __global__ void __launch_bounds__(kGtThreads, 1)
             for (int c = 0; c < kGtBN / 32; ++c) {
                 uint32_t v[32];
                 const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * kGtBN + 32 * c);
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
-                    "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
-                    "%30, %31}, [%32];"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-                      "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
-                      "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
-                      "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                    : "r"(taddr)
-                    : "memory");
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (i < p.n) {
-                    const int64_t jc = j0 + 32 * c;
-                    float *dst = row + 32 * c;
-                    if (jc + 32 <= p.n) {
-#pragma unroll
-                        for (int e = 0; e < 32; e += 4) {
-                            float4 x = make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]),
-                                                   __uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
-                            if (!first) {
-                                const float4 o = *reinterpret_cast<const float4 *>(dst + e);
-                                x.x += o.x;
-                                x.y += o.y;
-                                x.z += o.z;
-                                x.w += o.w;
-                            }
-                            *reinterpret_cast<float4 *>(dst + e) = x;
-                        }
-                    } else {
-                        for (int e = 0; e < 32; ++e)
-                            if (jc + e < p.n) dst[e] = first ? __uint_as_float(v[e]) : dst[e] + __uint_as_float(v[e]);
-                    }
-                }
+                gt_ld32(taddr, v);
+                gt_fold_t(p.B, p.ldb, p.n, i, j0 + 32 * c, v, first);
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             gt_arrive(&dempty[buf]);
@@ -347,12 +350,240 @@ __global__ void __launch_bounds__(kGtThreads, 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kGtTmemCols) : "memory");
 }
 
-// strictly-lower triangle from the upper one (the symmetric schedule computed every (i, j) with
-// j >= i); 32 x 32 tiles through shared memory, both sides coalesced
-__global__ void gram_mirror_lower(float *__restrict__ B, int64_t n, int64_t ldb) {
+// ---------------------------------------------------------------------------------------------
+// gram_tc2: the same product on CTA pairs (2-CTA cluster, tcgen05.mma.cta_group::2, M = N = 256).
+// The pair owns a 256 x 256 output tile; each CTA stages half of each operand (A: its 128 of the
+// M columns, B: its 128 of the N columns) with the lo parts next to them, so per SM the shared
+// memory carries half the B bytes of the single-CTA kernel per MMA and the L2 feeds 8 KB per 8-row
+// k-group instead of 12 KB for 1.5x the products (smem: TMA write + converter read/write + MMA reads
+// ~125 B/clk at the tensor core's tf32 rate, inside the 128 B/clk port; the single-CTA kernel
+// needed ~190 and ran 1.5x above the MMA floor).  Leader = cluster rank 0:
+//   both CTAs  warp 0: TMA producer (own halves, own `full` barrier); warps 2-5: converter (lo =
+//              a - tf32(a) into own smem, then ONE remote arrive on the leader's `conv`);
+//              warps 6-9: epilogue (own TMEM half = output rows 128 rank .. + 127 of the tile,
+//              then ONE remote arrive on the leader's `dempty`)
+//   leader     warp 1: MMA issuer (waits for both CTAs' converters, issues the pair MMAs, commits
+//              multicast to both CTAs' `empty` / `dfull`)
+// Summation order of the output is that of gram_tc (512-row chunks folded in chunk order).
+constexpr int kG2Tile = 256;                                      // pair tile (M = N = 256)
+constexpr int kG2Half = 128;                                      // columns of each operand per CTA
+constexpr int kG2BK = 16;
+static_assert(kG2BK == kGtBK, "the tensor map box is 32 x kGtBK");
+constexpr int kG2Stages = 6;
+constexpr int kG2HalfBytes = (kG2Half / 32) * kG2BK * 128;        // 8 KB: 4 TMA boxes of 32 x BK
+constexpr int kG2StageBytes = 4 * kG2HalfBytes;                   // A raw, B raw, A lo, B lo: 32 KB
+constexpr int kG2Smem = kG2Stages * kG2StageBytes + 1024 + 256;
+constexpr int kG2ChunkStages = 512 / kG2BK;
+// instruction descriptor: D fp32, A / B tf32, both MN-major, M = 256, N = 256
+constexpr uint32_t kG2Idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
+                              ((uint32_t)(kG2Tile >> 3) << 17) | ((uint32_t)(kG2Tile >> 4) << 24);
+
+__device__ __forceinline__ void g2_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(kG2Idesc), "r"(accumulate)
+        : "memory");
+}
+// arrive on the barrier at this CTA-local offset in both CTAs of the pair once the MMAs issued so
+// far have completed
+__device__ __forceinline__ void g2_commit_both(uint64_t *bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            gt_smem(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+// arrive on the leader's mbarrier (shared::cluster address) with the default .release.cta semantics:
+// the writer threads' fence.proxy.async + the named barrier before it order the stage's smem stores
+// for the tensor core; a .release.cluster arrive compiles to MEMBAR.ALL + ERRBAR and, one per stage
+// on the converter's critical path, measured 12 % of the pair kernel's stall samples (ncu)
+__device__ __forceinline__ void g2_remote_arrive(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void g2_named_sync(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+__global__ void __launch_bounds__(kGtThreads, 1)
+    gram_tc2(const __grid_constant__ CUtensorMap map, const GtParams p) {
+    extern __shared__ unsigned char g2_raw[];
+    unsigned char *smem = (unsigned char *)(((uintptr_t)g2_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kG2Stages * kG2StageBytes);  // own TMA landed
+    uint64_t *conv = full + kG2Stages;    // leader: both converters done with the stage (count 2)
+    uint64_t *empty = conv + kG2Stages;   // the stage's MMAs completed (multicast commit)
+    uint64_t *dfull = empty + kG2Stages;  // [2] accumulator b holds a finished job (multicast commit)
+    uint64_t *dempty = dfull + 2;         // [2] leader: both epilogues folded accumulator b (count 2)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(dempty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int nk = (int)((p.m + kG2BK - 1) / kG2BK);
+    const int nchunk = (nk + kG2ChunkStages - 1) / kG2ChunkStages;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kG2Stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&conv[s], 2);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&dfull[b], 1);
+            mbar_init(&dempty[b], 2);
+        }
+        fence_barrier_init();
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map) : "memory");
+    }
+    if (warp == 1) {  // both CTAs, same warp: one pair allocation (same TMEM address in both)
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(gt_smem(tmem_slot)),
+                     "n"(kGtTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive / multicast
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+#define G2_FOR_JOBS(...)                                                                           \
+    for (int r0 = pair; r0 < p.ntiles; r0 += 2 * npairs) {                                         \
+        const int nt = r0 + npairs < p.ntiles ? 2 : 1;                                             \
+        const int2 tl[2] = {p.tiles[r0], p.tiles[nt == 2 ? r0 + npairs : r0]};                     \
+        for (int k = 0; k < nchunk; ++k)                                                           \
+            for (int u = 0; u < nt; ++u) {                                                         \
+                const int2 tile = tl[u];                                                           \
+                const int kb0 = k * kG2ChunkStages;                                                \
+                const int kb1 = kb0 + kG2ChunkStages < nk ? kb0 + kG2ChunkStages : nk;             \
+                __VA_ARGS__                                                                        \
+            }                                                                                      \
+    }
+
+    if (warp == 0) {
+        if (lane == 0) {  // ===== TMA producer: this CTA's halves of both operands
+            int s = 0;
+            uint32_t ph = 0;
+            G2_FOR_JOBS({
+                const int ca = tile.x * kG2Tile + (int)rank * kG2Half;  // A: M columns of this CTA
+                const int cb = tile.y * kG2Tile + (int)rank * kG2Half;  // B: N columns of this CTA
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    unsigned char *st = smem + (size_t)s * kG2StageBytes;
+                    mbar_arrive_expect_tx(&full[s], (uint32_t)(2 * kG2HalfBytes));
+                    for (int c = 0; c < kG2Half / 32; ++c) {
+                        gt_tma_2d(st + c * (kG2BK * 128), &map, ca + 32 * c, kb * kG2BK, &full[s]);
+                        gt_tma_2d(st + kG2HalfBytes + c * (kG2BK * 128), &map, cb + 32 * c, kb * kG2BK, &full[s]);
+                    }
+                    if (++s == kG2Stages) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            })
+        }
+    } else if (warp == 1) {
+        if (rank == 0 && lane == 0) {  // ===== MMA issuer (leader)
+            int s = 0;
+            uint32_t ph = 0;
+            uint32_t dph[2] = {0u, 0u};
+            int buf = 0;
+            G2_FOR_JOBS({
+                const uint32_t dacc = tmem + (uint32_t)(buf * kG2Tile);
+                mbar_wait(&dempty[buf], dph[buf] ^ 1u);  // both epilogues folded its last job
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&conv[s], ph);  // both CTAs' raw and lo halves are in place
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t base = gt_smem(smem + (size_t)s * kG2StageBytes);
+                    const uint32_t a_raw = base, b_raw = base + kG2HalfBytes;
+                    const uint32_t a_lo = base + 2 * kG2HalfBytes, b_lo = base + 3 * kG2HalfBytes;
+#pragma unroll
+                    for (int kk = 0; kk < kG2BK / 8; ++kk) {
+                        const uint32_t ko = kk * 1024;  // 8 rows of 128 B
+                        const uint64_t da = gt_desc(a_raw + ko, kG2BK * 128, 512);
+                        const uint64_t db = gt_desc(b_raw + ko, kG2BK * 128, 512);
+                        const uint64_t dal = gt_desc(a_lo + ko, kG2BK * 128, 512);
+                        const uint64_t dbl = gt_desc(b_lo + ko, kG2BK * 128, 512);
+                        g2_mma(dacc, da, db, (kb > kb0 || kk > 0) ? 1u : 0u);  // hi·hi
+                        g2_mma(dacc, da, dbl, 1u);                             // hi·lo
+                        g2_mma(dacc, dal, db, 1u);                             // lo·hi
+                    }
+                    g2_commit_both(&empty[s]);  // frees the stage in both CTAs
+                    if (++s == kG2Stages) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+                g2_commit_both(&dfull[buf]);
+                dph[buf] ^= 1u;
+                buf ^= 1;
+            })
+        }
+    } else if (warp < 2 + kGtConvWarps) {  // ===== converter (warps 2-5, both CTAs)
+        const int ct = threadIdx.x - 64;
+        const uint32_t conv_leader = map_to_rank(gt_smem(conv), 0u);
+        int s = 0;
+        uint32_t ph = 0;
+        G2_FOR_JOBS({
+            (void)tile;
+            for (int kb = kb0; kb < kb1; ++kb) {
+                mbar_wait(&full[s], ph);
+                const float4 *raw = reinterpret_cast<const float4 *>(smem + (size_t)s * kG2StageBytes);
+                float4 *lo = reinterpret_cast<float4 *>(smem + (size_t)s * kG2StageBytes + 2 * kG2HalfBytes);
+#pragma unroll 4
+                for (int i = ct; i < (2 * kG2HalfBytes) / 16; i += kGtConv) {
+                    const float4 a = raw[i];
+                    lo[i] = make_float4(gt_lo(a.x), gt_lo(a.y), gt_lo(a.z), gt_lo(a.w));
+                }
+                fence_proxy_async_smem();  // generic stores -> visible to the tensor core (async proxy)
+                g2_named_sync(1, kGtConv);
+                if (ct == 0) g2_remote_arrive(conv_leader + (uint32_t)(s * sizeof(uint64_t)));
+                if (++s == kG2Stages) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+        })
+    } else {  // ===== epilogue (warps 6-9, both CTAs): TMEM lane quarter q, all 256 columns
+        const int q = warp & 3;
+        const int et = threadIdx.x - 32 * (2 + kGtConvWarps);
+        const uint32_t dempty_leader = map_to_rank(gt_smem(dempty), 0u);
+        uint32_t dph[2] = {0u, 0u};
+        int buf = 0;
+        G2_FOR_JOBS({
+            (void)kb1;
+            const int64_t i = (int64_t)tile.x * kG2Tile + (int64_t)rank * kG2Half + 32 * q + lane;
+            const int64_t j0 = (int64_t)tile.y * kG2Tile;
+            mbar_wait(&dfull[buf], dph[buf]);
+            dph[buf] ^= 1u;
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const bool first = k == 0;
+#pragma unroll 1
+            for (int c = 0; c < kG2Tile / 32; ++c) {
+                uint32_t v[32];
+                const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * kG2Tile + 32 * c);
+                gt_ld32(taddr, v);
+                gt_fold_t(p.B, p.ldb, p.n, i, j0 + 32 * c, v, first);
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            g2_named_sync(2, 32 * kGtEpiWarps);
+            if (et == 0) g2_remote_arrive(dempty_leader + (uint32_t)(buf * sizeof(uint64_t)));
+            buf ^= 1;
+        })
+    }
+#undef G2_FOR_JOBS
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    cluster_sync_all();  // no multicast commit or remote arrive may target a CTA that has left
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kGtTmemCols) : "memory");
+}
+
+// strictly-upper triangle from the lower one (the epilogues stored every tile transposed, so every
+// (i, j) with i >= j holds its value); 32 x 32 tiles through shared memory, both sides coalesced
+__global__ void gram_mirror_to_upper(float *__restrict__ B, int64_t n, int64_t ldb) {
     __shared__ float tile[32][33];
-    const int64_t bi = blockIdx.y, bj = blockIdx.x;  // destination tile (rows bi, columns bj), bi >= bj
-    if (bj > bi) return;
+    const int64_t bi = blockIdx.y, bj = blockIdx.x;  // destination tile (rows bi, columns bj), bi <= bj
+    if (bi > bj) return;
     const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
     for (int k = ty; k < 32; k += 8) {  // source: rows of tile (bj, bi)
         const int64_t r = bj * 32 + k, c = bi * 32 + tx;
@@ -360,8 +591,8 @@ __global__ void gram_mirror_lower(float *__restrict__ B, int64_t n, int64_t ldb)
     }
     __syncthreads();
     for (int k = ty; k < 32; k += 8) {
-        const int64_t r = bi * 32 + k, c = bj * 32 + tx;  // B[r][c] = B[c][r] for r > c
-        if (r < n && c < n && r > c) B[r * ldb + c] = tile[tx][k];
+        const int64_t r = bi * 32 + k, c = bj * 32 + tx;  // B[r][c] = B[c][r] for r < c
+        if (r < n && c < n && r < c) B[r * ldb + c] = tile[tx][k];
     }
 }
 

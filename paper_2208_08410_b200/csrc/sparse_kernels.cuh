@@ -36,9 +36,11 @@ constexpr int kSellW = 1024;                    // segments per sorting window (
 
 enum SpMode { MODE_T = 0, MODE_U = 1, MODE_Y = 2 };
 
-// the random gather of the fp32 vector (A/B variants: TSVD_SP_GATHER = 0 read-only path, 1 L2 only)
+// the random gather of the fp32 vector: TSVD_SP_GATHER = 1 (default) ld.global.cg (L2 only, 3.6 % faster
+// per pass on c4n than 0 = the read-only path; ncu: the pass is bound by the L1TEX unit, ~1 scattered
+// sector per clock per SM, and an L1 hit rate of 1 % buys nothing)
 #ifndef TSVD_SP_GATHER
-#define TSVD_SP_GATHER 0
+#define TSVD_SP_GATHER 1
 #endif
 __device__ __forceinline__ float sp_gather(const float *p) {
 #if TSVD_SP_GATHER == 1

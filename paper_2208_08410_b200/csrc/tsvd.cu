@@ -16,7 +16,12 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <climits>
+#include <condition_variable>
 #include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -121,6 +126,25 @@ PsFn pick_ps(int T, int nv, bool full = false) {
     }
 }
 
+// In-process rank groups (tsvd_get_inproc_id): W handles of ONE process, driven from W host threads,
+// typically on one GPU with TSVD_OPT_SM_LIMIT splitting its SMs.  The setup-time agreements (min of
+// an int, every rank's exchange-buffer pointer) go through this host rendezvous instead of NCCL, and
+// the peer buffers are the other handles' device pointers (no IPC); the data path — the persistent
+// kernel's stamped-word exchange and the per-iteration peer all-reduce — is the multi-GPU code as is.
+struct InprocGroup {
+    std::mutex mu;
+    std::condition_variable cv;
+    int world = 0, arrived = 0;
+    unsigned long long gen = 0;
+    std::vector<long long> v;
+    std::vector<void *> p;
+    long long rmin = 0;
+    std::vector<void *> rp;
+};
+std::mutex g_grp_mu;
+std::map<std::string, std::weak_ptr<InprocGroup>> g_grps;
+constexpr char kInprocMagic[16] = "TSVD-INPROC-ID";  // first 16 bytes of an in-process group id
+
 }  // namespace
 
 struct tsvd_s {
@@ -133,6 +157,8 @@ struct tsvd_s {
     cudaStream_t stream = nullptr, body_stream = nullptr;
     int32_t rank = 0, world = 1;
     ncclComm_t comm = nullptr;
+    std::shared_ptr<InprocGroup> grp;       // in-process ranks (instead of comm)
+    int sm_limit = 0;                       // TSVD_OPT_SM_LIMIT (0 = every SM of the device)
     int coll = COLL_NONE;
     int coll_opt = 0;
     double *sym = nullptr;                  // this rank's symmetric buffer (peer path)
@@ -266,6 +292,7 @@ struct tsvd_s {
     double gram_ms = 0.0;  // B0 build time of the last build
     int gram_blocks = 0;   // n_b of the symmetric task schedule of the last build (tcgen05: tiles computed)
     int2 *gram_tiles = nullptr;  // tcgen05 Gram: the symmetric tile list
+    bool gram_pair = false;      // ... of the CTA-pair kernel (256 x 256 tiles)
     int gram_ntiles = 0;
     int64_t gram_n = -1;
     cublasHandle_t cublas = nullptr;
@@ -314,6 +341,8 @@ struct tsvd_s {
     } while (0)
 #define NK(call)                                                                                    \
     do {                                                                                            \
+        if (!h->comm) return h->fail(TSVD_ERR_UNSUPPORTED, "%s: no NCCL communicator (in-process ranks "     \
+                                     "run the peer collective only)", #call);                      \
         ncclResult_t r_ = (call);                                                                   \
         if (r_ != ncclSuccess) return h->fail(TSVD_ERR_NCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
     } while (0)
@@ -523,7 +552,10 @@ static cudaError_t launch_k(tsvd_t h, void (*fn)(KArgs...), int grid, int block,
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[2];
     int na = 0;
-    if (h->pdl_opt) {
+    // PDL lets a successor's CTAs become resident while this kernel runs: with an SM budget shared
+    // by several handles (in-process ranks) that would take SMs another rank's cooperative grid
+    // needs, so it is off under TSVD_OPT_SM_LIMIT
+    if (h->pdl_opt && !h->sm_limit) {
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;
@@ -568,22 +600,105 @@ static tsvd_status reset_state(tsvd_t h) {
     return TSVD_OK;
 }
 
+// ---- setup-time collectives: NCCL across processes, the host rendezvous for in-process ranks
+// every rank contributes (val, ptr); returns the min of val and every rank's ptr in rank order
+// (LLONG_MIN if a rank did not arrive within 60 s)
+static long long grp_exchange(tsvd_t h, long long val, void *ptr, std::vector<void *> *all) {
+    InprocGroup &g = *h->grp;
+    std::unique_lock<std::mutex> lk(g.mu);
+    g.v[h->rank] = val;
+    g.p[h->rank] = ptr;
+    const unsigned long long my = g.gen;
+    if (++g.arrived == g.world) {
+        g.rmin = *std::min_element(g.v.begin(), g.v.end());
+        g.rp = g.p;
+        g.arrived = 0;
+        ++g.gen;
+        g.cv.notify_all();
+    } else if (!g.cv.wait_for(lk, std::chrono::seconds(60), [&] { return g.gen != my; })) {
+        return LLONG_MIN;
+    }
+    if (all) *all = g.rp;
+    return g.rmin;
+}
+
+// In-process ranks share one device: a host API call with an implicit device-wide synchronisation
+// (cudaFree, some allocations) in one rank's thread would wait for another rank's kernel that is
+// spinning for this rank's exchange words.  Every rank finishes its host-side preparation (buffers,
+// graph capture and instantiation) before any rank launches the run.
+static tsvd_status inproc_rendezvous(tsvd_t h) {
+    if (!h->grp) return TSVD_OK;
+    if (grp_exchange(h, 0, nullptr, nullptr) == LLONG_MIN)
+        return h->fail(TSVD_ERR_NCCL, "in-process group: a rank did not arrive within 60 s");
+    return TSVD_OK;
+}
+
+// v = min over the ranks
+static tsvd_status coll_min_int(tsvd_t h, int &v) {
+    if (h->grp) {
+        const long long r = grp_exchange(h, v, nullptr, nullptr);
+        if (r == LLONG_MIN) return h->fail(TSVD_ERR_NCCL, "in-process group: a rank did not arrive within 60 s");
+        v = (int)r;
+        return TSVD_OK;
+    }
+    int *d = nullptr;
+    CK(cudaMalloc((void **)&d, sizeof(int)));
+    CK(cudaMemcpy(d, &v, sizeof(int), cudaMemcpyHostToDevice));
+    NK(ncclAllReduce(d, d, 1, ncclInt, ncclMin, h->comm, h->stream));
+    CK(cudaMemcpyAsync(&v, d, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(d);
+    return TSVD_OK;
+}
+
+// base[r] = rank r's copy of an exchange buffer (mine for r == rank).  Across processes: CUDA IPC
+// handles all-gathered with NCCL and opened (maps[r] records what tsvd_destroy closes; ok = false if
+// an open failed); in-process ranks: the other handles' device pointers themselves
+static tsvd_status coll_share(tsvd_t h, void *mine, void **base, void **maps, bool &ok, std::string &err) {
+    ok = true;
+    if (h->grp) {
+        std::vector<void *> all;
+        if (grp_exchange(h, 0, mine, &all) == LLONG_MIN)
+            return h->fail(TSVD_ERR_NCCL, "in-process group: a rank did not arrive within 60 s");
+        for (int r = 0; r < h->world; ++r) base[r] = all[r];
+        return TSVD_OK;
+    }
+    cudaIpcMemHandle_t hm;
+    CK(cudaIpcGetMemHandle(&hm, mine));
+    char *dbuf = nullptr;
+    CK(cudaMalloc((void **)&dbuf, sizeof(cudaIpcMemHandle_t) * (h->world + 1)));
+    CK(cudaMemcpy(dbuf, &hm, sizeof(hm), cudaMemcpyHostToDevice));
+    NK(ncclAllGather(dbuf, dbuf + sizeof(hm), sizeof(hm), ncclUint8, h->comm, h->stream));
+    std::vector<cudaIpcMemHandle_t> all(h->world);
+    CK(cudaMemcpyAsync(all.data(), dbuf + sizeof(hm), sizeof(hm) * h->world, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(dbuf);
+    for (int r = 0; r < h->world; ++r) {
+        base[r] = mine;
+        if (r == h->rank) continue;
+        void *q = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&q, all[r], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            err = std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e);
+            ok = false;
+            base[r] = nullptr;
+            continue;
+        }
+        maps[r] = q;
+        base[r] = q;
+    }
+    return TSVD_OK;
+}
+
 // Receive areas of the persistent kernel's exchange (N7, world > 1): [2][world][G][SL] doubles +
-// flags [world][G] per rank, IPC handles all-gathered with NCCL.  Needs one column block per CTA
+// flags [world][G] per rank, mapped by coll_share.  Needs one column block per CTA
 // (slice width <= 128 columns); otherwise the multi-GPU run keeps the per-iteration kernels.
 static tsvd_status setup_px(tsvd_t h) {
     // the column slices must be the same on every rank: slice by the smallest grid of any rank
     // (a rank with fewer rows than CTA slots runs a smaller grid)
     int G = h->grid;
-    {
-        int *dg = nullptr;
-        CK(cudaMalloc((void **)&dg, sizeof(int)));
-        CK(cudaMemcpy(dg, &G, sizeof(int), cudaMemcpyHostToDevice));
-        NK(ncclAllReduce(dg, dg, 1, ncclInt, ncclMin, h->comm, h->stream));
-        CK(cudaMemcpyAsync(&G, dg, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
-        cudaFree(dg);
-    }
+    TRY(coll_min_int(h, G));
     const int CW = std::min(h->T_ps, 128);
     const int per = (int)(((h->n + G - 1) / G + 31) / 32 * 32);
     if (per > CW || h->world > kMaxRanks) return TSVD_OK;
@@ -591,50 +706,22 @@ static tsvd_status setup_px(tsvd_t h) {
     const size_t bytes = (size_t)2 * h->world * G * SL * sizeof(ulonglong2);
     CK(cudaMalloc((void **)&h->px_mem, bytes));
     CK(cudaMemset(h->px_mem, 0, bytes));
-    cudaIpcMemHandle_t mine;
-    CK(cudaIpcGetMemHandle(&mine, h->px_mem));
-    char *dbuf = nullptr;
-    CK(cudaMalloc((void **)&dbuf, sizeof(cudaIpcMemHandle_t) * (h->world + 1)));
-    CK(cudaMemcpy(dbuf, &mine, sizeof(mine), cudaMemcpyHostToDevice));
-    NK(ncclAllGather(dbuf, dbuf + sizeof(mine), sizeof(mine), ncclUint8, h->comm, h->stream));
-    std::vector<cudaIpcMemHandle_t> all(h->world);
-    CK(cudaMemcpyAsync(all.data(), dbuf + sizeof(mine), sizeof(mine) * h->world, cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    cudaFree(dbuf);
+    void *base[kMaxRanks] = {};
+    bool ok = true;
+    std::string err;
+    TRY(coll_share(h, h->px_mem, base, h->px_map, ok, err));
+    if (!ok) h->peer_error = "persistent exchange: " + err;
     PxView px{};
     px.world = h->world;
     px.rank = h->rank;
     px.G = G;
     px.per = per;
     px.SL = SL;
-    bool ok = true;
-    for (int r = 0; r < h->world; ++r) {
-        char *base = h->px_mem;
-        if (r != h->rank) {
-            void *q = nullptr;
-            cudaError_t e = cudaIpcOpenMemHandle(&q, all[r], cudaIpcMemLazyEnablePeerAccess);
-            if (e != cudaSuccess) {
-                cudaGetLastError();
-                h->peer_error = std::string("persistent exchange: cudaIpcOpenMemHandle: ") + cudaGetErrorString(e);
-                ok = false;
-                continue;
-            }
-            h->px_map[r] = q;
-            base = (char *)q;
-        }
-        px.rbuf[r] = (ulonglong2 *)base;
-    }
+    for (int r = 0; r < h->world; ++r) px.rbuf[r] = (ulonglong2 *)base[r];
     px.lbuf = (const ulonglong2 *)h->px_mem;
     // every rank must agree, or none uses the persistent exchange
-    int *dflag = nullptr;
-    CK(cudaMalloc((void **)&dflag, sizeof(int)));
-    const int okv = ok ? 1 : 0;
-    CK(cudaMemcpy(dflag, &okv, sizeof(int), cudaMemcpyHostToDevice));
-    NK(ncclAllReduce(dflag, dflag, 1, ncclInt, ncclMin, h->comm, h->stream));
-    int agreed = 0;
-    CK(cudaMemcpyAsync(&agreed, dflag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    cudaFree(dflag);
+    int agreed = ok ? 1 : 0;
+    TRY(coll_min_int(h, agreed));
     h->px = px;
     h->px_ok = agreed == 1;
     return TSVD_OK;
@@ -723,7 +810,7 @@ static tsvd_status ensure_alloc(tsvd_t h) {
 }
 
 // Symmetric buffers for the in-kernel all-reduce: [2 slots x (y | w | ||u||^2)] + flags[world].
-// Every rank cudaMallocs its own, the CUDA IPC handles are all-gathered with NCCL and opened.
+// Every rank cudaMallocs its own; coll_share maps every rank's (CUDA IPC across processes).
 static tsvd_status setup_peer(tsvd_t h) {
     const int64_t wofs = round_up(h->n, 32), sofs = wofs + round_up(h->k, 4);
     const int64_t slot = round_up(sofs + 1, 32);
@@ -731,16 +818,10 @@ static tsvd_status setup_peer(tsvd_t h) {
     const size_t bytes = flag_off + 256;
     CK(cudaMalloc((void **)&h->sym, bytes));
     CK(cudaMemset(h->sym, 0, bytes));
-    cudaIpcMemHandle_t mine;
-    CK(cudaIpcGetMemHandle(&mine, h->sym));
-    char *dbuf = nullptr;
-    CK(cudaMalloc((void **)&dbuf, sizeof(cudaIpcMemHandle_t) * (h->world + 1)));
-    CK(cudaMemcpy(dbuf, &mine, sizeof(mine), cudaMemcpyHostToDevice));
-    NK(ncclAllGather(dbuf, dbuf + sizeof(mine), sizeof(mine), ncclUint8, h->comm, h->stream));
-    std::vector<cudaIpcMemHandle_t> all(h->world);
-    CK(cudaMemcpyAsync(all.data(), dbuf + sizeof(mine), sizeof(mine) * h->world, cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    cudaFree(dbuf);
+    void *base[kMaxRanks] = {};
+    bool ok = true;
+    TRY(coll_share(h, h->sym, base, h->peer_map, ok, h->peer_error));
+    if (!ok) return TSVD_ERR_CUDA;
     PeerView pv{};
     pv.world = h->world;
     pv.rank = h->rank;
@@ -748,22 +829,8 @@ static tsvd_status setup_peer(tsvd_t h) {
     pv.wofs = wofs;
     pv.sofs = sofs;
     for (int r = 0; r < h->world; ++r) {
-        char *base;
-        if (r == h->rank) {
-            base = (char *)h->sym;
-        } else {
-            void *p = nullptr;
-            cudaError_t e = cudaIpcOpenMemHandle(&p, all[r], cudaIpcMemLazyEnablePeerAccess);
-            if (e != cudaSuccess) {
-                cudaGetLastError();
-                h->peer_error = std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e);
-                return TSVD_ERR_CUDA;
-            }
-            h->peer_map[r] = p;
-            base = (char *)p;
-        }
-        pv.buf[r] = (double *)base;
-        pv.rflags[r] = (unsigned *)(base + flag_off) + h->rank;
+        pv.buf[r] = (double *)base[r];
+        pv.rflags[r] = (unsigned *)((char *)base[r] + flag_off) + h->rank;
     }
     pv.flags = (unsigned *)((char *)h->sym + flag_off);
     h->pv = pv;
@@ -1493,6 +1560,18 @@ static std::vector<int2> gram_tiles(int64_t n) {
     return t;
 }
 
+// the same schedule for the CTA-pair kernel: 256 x 256 tiles (I, J) with J >= I, in groups of 4 I
+// blocks (1024 A columns, as above)
+static std::vector<int2> gram_tiles2(int64_t n) {
+    const int nT = (int)((n + kG2Tile - 1) / kG2Tile);
+    std::vector<int2> t;
+    for (int I0 = 0; I0 < nT; I0 += 4)
+        for (int J = I0; J < nT; ++J)
+            for (int I = I0; I < std::min(nT, I0 + 4); ++I)
+                if (J >= I) t.push_back(make_int2(I, J));
+    return t;
+}
+
 // B0 = A^T A (Alg. 3's Gram) on the tcgen05 tensor cores, 3xTF32 (gram_tc.cuh), the
 // symmetric tile schedule, then the strictly-lower triangle mirrored.  TSVD_GRAM_CUBLAS=1 keeps the
 // round-1 path (three cuBLAS TF32 GEMMs of a hi/lo split of A per block product) for A/B timing.
@@ -1540,8 +1619,11 @@ static tsvd_status build_gram(tsvd_t h) {
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return h->fail(TSVD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     }
-    if (h->gram_n != n) {
-        const std::vector<int2> tiles = gram_tiles(n);
+    // default: the CTA-pair kernel (gram_tc2); TSVD_GRAM_TC1=1 (A/B) or LO_GMEM: the single-CTA kernel
+    const bool pair = !lo_gmem && !getenv("TSVD_GRAM_TC1") && h->sms >= 2;
+    if (h->gram_n != n || h->gram_pair != pair) {
+        const std::vector<int2> tiles = pair ? gram_tiles2(n) : gram_tiles(n);
+        h->gram_pair = pair;
         cudaFree(h->gram_tiles);
         h->gram_tiles = nullptr;
         CK(cudaMalloc((void **)&h->gram_tiles, tiles.size() * sizeof(int2)));
@@ -1550,6 +1632,8 @@ static tsvd_status build_gram(tsvd_t h) {
         h->gram_n = n;
         CK(cudaFuncSetAttribute(gram_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGtSmem));
         CK(cudaFuncSetAttribute(gram_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGtSmem));
+        CK(cudaFuncSetAttribute(gram_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, kG2Smem));
+        CK(cudaFuncSetAttribute(gram_tc2, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
     }
     GtParams p{};
     p.tiles = h->gram_tiles;
@@ -1558,11 +1642,29 @@ static tsvd_status build_gram(tsvd_t h) {
     p.ldb = h->ldb0;
     p.m = m;
     p.B = h->B0;
-    if (lo_gmem) gram_tc<true><<<std::min(h->sms, h->gram_ntiles), kGtThreads, kGtSmem, h->stream>>>(map, map_lo, p);
-    else gram_tc<false><<<std::min(h->sms, h->gram_ntiles), kGtThreads, kGtSmem, h->stream>>>(map, map_lo, p);
+    if (pair) {  // one CTA pair per TPC: an even grid of at most one CTA per SM
+        const int G = 2 * std::max(1, std::min(h->sms / 2, h->gram_ntiles));
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(G);
+        cfg.blockDim = dim3(kGtThreads);
+        cfg.dynamicSmemBytes = kG2Smem;
+        cfg.stream = h->stream;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, gram_tc2, map, p));
+    } else if (lo_gmem) {
+        gram_tc<true><<<std::min(h->sms, h->gram_ntiles), kGtThreads, kGtSmem, h->stream>>>(map, map_lo, p);
+    } else {
+        gram_tc<false><<<std::min(h->sms, h->gram_ntiles), kGtThreads, kGtSmem, h->stream>>>(map, map_lo, p);
+    }
     CK(cudaGetLastError());
     const int64_t nb = (n + 31) / 32;
-    gram_mirror_lower<<<dim3((unsigned)nb, (unsigned)nb), dim3(32, 8), 0, h->stream>>>(h->B0, n, h->ldb0);
+    gram_mirror_to_upper<<<dim3((unsigned)nb, (unsigned)nb), dim3(32, 8), 0, h->stream>>>(h->B0, n, h->ldb0);
     CK(cudaGetLastError());
     h->gram_blocks = h->gram_ntiles;
     if (const char *dump = getenv("TSVD_GRAM_DUMP")) {  // debug: the Gram as n x ldb fp32 (tests, A/B)
@@ -1646,49 +1748,23 @@ static tsvd_status build_gram_cublas(tsvd_t h) {
 }
 
 // Explicit Gram, world > 1: exchange areas of the row-partitioned iterations (gb_persist): every
-// rank's [2][n] stamped y words + [2][world][G][2 + 2k] stamped sums, IPC handles all-gathered with
-// NCCL (as setup_px).  On any failure every rank falls back to replicated iterations.
+// rank's [2][n] stamped y words + [2][world][G][2 + 2k] stamped sums, shared as setup_px does.  On
+// any failure every rank falls back to replicated iterations.
 static tsvd_status setup_gx(tsvd_t h) {
     if (h->gx_mem || h->world > kMaxRanks || h->k > 129) return TSVD_OK;
     const size_t ny = (size_t)2 * h->n, ns = (size_t)2 * h->world * h->grid_gb * (2 + 2 * h->k);
     CK(cudaMalloc((void **)&h->gx_mem, (ny + ns) * sizeof(ulonglong2)));
     CK(cudaMemset(h->gx_mem, 0, (ny + ns) * sizeof(ulonglong2)));
-    cudaIpcMemHandle_t mine;
-    CK(cudaIpcGetMemHandle(&mine, h->gx_mem));
-    char *dbuf = nullptr;
-    CK(cudaMalloc((void **)&dbuf, sizeof(cudaIpcMemHandle_t) * (h->world + 1)));
-    CK(cudaMemcpy(dbuf, &mine, sizeof(mine), cudaMemcpyHostToDevice));
-    NK(ncclAllGather(dbuf, dbuf + sizeof(mine), sizeof(mine), ncclUint8, h->comm, h->stream));
-    std::vector<cudaIpcMemHandle_t> all(h->world);
-    CK(cudaMemcpyAsync(all.data(), dbuf + sizeof(mine), sizeof(mine) * h->world, cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    cudaFree(dbuf);
+    void *base[kMaxRanks] = {};
     bool ok = true;
+    std::string err;
+    TRY(coll_share(h, h->gx_mem, base, h->gx_map, ok, err));
     for (int r = 0; r < h->world; ++r) {
-        char *base = h->gx_mem;
-        if (r != h->rank) {
-            void *q = nullptr;
-            cudaError_t e = cudaIpcOpenMemHandle(&q, all[r], cudaIpcMemLazyEnablePeerAccess);
-            if (e != cudaSuccess) {
-                cudaGetLastError();
-                ok = false;
-                continue;
-            }
-            h->gx_map[r] = q;
-            base = (char *)q;
-        }
-        h->gx_y[r] = (ulonglong2 *)base;
-        h->gx_s[r] = (ulonglong2 *)base + ny;
+        h->gx_y[r] = (ulonglong2 *)base[r];
+        h->gx_s[r] = base[r] ? (ulonglong2 *)base[r] + ny : nullptr;
     }
-    int *dflag = nullptr;
-    CK(cudaMalloc((void **)&dflag, sizeof(int)));
-    const int okv = ok ? 1 : 0;
-    CK(cudaMemcpy(dflag, &okv, sizeof(int), cudaMemcpyHostToDevice));
-    NK(ncclAllReduce(dflag, dflag, 1, ncclInt, ncclMin, h->comm, h->stream));
-    int agreed = 0;
-    CK(cudaMemcpyAsync(&agreed, dflag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    cudaFree(dflag);
+    int agreed = ok ? 1 : 0;
+    TRY(coll_min_int(h, agreed));
     h->gx_ok = agreed == 1 && !getenv("TSVD_GX_REPLICATED");  // env: A/B against replicated iterations
     return TSVD_OK;
 }
@@ -1979,6 +2055,24 @@ tsvd_status tsvd_create(tsvd_t *out, int64_t m, int64_t n, int32_t k, double eps
     return TSVD_OK;
 }
 
+tsvd_status tsvd_get_inproc_id(void *out128) {
+    if (!out128) return TSVD_ERR_ARG;
+    static std::mutex mu;
+    static unsigned long long counter = 0;
+    unsigned long long c;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        c = ++counter;
+    }
+    unsigned char id[128] = {};
+    memcpy(id, kInprocMagic, sizeof(kInprocMagic));
+    const unsigned long long t = (unsigned long long)std::chrono::steady_clock::now().time_since_epoch().count();
+    memcpy(id + 16, &c, sizeof(c));
+    memcpy(id + 24, &t, sizeof(t));
+    memcpy(out128, id, sizeof(id));
+    return TSVD_OK;
+}
+
 tsvd_status tsvd_get_unique_id(void *out128) {
     if (!out128) return TSVD_ERR_ARG;
     ncclUniqueId id;
@@ -2001,6 +2095,7 @@ tsvd_status tsvd_set_comm(tsvd_t h, int32_t rank, int32_t world, const void *uid
         if (h->body_stream) cudaStreamDestroy(h->body_stream);
         h->dev = device;
         CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->dev));
+        if (h->sm_limit > 0) h->sms = std::min(h->sms, h->sm_limit);
         CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&h->body_stream, cudaStreamNonBlocking));
     }
@@ -2008,18 +2103,31 @@ tsvd_status tsvd_set_comm(tsvd_t h, int32_t rank, int32_t world, const void *uid
     h->world = world;
     h->coll = COLL_NONE;
     if (world > 1) {
-        ncclUniqueId id;
-        memcpy(&id, uid, sizeof(id));
-        NK(ncclCommInitRank(&h->comm, world, id, rank));
+        if (memcmp(uid, kInprocMagic, sizeof(kInprocMagic)) == 0) {  // in-process ranks (tsvd_get_inproc_id)
+            if (h->coll_opt != 0)
+                return h->fail(TSVD_ERR_UNSUPPORTED, "in-process ranks run the peer collective (COLLECTIVE = 0)");
+            const std::string key((const char *)uid, 128);
+            std::lock_guard<std::mutex> lk(g_grp_mu);
+            std::shared_ptr<InprocGroup> g = g_grps[key].lock();
+            if (!g) {
+                g = std::make_shared<InprocGroup>();
+                g->world = world;
+                g->v.assign(world, 0);
+                g->p.assign(world, nullptr);
+                g_grps[key] = g;
+            }
+            if (g->world != world) return h->fail(TSVD_ERR_ARG, "in-process group of %d ranks, not %d", g->world, world);
+            h->grp = g;
+        } else {
+            ncclUniqueId id;
+            memcpy(&id, uid, sizeof(id));
+            NK(ncclCommInitRank(&h->comm, world, id, rank));
+        }
         // every rank takes part in the handle exchange, then all agree on the collective to use
         const tsvd_status ps = setup_peer(h);
-        int ok = (ps == TSVD_OK) ? 1 : 0, *dok = nullptr;
-        CK(cudaMalloc((void **)&dok, sizeof(int)));
-        CK(cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice));
-        NK(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, h->comm, h->stream));
-        CK(cudaMemcpyAsync(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
-        cudaFree(dok);
+        int ok = (ps == TSVD_OK) ? 1 : 0;
+        TRY(coll_min_int(h, ok));
+        if (!ok && h->grp) return h->fail(TSVD_ERR_CUDA, "in-process group: %s", h->peer_error.c_str());
         h->coll = (ok && h->coll_opt == 0) ? COLL_PEER : COLL_NCCL;
     }
     return TSVD_OK;
@@ -2083,6 +2191,15 @@ tsvd_status tsvd_set_option(tsvd_t h, int32_t key, int64_t value) {
         if (h->allocated) return h->fail(TSVD_ERR_STATE, "V_PLACEMENT must precede the first run");
         h->v_host = (int)value;
         break;
+    case TSVD_OPT_SM_LIMIT: {
+        if (value < 0 || value > INT32_MAX) return h->fail(TSVD_ERR_ARG, "SM_LIMIT must be >= 0");
+        if (h->allocated || h->have_A) return h->fail(TSVD_ERR_STATE, "SM_LIMIT must precede set_dense / set_csr");
+        int dev_sms = 0;
+        CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->dev));
+        h->sm_limit = (int)value;
+        h->sms = value > 0 ? std::min<int>(dev_sms, (int)value) : dev_sms;
+        break;
+    }
     case TSVD_OPT_METHOD:
         if (value < 0 || value > 1) return h->fail(TSVD_ERR_ARG, "METHOD in 0..1");
         h->method = (int)value;
@@ -2494,6 +2611,8 @@ tsvd_status tsvd_set_csr(tsvd_t h, const int64_t *row_ptr, const int32_t *col_id
     if (!h) return TSVD_ERR_ARG;
     if (!row_ptr || nnz < 0 || (nnz > 0 && (!col_idx || !val))) return h->fail(TSVD_ERR_ARG, "NULL CSR array");
     if (h->wide) return h->fail(TSVD_ERR_UNSUPPORTED, "sparse inputs must have m >= n (V-first branch) in this version");
+    if (h->world > 1 && h->grp)
+        return h->fail(TSVD_ERR_UNSUPPORTED, "sparse inputs across in-process ranks (the sparse sum needs NCCL)");
     if (row_begin < 0 || row_end > h->m || row_end <= row_begin)
         return h->fail(TSVD_ERR_SHAPE, "row range [%lld, %lld) outside [0, %lld)", (long long)row_begin,
                        (long long)row_end, (long long)h->m);
@@ -2526,7 +2645,7 @@ tsvd_status tsvd_set_csr(tsvd_t h, const int64_t *row_ptr, const int32_t *col_id
     h->graph_l0 = -1;
     h->streaming = false;
     h->m_res = mg;
-    if (h->world > 1) h->coll = COLL_NCCL;
+    if (h->world > 1) h->coll = COLL_NCCL;  // the length-n vector: ncclAllReduce (bandwidth-bound)
     auto t0 = std::chrono::steady_clock::now();
     if (mem == TSVD_MEM_DEVICE) {
         h->row_ptr_d = const_cast<int64_t *>(row_ptr);
@@ -2657,6 +2776,7 @@ tsvd_status tsvd_gram_apply(tsvd_t h, const double *v, double *y) {
     memcpy(h->vec_host, v, (size_t)n * sizeof(double));
     CK(cudaMemcpyAsync(h->yw, h->vec_host, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
     // y_cur = v (unnormalised), c = S V^T v
+    TRY(inproc_rendezvous(h));
     TRY(launch_fin(h, h->stream, fin_params(h, FIN_LOAD_RAW, l, h->yw, 0ull, 0), SRC_PARTS));
     TRY(launch_gv(h, h->stream, l, false));
     TRY(launch_exchange(h, h->stream, l));
@@ -2705,6 +2825,7 @@ tsvd_status tsvd_run(tsvd_t h) {
         tsvd_status gs = TSVD_OK;
         if (!h->exec || h->graph_l0 != l0) gs = build_graph(h, l0);
         if (gs >= 0) {
+            TRY(inproc_rendezvous(h));
             CK(cudaGraphLaunch(h->exec, h->stream));
             h->loop_mode = use_persist(h) ? "graph-persistent" : "graph-while";
             ran = true;
@@ -2713,7 +2834,10 @@ tsvd_status tsvd_run(tsvd_t h) {
             TRY(reset_state(h));
         }
     }
-    if (!ran) TRY(run_host_loop(h, l0));
+    if (!ran) {
+        TRY(inproc_rendezvous(h));
+        TRY(run_host_loop(h, l0));
+    }
     if (!ran && use_persist(h)) h->loop_mode = h->timing ? "host-persistent+events" : "host-persistent";
     CK(cudaMemcpyAsync(h->stats_host, h->stats, (size_t)h->k * sizeof(CompStat), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
@@ -2862,7 +2986,7 @@ tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
              "\"stage_bytes\": %d, \"run_rows\": %d, \"split\": %d, \"two_T\": %d, \"fused_extract\": %s, \"pdl\": %s, "
              "\"serpentine\": %s}, ",
              h->T, h->NV, h->S, h->cps, h->grid, h->smem, h->stage_bytes, h->run_rows, h->split, h->T_two,
-             h->fused_ext_used ? "true" : "false", h->pdl_opt ? "true" : "false",
+             h->fused_ext_used ? "true" : "false", (h->pdl_opt && !h->sm_limit) ? "true" : "false",
              h->serp_opt && !h->streaming ? "true" : "false");
     s += tmp;
     snprintf(tmp, sizeof tmp,
@@ -2927,7 +3051,9 @@ void tsvd_destroy(tsvd_t h) {
     if (!h) return;
     cudaSetDevice(h->dev);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    if (h->comm) {  // barrier: no peer may still read our symmetric buffer when it is freed
+    if (h->grp) {  // barrier: no rank may still read our exchange buffers when they are freed
+        grp_exchange(h, 0, nullptr, nullptr);
+    } else if (h->comm) {  // barrier: no peer may still read our symmetric buffer when it is freed
         int *d = nullptr;
         if (cudaMalloc((void **)&d, sizeof(int)) == cudaSuccess) {
             ncclAllReduce(d, d, 1, ncclInt32, ncclSum, h->comm, h->stream);

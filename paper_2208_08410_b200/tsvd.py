@@ -36,6 +36,7 @@ OPT_PERSISTENT = 19  # 1 (default): a component's iterations in one cooperative 
 OPT_SPARSE_BLOCK = 20  # sparse: index-block width (elements) for L2-resident gathers; 0 = auto (set before set_csr)
 OPT_METHOD = 21  # 0 (default): implicit Gram-vector path; 1: explicit Gram (B0 = A^T A once, NEXT#1)
 OPT_V_PLACEMENT = 22  # 0 (default): V and V0 in HBM; 1: pinned host memory read over the host link
+OPT_SM_LIMIT = 23  # at most this many SMs (0 = all): several handles (in-process ranks) sharing one GPU
 F32, ROW_MAJOR, COL_MAJOR = 0, 0, 1
 
 _lib = None
@@ -60,6 +61,7 @@ def lib():
         L = ctypes.CDLL(path)
         L.tsvd_create.argtypes = [ctypes.POINTER(_vp), _i64, _i64, _i32, ctypes.c_double, ctypes.c_int, ctypes.c_int]
         L.tsvd_get_unique_id.argtypes = [_vp]
+        L.tsvd_get_inproc_id.argtypes = [_vp]
         L.tsvd_set_comm.argtypes = [_vp, _i32, _i32, _vp, _i32]
         L.tsvd_set_option.argtypes = [_vp, _i32, _i64]
         L.tsvd_set_init.argtypes = [_vp, _vp]
@@ -78,7 +80,7 @@ def lib():
         L.tsvd_last_error.restype = ctypes.c_char_p
         L.tsvd_destroy.argtypes = [_vp]
         L.tsvd_destroy.restype = None
-        for name in ("tsvd_create", "tsvd_get_unique_id", "tsvd_set_comm", "tsvd_set_option", "tsvd_set_init",
+        for name in ("tsvd_create", "tsvd_get_unique_id", "tsvd_get_inproc_id", "tsvd_set_comm", "tsvd_set_option", "tsvd_set_init",
                      "tsvd_set_dense", "tsvd_set_csr", "tsvd_set_factors", "tsvd_gram_apply", "tsvd_run",
                      "tsvd_get_U_S_V", "tsvd_get_info", "tsvd_get_report", "tsvd_time_gram_kernel"):
             getattr(L, name).restype = ctypes.c_int
@@ -113,6 +115,13 @@ def tsvd_create(m, n, k, eps, dtype=F32, layout=ROW_MAJOR):
 def tsvd_get_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     rc = lib().tsvd_get_unique_id(buf)
+    _check(None, rc)
+    return buf.raw
+
+
+def tsvd_get_inproc_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    rc = lib().tsvd_get_inproc_id(buf)
     _check(None, rc)
     return buf.raw
 

@@ -1,0 +1,190 @@
+"""Multi-rank parity on ONE GPU: W in-process ranks (tsvd_get_inproc_id), one host thread each, the
+GPU's SMs split between them (TSVD_OPT_SM_LIMIT = SMs / W).
+
+The ranks own contiguous row slabs (RSVD) — or column slabs of a column-major wide
+matrix (CSVD) — and run the multi-GPU code path unchanged: the persistent kernel's stamped-
+word exchange of the column slices (one reduction of [y_g | w_g] per iteration, Alg. 4)
+or, with OPT_PERSISTENT = 0, the per-iteration peer all-reduce in the finalize kernel.  Only the
+transport differs from a multi-GPU run (same-device stores instead of NVLink stores), so these
+tests pin the exchange protocol — stamps, slice ownership, rank-ordered sums, receive-area layout
+up to 8 ranks, the decisions every rank takes — on a 1-GPU box, where tests/test_gpu_multi.py
+(torchrun, one process per GPU) skips.
+
+Checks: the gathered result against the fp64 oracle at the north-star contract (sigma relative
+1e-4, |cos| >= 1 - 1e-4, elementwise vectors; tests/_parity.py), iteration counts within one (observed
+equal), and bitwise-equal S and V on every rank (every rank sums the same words in the same order).
+"""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected on the GPU box only
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2208_08410_b200 as P  # noqa: E402
+from _parity import assert_tsvd_close  # noqa: E402
+
+
+def _slab(world, rank, m):
+    base, rem = divmod(m, world)
+    r0 = rank * base + min(rank, rem)
+    return r0, r0 + base + (1 if rank < rem else 0)
+
+
+def _run_ranks(A, k, eps, V0, world, col=False, opts=None, timeout=600):
+    """Every rank in its own thread; returns [(rc, U_slab, S, V, kf, iters, report)] in rank order."""
+    m, n = A.shape
+    uid = P.tsvd_get_inproc_id()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    out, errors = [None] * world, []
+
+    def work(r):
+        try:
+            r0, r1 = _slab(world, r, n if col else m)
+            t = P.TSVD(m, n, k, eps, rank=r, world=world, uid=uid, device=0,
+                       layout=P.COL_MAJOR if col else P.ROW_MAJOR)
+            t.set_option(P.OPT_SM_LIMIT, sms // world)
+            for key, val in (opts or {}).items():
+                t.set_option(getattr(P, "OPT_" + key.upper()), val)
+            t.set_init(V0)
+            if col:  # (m, cols) with unit row stride: this rank's columns of the column-major matrix
+                t.set_dense(torch.from_numpy(np.ascontiguousarray(A[:, r0:r1].T)).cuda().t(), r0, r1)
+            else:
+                t.set_dense(torch.from_numpy(np.ascontiguousarray(A[r0:r1])).cuda(), r0, r1)
+            rc = t.run()
+            U, S, V = t.result()
+            kf, iters, _ = t.info()
+            rep = t.report()
+            t.close()
+            out[r] = (rc, U, S, V, kf, np.asarray(iters), rep)
+        except Exception as e:  # reported below; the other ranks time out (60 s) instead of hanging
+            errors.append((r, repr(e)))
+
+    threads = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(world)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join(timeout)
+    assert not errors, errors
+    assert all(o is not None for o in out), "a rank did not finish"
+    return out
+
+
+def _check(A, out, ref, k, col=False, collective="peer-nvlink"):
+    world = len(out)
+    for rc, U, S, V, kf, iters, rep in out:
+        assert rc == P.OK and kf == k, (rc, kf)
+        assert rep["world"] == world and rep["collective"] == collective
+        assert np.all(np.abs(iters[:k] - np.asarray(ref.iters[:k])) <= 1), (iters, ref.iters)
+    for r in range(1, world):  # replicated outputs: bitwise equal on every rank
+        np.testing.assert_array_equal(out[r][2], out[0][2])
+        if col:
+            np.testing.assert_array_equal(out[r][1], out[0][1])  # U replicated, V sharded
+        else:
+            np.testing.assert_array_equal(out[r][3], out[0][3])
+    if col:
+        U, V = out[0][1], np.concatenate([o[3] for o in out])
+    else:
+        U, V = np.concatenate([o[1] for o in out]), out[0][3]
+    assert_tsvd_close(U, out[0][2], V, ref, k)
+
+
+@pytest.mark.parametrize("world,persist", [(2, 1), (2, 0), (4, 1), (8, 1)])
+def test_inproc_ranks_vs_oracle(world, persist):
+    """Row partition at 2, 4 and 8 ranks (the 8-slot receive areas and stamped-word layout of the
+    largest supported world), persistent kernel and per-iteration peer path."""
+    m, n, k, eps = 3001 + 1000 * (world == 8), 517, 5, 1e-8
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(64, 5.0, 0.75), seed=11 + world)
+    V0 = synth.v0_normal(n, k, seed=12)
+    ref = oracle.tsvd(A, k, eps, V0)
+    out = _run_ranks(A, k, eps, V0, world, opts={"persistent": persist})
+    for o in out:
+        assert o[6]["persistent"]["enabled"] == bool(persist)
+    _check(A, out, ref, k)
+
+
+def test_inproc_ranks_max_iter_not_converged():
+    """The cap (reading R5) across ranks: a near-degenerate spectrum, MAX_ITER = 7: every rank
+    returns TSVD_WARN_NOT_CONVERGED with every component at the cap, equal to the oracle's capped run."""
+    m, n, k, eps, cap = 2000, 400, 3, 1e-12, 7
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(64, 5.0, 0.999), seed=5)
+    V0 = synth.v0_normal(n, k, seed=6)
+    ref = oracle.tsvd(A, k, eps, V0, max_iter=cap)
+    assert ref.status == oracle.OR_NOT_CONVERGED and list(ref.iters) == [cap] * k
+    out = _run_ranks(A, k, eps, V0, 2, opts={"max_iter": cap})
+    for rc, U, S, V, kf, iters, rep in out:
+        assert rc == P.WARN_NOT_CONVERGED and kf == k and list(iters) == [cap] * k
+    np.testing.assert_array_equal(out[1][2], out[0][2])
+    U = np.concatenate([o[1] for o in out])
+    assert_tsvd_close(U, out[0][2], out[0][3], ref, k)
+
+
+def test_inproc_wide_column_partition():
+    """CSVD: a wide matrix stored column-major, each rank a column slab (U-first branch,
+    Alg. 1 else-branch P:88-92)."""
+    m, n, k, eps = 517, 3001, 4, 1e-8
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(64, 5.0, 0.75), seed=31)
+    V0 = synth.v0_normal(m, k, seed=32)
+    ref = oracle.tsvd(A, k, eps, V0)
+    out = _run_ranks(A, k, eps, V0, 2, col=True)
+    _check(A, out, ref, k, col=True)
+
+
+def test_inproc_unsupported_paths_fail_loudly():
+    """Sparse inputs across in-process ranks need NCCL's all-reduce: TSVD_ERR_UNSUPPORTED, no hang."""
+    uid = P.tsvd_get_inproc_id()
+    errs = []
+
+    def work(r):
+        try:
+            t = P.TSVD(100, 50, 2, 1e-6, rank=r, world=2, uid=uid, device=0)
+            rp = np.arange(0, 51, dtype=np.int64)
+            try:
+                t.set_csr(rp, np.arange(50, dtype=np.int32) % 50, np.ones(50, np.float32), r * 50, r * 50 + 50)
+            except P.TsvdError as e:
+                errs.append(e.status)
+            t.close()
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join(120)
+    assert errs == [P.ERR_UNSUPPORTED] * 2, errs
+
+
+M2, N2, K2 = 65536, 16384, 16
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_inproc_c2_full_size(world):
+    """BASELINE configs[1] (65536 x 16384, k = 16, eps = 1e-6, the bench's Hadamard input) row-
+    partitioned over in-process ranks: the kernel variant the bench times at n = 16384
+    (gv_persist<256, 16, FULL>) with the cross-rank exchange, against the whole oracle run."""
+    s = 0.8 ** np.arange(32)
+    A = synth.hadamard_lowrank(M2, N2, s, seed=1)
+    V0 = synth.v0_normal(N2, K2, seed=2)
+    ref = _c2_oracle(A, V0)
+    out = _run_ranks(A, K2, 1e-6, V0, world)
+    for o in out:
+        assert o[6]["loop"] == "graph-persistent" and o[6]["persistent"]["enabled"]
+        assert o[6]["persistent"]["NV"] == 16 and o[6]["persistent"]["T"] == 256
+    _check(A, out, ref, K2)
+
+
+_C2 = {}
+
+
+def _c2_oracle(A, V0):
+    if "ref" not in _C2:
+        _C2["ref"] = oracle.tsvd(A, K2, 1e-6, V0)
+    return _C2["ref"]
