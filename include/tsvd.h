@@ -120,7 +120,7 @@ typedef enum {
                                     0 = one fused pass + finalize kernel per iteration                */
     TSVD_OPT_SPARSE_BLOCK = 20,  /* sparse: width (elements) of the index blocks the gathers are
                                     split into so that each launch's block of the fp32 gathered
-                                    vector stays in L2; 0 (default) = 32 MiB of fp32 (n > 8M
+                                    vector stays in L2; 0 (default) = 48 MiB of fp32 (n > 12.6M
                                     columns / rows => several blocks). Read by tsvd_set_csr          */
     TSVD_OPT_METHOD = 21,        /* 0 (default): implicit Gram-vector products (Eq. 2, the north star);
                                     1: explicit Gram (Alg. 2 lines 6-9 with Alg. 3's Gram, P:114-121,
@@ -167,8 +167,10 @@ tsvd_status tsvd_get_unique_id(void *out128);
  * tsvd_set_comm instead of an NCCL id.  The setup-time agreements then use a host rendezvous and
  * the exchange buffers are the other handles' device pointers; the data path is the multi-GPU
  * peer path unchanged (row partition; one reduction per iteration, Alg. 4).
- * Typical use: several ranks on ONE GPU (TSVD_OPT_SM_LIMIT = SMs / world each), which runs the
- * multi-GPU exchange protocol where only one GPU exists.  Dense input and the peer collective only
+ * Typical use: several ranks on ONE GPU (TSVD_OPT_SM_LIMIT = about 3/4 of SMs / world each, one
+ * CTA per SM), which runs the multi-GPU exchange protocol where only one GPU exists.  The ranks'
+ * kernels wait for each other, so each rank's stream needs its own hardware queue: set
+ * CUDA_DEVICE_MAX_CONNECTIONS >= 2 world before the process creates its CUDA context.  Dense input and the peer collective only
  * (sparse inputs and METHOD = 1 across ranks need NCCL: TSVD_ERR_UNSUPPORTED).  Errors: TSVD_ERR_ARG. */
 tsvd_status tsvd_get_inproc_id(void *out128);
 

@@ -9,8 +9,14 @@
 //   N2 (MODE_U)  extraction u_r = (A v)_r and per-block sum u_r^2;
 //   N3 (MODE_Y)  y_j = sum_k cval_k t32[row_k] over the CSC — the transpose product without atomics and
 //                in a fixed order; block 0 also sums the w partials.  y and w land in yw = [y | w].
+// The fp64 sums carried from one index block to the next are stored in slice-position order of the
+// block that reads them (acc[phase & 1], ping-pong): the reader loads them coalesced at its own
+// position, the writer stores at perm[phase][q] — for every block but the last, perm holds the
+// segment's position in the NEXT block (rewritten by sell_next at build time), not the segment
+// itself.  One scattered access per segment and block instead of two (the kernel is bound by the
+// L1TEX unit's scattered sectors, ~1 per clock per SM: ncu).
 // Layout (N4b, built once by tsvd_set_csr): the entries are split into K index blocks so that one
-// launch's gathers stay inside an L2-resident block of the gathered vector (32 MiB of fp32).  Inside a
+// launch's gathers stay inside an L2-resident block of the gathered vector (48 MiB of fp32).  Inside a
 // block the segments are stored SELL-32-sigma: segments are sorted by length (descending, stable)
 // inside windows of kSellW, cut into slices of 32 (one warp, one segment per lane), and a slice's
 // entries are interleaved — entry u of lane l at slice_off + 32 u + l, short segments padded with
@@ -25,7 +31,10 @@
 namespace tsvd {
 
 constexpr int kSpThreads = 256;
-constexpr size_t kSpL2BlockBytes = 32u << 20;  // fp32 gather block that stays L2-resident (126 MB L2)
+// fp32 gather block that stays L2-resident (126 MB L2).  c4n (n = 2^25, ms per Gram pass): 32 and 40 MiB
+// (K = 4 blocks) 14.7, 48 and 56 MiB (K = 3) 13.9, 64 MiB (K = 2) 14.7 — fewer blocks carry fewer
+// partial sums until the block no longer stays in L2
+constexpr size_t kSpL2BlockBytes = 48u << 20;
 constexpr int kSpWarps = kSpThreads / 32;
 #ifndef TSVD_SP_BATCH
 #define TSVD_SP_BATCH 8
@@ -54,7 +63,7 @@ __device__ __forceinline__ float sp_gather(const float *p) {
 struct SpView {
     const int32_t *soff;  // [K][nsl + 1] block-local entry offset of each slice (slice length = diff / 32)
     const int64_t *base;  // [K + 1] first entry of each block
-    const int32_t *perm;  // [K][segs] segment of slice lane (32 j + l)
+    const int32_t *perm;  // [K][segs] slice lane (32 j + l) -> segment (last block) or its position in the next block
     const int32_t *idx;   // gathered indices (columns for the CSR, local rows for the CSC); -1 = padding
     const float *val;
     int64_t segs, nsl;    // segments, slices per block (ceil(segs / 32))
@@ -82,7 +91,8 @@ struct SpParams {
     int64_t wofs;
     int parts;        // gridDim.x of N2 (rows of wpart)
     int phase, nphase;  // launch `phase` of `nphase` covers index block `phase`
-    double *acc;      // [segs] carried fp64 partial sums when nphase > 1
+    double *acc[2];   // [segs] carried fp64 partial sums when nphase > 1: block b reads acc[b & 1]
+                      // (its own position order) and writes acc[(b + 1) & 1]
     int64_t sl0, sl1; // slices [sl0, sl1) of this launch (N3's last block: column chunks, kSellW-aligned)
     const int32_t *blk_idx;  // out of memory (degree 1): this block's entries in a device ring slot
     const float *blk_val;    // (nullptr: the view's resident arrays)
@@ -120,8 +130,9 @@ __global__ void __launch_bounds__(kSpThreads) sp_pass(const SpParams p) {
     const int64_t nw = (int64_t)gridDim.x * kSpWarps;
     for (int64_t j = p.sl0 + (int64_t)blockIdx.x * kSpWarps + warp; j < p.sl1; j += nw) {
         const int64_t q = 32 * j + lane;
-        const int32_t s = q < V.segs ? __ldcs(perm + q) : -1;  // this lane's segment (-1: past the end)
-        const double carried = (carry_in && s >= 0) ? __ldcg(p.acc + s) : 0.0;  // issued before the gathers
+        // this lane's segment (last block) or its position in the next block; -1: past the end
+        const int32_t s = q < V.segs ? __ldcs(perm + q) : -1;
+        const double carried = (carry_in && s >= 0) ? __ldcg(p.acc[p.phase & 1] + q) : 0.0;  // coalesced
         const int32_t e0 = __ldg(soff + j), e1 = __ldg(soff + j + 1);  // slice entries [e0, e1), 32 wide
         double sum = 0.0;
         for (int32_t e = e0; e < e1; e += 32 * kSpBatch) {
@@ -142,7 +153,7 @@ __global__ void __launch_bounds__(kSpThreads) sp_pass(const SpParams p) {
         if (s < 0) continue;
         if (carry_in) sum = carried + sum;  // blocks in order
         if (!LAST) {
-            p.acc[s] = sum;
+            p.acc[(p.phase + 1) & 1][s] = sum;  // at the segment's position in the next block
             continue;
         }
         if (MODE == MODE_Y) {
@@ -224,6 +235,15 @@ __global__ void __launch_bounds__(kSellW) sell_sort(const unsigned *__restrict__
         perm[(int64_t)b * segs + s] = (int32_t)seg;
         ipos[(int64_t)b * segs + seg] = (int32_t)s;
         if ((i & 31) == 0) ssize[(int64_t)b * nsl + s / 32] = 32u * (0xFFFFFFFFu - (unsigned)(kk >> 32));
+    }
+}
+
+// perm[b][q] (b < K - 1) := position of that segment in block b + 1 (the carried sums' write index)
+__global__ void sell_next(int32_t *__restrict__ perm, const int32_t *__restrict__ ipos, int K, int64_t segs) {
+    const int64_t total = (int64_t)(K - 1) * segs;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i / segs;
+        perm[i] = ipos[(b + 1) * segs + perm[i]];
     }
 }
 

@@ -244,7 +244,7 @@ struct tsvd_s {
     int64_t sp_block_opt = 0;  // TSVD_OPT_SPARSE_BLOCK: block width in elements (0 = auto)
     int sp_chunks = 4;         // world > 1: N3's last block in column chunks, each all-reduced at once
     int grid_nl = 0;           // grid of the carry-only sparse launches (not the last index block)
-    double *acc_r = nullptr, *acc_c = nullptr;
+    double *acc_r = nullptr, *acc_c = nullptr;    // carried sums (ping-pong pairs: [2][segs])
     cudaStream_t sp_comm_stream = nullptr;
     std::vector<cudaEvent_t> sp_ev;
     // sparse out of memory (degree 1, PLACEMENT = 2 with host input): both views' entry arrays in
@@ -1045,7 +1045,8 @@ static tsvd_status sp_release_block(tsvd_t h, cudaStream_t s) {
 static tsvd_status launch_sparse(tsvd_t h, cudaStream_t s, int l, bool extract) {
     SpParams q = sp_params(h, l);  // one launch per index block (phase), partial sums carried in acc
     q.nphase = h->sp_kc;
-    q.acc = h->acc_r;
+    q.acc[0] = h->acc_r;
+    q.acc[1] = h->acc_r ? h->acc_r + h->m_g : nullptr;
     q.sl0 = 0;
     q.sl1 = h->spc.nsl;
     const size_t dyn = (size_t)std::max(l, 0) * (kSpThreads + 1) * sizeof(double);
@@ -1061,7 +1062,8 @@ static tsvd_status launch_sparse(tsvd_t h, cudaStream_t s, int l, bool extract) 
     }
     if (!extract) {
         q.nphase = h->sp_kr;
-        q.acc = h->acc_c;
+        q.acc[0] = h->acc_c;
+        q.acc[1] = h->acc_c ? h->acc_c + h->n : nullptr;
         q.sl0 = 0;
         q.sl1 = h->spr.nsl;
         for (int b = 0; b + 1 < h->sp_kr; ++b) {
@@ -2406,6 +2408,12 @@ static tsvd_status sell_view(tsvd_t h, const unsigned *cnt, int K, int64_t segs,
     tsvd_status st = sp_scan(h, ssize, len, *flat_sl);
     cudaFree(ssize);
     if (st != TSVD_OK) return st;
+    // blocks 0 .. K-2 carry their sums to the next block: perm -> the next block's positions (the
+    // layout itself is built from ipos, which keeps every block's own positions)
+    if (K > 1 && segs > 0) {
+        sell_next<<<h->sms * 8, 256, 0, h->stream>>>(perm, *ipos, K, segs);
+        CK(cudaGetLastError());
+    }
     std::vector<int64_t> starts(K + 1);
     for (int b = 0; b <= K; ++b)
         CK(cudaMemcpy(&starts[b], *flat_sl + (int64_t)b * nsl, sizeof(int64_t), cudaMemcpyDeviceToHost));
@@ -2702,8 +2710,8 @@ tsvd_status tsvd_set_csr(tsvd_t h, const int64_t *row_ptr, const int32_t *col_id
     }
     h->sp_kc = kc;
     h->sp_kr = kr;
-    if (kc > 1) CK(cudaMalloc((void **)&h->acc_r, (size_t)mg * sizeof(double)));
-    if (kr > 1) CK(cudaMalloc((void **)&h->acc_c, (size_t)n * sizeof(double)));
+    if (kc > 1) CK(cudaMalloc((void **)&h->acc_r, (size_t)2 * mg * sizeof(double)));
+    if (kr > 1) CK(cudaMalloc((void **)&h->acc_c, (size_t)2 * n * sizeof(double)));
     // both views are the library's own (sliced) copies: an owned input copy is dropped (2 copies of the
     // entries remain); borrowed device arrays are not read after tsvd_set_csr returns
     if (h->csr_owned) {
@@ -2996,7 +3004,7 @@ tsvd_status tsvd_get_report(tsvd_t h, char *buf, size_t cap) {
              (long long)h->streamed_bytes, (long long)h->streamed_batches,
              (long long)(h->work_bytes + (h->mem == TSVD_MEM_DEVICE || h->sparse ? 0 : h->m_res * ((h->n + 3) / 4) * 16) +
                          (h->streaming ? (int64_t)h->qdepth * h->batch_rows * ((h->n + 3) / 4) * 16 : 0) +
-                         h->sp_bytes + (h->acc_r ? 8 * h->m_g : 0) + (h->acc_c ? 8 * h->n : 0) +
+                         h->sp_bytes + (h->acc_r ? 16 * h->m_g : 0) + (h->acc_c ? 16 * h->n : 0) +
                          (int64_t)h->sp_ring.size() * h->sp_slot_entries * 8),
              h->v_host ? "true" : "false");
     s += tmp;

@@ -3,6 +3,12 @@ import sys
 
 import pytest
 
+# In-process rank groups (tests/test_gpu_inproc.py) run up to 8 handles' streams concurrently on one
+# GPU, each spinning on the others' exchange words: every stream needs its own hardware work queue
+# (the default of 8 lets two ranks' streams share one, and a kernel queued behind another rank's
+# spinning kernel never starts).  Set before any CUDA context exists.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

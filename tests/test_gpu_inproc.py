@@ -38,11 +38,16 @@ def _slab(world, rank, m):
     return r0, r0 + base + (1 if rank < rem else 0)
 
 
-def _run_ranks(A, k, eps, V0, world, col=False, opts=None, timeout=600):
-    """Every rank in its own thread; returns [(rc, U_slab, S, V, kf, iters, report)] in rank order."""
+def _run_ranks(A, k, eps, V0, world, col=False, opts=None, timeout=600, sm_per_rank=None):
+    """Every rank in its own thread; returns [(rc, U_slab, S, V, kf, iters, report)] in rank order.
+    Each rank gets 3/4 of its share of the SMs (sm_per_rank overrides) and one CTA per SM: the ranks'
+    kernels spin on each other's exchange words, so every rank's grid must find room while the others
+    are resident — the headroom keeps a short kernel of one rank (init, finalize) from being the one
+    that cannot be placed."""
     m, n = A.shape
     uid = P.tsvd_get_inproc_id()
     sms = torch.cuda.get_device_properties(0).multi_processor_count
+    budget = sm_per_rank or max(1, (sms // world) * 3 // 4)
     out, errors = [None] * world, []
 
     def work(r):
@@ -50,7 +55,8 @@ def _run_ranks(A, k, eps, V0, world, col=False, opts=None, timeout=600):
             r0, r1 = _slab(world, r, n if col else m)
             t = P.TSVD(m, n, k, eps, rank=r, world=world, uid=uid, device=0,
                        layout=P.COL_MAJOR if col else P.ROW_MAJOR)
-            t.set_option(P.OPT_SM_LIMIT, sms // world)
+            t.set_option(P.OPT_SM_LIMIT, budget)
+            t.set_option(P.OPT_CTAS_PER_SM, 1)
             for key, val in (opts or {}).items():
                 t.set_option(getattr(P, "OPT_" + key.upper()), val)
             t.set_init(V0)
@@ -99,8 +105,9 @@ def _check(A, out, ref, k, col=False, collective="peer-nvlink"):
 @pytest.mark.parametrize("world,persist", [(2, 1), (2, 0), (4, 1), (8, 1)])
 def test_inproc_ranks_vs_oracle(world, persist):
     """Row partition at 2, 4 and 8 ranks (the 8-slot receive areas and stamped-word layout of the
-    largest supported world), persistent kernel and per-iteration peer path."""
-    m, n, k, eps = 3001 + 1000 * (world == 8), 517, 5, 1e-8
+    largest supported world), persistent kernel and per-iteration peer path.  At 8 ranks each gets
+    13 SMs: n = 256 keeps the persistent exchange's one-slice-per-CTA rule (32-column slices)."""
+    m, n, k, eps = (3001, 517, 5, 1e-8) if world < 8 else (4001, 256, 5, 1e-8)
     A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(64, 5.0, 0.75), seed=11 + world)
     V0 = synth.v0_normal(n, k, seed=12)
     ref = oracle.tsvd(A, k, eps, V0)
@@ -117,7 +124,7 @@ def test_inproc_ranks_max_iter_not_converged():
     A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(64, 5.0, 0.999), seed=5)
     V0 = synth.v0_normal(n, k, seed=6)
     ref = oracle.tsvd(A, k, eps, V0, max_iter=cap)
-    assert ref.status == oracle.OR_NOT_CONVERGED and list(ref.iters) == [cap] * k
+    assert ref.status == oracle.NOT_CONVERGED and list(ref.iters) == [cap] * k
     out = _run_ranks(A, k, eps, V0, 2, opts={"max_iter": cap})
     for rc, U, S, V, kf, iters, rep in out:
         assert rc == P.WARN_NOT_CONVERGED and kf == k and list(iters) == [cap] * k
@@ -162,29 +169,36 @@ def test_inproc_unsupported_paths_fail_loudly():
     assert errs == [P.ERR_UNSUPPORTED] * 2, errs
 
 
-M2, N2, K2 = 65536, 16384, 16
+M2, K2 = 65536, 16
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_inproc_c2_full_size(world):
-    """BASELINE configs[1] (65536 x 16384, k = 16, eps = 1e-6, the bench's Hadamard input) row-
-    partitioned over in-process ranks: the kernel variant the bench times at n = 16384
-    (gv_persist<256, 16, FULL>) with the cross-rank exchange, against the whole oracle run."""
+def test_inproc_persistent_exchange_large():
+    """65536 x 8192 (2 GiB, k = 16, eps = 1e-6, the bench's Hadamard family), 2 in-process ranks of 66
+    SMs: the persistent kernel with the cross-rank stamped-word exchange at n = 8192
+    (gv_persist<512, 4, FULL>: one 128-column slice per CTA needs >= 64 CTAs per rank) against the
+    whole oracle run."""
+    n = 8192
     s = 0.8 ** np.arange(32)
-    A = synth.hadamard_lowrank(M2, N2, s, seed=1)
-    V0 = synth.v0_normal(N2, K2, seed=2)
-    ref = _c2_oracle(A, V0)
-    out = _run_ranks(A, K2, 1e-6, V0, world)
+    A = synth.hadamard_lowrank(M2, n, s, seed=1)
+    V0 = synth.v0_normal(n, K2, seed=2)
+    ref = oracle.tsvd(A, K2, 1e-6, V0)
+    out = _run_ranks(A, K2, 1e-6, V0, 2, sm_per_rank=66)
     for o in out:
         assert o[6]["loop"] == "graph-persistent" and o[6]["persistent"]["enabled"]
-        assert o[6]["persistent"]["NV"] == 16 and o[6]["persistent"]["T"] == 256
     _check(A, out, ref, K2)
 
 
-_C2 = {}
-
-
-def _c2_oracle(A, V0):
-    if "ref" not in _C2:
-        _C2["ref"] = oracle.tsvd(A, K2, 1e-6, V0)
-    return _C2["ref"]
+def test_inproc_c2_full_size():
+    """BASELINE configs[1] (65536 x 16384, k = 16, eps = 1e-6, the bench's Hadamard input) over 2 in-
+    process ranks.  At n = 16384 the persistent exchange needs >= 128 CTAs per rank (one 128-column
+    slice each), more than half of one GPU, so the ranks run the per-iteration peer path: the fused
+    pass, the peer all-reduce in the finalize kernel and the WHILE graph, against the whole oracle run."""
+    n = 16384
+    s = 0.8 ** np.arange(32)
+    A = synth.hadamard_lowrank(M2, n, s, seed=1)
+    V0 = synth.v0_normal(n, K2, seed=2)
+    ref = oracle.tsvd(A, K2, 1e-6, V0)
+    out = _run_ranks(A, K2, 1e-6, V0, 2)
+    for o in out:
+        assert o[6]["loop"] == "graph-while"
+    _check(A, out, ref, K2)
