@@ -26,8 +26,10 @@
  *   - Input pointers are BORROWED: they must stay valid and unmodified until the call that
  *     consumes them (tsvd_run / tsvd_gram_apply) returns.  Outputs are copied into caller-owned
  *     buffers.  The handle owns every device buffer, stream, graph and communicator it creates.
- *   - A handle is not thread-safe; one host thread per handle.  One handle per GPU per process.
- *   - Multi-GPU, one process per GPU.  Row partition (RSVD/HSVD, row-major tall A):
+ *   - A handle is not thread-safe; one host thread per handle.  One handle per GPU per process,
+ *     except the ranks of an in-process group (tsvd_get_inproc_id), which share a GPU.
+ *   - Multi-GPU, one process per GPU, or in-process ranks (tsvd_get_inproc_id: the
+ *     same code path with every rank a handle of one process).  Row partition (RSVD/HSVD, row-major tall A):
  *     each rank owns rows [row_begin, row_end) of A and of U; S and V are replicated.  Column
  *     partition (CSVD, column-major wide A): each rank owns columns [row_begin, row_end)
  *     of A and those rows of V; S and U are replicated.  Every rank calls every function with
@@ -124,8 +126,8 @@ typedef enum {
                                     columns / rows => several blocks). Read by tsvd_set_csr          */
     TSVD_OPT_METHOD = 21,        /* 0 (default): implicit Gram-vector products (Eq. 2, the north star);
                                     1: explicit Gram (Alg. 2 lines 6-9 with Alg. 3's Gram, P:114-121,
-                                    P:220-249): B0 = A^T A once (TF32x3 tensor-core GEMMs over the
-                                    symmetric block schedule of P:348), then per iteration
+                                    P:220-249): B0 = A^T A once (a tcgen05 3xTF32 kernel on CTA
+                                    pairs over the symmetric tile schedule of P:348), then per iteration
                                     y = B0 v - P c - V g with P = A^T U, Q = U^T U (exact deflation,
                                     no U^T U = I assumption); dense, resident, n <= 16384.  World > 1:
                                     B0 all-reduced once, iterations row-partitioned over B0 (y rows
