@@ -578,6 +578,253 @@ __global__ void __launch_bounds__(kGtThreads, 1)
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kGtTmemCols) : "memory");
 }
 
+// ---------------------------------------------------------------------------------------------
+// gram_tc3: the CTA-pair product with the A operand in TENSOR MEMORY.  gram_tc2 is shared-memory
+// bound (~127 of 128 B/clk per SM: TMA writes, converter reads/writes, and the tensor core reading
+// both operands of three MMAs).  Here each CTA's converter reads its A half (M columns) once from a
+// plain (unswizzled) shared-memory tile, and writes A and its lo part into a 4-slot TMEM ring with
+// tcgen05.st; all three MMAs take A from TMEM (tcgen05.mma ... [d], [a_tmem], b_desc), so the
+// shared-memory operand traffic is B only (raw twice, lo once).  TMEM: 2 accumulators of N = 192
+// columns + 4 slots x 32 columns of A = 512.  Tiles are 256 (M) x 192 (N), those touching j >= i.
+constexpr int kG3M = 256, kG3N = 192;                              // pair tile
+constexpr int kG3AHalf = 128, kG3BHalf = 96;                       // per-CTA operand columns
+constexpr int kG3BK = 16;
+static_assert(kG3BK == kGtBK, "the swizzled tensor map box is 32 x kGtBK");
+constexpr int kG3Stages = 8;
+constexpr int kG3ABytes = kG3AHalf * kG3BK * 4;                    // 8 KB plain [k][m]
+constexpr int kG3BBytes = (kG3BHalf / 32) * kG3BK * 128;           // 6 KB: 3 swizzled boxes of 32 x BK
+constexpr int kG3StageBytes = kG3ABytes + 2 * kG3BBytes;           // A raw, B raw, B lo: 20 KB
+constexpr int kG3Smem = kG3Stages * kG3StageBytes + 1024 + 512;
+constexpr int kG3Slots = 4;                                        // TMEM A ring (stages)
+constexpr int kG3SlotCols = 2 * (kG3BK / 8) * 8;                   // raw + lo per 8-row k-group: 32
+constexpr int kG3AccCols = kG3N;                                   // one accumulator
+constexpr int kG3RingCol = 2 * kG3AccCols;                         // 384: A ring after the two accumulators
+static_assert(kG3RingCol + kG3Slots * kG3SlotCols <= 512, "TMEM budget");
+constexpr int kG3ChunkStages = 512 / kG3BK;
+// instruction descriptor: D fp32, A / B tf32, A from TMEM (K-major), B MN-major, M = 256, N = 192
+constexpr uint32_t kG3Idesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
+                              ((uint32_t)(kG3N >> 3) << 17) | ((uint32_t)(kG3M >> 4) << 24);
+
+__device__ __forceinline__ void g3_mma(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(db), "r"(kG3Idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void g3_st16(uint32_t taddr, const float (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16};" ::"r"(taddr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+        "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+        "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
+        "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])),
+        "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(kGtThreads, 1)
+    gram_tc3(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_a, const GtParams p) {
+    extern __shared__ unsigned char g3_raw[];
+    unsigned char *smem = (unsigned char *)(((uintptr_t)g3_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kG3Stages * kG3StageBytes);  // own TMA landed
+    uint64_t *conv = full + kG3Stages;      // leader: both CTAs' B lo + TMEM A slot written (count 2)
+    uint64_t *empty = conv + kG3Stages;     // the stage's MMAs completed (multicast commit): smem stage free
+    uint64_t *tfree = empty + kG3Stages;    // [slots] the TMEM A slot's MMAs completed (multicast commit)
+    uint64_t *dfull = tfree + kG3Slots;     // [2] accumulator b holds a finished job (multicast commit)
+    uint64_t *dempty = dfull + 2;           // [2] leader: both epilogues folded accumulator b (count 2)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(dempty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int nk = (int)((p.m + kG3BK - 1) / kG3BK);
+    const int nchunk = (nk + kG3ChunkStages - 1) / kG3ChunkStages;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kG3Stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&conv[s], 2);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < kG3Slots; ++s) mbar_init(&tfree[s], 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&dfull[b], 1);
+            mbar_init(&dempty[b], 2);
+        }
+        fence_barrier_init();
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(gt_smem(tmem_slot)),
+                     "n"(kGtTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    cluster_sync_all();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+#define G3_FOR_JOBS(...)                                                                           \
+    for (int r0 = pair; r0 < p.ntiles; r0 += 2 * npairs) {                                         \
+        const int nt = r0 + npairs < p.ntiles ? 2 : 1;                                             \
+        const int2 tl[2] = {p.tiles[r0], p.tiles[nt == 2 ? r0 + npairs : r0]};                     \
+        for (int k = 0; k < nchunk; ++k)                                                           \
+            for (int u = 0; u < nt; ++u) {                                                         \
+                const int2 tile = tl[u];                                                           \
+                const int kb0 = k * kG3ChunkStages;                                                \
+                const int kb1 = kb0 + kG3ChunkStages < nk ? kb0 + kG3ChunkStages : nk;             \
+                __VA_ARGS__                                                                        \
+            }                                                                                      \
+    }
+
+    if (warp == 0) {
+        if (lane == 0) {  // ===== TMA producer: A half (plain), B half (swizzled)
+            int s = 0;
+            uint32_t ph = 0;
+            G3_FOR_JOBS({
+                const int ca = tile.x * kG3M + (int)rank * kG3AHalf;
+                const int cb = tile.y * kG3N + (int)rank * kG3BHalf;
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    unsigned char *st = smem + (size_t)s * kG3StageBytes;
+                    mbar_arrive_expect_tx(&full[s], (uint32_t)(kG3ABytes + kG3BBytes));
+                    gt_tma_2d(st, &map_a, ca, kb * kG3BK, &full[s]);
+                    for (int c = 0; c < kG3BHalf / 32; ++c)
+                        gt_tma_2d(st + kG3ABytes + c * (kG3BK * 128), &map_b, cb + 32 * c, kb * kG3BK, &full[s]);
+                    if (++s == kG3Stages) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            })
+        }
+    } else if (warp == 1) {
+        if (rank == 0 && lane == 0) {  // ===== MMA issuer (leader)
+            int s = 0, slot = 0;
+            uint32_t ph = 0;
+            uint32_t dph[2] = {0u, 0u};
+            int buf = 0;
+            G3_FOR_JOBS({
+                const uint32_t dacc = tmem + (uint32_t)(buf * kG3AccCols);
+                mbar_wait(&dempty[buf], dph[buf] ^ 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&conv[s], ph);  // both CTAs: B lo in smem, A raw / lo in TMEM slot
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t b_raw = gt_smem(smem + (size_t)s * kG3StageBytes + kG3ABytes);
+                    const uint32_t b_lo = b_raw + kG3BBytes;
+                    const uint32_t ta = tmem + (uint32_t)(kG3RingCol + slot * kG3SlotCols);
+#pragma unroll
+                    for (int kk = 0; kk < kG3BK / 8; ++kk) {
+                        const uint32_t ko = kk * 1024;  // 8 rows of 128 B
+                        const uint64_t db = gt_desc(b_raw + ko, kG3BK * 128, 512);
+                        const uint64_t dbl = gt_desc(b_lo + ko, kG3BK * 128, 512);
+                        const uint32_t a_raw = ta + (uint32_t)(kk * 16), a_lo = a_raw + 8;
+                        g3_mma(dacc, a_raw, db, (kb > kb0 || kk > 0) ? 1u : 0u);  // hi·hi
+                        g3_mma(dacc, a_raw, dbl, 1u);                             // hi·lo
+                        g3_mma(dacc, a_lo, db, 1u);                               // lo·hi
+                    }
+                    g2_commit_both(&empty[s]);     // smem stage free in both CTAs
+                    g2_commit_both(&tfree[slot]);  // TMEM A slot free in both CTAs
+                    if (++s == kG3Stages) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                    if (++slot == kG3Slots) slot = 0;
+                }
+                g2_commit_both(&dfull[buf]);
+                dph[buf] ^= 1u;
+                buf ^= 1;
+            })
+        }
+    } else if (warp < 2 + kGtConvWarps) {  // ===== converter (warps 2-5, both CTAs)
+        // thread -> TMEM lane (A row m): warp w may only access lanes 32 (w % 4) .. + 31
+        const int ct = threadIdx.x - 64;
+        const int m = 32 * (warp & 3) + lane;
+        const uint32_t conv_leader = map_to_rank(gt_smem(conv), 0u);
+        int s = 0, slot = 0, seq = 0;
+        uint32_t ph = 0;
+        G3_FOR_JOBS({
+            (void)tile;
+            for (int kb = kb0; kb < kb1; ++kb) {
+                mbar_wait(&full[s], ph);
+                unsigned char *st = smem + (size_t)s * kG3StageBytes;
+                // B: lo parts next to the raw ones (same swizzled positions)
+                const float4 *braw = reinterpret_cast<const float4 *>(st + kG3ABytes);
+                float4 *blo = reinterpret_cast<float4 *>(st + kG3ABytes + kG3BBytes);
+#pragma unroll
+                for (int i = ct; i < kG3BBytes / 16; i += kGtConv) {
+                    const float4 a = braw[i];
+                    blo[i] = make_float4(gt_lo(a.x), gt_lo(a.y), gt_lo(a.z), gt_lo(a.w));
+                }
+                // A: row m, k = 0..15 from the plain [k][m] tile
+                const float *as = reinterpret_cast<const float *>(st);
+                float r0[16], r1[16];  // per 8-row k-group: raw k0..7, lo k0..7
+#pragma unroll
+                for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const float a = as[(8 * kk + e) * kG3AHalf + m];
+                        float *dst = kk ? r1 : r0;
+                        dst[e] = a;
+                        dst[8 + e] = gt_lo(a);
+                    }
+                // the slot's previous MMAs must have completed before it is overwritten
+                if (seq >= kG3Slots) mbar_wait(&tfree[slot], (uint32_t)((seq / kG3Slots - 1) & 1));
+                const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(kG3RingCol + slot * kG3SlotCols);
+                g3_st16(ta, r0);
+                g3_st16(ta + 16, r1);
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                fence_proxy_async_smem();  // B lo (generic stores) -> visible to the tensor core
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                g2_named_sync(1, kGtConv);
+                if (ct == 0) g2_remote_arrive(conv_leader + (uint32_t)(s * sizeof(uint64_t)));
+                if (++s == kG3Stages) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+                if (++slot == kG3Slots) slot = 0;
+                ++seq;
+            }
+        })
+    } else {  // ===== epilogue (warps 6-9, both CTAs): TMEM lane quarter q, all N columns
+        const int q = warp & 3;
+        const int et = threadIdx.x - 32 * (2 + kGtConvWarps);
+        const uint32_t dempty_leader = map_to_rank(gt_smem(dempty), 0u);
+        uint32_t dph[2] = {0u, 0u};
+        int buf = 0;
+        G3_FOR_JOBS({
+            (void)kb1;
+            const int64_t i = (int64_t)tile.x * kG3M + (int64_t)rank * kG3AHalf + 32 * q + lane;
+            const int64_t j0 = (int64_t)tile.y * kG3N;
+            mbar_wait(&dfull[buf], dph[buf]);
+            dph[buf] ^= 1u;
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const bool first = k == 0;
+#pragma unroll 1
+            for (int c = 0; c < kG3N / 32; ++c) {
+                uint32_t v[32];
+                const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * kG3AccCols + 32 * c);
+                gt_ld32(taddr, v);
+                gt_fold_t(p.B, p.ldb, p.n, i, j0 + 32 * c, v, first);
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            g2_named_sync(2, 32 * kGtEpiWarps);
+            if (et == 0) g2_remote_arrive(dempty_leader + (uint32_t)(buf * sizeof(uint64_t)));
+            buf ^= 1;
+        })
+    }
+#undef G3_FOR_JOBS
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    cluster_sync_all();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kGtTmemCols) : "memory");
+}
+
 // strictly-upper triangle from the lower one (the epilogues stored every tile transposed, so every
 // (i, j) with i >= j holds its value); 32 x 32 tiles through shared memory, both sides coalesced
 __global__ void gram_mirror_to_upper(float *__restrict__ B, int64_t n, int64_t ldb) {

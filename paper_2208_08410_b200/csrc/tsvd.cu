@@ -292,7 +292,7 @@ struct tsvd_s {
     double gram_ms = 0.0;  // B0 build time of the last build
     int gram_blocks = 0;   // n_b of the symmetric task schedule of the last build (tcgen05: tiles computed)
     int2 *gram_tiles = nullptr;  // tcgen05 Gram: the symmetric tile list
-    bool gram_pair = false;      // ... of the CTA-pair kernel (256 x 256 tiles)
+    int gram_pair = 0;           // ... of kernel variant 1 (single CTA), 2 (pair), 3 (pair, A in TMEM)
     int gram_ntiles = 0;
     int64_t gram_n = -1;
     cublasHandle_t cublas = nullptr;
@@ -341,8 +341,8 @@ struct tsvd_s {
     } while (0)
 #define NK(call)                                                                                    \
     do {                                                                                            \
-        if (!h->comm) return h->fail(TSVD_ERR_UNSUPPORTED, "%s: no NCCL communicator (in-process ranks "     \
-                                     "run the peer collective only)", #call);                      \
+        if (h->grp) return h->fail(TSVD_ERR_UNSUPPORTED, "%s: no NCCL communicator (in-process ranks "       \
+                                   "run the peer collective only)", #call);                        \
         ncclResult_t r_ = (call);                                                                   \
         if (r_ != ncclSuccess) return h->fail(TSVD_ERR_NCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
     } while (0)
@@ -1574,6 +1574,17 @@ static std::vector<int2> gram_tiles2(int64_t n) {
     return t;
 }
 
+// ... and for the A-in-TMEM pair kernel: 256 (M) x 192 (N) tiles touching j >= i
+static std::vector<int2> gram_tiles3(int64_t n) {
+    const int nI = (int)((n + kG3M - 1) / kG3M), nJ = (int)((n + kG3N - 1) / kG3N);
+    std::vector<int2> t;
+    for (int I0 = 0; I0 < nI; I0 += 4)
+        for (int J = 0; J < nJ; ++J)
+            for (int I = I0; I < std::min(nI, I0 + 4); ++I)
+                if ((int64_t)kG3N * J + kG3N - 1 >= (int64_t)kG3M * I) t.push_back(make_int2(I, J));
+    return t;
+}
+
 // B0 = A^T A (Alg. 3's Gram) on the tcgen05 tensor cores, 3xTF32 (gram_tc.cuh), the
 // symmetric tile schedule, then the strictly-lower triangle mirrored.  TSVD_GRAM_CUBLAS=1 keeps the
 // round-1 path (three cuBLAS TF32 GEMMs of a hi/lo split of A per block product) for A/B timing.
@@ -1621,11 +1632,15 @@ static tsvd_status build_gram(tsvd_t h) {
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return h->fail(TSVD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     }
-    // default: the CTA-pair kernel (gram_tc2); TSVD_GRAM_TC1=1 (A/B) or LO_GMEM: the single-CTA kernel
-    const bool pair = !lo_gmem && !getenv("TSVD_GRAM_TC1") && h->sms >= 2;
-    if (h->gram_n != n || h->gram_pair != pair) {
-        const std::vector<int2> tiles = pair ? gram_tiles2(n) : gram_tiles(n);
-        h->gram_pair = pair;
+    // default: the CTA-pair kernel with A in TMEM (gram_tc3); A/B: TSVD_GRAM_TC=2 the pair kernel with
+    // both operands in shared memory, TSVD_GRAM_TC=1 (or LO_GMEM) the single-CTA kernel
+    int variant = 3;
+    if (const char *e = getenv("TSVD_GRAM_TC")) variant = atoi(e);
+    if (getenv("TSVD_GRAM_TC1") || lo_gmem || h->sms < 2) variant = 1;
+    const bool pair = variant >= 2;
+    if (h->gram_n != n || h->gram_pair != variant) {
+        const std::vector<int2> tiles = variant == 3 ? gram_tiles3(n) : variant == 2 ? gram_tiles2(n) : gram_tiles(n);
+        h->gram_pair = variant;
         cudaFree(h->gram_tiles);
         h->gram_tiles = nullptr;
         CK(cudaMalloc((void **)&h->gram_tiles, tiles.size() * sizeof(int2)));
@@ -1636,6 +1651,7 @@ static tsvd_status build_gram(tsvd_t h) {
         CK(cudaFuncSetAttribute(gram_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGtSmem));
         CK(cudaFuncSetAttribute(gram_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, kG2Smem));
         CK(cudaFuncSetAttribute(gram_tc2, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+        CK(cudaFuncSetAttribute(gram_tc3, cudaFuncAttributeMaxDynamicSharedMemorySize, kG3Smem));
     }
     GtParams p{};
     p.tiles = h->gram_tiles;
@@ -1654,11 +1670,22 @@ static tsvd_status build_gram(tsvd_t h) {
         attr[0].val.clusterDim.z = 1;
         cfg.gridDim = dim3(G);
         cfg.blockDim = dim3(kGtThreads);
-        cfg.dynamicSmemBytes = kG2Smem;
+        cfg.dynamicSmemBytes = variant == 3 ? kG3Smem : kG2Smem;
         cfg.stream = h->stream;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        CK(cudaLaunchKernelEx(&cfg, gram_tc2, map, p));
+        if (variant == 3) {
+            // A half: plain [k][m] boxes of 128 columns x 16 rows (read by the converter, not the MMA)
+            CUtensorMap map_a;
+            const cuuint32_t box_a[2] = {(cuuint32_t)kG3AHalf, (cuuint32_t)kG3BK};
+            CUresult r = encode(&map_a, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)h->A_use, dims, strides, box_a, estr,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return h->fail(TSVD_ERR_CUDA, "cuTensorMapEncodeTiled (A half) failed (%d)", (int)r);
+            CK(cudaLaunchKernelEx(&cfg, gram_tc3, map, map_a, p));
+        } else {
+            CK(cudaLaunchKernelEx(&cfg, gram_tc2, map, p));
+        }
     } else if (lo_gmem) {
         gram_tc<true><<<std::min(h->sms, h->gram_ntiles), kGtThreads, kGtSmem, h->stream>>>(map, map_lo, p);
     } else {

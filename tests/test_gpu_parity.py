@@ -440,32 +440,38 @@ def test_explicit_gram_parity(m, n, k, T):
 @pytest.mark.parametrize("nb", [3, 5])
 def test_explicit_gram_symmetric_schedule(nb, monkeypatch):
     """The Gram's symmetric task schedule (only the blocks on or above the diagonal are
-    multiplied, the strictly-lower ones mirrored): the tcgen05 CTA-pair kernel's schedule (256 x 256
-    tiles with J >= I), the single-CTA kernel's (128 x 256 tiles touching the upper triangle,
-    TSVD_GRAM_TC1=1) and the round-1 cuBLAS block schedule (n_b(n_b+1)/2 block products,
-    TSVD_GRAM_CUBLAS=1) with ragged blocks — all against the oracle and against each other."""
+    multiplied, the strictly-lower ones mirrored), for every kernel variant: the default tcgen05 CTA-
+    pair kernel with A in tensor memory (256 x 192 tiles touching j >= i), the pair kernel with both
+    operands in shared memory (TSVD_GRAM_TC=2: 256 x 256 tiles with J >= I), the single-CTA kernel
+    (TSVD_GRAM_TC=1: 128 x 256 tiles touching the upper triangle) and the round-1 cuBLAS block
+    schedule (TSVD_GRAM_CUBLAS=1: n_b(n_b+1)/2 block products) with ragged blocks — all against the
+    oracle and against each other."""
     m, n, k = 1800, 700, 4
     A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(48, 5.0, 0.75), seed=77)
     V0 = synth.v0_normal(n, k, seed=78)
     ref = oracle.tsvd(A, k, 1e-6, V0)
-    tc = _gpu_tsvd(A, k, 1e-6, V0, method=1)
-    nT = -(-n // 256)
-    assert tc[0] == P.OK and tc[7]["gram_blocks"] == nT * (nT + 1) // 2 < nT * nT
-    _assert_parity(A, ref, *tc[1:5], k)
-    monkeypatch.setenv("TSVD_GRAM_TC1", "1")
-    t1 = _gpu_tsvd(A, k, 1e-6, V0, method=1)
-    monkeypatch.delenv("TSVD_GRAM_TC1")
-    nI, nJ = -(-n // 128), -(-n // 256)
-    want_tiles = sum(1 for I in range(nI) for J in range(nJ) if 256 * J + 255 >= 128 * I)
-    assert t1[0] == P.OK and t1[7]["gram_blocks"] == want_tiles < nI * nJ
-    _assert_parity(A, ref, *t1[1:5], k)
-    np.testing.assert_allclose(t1[2], tc[2], rtol=1e-6)
+
+    def tiles(bm, bn):
+        nI, nJ = -(-n // bm), -(-n // bn)
+        return sum(1 for I in range(nI) for J in range(nJ) if bn * J + bn - 1 >= bm * I), nI * nJ
+
+    runs = {}
+    for variant, (bm, bn) in ((3, (256, 192)), (2, (256, 256)), (1, (128, 256))):
+        monkeypatch.setenv("TSVD_GRAM_TC", str(variant))
+        r = _gpu_tsvd(A, k, 1e-6, V0, method=1)
+        want, full = tiles(bm, bn)
+        assert r[0] == P.OK and r[7]["gram_blocks"] == want < full, (variant, r[7]["gram_blocks"], want)
+        _assert_parity(A, ref, *r[1:5], k)
+        runs[variant] = r
+    monkeypatch.delenv("TSVD_GRAM_TC")
+    for variant in (2, 1):
+        np.testing.assert_allclose(runs[variant][2], runs[3][2], rtol=1e-6)
     monkeypatch.setenv("TSVD_GRAM_CUBLAS", "1")
     monkeypatch.setenv("TSVD_GRAM_NB", str(nb))
     ex = _gpu_tsvd(A, k, 1e-6, V0, method=1)
     assert ex[0] == P.OK and ex[7]["gram_blocks"] == nb
     _assert_parity(A, ref, *ex[1:5], k)
-    np.testing.assert_allclose(ex[2], tc[2], rtol=1e-6)
+    np.testing.assert_allclose(ex[2], runs[3][2], rtol=1e-6)
 
 
 def test_many_components_fall_back_cleanly():
@@ -486,7 +492,7 @@ def test_many_components_fall_back_cleanly():
 def test_explicit_gram_one_product_elementwise(m, n):
     """One explicit-Gram iteration (fixed T = 1, k = 1): v1 = B0 v0 / ||B0 v0|| with B0 = A^T A from
     the tcgen05 3xTF32 kernel — a dense, unstructured product that exercises every tile, the
-    ragged edges (n, m not multiples of the 256 x 256 pair tile or the 16-row K chunk) and the mirror.
+    ragged edges (n, m not multiples of the 256 x 192 pair tile or the 16-row K chunk) and the mirror.
     Elementwise against the oracle's fp64 (A^T (A v0)) direction."""
     rng = np.random.default_rng(m + n)
     A = rng.standard_normal((m, n)).astype(np.float32)
