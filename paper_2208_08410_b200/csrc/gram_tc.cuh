@@ -98,8 +98,41 @@ __device__ __forceinline__ void gt_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(gt_smem(bar)) : "memory");
 }
 
+// shared-memory accesses by 32-bit shared address: the stage pointers are rounded up to the 1 KB
+// swizzle alignment through an integer cast, after which the compiler no longer knows they point
+// to shared memory and emits generic LD.E / ST.E (ncu: the converter's top stall)
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+__device__ __forceinline__ float lds32(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+
 // lo = a - tf32_trunc(a) (exact in fp32): the part of a the tensor core drops
 __device__ __forceinline__ float gt_lo(float a) { return a - __uint_as_float(__float_as_uint(a) & 0xFFFFE000u); }
+
+// lo parts of `count` float4 of a stage: raw at [src + 16 i], lo to [dst + 16 i] for i = t, t + T, ...;
+// U loads in flight before their stores (the volatile shared accesses keep program order)
+template <int U>
+__device__ __forceinline__ void gt_convert(uint32_t src, uint32_t dst, int t, int T, int count) {
+    for (int i0 = t; i0 < count; i0 += U * T) {
+        float4 a[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + u * T < count) a[u] = lds128(src + 16 * (i0 + u * T));
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + u * T < count)
+                sts128(dst + 16 * (i0 + u * T), make_float4(gt_lo(a[u].x), gt_lo(a[u].y), gt_lo(a[u].z), gt_lo(a[u].w)));
+    }
+}
 
 // the lo parts of a row slab in global memory (LO_GMEM)
 __global__ void gram_lo_split(const float *__restrict__ A, int64_t rows, int64_t cols, int64_t ld,
@@ -296,14 +329,8 @@ __global__ void __launch_bounds__(kGtThreads, 1)
             GT_FOR_JOBS({
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[s], ph);
-                    const float4 *raw = reinterpret_cast<const float4 *>(smem + (size_t)s * kGtStageBytes);
-                    float4 *lo =
-                        reinterpret_cast<float4 *>(smem + (size_t)s * kGtStageBytes + kGtABytes + kGtBBytes);
-#pragma unroll 4
-                    for (int i = ct; i < (kGtABytes + kGtBBytes) / 16; i += kGtConv) {
-                        const float4 a = raw[i];
-                        lo[i] = make_float4(gt_lo(a.x), gt_lo(a.y), gt_lo(a.z), gt_lo(a.w));
-                    }
+                    const uint32_t raw = gt_smem(smem + (size_t)s * kGtStageBytes);
+                    gt_convert<6>(raw, raw + kGtABytes + kGtBBytes, ct, kGtConv, (kGtABytes + kGtBBytes) / 16);
                     fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core (async proxy)
                     gt_arrive(&conv[s]);
                     if (++s == kGtStages) {
@@ -527,13 +554,8 @@ __global__ void __launch_bounds__(kGtThreads, 1)
             (void)tile;
             for (int kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(&full[s], ph);
-                const float4 *raw = reinterpret_cast<const float4 *>(smem + (size_t)s * kG2StageBytes);
-                float4 *lo = reinterpret_cast<float4 *>(smem + (size_t)s * kG2StageBytes + 2 * kG2HalfBytes);
-#pragma unroll 4
-                for (int i = ct; i < (2 * kG2HalfBytes) / 16; i += kGtConv) {
-                    const float4 a = raw[i];
-                    lo[i] = make_float4(gt_lo(a.x), gt_lo(a.y), gt_lo(a.z), gt_lo(a.w));
-                }
+                const uint32_t raw = gt_smem(smem + (size_t)s * kG2StageBytes);
+                gt_convert<8>(raw, raw + 2 * kG2HalfBytes, ct, kGtConv, (2 * kG2HalfBytes) / 16);
                 fence_proxy_async_smem();  // generic stores -> visible to the tensor core (async proxy)
                 g2_named_sync(1, kGtConv);
                 if (ct == 0) g2_remote_arrive(conv_leader + (uint32_t)(s * sizeof(uint64_t)));
@@ -751,27 +773,21 @@ __global__ void __launch_bounds__(kGtThreads, 1)
             (void)tile;
             for (int kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(&full[s], ph);
-                unsigned char *st = smem + (size_t)s * kG3StageBytes;
-                // B: lo parts next to the raw ones (same swizzled positions)
-                const float4 *braw = reinterpret_cast<const float4 *>(st + kG3ABytes);
-                float4 *blo = reinterpret_cast<float4 *>(st + kG3ABytes + kG3BBytes);
-#pragma unroll
-                for (int i = ct; i < kG3BBytes / 16; i += kGtConv) {
-                    const float4 a = braw[i];
-                    blo[i] = make_float4(gt_lo(a.x), gt_lo(a.y), gt_lo(a.z), gt_lo(a.w));
-                }
-                // A: row m, k = 0..15 from the plain [k][m] tile
-                const float *as = reinterpret_cast<const float *>(st);
+                const uint32_t st = gt_smem(smem + (size_t)s * kG3StageBytes);
+                // A: row m, k = 0..15 from the plain [k][m] tile (loads issued first)
                 float r0[16], r1[16];  // per 8-row k-group: raw k0..7, lo k0..7
 #pragma unroll
-                for (int kk = 0; kk < 2; ++kk)
+                for (int e = 0; e < 8; ++e) {
+                    r0[e] = lds32(st + 4u * (uint32_t)(e * kG3AHalf + m));
+                    r1[e] = lds32(st + 4u * (uint32_t)((8 + e) * kG3AHalf + m));
+                }
+                // B: lo parts next to the raw ones (same swizzled positions)
+                gt_convert<3>(st + kG3ABytes, st + kG3ABytes + kG3BBytes, ct, kGtConv, kG3BBytes / 16);
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        const float a = as[(8 * kk + e) * kG3AHalf + m];
-                        float *dst = kk ? r1 : r0;
-                        dst[e] = a;
-                        dst[8 + e] = gt_lo(a);
-                    }
+                for (int e = 0; e < 8; ++e) {
+                    r0[8 + e] = gt_lo(r0[e]);
+                    r1[8 + e] = gt_lo(r1[e]);
+                }
                 // the slot's previous MMAs must have completed before it is overwritten
                 if (seq >= kG3Slots) mbar_wait(&tfree[slot], (uint32_t)((seq / kG3Slots - 1) & 1));
                 const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(kG3RingCol + slot * kG3SlotCols);

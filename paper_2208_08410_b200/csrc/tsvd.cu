@@ -1632,9 +1632,10 @@ static tsvd_status build_gram(tsvd_t h) {
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return h->fail(TSVD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     }
-    // default: the CTA-pair kernel with A in TMEM (gram_tc3); A/B: TSVD_GRAM_TC=2 the pair kernel with
-    // both operands in shared memory, TSVD_GRAM_TC=1 (or LO_GMEM) the single-CTA kernel
-    int variant = 3;
+    // default: the CTA-pair kernel (gram_tc2).  A/B: TSVD_GRAM_TC=3 the pair kernel with A in TMEM
+    // (fewer shared-memory bytes, but measured 5-10 % slower: 98 vs 88-93 ms at C2, the box's power
+    // cap sets the clock under this tensor load), TSVD_GRAM_TC=1 (or LO_GMEM) the single-CTA kernel
+    int variant = 2;
     if (const char *e = getenv("TSVD_GRAM_TC")) variant = atoi(e);
     if (getenv("TSVD_GRAM_TC1") || lo_gmem || h->sms < 2) variant = 1;
     const bool pair = variant >= 2;
@@ -2137,6 +2138,8 @@ tsvd_status tsvd_set_comm(tsvd_t h, int32_t rank, int32_t world, const void *uid
                 return h->fail(TSVD_ERR_UNSUPPORTED, "in-process ranks run the peer collective (COLLECTIVE = 0)");
             const std::string key((const char *)uid, 128);
             std::lock_guard<std::mutex> lk(g_grp_mu);
+            for (auto it = g_grps.begin(); it != g_grps.end();)  // groups whose handles are all gone
+                it = it->second.expired() ? g_grps.erase(it) : std::next(it);
             std::shared_ptr<InprocGroup> g = g_grps[key].lock();
             if (!g) {
                 g = std::make_shared<InprocGroup>();
