@@ -568,6 +568,8 @@ def main():
                        "parallelism": f"row-partition x{world}",
                        "l2": "no flush: the matrix read every pass is larger than L2 (126 MB)"},
             "iterations": [int(x) for x in iters[:kf]], "k_found": kf, "status": rc,
+            # latency per power iteration (SURVEY §8(d) asks for it at C1, which fits L2)
+            "us_per_iteration": ms / args.steps * 1e3 / max(1, int(np.sum(iters[:kf]))),
             "check": {"sigma_max_rel_err_vs_planted": sig_err, "v_max_1_minus_cos_vs_planted": v_err},
             "passes_over_A_per_step": passes if not sparse else None,
             "value_counting_k_extraction_passes": alg_bytes_step * args.steps / (ms / 1e3) / 1e9,

@@ -59,6 +59,8 @@ struct PsParams {
     int32_t part32;          // every CTA's range is a single fp32 run (rows <= run_rows): fp32 partials
     unsigned long long *tl;  // debug timeline (TSVD_TIMELINE), same record layout as N1 + N5
     PxView px;               // world > 1: NVLink peer exchange of the column slices (one block)
+    int32_t vcache;          // the CTA's column slice of V[:, :l] cached in shared memory for the
+                             // launch (V does not change during a component): Vs[i (per + 1) + c]
     // component transitions inside the kernel (two-vector path, R21):
     // head_ext: the launch starts by reducing the partials of the two-vector pass (gv_fused<TWO>,
     //   fp64 partials, sq_part, u_out) that began this component: sigma_fresh = ||u||, U[:, fresh] =
@@ -178,6 +180,8 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
     double *gred = tot + 2 + p.wpart_ld;                           // [kPsGred(T)] slice reduction
     double *ys = gred + kPsGred(T);                                // [128] y of the column block
     double *Ssm = ys + 128;  // [l] sigma (the per-pass reductions read it twice: no L2 round trip)
+    double *Vs = Ssm + p.wpart_ld;  // vcache: [l][per + 1] (odd stride: the column-owner reads and
+                                    // the component-per-lane reads are both bank-conflict free)
     __shared__ int64_t slot_row[kMaxStages];
     __shared__ double ny_s;
     __shared__ int done_s;
@@ -233,6 +237,16 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
     for (int i = tid; i < l; i += T) {
         cvec[i] = p.c[i];
         Ssm[i] = p.S[i];  // (head: entry `fresh` is set from the head's own sigma below)
+    }
+    if (p.vcache) {  // this CTA's column slice of V[:, :l] (the slice geometry of the reduction below)
+        const int Gs = p.px.world > 1 ? p.px.G : G;
+        const int per = (int)(((p.n + Gs - 1) / Gs + 31) / 32 * 32);
+        const int64_t j0 = b < Gs ? (int64_t)b * per : (int64_t)p.n;
+        const int64_t j1 = (j0 + per) < (int64_t)p.n ? (j0 + per) : (int64_t)p.n;
+        for (int idx = tid; idx < l * per; idx += T) {
+            const int i = idx / per, c = idx - i * per;
+            Vs[i * (per + 1) + c] = j0 + c < j1 ? p.V[(j0 + c) * p.ldv + i] : 0.0;
+        }
     }
     if (tid == 0) ny_s = st->ny;
     __syncthreads();
@@ -556,10 +570,15 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
             }
             if (tid < CW) {
                 if (j < j1) {
-                    const double *Vj = p.V + j * p.ldv;
                     double corr = 0.0;  // (V (S w))_j
+                    if (p.vcache) {
+                        const double *Vj = Vs + (j - j0);
+                        for (int i = 0; i < l; ++i) corr += Vj[i * (per + 1)] * gvec[i];
+                    } else {
+                        const double *Vj = p.V + j * p.ldv;
 #pragma unroll 4
-                    for (int i = 0; i < l; ++i) corr += Vj[i] * gvec[i];
+                        for (int i = 0; i < l; ++i) corr += Vj[i] * gvec[i];
+                    }
                     y -= corr;
                     __stcg(ynew + j, y);
                     __stcg(p.puby + j, ((unsigned long long)(xeb_s + (unsigned)it + 1u) << 32) | __float_as_uint((float)y));
@@ -572,11 +591,18 @@ __global__ void __launch_bounds__(T) gv_persist(const PsParams p) {
             if (l > 0) {  // warp w: columns w, w + NW, ... of the block; lane: components lane + 32 q
                 const int jn = (int)((j1 - c0) < CW ? (j1 - c0) : CW);
                 for (int jj = warp; jj < jn; jj += NW) {
-                    const double *Vr = p.V + (c0 + jj) * p.ldv;
                     const double yj = ys[jj];
+                    if (p.vcache) {
+                        const double *Vr = Vs + (c0 + jj - j0);
 #pragma unroll
-                    for (int q = 0; q < kPsLanesV; ++q)
-                        if (lane + 32 * q < l) vacc[q] += Vr[lane + 32 * q] * yj;
+                        for (int q = 0; q < kPsLanesV; ++q)
+                            if (lane + 32 * q < l) vacc[q] += Vr[(lane + 32 * q) * (per + 1)] * yj;
+                    } else {
+                        const double *Vr = p.V + (c0 + jj) * p.ldv;
+#pragma unroll
+                        for (int q = 0; q < kPsLanesV; ++q)
+                            if (lane + 32 * q < l) vacc[q] += Vr[lane + 32 * q] * yj;
+                    }
                 }
             }
             __syncthreads();

@@ -299,6 +299,7 @@ struct tsvd_s {
     PsFn gv_ps = nullptr;  // N7: one persistent cooperative kernel per component (null: unsupported)
     int S_ps = 0;
     size_t smem_ps = 0;
+    int64_t vcache_doubles = 0;  // shared-memory V slice cache of the persistent kernel (0: none)
     int grid_gb = 0;  // explicit-Gram iteration grid (from n, identical on every rank)
     int T_ps = 0, NV_ps = 0;  // persistent kernel's CTA width (may differ from the N1 kernels')
     char *gx_mem = nullptr;             // explicit Gram, world > 1: [y area 2n | sums area] (IPC)
@@ -460,7 +461,13 @@ static tsvd_status plan(tsvd_t h) {
     if (occ < 1) return h->fail(TSVD_ERR_UNSUPPORTED, "fused kernel does not fit on an SM (T=%d smem=%zu)", T, h->smem);
     h->cps = std::min(cps, occ);
     // one row range per CTA (per 2-CTA cluster when split): at most one range per row
-    h->grid = (int)std::min<int64_t>((int64_t)h->sms * h->cps / split, h->m_g) * split;
+    // at least min_rows = 8 rows per CTA (A/B knob TSVD_MIN_ROWS_PER_CTA): a small matrix (C1, in
+    // L2) is latency-bound by the per-pass reduction over the CTAs' partials, not by its rows.  C1
+    // (512 x 256, k = 8): 66.6 us per iteration with one row per CTA (512 CTAs), 25.4 / 24.5 / 25.1 /
+    // 32.6 us with 4 / 8 / 16 / 32 rows; large inputs are unaffected (m_g / 8 >> SMs)
+    int64_t min_rows = 8;
+    if (const char *e = getenv("TSVD_MIN_ROWS_PER_CTA")) min_rows = std::max<int64_t>(1, atoll(e));
+    h->grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)h->sms * h->cps / split, (h->m_g + min_rows - 1) / min_rows)) * split;
     h->parts = h->grid / split;
     // fused-extraction variant: v_prev staged in shared memory, so fewer ring stages
     h->gv_two = nullptr;
@@ -504,7 +511,12 @@ static tsvd_status plan(tsvd_t h) {
         while (Sp > 2 && ((int64_t)Sp * h->stage_bytes + extra) * h->cps > kSmemBudget) --Sp;
         PsFn fn = pick_ps(Tp, NVp, n == (int64_t)4 * NVp * Tp && !getenv("TSVD_NO_FULL"));
         if (fn && ((int64_t)Sp * h->stage_bytes + extra) * h->cps <= kSmemBudget) {
-            const size_t sm = (size_t)Sp * h->stage_bytes + (size_t)extra;
+            // V[:, :k] of the CTA's column slice (k (per + 1) doubles) in the space left, if any:
+            // the per-pass V correction and V^T y read it from shared memory instead of L2
+            const int64_t per1 = ((n + h->grid - 1) / h->grid + 31) / 32 * 32;
+            const int64_t vneed = (int64_t)h->k * (per1 + 1);
+            h->vcache_doubles = ((int64_t)Sp * h->stage_bytes + extra + 8 * vneed) * h->cps <= kSmemBudget ? vneed : 0;
+            const size_t sm = (size_t)Sp * h->stage_bytes + (size_t)extra + 8 * (size_t)h->vcache_doubles;
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             if (h->carveout_opt) CK(max_carveout(fn));
             int occ_ps = 0;
@@ -1368,6 +1380,11 @@ static tsvd_status launch_persist(tsvd_t h, cudaStream_t s, int l, cudaEvent_t e
     p.tl = h->tl_d;
     p.px.world = 1;
     if (h->world > 1) p.px = h->px;
+    {  // the slice of V[:, :l] in shared memory when it fits the space plan() reserved
+        const int Gs = h->world > 1 ? p.px.G : h->grid;
+        const int64_t per = ((h->n + Gs - 1) / Gs + 31) / 32 * 32;
+        p.vcache = (l > 0 && (int64_t)l * (per + 1) <= h->vcache_doubles && !getenv("TSVD_NO_VCACHE")) ? 1 : 0;
+    }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident: grid barriers inside
