@@ -172,8 +172,11 @@ tsvd_status tsvd_get_unique_id(void *out128);
  * Typical use: several ranks on ONE GPU (TSVD_OPT_SM_LIMIT = about 3/4 of SMs / world each, one
  * CTA per SM), which runs the multi-GPU exchange protocol where only one GPU exists.  The ranks'
  * kernels wait for each other, so each rank's stream needs its own hardware queue: set
- * CUDA_DEVICE_MAX_CONNECTIONS >= 2 world before the process creates its CUDA context.  Dense input and the peer collective only
- * (sparse inputs and METHOD = 1 across ranks need NCCL: TSVD_ERR_UNSUPPORTED).  Errors: TSVD_ERR_ARG. */
+ * CUDA_DEVICE_MAX_CONNECTIONS >= 2 world before the process creates its CUDA context.  Where the
+ * multi-process path calls ncclAllReduce (sparse length-n vectors, METHOD = 1's B0 and extraction
+ * sums) in-process ranks sum the ranks' buffers in rank order between two host rendezvous
+ * (host-synchronous; a test vehicle, not a fast path).  TSVD_OPT_COLLECTIVE = 1 is refused with
+ * TSVD_ERR_UNSUPPORTED.  Errors: TSVD_ERR_ARG. */
 tsvd_status tsvd_get_inproc_id(void *out128);
 
 /* tsvd_set_comm — join an NCCL communicator of `world` ranks (this rank = `rank`, world <= 8, one

@@ -158,6 +158,8 @@ struct tsvd_s {
     int32_t rank = 0, world = 1;
     ncclComm_t comm = nullptr;
     std::shared_ptr<InprocGroup> grp;       // in-process ranks (instead of comm)
+    void *ar_tmp = nullptr;                 // in-process all-reduce scratch
+    size_t ar_bytes = 0;
     int sm_limit = 0;                       // TSVD_OPT_SM_LIMIT (0 = every SM of the device)
     int coll = COLL_NONE;
     int coll_opt = 0;
@@ -663,6 +665,57 @@ static tsvd_status coll_min_int(tsvd_t h, int &v) {
     return TSVD_OK;
 }
 
+// out[i] = sum over ranks of in_r[i], in rank order (in-process ranks: every rank's buffer is a
+// device pointer of this process)
+struct RankPtrs {
+    const void *p[kMaxRanks];
+};
+template <typename F>
+__global__ void sum_ranks(RankPtrs in, int world, F *__restrict__ out, int64_t count) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        F acc = static_cast<const F *>(in.p[0])[i];
+        for (int r = 1; r < world; ++r) acc += static_cast<const F *>(in.p[r])[i];
+        out[i] = acc;
+    }
+}
+
+// In-place sum all-reduce of `count` fp32 / fp64 elements on stream s: ncclAllReduce across
+// processes; for in-process ranks a host rendezvous (every rank's partial complete), a rank-ordered
+// sum of the ranks' buffers into a scratch buffer, a second rendezvous (every rank done reading),
+// and the copy back — host-synchronous, used only where the multi-process path calls NCCL (sparse
+// vectors, the explicit Gram's B0 and extraction sums)
+static tsvd_status coll_allreduce(tsvd_t h, void *buf, size_t count, bool f64, cudaStream_t s) {
+    if (!h->grp) {
+        NK(ncclAllReduce(buf, buf, count, f64 ? ncclDouble : ncclFloat, ncclSum, h->comm, s));
+        return TSVD_OK;
+    }
+    const size_t bytes = count * (f64 ? 8 : 4);
+    if (bytes > h->ar_bytes) {
+        CK(cudaStreamSynchronize(s));
+        if (h->ar_tmp) CK(cudaFree(h->ar_tmp));
+        h->ar_tmp = nullptr;
+        CK(cudaMalloc(&h->ar_tmp, bytes));
+        h->ar_bytes = bytes;
+    }
+    CK(cudaStreamSynchronize(s));
+    std::vector<void *> all;
+    if (grp_exchange(h, 0, buf, &all) == LLONG_MIN)
+        return h->fail(TSVD_ERR_NCCL, "in-process group: a rank did not arrive within 60 s");
+    RankPtrs rp{};
+    for (int r = 0; r < h->world; ++r) rp.p[r] = all[r];
+    const int blocks = (int)std::min<int64_t>(((int64_t)count + 255) / 256, (int64_t)h->sms * 8);
+    if (count) {
+        if (f64) sum_ranks<double><<<blocks, 256, 0, s>>>(rp, h->world, (double *)h->ar_tmp, (int64_t)count);
+        else sum_ranks<float><<<blocks, 256, 0, s>>>(rp, h->world, (float *)h->ar_tmp, (int64_t)count);
+        CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(s));
+    if (grp_exchange(h, 0, nullptr, nullptr) == LLONG_MIN)
+        return h->fail(TSVD_ERR_NCCL, "in-process group: a rank did not arrive within 60 s");
+    if (count) CK(cudaMemcpyAsync(buf, h->ar_tmp, bytes, cudaMemcpyDeviceToDevice, s));
+    return TSVD_OK;
+}
+
 // base[r] = rank r's copy of an exchange buffer (mine for r == rank).  Across processes: CUDA IPC
 // handles all-gathered with NCCL and opened (maps[r] records what tsvd_destroy closes; ok = false if
 // an open failed); in-process ranks: the other handles' device pointers themselves
@@ -1021,7 +1074,9 @@ static SpParams sp_params(tsvd_t h, int l) {
 }
 
 // the sparse pass overlaps its cross-rank sum with N3 (column chunks of the last index block)
-static bool sp_overlap(tsvd_t h) { return h->sparse && h->world > 1 && h->coll == COLL_NCCL && h->sp_chunks > 1; }
+static bool sp_overlap(tsvd_t h) {
+    return h->sparse && h->world > 1 && h->coll == COLL_NCCL && h->sp_chunks > 1 && !h->grp;
+}
 
 // Sparse pass: N2 (rows, one launch per column block) then N3 (columns, one launch per row block);
 // N2 alone for the extraction.  world > 1: N3's last block runs in column chunks and each chunk's
@@ -1233,12 +1288,12 @@ static PubParams pub_params(tsvd_t h, int mode, int l) {
 static tsvd_status launch_exchange(tsvd_t h, cudaStream_t s, int l) {
     if (h->sparse) {  // N3 already wrote [y_g | w_g]; the length-n sum is bandwidth-bound: NCCL
         if (h->world > 1 && !sp_overlap(h))
-            NK(ncclAllReduce(h->yw, h->yw, (size_t)(h->wofs + h->kpad), ncclDouble, ncclSum, h->comm, s));
+            TRY(coll_allreduce(h, h->yw, (size_t)(h->wofs + h->kpad), true, s));
         return TSVD_OK;
     }
     if (fused_reduce(h)) {  // N1 already summed its partials into yw / the symmetric slot
         if (h->coll == COLL_NCCL)
-            NK(ncclAllReduce(h->yw, h->yw, (size_t)(h->wofs + h->kpad), ncclDouble, ncclSum, h->comm, s));
+            TRY(coll_allreduce(h, h->yw, (size_t)(h->wofs + h->kpad), true, s));
         return TSVD_OK;
     }
     if (h->coll == COLL_PEER) {
@@ -1247,7 +1302,7 @@ static tsvd_status launch_exchange(tsvd_t h, cudaStream_t s, int l) {
         CK(launch_k(h, reduce_partials, h->fin_blocks, kFinThreads, 0, s, 1, (const double *)h->ypart, h->parts,
                     h->ypart_ld, (int)h->n, (const double *)h->wpart, (int)h->kpad, l, h->yw, h->wofs,
                     (const LoopState *)h->st));
-        NK(ncclAllReduce(h->yw, h->yw, (size_t)(h->wofs + h->kpad), ncclDouble, ncclSum, h->comm, s));
+        TRY(coll_allreduce(h, h->yw, (size_t)(h->wofs + h->kpad), true, s));
     }
     return TSVD_OK;
 }
@@ -1431,7 +1486,7 @@ static tsvd_status launch_extract(tsvd_t h, cudaStream_t s, int l) {
     } else {
         CK(launch_k(h, ext_reduce, 1, 32, 0, s, 1, (const double *)h->sq_part, h->parts, h->sig2,
                     (const LoopState *)h->st));
-        NK(ncclAllReduce(h->sig2, h->sig2, 1, ncclDouble, ncclSum, h->comm, s));
+        TRY(coll_allreduce(h, h->sig2, 1, true, s));
         ext_finish<SRC_YW><<<blocks, 256, 0, s>>>(p);
     }
     CK(cudaGetLastError());
@@ -1725,7 +1780,7 @@ static tsvd_status build_gram(tsvd_t h) {
     }
     // row-partitioned A (world > 1): B0 = sum_g A_g^T A_g, one all-reduce over NVLink (Alg. 3's
     // Reduce_sum, as an all-reduce so that every rank iterates on the same B0)
-    if (h->world > 1) NK(ncclAllReduce(h->B0, h->B0, (size_t)n * h->ldb0, ncclFloat, ncclSum, h->comm, h->stream));
+    if (h->world > 1) TRY(coll_allreduce(h, h->B0, (size_t)n * h->ldb0, false, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     h->B0_ok = true;
     h->gram_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1787,7 +1842,7 @@ static tsvd_status build_gram_cublas(tsvd_t h) {
     }
     // row-partitioned A (world > 1): B0 = sum_g A_g^T A_g, one all-reduce over NVLink (Alg. 3's
     // Reduce_sum, as an all-reduce so that every rank iterates on the same B0)
-    if (h->world > 1) NK(ncclAllReduce(h->B0, h->B0, (size_t)n * h->ldb0, ncclFloat, ncclSum, h->comm, h->stream));
+    if (h->world > 1) TRY(coll_allreduce(h, h->B0, (size_t)n * h->ldb0, false, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     h->B0_ok = true;
     h->gram_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1930,7 +1985,7 @@ static tsvd_status run_explicit(tsvd_t h, int l0) {
         if (h->world > 1) {  // [A_g^T u | U_g^T u | ||u_g||^2] summed over the ranks; identical on every rank
             CK(launch_k(h, gx_reduce, (int)std::min<int64_t>((n + l + 256) / 256, (int64_t)h->sms * 8), 256, 0,
                         h->stream, 1, x, h->yw, h->wofs));
-            NK(ncclAllReduce(h->yw, h->yw, (size_t)(h->wofs + h->kpad), ncclDouble, ncclSum, h->comm, h->stream));
+            TRY(coll_allreduce(h, h->yw, (size_t)(h->wofs + h->kpad), true, h->stream));
             x.parts = 1;
             x.ypart = h->yw;
             x.ypart_ld = 0;
@@ -2666,8 +2721,6 @@ tsvd_status tsvd_set_csr(tsvd_t h, const int64_t *row_ptr, const int32_t *col_id
     if (!h) return TSVD_ERR_ARG;
     if (!row_ptr || nnz < 0 || (nnz > 0 && (!col_idx || !val))) return h->fail(TSVD_ERR_ARG, "NULL CSR array");
     if (h->wide) return h->fail(TSVD_ERR_UNSUPPORTED, "sparse inputs must have m >= n (V-first branch) in this version");
-    if (h->world > 1 && h->grp)
-        return h->fail(TSVD_ERR_UNSUPPORTED, "sparse inputs across in-process ranks (the sparse sum needs NCCL)");
     if (row_begin < 0 || row_end > h->m || row_end <= row_begin)
         return h->fail(TSVD_ERR_SHAPE, "row range [%lld, %lld) outside [0, %lld)", (long long)row_begin,
                        (long long)row_end, (long long)h->m);
@@ -2700,7 +2753,7 @@ tsvd_status tsvd_set_csr(tsvd_t h, const int64_t *row_ptr, const int32_t *col_id
     h->graph_l0 = -1;
     h->streaming = false;
     h->m_res = mg;
-    if (h->world > 1) h->coll = COLL_NCCL;  // the length-n vector: ncclAllReduce (bandwidth-bound)
+    if (h->world > 1) h->coll = COLL_NCCL;  // the length-n vector: coll_allreduce (NCCL; bandwidth-bound)
     auto t0 = std::chrono::steady_clock::now();
     if (mem == TSVD_MEM_DEVICE) {
         h->row_ptr_d = const_cast<int64_t *>(row_ptr);
@@ -3139,7 +3192,7 @@ void tsvd_destroy(tsvd_t h) {
                         h->wpart, h->part, h->u64, h->sq_part, h->sig2, h->st, h->stats, h->sym, h->gbar,
                         h->trace_d, h->work, h->tl_d, h->vprev32, h->px_mem, h->y32, h->t32, h->At,
                         h->B0, h->Pm, h->Qm, h->gpart, h->zero64, h->g_hi, h->g_lo, h->pub, h->puby, h->gx_mem,
-                        h->gram_tiles};
+                        h->gram_tiles, h->ar_tmp};
     if (h->cublas) cublasDestroy(h->cublas);
     if (h->trace_f) fclose(h->trace_f);
     for (void *p : dev_ptrs)

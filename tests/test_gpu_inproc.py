@@ -144,29 +144,84 @@ def test_inproc_wide_column_partition():
     _check(A, out, ref, k, col=True)
 
 
-def test_inproc_unsupported_paths_fail_loudly():
-    """Sparse inputs across in-process ranks need NCCL's all-reduce: TSVD_ERR_UNSUPPORTED, no hang."""
+def _run_sparse_ranks(m, n, d, k, eps, V0, world, T, block=0, timeout=600):
+    """Sparse row slabs (each rank generates its own rows of synth.random_csr, as torchrun ranks do)."""
     uid = P.tsvd_get_inproc_id()
-    errs = []
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    out, errors = [None] * world, []
 
     def work(r):
         try:
-            t = P.TSVD(100, 50, 2, 1e-6, rank=r, world=2, uid=uid, device=0)
-            rp = np.arange(0, 51, dtype=np.int64)
-            try:
-                t.set_csr(rp, np.arange(50, dtype=np.int32) % 50, np.ones(50, np.float32), r * 50, r * 50 + 50)
-            except P.TsvdError as e:
-                errs.append(e.status)
+            r0, r1 = _slab(world, r, m)
+            t = P.TSVD(m, n, k, eps, rank=r, world=world, uid=uid, device=0)
+            t.set_option(P.OPT_SM_LIMIT, max(1, (sms // world) * 3 // 4))
+            t.set_option(P.OPT_FIXED_ITERS, T)
+            t.set_option(P.OPT_SPARSE_BLOCK, block)
+            t.set_init(V0)
+            t.set_csr(*synth.random_csr(m, n, d, seed=21, rows=(r0, r1), chunk=512), row_begin=r0, row_end=r1)
+            rc = t.run()
+            U, S, V = t.result()
+            kf, iters, _ = t.info()
+            rep = t.report()
             t.close()
-        except Exception as e:  # pragma: no cover
-            errs.append(repr(e))
+            out[r] = (rc, U, S, V, kf, np.asarray(iters), rep)
+        except Exception as e:
+            errors.append((r, repr(e)))
 
-    th = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(2)]
-    for x in th:
-        x.start()
-    for x in th:
-        x.join(120)
-    assert errs == [P.ERR_UNSUPPORTED] * 2, errs
+    threads = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(world)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join(timeout)
+    assert not errors, errors
+    assert all(o is not None for o in out), "a rank did not finish"
+    return out
+
+
+@pytest.mark.parametrize("world,block", [(2, 0), (2, 512), (4, 700)])
+def test_inproc_sparse_row_partition(world, block):
+    """Sparse CSR row slabs across in-process ranks (each rank's slab sliced into its own CSR/CSC
+    views, the length-n sum of [y_g | w_g] per pass) — forced index blocks (several launches per
+    product, carried sums) included — against the oracle on the full CSR in fixed-T mode (the
+    paper-like spectrum never converges)."""
+    m, n, d, k, eps, T = 6007, 4001, 9, 4, 1e-8, 12
+    full = synth.random_csr(m, n, d, seed=21, chunk=512)
+    V0 = synth.v0_normal(n, k, seed=12)
+    ref = oracle.tsvd_csr(*full, n, k, eps, V0, fixed_T=T)
+    out = _run_sparse_ranks(m, n, d, k, eps, V0, world, T, block)
+    for rc, U, S, V, kf, iters, rep in out:
+        assert rc == P.OK and kf == k and rep["world"] == world
+        assert list(iters[:k]) == [T] * k
+    for r in range(1, world):
+        np.testing.assert_array_equal(out[r][2], out[0][2])
+        np.testing.assert_array_equal(out[r][3], out[0][3])
+    U = np.concatenate([o[1] for o in out])
+    assert_tsvd_close(U, out[0][2], out[0][3], ref, k)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_inproc_explicit_gram(world):
+    """METHOD = 1 across in-process ranks: B0 = sum_g A_g^T A_g (tcgen05 kernel per rank, summed
+    across ranks), iterations row-partitioned over B0 with the in-kernel stamped-word exchange of the
+    y rows, extraction sums reduced per component — against the oracle."""
+    m, n, k, eps = 3001, 517, 4, 1e-8
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(64, 5.0, 0.75), seed=41)
+    V0 = synth.v0_normal(n, k, seed=42)
+    ref = oracle.tsvd(A, k, eps, V0)
+    out = _run_ranks(A, k, eps, V0, world, opts={"method": 1})
+    for o in out:
+        assert o[6]["method"] == "explicit-gram"
+    _check(A, out, ref, k)
+
+
+def test_inproc_nccl_collective_refused():
+    """TSVD_OPT_COLLECTIVE = 1 names NCCL, which in-process ranks do not have: refused at set_comm."""
+    t = P.TSVD(100, 50, 2, 1e-6)
+    t.set_option(P.OPT_COLLECTIVE, 1)
+    with pytest.raises(P.TsvdError) as ei:
+        P.tsvd_set_comm(t.h, 0, 2, P.tsvd_get_inproc_id(), 0)
+    assert ei.value.status == P.ERR_UNSUPPORTED
+    t.close()
 
 
 M2, K2 = 65536, 16
