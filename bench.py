@@ -469,7 +469,9 @@ def main():
         if rt.get("method") == "explicit-gram":  # gb_persist streams the n x n Gram B0 each iteration
             body = [int(iters[l]) for l in range(kf)]
             ps_passes = sum(body)
-            alg_bytes = sum(body[l] * (4.0 * n * n + 12.0 * n * l + 8.0 * n) for l in range(kf))
+            # world > 1: the iterations are row-partitioned over B0, this rank streams its n / world rows
+            nb0 = n * (rank + 1) // world - n * rank // world
+            alg_bytes = sum(body[l] * (4.0 * nb0 * n + 12.0 * nb0 * l + 8.0 * n) for l in range(kf))
             kernel = "gb_persist (explicit Gram: B0 = A^T A streamed per iteration)"
         n1_ms_per_launch = kern_ms / ps["launches"]
         per_launch_bytes = alg_bytes / ps["launches"]

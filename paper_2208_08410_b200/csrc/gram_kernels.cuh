@@ -345,8 +345,12 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     double *red = reinterpret_cast<double *>(bars + kMaxStages);  // [2][NR][NW]
 
     __shared__ int64_t slot_row[kMaxStages];  // row held by each ring slot (-1: no more rows)
-    __shared__ double xch[2];                  // SPLIT: the partner's half dot product
-    __shared__ __align__(8) uint64_t xbar[2];  // SPLIT: arrivals of the partner's value
+    // SPLIT: the partner's half dot product of row j in buffer j % kXb, completion on xbar[j % kXb]
+    // (the lag-one loop reads row j's value one row later, so the partner may already be sending
+    // rows j + 1, j + 2, j + 3: four buffers)
+    constexpr int kXb = 4;
+    __shared__ double xch[kXb];
+    __shared__ __align__(8) uint64_t xbar[kXb];
     const int crank = SPLIT == 2 ? (int)cluster_ctarank() : 0;
     const int part_id = blockIdx.x / SPLIT;
     const int nparts = gridDim.x / SPLIT;
@@ -385,10 +389,8 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-        if (SPLIT == 2) {
-            mbar_init(&xbar[0], 1);
-            mbar_init(&xbar[1], 1);
-        }
+        if (SPLIT == 2)
+            for (int b = 0; b < kXb; ++b) mbar_init(&xbar[b], 1);
         fence_barrier_init();
     }
     __syncthreads();
@@ -512,6 +514,104 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
     };
 
     int run = 0;
+    // SPLIT = 2 Gram pass, lag one row: row i's half dot product goes to the partner right after
+    // its local reduction, and the axpy of row i - 1 — whose partner half has had a whole row's time
+    // to arrive — is done next, re-reading row i - 1 from its ring slot (freed after that axpy).  The
+    // DSMEM round trip (~0.3-0.5 us per row in the exchange-then-wait order) leaves the critical path;
+    // the slot is held one row longer (prefetch depth S - 1 rows).  Same values, same order.
+    if constexpr (SPLIT == 2 && !EXTRACT && !TWO) {
+        double th_prev = 0.0;   // row i - 1: my half dot product (U term included on the owner)
+        float ur_prev = 0.f;    // its U_r entry of this thread's deflation column (owner, tid < l)
+        int64_t grow_prev = -1;
+        auto finish = [&](int j) {  // axpy of row j (slot j % S), then free the slot
+            const int sj = j % S, b = j % kXb;
+            if (tid == 0) mbar_wait_cluster(&xbar[b], (uint32_t)((j / kXb) & 1));
+            __syncthreads();  // the partner's half of row j is in xch[b]
+            const double other = *reinterpret_cast<volatile double *>(&xch[b]);
+            const double t = owner ? th_prev + other : other + th_prev;
+            const float tf = (float)t;
+            const float4 *row = reinterpret_cast<const float4 *>(smem + (size_t)sj * p.stage_bytes);
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                const int idx = k * T + tid;
+                float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (idx < my_n4) {
+                    a = row[idx];
+                    if (tail && c4_0 + idx == p.n4 - 1) {
+                        if (tail < 2) a.y = 0.f;
+                        if (tail < 3) a.z = 0.f;
+                        a.w = 0.f;
+                    }
+                }
+                ya[k].x = fmaf(tf, a.x, ya[k].x);
+                ya[k].y = fmaf(tf, a.y, ya[k].y);
+                ya[k].z = fmaf(tf, a.z, ya[k].z);
+                ya[k].w = fmaf(tf, a.w, ya[k].w);
+            }
+            if (tid < l) wacc += t * (double)ur_prev;
+            if (p.store_t && tid == 0 && owner) {
+                p.u_out[grow_prev] = t;
+                sq += t * t;
+            }
+            if (++run == p.run_rows) {
+                flush();
+                run = 0;
+            }
+            __syncthreads();  // every thread is done with slot sj and xch[b]
+            if (tid == 0) {
+                fence_proxy_async_smem();
+                feed(sj);
+            }
+        };
+        for (int i = 0;; ++i) {
+            const int s = i % S;
+            mbar_wait(&bars[s], (uint32_t)((i / S) & 1));
+            if (i == 0 && p.trace && tid == 0) p.trace[blockIdx.x * 4 + 1] = globaltimer_ns();
+            const int64_t grow = slot_row[s];  // same value in every thread: uniform exit
+            if (grow < 0) {
+                if (i > 0) finish(i - 1);
+                break;
+            }
+            const float4 *row = reinterpret_cast<const float4 *>(smem + (size_t)s * p.stage_bytes);
+            float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                const int idx = k * T + tid;
+                float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (idx < my_n4) {
+                    a = row[idx];
+                    if (tail && c4_0 + idx == p.n4 - 1) {
+                        if (tail < 2) a.y = 0.f;
+                        if (tail < 3) a.z = 0.f;
+                        a.w = 0.f;
+                    }
+                }
+                q0 = fmaf(a.x, vr[k].x, q0);
+                q1 = fmaf(a.y, vr[k].y, q1);
+                q2 = fmaf(a.z, vr[k].z, q2);
+                q3 = fmaf(a.w, vr[k].w, q3);
+            }
+            double part = (double)((q0 + q1) + (q2 + q3));
+            float ur = 0.f;
+            if (tid < l) {
+                ur = reinterpret_cast<const float *>(reinterpret_cast<const unsigned char *>(row) + p.row_bytes)[tid];
+                part -= (double)ur * cval;
+            }
+            part = warp_sum(part);
+            if (lane == 0) red[(i & 1) * NW + warp] = part;
+            __syncthreads();  // row i's partial dots visible
+            const double th = sum_warps<NW>(red + (i & 1) * NW, lane);
+            if (tid == 0) {
+                const int b = i % kXb;
+                mbar_arrive_expect_tx(&xbar[b], (uint32_t)sizeof(double));
+                st_async_f64(peer_xch + b * (uint32_t)sizeof(double), th, peer_xbar + b * (uint32_t)sizeof(uint64_t));
+            }
+            if (i > 0) finish(i - 1);
+            th_prev = th;
+            ur_prev = ur;
+            grow_prev = grow;
+        }
+    } else
     for (int i = 0;; ++i) {
         const int s = i % S;
         mbar_wait(&bars[s], (uint32_t)((i / S) & 1));
@@ -593,11 +693,11 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
             }
         }
         if (SPLIT == 2) {  // half dot products: send mine, wait for the partner's, add in rank order
-            const int b = i & 1;
+            const int b = i % kXb;
             if (tid == 0) {
                 mbar_arrive_expect_tx(&xbar[b], (uint32_t)sizeof(double));  // my arrival + 8 bytes due
                 st_async_f64(peer_xch + b * (uint32_t)sizeof(double), t, peer_xbar + b * (uint32_t)sizeof(uint64_t));
-                mbar_wait_cluster(&xbar[b], (uint32_t)((i >> 1) & 1));
+                mbar_wait_cluster(&xbar[b], (uint32_t)((i / kXb) & 1));
             }
             __syncthreads();
             const double other = *reinterpret_cast<volatile double *>(&xch[b]);
