@@ -6,8 +6,9 @@
 // assumes U^T U = I (reading R7).  Exact instead: with B0 = A^T A, P = A^T U (n x l) and Q = U^T U,
 //     X'^T X' = B0 - P S V^T - V S P^T + V S Q S V^T,
 // so  y = B0 v - P c - V g,   c = S (V^T v),   g = S (P^T v - Q c).
-// B0 is built once (three TF32 tensor-core GEMMs of a hi/lo split of A: fp32-level products, the
-// paper's Alg. 3 Gram), P and Q grow by one column per component from the extraction pass
+// B0 is built once (the paper's Alg. 3 Gram: the tcgen05 3xTF32 CTA-pair kernel of gram_tc.cuh,
+// fp32-level products; TSVD_GRAM_CUBLAS=1 keeps round 1's three cuBLAS TF32 GEMMs of a hi/lo split
+// of A), P and Q grow by one column per component from the extraction pass
 // (u = A v / sigma, P[:, l] = A^T u, Q[l, :] = U^T u: one pass of the fused kernel with c = 0).
 // Per iteration the n x n B0 is streamed once (n^2 * 4 bytes instead of 4 m n): gb_persist runs all
 // iterations of a component in one cooperative kernel, each CTA owning whole rows of B0, so y_r is
@@ -17,7 +18,8 @@
 
 namespace tsvd {
 
-// hi/lo split of fp32 A into two TF32-exact fp32 arrays: hi = rna_tf32(a), lo = rna_tf32(a - hi);
+// (round-1 cuBLAS path, TSVD_GRAM_CUBLAS=1) hi/lo split of fp32 A into two TF32-exact fp32 arrays:
+// hi = rna_tf32(a), lo = rna_tf32(a - hi);
 // hi hi^T + hi lo^T + lo hi^T recovers a a^T to ~2^-21 relative (the three-term TF32 product)
 __global__ void split_tf32(const float *__restrict__ A, int64_t rows, int64_t cols, int64_t lda,
                            float *__restrict__ hi, float *__restrict__ lo) {
@@ -309,15 +311,27 @@ __global__ void __launch_bounds__(T) gb_persist(const GbParams p) {
         const unsigned sxn = xe + 1u;  // world > 1: this iteration's exchange stamp
         const double cv = tid < l ? cvec[tid] : 0.0, gv = tid < l ? gvec[tid] : 0.0;
         double a_yy = 0.0, a_vy = 0.0, a_vt = 0.0, a_pt = 0.0;
-        for (int k = 0; k < nr; ++k) {
-            // deflation terms of this row, loaded while the row lands (rows are known per slot)
-            mbar_wait(&bars[cs], cph);
-            const int64_t r = slot_row[cs];
-            double vri = 0.0, pri = 0.0;
+        // the row-dependent loads besides the TMA row (V_r, P_r deflation entries, y_cur[r] of the
+        // stop test) are issued one row ahead: slot_row of the next slot was written by the producer
+        // at least one block barrier ago when S >= 3 (it feeds a slot right after the barrier of the
+        // row that freed it), so their global-memory latency no longer sits between the row landing
+        // and its dot product (per row 1.75 us against 1.5 us of HBM time before)
+        double vri_n = 0.0, pri_n = 0.0, ycr_n = 0.0;
+        auto row_loads = [&](int slot) {
+            const int64_t rr = slot_row[slot];
             if (tid < l) {
-                vri = p.V[r * p.ldv + tid];
-                pri = (double)p.P[r * p.ldp + tid];
+                vri_n = p.V[rr * p.ldv + tid];
+                pri_n = (double)p.P[rr * p.ldp + tid];
             }
+            if (tid == 0) ycr_n = __ldcg(ycur + rr);
+        };
+        if (nr > 0) row_loads(cs);
+        for (int k = 0; k < nr; ++k) {
+            const int64_t r = slot_row[cs];
+            if (S < 3 && k > 0) row_loads(cs);  // (a 2-stage ring: the next row's slot may be unwritten)
+            const double vri = vri_n, pri = pri_n, ycr = ycr_n;
+            if (S >= 3 && k + 1 < nr) row_loads(cs + 1 == S ? 0 : cs + 1);
+            mbar_wait(&bars[cs], cph);
             const float4 *row = reinterpret_cast<const float4 *>(smem + (size_t)cs * p.stage_bytes);
             float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
 #pragma unroll
@@ -356,7 +370,7 @@ __global__ void __launch_bounds__(T) gb_persist(const GbParams p) {
             if (tid == 0) {
                 __stcg(ynew + r, y);
                 a_yy += y * y;
-                a_vy += (__ldcg(ycur + r) * inv) * y;
+                a_vy += (ycr * inv) * y;
             }
             if (mx && tid < p.world)  // y_r to every rank (one thread per destination rank)
                 ll_send(p.yx[tid] + (int64_t)(sxn & 1u) * p.n + r, sxn, y);

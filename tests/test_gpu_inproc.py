@@ -38,7 +38,7 @@ def _slab(world, rank, m):
     return r0, r0 + base + (1 if rank < rem else 0)
 
 
-def _run_ranks(A, k, eps, V0, world, col=False, opts=None, timeout=600, sm_per_rank=None):
+def _run_ranks(A, k, eps, V0, world, col=False, opts=None, timeout=600, sm_per_rank=None, host=False):
     """Every rank in its own thread; returns [(rc, U_slab, S, V, kf, iters, report)] in rank order.
     Each rank gets 3/4 of its share of the SMs (sm_per_rank overrides) and one CTA per SM: the ranks'
     kernels spin on each other's exchange words, so every rank's grid must find room while the others
@@ -62,6 +62,8 @@ def _run_ranks(A, k, eps, V0, world, col=False, opts=None, timeout=600, sm_per_r
             t.set_init(V0)
             if col:  # (m, cols) with unit row stride: this rank's columns of the column-major matrix
                 t.set_dense(torch.from_numpy(np.ascontiguousarray(A[:, r0:r1].T)).cuda().t(), r0, r1)
+            elif host:  # pinned host slab (out-of-memory streaming reads it every pass)
+                t.set_dense(torch.from_numpy(np.ascontiguousarray(A[r0:r1])).pin_memory(), r0, r1)
             else:
                 t.set_dense(torch.from_numpy(np.ascontiguousarray(A[r0:r1])).cuda(), r0, r1)
             rc = t.run()
@@ -131,6 +133,36 @@ def test_inproc_ranks_max_iter_not_converged():
     np.testing.assert_array_equal(out[1][2], out[0][2])
     U = np.concatenate([o[1] for o in out])
     assert_tsvd_close(U, out[0][2], out[0][3], ref, k)
+
+
+def test_inproc_streamed_out_of_memory():
+    """Out of memory, degree 1, across ranks: each rank's slab in pinned host memory,
+    a resident prefix of 100 rows and the rest streamed in 333-row batches through a 2-slot ring,
+    every pass — the per-iteration peer all-reduce between the streamed passes."""
+    m, n, k, eps = 2000, 384, 3, 1e-8
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(96, 6.0, 0.7), seed=51)
+    V0 = synth.v0_normal(n, k, seed=52)
+    ref = oracle.tsvd(A, k, eps, V0)
+    row_bytes = ((n + 3) // 4) * 16
+    out = _run_ranks(A, k, eps, V0, 2, host=True,
+                     opts={"placement": P.PLACEMENT_STREAM, "resident_bytes": 100 * row_bytes,
+                           "batch_rows": 333, "queue_depth": 2})
+    for o in out:
+        pl = o[6]["placement"]
+        assert pl["streaming"] is True and pl["resident_rows"] == 100 and pl["streamed_bytes"] > 0
+    _check(A, out, ref, k)
+
+
+def test_inproc_v_on_host():
+    """The heavy co-factor V on the host (TSVD_OPT_V_PLACEMENT = 1) on every rank."""
+    m, n, k, eps = 3001, 517, 4, 1e-8
+    A = synth.known_spectrum_qr(m, n, synth.geometric_spectrum(64, 5.0, 0.75), seed=61)
+    V0 = synth.v0_normal(n, k, seed=62)
+    ref = oracle.tsvd(A, k, eps, V0)
+    out = _run_ranks(A, k, eps, V0, 2, opts={"v_placement": 1})
+    for o in out:
+        assert o[6]["placement"]["v_on_host"] is True
+    _check(A, out, ref, k)
 
 
 def test_inproc_wide_column_partition():
