@@ -770,7 +770,12 @@ static tsvd_status setup_px(tsvd_t h) {
     const int SL = (int)round_up(per + h->kpad, 4);
     const size_t bytes = (size_t)2 * h->world * G * SL * sizeof(ulonglong2);
     CK(cudaMalloc((void **)&h->px_mem, bytes));
-    CK(cudaMemset(h->px_mem, 0, bytes));
+    // zeroed on the handle's stream and waited for BEFORE the pointer is shared: a plain cudaMemset
+    // runs on the legacy stream, unordered with the peers' (non-blocking) streams, and a late memset
+    // wiped stamped words a peer had already written (the receiver then waited out the 30 s timeout;
+    // seen with in-process ranks, where the window is widest)
+    CK(cudaMemsetAsync(h->px_mem, 0, bytes, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
     void *base[kMaxRanks] = {};
     bool ok = true;
     std::string err;
@@ -882,7 +887,8 @@ static tsvd_status setup_peer(tsvd_t h) {
     const size_t flag_off = (size_t)2 * slot * sizeof(double);
     const size_t bytes = flag_off + 256;
     CK(cudaMalloc((void **)&h->sym, bytes));
-    CK(cudaMemset(h->sym, 0, bytes));
+    CK(cudaMemsetAsync(h->sym, 0, bytes, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
     void *base[kMaxRanks] = {};
     bool ok = true;
     TRY(coll_share(h, h->sym, base, h->peer_map, ok, h->peer_error));
@@ -1856,7 +1862,8 @@ static tsvd_status setup_gx(tsvd_t h) {
     if (h->gx_mem || h->world > kMaxRanks || h->k > 129) return TSVD_OK;
     const size_t ny = (size_t)2 * h->n, ns = (size_t)2 * h->world * h->grid_gb * (2 + 2 * h->k);
     CK(cudaMalloc((void **)&h->gx_mem, (ny + ns) * sizeof(ulonglong2)));
-    CK(cudaMemset(h->gx_mem, 0, (ny + ns) * sizeof(ulonglong2)));
+    CK(cudaMemsetAsync(h->gx_mem, 0, (ny + ns) * sizeof(ulonglong2), h->stream));
+    CK(cudaStreamSynchronize(h->stream));
     void *base[kMaxRanks] = {};
     bool ok = true;
     std::string err;
