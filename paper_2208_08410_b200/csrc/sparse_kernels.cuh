@@ -102,7 +102,10 @@ struct SpParams {
 // the others only carry their partial sums.  Dynamic shared memory (MODE_T, LAST): l * (kSpThreads + 1)
 // doubles (per-thread w partials, c).
 template <int MODE, bool LAST>
-__global__ void __launch_bounds__(kSpThreads) sp_pass(const SpParams p) {
+#ifndef TSVD_SP_MINB
+#define TSVD_SP_MINB 1
+#endif
+__global__ void __launch_bounds__(kSpThreads, TSVD_SP_MINB) sp_pass(const SpParams p) {
     extern __shared__ double wsm[];
     __shared__ double red[kSpWarps];
     const LoopState *st = p.st;
