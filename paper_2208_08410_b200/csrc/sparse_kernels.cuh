@@ -102,6 +102,9 @@ struct SpParams {
 // the others only carry their partial sums.  Dynamic shared memory (MODE_T, LAST): l * (kSpThreads + 1)
 // doubles (per-thread w partials, c).
 template <int MODE, bool LAST>
+#ifndef TSVD_SP_ACC_CS
+#define TSVD_SP_ACC_CS 0
+#endif
 #ifndef TSVD_SP_MINB
 #define TSVD_SP_MINB 1
 #endif
@@ -135,7 +138,11 @@ __global__ void __launch_bounds__(kSpThreads, TSVD_SP_MINB) sp_pass(const SpPara
         const int64_t q = 32 * j + lane;
         // this lane's segment (last block) or its position in the next block; -1: past the end
         const int32_t s = q < V.segs ? __ldcs(perm + q) : -1;
+#if TSVD_SP_ACC_CS
+        const double carried = (carry_in && s >= 0) ? __ldcs(p.acc[p.phase & 1] + q) : 0.0;  // coalesced
+#else
         const double carried = (carry_in && s >= 0) ? __ldcg(p.acc[p.phase & 1] + q) : 0.0;  // coalesced
+#endif
         const int32_t e0 = __ldg(soff + j), e1 = __ldg(soff + j + 1);  // slice entries [e0, e1), 32 wide
         double sum = 0.0;
         for (int32_t e = e0; e < e1; e += 32 * kSpBatch) {
@@ -156,7 +163,11 @@ __global__ void __launch_bounds__(kSpThreads, TSVD_SP_MINB) sp_pass(const SpPara
         if (s < 0) continue;
         if (carry_in) sum = carried + sum;  // blocks in order
         if (!LAST) {
+#if TSVD_SP_ACC_CS
+            __stcs(p.acc[(p.phase + 1) & 1] + s, sum);  // evict-first: keep L2 for the gathered block
+#else
             p.acc[(p.phase + 1) & 1][s] = sum;  // at the segment's position in the next block
+#endif
             continue;
         }
         if (MODE == MODE_Y) {
