@@ -321,6 +321,9 @@ __device__ __forceinline__ void set_cond(unsigned long long h, int use, unsigned
 // ---------------------------------------------------------------- N1: fused Gram-vector pass
 // Grid: one persistent CTA per (SM x CTAs/SM), each owning a contiguous row range.
 // Block: T threads; thread `tid` owns float4 columns {k*T + tid : k < NV} of every row.
+#ifndef TSVD_TWO_TMEM_F4
+#define TSVD_TWO_TMEM_F4 4   // float4 of v_prev per tcgen05.ld in the two-vector pass (2 or 4; A/B)
+#endif
 // SPLIT = 2 (n > 4*T*NV, up to 32768): a 2-CTA cluster shares each row range, CTA rank q staging
 // and owning the q-th half of every row; the two half dot products are exchanged through
 // distributed shared memory (remote store + remote mbarrier arrive) and added in rank order,
@@ -624,7 +627,11 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
         float4 a[NV];
         float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
         float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;  // TWO: dot with v_prev
-        uint32_t vt8[8];                                // kTmemV: two float4 of v_prev from TMEM
+        // kTmemV: KV float4 of v_prev per tcgen05.ld (one wait::ld per KV float4 of the row): 4 for the
+        // 256 x 16 variant (240 registers, no spill; two-vector pass 699.7 -> 681.2 us in ncu at C2),
+        // 2 for 512 x 8 (128-register budget: 4 spills)
+        constexpr int KV = (T == 256 && NV == 16) ? TSVD_TWO_TMEM_F4 : 2;
+        uint32_t vt8[4 * KV];
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
             const int idx = k * T + tid;
@@ -642,17 +649,29 @@ __global__ void __launch_bounds__(T) gv_fused(const GvParams p) {
             q1 = fmaf(a[k].y, vr[k].y, q1);
             q2 = fmaf(a[k].z, vr[k].z, q2);
             q3 = fmaf(a[k].w, vr[k].w, q3);
-            if (kTmemV) {  // columns 4k..4k+3 of this thread's v_prev, two float4 per TMEM load
-                if ((k & 1) == 0) {
-                    asm volatile(
-                        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t"
-                        "tcgen05.wait::ld.sync.aligned;"
-                        : "=r"(vt8[0]), "=r"(vt8[1]), "=r"(vt8[2]), "=r"(vt8[3]), "=r"(vt8[4]), "=r"(vt8[5]),
-                          "=r"(vt8[6]), "=r"(vt8[7])
-                        : "r"(tm_addr + (uint32_t)(4 * k))
-                        : "memory");
+            if (kTmemV) {  // columns 4k..4k+3 of this thread's v_prev, KV float4 per TMEM load
+                if ((k % KV) == 0) {
+                    if constexpr (KV == 4) {
+                        asm volatile(
+                            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+                            "%12, %13, %14, %15}, [%16];\n\t"
+                            "tcgen05.wait::ld.sync.aligned;"
+                            : "=r"(vt8[0]), "=r"(vt8[1]), "=r"(vt8[2]), "=r"(vt8[3]), "=r"(vt8[4]), "=r"(vt8[5]),
+                              "=r"(vt8[6]), "=r"(vt8[7]), "=r"(vt8[8]), "=r"(vt8[9]), "=r"(vt8[10]), "=r"(vt8[11]),
+                              "=r"(vt8[12]), "=r"(vt8[13]), "=r"(vt8[14]), "=r"(vt8[15])
+                            : "r"(tm_addr + (uint32_t)(4 * k))
+                            : "memory");
+                    } else {
+                        asm volatile(
+                            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t"
+                            "tcgen05.wait::ld.sync.aligned;"
+                            : "=r"(vt8[0]), "=r"(vt8[1]), "=r"(vt8[2]), "=r"(vt8[3]), "=r"(vt8[4]), "=r"(vt8[5]),
+                              "=r"(vt8[6]), "=r"(vt8[7])
+                            : "r"(tm_addr + (uint32_t)(4 * k))
+                            : "memory");
+                    }
                 }
-                const int o = 4 * (k & 1);
+                const int o = 4 * (k % KV);
                 p0 = fmaf(a[k].x, __uint_as_float(vt8[o + 0]), p0);
                 p1 = fmaf(a[k].y, __uint_as_float(vt8[o + 1]), p1);
                 p2 = fmaf(a[k].z, __uint_as_float(vt8[o + 2]), p2);
