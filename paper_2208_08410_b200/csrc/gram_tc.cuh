@@ -608,32 +608,38 @@ __global__ void __launch_bounds__(kGtThreads, 1)
 // tcgen05.st; all three MMAs take A from TMEM (tcgen05.mma ... [d], [a_tmem], b_desc), so the
 // shared-memory operand traffic is B only (raw twice, lo once).  TMEM: 2 accumulators of N = 192
 // columns + 4 slots x 32 columns of A = 512.  Tiles are 256 (M) x 192 (N), those touching j >= i.
-constexpr int kG3M = 256, kG3N = 192;                              // pair tile
-constexpr int kG3AHalf = 128, kG3BHalf = 96;                       // per-CTA operand columns
+constexpr int kG3M = 256;                                          // pair tile rows (M)
+constexpr int kG3AHalf = 128;                                      // per-CTA A columns
 constexpr int kG3BK = 16;
 static_assert(kG3BK == kGtBK, "the swizzled tensor map box is 32 x kGtBK");
 constexpr int kG3Stages = 8;
 constexpr int kG3ABytes = kG3AHalf * kG3BK * 4;                    // 8 KB plain [k][m]
-constexpr int kG3BBytes = (kG3BHalf / 32) * kG3BK * 128;           // 6 KB: 3 swizzled boxes of 32 x BK
-constexpr int kG3StageBytes = kG3ABytes + 2 * kG3BBytes;           // A raw, B raw, B lo: 20 KB
-constexpr int kG3Smem = kG3Stages * kG3StageBytes + 1024 + 512;
-constexpr int kG3Slots = 4;                                        // TMEM A ring (stages)
 constexpr int kG3SlotCols = 2 * (kG3BK / 8) * 8;                   // raw + lo per 8-row k-group: 32
-constexpr int kG3AccCols = kG3N;                                   // one accumulator
-constexpr int kG3RingCol = 2 * kG3AccCols;                         // 384: A ring after the two accumulators
-static_assert(kG3RingCol + kG3Slots * kG3SlotCols <= 512, "TMEM budget");
 constexpr int kG3ChunkStages = 512 / kG3BK;
-// instruction descriptor: D fp32, A / B tf32, A from TMEM (K-major), B MN-major, M = 256, N = 192
-constexpr uint32_t kG3Idesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
-                              ((uint32_t)(kG3N >> 3) << 17) | ((uint32_t)(kG3M >> 4) << 24);
+// the N-dependent layout: N = 192 (two accumulators + a 4-slot A ring) or 128 (8 slots)
+template <int N>
+struct G3 {
+    static constexpr int BHalf = N / 2;                            // per-CTA B columns
+    static constexpr int BBytes = (BHalf / 32) * kG3BK * 128;      // swizzled boxes of 32 x BK
+    static constexpr int StageBytes = kG3ABytes + 2 * BBytes;      // A raw, B raw, B lo
+    static constexpr int Smem = kG3Stages * StageBytes + 1024 + 512;
+    static constexpr int RingCol = 2 * N;                          // A ring after the two accumulators
+    static constexpr int Slots = (512 - RingCol) / kG3SlotCols;
+    static_assert(Slots >= 2 && BHalf % 32 == 0, "TMEM budget / TMA box width");
+    // instruction descriptor: D fp32, A / B tf32, A from TMEM (K-major), B MN-major, M = 256, N
+    static constexpr uint32_t Idesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
+                                      ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kG3M >> 4) << 24);
+};
 
-__device__ __forceinline__ void g3_mma(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t accumulate) {
+__device__ __forceinline__ void g3_mma(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                       uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "r"(tmem_a), "l"(db), "r"(kG3Idesc), "r"(accumulate)
+        "r"(tmem_a), "l"(db), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+
 __device__ __forceinline__ void g3_st16(uint32_t taddr, const float (&v)[16]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
@@ -646,15 +652,16 @@ __device__ __forceinline__ void g3_st16(uint32_t taddr, const float (&v)[16]) {
         : "memory");
 }
 
+template <int N>
 __global__ void __launch_bounds__(kGtThreads, 1)
     gram_tc3(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_a, const GtParams p) {
     extern __shared__ unsigned char g3_raw[];
     unsigned char *smem = (unsigned char *)(((uintptr_t)g3_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kG3Stages * kG3StageBytes);  // own TMA landed
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kG3Stages * G3<N>::StageBytes);  // own TMA landed
     uint64_t *conv = full + kG3Stages;      // leader: both CTAs' B lo + TMEM A slot written (count 2)
     uint64_t *empty = conv + kG3Stages;     // the stage's MMAs completed (multicast commit): smem stage free
     uint64_t *tfree = empty + kG3Stages;    // [slots] the TMEM A slot's MMAs completed (multicast commit)
-    uint64_t *dfull = tfree + kG3Slots;     // [2] accumulator b holds a finished job (multicast commit)
+    uint64_t *dfull = tfree + G3<N>::Slots;     // [2] accumulator b holds a finished job (multicast commit)
     uint64_t *dempty = dfull + 2;           // [2] leader: both epilogues folded accumulator b (count 2)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(dempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -669,7 +676,7 @@ __global__ void __launch_bounds__(kGtThreads, 1)
             mbar_init(&conv[s], 2);
             mbar_init(&empty[s], 1);
         }
-        for (int s = 0; s < kG3Slots; ++s) mbar_init(&tfree[s], 1);
+        for (int s = 0; s < G3<N>::Slots; ++s) mbar_init(&tfree[s], 1);
         for (int b = 0; b < 2; ++b) {
             mbar_init(&dfull[b], 1);
             mbar_init(&dempty[b], 2);
@@ -708,13 +715,13 @@ __global__ void __launch_bounds__(kGtThreads, 1)
             uint32_t ph = 0;
             G3_FOR_JOBS({
                 const int ca = tile.x * kG3M + (int)rank * kG3AHalf;
-                const int cb = tile.y * kG3N + (int)rank * kG3BHalf;
+                const int cb = tile.y * N + (int)rank * G3<N>::BHalf;
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[s], ph ^ 1u);
-                    unsigned char *st = smem + (size_t)s * kG3StageBytes;
-                    mbar_arrive_expect_tx(&full[s], (uint32_t)(kG3ABytes + kG3BBytes));
+                    unsigned char *st = smem + (size_t)s * G3<N>::StageBytes;
+                    mbar_arrive_expect_tx(&full[s], (uint32_t)(kG3ABytes + G3<N>::BBytes));
                     gt_tma_2d(st, &map_a, ca, kb * kG3BK, &full[s]);
-                    for (int c = 0; c < kG3BHalf / 32; ++c)
+                    for (int c = 0; c < G3<N>::BHalf / 32; ++c)
                         gt_tma_2d(st + kG3ABytes + c * (kG3BK * 128), &map_b, cb + 32 * c, kb * kG3BK, &full[s]);
                     if (++s == kG3Stages) {
                         s = 0;
@@ -730,24 +737,24 @@ __global__ void __launch_bounds__(kGtThreads, 1)
             uint32_t dph[2] = {0u, 0u};
             int buf = 0;
             G3_FOR_JOBS({
-                const uint32_t dacc = tmem + (uint32_t)(buf * kG3AccCols);
+                const uint32_t dacc = tmem + (uint32_t)(buf * N);
                 mbar_wait(&dempty[buf], dph[buf] ^ 1u);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&conv[s], ph);  // both CTAs: B lo in smem, A raw / lo in TMEM slot
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint32_t b_raw = gt_smem(smem + (size_t)s * kG3StageBytes + kG3ABytes);
-                    const uint32_t b_lo = b_raw + kG3BBytes;
-                    const uint32_t ta = tmem + (uint32_t)(kG3RingCol + slot * kG3SlotCols);
+                    const uint32_t b_raw = gt_smem(smem + (size_t)s * G3<N>::StageBytes + kG3ABytes);
+                    const uint32_t b_lo = b_raw + G3<N>::BBytes;
+                    const uint32_t ta = tmem + (uint32_t)(G3<N>::RingCol + slot * kG3SlotCols);
 #pragma unroll
                     for (int kk = 0; kk < kG3BK / 8; ++kk) {
                         const uint32_t ko = kk * 1024;  // 8 rows of 128 B
                         const uint64_t db = gt_desc(b_raw + ko, kG3BK * 128, 512);
                         const uint64_t dbl = gt_desc(b_lo + ko, kG3BK * 128, 512);
                         const uint32_t a_raw = ta + (uint32_t)(kk * 16), a_lo = a_raw + 8;
-                        g3_mma(dacc, a_raw, db, (kb > kb0 || kk > 0) ? 1u : 0u);  // hi·hi
-                        g3_mma(dacc, a_raw, dbl, 1u);                             // hi·lo
-                        g3_mma(dacc, a_lo, db, 1u);                               // lo·hi
+                        g3_mma(dacc, a_raw, db, G3<N>::Idesc, (kb > kb0 || kk > 0) ? 1u : 0u);  // hi·hi
+                        g3_mma(dacc, a_raw, dbl, G3<N>::Idesc, 1u);                             // hi·lo
+                        g3_mma(dacc, a_lo, db, G3<N>::Idesc, 1u);                               // lo·hi
                     }
                     g2_commit_both(&empty[s]);     // smem stage free in both CTAs
                     g2_commit_both(&tfree[slot]);  // TMEM A slot free in both CTAs
@@ -755,7 +762,7 @@ __global__ void __launch_bounds__(kGtThreads, 1)
                         s = 0;
                         ph ^= 1u;
                     }
-                    if (++slot == kG3Slots) slot = 0;
+                    if (++slot == G3<N>::Slots) slot = 0;
                 }
                 g2_commit_both(&dfull[buf]);
                 dph[buf] ^= 1u;
@@ -773,7 +780,7 @@ __global__ void __launch_bounds__(kGtThreads, 1)
             (void)tile;
             for (int kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(&full[s], ph);
-                const uint32_t st = gt_smem(smem + (size_t)s * kG3StageBytes);
+                const uint32_t st = gt_smem(smem + (size_t)s * G3<N>::StageBytes);
                 // A: row m, k = 0..15 from the plain [k][m] tile (loads issued first)
                 float r0[16], r1[16];  // per 8-row k-group: raw k0..7, lo k0..7
 #pragma unroll
@@ -782,15 +789,15 @@ __global__ void __launch_bounds__(kGtThreads, 1)
                     r1[e] = lds32(st + 4u * (uint32_t)((8 + e) * kG3AHalf + m));
                 }
                 // B: lo parts next to the raw ones (same swizzled positions)
-                gt_convert<3>(st + kG3ABytes, st + kG3ABytes + kG3BBytes, ct, kGtConv, kG3BBytes / 16);
+                gt_convert<(G3<N>::BBytes / 16 + kGtConv - 1) / kGtConv>(st + kG3ABytes, st + kG3ABytes + G3<N>::BBytes, ct, kGtConv, G3<N>::BBytes / 16);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                     r0[8 + e] = gt_lo(r0[e]);
                     r1[8 + e] = gt_lo(r1[e]);
                 }
                 // the slot's previous MMAs must have completed before it is overwritten
-                if (seq >= kG3Slots) mbar_wait(&tfree[slot], (uint32_t)((seq / kG3Slots - 1) & 1));
-                const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(kG3RingCol + slot * kG3SlotCols);
+                if (seq >= G3<N>::Slots) mbar_wait(&tfree[slot], (uint32_t)((seq / G3<N>::Slots - 1) & 1));
+                const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(G3<N>::RingCol + slot * kG3SlotCols);
                 g3_st16(ta, r0);
                 g3_st16(ta + 16, r1);
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -802,7 +809,7 @@ __global__ void __launch_bounds__(kGtThreads, 1)
                     s = 0;
                     ph ^= 1u;
                 }
-                if (++slot == kG3Slots) slot = 0;
+                if (++slot == G3<N>::Slots) slot = 0;
                 ++seq;
             }
         })
@@ -815,15 +822,15 @@ __global__ void __launch_bounds__(kGtThreads, 1)
         G3_FOR_JOBS({
             (void)kb1;
             const int64_t i = (int64_t)tile.x * kG3M + (int64_t)rank * kG3AHalf + 32 * q + lane;
-            const int64_t j0 = (int64_t)tile.y * kG3N;
+            const int64_t j0 = (int64_t)tile.y * N;
             mbar_wait(&dfull[buf], dph[buf]);
             dph[buf] ^= 1u;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const bool first = k == 0;
 #pragma unroll 1
-            for (int c = 0; c < kG3N / 32; ++c) {
+            for (int c = 0; c < N / 32; ++c) {
                 uint32_t v[32];
-                const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * kG3AccCols + 32 * c);
+                const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * N + 32 * c);
                 gt_ld32(taddr, v);
                 gt_fold_t(p.B, p.ldb, p.n, i, j0 + 32 * c, v, first);
             }

@@ -1653,13 +1653,13 @@ static std::vector<int2> gram_tiles2(int64_t n) {
 }
 
 // ... and for the A-in-TMEM pair kernel: 256 (M) x 192 (N) tiles touching j >= i
-static std::vector<int2> gram_tiles3(int64_t n) {
-    const int nI = (int)((n + kG3M - 1) / kG3M), nJ = (int)((n + kG3N - 1) / kG3N);
+static std::vector<int2> gram_tiles3(int64_t n, int N) {
+    const int nI = (int)((n + kG3M - 1) / kG3M), nJ = (int)((n + N - 1) / N);
     std::vector<int2> t;
     for (int I0 = 0; I0 < nI; I0 += 4)
         for (int J = 0; J < nJ; ++J)
             for (int I = I0; I < std::min(nI, I0 + 4); ++I)
-                if ((int64_t)kG3N * J + kG3N - 1 >= (int64_t)kG3M * I) t.push_back(make_int2(I, J));
+                if ((int64_t)N * J + N - 1 >= (int64_t)kG3M * I) t.push_back(make_int2(I, J));
     return t;
 }
 
@@ -1710,7 +1710,8 @@ static tsvd_status build_gram(tsvd_t h) {
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return h->fail(TSVD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     }
-    // default: the CTA-pair kernel (gram_tc2).  A/B: TSVD_GRAM_TC=3 the pair kernel with A in TMEM
+    // default: the CTA-pair kernel (gram_tc2).  A/B: TSVD_GRAM_TC=3 (N = 192) / 4 (N = 128, 8 TMEM
+    // slots) the pair kernel with A in TMEM
     // (fewer shared-memory bytes, but measured 5-10 % slower: 98 vs 88-93 ms at C2, the box's power
     // cap sets the clock under this tensor load), TSVD_GRAM_TC=1 (or LO_GMEM) the single-CTA kernel
     int variant = 2;
@@ -1718,7 +1719,8 @@ static tsvd_status build_gram(tsvd_t h) {
     if (getenv("TSVD_GRAM_TC1") || lo_gmem || h->sms < 2) variant = 1;
     const bool pair = variant >= 2;
     if (h->gram_n != n || h->gram_pair != variant) {
-        const std::vector<int2> tiles = variant == 3 ? gram_tiles3(n) : variant == 2 ? gram_tiles2(n) : gram_tiles(n);
+        const std::vector<int2> tiles = variant == 4 ? gram_tiles3(n, 128) : variant == 3 ? gram_tiles3(n, 192)
+                                      : variant == 2 ? gram_tiles2(n) : gram_tiles(n);
         h->gram_pair = variant;
         cudaFree(h->gram_tiles);
         h->gram_tiles = nullptr;
@@ -1730,7 +1732,8 @@ static tsvd_status build_gram(tsvd_t h) {
         CK(cudaFuncSetAttribute(gram_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGtSmem));
         CK(cudaFuncSetAttribute(gram_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, kG2Smem));
         CK(cudaFuncSetAttribute(gram_tc2, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
-        CK(cudaFuncSetAttribute(gram_tc3, cudaFuncAttributeMaxDynamicSharedMemorySize, kG3Smem));
+        CK(cudaFuncSetAttribute(gram_tc3<192>, cudaFuncAttributeMaxDynamicSharedMemorySize, G3<192>::Smem));
+        CK(cudaFuncSetAttribute(gram_tc3<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, G3<128>::Smem));
     }
     GtParams p{};
     p.tiles = h->gram_tiles;
@@ -1749,11 +1752,11 @@ static tsvd_status build_gram(tsvd_t h) {
         attr[0].val.clusterDim.z = 1;
         cfg.gridDim = dim3(G);
         cfg.blockDim = dim3(kGtThreads);
-        cfg.dynamicSmemBytes = variant == 3 ? kG3Smem : kG2Smem;
+        cfg.dynamicSmemBytes = variant == 4 ? G3<128>::Smem : variant == 3 ? G3<192>::Smem : kG2Smem;
         cfg.stream = h->stream;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (variant == 3) {
+        if (variant >= 3) {
             // A half: plain [k][m] boxes of 128 columns x 16 rows (read by the converter, not the MMA)
             CUtensorMap map_a;
             const cuuint32_t box_a[2] = {(cuuint32_t)kG3AHalf, (cuuint32_t)kG3BK};
@@ -1761,7 +1764,8 @@ static tsvd_status build_gram(tsvd_t h) {
                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) return h->fail(TSVD_ERR_CUDA, "cuTensorMapEncodeTiled (A half) failed (%d)", (int)r);
-            CK(cudaLaunchKernelEx(&cfg, gram_tc3, map, map_a, p));
+            if (variant == 4) CK(cudaLaunchKernelEx(&cfg, gram_tc3<128>, map, map_a, p));
+            else CK(cudaLaunchKernelEx(&cfg, gram_tc3<192>, map, map_a, p));
         } else {
             CK(cudaLaunchKernelEx(&cfg, gram_tc2, map, p));
         }

@@ -440,9 +440,10 @@ def test_explicit_gram_parity(m, n, k, T):
 @pytest.mark.parametrize("nb", [3, 5])
 def test_explicit_gram_symmetric_schedule(nb, monkeypatch):
     """The Gram's symmetric task schedule (only the blocks on or above the diagonal are
-    multiplied, the strictly-lower ones mirrored), for every kernel variant: the default tcgen05 CTA-
-    pair kernel with A in tensor memory (256 x 192 tiles touching j >= i), the pair kernel with both
-    operands in shared memory (TSVD_GRAM_TC=2: 256 x 256 tiles with J >= I), the single-CTA kernel
+    multiplied, the strictly-lower ones mirrored), for every kernel variant: the tcgen05 CTA-pair
+    kernels with A in tensor memory (TSVD_GRAM_TC=3 / 4: 256 x 192 / 256 x 128 tiles touching
+    j >= i), the default pair kernel with both operands in shared memory (TSVD_GRAM_TC=2: 256 x 256
+    tiles with J >= I), the single-CTA kernel
     (TSVD_GRAM_TC=1: 128 x 256 tiles touching the upper triangle) and the round-1 cuBLAS block
     schedule (TSVD_GRAM_CUBLAS=1: n_b(n_b+1)/2 block products) with ragged blocks — all against the
     oracle and against each other."""
@@ -456,7 +457,7 @@ def test_explicit_gram_symmetric_schedule(nb, monkeypatch):
         return sum(1 for I in range(nI) for J in range(nJ) if bn * J + bn - 1 >= bm * I), nI * nJ
 
     runs = {}
-    for variant, (bm, bn) in ((3, (256, 192)), (2, (256, 256)), (1, (128, 256))):
+    for variant, (bm, bn) in ((4, (256, 128)), (3, (256, 192)), (2, (256, 256)), (1, (128, 256))):
         monkeypatch.setenv("TSVD_GRAM_TC", str(variant))
         r = _gpu_tsvd(A, k, 1e-6, V0, method=1)
         want, full = tiles(bm, bn)
@@ -464,7 +465,7 @@ def test_explicit_gram_symmetric_schedule(nb, monkeypatch):
         _assert_parity(A, ref, *r[1:5], k)
         runs[variant] = r
     monkeypatch.delenv("TSVD_GRAM_TC")
-    for variant in (2, 1):
+    for variant in (4, 2, 1):
         np.testing.assert_allclose(runs[variant][2], runs[3][2], rtol=1e-6)
     monkeypatch.setenv("TSVD_GRAM_CUBLAS", "1")
     monkeypatch.setenv("TSVD_GRAM_NB", str(nb))
