@@ -172,7 +172,9 @@ tsvd_status tsvd_get_unique_id(void *out128);
  * Typical use: several ranks on ONE GPU (TSVD_OPT_SM_LIMIT = about 3/4 of SMs / world each, one
  * CTA per SM), which runs the multi-GPU exchange protocol where only one GPU exists.  The ranks'
  * kernels wait for each other, so each rank's stream needs its own hardware queue: set
- * CUDA_DEVICE_MAX_CONNECTIONS >= 2 world before the process creates its CUDA context.  Where the
+ * CUDA_DEVICE_MAX_CONNECTIONS >= 2 world before the process creates its CUDA context, and no other
+ * thread of the process may make a device-synchronising CUDA call (cudaFree, cudaDeviceSynchronize,
+ * tsvd_destroy of an unrelated handle, ...) while the ranks run.  Where the
  * multi-process path calls ncclAllReduce (sparse length-n vectors, METHOD = 1's B0 and extraction
  * sums) in-process ranks sum the ranks' buffers in rank order between two host rendezvous
  * (host-synchronous; a test vehicle, not a fast path).  TSVD_OPT_COLLECTIVE = 1 is refused with

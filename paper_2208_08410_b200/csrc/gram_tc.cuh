@@ -394,9 +394,11 @@ __global__ void __launch_bounds__(kGtThreads, 1)
 // Summation order of the output is that of gram_tc (512-row chunks folded in chunk order).
 constexpr int kG2Tile = 256;                                      // pair tile (M = N = 256)
 constexpr int kG2Half = 128;                                      // columns of each operand per CTA
-constexpr int kG2BK = 16;
-static_assert(kG2BK == kGtBK, "the tensor map box is 32 x kGtBK");
-constexpr int kG2Stages = 6;
+#ifndef TSVD_G2_BK
+#define TSVD_G2_BK 16   // rows per ring stage (A/B: 32 with 3 stages)
+#endif
+constexpr int kG2BK = TSVD_G2_BK;                                 // the tensor map box is 32 x kG2BK
+constexpr int kG2Stages = kG2BK == 16 ? 6 : 3;
 constexpr int kG2HalfBytes = (kG2Half / 32) * kG2BK * 128;        // 8 KB: 4 TMA boxes of 32 x BK
 constexpr int kG2StageBytes = 4 * kG2HalfBytes;                   // A raw, B raw, A lo, B lo: 32 KB
 constexpr int kG2Smem = kG2Stages * kG2StageBytes + 1024 + 256;

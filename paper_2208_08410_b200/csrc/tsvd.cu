@@ -617,8 +617,12 @@ static tsvd_status reset_state(tsvd_t h) {
 // ---- setup-time collectives: NCCL across processes, the host rendezvous for in-process ranks
 // every rank contributes (val, ptr); returns the min of val and every rank's ptr in rank order
 // (LLONG_MIN if a rank did not arrive within 60 s)
-static long long grp_exchange(tsvd_t h, long long val, void *ptr, std::vector<void *> *all) {
+static long long grp_exchange(tsvd_t h, long long val, void *ptr, std::vector<void *> *all, const char *tag = "") {
     InprocGroup &g = *h->grp;
+    static const bool dbg = getenv("TSVD_GRP_DEBUG") != nullptr;  // debug: rendezvous trace on stderr
+    if (dbg)
+        fprintf(stderr, "[grp %p rank %d enter %s gen %llu t %.3f]\n", (void *)&g, h->rank, tag, g.gen,
+                std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count());
     std::unique_lock<std::mutex> lk(g.mu);
     g.v[h->rank] = val;
     g.p[h->rank] = ptr;
@@ -630,6 +634,7 @@ static long long grp_exchange(tsvd_t h, long long val, void *ptr, std::vector<vo
         ++g.gen;
         g.cv.notify_all();
     } else if (!g.cv.wait_for(lk, std::chrono::seconds(60), [&] { return g.gen != my; })) {
+        if (dbg) fprintf(stderr, "[grp %p rank %d TIMEOUT %s gen %llu]\n", (void *)&g, h->rank, tag, my);
         return LLONG_MIN;
     }
     if (all) *all = g.rp;
@@ -642,7 +647,7 @@ static long long grp_exchange(tsvd_t h, long long val, void *ptr, std::vector<vo
 // graph capture and instantiation) before any rank launches the run.
 static tsvd_status inproc_rendezvous(tsvd_t h) {
     if (!h->grp) return TSVD_OK;
-    if (grp_exchange(h, 0, nullptr, nullptr) == LLONG_MIN)
+    if (grp_exchange(h, 0, nullptr, nullptr, "rendezvous") == LLONG_MIN)
         return h->fail(TSVD_ERR_NCCL, "in-process group: a rank did not arrive within 60 s");
     return TSVD_OK;
 }
@@ -650,7 +655,7 @@ static tsvd_status inproc_rendezvous(tsvd_t h) {
 // v = min over the ranks
 static tsvd_status coll_min_int(tsvd_t h, int &v) {
     if (h->grp) {
-        const long long r = grp_exchange(h, v, nullptr, nullptr);
+        const long long r = grp_exchange(h, v, nullptr, nullptr, "min");
         if (r == LLONG_MIN) return h->fail(TSVD_ERR_NCCL, "in-process group: a rank did not arrive within 60 s");
         v = (int)r;
         return TSVD_OK;
@@ -699,7 +704,7 @@ static tsvd_status coll_allreduce(tsvd_t h, void *buf, size_t count, bool f64, c
     }
     CK(cudaStreamSynchronize(s));
     std::vector<void *> all;
-    if (grp_exchange(h, 0, buf, &all) == LLONG_MIN)
+    if (grp_exchange(h, 0, buf, &all, "allreduce-1") == LLONG_MIN)
         return h->fail(TSVD_ERR_NCCL, "in-process group: a rank did not arrive within 60 s");
     RankPtrs rp{};
     for (int r = 0; r < h->world; ++r) rp.p[r] = all[r];
@@ -710,7 +715,7 @@ static tsvd_status coll_allreduce(tsvd_t h, void *buf, size_t count, bool f64, c
         CK(cudaGetLastError());
     }
     CK(cudaStreamSynchronize(s));
-    if (grp_exchange(h, 0, nullptr, nullptr) == LLONG_MIN)
+    if (grp_exchange(h, 0, nullptr, nullptr, "allreduce-2") == LLONG_MIN)
         return h->fail(TSVD_ERR_NCCL, "in-process group: a rank did not arrive within 60 s");
     if (count) CK(cudaMemcpyAsync(buf, h->ar_tmp, bytes, cudaMemcpyDeviceToDevice, s));
     return TSVD_OK;
@@ -723,7 +728,7 @@ static tsvd_status coll_share(tsvd_t h, void *mine, void **base, void **maps, bo
     ok = true;
     if (h->grp) {
         std::vector<void *> all;
-        if (grp_exchange(h, 0, mine, &all) == LLONG_MIN)
+        if (grp_exchange(h, 0, mine, &all, "share") == LLONG_MIN)
             return h->fail(TSVD_ERR_NCCL, "in-process group: a rank did not arrive within 60 s");
         for (int r = 0; r < h->world; ++r) base[r] = all[r];
         return TSVD_OK;
@@ -1698,18 +1703,6 @@ static tsvd_status build_gram(tsvd_t h) {
         gram_lo_split<<<h->sms * 8, 256, 0, h->stream>>>(h->A_use, m, n, h->ld_use, h->g_lo);
         CK(cudaGetLastError());
     }
-    CUtensorMap map, map_lo;
-    const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)m};
-    const cuuint64_t strides[1] = {(cuuint64_t)h->ld_use * sizeof(float)};
-    const cuuint32_t box[2] = {32, (cuuint32_t)kGtBK};
-    const cuuint32_t estr[2] = {1, 1};
-    for (int w = 0; w < 2; ++w) {
-        CUresult r = encode(w ? &map_lo : &map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                            (void *)(w && lo_gmem ? h->g_lo : h->A_use), dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return h->fail(TSVD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-    }
     // default: the CTA-pair kernel (gram_tc2).  A/B: TSVD_GRAM_TC=3 (N = 192) / 4 (N = 128, 8 TMEM
     // slots) the pair kernel with A in TMEM
     // (fewer shared-memory bytes, but measured 5-10 % slower: 98 vs 88-93 ms at C2, the box's power
@@ -1718,6 +1711,18 @@ static tsvd_status build_gram(tsvd_t h) {
     if (const char *e = getenv("TSVD_GRAM_TC")) variant = atoi(e);
     if (getenv("TSVD_GRAM_TC1") || lo_gmem || h->sms < 2) variant = 1;
     const bool pair = variant >= 2;
+    CUtensorMap map, map_lo;
+    const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)m};
+    const cuuint64_t strides[1] = {(cuuint64_t)h->ld_use * sizeof(float)};
+    const cuuint32_t box[2] = {32, (cuuint32_t)(variant == 2 ? kG2BK : kGtBK)};  // 32 columns x the stage's rows
+    const cuuint32_t estr[2] = {1, 1};
+    for (int w = 0; w < 2; ++w) {
+        CUresult r = encode(w ? &map_lo : &map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                            (void *)(w && lo_gmem ? h->g_lo : h->A_use), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return h->fail(TSVD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    }
     if (h->gram_n != n || h->gram_pair != variant) {
         const std::vector<int2> tiles = variant == 4 ? gram_tiles3(n, 128) : variant == 3 ? gram_tiles3(n, 192)
                                       : variant == 2 ? gram_tiles2(n) : gram_tiles(n);
@@ -2007,6 +2012,10 @@ static tsvd_status run_explicit(tsvd_t h, int l0) {
         CK(launch_k(h, gram_ext_finish, blocks, 256, 0, h->stream, 1, x));
         CK(cudaMemcpyAsync(h->st_host, h->st, sizeof(LoopState), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
+        if (getenv("TSVD_GRP_DEBUG"))
+            fprintf(stderr, "[explicit rank %d component %d done: it %d status %d t %.3f]\n", h->rank, l,
+                    h->st_host->it, h->st_host->status,
+                    std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count());
         if (h->timing) {
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, e0, e1));
@@ -3171,7 +3180,7 @@ void tsvd_destroy(tsvd_t h) {
     cudaSetDevice(h->dev);
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->grp) {  // barrier: no rank may still read our exchange buffers when they are freed
-        grp_exchange(h, 0, nullptr, nullptr);
+        grp_exchange(h, 0, nullptr, nullptr, "destroy");
     } else if (h->comm) {  // barrier: no peer may still read our symmetric buffer when it is freed
         int *d = nullptr;
         if (cudaMalloc((void **)&d, sizeof(int)) == cudaSuccess) {

@@ -14,6 +14,8 @@ Checks: the gathered result against the fp64 oracle at the north-star contract (
 1e-4, |cos| >= 1 - 1e-4, elementwise vectors; tests/_parity.py), iteration counts within one (observed
 equal), and bitwise-equal S and V on every rank (every rank sums the same words in the same order).
 """
+import contextlib
+import gc
 import threading
 
 import numpy as np
@@ -30,6 +32,22 @@ if not torch.cuda.is_available():  # pragma: no cover - collected on the GPU box
 
 import paper_2208_08410_b200 as P  # noqa: E402
 from _parity import assert_tsvd_close  # noqa: E402
+
+
+@contextlib.contextmanager
+def _no_gc():
+    """While in-process ranks run, no other thread of this process may make a device-synchronising
+    CUDA call (cudaFree, ...): it would wait for a rank's kernel that spins on another rank whose host
+    thread is the one blocked.  Earlier tests leave TSVD objects for the cyclic garbage collector, whose
+    __del__ (tsvd_destroy: cudaFree) would run in whichever thread triggers a collection — collect
+    them now and keep the collector off until every rank has finished."""
+    gc.collect()
+    torch.cuda.synchronize()
+    gc.disable()
+    try:
+        yield
+    finally:
+        gc.enable()
 
 
 def _slab(world, rank, m):
@@ -49,6 +67,16 @@ def _run_ranks(A, k, eps, V0, world, col=False, opts=None, timeout=600, sm_per_r
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     budget = sm_per_rank or max(1, (sms // world) * 3 // 4)
     out, errors = [None] * world, []
+    # every rank's slab is staged here, in the main thread: the rank threads make library calls only
+    slabs = []
+    for r in range(world):
+        r0, r1 = _slab(world, r, n if col else m)
+        if col:  # (m, cols) with unit row stride: this rank's columns of the column-major matrix
+            slabs.append(torch.from_numpy(np.ascontiguousarray(A[:, r0:r1].T)).cuda().t())
+        elif host:  # pinned host slab (out-of-memory streaming reads it every pass)
+            slabs.append(torch.from_numpy(np.ascontiguousarray(A[r0:r1])).pin_memory())
+        else:
+            slabs.append(torch.from_numpy(np.ascontiguousarray(A[r0:r1])).cuda())
 
     def work(r):
         try:
@@ -60,12 +88,7 @@ def _run_ranks(A, k, eps, V0, world, col=False, opts=None, timeout=600, sm_per_r
             for key, val in (opts or {}).items():
                 t.set_option(getattr(P, "OPT_" + key.upper()), val)
             t.set_init(V0)
-            if col:  # (m, cols) with unit row stride: this rank's columns of the column-major matrix
-                t.set_dense(torch.from_numpy(np.ascontiguousarray(A[:, r0:r1].T)).cuda().t(), r0, r1)
-            elif host:  # pinned host slab (out-of-memory streaming reads it every pass)
-                t.set_dense(torch.from_numpy(np.ascontiguousarray(A[r0:r1])).pin_memory(), r0, r1)
-            else:
-                t.set_dense(torch.from_numpy(np.ascontiguousarray(A[r0:r1])).cuda(), r0, r1)
+            t.set_dense(slabs[r], r0, r1)
             rc = t.run()
             U, S, V = t.result()
             kf, iters, _ = t.info()
@@ -76,10 +99,11 @@ def _run_ranks(A, k, eps, V0, world, col=False, opts=None, timeout=600, sm_per_r
             errors.append((r, repr(e)))
 
     threads = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(world)]
-    for th in threads:
-        th.start()
-    for th in threads:
-        th.join(timeout)
+    with _no_gc():
+        for th in threads:
+            th.start()
+        for th in threads:
+            th.join(timeout)
     assert not errors, errors
     assert all(o is not None for o in out), "a rank did not finish"
     return out
@@ -201,10 +225,11 @@ def _run_sparse_ranks(m, n, d, k, eps, V0, world, T, block=0, timeout=600):
             errors.append((r, repr(e)))
 
     threads = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(world)]
-    for th in threads:
-        th.start()
-    for th in threads:
-        th.join(timeout)
+    with _no_gc():
+        for th in threads:
+            th.start()
+        for th in threads:
+            th.join(timeout)
     assert not errors, errors
     assert all(o is not None for o in out), "a rank did not finish"
     return out
